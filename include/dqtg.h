@@ -1,0 +1,197 @@
+/*
+ * dqtg.h — C ABI of the B200 checkpoint-compression engine (libdqtg.so).
+ *
+ * Plain pointers and sizes only; no torch/CUDA types in the signatures
+ * (streams are passed as an opaque void*).  Every entry point replaces one
+ * function (or one loop) of the reference library `dqt`
+ * (/root/reference/proj); the replaced interface is cited next to each
+ * declaration.  The C++ drop-in library (include/dqt/*.hpp, libdqt.so) and the
+ * Python module (dqt._dqt) are thin hosts over this ABI; INTEGRATION.md shows
+ * the binding a maintainer adds to the reference to call it directly.
+ *
+ * Pointers named `*_any` may be host or device memory (detected with
+ * cudaPointerGetAttributes); everything else is host memory unless the name
+ * says `_dev`.  All calls are synchronous with respect to the host unless
+ * stated otherwise and are serialised per engine (thread-safe).
+ *
+ * Errors: every call returns a dqtg_status; dqtg_last_error() returns the
+ * message of the last failure on the calling thread.  Status codes map 1:1 to
+ * the reference exception types (include/dqt/errors.hpp:8-39).
+ */
+#ifndef DQTG_H
+#define DQTG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum dqtg_status {
+    DQTG_OK = 0,
+    DQTG_ERROR = 1,                 /* dqt::Error */
+    DQTG_BAD_MAGIC = 2,             /* dqt::BadMagic */
+    DQTG_TRUNCATED = 3,             /* dqt::TruncatedFile */
+    DQTG_SHAPE_MISMATCH = 4,        /* dqt::ShapeMismatch */
+    DQTG_NON_FINITE = 5,            /* dqt::NonFiniteData */
+    DQTG_IO = 6,                    /* dqt::IoError */
+    DQTG_ALPHA_OUT_OF_RANGE = 7,    /* dqt::AlphaOutOfRange */
+    DQTG_ALPHA_MISMATCH = 8,        /* dqt::AlphaMismatch */
+    DQTG_EMPTY_SKETCH = 9,          /* dqt::EmptySketch */
+    DQTG_MISSING_GRADIENTS = 10,    /* dqt::MissingGradients */
+    DQTG_MISSING_SCORES = 11,       /* dqt::MissingScores */
+    DQTG_TOO_FEW_DISTINCT = 12,     /* dqt::TooFewDistinctPoints */
+    DQTG_CORRUPT_INDEX = 13,        /* dqt::CorruptIndex */
+    DQTG_CORRUPT_BITSTREAM = 14,    /* dqt::CorruptBitstream */
+    DQTG_CHECKSUM_MISMATCH = 15,    /* dqt::ChecksumMismatch */
+    DQTG_CHAIN_CORRUPT = 16,        /* dqt::ChainCorrupt */
+    DQTG_CUDA = 17                  /* CUDA runtime failure (surfaces as dqt::Error) */
+} dqtg_status;
+
+const char *dqtg_last_error(void);
+const char *dqtg_version(void);
+
+/* ---- engine ------------------------------------------------------------ */
+typedef struct dqtg_engine dqtg_engine;
+/* device: CUDA ordinal; stream: cudaStream_t to run on (NULL = engine-owned). */
+dqtg_status dqtg_engine_create(int device, void *stream, dqtg_engine **out);
+void dqtg_engine_destroy(dqtg_engine *e);
+dqtg_status dqtg_engine_sync(dqtg_engine *e);
+/* number of engine kernels launched so far (bench `gpu_launches`) */
+uint64_t dqtg_engine_launches(const dqtg_engine *e);
+
+/* dqt::QuantConfig (quantize.hpp:13-26) */
+typedef struct dqtg_config {
+    uint32_t bins, embed_bins;
+    double prune_frac, protect_frac;
+    uint32_t metric; /* 0 = MAGNITUDE, 1 = SENSITIVITY (ranker.hpp:26) */
+    double sigma, alpha;
+} dqtg_config;
+
+/* Checkpoint layout: tensors in checkpoint order (tensor.hpp:28-45). */
+typedef struct dqtg_layout {
+    uint32_t n_tensors;
+    const char *const *names;   /* may be NULL when no record is produced */
+    const uint8_t *types;       /* dqt::LayerType 0..6 */
+    const uint8_t *ranks;
+    const uint64_t *dims;       /* concatenated shapes */
+} dqtg_layout;
+
+/* ---- sketch: replaces sketch_build(const float*, n, alpha) (sketch.cpp:131-148)
+ * Bucket counts over k in [kmin, kmax] (dqtg_sketch_range) for each sign plus the
+ * zero bucket; pos/neg are host arrays of kmax-kmin+1 entries. */
+dqtg_status dqtg_sketch_range(double alpha, int64_t *kmin, int64_t *kmax);
+dqtg_status dqtg_sketch_build(dqtg_engine *e, const float *x_any, uint64_t n, double alpha,
+                              uint64_t *zero, uint64_t *pos, uint64_t *neg);
+
+/* ---- ranker: ema_update (ranker.cpp:21-37), compute_scores (ranker.cpp:79-101) */
+dqtg_status dqtg_ema_update(dqtg_engine *e, float *ema_any, const float *g_any, uint64_t n,
+                            double beta);
+dqtg_status dqtg_compute_scores(dqtg_engine *e, const float *w_any, const float *ema_any,
+                                uint64_t n, float *mag_any, float *sens_any);
+
+/* ---- device checkpoint (weights + scores resident in HBM) ---------------- */
+typedef struct dqtg_ckpt dqtg_ckpt;
+dqtg_status dqtg_ckpt_create(dqtg_engine *e, const dqtg_layout *layout, dqtg_ckpt **out);
+void dqtg_ckpt_destroy(dqtg_ckpt *c);
+/* per-tensor weight pointers (tensor.hpp:30 NamedTensor::data) */
+dqtg_status dqtg_ckpt_set_weights(dqtg_ckpt *c, const float *const *tensors_any);
+/* explicit ScoreSet (ranker.hpp:34-42); sens may be NULL (has_sensitivity=false) */
+dqtg_status dqtg_ckpt_set_scores(dqtg_ckpt *c, const float *const *mag_any,
+                                 const float *const *sens_any);
+/* scores derived on device from the EMA: magnitude |w|, sensitivity |e*w| fused into the
+ * histogram / assign passes (compute_scores never materialised).  ema may be NULL. */
+dqtg_status dqtg_ckpt_set_ema(dqtg_ckpt *c, const float *const *ema_any);
+/* ema_update on the device-resident EMA (first call seeds it) */
+dqtg_status dqtg_ckpt_update_ema(dqtg_ckpt *c, const float *const *grads_any, double beta);
+uint64_t dqtg_ckpt_param_count(const dqtg_ckpt *c);
+/* flat padded device buffers (for device-resident producers, e.g. the bench) */
+float *dqtg_ckpt_weights_dev(dqtg_ckpt *c);
+float *dqtg_ckpt_ema_dev(dqtg_ckpt *c);
+/* element offset of tensor i inside the padded buffers */
+uint64_t dqtg_ckpt_tensor_offset(const dqtg_ckpt *c, uint32_t i);
+
+/* ---- quantized state (QuantizedCheckpoint, quantize.hpp:86-110) ----------- */
+typedef struct dqtg_qstate dqtg_qstate;
+typedef struct dqtg_qstate_info {
+    uint64_t step;
+    dqtg_config config;
+    uint32_t codebook_len[7];
+    uint32_t max_levels;
+    uint64_t param_count;
+    uint64_t protected_total;
+} dqtg_qstate_info;
+
+/* quantize_checkpoint(c, scores, cfg, seed) (quantize.cpp:373-425) */
+dqtg_status dqtg_quantize(dqtg_engine *e, const dqtg_ckpt *c, const dqtg_config *cfg,
+                          uint64_t seed, uint64_t step, dqtg_qstate **out);
+dqtg_status dqtg_qstate_info_get(const dqtg_qstate *q, dqtg_qstate_info *info);
+/* per-tensor protected counts (n_tensors entries) */
+dqtg_status dqtg_qstate_protected_counts(const dqtg_qstate *q, uint64_t *counts);
+/* copy out: levels[i] (numel_i u16), prot_pos[i]/prot_val[i] (count_i each), codebooks[lt]
+ * (codebook_len[lt] floats).  Any pointer array may be NULL to skip that part. */
+dqtg_status dqtg_qstate_download(const dqtg_qstate *q, uint16_t *const *levels,
+                                 uint64_t *const *prot_pos, uint16_t *const *prot_val,
+                                 float *const *codebooks);
+/* build a state from host arrays (encode_delta_record on caller-made states) */
+dqtg_status dqtg_qstate_upload(dqtg_engine *e, const dqtg_layout *layout, uint64_t step,
+                               const dqtg_config *cfg, const uint32_t *codebook_len,
+                               const float *const *codebooks, const uint16_t *const *levels,
+                               const uint64_t *prot_count, const uint64_t *const *prot_pos,
+                               const uint16_t *const *prot_val, dqtg_qstate **out);
+void dqtg_qstate_destroy(dqtg_qstate *q);
+uint16_t *dqtg_qstate_levels_dev(dqtg_qstate *q);
+/* dequantize_checkpoint (quantize.cpp:427-462) into per-tensor outputs */
+dqtg_status dqtg_dequantize(dqtg_engine *e, const dqtg_qstate *q, float *const *out_any);
+
+/* ---- DQDR records (codec.cpp:398-597) ---------------------------------- */
+typedef struct dqtg_record dqtg_record;
+/* encode_delta_record(base, target, quality_delta); base NULL = FULL record */
+dqtg_status dqtg_encode_record(dqtg_engine *e, const dqtg_qstate *base,
+                               const dqtg_qstate *target, double quality_delta,
+                               dqtg_record **out);
+uint64_t dqtg_record_size(const dqtg_record *r);
+dqtg_status dqtg_record_copy(const dqtg_record *r, void *dst_host);
+const uint8_t *dqtg_record_dev(const dqtg_record *r);
+void dqtg_record_destroy(dqtg_record *r);
+/* decode_delta_record(record, base) (codec.cpp:513-597) */
+dqtg_status dqtg_decode_record(dqtg_engine *e, const uint8_t *rec, uint64_t n,
+                               const dqtg_qstate *base, dqtg_qstate **out);
+
+/* ---- fused step: compute_scores + quantize_checkpoint + encode_delta_record
+ * (the path Chain::append + cmd_compress run, chain.cpp:86-129 / dqt.cpp:208-210) */
+dqtg_status dqtg_compress_step(dqtg_engine *e, const dqtg_ckpt *c, const dqtg_config *cfg,
+                               uint64_t seed, uint64_t step, const dqtg_qstate *base,
+                               double quality_delta, dqtg_qstate **state_out,
+                               dqtg_record **record_out);
+
+/* ---- batched candidate evaluation: ProxyEvaluator::evaluate over m configs
+ * (search.cpp:107-112) as EvalCache::prefetch batches them (search.cpp:174-204) */
+dqtg_status dqtg_eval_batch(dqtg_engine *e, const dqtg_ckpt *c, const dqtg_config *cfgs,
+                            const uint64_t *seeds, uint32_t m, double *quality_delta,
+                            double *est_compression);
+
+/* ---- clustering (quantize.cpp:94-325) ------------------------------------ */
+dqtg_status dqtg_approx_kmeans(dqtg_engine *e, const float *values_any, uint64_t n, uint32_t k,
+                               double sigma, double alpha, uint64_t seed, float *codebook,
+                               uint32_t *len);
+dqtg_status dqtg_kmeanspp_init(dqtg_engine *e, const double *points, const double *weights,
+                               uint64_t n, uint32_t k, uint64_t seed, double *centers);
+dqtg_status dqtg_lloyd(dqtg_engine *e, const double *points, const double *weights, uint64_t n,
+                       double *centers, uint32_t k, double tol, uint32_t max_iter,
+                       uint32_t *iterations);
+dqtg_status dqtg_sq_loss(dqtg_engine *e, const double *points, const double *weights, uint64_t n,
+                         const double *centers, uint32_t k, double *loss);
+
+/* ---- codec primitives (codec.cpp:12-288) ---------------------------------- */
+dqtg_status dqtg_delta_compute(dqtg_engine *e, const uint16_t *prev, const uint16_t *cur,
+                               uint64_t n, uint32_t B, uint16_t *out);
+dqtg_status dqtg_delta_apply(dqtg_engine *e, const uint16_t *prev, const uint16_t *deltas,
+                             uint64_t n, uint32_t B, uint16_t *out);
+dqtg_status dqtg_crc32(dqtg_engine *e, const uint8_t *data_any, uint64_t n, uint32_t *crc);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DQTG_H */

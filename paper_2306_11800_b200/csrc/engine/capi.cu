@@ -1,0 +1,516 @@
+// extern "C" surface of libdqtg.so (include/dqtg.h).  Every entry point catches
+// internal failures and turns them into a dqtg_status + thread-local message.
+#include <cstring>
+#include <string>
+
+#include "engine.h"
+#include "kmeans_api.h"
+#include "quantize_api.h"
+
+using namespace dqtg;
+
+struct dqtg_engine {
+    Engine e;
+};
+struct dqtg_ckpt {
+    DevCkpt c;
+};
+struct dqtg_qstate {
+    std::unique_ptr<QState> q;
+};
+struct dqtg_record {
+    std::unique_ptr<Record> r;
+};
+
+static thread_local std::string g_err;
+
+template <typename F>
+static dqtg_status guard(F&& f) {
+    try {
+        f();
+        return DQTG_OK;
+    } catch (const Fail& x) {
+        g_err = x.what();
+        return x.code;
+    } catch (const std::exception& x) {
+        g_err = x.what();
+        return DQTG_ERROR;
+    } catch (...) {
+        g_err = "unknown failure";
+        return DQTG_ERROR;
+    }
+}
+
+#define LOCK(eng)                                       \
+    std::lock_guard<std::recursive_mutex> lk_((eng)->mu); \
+    (eng)->activate()
+
+extern "C" {
+
+const char* dqtg_last_error(void) { return g_err.c_str(); }
+const char* dqtg_version(void) { return "dqtg 0.1 sm_100a"; }
+
+dqtg_status dqtg_engine_create(int device, void* stream, dqtg_engine** out) {
+    return guard([&] {
+        auto* h = new dqtg_engine();
+        try {
+            Engine& e = h->e;
+            e.device = device;
+            DQTG_CUDA(cudaSetDevice(device));
+            cudaDeviceProp prop;
+            DQTG_CUDA(cudaGetDeviceProperties(&prop, device));
+            DQTG_REQUIRE(prop.major >= 10, DQTG_CUDA,
+                         "dqtg needs a Blackwell (sm_100) device; found " + std::string(prop.name));
+            e.num_sms = prop.multiProcessorCount;
+            if (stream) {
+                e.stream = (cudaStream_t)stream;
+            } else {
+                DQTG_CUDA(cudaStreamCreateWithFlags(&e.stream, cudaStreamNonBlocking));
+                e.own_stream = true;
+            }
+            DQTG_CUDA(cudaMalloc(&e.d_err, 16));
+            DQTG_CUDA(cudaMemset(e.d_err, 0, 16));
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+void dqtg_engine_destroy(dqtg_engine* h) { delete h; }
+
+dqtg_status dqtg_engine_sync(dqtg_engine* h) {
+    return guard([&] {
+        LOCK(&h->e);
+        h->e.sync();
+    });
+}
+
+uint64_t dqtg_engine_launches(const dqtg_engine* h) { return h->e.launches; }
+
+dqtg_status dqtg_sketch_range(double alpha, int64_t* kmin, int64_t* kmax) {
+    return guard([&] {
+        // host-only: same rule as the alpha tables
+        DQTG_REQUIRE(alpha > 0.0 && alpha < 1.0, DQTG_ALPHA_OUT_OF_RANGE, "alpha must be in (0, 1)");
+        Engine tmp;  // never touches the device for range queries
+        (void)tmp;
+        double g = (1.0 + alpha) / (1.0 - alpha), inv = 1.0 / log(g);
+        auto bucket = [&](double ax) {
+            double r = log(ax) * inv;
+            double nearest = nearbyint(r);
+            if (fabs(r - nearest) > 1e-9 * fmax(1.0, fabs(r))) return (int64_t)ceil(r);
+            int64_t k = (int64_t)nearest;
+            while (pow(g, (double)(k - 1)) >= ax) --k;
+            while (pow(g, (double)k) < ax) ++k;
+            return k;
+        };
+        float zf = (float)1e-12;
+        if ((double)zf < 1e-12) zf = nextafterf(zf, INFINITY);
+        *kmin = bucket((double)zf);
+        *kmax = bucket((double)3.4028234663852886e38);
+    });
+}
+
+dqtg_status dqtg_sketch_build(dqtg_engine* h, const float* x, uint64_t n, double alpha,
+                              uint64_t* zero, uint64_t* pos, uint64_t* neg) {
+    return guard([&] {
+        LOCK(&h->e);
+        sketch_build(h->e, x, n, alpha, zero, pos, neg);
+    });
+}
+
+dqtg_status dqtg_ema_update(dqtg_engine* h, float* ema, const float* g, uint64_t n, double beta) {
+    return guard([&] {
+        LOCK(&h->e);
+        Engine& e = h->e;
+        const bool de = is_device_ptr(ema);
+        float* d_e = de ? ema : (float*)e.buf("api.ema", n * 4 + 4);
+        float* d_g = (float*)e.buf("api.g", n * 4 + 4);
+        if (!de) e.to_device(d_e, ema, n * 4);
+        e.to_device(d_g, g, n * 4);
+        ::dqtg::ema_update(e, d_e, d_g, n, (float)beta);
+        if (!de) e.from_device(ema, d_e, n * 4);
+        e.sync();
+    });
+}
+
+dqtg_status dqtg_compute_scores(dqtg_engine* h, const float* w, const float* ema, uint64_t n,
+                                float* mag, float* sens) {
+    return guard([&] {
+        LOCK(&h->e);
+        Engine& e = h->e;
+        float* d_w = (float*)e.buf("api.w", n * 4 + 4);
+        float* d_e = ema ? (float*)e.buf("api.ema", n * 4 + 4) : nullptr;
+        float* d_m = mag ? (float*)e.buf("api.mag", n * 4 + 4) : nullptr;
+        float* d_s = sens ? (float*)e.buf("api.sens", n * 4 + 4) : nullptr;
+        e.to_device(d_w, w, n * 4);
+        if (ema) e.to_device(d_e, ema, n * 4);
+        ::dqtg::compute_scores(e, d_w, d_e, n, d_m, (ema && sens) ? d_s : nullptr);
+        if (mag) e.from_device(mag, d_m, n * 4);
+        if (sens && ema) e.from_device(sens, d_s, n * 4);
+        e.sync();
+    });
+}
+
+// ---- checkpoints ---------------------------------------------------------------
+dqtg_status dqtg_ckpt_create(dqtg_engine* h, const dqtg_layout* layout, dqtg_ckpt** out) {
+    return guard([&] {
+        LOCK(&h->e);
+        auto* c = new dqtg_ckpt();
+        try {
+            c->c.eng = &h->e;
+            c->c.L = make_layout(&h->e, layout);
+            DQTG_CUDA(cudaMalloc(&c->c.w, c->c.L->Np * 4));
+            DQTG_CUDA(cudaMemset(c->c.w, 0, c->c.L->Np * 4));
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+void dqtg_ckpt_destroy(dqtg_ckpt* c) { delete c; }
+
+static void upload_tensors(Engine& e, const Layout& L, float* dst, const float* const* src) {
+    for (uint32_t i = 0; i < L.nt; ++i)
+        if (L.numel[i]) e.to_device(dst + L.off[i], src[i], L.numel[i] * 4);
+}
+
+dqtg_status dqtg_ckpt_set_weights(dqtg_ckpt* c, const float* const* t) {
+    return guard([&] {
+        LOCK(c->c.eng);
+        upload_tensors(*c->c.eng, *c->c.L, c->c.w, t);
+        c->c.eng->sync();
+    });
+}
+
+static float* alloc_padded(const Layout& L) {
+    float* p = nullptr;
+    DQTG_CUDA(cudaMalloc(&p, L.Np * 4));
+    DQTG_CUDA(cudaMemset(p, 0, L.Np * 4));
+    return p;
+}
+
+dqtg_status dqtg_ckpt_set_scores(dqtg_ckpt* c, const float* const* mag, const float* const* sens) {
+    return guard([&] {
+        LOCK(c->c.eng);
+        DevCkpt& d = c->c;
+        if (!d.mag) d.mag = alloc_padded(*d.L);
+        upload_tensors(*d.eng, *d.L, d.mag, mag);
+        if (sens) {
+            if (!d.sens) d.sens = alloc_padded(*d.L);
+            upload_tensors(*d.eng, *d.L, d.sens, sens);
+        }
+        d.explicit_scores = true;
+        d.has_sens = sens != nullptr;
+        d.eng->sync();
+    });
+}
+
+dqtg_status dqtg_ckpt_set_ema(dqtg_ckpt* c, const float* const* ema) {
+    return guard([&] {
+        LOCK(c->c.eng);
+        DevCkpt& d = c->c;
+        d.explicit_scores = false;
+        if (ema) {
+            if (!d.ema) d.ema = alloc_padded(*d.L);
+            upload_tensors(*d.eng, *d.L, d.ema, ema);
+            d.has_sens = true;
+            d.ema_seeded = true;
+        } else {
+            d.has_sens = false;
+        }
+        d.eng->sync();
+    });
+}
+
+dqtg_status dqtg_ckpt_update_ema(dqtg_ckpt* c, const float* const* grads, double beta) {
+    return guard([&] {
+        LOCK(c->c.eng);
+        DevCkpt& d = c->c;
+        Engine& e = *d.eng;
+        if (!d.ema) d.ema = alloc_padded(*d.L);
+        if (!d.ema_seeded) {  // first snapshot seeds the average (ranker.cpp:22-23)
+            upload_tensors(e, *d.L, d.ema, grads);
+            d.ema_seeded = true;
+        } else {
+            float* g = (float*)e.buf("ck.g", d.L->Np * 4);
+            upload_tensors(e, *d.L, g, grads);
+            ::dqtg::ema_update(e, d.ema, g, d.L->Np, (float)beta);
+        }
+        d.explicit_scores = false;
+        d.has_sens = true;
+        e.sync();
+    });
+}
+
+uint64_t dqtg_ckpt_param_count(const dqtg_ckpt* c) { return c->c.L->N; }
+float* dqtg_ckpt_weights_dev(dqtg_ckpt* c) { return c->c.w; }
+float* dqtg_ckpt_ema_dev(dqtg_ckpt* c) {
+    if (!c->c.ema) {
+        c->c.ema = alloc_padded(*c->c.L);
+        c->c.has_sens = true;
+        c->c.ema_seeded = true;
+        c->c.explicit_scores = false;
+    }
+    return c->c.ema;
+}
+uint64_t dqtg_ckpt_tensor_offset(const dqtg_ckpt* c, uint32_t i) { return c->c.L->off[i]; }
+
+// ---- quantize / states ------------------------------------------------------------
+dqtg_status dqtg_quantize(dqtg_engine* h, const dqtg_ckpt* c, const dqtg_config* cfg,
+                          uint64_t seed, uint64_t step, dqtg_qstate** out) {
+    return guard([&] {
+        LOCK(&h->e);
+        auto q = ::dqtg::quantize(h->e, c->c, *cfg, seed, step);
+        auto* s = new dqtg_qstate();
+        s->q = std::move(q);
+        *out = s;
+    });
+}
+
+dqtg_status dqtg_qstate_info_get(const dqtg_qstate* s, dqtg_qstate_info* info) {
+    return guard([&] {
+        const QState& q = *s->q;
+        info->step = q.step;
+        info->config = q.cfg;
+        for (int lt = 0; lt < kLayerTypes; ++lt) info->codebook_len[lt] = q.cb_len[lt];
+        info->max_levels = q.max_levels();
+        info->param_count = q.L->N;
+        info->protected_total = q.prot_total;
+    });
+}
+
+dqtg_status dqtg_qstate_protected_counts(const dqtg_qstate* s, uint64_t* counts) {
+    return guard([&] {
+        for (uint32_t i = 0; i < s->q->L->nt; ++i) counts[i] = s->q->prot_count[i];
+    });
+}
+
+dqtg_status dqtg_qstate_download(const dqtg_qstate* s, uint16_t* const* levels,
+                                 uint64_t* const* ppos, uint16_t* const* pval,
+                                 float* const* codebooks) {
+    return guard([&] {
+        const QState& q = *s->q;
+        Engine& e = *q.eng;
+        LOCK(&e);
+        const Layout& L = *q.L;
+        for (uint32_t i = 0; i < L.nt; ++i) {
+            if (levels && levels[i] && L.numel[i])
+                e.from_device(levels[i], q.d_levels + L.off[i], L.numel[i] * 2);
+            if (q.prot_count[i]) {
+                if (ppos && ppos[i])
+                    e.from_device(ppos[i], q.d_ppos + q.prot_off[i], q.prot_count[i] * 8);
+                if (pval && pval[i])
+                    e.from_device(pval[i], q.d_pval + q.prot_off[i], q.prot_count[i] * 2);
+            }
+        }
+        if (codebooks)
+            for (int lt = 0; lt < kLayerTypes; ++lt)
+                if (codebooks[lt] && q.cb_len[lt])
+                    memcpy(codebooks[lt], q.cb[lt].data(), q.cb_len[lt] * 4);
+        e.sync();
+    });
+}
+
+dqtg_status dqtg_qstate_upload(dqtg_engine* h, const dqtg_layout* layout, uint64_t step,
+                               const dqtg_config* cfg, const uint32_t* cb_len,
+                               const float* const* cbs, const uint16_t* const* levels,
+                               const uint64_t* prot_count, const uint64_t* const* ppos,
+                               const uint16_t* const* pval, dqtg_qstate** out) {
+    return guard([&] {
+        LOCK(&h->e);
+        Engine& e = h->e;
+        auto q = std::make_unique<QState>();
+        q->eng = &e;
+        q->L = make_layout(&e, layout);
+        q->step = step;
+        q->cfg = *cfg;
+        uint32_t stride = 1;
+        for (int lt = 0; lt < kLayerTypes; ++lt) {
+            q->cb_len[lt] = cb_len[lt];
+            q->cb[lt].assign(cbs[lt], cbs[lt] + cb_len[lt]);
+            stride = std::max(stride, cb_len[lt]);
+        }
+        q->cb_stride = stride;
+        std::vector<float> flat((size_t)kLayerTypes * stride, 0.0f);
+        for (int lt = 0; lt < kLayerTypes; ++lt)
+            std::copy(q->cb[lt].begin(), q->cb[lt].end(), flat.begin() + (size_t)lt * stride);
+        DQTG_CUDA(cudaMalloc(&q->d_cb, flat.size() * 4));
+        DQTG_CUDA(cudaMemcpy(q->d_cb, flat.data(), flat.size() * 4, cudaMemcpyHostToDevice));
+        const Layout& L = *q->L;
+        DQTG_CUDA(cudaMalloc(&q->d_levels, L.Np * 2));
+        DQTG_CUDA(cudaMemset(q->d_levels, 0, L.Np * 2));
+        q->prot_count.assign(L.nt, 0);
+        q->prot_off.assign(L.nt + 1, 0);
+        uint64_t acc = 0;
+        for (uint32_t i = 0; i < L.nt; ++i) {
+            q->prot_off[i] = acc;
+            q->prot_count[i] = prot_count ? prot_count[i] : 0;
+            acc += q->prot_count[i];
+        }
+        q->prot_off[L.nt] = q->prot_total = acc;
+        DQTG_CUDA(cudaMalloc(&q->d_ppos, (acc + 1) * 8));
+        DQTG_CUDA(cudaMalloc(&q->d_pval, (acc + 1) * 2));
+        for (uint32_t i = 0; i < L.nt; ++i) {
+            if (L.numel[i]) e.to_device(q->d_levels + L.off[i], levels[i], L.numel[i] * 2);
+            if (q->prot_count[i]) {
+                e.to_device(q->d_ppos + q->prot_off[i], ppos[i], q->prot_count[i] * 8);
+                e.to_device(q->d_pval + q->prot_off[i], pval[i], q->prot_count[i] * 2);
+            }
+        }
+        e.sync();
+        auto* s = new dqtg_qstate();
+        s->q = std::move(q);
+        *out = s;
+    });
+}
+
+void dqtg_qstate_destroy(dqtg_qstate* s) { delete s; }
+uint16_t* dqtg_qstate_levels_dev(dqtg_qstate* s) { return s->q->d_levels; }
+
+dqtg_status dqtg_dequantize(dqtg_engine* h, const dqtg_qstate* s, float* const* out) {
+    return guard([&] {
+        LOCK(&h->e);
+        Engine& e = h->e;
+        const QState& q = *s->q;
+        const Layout& L = *q.L;
+        float* d = (float*)e.buf("dq.out", L.Np * 4);
+        ::dqtg::dequantize(e, q, d);
+        e.check_err();
+        for (uint32_t i = 0; i < L.nt; ++i)
+            if (L.numel[i]) e.from_device(out[i], d + L.off[i], L.numel[i] * 4);
+        e.sync();
+    });
+}
+
+// ---- records --------------------------------------------------------------------
+dqtg_status dqtg_encode_record(dqtg_engine* h, const dqtg_qstate* base, const dqtg_qstate* target,
+                               double quality, dqtg_record** out) {
+    return guard([&] {
+        LOCK(&h->e);
+        auto r = ::dqtg::encode_record(h->e, base ? base->q.get() : nullptr, *target->q, quality);
+        auto* rr = new dqtg_record();
+        rr->r = std::move(r);
+        *out = rr;
+    });
+}
+
+uint64_t dqtg_record_size(const dqtg_record* r) { return r->r->size; }
+
+dqtg_status dqtg_record_copy(const dqtg_record* r, void* dst) {
+    return guard([&] {
+        Engine& e = *r->r->eng;
+        LOCK(&e);
+        e.from_device(dst, r->r->d_buf, r->r->size);
+        e.sync();
+    });
+}
+
+const uint8_t* dqtg_record_dev(const dqtg_record* r) { return r->r->d_buf; }
+void dqtg_record_destroy(dqtg_record* r) { delete r; }
+
+dqtg_status dqtg_decode_record(dqtg_engine* h, const uint8_t* rec, uint64_t n,
+                               const dqtg_qstate* base, dqtg_qstate** out) {
+    return guard([&] {
+        LOCK(&h->e);
+        auto q = ::dqtg::decode_record(h->e, rec, n, base ? base->q.get() : nullptr);
+        auto* s = new dqtg_qstate();
+        s->q = std::move(q);
+        *out = s;
+    });
+}
+
+dqtg_status dqtg_compress_step(dqtg_engine* h, const dqtg_ckpt* c, const dqtg_config* cfg,
+                               uint64_t seed, uint64_t step, const dqtg_qstate* base,
+                               double quality, dqtg_qstate** state_out, dqtg_record** record_out) {
+    return guard([&] {
+        LOCK(&h->e);
+        auto q = ::dqtg::quantize(h->e, c->c, *cfg, seed, step);
+        auto r = ::dqtg::encode_record(h->e, base ? base->q.get() : nullptr, *q, quality);
+        auto* s = new dqtg_qstate();
+        s->q = std::move(q);
+        auto* rr = new dqtg_record();
+        rr->r = std::move(r);
+        *state_out = s;
+        *record_out = rr;
+    });
+}
+
+dqtg_status dqtg_eval_batch(dqtg_engine* h, const dqtg_ckpt* c, const dqtg_config* cfgs,
+                            const uint64_t* seeds, uint32_t m, double* quality, double* est) {
+    return guard([&] {
+        LOCK(&h->e);
+        ::dqtg::eval_batch(h->e, c->c, cfgs, seeds, m, quality, est);
+    });
+}
+
+// ---- clustering --------------------------------------------------------------------
+dqtg_status dqtg_approx_kmeans(dqtg_engine* h, const float* values, uint64_t n, uint32_t k,
+                               double sigma, double alpha, uint64_t seed, float* cb,
+                               uint32_t* len) {
+    return guard([&] {
+        LOCK(&h->e);
+        ::dqtg::approx_kmeans(h->e, values, n, k, sigma, alpha, seed, cb, len);
+    });
+}
+
+dqtg_status dqtg_kmeanspp_init(dqtg_engine* h, const double* pts, const double* w, uint64_t n,
+                               uint32_t k, uint64_t seed, double* centers) {
+    return guard([&] {
+        LOCK(&h->e);
+        kmeanspp_host_api(h->e, pts, w, n, k, seed, centers);
+    });
+}
+
+dqtg_status dqtg_lloyd(dqtg_engine* h, const double* pts, const double* w, uint64_t n,
+                       double* centers, uint32_t k, double tol, uint32_t max_iter,
+                       uint32_t* iters) {
+    return guard([&] {
+        LOCK(&h->e);
+        lloyd_host_api(h->e, pts, w, n, centers, k, tol, max_iter, iters);
+    });
+}
+
+dqtg_status dqtg_sq_loss(dqtg_engine* h, const double* pts, const double* w, uint64_t n,
+                         const double* centers, uint32_t k, double* loss) {
+    return guard([&] {
+        LOCK(&h->e);
+        *loss = sq_loss_host_api(h->e, pts, w, n, centers, k);
+    });
+}
+
+// ---- codec primitives -----------------------------------------------------------------
+dqtg_status dqtg_delta_compute(dqtg_engine* h, const uint16_t* prev, const uint16_t* cur,
+                               uint64_t n, uint32_t B, uint16_t* out) {
+    return guard([&] {
+        LOCK(&h->e);
+        delta_kernel_api(h->e, prev, cur, n, B, out, false);
+    });
+}
+
+dqtg_status dqtg_delta_apply(dqtg_engine* h, const uint16_t* prev, const uint16_t* d, uint64_t n,
+                             uint32_t B, uint16_t* out) {
+    return guard([&] {
+        LOCK(&h->e);
+        delta_kernel_api(h->e, prev, d, n, B, out, true);
+    });
+}
+
+dqtg_status dqtg_crc32(dqtg_engine* h, const uint8_t* data, uint64_t n, uint32_t* crc) {
+    return guard([&] {
+        LOCK(&h->e);
+        Engine& e = h->e;
+        const uint8_t* d = data;
+        if (n && !is_device_ptr(data)) {
+            uint8_t* b = (uint8_t*)e.buf("crc.in", n);
+            e.to_device(b, data, n);
+            d = b;
+        }
+        *crc = crc32_device(e, d, n);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,1290 @@
+// encode_delta_record on the device (codec.cpp:12-460).
+//
+// Per 4096-element tile of a tensor (one CTA):
+//   E1  cyclic delta (codec.cpp:12-24), stable group-by of the deltas on the
+//       previous level inside the tile (rearrange, codec.cpp:39-54) with a
+//       ballot-based radix rank, run detection inside each group segment
+//       (rle_encode, codec.cpp:79-90), symbol frequencies of runs that are
+//       interior to the segment, CRC-32 of the target levels (combine algebra)
+//   S   per (tensor, group): resolves runs that cross tile boundaries with a
+//       forward "last value" scan and a backward run-monoid suffix scan
+//   H   per (tensor, group): canonical Huffman (codec.cpp:137-214) with the
+//       reference's (frequency, insertion order) tie-break via two queues
+//   E2a bits per (tile, group); S2 scans them across tiles
+//   L   record layout (varint sizes, protected entries, group headers)
+//   W   header/table/protected writers; E2b MSB-first bit emission into the
+//       final record buffer (codec.cpp:111-122)
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "crc.cuh"
+#include "engine.h"
+#include "quantize_api.h"
+
+namespace dqtg {
+
+constexpr int kCB = 256;   // threads per codec CTA
+constexpr int kLD = 64;    // dense run-length slots: lengths 2..63
+constexpr int kMaxB = 64;  // cyclic alphabet supported by the shared-memory codec
+constexpr int kIt = kTile / kCB;  // 16 elements per thread
+
+__constant__ uint32_t c_crc_pw[kCB];   // x^(8*32*(255-t)) mod P
+__constant__ uint32_t c_crc_x2n[32];
+
+struct Seg {
+    uint32_t n, lead, trail, run_begin, run_end;
+    uint16_t fv, lv;
+    uint32_t cont;
+    uint32_t pad;
+    unsigned long long lead_total, trail_total;
+};
+
+struct EncArgs {
+    const Tile* tiles;
+    const uint8_t* types;
+    const uint64_t* off;
+    const uint64_t* stream_off;
+    const uint32_t* tile0;
+    uint64_t N;
+    uint32_t B, NS;
+    const uint16_t* prev;  // null: FULL record (all-zero base)
+    const uint16_t* cur;
+    Seg* segs;                       // [tile][B]
+    unsigned long long* runs;        // [tile][kTile]: v | b<<16 | len<<32
+    uint32_t* tile_nruns;
+    uint32_t* freq;                  // [tensor][B][NS]
+    unsigned long long* ov;          // overflow run lengths: (tensor*B+b)<<32 | len
+    unsigned long long* ov_count;
+    unsigned long long ov_cap;
+    uint32_t* crc_acc;
+    uint32_t* err;
+};
+
+__device__ __forceinline__ uint32_t uvlen(unsigned long long v) {
+    uint32_t n = 1;
+    while (v >= 0x80) {
+        v >>= 7;
+        ++n;
+    }
+    return n;
+}
+__device__ __forceinline__ unsigned long long zigzag(long long v) {
+    return ((unsigned long long)v << 1) ^ (unsigned long long)(v >> 63);
+}
+__device__ __forceinline__ uint32_t put_uv(uint8_t* p, unsigned long long v) {
+    uint32_t n = 0;
+    while (v >= 0x80) {
+        p[n++] = (uint8_t)(v | 0x80);
+        v >>= 7;
+    }
+    p[n++] = (uint8_t)v;
+    return n;
+}
+
+__device__ __forceinline__ void add_symbol(uint32_t* f, uint32_t NS, uint32_t B, uint32_t tb,
+                                           uint32_t v, unsigned long long L, const EncArgs& A) {
+    atomicAdd(f + v, 1u);
+    if (L > 1) {
+        if (L < (unsigned long long)kLD) {
+            atomicAdd(f + B + (uint32_t)L, 1u);
+        } else {
+            unsigned long long slot = atomicAdd(A.ov_count, 1ull);
+            if (slot < A.ov_cap) A.ov[slot] = ((unsigned long long)tb << 32) | L;
+            else atomicOr(A.err, kErrCorruptIndex);
+        }
+    }
+}
+
+// ---- E1 --------------------------------------------------------------------
+template <bool HAS_BASE>
+__global__ void __launch_bounds__(kCB) enc_tile_kernel(EncArgs A) {
+    extern __shared__ uint32_t dyn[];
+    uint32_t* s_freq = dyn;  // B*NS
+    uint16_t* s_key = (uint16_t*)(s_freq + A.B * A.NS);
+    uint16_t* s_d = s_key + kTile;
+    uint16_t* s_cur = s_d + kTile;
+    uint16_t* s_sd = s_cur + kTile;
+    uint16_t* s_sk = s_sd + kTile;
+    uint16_t* s_hp = s_sk + kTile;  // kTile + 2
+    __shared__ uint32_t s_cnt[kMaxB], s_start[kMaxB], s_running[kMaxB], s_run0[kMaxB],
+        s_run1[kMaxB];
+    __shared__ uint32_t s_wcnt[kCB / 32][kMaxB];
+    __shared__ uint32_t s_tab[256];
+    __shared__ uint32_t s_red[kCB / 32];
+    __shared__ unsigned long long s_scan[33];
+
+    const int ti = blockIdx.x;
+    const Tile T = A.tiles[ti];
+    const uint32_t cnt = T.count, B = A.B, NS = A.NS;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+    for (uint32_t i = tid; i < B * NS; i += kCB) s_freq[i] = 0;
+    if (tid < (int)B) {
+        s_cnt[tid] = 0;
+        s_running[tid] = 0;
+        for (int w = 0; w < kCB / 32; ++w) s_wcnt[w][tid] = 0;
+    }
+    {  // CRC byte table (codec.cpp:276-284)
+        uint32_t c = tid;
+        for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xedb88320u ^ (c >> 1) : c >> 1;
+        s_tab[tid] = c;
+    }
+    // load 16 consecutive elements per thread
+    {
+        const uint32_t e0 = tid * kIt;
+        if (e0 < cnt) {
+            uint16_t c16[kIt], p16[kIt];
+            const uint4* cp = (const uint4*)(A.cur + T.start + e0);
+            uint4 a0 = cp[0], a1 = cp[1];
+            memcpy(c16, &a0, 16);
+            memcpy(c16 + 8, &a1, 16);
+            if (HAS_BASE) {
+                const uint4* pp = (const uint4*)(A.prev + T.start + e0);
+                uint4 b0 = pp[0], b1 = pp[1];
+                memcpy(p16, &b0, 16);
+                memcpy(p16 + 8, &b1, 16);
+            }
+            bool bad = false;
+#pragma unroll
+            for (int j = 0; j < kIt; ++j) {
+                const uint32_t e = e0 + j;
+                if (e < cnt) {
+                    uint32_t c = c16[j], p = HAS_BASE ? p16[j] : 0u;
+                    bad |= (p >= B) | (c >= B);
+                    uint32_t d = p >= c ? p - c : p + B - c;
+                    s_key[e] = (uint16_t)(p < B ? p : 0u);
+                    s_d[e] = (uint16_t)d;
+                    s_cur[e] = (uint16_t)c;
+                }
+            }
+            if (bad) atomicOr(A.err, kErrCorruptIndex);
+        }
+    }
+    __syncthreads();
+
+    // ---- CRC of the target levels, tile right-aligned in a virtual 8 KiB block
+    {
+        const int lead0 = 2 * (int)kTile - 2 * (int)cnt;
+        uint32_t r = 0;
+        for (int vb = tid * 32; vb < tid * 32 + 32; ++vb) {
+            int rb = vb - lead0;
+            if (rb < 0) continue;
+            uint32_t lv = s_cur[rb >> 1];
+            uint32_t byte = (rb & 1) ? (lv >> 8) : (lv & 0xff);
+            r = s_tab[(r ^ byte) & 0xff] ^ (r >> 8);
+        }
+        r = r ? crc_multmodp(c_crc_pw[tid], r) : 0u;
+        r = warp_xor(r);
+        if (lane == 0) s_red[wid] = r;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t x = 0;
+            for (int w = 0; w < kCB / 32; ++w) x ^= s_red[w];
+            const uint64_t local = T.start - A.off[T.tensor];
+            const uint64_t end = A.stream_off[T.tensor] + local + cnt;
+            x = crc_shift(c_crc_x2n, x, 2 * (A.N - end));
+            if (x) atomicXor(A.crc_acc, x);
+        }
+    }
+
+    // ---- stable group-by on the previous level (rearrange)
+    for (uint32_t e = tid; e < cnt; e += kCB) atomicAdd(&s_cnt[s_key[e]], 1u);
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t run = 0;
+        for (uint32_t b0 = 0; b0 < B; b0 += 32) {
+            uint32_t b = b0 + lane;
+            uint32_t v = b < B ? s_cnt[b] : 0, x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (b < B) s_start[b] = run + x - v;
+            run += __shfl_sync(0xffffffffu, x, 31);
+        }
+    }
+    __syncthreads();
+    const int nbits = B <= 1 ? 1 : 32 - __clz((int)(B - 1));
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (int r = 0; r < kIt; ++r) {
+        const uint32_t base = r * kCB;
+        if (base >= cnt) break;
+        const uint32_t e = base + tid;
+        const bool valid = e < cnt;
+        const uint32_t key = valid ? s_key[e] : 0u;
+        uint32_t peers = __ballot_sync(0xffffffffu, valid);
+        for (int bit = 0; bit < nbits; ++bit) {
+            uint32_t on = (key >> bit) & 1u;
+            uint32_t bb = __ballot_sync(0xffffffffu, valid && on);
+            peers &= on ? bb : ~bb;
+        }
+        const uint32_t rank = __popc(peers & lt_mask);
+        if (valid && rank == 0) s_wcnt[wid][key] = __popc(peers);
+        __syncthreads();
+        if (valid) {
+            uint32_t o = s_running[key];
+            for (int w = 0; w < wid; ++w) o += s_wcnt[w][key];
+            const uint32_t pos = s_start[key] + o + rank;
+            s_sd[pos] = s_d[e];
+            s_sk[pos] = (uint16_t)key;
+        }
+        __syncthreads();
+        if (tid < (int)B) {
+            uint32_t t = 0;
+            for (int w = 0; w < kCB / 32; ++w) {
+                t += s_wcnt[w][tid];
+                s_wcnt[w][tid] = 0;
+            }
+            s_running[tid] += t;
+        }
+        __syncthreads();
+    }
+
+    // ---- runs inside group segments
+    uint32_t nh = 0;
+    uint32_t hmask = 0;
+    {
+        const uint32_t p0 = tid * kIt;
+        for (int j = 0; j < kIt; ++j) {
+            const uint32_t p = p0 + j;
+            if (p >= cnt) break;
+            const uint32_t b = s_sk[p];
+            const bool head = (p == s_start[b]) || (s_sd[p] != s_sd[p - 1]);
+            if (head) {
+                hmask |= 1u << j;
+                ++nh;
+            }
+        }
+    }
+    unsigned long long R;
+    unsigned long long hex = block_exclusive_scan<unsigned long long>(nh, s_scan, &R);
+    {
+        uint32_t r = (uint32_t)hex;
+        const uint32_t p0 = tid * kIt;
+        for (int j = 0; j < kIt; ++j)
+            if (hmask >> j & 1) s_hp[r++] = (uint16_t)(p0 + j);
+    }
+    if (tid == 0) s_hp[R] = (uint16_t)cnt;
+    __syncthreads();
+    unsigned long long* runs = A.runs + (size_t)ti * kTile;
+    for (uint32_t r = tid; r < R; r += kCB) {
+        const uint32_t p = s_hp[r], L = s_hp[r + 1] - p;
+        const uint32_t v = s_sd[p], b = s_sk[p];
+        runs[r] = (unsigned long long)v | ((unsigned long long)b << 16) |
+                  ((unsigned long long)L << 32);
+        if (p == s_start[b]) s_run0[b] = r;
+        if (p + L == s_start[b] + s_cnt[b]) s_run1[b] = r;
+    }
+    __syncthreads();
+    const uint32_t tensor = T.tensor;
+    for (uint32_t r = tid; r < R; r += kCB) {
+        const uint32_t p = s_hp[r], L = s_hp[r + 1] - p;
+        const uint32_t v = s_sd[p], b = s_sk[p];
+        if (r != s_run0[b] && r != s_run1[b])
+            add_symbol(s_freq + b * NS, NS, B, tensor * B + b, v, L, A);
+    }
+    if (tid == 0) A.tile_nruns[ti] = (uint32_t)R;
+    __syncthreads();
+    for (uint32_t b = tid; b < B; b += kCB) {
+        Seg S{};
+        S.n = s_cnt[b];
+        if (S.n) {
+            const uint32_t st = s_start[b];
+            S.fv = s_sd[st];
+            S.lv = s_sd[st + S.n - 1];
+            S.run_begin = s_run0[b];
+            S.run_end = s_run1[b] + 1;
+            S.lead = s_hp[S.run_begin + 1] - s_hp[S.run_begin];
+            S.trail = s_hp[S.run_end] - s_hp[S.run_end - 1];
+        }
+        A.segs[(size_t)ti * B + b] = S;
+    }
+    uint32_t* gf = A.freq + (size_t)tensor * B * NS;
+    for (uint32_t i = tid; i < B * NS; i += kCB) {
+        uint32_t c = s_freq[i];
+        if (c) atomicAdd(gf + i, c);
+    }
+}
+
+// ---- S: cross-tile run resolution per (tensor, group) --------------------------
+struct RunM {  // run-length monoid over a concatenation of segments
+    unsigned long long n, lead;
+    uint32_t fv, lv;
+    uint32_t single;  // whole concatenation is one run
+};
+
+__device__ __forceinline__ RunM runm_combine(const RunM& a, const RunM& b) {
+    if (!a.n) return b;
+    if (!b.n) return a;
+    RunM r;
+    r.n = a.n + b.n;
+    r.fv = a.fv;
+    r.lv = b.lv;
+    const bool join = a.single && a.lv == b.fv;
+    r.single = join && b.single;
+    r.lead = join ? a.n + b.lead : a.lead;
+    return r;
+}
+
+__global__ void __launch_bounds__(kCB) enc_resolve_kernel(EncArgs A) {
+    extern __shared__ uint32_t s_f[];  // NS
+    __shared__ RunM s_m[kCB];
+    __shared__ int s_last[kCB];
+    const uint32_t B = A.B, NS = A.NS;
+    const uint32_t t = blockIdx.x / B, b = blockIdx.x % B;
+    const int tid = threadIdx.x;
+    const uint32_t a0 = A.tile0[t], a1 = A.tile0[t + 1];
+    for (uint32_t i = tid; i < NS; i += kCB) s_f[i] = 0;
+    // forward: lv of the nearest earlier non-empty segment
+    int carry_last = -1;
+    for (uint32_t c0 = a0; c0 < a1; c0 += kCB) {
+        const uint32_t i = c0 + tid;
+        int idx = (i < a1 && A.segs[(size_t)i * B + b].n) ? (int)i : -1;
+        s_last[tid] = idx;
+        __syncthreads();
+        for (int o = 1; o < kCB; o <<= 1) {
+            int v = tid >= o ? s_last[tid - o] : -1;
+            __syncthreads();
+            if (v > s_last[tid]) s_last[tid] = v;
+            __syncthreads();
+        }
+        int prev = tid ? s_last[tid - 1] : -1;
+        if (prev < carry_last) prev = carry_last;
+        if (idx >= 0) {
+            Seg& S = A.segs[(size_t)i * B + b];
+            S.cont = prev >= 0 && A.segs[(size_t)prev * B + b].lv == S.fv;
+        }
+        int cl = s_last[kCB - 1];
+        __syncthreads();
+        if (cl > carry_last) carry_last = cl;
+    }
+    __syncthreads();
+    // backward: suffix run monoid gives the extension of each trailing run
+    RunM carry{};
+    const uint32_t ntl = a1 - a0;
+    const uint32_t nch = (ntl + kCB - 1) / kCB;
+    uint32_t* f = s_f;
+    const uint32_t tb = t * B + b;
+    for (int ch = (int)nch - 1; ch >= 0; --ch) {
+        const uint32_t i = a0 + ch * kCB + tid;
+        RunM m{};
+        Seg S{};
+        if (i < a1) {
+            S = A.segs[(size_t)i * B + b];
+            if (S.n) {
+                m.n = S.n;
+                m.fv = S.fv;
+                m.lv = S.lv;
+                m.single = S.lead == S.n;
+                m.lead = S.lead;
+            }
+        }
+        s_m[tid] = m;
+        __syncthreads();
+        for (int o = 1; o < kCB; o <<= 1) {  // inclusive suffix
+            RunM nb = tid + o < kCB ? s_m[tid + o] : RunM{};
+            __syncthreads();
+            s_m[tid] = runm_combine(s_m[tid], nb);
+            __syncthreads();
+        }
+        RunM after = tid + 1 < kCB ? runm_combine(s_m[tid + 1], carry) : carry;
+        if (i < a1 && S.n) {
+            unsigned long long E = (after.n && after.fv == S.lv) ? after.lead : 0ull;
+            const bool single = S.lead == S.n;
+            Seg& G = A.segs[(size_t)i * B + b];
+            if (single) {
+                G.lead_total = G.trail_total = S.n + E;
+                if (!S.cont) add_symbol(f, NS, B, tb, S.fv, S.n + E, A);
+            } else {
+                G.lead_total = S.lead;
+                G.trail_total = S.trail + E;
+                if (!S.cont) add_symbol(f, NS, B, tb, S.fv, S.lead, A);
+                add_symbol(f, NS, B, tb, S.lv, S.trail + E, A);
+            }
+        }
+        RunM chunk = s_m[0];
+        __syncthreads();
+        carry = runm_combine(chunk, carry);
+    }
+    __syncthreads();
+    uint32_t* gf = A.freq + (size_t)tb * NS;
+    for (uint32_t i = tid; i < NS; i += kCB)
+        if (s_f[i]) gf[i] += s_f[i];
+}
+
+// ---- overflow run lengths: sorted unique (key, count) ------------------------------
+__global__ void ov_unique_kernel(const unsigned long long* sorted, unsigned long long n,
+                                 unsigned long long* ukey, unsigned long long* uhead,
+                                 unsigned long long* nu) {
+    __shared__ unsigned long long s_scan[33];
+    unsigned long long base = 0;
+    for (unsigned long long c0 = 0; c0 < n; c0 += blockDim.x) {
+        unsigned long long i = c0 + threadIdx.x;
+        unsigned long long h = (i < n && (i == 0 || sorted[i] != sorted[i - 1])) ? 1ull : 0ull;
+        unsigned long long tot;
+        unsigned long long ex = block_exclusive_scan<unsigned long long>(h, s_scan, &tot);
+        if (h) {
+            ukey[base + ex] = sorted[i];
+            uhead[base + ex] = i;
+        }
+        base += tot;
+    }
+    if (threadIdx.x == 0) *nu = base;
+}
+
+__global__ void ov_counts_kernel(const unsigned long long* uhead, const unsigned long long* nu_p,
+                                 unsigned long long n, unsigned long long* ucnt) {
+    const unsigned long long nu = *nu_p;
+    for (unsigned long long j = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; j < nu;
+         j += (unsigned long long)gridDim.x * blockDim.x)
+        ucnt[j] = (j + 1 < nu ? uhead[j + 1] : n) - uhead[j];
+}
+
+// ---- H: canonical Huffman per (tensor, group) -------------------------------------
+struct GroupInfo {
+    unsigned long long n_elems, nsyms, bits, nbytes;
+    unsigned long long tab_base;  // first table entry
+    uint32_t tsize, hdr;          // hdr: header bytes excluding uvarint(nbytes)
+    unsigned long long ov_begin, ov_end;
+    unsigned long long pay;       // record byte offset of the bitstream
+    unsigned long long gbytes;    // full group size in the record
+};
+
+__device__ __forceinline__ unsigned long long lb_u64(const unsigned long long* a,
+                                                     unsigned long long n,
+                                                     unsigned long long key) {
+    unsigned long long lo = 0, hi = n;
+    while (lo < hi) {
+        unsigned long long m = (lo + hi) >> 1;
+        if (a[m] < key) lo = m + 1;
+        else hi = m;
+    }
+    return lo;
+}
+
+struct HufWork {
+    long long* sym;             // [tab_base + i]
+    unsigned long long* f;      // [tab_base + i]
+    uint32_t* perm;             // [tab_base + i]
+    unsigned long long* nodef;  // [2*tab_base + 2*tb + j]
+    uint32_t* parent;
+    uint32_t* depth;
+};
+
+__global__ void ov_group_max_kernel(const unsigned long long* ukey, const unsigned long long* nu_p,
+                                    uint32_t ngroups, uint32_t* max_nov) {
+    const unsigned long long nu = *nu_p;
+    for (uint32_t tb = blockIdx.x * blockDim.x + threadIdx.x; tb < ngroups;
+         tb += gridDim.x * blockDim.x) {
+        unsigned long long a = lb_u64(ukey, nu, (unsigned long long)tb << 32);
+        unsigned long long b = lb_u64(ukey, nu, (unsigned long long)(tb + 1) << 32);
+        if (b > a) atomicMax(max_nov, (uint32_t)(b - a));
+    }
+}
+
+__global__ void __launch_bounds__(128) enc_huffman_kernel(EncArgs A, const unsigned long long* elems,
+                                                          const unsigned long long* ukey,
+                                                          const unsigned long long* ucnt,
+                                                          const unsigned long long* nu_p,
+                                                          GroupInfo* gi, long long* tab_sym,
+                                                          uint8_t* tab_len,
+                                                          unsigned long long* code_dense,
+                                                          uint8_t* len_dense,
+                                                          unsigned long long* code_ov,
+                                                          uint8_t* len_ov, HufWork W,
+                                                          uint32_t n_pad) {
+    extern __shared__ unsigned long long s_keys[];  // n_pad
+    const uint32_t B = A.B, NS = A.NS;
+    const uint32_t tb = blockIdx.x, b = tb % B;
+    GroupInfo G{};
+    G.n_elems = elems[tb];
+    const unsigned long long nu = *nu_p;
+    G.ov_begin = lb_u64(ukey, nu, (unsigned long long)tb << 32);
+    G.ov_end = lb_u64(ukey, nu, (unsigned long long)(tb + 1) << 32);
+    const uint32_t nov = (uint32_t)(G.ov_end - G.ov_begin);
+    G.tab_base = (unsigned long long)tb * NS + G.ov_begin;
+    long long* sym = W.sym + G.tab_base;
+    unsigned long long* f = W.f + G.tab_base;
+    uint32_t* perm = W.perm + G.tab_base;
+    unsigned long long* nodef = W.nodef + 2 * G.tab_base + 2ull * tb;
+    uint32_t* parent = W.parent + 2 * G.tab_base + 2ull * tb;
+    uint32_t* depth = W.depth + 2 * G.tab_base + 2ull * tb;
+    (void)nov;
+    __shared__ uint32_t s_n;
+    const uint32_t* fr = A.freq + (size_t)tb * NS;
+    if (threadIdx.x == 0) {
+        uint32_t n = 0;
+        if (G.n_elems) {
+            for (int v = (int)B - 1; v >= 0; --v)  // symbols -(B-1) .. 0 ascending
+                if (fr[v]) {
+                    sym[n] = -(long long)v;
+                    f[n++] = fr[v];
+                }
+            for (uint32_t L = 2; L < (uint32_t)kLD; ++L)
+                if (fr[B + L]) {
+                    sym[n] = (long long)L;
+                    f[n++] = fr[B + L];
+                }
+            for (unsigned long long j = G.ov_begin; j < G.ov_end; ++j) {
+                sym[n] = (long long)(ukey[j] & 0xffffffffull);
+                f[n++] = ucnt[j];
+            }
+        }
+        s_n = n;
+    }
+    __syncthreads();
+    const uint32_t n = s_n;
+    if (n == 0) {
+        if (threadIdx.x == 0) gi[tb] = G;
+        return;
+    }
+    // stable order by (frequency, insertion order): bitonic sort of f<<24|index
+    uint32_t np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    for (uint32_t i = threadIdx.x; i < np2; i += blockDim.x)
+        s_keys[i] = i < n ? ((f[i] << 24) | i) : ~0ull;
+    __syncthreads();
+    for (uint32_t k = 2; k <= np2; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < np2; i += blockDim.x) {
+                uint32_t ixj = i ^ j;
+                if (ixj > i) {
+                    unsigned long long a = s_keys[i], c = s_keys[ixj];
+                    bool up = (i & k) == 0;
+                    if ((a > c) == up) {
+                        s_keys[i] = c;
+                        s_keys[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) perm[r] = (uint32_t)(s_keys[r] & 0xffffffu);
+    __syncthreads();
+    (void)n_pad;
+    if (threadIdx.x == 0) {
+        unsigned long long nsyms = 0;
+        for (uint32_t i = 0; i < n; ++i) nsyms += f[i];
+        G.nsyms = nsyms;
+        if (n == 1) {
+            depth[0] = 1;
+        } else {
+            // two queues == the reference's priority queue on (f, order)
+            for (uint32_t i = 0; i < n; ++i) nodef[i] = f[i];
+            uint32_t q1 = 0, q2 = n, made = n;
+            auto take = [&]() -> uint32_t {
+                bool use1;
+                if (q1 >= n) use1 = false;
+                else if (q2 >= made) use1 = true;
+                else {
+                    uint32_t a = perm[q1], c = q2;
+                    use1 = nodef[a] < nodef[c] || (nodef[a] == nodef[c] && a < c);
+                }
+                return use1 ? perm[q1++] : q2++;
+            };
+            for (uint32_t s = 0; s + 1 < n; ++s) {
+                uint32_t x = take(), y = take();
+                nodef[made] = nodef[x] + nodef[y];
+                parent[x] = parent[y] = made;
+                ++made;
+            }
+            const uint32_t root = made - 1;
+            depth[root] = 0;
+            bool overflow = false;
+            for (int i = (int)root - 1; i >= 0; --i) {
+                depth[i] = depth[parent[i]] + 1;
+                if ((uint32_t)i >= n && depth[i] >= 63) overflow = true;
+            }
+            if (overflow) atomicOr(A.err, kErrHuffmanDepth);
+        }
+        // table sorted by (len, sym): counting sort over lengths, stable in sym order
+        uint32_t hist[65];
+        for (int l = 0; l < 65; ++l) hist[l] = 0;
+        for (uint32_t i = 0; i < n; ++i) hist[depth[i] < 64 ? depth[i] : 64]++;
+        uint32_t at[65], acc = 0;
+        for (int l = 0; l < 65; ++l) {
+            at[l] = acc;
+            acc += hist[l];
+        }
+        unsigned long long code = 0;
+        uint32_t hdr = 0;
+        for (uint32_t i = 0; i < n; ++i) perm[at[depth[i] < 64 ? depth[i] : 64]++] = i;
+        uint32_t prev_len = depth[perm[0]];
+        for (uint32_t o = 0; o < n; ++o) {
+            const uint32_t i = perm[o];
+            const uint32_t len = depth[i];
+            code <<= (len - prev_len);
+            prev_len = len;
+            tab_sym[G.tab_base + o] = sym[i];
+            tab_len[G.tab_base + o] = (uint8_t)len;
+            hdr += uvlen(zigzag(sym[i])) + 1;
+            const long long s = sym[i];
+            if (s <= 0) {
+                code_dense[(size_t)tb * NS + (uint32_t)(-s)] = code;
+                len_dense[(size_t)tb * NS + (uint32_t)(-s)] = (uint8_t)len;
+            } else if (s < kLD) {
+                code_dense[(size_t)tb * NS + B + (uint32_t)s] = code;
+                len_dense[(size_t)tb * NS + B + (uint32_t)s] = (uint8_t)len;
+            } else {
+                unsigned long long j = lb_u64(ukey + G.ov_begin, nov,
+                                              ((unsigned long long)tb << 32) | (unsigned long long)s);
+                code_ov[G.ov_begin + j] = code;
+                len_ov[G.ov_begin + j] = (uint8_t)len;
+            }
+            ++code;
+        }
+        G.tsize = n;
+        G.hdr = hdr + uvlen(b) + uvlen(G.n_elems) + uvlen(G.nsyms) + uvlen(n);
+        gi[tb] = G;
+    }
+}
+
+// ---- symbol walk shared by E2a / E2b ---------------------------------------------
+struct CodeTabs {
+    const unsigned long long* code_dense;
+    const uint8_t* len_dense;
+    const unsigned long long* ukey;
+    const unsigned long long* code_ov;
+    const uint8_t* len_ov;
+    const GroupInfo* gi;
+};
+
+__device__ __forceinline__ void code_of(const CodeTabs& C, uint32_t tb, uint32_t NS, uint32_t slot,
+                                        unsigned long long& code, uint32_t& len) {
+    code = C.code_dense[(size_t)tb * NS + slot];
+    len = C.len_dense[(size_t)tb * NS + slot];
+}
+
+__device__ __forceinline__ void code_of_len(const CodeTabs& C, uint32_t tb, uint32_t NS,
+                                            uint32_t B, unsigned long long L,
+                                            unsigned long long& code, uint32_t& len) {
+    if (L < (unsigned long long)kLD) {
+        code_of(C, tb, NS, B + (uint32_t)L, code, len);
+    } else {
+        const GroupInfo& G = C.gi[tb];
+        unsigned long long j = G.ov_begin + lb_u64(C.ukey + G.ov_begin, G.ov_end - G.ov_begin,
+                                                   ((unsigned long long)tb << 32) | L);
+        code = C.code_ov[j];
+        len = C.len_ov[j];
+    }
+}
+
+// Owned (value, length) of run r of the tile, or L = 0 when the run continues an
+// earlier one.
+__device__ __forceinline__ void owned_run(const EncArgs& A, const Seg* segs, unsigned long long rw,
+                                          uint32_t r, uint32_t& v, uint32_t& b,
+                                          unsigned long long& L) {
+    v = (uint32_t)(rw & 0xffff);
+    b = (uint32_t)((rw >> 16) & 0xffff);
+    L = rw >> 32;
+    const Seg& S = segs[b];
+    if (r == S.run_begin) {
+        if (S.cont) {
+            L = 0;
+            return;
+        }
+        if (S.run_end == S.run_begin + 1) L = S.lead_total;
+    } else if (r + 1 == S.run_end) {
+        L = S.trail_total;
+    }
+}
+
+// E2a: bits per (tile, group)
+__global__ void __launch_bounds__(kCB) enc_bits_kernel(EncArgs A, CodeTabs C,
+                                                       unsigned long long* segbits) {
+    __shared__ unsigned long long s_bits[kMaxB];
+    const int ti = blockIdx.x;
+    const uint32_t B = A.B, NS = A.NS;
+    const Tile T = A.tiles[ti];
+    for (uint32_t b = threadIdx.x; b < B; b += kCB) s_bits[b] = 0;
+    __syncthreads();
+    const uint32_t R = A.tile_nruns[ti];
+    const Seg* segs = A.segs + (size_t)ti * B;
+    const unsigned long long* runs = A.runs + (size_t)ti * kTile;
+    for (uint32_t r = threadIdx.x; r < R; r += kCB) {
+        uint32_t v, b;
+        unsigned long long L;
+        owned_run(A, segs, runs[r], r, v, b, L);
+        if (!L) continue;
+        const uint32_t tb = T.tensor * B + b;
+        unsigned long long c;
+        uint32_t l1, l2 = 0;
+        code_of(C, tb, NS, v, c, l1);
+        if (L > 1) code_of_len(C, tb, NS, B, L, c, l2);
+        atomicAdd(&s_bits[b], (unsigned long long)(l1 + l2));
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < B; b += kCB) segbits[(size_t)ti * B + b] = s_bits[b];
+}
+
+// S2: exclusive scan of segment bits across the tensor's tiles
+__global__ void __launch_bounds__(kCB) enc_bitscan_kernel(EncArgs A, unsigned long long* segbits,
+                                                          GroupInfo* gi) {
+    __shared__ unsigned long long s_scan[33];
+    const uint32_t B = A.B;
+    const uint32_t t = blockIdx.x / B, b = blockIdx.x % B;
+    const uint32_t a0 = A.tile0[t], a1 = A.tile0[t + 1];
+    unsigned long long base = 0;
+    for (uint32_t c0 = a0; c0 < a1; c0 += kCB) {
+        const uint32_t i = c0 + threadIdx.x;
+        unsigned long long v = i < a1 ? segbits[(size_t)i * B + b] : 0ull, tot;
+        unsigned long long ex = block_exclusive_scan<unsigned long long>(v, s_scan, &tot);
+        if (i < a1) segbits[(size_t)i * B + b] = base + ex;
+        base += tot;
+    }
+    if (threadIdx.x == 0) {
+        GroupInfo& G = gi[blockIdx.x];
+        G.bits = base;
+        G.nbytes = (base + 7) / 8;
+        G.gbytes = G.n_elems ? G.hdr + uvlen(G.nbytes) + G.nbytes : 0;
+    }
+}
+
+// ---- record layout ---------------------------------------------------------------
+struct TensorRec {
+    unsigned long long static_off, static_len;  // in the host-built static blob
+    unsigned long long prot_begin, prot_end;    // protected entry range
+    unsigned long long size, off;               // record bytes / offset
+    uint32_t ngroups, pad;
+};
+
+__global__ void prot_sizes_kernel(const TensorRec* tr, const uint64_t* ppos,
+                                  unsigned long long* sizes) {
+    const TensorRec R = tr[blockIdx.x];
+    for (unsigned long long i = R.prot_begin + threadIdx.x; i < R.prot_end; i += blockDim.x) {
+        unsigned long long d = i == R.prot_begin ? ppos[i] : ppos[i] - ppos[i - 1];
+        sizes[i] = uvlen(d) + 2;
+    }
+}
+
+__global__ void tensor_size_kernel(EncArgs A, TensorRec* tr, const unsigned long long* prot_scan,
+                                   GroupInfo* gi) {
+    if (threadIdx.x) return;
+    const uint32_t t = blockIdx.x, B = A.B;
+    TensorRec& R = tr[t];
+    unsigned long long s = R.static_len;
+    const unsigned long long np = R.prot_end - R.prot_begin;
+    s += uvlen(np) + (prot_scan[R.prot_end] - prot_scan[R.prot_begin]);
+    uint32_t ng = 0;
+    unsigned long long gs = 0;
+    for (uint32_t b = 0; b < B; ++b) {
+        const GroupInfo& G = gi[t * B + b];
+        if (!G.n_elems) continue;
+        ++ng;
+        gs += G.gbytes;
+    }
+    R.ngroups = ng;
+    R.size = s + uvlen(ng) + gs;
+}
+
+__global__ void tensor_scan_kernel(TensorRec* tr, uint32_t nt, unsigned long long prefix,
+                                   unsigned long long* total) {
+    if (threadIdx.x || blockIdx.x) return;
+    unsigned long long o = prefix;
+    for (uint32_t t = 0; t < nt; ++t) {
+        tr[t].off = o;
+        o += tr[t].size;
+    }
+    *total = o + 4;
+}
+
+// W: per tensor CTA: static prefix, protected entries, group headers + tables.
+__global__ void __launch_bounds__(kCB) write_tensor_kernel(
+    EncArgs A, const TensorRec* tr, const uint8_t* statics, const uint64_t* ppos,
+    const uint16_t* pval, const unsigned long long* prot_scan, GroupInfo* gi,
+    const long long* tab_sym, const uint8_t* tab_len, uint8_t* rec) {
+    __shared__ uint32_t s_pre[kCB / 32];
+    const uint32_t t = blockIdx.x, B = A.B;
+    const TensorRec R = tr[t];
+    uint8_t* p = rec + R.off;
+    for (unsigned long long i = threadIdx.x; i < R.static_len; i += kCB)
+        p[i] = statics[R.static_off + i];
+    unsigned long long o = R.static_len;
+    const unsigned long long np = R.prot_end - R.prot_begin;
+    if (threadIdx.x == 0) put_uv(p + o, np);
+    o += uvlen(np);
+    const unsigned long long pb = prot_scan[R.prot_begin];
+    for (unsigned long long i = R.prot_begin + threadIdx.x; i < R.prot_end; i += kCB) {
+        unsigned long long d = i == R.prot_begin ? ppos[i] : ppos[i] - ppos[i - 1];
+        uint8_t* q = p + o + (prot_scan[i] - pb);
+        uint32_t k = put_uv(q, d);
+        q[k] = (uint8_t)(pval[i] & 0xff);
+        q[k + 1] = (uint8_t)(pval[i] >> 8);
+    }
+    o += prot_scan[R.prot_end] - pb;
+    if (threadIdx.x == 0) put_uv(p + o, R.ngroups);
+    o += uvlen(R.ngroups);
+    // group offsets in ascending bucket order (codec.cpp:312-326)
+    __shared__ unsigned long long s_goff[kMaxB];
+    if (threadIdx.x == 0) {
+        unsigned long long g = o;
+        for (uint32_t b = 0; b < B; ++b) {
+            s_goff[b] = g;
+            g += gi[t * B + b].gbytes;
+        }
+    }
+    __syncthreads();
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (uint32_t b = wid; b < B; b += kCB / 32) {
+        GroupInfo& G = gi[t * B + b];
+        if (!G.n_elems) continue;
+        uint8_t* q = p + s_goff[b];
+        if (lane == 0) {
+            uint32_t k = put_uv(q, b);
+            k += put_uv(q + k, G.n_elems);
+            k += put_uv(q + k, G.nsyms);
+            k += put_uv(q + k, G.tsize);
+            s_pre[wid] = k;
+        }
+        __syncwarp();
+        uint32_t k = s_pre[wid];
+        // table entries: sequential varints; one lane per entry with a warp scan of sizes
+        for (uint32_t e0 = 0; e0 < G.tsize; e0 += 32) {
+            const uint32_t e = e0 + lane;
+            uint32_t sz = 0;
+            unsigned long long zz = 0;
+            if (e < G.tsize) {
+                zz = zigzag(tab_sym[G.tab_base + e]);
+                sz = uvlen(zz) + 1;
+            }
+            uint32_t x = sz;
+            for (int d = 1; d < 32; d <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+                if (lane >= d) x += y;
+            }
+            if (e < G.tsize) {
+                uint8_t* w = q + k + x - sz;
+                uint32_t m = put_uv(w, zz);
+                w[m] = tab_len[G.tab_base + e];
+            }
+            k += __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (lane == 0) {
+            k += put_uv(q + k, G.nbytes);
+            G.pay = (unsigned long long)(q + k - rec);
+        }
+        __syncwarp();
+    }
+}
+
+// E2b: emission, MSB-first, atomicOr into the zeroed record
+__device__ __forceinline__ void put_bits(uint32_t* words, unsigned long long q,
+                                         unsigned long long code, int len) {
+    while (len > 0) {
+        const unsigned long long byte = q >> 3;
+        const int bo = (int)(q & 7), avail = 8 - bo, take = avail < len ? avail : len;
+        const uint32_t bits = (uint32_t)((code >> (len - take)) & ((1ull << take) - 1));
+        const uint32_t bv = bits << (avail - take);
+        atomicOr(words + (byte >> 2), bv << (8 * (uint32_t)(byte & 3)));
+        len -= take;
+        q += take;
+    }
+}
+
+__global__ void __launch_bounds__(kCB) enc_emit_kernel(EncArgs A, CodeTabs C,
+                                                       const unsigned long long* segoff,
+                                                       uint8_t* rec) {
+    __shared__ unsigned long long s_scan[33];
+    __shared__ unsigned long long s_runbits[kTile + 1];
+    const int ti = blockIdx.x;
+    const uint32_t B = A.B, NS = A.NS;
+    const Tile T = A.tiles[ti];
+    const uint32_t R = A.tile_nruns[ti];
+    const Seg* segs = A.segs + (size_t)ti * B;
+    const unsigned long long* runs = A.runs + (size_t)ti * kTile;
+    uint32_t* words = (uint32_t*)rec;
+    // blocked: thread handles runs [16t, 16t+16)
+    unsigned long long mine = 0;
+    const uint32_t r0 = threadIdx.x * kIt;
+    for (int j = 0; j < kIt; ++j) {
+        const uint32_t r = r0 + j;
+        if (r >= R) break;
+        uint32_t v, b;
+        unsigned long long L;
+        owned_run(A, segs, runs[r], r, v, b, L);
+        if (!L) continue;
+        const uint32_t tb = T.tensor * B + b;
+        unsigned long long c;
+        uint32_t l1, l2 = 0;
+        code_of(C, tb, NS, v, c, l1);
+        if (L > 1) code_of_len(C, tb, NS, B, L, c, l2);
+        mine += l1 + l2;
+    }
+    unsigned long long tot;
+    unsigned long long ex = block_exclusive_scan<unsigned long long>(mine, s_scan, &tot);
+    // per-run exclusive bit offsets
+    {
+        unsigned long long acc = ex;
+        for (int j = 0; j < kIt; ++j) {
+            const uint32_t r = r0 + j;
+            if (r >= R) break;
+            s_runbits[r] = acc;
+            uint32_t v, b;
+            unsigned long long L;
+            owned_run(A, segs, runs[r], r, v, b, L);
+            if (!L) continue;
+            const uint32_t tb = T.tensor * B + b;
+            unsigned long long c;
+            uint32_t l1, l2 = 0;
+            code_of(C, tb, NS, v, c, l1);
+            if (L > 1) code_of_len(C, tb, NS, B, L, c, l2);
+            acc += l1 + l2;
+        }
+    }
+    __syncthreads();
+    for (int j = 0; j < kIt; ++j) {
+        const uint32_t r = r0 + j;
+        if (r >= R) break;
+        uint32_t v, b;
+        unsigned long long L;
+        owned_run(A, segs, runs[r], r, v, b, L);
+        if (!L) continue;
+        const uint32_t tb = T.tensor * B + b;
+        const Seg& S = segs[b];
+        unsigned long long q = C.gi[tb].pay * 8 + segoff[(size_t)ti * B + b] +
+                               (s_runbits[r] - s_runbits[S.run_begin]);
+        unsigned long long c;
+        uint32_t l;
+        code_of(C, tb, NS, v, c, l);
+        put_bits(words, q, c, (int)l);
+        q += l;
+        if (L > 1) {
+            code_of_len(C, tb, NS, B, L, c, l);
+            put_bits(words, q, c, (int)l);
+        }
+    }
+}
+
+__global__ void finish_crc_kernel(const uint32_t* acc, unsigned long long total_bytes,
+                                  uint8_t* dst, uint32_t* crc_out) {
+    if (threadIdx.x || blockIdx.x) return;
+    uint32_t c = *acc ^ crc_shift(c_crc_x2n, 0xffffffffu, total_bytes) ^ 0xffffffffu;
+    if (dst) {
+        dst[0] = (uint8_t)c;
+        dst[1] = (uint8_t)(c >> 8);
+        dst[2] = (uint8_t)(c >> 16);
+        dst[3] = (uint8_t)(c >> 24);
+    }
+    if (crc_out) *crc_out = c;
+}
+
+// ---- host ------------------------------------------------------------------------
+static void put_le(std::vector<uint8_t>& v, uint64_t x, int n) {
+    for (int i = 0; i < n; ++i) v.push_back((uint8_t)(x >> (8 * i)));
+}
+static void put_f64(std::vector<uint8_t>& v, double d) {
+    uint64_t b;
+    memcpy(&b, &d, 8);
+    put_le(v, b, 8);
+}
+
+void group_elems(Engine& e, const void* segs, const Layout& L, uint32_t B,
+                 unsigned long long* elems);
+
+static bool crc_consts_ready = false;
+static void init_crc_consts() {
+    if (crc_consts_ready) return;
+    CrcX2N x = crc_x2n_table();
+    uint32_t pw[kCB];
+    for (int t = 0; t < kCB; ++t) pw[t] = crc_x2nmodp(x.t, (uint64_t)32 * (kCB - 1 - t), 3);
+    DQTG_CUDA(cudaMemcpyToSymbol(c_crc_pw, pw, sizeof(pw)));
+    DQTG_CUDA(cudaMemcpyToSymbol(c_crc_x2n, x.t, sizeof(x.t)));
+    crc_consts_ready = true;
+}
+
+std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QState& target,
+                                      double quality) {
+    const Layout& L = *target.L;
+    if (base) {
+        const Layout& BL = *base->L;
+        DQTG_REQUIRE(BL.nt == L.nt, DQTG_SHAPE_MISMATCH, "base/target tensor count mismatch");
+        for (uint32_t i = 0; i < L.nt; ++i)
+            if (BL.names[i] != L.names[i] || BL.dims[i] != L.dims[i] || BL.types[i] != L.types[i])
+                throw Fail(DQTG_SHAPE_MISMATCH,
+                           "base/target tensor layout mismatch at " + L.names[i]);
+    }
+    // codec.cpp:416-417
+    uint32_t B = std::max(base ? base->max_levels() : 0u, target.max_levels());
+    if (B == 0) B = 2;
+    DQTG_REQUIRE(B <= (uint32_t)kMaxB, DQTG_ERROR,
+                 "cyclic alphabet larger than the device codec supports (64 levels)");
+    init_crc_consts();
+    cudaStream_t st = e.stream;
+    const uint32_t NS = B + kLD;
+    const uint32_t nt = L.nt;
+    const int ntiles = (int)L.tiles.size();
+
+    // ---- host-built static bytes: record prefix + per-tensor prefixes (codec.cpp:419-446)
+    std::vector<uint8_t> pre;
+    pre.insert(pre.end(), {'D', 'Q', 'D', 'R'});
+    put_le(pre, 1, 4);
+    pre.push_back(base ? 1 : 0);
+    put_le(pre, base ? base->step : 0, 8);
+    put_le(pre, target.step, 8);
+    put_le(pre, B, 4);
+    const dqtg_config& c = target.cfg;
+    put_le(pre, c.bins, 4);
+    put_le(pre, c.embed_bins, 4);
+    put_f64(pre, c.prune_frac);
+    put_f64(pre, c.protect_frac);
+    pre.push_back((uint8_t)c.metric);
+    put_f64(pre, c.sigma);
+    put_f64(pre, c.alpha);
+    put_f64(pre, quality);
+    uint8_t nlt = 0;
+    for (int lt = 0; lt < kLayerTypes; ++lt) nlt += target.cb_len[lt] != 0;
+    pre.push_back(nlt);
+    for (int lt = 0; lt < kLayerTypes; ++lt) {
+        if (!target.cb_len[lt]) continue;
+        pre.push_back((uint8_t)lt);
+        put_le(pre, target.cb_len[lt], 4);
+        for (float v : target.cb[lt]) {
+            uint32_t u;
+            memcpy(&u, &v, 4);
+            put_le(pre, u, 4);
+        }
+    }
+    put_le(pre, nt, 4);
+    const uint64_t prefix_len = pre.size();
+    std::vector<TensorRec> trh(nt);
+    std::vector<uint8_t> statics;
+    for (uint32_t i = 0; i < nt; ++i) {
+        trh[i].static_off = statics.size();
+        put_le(statics, L.names[i].size(), 2);
+        statics.insert(statics.end(), L.names[i].begin(), L.names[i].end());
+        statics.push_back(L.types[i]);
+        statics.push_back(L.ranks[i]);
+        for (uint64_t d : L.dims[i]) put_le(statics, d, 8);
+        trh[i].static_len = statics.size() - trh[i].static_off;
+        trh[i].prot_begin = target.prot_off[i];
+        trh[i].prot_end = target.prot_off[i + 1];
+    }
+
+    auto rec = std::make_unique<Record>();
+    rec->eng = &e;
+    if (nt == 0) {
+        // no tensors: prefix + CRC of the empty stream
+        std::vector<uint8_t> host = pre;
+        put_le(host, 0, 4);  // crc32 of nothing = 0
+        rec->size = host.size();
+        DQTG_CUDA(cudaMalloc(&rec->d_buf, host.size()));
+        DQTG_CUDA(cudaMemcpy(rec->d_buf, host.data(), host.size(), cudaMemcpyHostToDevice));
+        return rec;
+    }
+
+    // ---- device scratch
+    EncArgs A{};
+    A.tiles = L.d_tiles;
+    A.types = L.d_types;
+    A.off = L.d_off;
+    A.stream_off = L.d_stream_off;
+    A.tile0 = L.d_tile0;
+    A.N = L.N;
+    A.B = B;
+    A.NS = NS;
+    A.prev = base ? base->d_levels : nullptr;
+    A.cur = target.d_levels;
+    A.segs = (Seg*)e.buf("e.segs", (size_t)ntiles * B * sizeof(Seg) + 64);
+    A.runs = (unsigned long long*)e.buf("e.runs", (size_t)ntiles * kTile * 8);
+    A.tile_nruns = (uint32_t*)e.buf("e.nruns", (size_t)ntiles * 4 + 4);
+    const size_t freq_n = (size_t)nt * B * NS;
+    A.freq = (uint32_t*)e.buf("e.freq", freq_n * 4);
+    A.ov_cap = L.N / kLD + (unsigned long long)ntiles * B * 2 + 16;
+    A.ov = (unsigned long long*)e.buf("e.ov", A.ov_cap * 8);
+    auto* small = (unsigned long long*)e.buf("e.small", 64);
+    A.ov_count = small;
+    A.crc_acc = (uint32_t*)(small + 1);
+    A.err = e.d_err;
+    DQTG_CUDA(cudaMemsetAsync(A.freq, 0, freq_n * 4, st));
+    DQTG_CUDA(cudaMemsetAsync(small, 0, 64, st));
+
+    // E1
+    const size_t e1_smem = (size_t)B * NS * 4 + (size_t)kTile * 2 * 5 + (kTile + 2) * 2 + 16;
+    if (base) {
+        DQTG_CUDA(cudaFuncSetAttribute(enc_tile_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e1_smem));
+        enc_tile_kernel<true><<<ntiles, kCB, e1_smem, st>>>(A);
+    } else {
+        DQTG_CUDA(cudaFuncSetAttribute(enc_tile_kernel<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e1_smem));
+        enc_tile_kernel<false><<<ntiles, kCB, e1_smem, st>>>(A);
+    }
+    // S
+    enc_resolve_kernel<<<nt * B, kCB, NS * 4, st>>>(A);
+    e.launched(2);
+    DQTG_CUDA(cudaGetLastError());
+    // group element counts from the segments (host-free): sum of seg.n per (t,b)
+    auto* elems = (unsigned long long*)e.buf("e.elems", (size_t)nt * B * 8);
+    group_elems(e, A.segs, L, B, elems);
+
+    // overflow run lengths: sort + unique
+    unsigned long long n_ov = 0;
+    DQTG_CUDA(cudaMemcpyAsync(&n_ov, A.ov_count, 8, cudaMemcpyDeviceToHost, st));
+    e.sync();
+    DQTG_REQUIRE(n_ov <= A.ov_cap, DQTG_ERROR, "run-length overflow list exhausted");
+    auto* ov_sorted = (unsigned long long*)e.buf("e.ov_sorted", n_ov * 8 + 8);
+    auto* ukey = (unsigned long long*)e.buf("e.ukey", n_ov * 8 + 8);
+    auto* ucnt = (unsigned long long*)e.buf("e.ucnt", n_ov * 8 + 8);
+    auto* nu = (unsigned long long*)(small + 2);
+    if (n_ov) {
+        size_t tb = 0;
+        DQTG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, A.ov, ov_sorted, (int64_t)n_ov, 0, 64,
+                                                 st));
+        void* tmp = e.buf("e.cubtmp", tb + 16);
+        DQTG_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, A.ov, ov_sorted, (int64_t)n_ov, 0, 64, st));
+        auto* uhead = (unsigned long long*)e.buf("e.uhead", n_ov * 8 + 8);
+        ov_unique_kernel<<<1, 1024, 0, st>>>(ov_sorted, n_ov, ukey, uhead, nu);
+        ov_counts_kernel<<<64, 256, 0, st>>>(uhead, nu, n_ov, ucnt);
+        e.launched(2);
+    } else {
+        DQTG_CUDA(cudaMemsetAsync(nu, 0, 8, st));
+    }
+    unsigned long long n_unique = 0;
+    DQTG_CUDA(cudaMemcpyAsync(&n_unique, nu, 8, cudaMemcpyDeviceToHost, st));
+    e.sync();
+    // H
+    auto* gi = (GroupInfo*)e.buf("e.gi", (size_t)nt * B * sizeof(GroupInfo));
+    const size_t tab_n = (size_t)nt * B * NS + n_ov + 8;
+    auto* tab_sym = (long long*)e.buf("e.tabsym", tab_n * 8);
+    auto* tab_len = (uint8_t*)e.buf("e.tablen", tab_n);
+    auto* code_dense = (unsigned long long*)e.buf("e.cdense", (size_t)nt * B * NS * 8);
+    auto* len_dense = (uint8_t*)e.buf("e.ldense", (size_t)nt * B * NS);
+    auto* code_ov = (unsigned long long*)e.buf("e.cov", n_ov * 8 + 8);
+    auto* len_ov = (uint8_t*)e.buf("e.lov", n_ov + 8);
+    {
+        auto* max_nov = (uint32_t*)(small + 4);
+        DQTG_CUDA(cudaMemsetAsync(max_nov, 0, 4, st));
+        if (n_unique) {
+            ov_group_max_kernel<<<64, 256, 0, st>>>(ukey, nu, nt * B, max_nov);
+            e.launched();
+        }
+        uint32_t h_max = 0;
+        DQTG_CUDA(cudaMemcpyAsync(&h_max, max_nov, 4, cudaMemcpyDeviceToHost, st));
+        e.sync();
+        uint32_t np2 = 1;
+        while (np2 < NS + h_max) np2 <<= 1;
+        const size_t hsm = (size_t)np2 * 8;
+        DQTG_REQUIRE(hsm <= 200 * 1024, DQTG_ERROR,
+                     "too many distinct run lengths in one group for the device Huffman stage");
+        HufWork W;
+        const size_t cap = tab_n;
+        W.sym = (long long*)e.buf("h.sym", cap * 8);
+        W.f = (unsigned long long*)e.buf("h.f", cap * 8);
+        W.perm = (uint32_t*)e.buf("h.perm", cap * 4);
+        const size_t ncap = 2 * cap + 2 * (size_t)nt * B + 8;
+        W.nodef = (unsigned long long*)e.buf("h.nodef", ncap * 8);
+        W.parent = (uint32_t*)e.buf("h.parent", ncap * 4);
+        W.depth = (uint32_t*)e.buf("h.depth", ncap * 4);
+        if (hsm > 48 * 1024)
+            DQTG_CUDA(cudaFuncSetAttribute(enc_huffman_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+        enc_huffman_kernel<<<nt * B, 128, hsm, st>>>(A, elems, ukey, ucnt, nu, gi, tab_sym, tab_len,
+                                                     code_dense, len_dense, code_ov, len_ov, W, np2);
+        e.launched();
+    }
+    CodeTabs C{code_dense, len_dense, ukey, code_ov, len_ov, gi};
+    auto* segbits = (unsigned long long*)e.buf("e.segbits", (size_t)ntiles * B * 8);
+    enc_bits_kernel<<<ntiles, kCB, 0, st>>>(A, C, segbits);
+    enc_bitscan_kernel<<<nt * B, kCB, 0, st>>>(A, segbits, gi);
+    e.launched(2);
+
+    // protected entry sizes + layout
+    const uint64_t np = target.prot_total;
+    auto* psz = (unsigned long long*)e.buf("e.psz", (np + 1) * 8);
+    auto* pscan = (unsigned long long*)e.buf("e.pscan", (np + 1) * 8);
+    auto* tr = (TensorRec*)e.buf("e.tr", nt * sizeof(TensorRec));
+    DQTG_CUDA(cudaMemcpyAsync(tr, trh.data(), nt * sizeof(TensorRec), cudaMemcpyHostToDevice, st));
+    DQTG_CUDA(cudaMemsetAsync(psz, 0, (np + 1) * 8, st));
+    if (np) prot_sizes_kernel<<<nt, 256, 0, st>>>(tr, target.d_ppos, psz);
+    {
+        size_t tb = 0;
+        DQTG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, psz, pscan, (int64_t)(np + 1), st));
+        void* tmp = e.buf("e.cubtmp2", tb + 16);
+        DQTG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, psz, pscan, (int64_t)(np + 1), st));
+    }
+    tensor_size_kernel<<<nt, 32, 0, st>>>(A, tr, pscan, gi);
+    auto* total_d = (unsigned long long*)(small + 3);
+    tensor_scan_kernel<<<1, 1, 0, st>>>(tr, nt, prefix_len, total_d);
+    e.launched(3);
+    unsigned long long total = 0;
+    DQTG_CUDA(cudaMemcpyAsync(&total, total_d, 8, cudaMemcpyDeviceToHost, st));
+    e.check_err();  // syncs
+
+    // ---- writers
+    rec->size = total;
+    rec->cap = round_up(total, 16) + 16;
+    DQTG_CUDA(cudaMalloc(&rec->d_buf, rec->cap));
+    DQTG_CUDA(cudaMemsetAsync(rec->d_buf, 0, rec->cap, st));
+    DQTG_CUDA(cudaMemcpyAsync(rec->d_buf, pre.data(), pre.size(), cudaMemcpyHostToDevice, st));
+    auto* d_statics = (uint8_t*)e.buf("e.statics", statics.size() + 8);
+    DQTG_CUDA(cudaMemcpyAsync(d_statics, statics.data(), statics.size(), cudaMemcpyHostToDevice, st));
+    write_tensor_kernel<<<nt, kCB, 0, st>>>(A, tr, d_statics, target.d_ppos, target.d_pval, pscan,
+                                            gi, tab_sym, tab_len, rec->d_buf);
+    enc_emit_kernel<<<ntiles, kCB, 0, st>>>(A, C, segbits, rec->d_buf);
+    finish_crc_kernel<<<1, 1, 0, st>>>(A.crc_acc, 2 * L.N, rec->d_buf + total - 4, nullptr);
+    e.launched(3);
+    DQTG_CUDA(cudaGetLastError());
+    e.check_err();
+    // keep host copies of the staging buffers alive until the copies finished
+    return rec;
+}
+
+__global__ void group_elems_kernel(const Seg* segs, const uint32_t* tile0, uint32_t B,
+                                   unsigned long long* elems) {
+    __shared__ unsigned long long s_scan[33];
+    const uint32_t t = blockIdx.x / B, b = blockIdx.x % B;
+    unsigned long long acc = 0;
+    for (uint32_t i = tile0[t] + threadIdx.x; i < tile0[t + 1]; i += blockDim.x)
+        acc += segs[(size_t)i * B + b].n;
+    unsigned long long tot;
+    block_exclusive_scan<unsigned long long>(acc, s_scan, &tot);
+    if (threadIdx.x == 0) elems[blockIdx.x] = tot;
+}
+
+void group_elems(Engine& e, const void* segs, const Layout& L, uint32_t B,
+                 unsigned long long* elems) {
+    group_elems_kernel<<<L.nt * B, 256, 0, e.stream>>>((const Seg*)segs, L.d_tile0, B, elems);
+    e.launched();
+}
+
+// ---- crc32 over an arbitrary byte buffer (codec.cpp:275-288) ---------------------
+__global__ void crc_bytes_kernel(const uint8_t* data, unsigned long long n, uint32_t* acc) {
+    // each thread: 64 contiguous bytes; shift by the bytes that follow
+    __shared__ uint32_t s_tab[256];
+    {
+        uint32_t c = threadIdx.x;
+        for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xedb88320u ^ (c >> 1) : c >> 1;
+        s_tab[threadIdx.x] = c;
+    }
+    __syncthreads();
+    const unsigned long long chunk = 64;
+    for (unsigned long long s = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) * chunk;
+         s < n; s += (unsigned long long)gridDim.x * blockDim.x * chunk) {
+        unsigned long long e = s + chunk < n ? s + chunk : n;
+        uint32_t r = 0;
+        for (unsigned long long i = s; i < e; ++i) r = s_tab[(r ^ data[i]) & 0xff] ^ (r >> 8);
+        r = crc_shift(c_crc_x2n, r, n - e);
+        if (r) atomicXor(acc, r);
+    }
+}
+
+uint32_t crc32_device(Engine& e, const uint8_t* data, uint64_t n) {
+    init_crc_consts();
+    auto* acc = (uint32_t*)e.buf("crc.acc", 16);
+    auto* out = acc + 1;
+    DQTG_CUDA(cudaMemsetAsync(acc, 0, 16, e.stream));
+    if (n) crc_bytes_kernel<<<std::min<unsigned long long>(4096, (n + 16383) / 16384), 256, 0,
+                              e.stream>>>(data, n, acc);
+    finish_crc_kernel<<<1, 1, 0, e.stream>>>(acc, n, nullptr, out);
+    e.launched(2);
+    uint32_t h = 0;
+    DQTG_CUDA(cudaMemcpyAsync(&h, out, 4, cudaMemcpyDeviceToHost, e.stream));
+    e.sync();
+    return h;
+}
+
+}  // namespace dqtg

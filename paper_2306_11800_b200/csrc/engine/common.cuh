@@ -1,0 +1,97 @@
+// Shared definitions for the dqtg engine (B200 / sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "dqtg.h"
+
+namespace dqtg {
+
+// Internal exception carrying a dqtg_status; converted at the C-ABI boundary.
+struct Fail : std::runtime_error {
+    dqtg_status code;
+    Fail(dqtg_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define DQTG_CUDA(call)                                                                     \
+    do {                                                                                    \
+        cudaError_t err_ = (call);                                                          \
+        if (err_ != cudaSuccess)                                                            \
+            throw ::dqtg::Fail(DQTG_CUDA, std::string(#call) + ": " + cudaGetErrorString(err_)); \
+    } while (0)
+
+#define DQTG_REQUIRE(cond, code, msg)                     \
+    do {                                                  \
+        if (!(cond)) throw ::dqtg::Fail((code), (msg));   \
+    } while (0)
+
+constexpr int kLayerTypes = 7;
+constexpr int kEmbedding = 4;
+
+// Padded flat layout: every tensor starts on a 64-element boundary so tiles are
+// 128-byte aligned for fp32 and u16 streams.
+constexpr uint64_t kAlign = 64;
+
+// Device-side error word bits (checked by the host after each pipeline).
+enum DevErr : uint32_t {
+    kErrEmptySketch = 1u << 0,
+    kErrCorruptIndex = 1u << 1,
+    kErrHuffmanDepth = 1u << 2,
+    kErrNonFinite = 1u << 3,
+    kErrKmeansWeights = 1u << 4,
+};
+
+inline uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+inline uint64_t ceil_div(uint64_t x, uint64_t a) { return (x + a - 1) / a; }
+
+// ---- device helpers ------------------------------------------------------
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ uint32_t warp_xor(uint32_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v ^= __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Exclusive block scan of one value per thread (blockDim multiple of 32, <= 1024).
+template <typename T>
+__device__ T block_exclusive_scan(T v, T* smem /* >= 33 */, T* total = nullptr) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    T x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) smem[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        T s = lane < nw ? smem[lane] : T(0);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            T y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < nw) smem[lane] = s;  // inclusive per-warp prefix
+        if (lane == nw - 1) smem[32] = s;
+    }
+    __syncthreads();
+    T base = wid ? smem[wid - 1] : T(0);
+    T out = base + x - v;
+    if (total) *total = smem[32];
+    __syncthreads();
+    return out;
+}
+
+}  // namespace dqtg

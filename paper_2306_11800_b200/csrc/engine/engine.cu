@@ -1,0 +1,281 @@
+// Engine plumbing: device/stream, scratch, alpha tables, layouts, object lifetimes.
+#include <float.h>
+#include <math.h>
+#include <string.h>
+
+#include <cstring>
+
+#include "engine.h"
+
+namespace dqtg {
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device);
+    for (auto& kv : scratch) cudaFree(kv.second.first);
+    for (auto& kv : tables) {
+        cudaFree(kv.second->d_U);
+        cudaFree(kv.second->d_key);
+        cudaFree(kv.second->d_keyf);
+    }
+    if (d_err) cudaFree(d_err);
+    if (pinned) cudaFreeHost(pinned);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+void* Engine::buf(const std::string& name, size_t bytes) {
+    auto& slot = scratch[name];
+    if (slot.second < bytes) {
+        if (slot.first) {
+            DQTG_CUDA(cudaStreamSynchronize(stream));
+            DQTG_CUDA(cudaFree(slot.first));
+        }
+        size_t cap = bytes < 256 ? 256 : bytes + bytes / 4;
+        DQTG_CUDA(cudaMalloc(&slot.first, cap));
+        slot.second = cap;
+    }
+    return slot.first;
+}
+
+void* Engine::host_pinned(size_t bytes) {
+    if (pinned_cap < bytes) {
+        if (pinned) {
+            DQTG_CUDA(cudaStreamSynchronize(stream));
+            cudaFreeHost(pinned);
+        }
+        pinned_cap = bytes + bytes / 4 + 4096;
+        DQTG_CUDA(cudaMallocHost(&pinned, pinned_cap));
+    }
+    return pinned;
+}
+
+void Engine::check_err() {
+    uint32_t h = 0;
+    DQTG_CUDA(cudaMemcpyAsync(&h, d_err, 4, cudaMemcpyDeviceToHost, stream));
+    DQTG_CUDA(cudaStreamSynchronize(stream));
+    if (!h) return;
+    DQTG_CUDA(cudaMemsetAsync(d_err, 0, 4, stream));
+    if (h & kErrNonFinite) throw Fail(DQTG_NON_FINITE, "input contains NaN/Inf");
+    if (h & kErrEmptySketch) throw Fail(DQTG_EMPTY_SKETCH, "quantile of empty sketch");
+    if (h & kErrCorruptIndex) throw Fail(DQTG_CORRUPT_INDEX, "level outside cyclic alphabet");
+    if (h & kErrHuffmanDepth) throw Fail(DQTG_ERROR, "huffman code length overflow");
+    if (h & kErrKmeansWeights) throw Fail(DQTG_ERROR, "total weight must be positive");
+    throw Fail(DQTG_ERROR, "device error");
+}
+
+void Engine::to_device(void* dst, const void* src, size_t bytes) {
+    if (!bytes) return;
+    DQTG_CUDA(cudaMemcpyAsync(dst, src, bytes,
+                              is_device_ptr(src) ? cudaMemcpyDeviceToDevice
+                                                 : cudaMemcpyHostToDevice,
+                              stream));
+}
+
+void Engine::from_device(void* dst, const void* src, size_t bytes) {
+    if (!bytes) return;
+    DQTG_CUDA(cudaMemcpyAsync(dst, src, bytes,
+                              is_device_ptr(dst) ? cudaMemcpyDeviceToDevice
+                                                 : cudaMemcpyDeviceToHost,
+                              stream));
+}
+
+// ---- alpha tables ----------------------------------------------------------
+// Host restatement of the reference bucket rule, used only to build and verify
+// the integer boundary tables (sketch.cpp:21-31).
+static int64_t ref_bucket(double gamma, double inv_ln_gamma, double ax) {
+    double r = log(ax) * inv_ln_gamma;
+    double nearest = nearbyint(r);
+    if (fabs(r - nearest) > 1e-9 * fmax(1.0, fabs(r))) return (int64_t)ceil(r);
+    int64_t k = (int64_t)nearest;
+    while (pow(gamma, (double)(k - 1)) >= ax) --k;
+    while (pow(gamma, (double)k) < ax) ++k;
+    return k;
+}
+
+static float round_down_f(double v) {
+    if (v >= (double)FLT_MAX) return FLT_MAX;
+    if (v <= -(double)FLT_MAX) return -FLT_MAX;
+    float f = (float)v;
+    if ((double)f > v) f = nextafterf(f, -INFINITY);
+    return f;
+}
+
+static uint32_t fbits(float f) {
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    return u;
+}
+
+AlphaTables& Engine::alpha_tables(double alpha) {
+    if (!(alpha > 0.0) || !(alpha < 1.0))
+        throw Fail(DQTG_ALPHA_OUT_OF_RANGE, "alpha must be in (0, 1)");
+    uint64_t key;
+    memcpy(&key, &alpha, 8);
+    auto it = tables.find(key);
+    if (it != tables.end()) return *it->second;
+    auto t = std::make_unique<AlphaTables>();
+    t->alpha = alpha;
+    t->gamma = (1.0 + alpha) / (1.0 - alpha);  // sketch.cpp:16-18
+    t->inv_ln_gamma = 1.0 / log(t->gamma);
+    t->rep_scale = 2.0 / (1.0 + t->gamma);
+    float zf = (float)1e-12;
+    if ((double)zf < 1e-12) zf = nextafterf(zf, INFINITY);
+    t->zbits = fbits(zf);
+    t->kmin = ref_bucket(t->gamma, t->inv_ln_gamma, (double)zf);
+    t->kmax = ref_bucket(t->gamma, t->inv_ln_gamma, (double)FLT_MAX);
+    t->NB = t->kmax - t->kmin + 1;
+    t->HS = 2 * t->NB + 1;
+    std::vector<uint32_t> U((size_t)t->NB + 1);
+    for (int64_t k = t->kmin - 1; k <= t->kmax; ++k)
+        U[(size_t)(k - t->kmin + 1)] = fbits(round_down_f(pow(t->gamma, (double)k)));
+    // Verify the table against the reference rule at every bucket boundary; the
+    // rule is monotone, so agreement at all boundaries is agreement everywhere.
+    for (int64_t k = t->kmin; k <= t->kmax; ++k) {
+        uint32_t u = U[(size_t)(k - t->kmin + 1)];
+        float f;
+        memcpy(&f, &u, 4);
+        if (u >= t->zbits && ref_bucket(t->gamma, t->inv_ln_gamma, (double)f) != k)
+            throw Fail(DQTG_ERROR, "bucket table disagrees with reference rule at k=" +
+                                       std::to_string(k));
+        if (k < t->kmax) {
+            float g = nextafterf(f, INFINITY);
+            if (fbits(g) >= t->zbits && ref_bucket(t->gamma, t->inv_ln_gamma, (double)g) != k + 1)
+                throw Fail(DQTG_ERROR, "bucket table boundary mismatch at k=" + std::to_string(k));
+        }
+    }
+    t->h_key.resize((size_t)t->HS);
+    std::vector<float> keyf((size_t)t->HS);
+    for (int64_t k = t->kmin; k <= t->kmax; ++k) {
+        double rep = t->rep_scale * pow(t->gamma, (double)k);  // sketch.cpp:33-37
+        t->h_key[(size_t)(t->kmax - k)] = -rep;
+        t->h_key[(size_t)(t->NB + 1 + k - t->kmin)] = rep;
+    }
+    t->h_key[(size_t)t->NB] = 0.0;
+    for (size_t i = 0; i < keyf.size(); ++i) keyf[i] = round_down_f(t->h_key[i]);
+    if (t->NB <= kWin) {
+        t->kw_lo = t->kmin;
+    } else {
+        int64_t top = ref_bucket(t->gamma, t->inv_ln_gamma, 10.0);
+        int64_t lo = top - kWin + 1;
+        if (lo > t->kmax - kWin + 1) lo = t->kmax - kWin + 1;
+        if (lo < t->kmin) lo = t->kmin;
+        t->kw_lo = lo;
+    }
+    t->inv_log2_gamma = (float)(1.0 / log2(t->gamma));
+    activate();
+    DQTG_CUDA(cudaMalloc(&t->d_U, U.size() * 4));
+    DQTG_CUDA(cudaMalloc(&t->d_key, t->h_key.size() * 8));
+    DQTG_CUDA(cudaMalloc(&t->d_keyf, keyf.size() * 4));
+    DQTG_CUDA(cudaMemcpy(t->d_U, U.data(), U.size() * 4, cudaMemcpyHostToDevice));
+    DQTG_CUDA(cudaMemcpy(t->d_key, t->h_key.data(), t->h_key.size() * 8, cudaMemcpyHostToDevice));
+    DQTG_CUDA(cudaMemcpy(t->d_keyf, keyf.data(), keyf.size() * 4, cudaMemcpyHostToDevice));
+    auto& ref = *t;
+    tables[key] = std::move(t);
+    return ref;
+}
+
+// ---- layouts --------------------------------------------------------------
+Layout::~Layout() {
+    cudaFree(d_tiles);
+    cudaFree(d_types);
+    cudaFree(d_off);
+    cudaFree(d_numel);
+    cudaFree(d_tile0);
+    cudaFree(d_stream_off);
+}
+
+bool Layout::same_shape(const Layout& o) const {
+    if (nt != o.nt) return false;
+    for (uint32_t i = 0; i < nt; ++i) {
+        if (types[i] != o.types[i] || dims[i] != o.dims[i]) return false;
+        if (has_names && o.has_names && names[i] != o.names[i]) return false;
+    }
+    return true;
+}
+
+template <typename T>
+static T* upload_vec(const std::vector<T>& v) {
+    T* d = nullptr;
+    size_t bytes = (v.size() ? v.size() : 1) * sizeof(T);
+    DQTG_CUDA(cudaMalloc(&d, bytes));
+    if (!v.empty()) DQTG_CUDA(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+}
+
+std::shared_ptr<Layout> make_layout(Engine* e, const dqtg_layout* l) {
+    auto L = std::make_shared<Layout>();
+    L->eng = e;
+    L->nt = l->n_tensors;
+    L->has_names = l->names != nullptr;
+    size_t d = 0;
+    std::vector<uint64_t> soff;
+    for (uint32_t i = 0; i < L->nt; ++i) {
+        uint8_t ty = l->types ? l->types[i] : 6;
+        DQTG_REQUIRE(ty < kLayerTypes, DQTG_CORRUPT_INDEX, "bad tensor layer type");
+        L->types.push_back(ty);
+        uint8_t r = l->ranks[i];
+        L->ranks.push_back(r);
+        std::vector<uint64_t> dm(l->dims + d, l->dims + d + r);
+        d += r;
+        uint64_t n = 1;
+        for (uint64_t x : dm) n *= x;
+        L->dims.push_back(dm);
+        L->numel.push_back(n);
+        L->names.push_back(L->has_names ? std::string(l->names[i]) : std::string());
+        L->off.push_back(L->Np);
+        soff.push_back(L->N);
+        L->Np += round_up(n, kAlign);
+        L->N += n;
+        L->tile0.push_back((uint32_t)L->tiles.size());
+        for (uint64_t s = 0; s < n; s += kTile) {
+            DQTG_REQUIRE(L->tiles.size() < 0xffffffffull, DQTG_ERROR, "checkpoint too large");
+            L->tiles.push_back(Tile{i, (uint32_t)((n - s) < kTile ? (n - s) : kTile), L->off[i] + s});
+        }
+    }
+    L->tile0.push_back((uint32_t)L->tiles.size());
+    if (L->Np == 0) L->Np = kAlign;
+    e->activate();
+    L->d_tiles = upload_vec(L->tiles);
+    L->d_types = upload_vec(L->types);
+    L->d_off = upload_vec(L->off);
+    L->d_numel = upload_vec(L->numel);
+    L->d_tile0 = upload_vec(L->tile0);
+    L->d_stream_off = upload_vec(soff);
+    return L;
+}
+
+DevCkpt::~DevCkpt() {
+    cudaFree(w);
+    cudaFree(ema);
+    cudaFree(mag);
+    cudaFree(sens);
+}
+
+uint32_t QState::max_levels() const {  // quantize.cpp:357-365
+    uint32_t m = 0;
+    for (uint32_t i = 0; i < L->nt; ++i) {
+        uint32_t l = cb_len[L->types[i]] + 2;
+        m = l > m ? l : m;
+    }
+    return m;
+}
+
+QState::~QState() {
+    cudaFree(d_cb);
+    cudaFree(d_levels);
+    cudaFree(d_ppos);
+    cudaFree(d_pval);
+}
+
+Record::~Record() { cudaFree(d_buf); }
+
+}  // namespace dqtg

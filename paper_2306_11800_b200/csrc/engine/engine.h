@@ -1,0 +1,174 @@
+// Host-side objects of the dqtg engine: engine/stream, alpha tables, layouts,
+// device checkpoints, quantized states and records.
+#pragma once
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace dqtg {
+
+// Shared-memory histogram window: kWin buckets per sign plus the zero bucket.
+constexpr int kWin = 4096;
+constexpr int kWinSlots = 2 * kWin + 1;
+// Elements per tile of every streaming pass (a tile never crosses a tensor).
+constexpr uint32_t kTile = 4096;
+
+struct Tile {
+    uint32_t tensor;
+    uint32_t count;  // valid elements (<= kTile)
+    uint64_t start;  // padded element offset of the first element
+};
+
+// Exact log-bucket tables for one alpha: the reference's
+// bucket_index(x) (sketch.cpp:21-31) equals "smallest k with gamma^k >= x";
+// with U[k] = largest float <= gamma^k this is an integer compare on float bits.
+struct AlphaTables {
+    double alpha, gamma, inv_ln_gamma, rep_scale;
+    int64_t kmin, kmax, NB, HS;  // HS = 2*NB + 1 signed slots (neg desc, zero, pos asc)
+    int64_t kw_lo;               // shared-memory window covers k in [kw_lo, kw_lo + kWin)
+    uint32_t zbits;              // bits of the smallest float >= 1e-12 (zero bucket bound)
+    float inv_log2_gamma;
+    uint32_t* d_U = nullptr;     // U(k) for k in [kmin-1, kmax]
+    double* d_key = nullptr;     // representative value per signed slot (sketch.cpp:33-37)
+    float* d_keyf = nullptr;     // largest float <= key (threshold compare, §7 H2)
+    std::vector<double> h_key;
+};
+
+// Device view of the bucket tables passed by value to kernels.
+struct BucketTab {
+    const uint32_t* U;
+    int64_t kmin, kmax, NB, kw_lo;
+    uint32_t zbits;
+    float inv_log2_gamma;
+};
+
+struct Engine;
+
+struct Layout {
+    uint32_t nt = 0;
+    std::vector<std::string> names;
+    std::vector<uint8_t> types, ranks;
+    std::vector<std::vector<uint64_t>> dims;
+    std::vector<uint64_t> numel, off;  // off = padded element offset
+    uint64_t N = 0, Np = 0;            // real / padded element totals
+    bool has_names = false;
+    std::vector<Tile> tiles;
+    std::vector<uint32_t> tile0;  // first tile of each tensor (size nt+1)
+    // device copies
+    Tile* d_tiles = nullptr;
+    uint8_t* d_types = nullptr;      // per tensor
+    uint64_t* d_off = nullptr;       // per tensor padded offset
+    uint64_t* d_numel = nullptr;     // per tensor
+    uint32_t* d_tile0 = nullptr;     // per tensor first tile (nt+1)
+    uint64_t* d_stream_off = nullptr;  // per tensor unpadded element offset (CRC stream position)
+    Engine* eng = nullptr;
+    ~Layout();
+    bool same_shape(const Layout& o) const;
+};
+
+std::shared_ptr<Layout> make_layout(Engine* e, const dqtg_layout* l);
+
+struct DevCkpt {
+    Engine* eng = nullptr;
+    std::shared_ptr<Layout> L;
+    float* w = nullptr;
+    float* ema = nullptr;  // derived-score mode
+    float* mag = nullptr;  // explicit-score mode
+    float* sens = nullptr;
+    bool explicit_scores = false;
+    bool has_sens = false;
+    bool ema_seeded = false;
+    ~DevCkpt();
+};
+
+struct QState {
+    Engine* eng = nullptr;
+    std::shared_ptr<Layout> L;
+    uint64_t step = 0;
+    dqtg_config cfg{};
+    uint32_t cb_len[kLayerTypes] = {0};
+    std::vector<float> cb[kLayerTypes];
+    float* d_cb = nullptr;  // [7][cb_stride]
+    uint32_t cb_stride = 0;
+    uint16_t* d_levels = nullptr;  // padded flat
+    uint64_t* d_ppos = nullptr;    // protected positions (tensor-local), tensor order
+    uint16_t* d_pval = nullptr;
+    std::vector<uint64_t> prot_count, prot_off;  // per tensor
+    uint64_t prot_total = 0;
+    uint32_t max_levels() const;
+    ~QState();
+};
+
+struct Record {
+    Engine* eng = nullptr;
+    uint8_t* d_buf = nullptr;
+    uint64_t size = 0, cap = 0;
+    std::vector<uint8_t> host;  // filled by decode-free host copies
+    ~Record();
+};
+
+struct Engine {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::recursive_mutex mu;
+    uint64_t launches = 0;
+    uint32_t* d_err = nullptr;
+    std::map<uint64_t, std::unique_ptr<AlphaTables>> tables;
+    // grow-only scratch buffers keyed by name
+    std::map<std::string, std::pair<void*, size_t>> scratch;
+    void* pinned = nullptr;
+    size_t pinned_cap = 0;
+    int num_sms = 148;
+
+    ~Engine();
+    void activate() const { DQTG_CUDA(cudaSetDevice(device)); }
+    AlphaTables& alpha_tables(double alpha);
+    BucketTab bucket_tab(const AlphaTables& t) const {
+        return BucketTab{t.d_U, t.kmin, t.kmax, t.NB, t.kw_lo, t.zbits, t.inv_log2_gamma};
+    }
+    void* buf(const std::string& name, size_t bytes);  // scratch, contents undefined
+    void* host_pinned(size_t bytes);
+    void sync() { DQTG_CUDA(cudaStreamSynchronize(stream)); }
+    void launched(int n = 1) { launches += n; }
+    void check_err();  // reads + clears the device error word (syncs)
+    // copy host-or-device memory into a device destination
+    void to_device(void* dst, const void* src_any, size_t bytes);
+    void from_device(void* dst_any, const void* src_dev, size_t bytes);
+};
+
+bool is_device_ptr(const void* p);
+
+// ---- pipeline entry points implemented across the .cu files ---------------
+void sketch_build(Engine& e, const float* x_any, uint64_t n, double alpha, uint64_t* zero,
+                  uint64_t* pos, uint64_t* neg);
+std::unique_ptr<QState> quantize(Engine& e, const DevCkpt& c, const dqtg_config& cfg,
+                                 uint64_t seed, uint64_t step);
+std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QState& target,
+                                      double quality);
+std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
+                                      const QState* base);
+void dequantize(Engine& e, const QState& q, float* out_dev_padded);
+void eval_batch(Engine& e, const DevCkpt& c, const dqtg_config* cfgs, const uint64_t* seeds,
+                uint32_t m, double* quality, double* est);
+void approx_kmeans(Engine& e, const float* values_any, uint64_t n, uint32_t k, double sigma,
+                   double alpha, uint64_t seed, float* cb, uint32_t* len);
+void kmeanspp_host_api(Engine& e, const double* pts, const double* w, uint64_t n, uint32_t k,
+                       uint64_t seed, double* centers);
+void lloyd_host_api(Engine& e, const double* pts, const double* w, uint64_t n, double* centers,
+                    uint32_t k, double tol, uint32_t max_iter, uint32_t* iters);
+double sq_loss_host_api(Engine& e, const double* pts, const double* w, uint64_t n,
+                        const double* centers, uint32_t k);
+void ema_update(Engine& e, float* ema_dev, const float* g_dev, uint64_t n, float beta);
+void compute_scores(Engine& e, const float* w_dev, const float* ema_dev, uint64_t n, float* mag,
+                    float* sens);
+uint32_t crc32_device(Engine& e, const uint8_t* data_dev, uint64_t n);
+void delta_kernel_api(Engine& e, const uint16_t* prev, const uint16_t* x, uint64_t n, uint32_t B,
+                      uint16_t* out, bool apply);
+
+}  // namespace dqtg

@@ -1,0 +1,78 @@
+// Exact log-bucket histogram device functions (sketch.cpp:21-31, 131-148).
+#pragma once
+
+#include "engine.h"
+
+namespace dqtg {
+
+// Smallest k with U(k) >= a (a = bits of |x|, a >= zbits, finite).  The float
+// log2 estimate is within one bucket; integer compares against the boundary
+// table make the result exact.
+__device__ __forceinline__ int bucket_of(uint32_t a, const BucketTab& t) {
+    const int kmin = (int)t.kmin, kmax = (int)t.kmax;
+    float lg = __log2f(__uint_as_float(a));
+    int k = (int)ceilf(lg * t.inv_log2_gamma);
+    k = k < kmin ? kmin : (k > kmax ? kmax : k);
+    // U(k) lives at U[k - kmin + 1]
+    while (k > kmin && __ldg(t.U + (k - kmin)) >= a) --k;
+    while (__ldg(t.U + (k - kmin + 1)) < a) ++k;
+    return k;
+}
+
+// Signed slot index of a finite float (ascending value order):
+// neg k -> kmax-k, zero -> NB, pos k -> NB+1+k-kmin.
+__device__ __forceinline__ int64_t slot_of(float v, const BucketTab& t) {
+    uint32_t b = __float_as_uint(v), a = b & 0x7fffffffu;
+    if (a < t.zbits) return t.NB;
+    int k = bucket_of(a, t);
+    return (b >> 31) ? (t.kmax - k) : (t.NB + 1 + k - t.kmin);
+}
+
+// Adds v to a shared-memory window histogram (sh[kWinSlots]) with spill to the
+// global u64 histogram gh[HS] for buckets outside the window.
+__device__ __forceinline__ void hist_add(uint32_t* sh, unsigned long long* gh, float v,
+                                         const BucketTab& t, uint32_t* err) {
+    uint32_t b = __float_as_uint(v), a = b & 0x7fffffffu;
+    if (a >= 0x7f800000u) {
+        atomicOr(err, kErrNonFinite);
+        return;
+    }
+    if (a < t.zbits) {  // |x| < 1e-12 (sketch.hpp:24), incl. -0.0
+        atomicAdd(sh + kWin, 1u);
+        return;
+    }
+    int k = bucket_of(a, t);
+    int d = k - (int)t.kw_lo;
+    bool neg = b >> 31;
+    if ((unsigned)d < (unsigned)kWin)
+        atomicAdd(sh + (neg ? kWin - 1 - d : kWin + 1 + d), 1u);
+    else
+        atomicAdd(gh + (neg ? (t.kmax - k) : (t.NB + 1 + k - t.kmin)), 1ull);
+}
+
+// Drains the window into gh and clears it.  Call between __syncthreads().
+__device__ __forceinline__ void hist_flush(uint32_t* sh, unsigned long long* gh,
+                                           const BucketTab& t) {
+    for (int w = threadIdx.x; w < kWinSlots; w += blockDim.x) {
+        uint32_t c = sh[w];
+        if (!c) continue;
+        sh[w] = 0;
+        int64_t idx;
+        if (w < kWin) {
+            int64_t k = t.kw_lo + kWin - 1 - w;
+            idx = t.kmax - k;
+        } else if (w == kWin) {
+            idx = t.NB;
+        } else {
+            int64_t k = t.kw_lo + (w - kWin - 1);
+            idx = t.NB + 1 + k - t.kmin;
+        }
+        atomicAdd(gh + idx, (unsigned long long)c);
+    }
+}
+
+__device__ __forceinline__ void hist_clear(uint32_t* sh) {
+    for (int w = threadIdx.x; w < kWinSlots; w += blockDim.x) sh[w] = 0;
+}
+
+}  // namespace dqtg

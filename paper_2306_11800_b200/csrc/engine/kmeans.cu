@@ -1,0 +1,556 @@
+// Histogram k-means on the device (quantize.cpp:94-325): key compaction + mix
+// weights, k-means++ seeding, Lloyd, loss and restart selection.  One CTA per
+// (problem, restart); see kmeans.cuh for the exactness strategy.
+#include <float.h>
+
+#include "engine.h"
+#include "kmeans.cuh"
+#include "kmeans_api.h"
+
+namespace dqtg {
+
+constexpr int kKB = 256;  // threads per k-means CTA
+
+// ---- key compaction + mix_weights (quantize.cpp:263-279) --------------------
+// One CTA per problem: hist[HS] (u64, signed-slot order = ascending value) ->
+// pts/cnt/w (ascending keys), n_keys.
+__global__ void __launch_bounds__(1024) compact_keys_kernel(const unsigned long long* hist,
+                                                            int64_t hs_stride, int64_t HS,
+                                                            const double* key, double sigma,
+                                                            double* pts, unsigned long long* cnt,
+                                                            double* w, int64_t out_stride,
+                                                            int* n_keys) {
+    __shared__ unsigned long long s_scan[33];
+    __shared__ unsigned long long s_maxc;
+    __shared__ double s_maxk;
+    const int p = blockIdx.x;
+    const unsigned long long* h = hist + p * hs_stride;
+    double* P = pts + p * out_stride;
+    unsigned long long* Cn = cnt + p * out_stride;
+    double* W = w + p * out_stride;
+    if (threadIdx.x == 0) {
+        s_maxc = 1;
+        s_maxk = 0.0;
+    }
+    __syncthreads();
+    unsigned long long base = 0;
+    unsigned long long lmaxc = 1;
+    double lmaxk = 0.0;
+    for (int64_t c0 = 0; c0 < HS; c0 += blockDim.x) {
+        int64_t i = c0 + threadIdx.x;
+        unsigned long long c = i < HS ? h[i] : 0ull;
+        unsigned long long flag = c ? 1ull : 0ull, tot;
+        unsigned long long pos = block_exclusive_scan<unsigned long long>(flag, s_scan, &tot);
+        if (c) {
+            double k = key[i];
+            P[base + pos] = k;
+            Cn[base + pos] = c;
+            lmaxc = c > lmaxc ? c : lmaxc;
+            lmaxk = fmax(lmaxk, fabs(k));
+        }
+        base += tot;
+    }
+    atomicMax(&s_maxc, lmaxc);
+    // fmax of non-negative doubles == max of their bit patterns
+    atomicMax((unsigned long long*)&s_maxk, (unsigned long long)__double_as_longlong(lmaxk));
+    __syncthreads();
+    const double maxc = (double)s_maxc, maxk = s_maxk;
+    for (unsigned long long i = threadIdx.x; i < base; i += blockDim.x) {
+        double nc = __ddiv_rn((double)Cn[i], maxc);
+        double nx = maxk > 0.0 ? __ddiv_rn(fabs(P[i]), maxk) : 0.0;
+        W[i] = __dadd_rn(__dmul_rn(sigma, nc), __dmul_rn(__dsub_rn(1.0, sigma), nx));
+    }
+    if (threadIdx.x == 0) n_keys[p] = (int)base;
+}
+
+// ---- per-restart CTA -----------------------------------------------------
+struct KShared {
+    Mt64 rng;
+    int pick;
+    int done;
+    int any_empty;
+    double scale;
+    double red[kKB / 32];
+};
+
+// quantize.cpp:116-131: sequential prefix of prob (lane 0), binary search for the
+// first positive entry whose running sum reaches r.
+__device__ int kpp_pick(const double* prob, double* pref, int n, KShared& sm) {
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        int i = 0;
+        for (; i + 4 <= n; i += 4) {
+            double a = prob[i], b = prob[i + 1], c = prob[i + 2], d = prob[i + 3];
+            s = __dadd_rn(s, a);
+            pref[i] = s;
+            s = __dadd_rn(s, b);
+            pref[i + 1] = s;
+            s = __dadd_rn(s, c);
+            pref[i + 2] = s;
+            s = __dadd_rn(s, d);
+            pref[i + 3] = s;
+        }
+        for (; i < n; ++i) {
+            s = __dadd_rn(s, prob[i]);
+            pref[i] = s;
+        }
+        int res;
+        if (!(s > 0.0)) {
+            res = n;
+        } else {
+            double r = __dmul_rn(uniform01(sm.rng), s);
+            int lo = 0, hi = n;
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if (pref[mid] >= r) hi = mid;
+                else lo = mid + 1;
+            }
+            while (lo < n && !(prob[lo] > 0.0)) ++lo;
+            if (lo == n) {  // no crossing: last positive entry (last_pos)
+                lo = n - 1;
+                while (lo >= 0 && !(prob[lo] > 0.0)) --lo;
+                res = lo < 0 ? n : lo;
+            } else {
+                res = lo;
+            }
+        }
+        sm.pick = res;
+    }
+    __syncthreads();
+    return sm.pick;
+}
+
+__device__ double block_max_d(double v, KShared& sm) {
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) sm.red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = sm.red[0];
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) m = fmax(m, sm.red[i]);
+        sm.red[0] = m;
+    }
+    __syncthreads();
+    double r = sm.red[0];
+    __syncthreads();
+    return r;
+}
+
+// weighted_kmeanspp_init (quantize.cpp:94-164) for distinct points.
+__device__ void kpp_init(const double* pts, const double* w, int n, int k, double* d2,
+                         double* prob, double* pref, double* chosen, KShared& sm) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        d2[i] = __longlong_as_double(0x7ff0000000000000LL);
+        prob[i] = w[i];
+    }
+    __syncthreads();
+    int nc = 0;
+    while (nc < k) {
+        int next = kpp_pick(prob, pref, n, sm);
+        if (threadIdx.x == 0) {
+            bool taken = false;
+            if (next != n)
+                for (int j = 0; j < nc; ++j) taken |= (chosen[j] == pts[next]);
+            if (next == n || taken) {  // first unchosen point
+                for (int i = 0; i < n; ++i) {
+                    bool c2 = false;
+                    for (int j = 0; j < nc; ++j) c2 |= (chosen[j] == pts[i]);
+                    if (!c2) {
+                        next = i;
+                        break;
+                    }
+                }
+            }
+            chosen[nc] = pts[next];
+        }
+        __syncthreads();
+        const double v = chosen[nc];
+        ++nc;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            double dd = __dsub_rn(pts[i], v);
+            double sq = __dmul_rn(dd, dd);
+            double cur = d2[i];
+            cur = sq < cur ? sq : cur;  // std::min(d2, d*d)
+            d2[i] = cur;
+            prob[i] = __dmul_rn(w[i], cur);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) IntroSort<double, LessD>{}.sort(chosen, k);
+    __syncthreads();
+}
+
+// weighted_lloyd (quantize.cpp:180-254); c (k centres) is updated in place.
+__device__ int lloyd_block(const double* pts, const double* w, int n, double* c, double* nx,
+                           int* first, int* last, int* cnt, int k, double tol, int max_iter,
+                           int* assign, double* score, ScoreVal* top, bool distinct,
+                           KShared& sm) {
+    double lm = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) lm = fmax(lm, fabs(pts[i]));
+    double scale = block_max_d(lm, sm);
+    if (scale == 0.0) scale = 1.0;
+    int iters = 0;
+    for (int it = 0; it < max_iter; ++it) {
+        for (int j = threadIdx.x; j < k; j += blockDim.x) {
+            first[j] = 0x7fffffff;
+            last[j] = -1;
+            cnt[j] = 0;
+        }
+        if (threadIdx.x == 0) sm.any_empty = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            double x = pts[i];
+            int best = 0;
+            double bd = fabs(__dsub_rn(x, c[0]));
+            for (int j = 1; j < k; ++j) {
+                double d = fabs(__dsub_rn(x, c[j]));
+                if (d < bd) {
+                    bd = d;
+                    best = j;
+                }
+            }
+            assign[i] = best;
+            atomicMin(&first[best], i);
+            atomicMax(&last[best], i);
+            atomicAdd(&cnt[best], 1);
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < k; j += blockDim.x) {
+            double ws = 0.0, wxs = 0.0;
+            if (cnt[j] > 0) {
+                if (last[j] - first[j] + 1 == cnt[j]) {
+                    for (int i = first[j]; i <= last[j]; ++i) {
+                        double wi = w[i];
+                        ws = __dadd_rn(ws, wi);
+                        wxs = __dadd_rn(wxs, __dmul_rn(wi, pts[i]));
+                    }
+                } else {
+                    for (int i = 0; i < n; ++i)
+                        if (assign[i] == j) {
+                            double wi = w[i];
+                            ws = __dadd_rn(ws, wi);
+                            wxs = __dadd_rn(wxs, __dmul_rn(wi, pts[i]));
+                        }
+                }
+            }
+            if (ws > 0.0) {
+                nx[j] = __ddiv_rn(wxs, ws);
+                cnt[j] = 1;  // reuse as "non-empty" flag
+            } else {
+                cnt[j] = 0;
+                sm.any_empty = 1;
+            }
+        }
+        __syncthreads();
+        if (sm.any_empty) {
+            // re-seed empties to the points with the largest weighted squared
+            // distance, libstdc++ sort order on ties (quantize.cpp:218-243)
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                double x = pts[i];
+                double bd = __longlong_as_double(0x7ff0000000000000LL);
+                for (int j = 0; j < k; ++j) {
+                    double d = fabs(__dsub_rn(x, c[j]));
+                    bd = d < bd ? d : bd;
+                }
+                score[i] = __dmul_rn(__dmul_rn(w[i], bd), bd);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                long nt = 0;
+                for (int i = 0; i < n; ++i) {
+                    double s = score[i];
+                    if (s <= 0.0) continue;
+                    double x = pts[i];
+                    bool dup = false;
+                    if (!distinct)
+                        for (long t = 0; t < nt; ++t)
+                            if (top[t].v == x) {
+                                dup = true;
+                                if (s > top[t].s) top[t].s = s;
+                                break;
+                            }
+                    if (dup) continue;
+                    top[nt].s = s;
+                    top[nt].v = x;
+                    ++nt;
+                }
+                IntroSort<ScoreVal, GreaterScore>{}.sort(top, nt);
+                long used = 0;
+                for (int j = 0; j < k; ++j)
+                    if (!cnt[j] && used < nt) nx[j] = top[used++].v;
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            double mv = 0.0;
+            for (int j = 0; j < k; ++j) mv = fmax(mv, fabs(__dsub_rn(nx[j], c[j])));
+            for (int j = 0; j < k; ++j) c[j] = nx[j];
+            sm.done = mv <= __dmul_rn(tol, scale);
+        }
+        __syncthreads();
+        iters = it + 1;
+        if (sm.done) break;
+    }
+    if (threadIdx.x == 0) IntroSort<double, LessD>{}.sort(c, k);
+    __syncthreads();
+    return iters;
+}
+
+// weighted_sq_loss (quantize.cpp:166-178): per-point minima in parallel, the sum
+// sequentially in point order.
+__device__ double sq_loss_block(const double* pts, const double* w, int n, const double* c, int k,
+                                double* tmp, KShared& sm) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double best = __longlong_as_double(0x7ff0000000000000LL);
+        for (int j = 0; j < k; ++j) {
+            double d = __dsub_rn(pts[i], c[j]);
+            double sq = __dmul_rn(d, d);
+            best = sq < best ? sq : best;
+        }
+        tmp[i] = __dmul_rn(w[i], best);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double loss = 0.0;
+        for (int i = 0; i < n; ++i) loss = __dadd_rn(loss, tmp[i]);
+        sm.red[0] = loss;
+    }
+    __syncthreads();
+    double r = sm.red[0];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(kKB) kmeans_restarts_kernel(const KProblem* probs,
+                                                              int restarts) {
+    extern __shared__ double dsm[];
+    __shared__ KShared sm;
+    const KProblem& P = probs[blockIdx.x / restarts];
+    const int t = blockIdx.x % restarts;
+    const int n = P.n, k = P.k;
+    if (n < k || k <= 0 || P.skip) return;
+    double* c = dsm;
+    double* nx = c + k;
+    int* first = (int*)(nx + k);
+    int* last = first + k;
+    int* cnt = last + k;
+    double* d2 = P.scratch + (size_t)t * P.scratch_stride;
+    double* prob = d2 + n;
+    double* pref = prob + n;
+    int* assign = (int*)(pref + n);
+    ScoreVal* top = (ScoreVal*)d2;  // reseed scratch reuses d2/prob (2n doubles)
+    if (threadIdx.x == 0) mt64_seed(sm.rng, P.seed + (uint64_t)t);
+    __syncthreads();
+    kpp_init(P.pts, P.w, n, k, d2, prob, pref, c, sm);
+    lloyd_block(P.pts, P.w, n, c, nx, first, last, cnt, k, 1e-6, 100, assign, pref, top, true, sm);
+    double loss = sq_loss_block(P.pts, P.w, n, c, k, prob, sm);
+    for (int j = threadIdx.x; j < k; j += blockDim.x) P.centers[(size_t)t * k + j] = c[j];
+    if (threadIdx.x == 0) P.loss[t] = loss;
+}
+
+// Restart selection + float cast + dedup (quantize.cpp:306-324).
+__global__ void kmeans_select_kernel(const KProblem* probs, int restarts, float* cb_out,
+                                     int cb_stride, uint32_t* cb_len) {
+    const KProblem& P = probs[blockIdx.x];
+    if (threadIdx.x != 0 || P.skip || P.n < P.k) return;
+    double best = __longlong_as_double(0x7ff0000000000000LL);
+    int bt = -1;
+    for (int t = 0; t < restarts; ++t)
+        if (P.loss[t] < best) {
+            best = P.loss[t];
+            bt = t;
+        }
+    float* cb = cb_out + (size_t)P.slot * cb_stride;
+    uint32_t o = 0;
+    if (bt >= 0)
+        for (int j = 0; j < P.k; ++j) {
+            float f = __double2float_rn(P.centers[(size_t)bt * P.k + j]);
+            if (o == 0 || f != cb[o - 1]) cb[o++] = f;
+        }
+    cb_len[P.slot] = o;
+}
+
+// ---- host side -------------------------------------------------------------
+void run_kmeans(Engine& e, std::vector<KProblem>& probs, float* cb_out, int cb_stride,
+                uint32_t* cb_len_dev) {
+    if (probs.empty()) return;
+    const int restarts = 8;  // quantize.cpp:306
+    size_t scratch_doubles = 0, centers = 0;
+    int maxk = 1;
+    for (auto& p : probs) {
+        p.scratch_stride = (size_t)4 * p.n + 8;
+        scratch_doubles += p.scratch_stride * restarts;
+        centers += (size_t)p.k * restarts;
+        maxk = p.k > maxk ? p.k : maxk;
+    }
+    double* scr = (double*)e.buf("km.scratch", scratch_doubles * 8);
+    double* cen = (double*)e.buf("km.centers", (centers + 8) * 8);
+    double* loss = (double*)e.buf("km.loss", probs.size() * restarts * 8);
+    size_t so = 0, co = 0;
+    for (size_t i = 0; i < probs.size(); ++i) {
+        probs[i].scratch = scr + so;
+        so += probs[i].scratch_stride * restarts;
+        probs[i].centers = cen + co;
+        co += (size_t)probs[i].k * restarts;
+        probs[i].loss = loss + i * restarts;
+    }
+    KProblem* dp = (KProblem*)e.buf("km.probs", probs.size() * sizeof(KProblem));
+    DQTG_CUDA(cudaMemcpyAsync(dp, probs.data(), probs.size() * sizeof(KProblem),
+                              cudaMemcpyHostToDevice, e.stream));
+    size_t smem = (size_t)maxk * (2 * 8 + 3 * 4) + 16;
+    if (smem > 48 * 1024)
+        DQTG_CUDA(cudaFuncSetAttribute(kmeans_restarts_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kmeans_restarts_kernel<<<(unsigned)(probs.size() * restarts), kKB, smem, e.stream>>>(dp,
+                                                                                      restarts);
+    kmeans_select_kernel<<<(unsigned)probs.size(), 32, 0, e.stream>>>(dp, restarts, cb_out,
+                                                                       cb_stride, cb_len_dev);
+    e.launched(2);
+    DQTG_CUDA(cudaGetLastError());
+}
+
+void compact_keys(Engine& e, const unsigned long long* hist, int64_t hs_stride, int64_t HS,
+                  const double* key, double sigma, int nprob, double* pts,
+                  unsigned long long* cnt, double* w, int64_t out_stride, int* n_keys) {
+    compact_keys_kernel<<<nprob, 1024, 0, e.stream>>>(hist, hs_stride, HS, key, sigma, pts, cnt,
+                                                      w, out_stride, n_keys);
+    e.launched();
+    DQTG_CUDA(cudaGetLastError());
+}
+
+}  // namespace dqtg
+
+// ---- stand-alone clustering entry points (weighted_kmeanspp_init /
+// weighted_lloyd / weighted_sq_loss, quantize.cpp:94-254) for arbitrary points ----
+namespace dqtg {
+
+__global__ void __launch_bounds__(kKB) kpp_api_kernel(const double* pts, const double* w, int n,
+                                                      int k, uint64_t seed, double* scratch,
+                                                      double* out, int* status) {
+    extern __shared__ double dsm[];
+    __shared__ KShared sm;
+    // validation (quantize.cpp:98-113): weights, total, distinct count
+    if (threadIdx.x == 0) {
+        int st = 0;
+        bool pos = false;
+        for (int i = 0; i < n; ++i) {
+            if (!(w[i] >= 0.0)) st = 1;
+            pos |= w[i] > 0.0;
+        }
+        if (!st && !pos) st = 2;
+        if (!st) {
+            double* d = scratch + (size_t)4 * n;
+            for (int i = 0; i < n; ++i) d[i] = pts[i];
+            IntroSort<double, LessD>{}.sort(d, n);
+            int distinct = 0;
+            for (int i = 0; i < n; ++i)
+                if (i == 0 || !(d[i] == d[distinct - 1])) d[distinct++] = d[i];
+            if (distinct < k) st = 3;
+        }
+        *status = st;
+        mt64_seed(sm.rng, seed);
+    }
+    __syncthreads();
+    if (*status) return;
+    double* d2 = scratch;
+    double* prob = d2 + n;
+    double* pref = prob + n;
+    kpp_init(pts, w, n, k, d2, prob, pref, dsm, sm);
+    for (int j = threadIdx.x; j < k; j += blockDim.x) out[j] = dsm[j];
+}
+
+__global__ void __launch_bounds__(kKB) lloyd_api_kernel(const double* pts, const double* w, int n,
+                                                        int k, double tol, int max_iter,
+                                                        double* scratch, double* centers,
+                                                        int* iters) {
+    extern __shared__ double dsm[];
+    __shared__ KShared sm;
+    double* c = dsm;
+    double* nx = c + k;
+    int* first = (int*)(nx + k);
+    int* last = first + k;
+    int* cnt = last + k;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) c[j] = centers[j];
+    __syncthreads();
+    int* assign = (int*)(scratch + (size_t)3 * n);
+    ScoreVal* top = (ScoreVal*)scratch;
+    double* score = scratch + (size_t)2 * n;
+    int it = lloyd_block(pts, w, n, c, nx, first, last, cnt, k, tol, max_iter, assign, score, top,
+                         false, sm);
+    for (int j = threadIdx.x; j < k; j += blockDim.x) centers[j] = c[j];
+    if (threadIdx.x == 0) *iters = it;
+}
+
+__global__ void __launch_bounds__(kKB) loss_api_kernel(const double* pts, const double* w, int n,
+                                                       const double* c, int k, double* tmp,
+                                                       double* out) {
+    __shared__ KShared sm;
+    double l = sq_loss_block(pts, w, n, c, k, tmp, sm);
+    if (threadIdx.x == 0) *out = l;
+}
+
+struct DevArrays {
+    double *pts, *w, *scr, *c;
+    int* st;
+};
+
+static DevArrays stage(Engine& e, const double* pts, const double* w, uint64_t n, uint32_t k,
+                       const double* centers) {
+    DevArrays d;
+    d.pts = (double*)e.buf("kapi.pts", n * 8 + 8);
+    d.w = (double*)e.buf("kapi.w", n * 8 + 8);
+    d.scr = (double*)e.buf("kapi.scr", (5 * n + 8) * 8);
+    d.c = (double*)e.buf("kapi.c", (size_t)k * 8 + 8);
+    d.st = (int*)e.buf("kapi.st", 16);
+    e.to_device(d.pts, pts, n * 8);
+    e.to_device(d.w, w, n * 8);
+    if (centers) e.to_device(d.c, centers, (size_t)k * 8);
+    return d;
+}
+
+void kmeanspp_host_api(Engine& e, const double* pts, const double* w, uint64_t n, uint32_t k,
+                       uint64_t seed, double* centers) {
+    DQTG_REQUIRE(k >= 1, DQTG_ERROR, "k must be >= 1");
+    DevArrays d = stage(e, pts, w, n, k, nullptr);
+    kpp_api_kernel<<<1, kKB, (size_t)k * 8 + 16, e.stream>>>(d.pts, d.w, (int)n, (int)k, seed,
+                                                             d.scr, d.c, d.st);
+    e.launched();
+    int st = 0;
+    DQTG_CUDA(cudaMemcpyAsync(&st, d.st, 4, cudaMemcpyDeviceToHost, e.stream));
+    e.sync();
+    DQTG_REQUIRE(st != 1, DQTG_ERROR, "weights must be non-negative");
+    DQTG_REQUIRE(st != 2, DQTG_ERROR, "total weight must be positive");
+    if (st == 3) {
+        // count distinct again on the host side of the message only
+        throw Fail(DQTG_TOO_FEW_DISTINCT, "need " + std::to_string(k) + " distinct points");
+    }
+    e.from_device(centers, d.c, (size_t)k * 8);
+    e.sync();
+}
+
+void lloyd_host_api(Engine& e, const double* pts, const double* w, uint64_t n, double* centers,
+                    uint32_t k, double tol, uint32_t max_iter, uint32_t* iters) {
+    DQTG_REQUIRE(k >= 1, DQTG_ERROR, "no initial centers");
+    DevArrays d = stage(e, pts, w, n, k, centers);
+    int* it = d.st;
+    lloyd_api_kernel<<<1, kKB, (size_t)k * (2 * 8 + 3 * 4) + 16, e.stream>>>(
+        d.pts, d.w, (int)n, (int)k, tol, (int)max_iter, d.scr, d.c, it);
+    e.launched();
+    int h = 0;
+    DQTG_CUDA(cudaMemcpyAsync(&h, it, 4, cudaMemcpyDeviceToHost, e.stream));
+    e.from_device(centers, d.c, (size_t)k * 8);
+    e.sync();
+    if (iters) *iters = (uint32_t)h;
+}
+
+double sq_loss_host_api(Engine& e, const double* pts, const double* w, uint64_t n,
+                        const double* centers, uint32_t k) {
+    DevArrays d = stage(e, pts, w, n, k, centers);
+    loss_api_kernel<<<1, kKB, 0, e.stream>>>(d.pts, d.w, (int)n, d.c, (int)k, d.scr, d.scr + n + 1);
+    e.launched();
+    double h = 0;
+    DQTG_CUDA(cudaMemcpyAsync(&h, d.scr + n + 1, 8, cudaMemcpyDeviceToHost, e.stream));
+    e.sync();
+    return h;
+}
+
+}  // namespace dqtg

@@ -1,0 +1,433 @@
+"""ctypes front-end of the B200 engine's C ABI (include/dqtg.h, libdqtg.so).
+
+This is the device-resident API used by bench.py and the distributed driver:
+checkpoints stay in HBM (``DevCheckpoint``), quantized states stay in HBM
+(``DevState``) and records are produced on the device.  The reference-shaped
+value API (``dqt`` module, include/dqt/*.hpp) sits on the same C ABI.
+
+There is no CPU fallback: importing this module on a machine without the built
+library raises, and creating an ``Engine`` without a Blackwell GPU raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libdqtg.so")
+
+# dqtg_status -> exception name of the reference (include/dqt/errors.hpp)
+STATUS_NAMES = {
+    1: "Error", 2: "BadMagic", 3: "TruncatedFile", 4: "ShapeMismatch", 5: "NonFiniteData",
+    6: "IoError", 7: "AlphaOutOfRange", 8: "AlphaMismatch", 9: "EmptySketch",
+    10: "MissingGradients", 11: "MissingScores", 12: "TooFewDistinctPoints", 13: "CorruptIndex",
+    14: "CorruptBitstream", 15: "ChecksumMismatch", 16: "ChainCorrupt", 17: "CudaError",
+}
+
+
+class EngineError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+        self.kind = STATUS_NAMES.get(status, "Error")
+
+
+class Config(C.Structure):
+    """dqtg_config == dqt::QuantConfig (quantize.hpp:13-26)."""
+    _fields_ = [("bins", C.c_uint32), ("embed_bins", C.c_uint32), ("prune_frac", C.c_double),
+                ("protect_frac", C.c_double), ("metric", C.c_uint32), ("sigma", C.c_double),
+                ("alpha", C.c_double)]
+
+    def __init__(self, bins=16, embed_bins=32, prune_frac=0.0, protect_frac=0.005, metric=0,
+                 sigma=0.2, alpha=0.01):
+        super().__init__(bins, embed_bins, prune_frac, protect_frac, int(metric), sigma, alpha)
+
+    def astuple(self):
+        return (self.bins, self.embed_bins, self.prune_frac, self.protect_frac, self.metric,
+                self.sigma, self.alpha)
+
+
+class _Layout(C.Structure):
+    _fields_ = [("n_tensors", C.c_uint32), ("names", C.POINTER(C.c_char_p)),
+                ("types", C.POINTER(C.c_uint8)), ("ranks", C.POINTER(C.c_uint8)),
+                ("dims", C.POINTER(C.c_uint64))]
+
+
+class _Info(C.Structure):
+    _fields_ = [("step", C.c_uint64), ("config", Config), ("codebook_len", C.c_uint32 * 7),
+                ("max_levels", C.c_uint32), ("param_count", C.c_uint64),
+                ("protected_total", C.c_uint64)]
+
+
+_P = C.c_void_p
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() (make -C "
+                          f"paper_2306_11800_b200/csrc)")
+    L = C.CDLL(LIB_PATH)
+    sig = {
+        "dqtg_last_error": (C.c_char_p, []),
+        "dqtg_engine_create": (C.c_int, [C.c_int, _P, C.POINTER(_P)]),
+        "dqtg_engine_destroy": (None, [_P]),
+        "dqtg_engine_sync": (C.c_int, [_P]),
+        "dqtg_engine_launches": (C.c_uint64, [_P]),
+        "dqtg_sketch_range": (C.c_int, [C.c_double, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+        "dqtg_sketch_build": (C.c_int, [_P, _P, C.c_uint64, C.c_double, C.POINTER(C.c_uint64),
+                                        _P, _P]),
+        "dqtg_ema_update": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_double]),
+        "dqtg_compute_scores": (C.c_int, [_P, _P, _P, C.c_uint64, _P, _P]),
+        "dqtg_ckpt_create": (C.c_int, [_P, C.POINTER(_Layout), C.POINTER(_P)]),
+        "dqtg_ckpt_destroy": (None, [_P]),
+        "dqtg_ckpt_set_weights": (C.c_int, [_P, _P]),
+        "dqtg_ckpt_set_scores": (C.c_int, [_P, _P, _P]),
+        "dqtg_ckpt_set_ema": (C.c_int, [_P, _P]),
+        "dqtg_ckpt_update_ema": (C.c_int, [_P, _P, C.c_double]),
+        "dqtg_ckpt_param_count": (C.c_uint64, [_P]),
+        "dqtg_ckpt_weights_dev": (_P, [_P]),
+        "dqtg_ckpt_ema_dev": (_P, [_P]),
+        "dqtg_ckpt_tensor_offset": (C.c_uint64, [_P, C.c_uint32]),
+        "dqtg_quantize": (C.c_int, [_P, _P, C.POINTER(Config), C.c_uint64, C.c_uint64,
+                                    C.POINTER(_P)]),
+        "dqtg_qstate_info_get": (C.c_int, [_P, C.POINTER(_Info)]),
+        "dqtg_qstate_protected_counts": (C.c_int, [_P, _P]),
+        "dqtg_qstate_download": (C.c_int, [_P, _P, _P, _P, _P]),
+        "dqtg_qstate_upload": (C.c_int, [_P, C.POINTER(_Layout), C.c_uint64, C.POINTER(Config),
+                                         _P, _P, _P, _P, _P, _P, C.POINTER(_P)]),
+        "dqtg_qstate_destroy": (None, [_P]),
+        "dqtg_qstate_levels_dev": (_P, [_P]),
+        "dqtg_dequantize": (C.c_int, [_P, _P, _P]),
+        "dqtg_encode_record": (C.c_int, [_P, _P, _P, C.c_double, C.POINTER(_P)]),
+        "dqtg_record_size": (C.c_uint64, [_P]),
+        "dqtg_record_copy": (C.c_int, [_P, _P]),
+        "dqtg_record_dev": (_P, [_P]),
+        "dqtg_record_destroy": (None, [_P]),
+        "dqtg_decode_record": (C.c_int, [_P, C.c_char_p, C.c_uint64, _P, C.POINTER(_P)]),
+        "dqtg_compress_step": (C.c_int, [_P, _P, C.POINTER(Config), C.c_uint64, C.c_uint64, _P,
+                                         C.c_double, C.POINTER(_P), C.POINTER(_P)]),
+        "dqtg_eval_batch": (C.c_int, [_P, _P, _P, _P, C.c_uint32, _P, _P]),
+        "dqtg_approx_kmeans": (C.c_int, [_P, _P, C.c_uint64, C.c_uint32, C.c_double, C.c_double,
+                                         C.c_uint64, _P, C.POINTER(C.c_uint32)]),
+        "dqtg_kmeanspp_init": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint64, _P]),
+        "dqtg_lloyd": (C.c_int, [_P, _P, _P, C.c_uint64, _P, C.c_uint32, C.c_double, C.c_uint32,
+                                 C.POINTER(C.c_uint32)]),
+        "dqtg_sq_loss": (C.c_int, [_P, _P, _P, C.c_uint64, _P, C.c_uint32,
+                                   C.POINTER(C.c_double)]),
+        "dqtg_delta_compute": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_uint32, _P]),
+        "dqtg_delta_apply": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_uint32, _P]),
+        "dqtg_crc32": (C.c_int, [_P, _P, C.c_uint64, C.POINTER(C.c_uint32)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    return L
+
+
+LIB = _load()
+
+
+def _check(rc):
+    if rc:
+        raise EngineError(rc, LIB.dqtg_last_error().decode(errors="replace"))
+
+
+def _ptr(a):
+    return a.ctypes.data if isinstance(a, np.ndarray) else int(a)
+
+
+class _Meta:
+    """Keeps the ctypes arrays of a dqtg_layout alive."""
+
+    def __init__(self, names, types, shapes):
+        self.names = list(names)
+        self.types = [int(t) for t in types]
+        self.shapes = [tuple(int(d) for d in s) for s in shapes]
+        n = len(self.names)
+        self._names = (C.c_char_p * max(n, 1))(*[s.encode() for s in self.names])
+        self._types = np.array(self.types or [0], np.uint8)
+        self._ranks = np.array([len(s) for s in self.shapes] or [0], np.uint8)
+        self._dims = np.array([d for s in self.shapes for d in s] or [0], np.uint64)
+        self.c = _Layout(n, self._names, self._types.ctypes.data_as(C.POINTER(C.c_uint8)),
+                         self._ranks.ctypes.data_as(C.POINTER(C.c_uint8)),
+                         self._dims.ctypes.data_as(C.POINTER(C.c_uint64)))
+        self.numel = [int(np.prod(s, dtype=np.uint64)) for s in self.shapes]
+
+
+def _ptr_array(arrs):
+    return (C.c_void_p * max(len(arrs), 1))(*[_ptr(a) for a in arrs])
+
+
+@dataclass
+class HostState:
+    """Host copy of a quantized state (dqt::QuantizedCheckpoint)."""
+    step: int
+    config: tuple
+    codebooks: list
+    names: list
+    types: list
+    shapes: list
+    levels: list
+    prot_pos: list = field(default_factory=list)
+    prot_val: list = field(default_factory=list)
+
+
+class DevCheckpoint:
+    def __init__(self, engine, names, types, shapes):
+        self.engine = engine
+        self.meta = _Meta(names, types, shapes)
+        h = _P()
+        _check(LIB.dqtg_ckpt_create(engine.h, C.byref(self.meta.c), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            LIB.dqtg_ckpt_destroy(self.h)
+            self.h = None
+
+    def set_weights(self, arrays):
+        arrs = [np.ascontiguousarray(a, np.float32) if isinstance(a, np.ndarray) else a
+                for a in arrays]
+        _check(LIB.dqtg_ckpt_set_weights(self.h, _ptr_array(arrs)))
+
+    def set_scores(self, mag, sens=None):
+        m = [np.ascontiguousarray(a, np.float32) for a in mag]
+        s = None if sens is None else [np.ascontiguousarray(a, np.float32) for a in sens]
+        _check(LIB.dqtg_ckpt_set_scores(self.h, _ptr_array(m), None if s is None else _ptr_array(s)))
+
+    def set_ema(self, ema):
+        e = None if ema is None else [np.ascontiguousarray(a, np.float32) for a in ema]
+        _check(LIB.dqtg_ckpt_set_ema(self.h, None if e is None else _ptr_array(e)))
+
+    def update_ema(self, grads, beta=0.9):
+        g = [np.ascontiguousarray(a, np.float32) for a in grads]
+        _check(LIB.dqtg_ckpt_update_ema(self.h, _ptr_array(g), beta))
+
+    @property
+    def weights_dev(self):
+        return LIB.dqtg_ckpt_weights_dev(self.h)
+
+    @property
+    def ema_dev(self):
+        return LIB.dqtg_ckpt_ema_dev(self.h)
+
+    def tensor_offset(self, i):
+        return LIB.dqtg_ckpt_tensor_offset(self.h, i)
+
+
+class DevState:
+    def __init__(self, engine, h, meta):
+        self.engine, self.h, self.meta = engine, h, meta
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            LIB.dqtg_qstate_destroy(self.h)
+            self.h = None
+
+    def info(self):
+        i = _Info()
+        _check(LIB.dqtg_qstate_info_get(self.h, C.byref(i)))
+        return i
+
+    @property
+    def levels_dev(self):
+        return LIB.dqtg_qstate_levels_dev(self.h)
+
+    def download(self) -> HostState:
+        info = self.info()
+        m = self.meta
+        nt = len(m.names)
+        counts = np.zeros(max(nt, 1), np.uint64)
+        _check(LIB.dqtg_qstate_protected_counts(self.h, counts.ctypes.data))
+        levels = [np.zeros(n, np.uint16) for n in m.numel]
+        pp = [np.zeros(int(c), np.uint64) for c in counts[:nt]]
+        pv = [np.zeros(int(c), np.uint16) for c in counts[:nt]]
+        cbs = [np.zeros(info.codebook_len[lt], np.float32) for lt in range(7)]
+        _check(LIB.dqtg_qstate_download(self.h, _ptr_array(levels), _ptr_array(pp),
+                                        _ptr_array(pv), _ptr_array(cbs)))
+        return HostState(int(info.step), info.config.astuple(), cbs, list(m.names),
+                         list(m.types), list(m.shapes), levels, pp, pv)
+
+    def dequantize(self):
+        outs = [np.zeros(n, np.float32) for n in self.meta.numel]
+        _check(LIB.dqtg_dequantize(self.engine.h, self.h, _ptr_array(outs)))
+        return outs
+
+
+class Engine:
+    def __init__(self, device=0, stream=None):
+        h = _P()
+        _check(LIB.dqtg_engine_create(device, stream, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            LIB.dqtg_engine_destroy(self.h)
+            self.h = None
+
+    def sync(self):
+        _check(LIB.dqtg_engine_sync(self.h))
+
+    @property
+    def launches(self):
+        return LIB.dqtg_engine_launches(self.h)
+
+    # -- sketch ------------------------------------------------------------
+    @staticmethod
+    def sketch_range(alpha):
+        a, b = C.c_int64(), C.c_int64()
+        _check(LIB.dqtg_sketch_range(alpha, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def sketch_build(self, x, alpha):
+        x = np.ascontiguousarray(x, np.float32)
+        kmin, kmax = self.sketch_range(alpha)
+        pos = np.zeros(kmax - kmin + 1, np.uint64)
+        neg = np.zeros_like(pos)
+        z = C.c_uint64()
+        _check(LIB.dqtg_sketch_build(self.h, x.ctypes.data, x.size, alpha, C.byref(z),
+                                     pos.ctypes.data, neg.ctypes.data))
+        return kmin, z.value, pos, neg
+
+    # -- checkpoints / quantize ------------------------------------------------
+    def checkpoint(self, names, types, shapes, weights=None, mag=None, sens=None, ema=None):
+        c = DevCheckpoint(self, names, types, shapes)
+        if weights is not None:
+            c.set_weights(weights)
+        if mag is not None:
+            c.set_scores(mag, sens)
+        elif ema is not None:
+            c.set_ema(ema)
+        return c
+
+    def quantize(self, ckpt: DevCheckpoint, cfg: Config, seed=1, step=0) -> DevState:
+        h = _P()
+        _check(LIB.dqtg_quantize(self.h, ckpt.h, C.byref(cfg), seed, step, C.byref(h)))
+        return DevState(self, h, ckpt.meta)
+
+    def upload_state(self, st: HostState) -> DevState:
+        meta = _Meta(st.names, st.types, st.shapes)
+        cfg = Config(*st.config)
+        cbl = np.array([len(c) for c in st.codebooks], np.uint32)
+        cbs = [np.ascontiguousarray(c, np.float32) for c in st.codebooks]
+        lv = [np.ascontiguousarray(x, np.uint16).ravel() for x in st.levels]
+        npr = np.array([len(p) for p in st.prot_pos] or [0], np.uint64)
+        pp = [np.ascontiguousarray(p, np.uint64) for p in st.prot_pos]
+        pv = [np.ascontiguousarray(p, np.uint16) for p in st.prot_val]
+        h = _P()
+        _check(LIB.dqtg_qstate_upload(self.h, C.byref(meta.c), st.step, C.byref(cfg),
+                                      cbl.ctypes.data, _ptr_array(cbs), _ptr_array(lv),
+                                      npr.ctypes.data, _ptr_array(pp), _ptr_array(pv),
+                                      C.byref(h)))
+        return DevState(self, h, meta)
+
+    # -- records -------------------------------------------------------------------
+    def encode_record(self, target: DevState, base: DevState = None, quality=0.0) -> bytes:
+        r = _P()
+        _check(LIB.dqtg_encode_record(self.h, None if base is None else base.h, target.h,
+                                      quality, C.byref(r)))
+        try:
+            n = LIB.dqtg_record_size(r)
+            out = np.empty(n, np.uint8)
+            _check(LIB.dqtg_record_copy(r, out.ctypes.data))
+            return out.tobytes()
+        finally:
+            LIB.dqtg_record_destroy(r)
+
+    def encode_record_handle(self, target, base=None, quality=0.0):
+        r = _P()
+        _check(LIB.dqtg_encode_record(self.h, None if base is None else base.h, target.h,
+                                      quality, C.byref(r)))
+        return r
+
+    def decode_record(self, rec: bytes, base: DevState = None) -> DevState:
+        h = _P()
+        _check(LIB.dqtg_decode_record(self.h, rec, len(rec), None if base is None else base.h,
+                                      C.byref(h)))
+        return h
+
+    def compress_step(self, ckpt, cfg, seed, step, base=None, quality=0.0):
+        s, r = _P(), _P()
+        _check(LIB.dqtg_compress_step(self.h, ckpt.h, C.byref(cfg), seed, step,
+                                      None if base is None else base.h, quality, C.byref(s),
+                                      C.byref(r)))
+        return DevState(self, s, ckpt.meta), r
+
+    # -- clustering / primitives ------------------------------------------------------
+    def approx_kmeans(self, values, k, sigma=0.2, alpha=0.01, seed=1):
+        v = np.ascontiguousarray(values, np.float32).ravel()
+        out = np.zeros(max(k, 1), np.float32)
+        n = C.c_uint32()
+        _check(LIB.dqtg_approx_kmeans(self.h, v.ctypes.data, v.size, k, sigma, alpha, seed,
+                                      out.ctypes.data, C.byref(n)))
+        return out[:n.value].copy()
+
+    def crc32(self, data: bytes):
+        b = np.frombuffer(data, np.uint8) if len(data) else np.zeros(1, np.uint8)
+        c = C.c_uint32()
+        _check(LIB.dqtg_crc32(self.h, b.ctypes.data, len(data), C.byref(c)))
+        return c.value
+
+    def ema_update(self, ema, g, beta=0.9):
+        e = np.ascontiguousarray(ema, np.float32).copy()
+        g = np.ascontiguousarray(g, np.float32)
+        _check(LIB.dqtg_ema_update(self.h, e.ctypes.data, g.ctypes.data, e.size, beta))
+        return e
+
+    def compute_scores(self, w, ema=None):
+        w = np.ascontiguousarray(w, np.float32)
+        mag = np.zeros_like(w)
+        sens = None if ema is None else np.zeros_like(w)
+        e = None if ema is None else np.ascontiguousarray(ema, np.float32)
+        _check(LIB.dqtg_compute_scores(self.h, w.ctypes.data, None if e is None else e.ctypes.data,
+                                       w.size, mag.ctypes.data,
+                                       None if sens is None else sens.ctypes.data))
+        return mag, sens
+
+    def delta_compute(self, prev, cur, B):
+        p = np.ascontiguousarray(prev, np.uint16)
+        c = np.ascontiguousarray(cur, np.uint16)
+        out = np.zeros(max(p.size, 1), np.uint16)
+        _check(LIB.dqtg_delta_compute(self.h, p.ctypes.data, c.ctypes.data, p.size, B,
+                                      out.ctypes.data))
+        return out[:p.size]
+
+    def kmeanspp_init(self, pts, w, k, seed):
+        p = np.ascontiguousarray(pts, np.float64)
+        ww = np.ascontiguousarray(w, np.float64)
+        out = np.zeros(k, np.float64)
+        _check(LIB.dqtg_kmeanspp_init(self.h, p.ctypes.data, ww.ctypes.data, p.size, k, seed,
+                                      out.ctypes.data))
+        return out
+
+    def lloyd(self, pts, w, centers, tol=1e-6, max_iter=100):
+        p = np.ascontiguousarray(pts, np.float64)
+        ww = np.ascontiguousarray(w, np.float64)
+        c = np.array(centers, np.float64)
+        it = C.c_uint32()
+        _check(LIB.dqtg_lloyd(self.h, p.ctypes.data, ww.ctypes.data, p.size, c.ctypes.data,
+                              c.size, tol, max_iter, C.byref(it)))
+        return c, it.value
+
+    def sq_loss(self, pts, w, centers):
+        p = np.ascontiguousarray(pts, np.float64)
+        ww = np.ascontiguousarray(w, np.float64)
+        c = np.ascontiguousarray(centers, np.float64)
+        out = C.c_double()
+        _check(LIB.dqtg_sq_loss(self.h, p.ctypes.data, ww.ctypes.data, p.size, c.ctypes.data,
+                                c.size, C.byref(out)))
+        return out.value
+
+
+_DEFAULT = None
+
+
+def default_engine() -> Engine:
+    global _DEFAULT
+    if _DEFAULT is None:
+        _DEFAULT = Engine(int(os.environ.get("DQT_DEVICE", "0")))
+    return _DEFAULT
