@@ -1,0 +1,440 @@
+#!/usr/bin/env python3
+"""Benchmark: checkpoint compress + delta-encode throughput (fp32-in GB/s) on B200.
+
+Workload (BASELINE.json configs[1], "C2"): GPT-2-small layout (124,439,808 fp32
+params, 148 tensors, layer types per SURVEY.md §8d), a synthetic training
+trajectory generated on the GPU with the reference generator's dynamics
+(w0 = 0.05 N(0,1); g = w + 0.0025 N(0,1); w -= lr g; lr = 0.1 * 0.9^t,
+trajectory.cpp:75-113), gradient EMA over the first two gradients, default
+QuantConfig (bins 16, embed 32, prune 0, protect 0.005, MAGNITUDE, sigma 0.2,
+alpha 0.01).  One step = compute_scores (fused) + quantize_checkpoint +
+encode_delta_record against the previous snapshot's quantized state — the
+Chain::append path — for the next snapshot of the series.
+
+value: device-resident (weights + EMA in HBM, previous levels in HBM, record
+produced in HBM), CUDA events on the engine stream, max over ranks.
+e2e:   same step through the C ABI with HOST buffers: pinned weights H2D, the
+step, record D2H, every step.
+Inputs per step (1 GB of weights+EMA) exceed the 126 MB L2, so no flush is needed.
+
+--impl reference: the unmodified reference library (oracle/_ref, compiled from
+/root/reference/proj sources) on the host cores, on a bounded sample of the
+same workload (two GPT-2 blocks + ln_f, 14.2 M params), same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "checkpoint compress+delta GB/s (fp32 in)"
+
+# ---------------------------------------------------------------------------- workload
+EMB, ATT, NORM, BIAS, LIN = 4, 2, 3, 5, 1
+
+
+def gpt2_small_layout(blocks=range(12), with_embed=True, with_lnf=True):
+    d, v, ctx = 768, 50257, 1024
+    L = []
+    if with_embed:
+        L += [("transformer.wte.weight", EMB, (v, d)), ("transformer.wpe.weight", EMB, (ctx, d))]
+    for i in blocks:
+        p = f"transformer.h.{i}."
+        L += [(p + "ln_1.weight", NORM, (d,)), (p + "ln_1.bias", BIAS, (d,)),
+              (p + "attn.c_attn.weight", ATT, (d, 3 * d)), (p + "attn.c_attn.bias", BIAS, (3 * d,)),
+              (p + "attn.c_proj.weight", ATT, (d, d)), (p + "attn.c_proj.bias", BIAS, (d,)),
+              (p + "ln_2.weight", NORM, (d,)), (p + "ln_2.bias", BIAS, (d,)),
+              (p + "mlp.c_fc.weight", LIN, (d, 4 * d)), (p + "mlp.c_fc.bias", BIAS, (4 * d,)),
+              (p + "mlp.c_proj.weight", LIN, (4 * d, d)), (p + "mlp.c_proj.bias", BIAS, (d,))]
+    if with_lnf:
+        L += [("transformer.ln_f.weight", NORM, (d,)), ("transformer.ln_f.bias", BIAS, (d,))]
+    return L
+
+
+def numel(shape):
+    return int(np.prod(shape, dtype=np.int64))
+
+
+def read_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- reference arm
+def reference_sample_inputs(seed=7):
+    """Bounded CPU sample of the C2 workload: blocks 0-1 + ln_f of GPT-2 small."""
+    layout = gpt2_small_layout(blocks=range(2), with_embed=False)
+    N = sum(numel(s) for _, _, s in layout)
+    rng = np.random.default_rng(seed)
+    w1 = (0.05 * rng.standard_normal(N)).astype(np.float32)
+    g1 = (w1 + 0.0025 * rng.standard_normal(N)).astype(np.float32)
+    w2 = (w1 - np.float32(0.1) * g1).astype(np.float32)
+    g2 = (w2 + 0.0025 * rng.standard_normal(N)).astype(np.float32)
+    return layout, w1, w2, g1, g2
+
+
+def _ref_ckpt(d, layout, flat, step):
+    c = d.Checkpoint()
+    c.step = step
+    o = 0
+    for name, lt, shape in layout:
+        n = numel(shape)
+        c.add_tensor(name, flat[o:o + n].reshape(shape), d.LayerType(lt))
+        o += n
+    return c
+
+
+def reference_step_timer():
+    """Returns (time_one_step(), params, records) using the reference library."""
+    from oracle import ref as R
+
+    if not R.available():
+        subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "ref"])
+    d = R.load()
+    layout, w1, w2, g1, g2 = reference_sample_inputs()
+    c1, c2 = _ref_ckpt(d, layout, w1, 1), _ref_ckpt(d, layout, w2, 2)
+    ema = d.ema_init(0.9)
+    d.ema_update(ema, _ref_ckpt(d, layout, g1, 1))
+    d.ema_update(ema, _ref_ckpt(d, layout, g2, 2))
+    cfg = d.QuantConfig()
+    s1 = d.compute_scores(c1, ema)
+    q1 = d.quantize_checkpoint(c1, s1, cfg, 1)
+    out = {}
+
+    def step():
+        t = time.perf_counter()
+        s2 = d.compute_scores(c2, ema)
+        q2 = d.quantize_checkpoint(c2, s2, cfg, 1)
+        rec = d.encode_delta_record(q2, q1)
+        dt = time.perf_counter() - t
+        out["record"] = bytes(rec)
+        return dt
+
+    N = sum(numel(s) for _, _, s in layout)
+    return step, N, out
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    step, N, out = reference_step_timer()
+    for _ in range(args.warmup):
+        step()
+    ts = [step() for _ in range(args.steps)]
+    t = sum(ts)
+    value = 4.0 * N * args.steps / t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": "C2 GPT-2-small compress+delta, bounded CPU sample "
+                               "(blocks 0-1 + ln_f, 14.2M params)", "params": N},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "reference",
+                         "sample": f"{N} params (GPT-2 small blocks 0-1 + ln_f), "
+                                   f"{args.steps} steps of quantize+encode_delta"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- our arm
+ALGO_BYTES = {  # algorithmic HBM bytes per parameter per launch
+    "pass_a_kernel": 8.0,   # read w + EMA
+    "pass_b_kernel": 8.0,   # read w + EMA
+    "pass_c_kernel": 10.0,  # read w + EMA, write levels
+    "enc_tile_kernel": 4.0,  # read levels + previous levels
+}
+
+
+def gen_series(torch, layout, n_snap, seed, device):
+    """Synthetic trajectory on the GPU (reference generator dynamics)."""
+    N = sum(numel(s) for _, _, s in layout)
+    g = torch.Generator(device=device).manual_seed(seed)
+    w = 0.05 * torch.randn(N, generator=g, device=device, dtype=torch.float32)
+    lr = 0.1
+    snaps, grads = [], []
+    for s in range(n_snap):
+        snaps.append(w.clone())
+        gr = w + 0.0025 * torch.randn(N, generator=g, device=device, dtype=torch.float32)
+        if s < 2:
+            grads.append(gr)
+        w = w - lr * gr
+        lr *= 0.9
+    ema = grads[0].clone()
+    ema = 0.9 * grads[1] + (1.0 - 0.9) * ema
+    return snaps, ema
+
+
+def tensor_ptrs(base_ptr, layout):
+    ptrs, o = [], 0
+    for _, _, s in layout:
+        ptrs.append(base_ptr + 4 * o)
+        o += numel(s)
+    return ptrs
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    from paper_2306_11800_b200 import engine as E
+
+    stream = torch.cuda.current_stream(dev)
+    eng = E.Engine(local, stream.cuda_stream)
+    layout = gpt2_small_layout()
+    names = [n for n, _, _ in layout]
+    types = [t for _, t, _ in layout]
+    shapes = [s for _, _, s in layout]
+    N = sum(numel(s) for s in shapes)
+    cfg = E.Config()
+    n_snap = args.warmup + args.steps + 1
+
+    snaps, ema = gen_series(torch, layout, n_snap, 1234 + rank, dev)
+    torch.cuda.synchronize()
+    ckpts = []
+    for s in snaps:
+        c = E.DevCheckpoint(eng, names, types, shapes)
+        c.set_weights(tensor_ptrs(s.data_ptr(), layout))
+        c.set_ema(tensor_ptrs(ema.data_ptr(), layout))
+        ckpts.append(c)
+    host_snaps = [s.cpu().numpy() for s in snaps[:3]]
+    del snaps
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # FULL record for snapshot 0, then a chain of DELTA records
+    state = eng.quantize(ckpts[0], cfg, 1, 0)
+    rec_bytes = []
+
+    def step(i, prev):
+        st, r = eng.compress_step(ckpts[i], cfg, 1, i, prev)
+        rec_bytes.append(E.LIB.dqtg_record_size(r))
+        E.LIB.dqtg_record_destroy(r)
+        return st
+
+    for i in range(1, args.warmup + 1):
+        state = step(i, state)
+    barrier()
+    launches0 = eng.launches
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        t0.record(stream)
+        for i in range(args.warmup + 1, args.warmup + 1 + args.steps):
+            state = step(i, state)
+        t1.record(stream)
+        barrier()
+    ms = t0.elapsed_time(t1)
+    launches = eng.launches - launches0
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_step = ms / args.steps
+    value = 4.0 * N * world * args.steps / (ms / 1e3) / 1e9
+    rec_mean = float(np.mean(rec_bytes[-args.steps:]))
+    cr = 4.0 * N / rec_mean
+
+    # live per-kernel timing (CUDA events on the engine stream) for the roofline
+    eng.profile(True)
+    prof_steps = min(3, args.steps)
+    for i in range(prof_steps):
+        state = step(args.warmup + 1 + (i % args.steps), state)
+    eng.sync()
+    prof = eng.profile_report()
+    eng.profile(False)
+    peak, peak_kind = read_peak()
+    tot_ms = sum(v[1] for v in prof.values())
+    dom = max((k for k in prof if k in ALGO_BYTES), key=lambda k: prof[k][1])
+    n_l, dom_ms = prof[dom]
+    dom_avg_s = dom_ms / n_l / 1e3
+    achieved = ALGO_BYTES[dom] * N / dom_avg_s / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(dom)
+    except Exception:
+        pass
+    step_algo = (12.0 + 4.0 / cr) * N  # SURVEY.md §8d, sensitivity present
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                "kernel_share_of_step": dom_ms / tot_ms if tot_ms else None,
+                "step_algorithmic_gbs": step_algo / (ms_step / 1e3) / 1e9,
+                "step_frac": step_algo / (ms_step / 1e3) / 1e9 / peak,
+                "kernels_ms_per_step": {k: round(v[1] / prof_steps, 4) for k, v in
+                                        sorted(prof.items(), key=lambda kv: -kv[1][1])}}
+
+    # e2e through the C ABI with host buffers (pinned), record read back each step
+    pinned = [torch.from_numpy(h).pin_memory() for h in host_snaps]
+    e2e_ck = E.DevCheckpoint(eng, names, types, shapes)
+    e2e_ck.set_ema(tensor_ptrs(ema.data_ptr(), layout))
+    e2e_ck.set_weights(tensor_ptrs(pinned[0].data_ptr(), layout))
+    e2e_state = eng.quantize(e2e_ck, cfg, 1, 0)
+    rec_host = torch.empty(int(4 * N), dtype=torch.uint8).pin_memory()
+    e2e_steps = max(3, min(args.steps, 5))
+    h2d = d2h = 0
+
+    def e2e_step(i, prev):
+        nonlocal h2d, d2h
+        e2e_ck.set_weights(tensor_ptrs(pinned[i % len(pinned)].data_ptr(), layout))
+        st, r = eng.compress_step(e2e_ck, cfg, 1, i, prev)
+        n = E.LIB.dqtg_record_size(r)
+        E._check(E.LIB.dqtg_record_copy(r, rec_host.data_ptr()))
+        E.LIB.dqtg_record_destroy(r)
+        h2d += 4 * N
+        d2h += n
+        return st
+
+    e2e_state = e2e_step(1, e2e_state)
+    barrier()
+    h2d = d2h = 0
+    te = time.perf_counter()
+    for i in range(2, 2 + e2e_steps):
+        e2e_state = e2e_step(i, e2e_state)
+    barrier()
+    e2e_s = time.perf_counter() - te
+    if world > 1:
+        tt = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e = {"value": 4.0 * N * world * e2e_steps / e2e_s / 1e9, "unit": "GB/s",
+           "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
+           "path": "dqtg_ckpt_set_weights(pinned host) + dqtg_compress_step + dqtg_record_copy"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        stepf, Ns, _ = reference_step_timer()
+        stepf()
+        ts = []
+        t_end = time.perf_counter() + args.cpu_seconds
+        while time.perf_counter() < t_end or len(ts) < 2:
+            ts.append(stepf())
+        v = 4.0 * Ns * len(ts) / sum(ts) / 1e9
+        cpu = {"value": v, "unit": "GB/s", "cores": 1, "kind": "reference",
+               "sample": f"{Ns} params (GPT-2 small blocks 0-1 + ln_f), {len(ts)} steps of "
+                         f"compute_scores+quantize_checkpoint+encode_delta_record, oracle/_ref"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (GPU trajectory with the reference generator dynamics)",
+            "config": {"workload": "C2: GPT-2-small layout 124.4M fp32 params, delta chain",
+                       "params_per_gpu": N, "quant_config": "default (bins16/embed32/"
+                       "protect0.005/MAGNITUDE/sigma0.2/alpha0.01), EMA sensitivity",
+                       "parallelism": f"weak x{world} (independent shards)" if world > 1 else "1 GPU",
+                       "l2": "inputs (1 GB/step) larger than L2; no flush",
+                       "record_bytes": rec_mean, "compression_ratio": cr},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -5,7 +5,7 @@
  * (streams are passed as an opaque void*).  Every entry point replaces one
  * function (or one loop) of the reference library `dqt`
  * (/root/reference/proj); the replaced interface is cited next to each
- * declaration.  The C++ drop-in library (include/dqt/*.hpp, libdqt.so) and the
+ * declaration.  The C++ drop-in library (include/dqt/ headers, libdqt.so) and the
  * Python module (dqt._dqt) are thin hosts over this ABI; INTEGRATION.md shows
  * the binding a maintainer adds to the reference to call it directly.
  *
@@ -60,6 +60,10 @@ void dqtg_engine_destroy(dqtg_engine *e);
 dqtg_status dqtg_engine_sync(dqtg_engine *e);
 /* number of engine kernels launched so far (bench `gpu_launches`) */
 uint64_t dqtg_engine_launches(const dqtg_engine *e);
+/* per-kernel CUDA-event timing on the engine stream: enable, then read a JSON
+ * object {"kernel": [launches, total_ms], ...} (resets the accumulated spans). */
+dqtg_status dqtg_engine_profile(dqtg_engine *e, int enable);
+dqtg_status dqtg_engine_profile_report(dqtg_engine *e, char *json, uint64_t cap);
 
 /* dqt::QuantConfig (quantize.hpp:13-26) */
 typedef struct dqtg_config {
@@ -165,6 +169,20 @@ dqtg_status dqtg_compress_step(dqtg_engine *e, const dqtg_ckpt *c, const dqtg_co
                                uint64_t seed, uint64_t step, const dqtg_qstate *base,
                                double quality_delta, dqtg_qstate **state_out,
                                dqtg_record **record_out);
+
+/* partition_params (quantize.cpp:34-92): per-element part codes, 0 quantize,
+ * 1 prune, 2 protect, written to masks[i] (numel_i bytes each) */
+dqtg_status dqtg_partition(dqtg_engine *e, const dqtg_ckpt *c, const dqtg_config *cfg,
+                           uint8_t *const *masks);
+/* proxy_quality_delta(original, reconstructed) (search.cpp:30-61); per-layer-type
+ * sums are reduced in a fixed parallel order (tolerance, not bit parity: §7 H9) */
+dqtg_status dqtg_proxy_quality(dqtg_engine *e, const dqtg_layout *layout,
+                               const float *const *orig_any, const float *const *recon_any,
+                               double *quality);
+/* per-tensor level histograms of a state, counts[i * stride + level] — the exact
+ * integer input of estimate_compression (search.cpp:63-85) */
+dqtg_status dqtg_level_counts(dqtg_engine *e, const dqtg_qstate *q, uint32_t stride,
+                              uint64_t *counts);
 
 /* ---- batched candidate evaluation: ProxyEvaluator::evaluate over m configs
  * (search.cpp:107-112) as EvalCache::prefetch batches them (search.cpp:174-204) */

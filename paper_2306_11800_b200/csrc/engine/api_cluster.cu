@@ -36,7 +36,7 @@ void approx_kmeans(Engine& e, const float* values_any, uint64_t n, uint32_t k, d
     auto* gh = (unsigned long long*)e.buf("ak.gh", T.HS * 8);
     DQTG_CUDA(cudaMemsetAsync(gh, 0, T.HS * 8, e.stream));
     int grid = (int)std::min<uint64_t>((uint64_t)e.num_sms * 4, (n + 4095) / 4096);
-    value_sketch_kernel<<<grid, 256, kWinSlots * 4, e.stream>>>(x, n, e.bucket_tab(T), gh, e.d_err);
+    { DQTG_SPAN(e, "value_sketch_kernel"); value_sketch_kernel<<<grid, 256, kWinSlots * 4, e.stream>>>(x, n, e.bucket_tab(T), gh, e.d_err); }
     e.launched();
     auto* pts = (double*)e.buf("ak.pts", T.HS * 8);
     auto* kw = (double*)e.buf("ak.kw", T.HS * 8);
@@ -66,11 +66,6 @@ void approx_kmeans(Engine& e, const float* values_any, uint64_t n, uint32_t k, d
     e.sync();
     if (*len) e.from_device(cb, d_cb, (size_t)*len * 4);
     e.check_err();
-}
-
-void eval_batch(Engine&, const DevCkpt&, const dqtg_config*, const uint64_t*, uint32_t, double*,
-                double*) {
-    throw Fail(DQTG_ERROR, "eval_batch: not implemented yet");
 }
 
 std::unique_ptr<QState> decode_record(Engine&, const uint8_t*, uint64_t, const QState*) {

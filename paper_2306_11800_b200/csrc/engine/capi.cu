@@ -1,5 +1,7 @@
 // extern "C" surface of libdqtg.so (include/dqtg.h).  Every entry point catches
 // internal failures and turns them into a dqtg_status + thread-local message.
+#include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <string>
 
@@ -88,6 +90,45 @@ dqtg_status dqtg_engine_sync(dqtg_engine* h) {
 }
 
 uint64_t dqtg_engine_launches(const dqtg_engine* h) { return h->e.launches; }
+
+dqtg_status dqtg_engine_profile(dqtg_engine* h, int enable) {
+    return guard([&] {
+        LOCK(&h->e);
+        h->e.profiling = enable != 0;
+    });
+}
+
+dqtg_status dqtg_engine_profile_report(dqtg_engine* h, char* json, uint64_t cap) {
+    return guard([&] {
+        LOCK(&h->e);
+        Engine& e = h->e;
+        e.sync();
+        std::vector<std::pair<std::string, std::pair<uint64_t, double>>> acc;
+        for (auto& s : e.spans) {
+            float ms = 0.0f;
+            DQTG_CUDA(cudaEventElapsedTime(&ms, s.a, s.b));
+            auto it = std::find_if(acc.begin(), acc.end(),
+                                   [&](const auto& kv) { return kv.first == s.name; });
+            if (it == acc.end()) acc.push_back({s.name, {1, ms}});
+            else {
+                it->second.first++;
+                it->second.second += ms;
+            }
+        }
+        std::string out = "{";
+        for (size_t i = 0; i < acc.size(); ++i) {
+            char b[256];
+            snprintf(b, sizeof(b), "%s\"%s\": [%llu, %.6f]", i ? ", " : "", acc[i].first.c_str(),
+                     (unsigned long long)acc[i].second.first, acc[i].second.second);
+            out += b;
+        }
+        out += "}";
+        e.spans.clear();
+        e.ev_used = 0;
+        DQTG_REQUIRE(out.size() + 1 <= cap, DQTG_ERROR, "profile buffer too small");
+        memcpy(json, out.c_str(), out.size() + 1);
+    });
+}
 
 dqtg_status dqtg_sketch_range(double alpha, int64_t* kmin, int64_t* kmax) {
     return guard([&] {
@@ -436,6 +477,42 @@ dqtg_status dqtg_compress_step(dqtg_engine* h, const dqtg_ckpt* c, const dqtg_co
         rr->r = std::move(r);
         *state_out = s;
         *record_out = rr;
+    });
+}
+
+dqtg_status dqtg_partition(dqtg_engine* h, const dqtg_ckpt* c, const dqtg_config* cfg,
+                           uint8_t* const* masks) {
+    return guard([&] {
+        LOCK(&h->e);
+        ::dqtg::partition(h->e, c->c, *cfg, masks);
+    });
+}
+
+dqtg_status dqtg_proxy_quality(dqtg_engine* h, const dqtg_layout* layout,
+                               const float* const* orig, const float* const* recon,
+                               double* out) {
+    return guard([&] {
+        LOCK(&h->e);
+        Engine& e = h->e;
+        DevCkpt c;
+        c.eng = &e;
+        c.L = make_layout(&e, layout);
+        DQTG_CUDA(cudaMalloc(&c.w, c.L->Np * 4));
+        float* r = (float*)e.buf("pq.recon", c.L->Np * 4);
+        for (uint32_t i = 0; i < c.L->nt; ++i)
+            if (c.L->numel[i]) {
+                e.to_device(c.w + c.L->off[i], orig[i], c.L->numel[i] * 4);
+                e.to_device(r + c.L->off[i], recon[i], c.L->numel[i] * 4);
+            }
+        *out = ::dqtg::proxy_quality(e, c, r);
+    });
+}
+
+dqtg_status dqtg_level_counts(dqtg_engine* h, const dqtg_qstate* q, uint32_t stride,
+                              uint64_t* counts) {
+    return guard([&] {
+        LOCK(&h->e);
+        ::dqtg::level_counts(h->e, *q->q, counts, (int)stride);
     });
 }
 

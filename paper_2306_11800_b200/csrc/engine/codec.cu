@@ -1107,14 +1107,14 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
     if (base) {
         DQTG_CUDA(cudaFuncSetAttribute(enc_tile_kernel<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e1_smem));
-        enc_tile_kernel<true><<<ntiles, kCB, e1_smem, st>>>(A);
+        { DQTG_SPAN(e, "enc_tile_kernel"); enc_tile_kernel<true><<<ntiles, kCB, e1_smem, st>>>(A); }
     } else {
         DQTG_CUDA(cudaFuncSetAttribute(enc_tile_kernel<false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e1_smem));
-        enc_tile_kernel<false><<<ntiles, kCB, e1_smem, st>>>(A);
+        { DQTG_SPAN(e, "enc_tile_kernel"); enc_tile_kernel<false><<<ntiles, kCB, e1_smem, st>>>(A); }
     }
     // S
-    enc_resolve_kernel<<<nt * B, kCB, NS * 4, st>>>(A);
+    { DQTG_SPAN(e, "enc_resolve_kernel"); enc_resolve_kernel<<<nt * B, kCB, NS * 4, st>>>(A); }
     e.launched(2);
     DQTG_CUDA(cudaGetLastError());
     // group element counts from the segments (host-free): sum of seg.n per (t,b)
@@ -1137,8 +1137,8 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
         void* tmp = e.buf("e.cubtmp", tb + 16);
         DQTG_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, A.ov, ov_sorted, (int64_t)n_ov, 0, 64, st));
         auto* uhead = (unsigned long long*)e.buf("e.uhead", n_ov * 8 + 8);
-        ov_unique_kernel<<<1, 1024, 0, st>>>(ov_sorted, n_ov, ukey, uhead, nu);
-        ov_counts_kernel<<<64, 256, 0, st>>>(uhead, nu, n_ov, ucnt);
+        { DQTG_SPAN(e, "ov_unique_kernel"); ov_unique_kernel<<<1, 1024, 0, st>>>(ov_sorted, n_ov, ukey, uhead, nu); }
+        { DQTG_SPAN(e, "ov_counts_kernel"); ov_counts_kernel<<<64, 256, 0, st>>>(uhead, nu, n_ov, ucnt); }
         e.launched(2);
     } else {
         DQTG_CUDA(cudaMemsetAsync(nu, 0, 8, st));
@@ -1159,7 +1159,7 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
         auto* max_nov = (uint32_t*)(small + 4);
         DQTG_CUDA(cudaMemsetAsync(max_nov, 0, 4, st));
         if (n_unique) {
-            ov_group_max_kernel<<<64, 256, 0, st>>>(ukey, nu, nt * B, max_nov);
+            { DQTG_SPAN(e, "ov_group_max_kernel"); ov_group_max_kernel<<<64, 256, 0, st>>>(ukey, nu, nt * B, max_nov); }
             e.launched();
         }
         uint32_t h_max = 0;
@@ -1182,14 +1182,14 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
         if (hsm > 48 * 1024)
             DQTG_CUDA(cudaFuncSetAttribute(enc_huffman_kernel,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
-        enc_huffman_kernel<<<nt * B, 128, hsm, st>>>(A, elems, ukey, ucnt, nu, gi, tab_sym, tab_len,
-                                                     code_dense, len_dense, code_ov, len_ov, W, np2);
+        { DQTG_SPAN(e, "enc_huffman_kernel"); enc_huffman_kernel<<<nt * B, 128, hsm, st>>>(A, elems, ukey, ucnt, nu, gi, tab_sym, tab_len,
+                                                     code_dense, len_dense, code_ov, len_ov, W, np2); }
         e.launched();
     }
     CodeTabs C{code_dense, len_dense, ukey, code_ov, len_ov, gi};
     auto* segbits = (unsigned long long*)e.buf("e.segbits", (size_t)ntiles * B * 8);
-    enc_bits_kernel<<<ntiles, kCB, 0, st>>>(A, C, segbits);
-    enc_bitscan_kernel<<<nt * B, kCB, 0, st>>>(A, segbits, gi);
+    { DQTG_SPAN(e, "enc_bits_kernel"); enc_bits_kernel<<<ntiles, kCB, 0, st>>>(A, C, segbits); }
+    { DQTG_SPAN(e, "enc_bitscan_kernel"); enc_bitscan_kernel<<<nt * B, kCB, 0, st>>>(A, segbits, gi); }
     e.launched(2);
 
     // protected entry sizes + layout
@@ -1199,16 +1199,16 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
     auto* tr = (TensorRec*)e.buf("e.tr", nt * sizeof(TensorRec));
     DQTG_CUDA(cudaMemcpyAsync(tr, trh.data(), nt * sizeof(TensorRec), cudaMemcpyHostToDevice, st));
     DQTG_CUDA(cudaMemsetAsync(psz, 0, (np + 1) * 8, st));
-    if (np) prot_sizes_kernel<<<nt, 256, 0, st>>>(tr, target.d_ppos, psz);
+    if (np) { DQTG_SPAN(e, "prot_sizes_kernel"); prot_sizes_kernel<<<nt, 256, 0, st>>>(tr, target.d_ppos, psz); }
     {
         size_t tb = 0;
         DQTG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, psz, pscan, (int64_t)(np + 1), st));
         void* tmp = e.buf("e.cubtmp2", tb + 16);
         DQTG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, psz, pscan, (int64_t)(np + 1), st));
     }
-    tensor_size_kernel<<<nt, 32, 0, st>>>(A, tr, pscan, gi);
+    { DQTG_SPAN(e, "tensor_size_kernel"); tensor_size_kernel<<<nt, 32, 0, st>>>(A, tr, pscan, gi); }
     auto* total_d = (unsigned long long*)(small + 3);
-    tensor_scan_kernel<<<1, 1, 0, st>>>(tr, nt, prefix_len, total_d);
+    { DQTG_SPAN(e, "tensor_scan_kernel"); tensor_scan_kernel<<<1, 1, 0, st>>>(tr, nt, prefix_len, total_d); }
     e.launched(3);
     unsigned long long total = 0;
     DQTG_CUDA(cudaMemcpyAsync(&total, total_d, 8, cudaMemcpyDeviceToHost, st));
@@ -1222,10 +1222,10 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
     DQTG_CUDA(cudaMemcpyAsync(rec->d_buf, pre.data(), pre.size(), cudaMemcpyHostToDevice, st));
     auto* d_statics = (uint8_t*)e.buf("e.statics", statics.size() + 8);
     DQTG_CUDA(cudaMemcpyAsync(d_statics, statics.data(), statics.size(), cudaMemcpyHostToDevice, st));
-    write_tensor_kernel<<<nt, kCB, 0, st>>>(A, tr, d_statics, target.d_ppos, target.d_pval, pscan,
-                                            gi, tab_sym, tab_len, rec->d_buf);
-    enc_emit_kernel<<<ntiles, kCB, 0, st>>>(A, C, segbits, rec->d_buf);
-    finish_crc_kernel<<<1, 1, 0, st>>>(A.crc_acc, 2 * L.N, rec->d_buf + total - 4, nullptr);
+    { DQTG_SPAN(e, "write_tensor_kernel"); write_tensor_kernel<<<nt, kCB, 0, st>>>(A, tr, d_statics, target.d_ppos, target.d_pval, pscan,
+                                            gi, tab_sym, tab_len, rec->d_buf); }
+    { DQTG_SPAN(e, "enc_emit_kernel"); enc_emit_kernel<<<ntiles, kCB, 0, st>>>(A, C, segbits, rec->d_buf); }
+    { DQTG_SPAN(e, "finish_crc_kernel"); finish_crc_kernel<<<1, 1, 0, st>>>(A.crc_acc, 2 * L.N, rec->d_buf + total - 4, nullptr); }
     e.launched(3);
     DQTG_CUDA(cudaGetLastError());
     e.check_err();
@@ -1247,7 +1247,7 @@ __global__ void group_elems_kernel(const Seg* segs, const uint32_t* tile0, uint3
 
 void group_elems(Engine& e, const void* segs, const Layout& L, uint32_t B,
                  unsigned long long* elems) {
-    group_elems_kernel<<<L.nt * B, 256, 0, e.stream>>>((const Seg*)segs, L.d_tile0, B, elems);
+    { DQTG_SPAN(e, "group_elems_kernel"); group_elems_kernel<<<L.nt * B, 256, 0, e.stream>>>((const Seg*)segs, L.d_tile0, B, elems); }
     e.launched();
 }
 
@@ -1277,9 +1277,9 @@ uint32_t crc32_device(Engine& e, const uint8_t* data, uint64_t n) {
     auto* acc = (uint32_t*)e.buf("crc.acc", 16);
     auto* out = acc + 1;
     DQTG_CUDA(cudaMemsetAsync(acc, 0, 16, e.stream));
-    if (n) crc_bytes_kernel<<<std::min<unsigned long long>(4096, (n + 16383) / 16384), 256, 0,
-                              e.stream>>>(data, n, acc);
-    finish_crc_kernel<<<1, 1, 0, e.stream>>>(acc, n, nullptr, out);
+    if (n) { DQTG_SPAN(e, "crc_bytes_kernel"); crc_bytes_kernel<<<std::min<unsigned long long>(4096, (n + 16383) / 16384), 256, 0,
+                              e.stream>>>(data, n, acc); }
+    { DQTG_SPAN(e, "finish_crc_kernel"); finish_crc_kernel<<<1, 1, 0, e.stream>>>(acc, n, nullptr, out); }
     e.launched(2);
     uint32_t h = 0;
     DQTG_CUDA(cudaMemcpyAsync(&h, out, 4, cudaMemcpyDeviceToHost, e.stream));

@@ -19,8 +19,18 @@ bool is_device_ptr(const void* p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+cudaEvent_t Engine::take_event() {
+    if (ev_used == event_pool.size()) {
+        cudaEvent_t ev;
+        DQTG_CUDA(cudaEventCreate(&ev));
+        event_pool.push_back(ev);
+    }
+    return event_pool[ev_used++];
+}
+
 Engine::~Engine() {
     cudaSetDevice(device);
+    for (auto ev : event_pool) cudaEventDestroy(ev);
     for (auto& kv : scratch) cudaFree(kv.second.first);
     for (auto& kv : tables) {
         cudaFree(kv.second->d_U);

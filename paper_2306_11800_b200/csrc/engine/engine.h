@@ -125,6 +125,16 @@ struct Engine {
     void* pinned = nullptr;
     size_t pinned_cap = 0;
     int num_sms = 148;
+    // optional per-kernel CUDA-event timing (dqtg_engine_profile)
+    bool profiling = false;
+    struct Span {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Span> spans;
+    std::vector<cudaEvent_t> event_pool;
+    size_t ev_used = 0;
+    cudaEvent_t take_event();
 
     ~Engine();
     void activate() const { DQTG_CUDA(cudaSetDevice(device)); }
@@ -144,6 +154,23 @@ struct Engine {
 
 bool is_device_ptr(const void* p);
 
+// Scoped CUDA-event span around one kernel launch (only when profiling).
+struct KSpan {
+    Engine& e;
+    int idx = -1;
+    KSpan(Engine& eng, const char* name) : e(eng) {
+        if (!e.profiling) return;
+        Engine::Span s{name, e.take_event(), e.take_event()};
+        cudaEventRecord(s.a, e.stream);
+        idx = (int)e.spans.size();
+        e.spans.push_back(s);
+    }
+    ~KSpan() {
+        if (idx >= 0) cudaEventRecord(e.spans[idx].b, e.stream);
+    }
+};
+#define DQTG_SPAN(e, name) ::dqtg::KSpan dqtg_span_##__LINE__((e), (name))
+
 // ---- pipeline entry points implemented across the .cu files ---------------
 void sketch_build(Engine& e, const float* x_any, uint64_t n, double alpha, uint64_t* zero,
                   uint64_t* pos, uint64_t* neg);
@@ -154,6 +181,9 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
 std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
                                       const QState* base);
 void dequantize(Engine& e, const QState& q, float* out_dev_padded);
+void partition(Engine& e, const DevCkpt& c, const dqtg_config& cfg, uint8_t* const* masks);
+double proxy_quality(Engine& e, const DevCkpt& orig, const float* recon_dev_padded);
+void level_counts(Engine& e, const QState& q, uint64_t* counts, int lstride);
 void eval_batch(Engine& e, const DevCkpt& c, const dqtg_config* cfgs, const uint64_t* seeds,
                 uint32_t m, double* quality, double* est);
 void approx_kmeans(Engine& e, const float* values_any, uint64_t n, uint32_t k, double sigma,

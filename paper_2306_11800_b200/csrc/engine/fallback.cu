@@ -165,15 +165,15 @@ static void codebook_from_values(Engine& e, float* vals, uint64_t m, uint32_t k,
     cudaStream_t st = e.stream;
     auto* flags = (uint32_t*)e.buf("fb.flags", 8);
     DQTG_CUDA(cudaMemsetAsync(flags, 0, 8, st));
-    zero_signs_kernel<<<(unsigned)std::min<uint64_t>(1024, (m + 255) / 256 + 1), 256, 0, st>>>(
-        vals, m, flags);
+    { DQTG_SPAN(e, "zero_signs_kernel"); zero_signs_kernel<<<(unsigned)std::min<uint64_t>(1024, (m + 255) / 256 + 1), 256, 0, st>>>(
+        vals, m, flags); }
     uint32_t hf = 0;
     DQTG_CUDA(cudaMemcpyAsync(&hf, flags, 4, cudaMemcpyDeviceToHost, st));
     e.sync();
     if (hf == 3u) {  // both signed zeros present: sign of the zero key follows std::sort
         float* tmp = (float*)e.buf("fb.tmp", m * 4);
         DQTG_CUDA(cudaMemcpyAsync(tmp, vals, m * 4, cudaMemcpyDeviceToDevice, st));
-        first_zero_kernel<<<1, 1, 0, st>>>(tmp, m, flags + 1);
+        { DQTG_SPAN(e, "first_zero_kernel"); first_zero_kernel<<<1, 1, 0, st>>>(tmp, m, flags + 1); }
         e.launched();
     }
     float* sorted = (float*)e.buf("fb.sorted", m * 4);
@@ -185,20 +185,20 @@ static void codebook_from_values(Engine& e, float* vals, uint64_t m, uint32_t k,
     auto* heads = (unsigned long long*)e.buf("fb.heads", m * 8);
     auto* counts = (unsigned long long*)e.buf("fb.counts", m * 8);
     auto* nd_d = (unsigned long long*)e.buf("fb.nd", 8);
-    unique_kernel<<<1, 1024, 0, st>>>(sorted, m, flags, flags + 1, keys, heads, nd_d);
+    { DQTG_SPAN(e, "unique_kernel"); unique_kernel<<<1, 1024, 0, st>>>(sorted, m, flags, flags + 1, keys, heads, nd_d); }
     unsigned long long nd = 0;
     DQTG_CUDA(cudaMemcpyAsync(&nd, nd_d, 8, cudaMemcpyDeviceToHost, st));
     e.sync();
-    counts_from_heads_kernel<<<(unsigned)((nd + 255) / 256 + 1), 256, 0, st>>>(heads, nd, m,
-                                                                               counts);
+    { DQTG_SPAN(e, "counts_from_heads_kernel"); counts_from_heads_kernel<<<(unsigned)((nd + 255) / 256 + 1), 256, 0, st>>>(heads, nd, m,
+                                                                               counts); }
     e.launched(3);
     if (nd <= k) {  // quantize.cpp:294-297
-        write_distinct_cb_kernel<<<1, 1, 0, st>>>(keys, nd, cb, cb_len_dev);
+        { DQTG_SPAN(e, "write_distinct_cb_kernel"); write_distinct_cb_kernel<<<1, 1, 0, st>>>(keys, nd, cb, cb_len_dev); }
         e.launched();
         return;
     }
     auto* w = (double*)e.buf("fb.w", nd * 8);
-    mix_weights_kernel<<<1, 1024, 0, st>>>(keys, counts, nd, sigma, w);
+    { DQTG_SPAN(e, "mix_weights_kernel"); mix_weights_kernel<<<1, 1024, 0, st>>>(keys, counts, nd, sigma, w); }
     e.launched();
     // the k-means writes the codebook through slot 0 of a one-slot view
     std::vector<KProblem> probs(1);
@@ -219,14 +219,14 @@ void distinct_value_codebook(Engine& e, const PassIn& a, const LtParams* d_lp, i
     auto* tile_cnt = (uint32_t*)e.buf("fb.tcnt", (size_t)ntiles * 4 + 4);
     auto* tile_off = (unsigned long long*)e.buf("fb.toff", (size_t)(ntiles + 1) * 8);
     bool expl = a.mag != nullptr;
-    gather_q_kernel<<<ntiles, 256, 0, e.stream>>>(a, expl, d_lp, lt, 0, tile_cnt, tile_off,
-                                                  nullptr);
+    { DQTG_SPAN(e, "gather_q_kernel"); gather_q_kernel<<<ntiles, 256, 0, e.stream>>>(a, expl, d_lp, lt, 0, tile_cnt, tile_off,
+                                                  nullptr); }
     scan_tiles(e, tile_cnt, ntiles, tile_off);
     unsigned long long m = 0;
     DQTG_CUDA(cudaMemcpyAsync(&m, tile_off + ntiles, 8, cudaMemcpyDeviceToHost, e.stream));
     e.sync();
     float* vals = (float*)e.buf("fb.vals", m * 4 + 4);
-    gather_q_kernel<<<ntiles, 256, 0, e.stream>>>(a, expl, d_lp, lt, 1, tile_cnt, tile_off, vals);
+    { DQTG_SPAN(e, "gather_q_kernel"); gather_q_kernel<<<ntiles, 256, 0, e.stream>>>(a, expl, d_lp, lt, 1, tile_cnt, tile_off, vals); }
     e.launched(2);
     codebook_from_values(e, vals, m, k, cfg.sigma, seed, cb + (size_t)lt * cb_stride,
                          cb_len_dev + lt);
@@ -257,8 +257,8 @@ __global__ void count_protected_kernel(const Tile* tiles, const uint8_t* types,
 
 void count_protected(Engine& e, const Layout& L, const uint16_t* levels, const uint32_t* cb_len,
                      uint32_t* tile_prot) {
-    count_protected_kernel<<<(unsigned)L.tiles.size(), 256, 0, e.stream>>>(
-        L.d_tiles, L.d_types, levels, cb_len, tile_prot);
+    { DQTG_SPAN(e, "count_protected_kernel"); count_protected_kernel<<<(unsigned)L.tiles.size(), 256, 0, e.stream>>>(
+        L.d_tiles, L.d_types, levels, cb_len, tile_prot); }
     e.launched();
 }
 

@@ -400,10 +400,10 @@ void run_kmeans(Engine& e, std::vector<KProblem>& probs, float* cb_out, int cb_s
     if (smem > 48 * 1024)
         DQTG_CUDA(cudaFuncSetAttribute(kmeans_restarts_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kmeans_restarts_kernel<<<(unsigned)(probs.size() * restarts), kKB, smem, e.stream>>>(dp,
-                                                                                      restarts);
-    kmeans_select_kernel<<<(unsigned)probs.size(), 32, 0, e.stream>>>(dp, restarts, cb_out,
-                                                                       cb_stride, cb_len_dev);
+    { DQTG_SPAN(e, "kmeans_restarts_kernel"); kmeans_restarts_kernel<<<(unsigned)(probs.size() * restarts), kKB, smem, e.stream>>>(dp,
+                                                                                      restarts); }
+    { DQTG_SPAN(e, "kmeans_select_kernel"); kmeans_select_kernel<<<(unsigned)probs.size(), 32, 0, e.stream>>>(dp, restarts, cb_out,
+                                                                       cb_stride, cb_len_dev); }
     e.launched(2);
     DQTG_CUDA(cudaGetLastError());
 }
@@ -411,8 +411,8 @@ void run_kmeans(Engine& e, std::vector<KProblem>& probs, float* cb_out, int cb_s
 void compact_keys(Engine& e, const unsigned long long* hist, int64_t hs_stride, int64_t HS,
                   const double* key, double sigma, int nprob, double* pts,
                   unsigned long long* cnt, double* w, int64_t out_stride, int* n_keys) {
-    compact_keys_kernel<<<nprob, 1024, 0, e.stream>>>(hist, hs_stride, HS, key, sigma, pts, cnt,
-                                                      w, out_stride, n_keys);
+    { DQTG_SPAN(e, "compact_keys_kernel"); compact_keys_kernel<<<nprob, 1024, 0, e.stream>>>(hist, hs_stride, HS, key, sigma, pts, cnt,
+                                                      w, out_stride, n_keys); }
     e.launched();
     DQTG_CUDA(cudaGetLastError());
 }
@@ -511,8 +511,8 @@ void kmeanspp_host_api(Engine& e, const double* pts, const double* w, uint64_t n
                        uint64_t seed, double* centers) {
     DQTG_REQUIRE(k >= 1, DQTG_ERROR, "k must be >= 1");
     DevArrays d = stage(e, pts, w, n, k, nullptr);
-    kpp_api_kernel<<<1, kKB, (size_t)k * 8 + 16, e.stream>>>(d.pts, d.w, (int)n, (int)k, seed,
-                                                             d.scr, d.c, d.st);
+    { DQTG_SPAN(e, "kpp_api_kernel"); kpp_api_kernel<<<1, kKB, (size_t)k * 8 + 16, e.stream>>>(d.pts, d.w, (int)n, (int)k, seed,
+                                                             d.scr, d.c, d.st); }
     e.launched();
     int st = 0;
     DQTG_CUDA(cudaMemcpyAsync(&st, d.st, 4, cudaMemcpyDeviceToHost, e.stream));
@@ -532,8 +532,8 @@ void lloyd_host_api(Engine& e, const double* pts, const double* w, uint64_t n, d
     DQTG_REQUIRE(k >= 1, DQTG_ERROR, "no initial centers");
     DevArrays d = stage(e, pts, w, n, k, centers);
     int* it = d.st;
-    lloyd_api_kernel<<<1, kKB, (size_t)k * (2 * 8 + 3 * 4) + 16, e.stream>>>(
-        d.pts, d.w, (int)n, (int)k, tol, (int)max_iter, d.scr, d.c, it);
+    { DQTG_SPAN(e, "lloyd_api_kernel"); lloyd_api_kernel<<<1, kKB, (size_t)k * (2 * 8 + 3 * 4) + 16, e.stream>>>(
+        d.pts, d.w, (int)n, (int)k, tol, (int)max_iter, d.scr, d.c, it); }
     e.launched();
     int h = 0;
     DQTG_CUDA(cudaMemcpyAsync(&h, it, 4, cudaMemcpyDeviceToHost, e.stream));
@@ -545,7 +545,7 @@ void lloyd_host_api(Engine& e, const double* pts, const double* w, uint64_t n, d
 double sq_loss_host_api(Engine& e, const double* pts, const double* w, uint64_t n,
                         const double* centers, uint32_t k) {
     DevArrays d = stage(e, pts, w, n, k, centers);
-    loss_api_kernel<<<1, kKB, 0, e.stream>>>(d.pts, d.w, (int)n, d.c, (int)k, d.scr, d.scr + n + 1);
+    { DQTG_SPAN(e, "loss_api_kernel"); loss_api_kernel<<<1, kKB, 0, e.stream>>>(d.pts, d.w, (int)n, d.c, (int)k, d.scr, d.scr + n + 1); }
     e.launched();
     double h = 0;
     DQTG_CUDA(cudaMemcpyAsync(&h, d.scr + n + 1, 8, cudaMemcpyDeviceToHost, e.stream));

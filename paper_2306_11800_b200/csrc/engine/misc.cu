@@ -31,7 +31,7 @@ void sketch_build(Engine& e, const float* x_any, uint64_t n, double alpha, uint6
     DQTG_CUDA(cudaMemsetAsync(gh, 0, T.HS * 8, e.stream));
     if (n) {
         int grid = (int)std::min<uint64_t>((uint64_t)e.num_sms * 4, (n + 4095) / 4096);
-        sketch_kernel<<<grid, 256, kWinSlots * 4, e.stream>>>(x, n, e.bucket_tab(T), gh, e.d_err);
+        { DQTG_SPAN(e, "sketch_kernel"); sketch_kernel<<<grid, 256, kWinSlots * 4, e.stream>>>(x, n, e.bucket_tab(T), gh, e.d_err); }
         e.launched();
     }
     std::vector<unsigned long long> h(T.HS);
@@ -54,7 +54,7 @@ __global__ void ema_kernel(float* e, const float* g, uint64_t n, float b) {
 void ema_update(Engine& e, float* ema_dev, const float* g_dev, uint64_t n, float beta) {
     if (!n) return;
     int grid = (int)std::min<uint64_t>((uint64_t)e.num_sms * 8, (n + 255) / 256);
-    ema_kernel<<<grid, 256, 0, e.stream>>>(ema_dev, g_dev, n, beta);
+    { DQTG_SPAN(e, "ema_kernel"); ema_kernel<<<grid, 256, 0, e.stream>>>(ema_dev, g_dev, n, beta); }
     e.launched();
     DQTG_CUDA(cudaGetLastError());
 }
@@ -73,7 +73,7 @@ void compute_scores(Engine& e, const float* w, const float* ema, uint64_t n, flo
                     float* sens) {
     if (!n) return;
     int grid = (int)std::min<uint64_t>((uint64_t)e.num_sms * 8, (n + 255) / 256);
-    scores_kernel<<<grid, 256, 0, e.stream>>>(w, ema, n, mag, sens);
+    { DQTG_SPAN(e, "scores_kernel"); scores_kernel<<<grid, 256, 0, e.stream>>>(w, ema, n, mag, sens); }
     e.launched();
     DQTG_CUDA(cudaGetLastError());
 }
@@ -102,7 +102,7 @@ void delta_kernel_api(Engine& e, const uint16_t* prev, const uint16_t* x, uint64
     e.to_device(dp, prev, n * 2);
     e.to_device(dx, x, n * 2);
     int grid = (int)std::min<uint64_t>((uint64_t)e.num_sms * 8, (n + 255) / 256);
-    delta_kernel<<<grid, 256, 0, e.stream>>>(dp, dx, n, B, dout, apply, e.d_err);
+    { DQTG_SPAN(e, "delta_kernel"); delta_kernel<<<grid, 256, 0, e.stream>>>(dp, dx, n, B, dout, apply, e.d_err); }
     e.launched();
     e.from_device(out, dout, n * 2);
     e.check_err();

@@ -11,6 +11,8 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstring>
+#include <map>
 
 #include "engine.h"
 #include "hist.cuh"
@@ -298,7 +300,8 @@ __global__ void __launch_bounds__(kPB) pass_c_kernel(PassIn a, const LtParams* l
 __global__ void dequant_kernel(const Tile* tiles, const uint8_t* types, const uint64_t* tensor_off,
                                const float* cb, int cb_stride, const uint32_t* cb_len,
                                const uint16_t* levels, const unsigned long long* tile_prot_off,
-                               const uint16_t* pval, float* out, uint32_t* err) {
+                               const uint64_t* ppos, const uint16_t* pval, float* out,
+                               uint32_t* err) {
     __shared__ unsigned long long s_scan[33];
     const Tile T = tiles[blockIdx.x];
     const int lt = types[T.tensor];
@@ -314,7 +317,10 @@ __global__ void dequant_kernel(const Tile* tiles, const uint8_t* types, const ui
             float v;
             if (l < k) v = c[l];
             else if (l == k) v = 0.0f;
-            else if (l == k + 1) v = __uint_as_float((uint32_t)pval[o + ex] << 16);
+            else if (l == k + 1) {
+                if (ppos[o + ex] != (T.start - tensor_off[T.tensor]) + i) atomicOr(err, kErrCorruptIndex);
+                v = __uint_as_float((uint32_t)pval[o + ex] << 16);
+            }
             else {
                 atomicOr(err, kErrCorruptIndex);
                 v = 0.0f;
@@ -323,6 +329,141 @@ __global__ void dequant_kernel(const Tile* tiles, const uint8_t* types, const ui
         }
         o += tot;
     }
+}
+
+// ---- partition masks (quantize.cpp:34-92 as a stand-alone entry point) --------
+template <bool EXPL>
+__global__ void __launch_bounds__(kPB) mask_kernel(PassIn a, const LtParams* lp, uint8_t* out) {
+    const Tile T = a.tiles[blockIdx.x];
+    const int lt = a.types[T.tensor];
+    const LtParams P = lp[lt];
+    for (uint32_t i = threadIdx.x * 4; i < T.count; i += kPB * 4) {
+        const uint64_t idx = T.start + i;
+        float4 wv = ld4(a.w + idx);
+        float m[4], s[4];
+        load_scores<EXPL>(a, idx, wv, m, s);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (i + j < T.count) out[idx + j] = (uint8_t)classify(m[j], s[j], a.has_sens, a.metric, P);
+    }
+}
+
+// ---- candidate evaluation (ProxyEvaluator::evaluate, search.cpp:107-112) ------
+// Same partition + assignment as pass C, but instead of storing levels it
+// accumulates sum (w - dequant(w))^2 per tile (fixed reduction order) and the
+// per-tensor level histogram that estimate_compression needs.
+__device__ __forceinline__ double block_sum_d(double v, double* red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    __syncthreads();
+    return t;
+}
+
+template <bool EXPL>
+__global__ void __launch_bounds__(kPB) eval_c_kernel(PassIn a, const LtParams* lp, const float* cb,
+                                                     int cb_stride, const uint32_t* cb_len,
+                                                     double* tile_diff,
+                                                     unsigned long long* lvl_counts,
+                                                     int lstride) {
+    extern __shared__ float s_cb[];
+    __shared__ double s_red[kPB / 32];
+    __shared__ uint32_t s_cnt[66];
+    const int ti = blockIdx.x;
+    const Tile T = a.tiles[ti];
+    const int lt = a.types[T.tensor];
+    const uint32_t k = cb_len[lt];
+    for (uint32_t j = threadIdx.x; j < k; j += blockDim.x) s_cb[j] = cb[lt * cb_stride + j];
+    for (int j = threadIdx.x; j < 66; j += blockDim.x) s_cnt[j] = 0;
+    const LtParams P = lp[lt];
+    __syncthreads();
+    double acc = 0.0;
+    for (uint32_t i = threadIdx.x * 4; i < T.count; i += kPB * 4) {
+        const uint64_t idx = T.start + i;
+        float4 wv = ld4(a.w + idx);
+        float m[4], s[4];
+        load_scores<EXPL>(a, idx, wv, m, s);
+        const float wa[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (i + j >= T.count) break;
+            int part = classify(m[j], s[j], a.has_sens, a.metric, P);
+            uint32_t lv;
+            float deq;
+            if (part == 0) {
+                lv = nearest_center(s_cb, k, wa[j]);
+                deq = s_cb[lv];
+            } else if (part == 1) {
+                lv = k;
+                deq = 0.0f;
+            } else {
+                lv = k + 1;
+                deq = __uint_as_float((uint32_t)bf16_rne(wa[j]) << 16);
+            }
+            double d = __dsub_rn((double)wa[j], (double)deq);
+            acc = __dadd_rn(acc, __dmul_rn(d, d));
+            if (lv < 66) atomicAdd(&s_cnt[lv], 1u);
+        }
+    }
+    double t = block_sum_d(acc, s_red);
+    if (threadIdx.x == 0) tile_diff[ti] = t;
+    __syncthreads();
+    for (int j = threadIdx.x; j < (int)k + 2 && j < lstride; j += blockDim.x)
+        if (s_cnt[j]) atomicAdd(lvl_counts + (size_t)T.tensor * lstride + j, (unsigned long long)s_cnt[j]);
+}
+
+// sum of squares (or squared differences) per tile, fixed order
+__global__ void __launch_bounds__(kPB) tile_sq_kernel(const Tile* tiles, const float* x,
+                                                      const float* y, double* tile_out) {
+    __shared__ double s_red[kPB / 32];
+    const Tile T = tiles[blockIdx.x];
+    double acc = 0.0;
+    for (uint32_t i = threadIdx.x; i < T.count; i += kPB) {
+        double d = (double)x[T.start + i];
+        if (y) d = __dsub_rn(d, (double)y[T.start + i]);
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+    }
+    double t = block_sum_d(acc, s_red);
+    if (threadIdx.x == 0) tile_out[blockIdx.x] = t;
+}
+
+// per-layer-type totals over tiles, fixed order (contiguous chunks per thread)
+__global__ void __launch_bounds__(512) lt_sum_kernel(const Tile* tiles, const uint8_t* types,
+                                                      int ntiles, const double* tile_vals,
+                                                      double* out /*[7]*/) {
+    __shared__ double s_part[512][kLayerTypes];
+    double loc[kLayerTypes] = {0, 0, 0, 0, 0, 0, 0};
+    const int per = (ntiles + blockDim.x - 1) / blockDim.x;
+    const int a0 = threadIdx.x * per, a1 = min(ntiles, a0 + per);
+    for (int i = a0; i < a1; ++i) {
+        const int lt = types[tiles[i].tensor];
+        loc[lt] = __dadd_rn(loc[lt], tile_vals[i]);
+    }
+    for (int lt = 0; lt < kLayerTypes; ++lt) s_part[threadIdx.x][lt] = loc[lt];
+    __syncthreads();
+    if (threadIdx.x < kLayerTypes) {
+        double t = 0.0;
+        for (int j = 0; j < (int)blockDim.x; ++j) t = __dadd_rn(t, s_part[j][threadIdx.x]);
+        out[threadIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(256) level_count_kernel(const Tile* tiles, const uint16_t* levels,
+                                                          unsigned long long* counts, int lstride) {
+    __shared__ uint32_t s_cnt[1024];
+    const Tile T = tiles[blockIdx.x];
+    for (int j = threadIdx.x; j < lstride && j < 1024; j += blockDim.x) s_cnt[j] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < T.count; i += blockDim.x) {
+        uint32_t l = levels[T.start + i];
+        if ((int)l < lstride && l < 1024) atomicAdd(&s_cnt[l], 1u);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < lstride && j < 1024; j += blockDim.x)
+        if (s_cnt[j]) atomicAdd(counts + (size_t)T.tensor * lstride + j, (unsigned long long)s_cnt[j]);
 }
 
 // ---- host orchestration ---------------------------------------------------------
@@ -335,8 +476,8 @@ static PassIn pass_in(Engine& e, const DevCkpt& c, const AlphaTables& T, int met
     a.tensor_off = L.d_off;
     a.w = c.w;
     a.ema = c.ema;
-    a.mag = c.mag;
-    a.sens = c.sens;
+    a.mag = c.explicit_scores ? c.mag : nullptr;
+    a.sens = c.explicit_scores ? c.sens : nullptr;
     a.has_sens = c.has_sens;
     a.metric = metric;
     a.tab = e.bucket_tab(T);
@@ -395,25 +536,184 @@ void quantize_plan(const Layout& L, const dqtg_config& cfg, bool has_sens, Quant
     }
 }
 
+// Work area of one quantization (one config) on the engine.
+struct Stage {
+    std::string tag;
+    QuantPlan plan;
+    dqtg_config cfg{};
+    uint64_t seed = 0;
+    LtParams* d_lp = nullptr;
+    unsigned long long *gh_val = nullptr, *tile_off = nullptr, *tensor_prot = nullptr;
+    uint32_t* tile_prot = nullptr;
+    double *pts = nullptr, *kw = nullptr;
+    unsigned long long* kc = nullptr;
+    int* n_keys = nullptr;
+    int h_nkeys[kLayerTypes] = {0};
+    std::vector<unsigned long long> h_tprot;
+    float* d_cb = nullptr;  // [7][cb_stride]
+    uint32_t cb_stride = 1;
+    uint32_t* cb_len = nullptr;
+};
+
+static void stage_alloc(Engine& e, const Layout& L, int64_t HS, Stage& s, float* cb_dst) {
+    const int ntiles = (int)L.tiles.size();
+    const std::string& t = s.tag;
+    s.d_lp = (LtParams*)e.buf(t + "lp", sizeof(LtParams) * kLayerTypes);
+    s.gh_val = (unsigned long long*)e.buf(t + "gh_val", (size_t)kLayerTypes * HS * 8);
+    s.tile_prot = (uint32_t*)e.buf(t + "tile_prot", (size_t)ntiles * 4 + 4);
+    s.tile_off = (unsigned long long*)e.buf(t + "tile_off", (size_t)(ntiles + 1) * 8);
+    s.tensor_prot = (unsigned long long*)e.buf(t + "tensor_prot", (size_t)(L.nt + 1) * 8);
+    s.pts = (double*)e.buf(t + "pts", (size_t)kLayerTypes * HS * 8);
+    s.kw = (double*)e.buf(t + "kw", (size_t)kLayerTypes * HS * 8);
+    s.kc = (unsigned long long*)e.buf(t + "kc", (size_t)kLayerTypes * HS * 8);
+    s.n_keys = (int*)e.buf(t + "nkeys", kLayerTypes * 4);
+    s.cb_len = (uint32_t*)e.buf(t + "cblen", kLayerTypes * 4);
+    s.cb_stride = std::max(1u, std::max(s.cfg.bins, s.cfg.embed_bins));
+    s.d_cb = cb_dst ? cb_dst : (float*)e.buf(t + "cb", (size_t)kLayerTypes * s.cb_stride * 4);
+}
+
+// pass A into gh_mag/gh_sens ([7][HS] each) for the given masks
+static void stage_pass_a(Engine& e, const DevCkpt& c, const PassIn& a, uint32_t mask_mag,
+                         uint32_t mask_sens, unsigned long long* gh_mag,
+                         unsigned long long* gh_sens) {
+    const int ntiles = a.ntiles;
+    const size_t smem = (size_t)2 * kWinSlots * 4;
+    int grid = stream_grid(e, ntiles, 3);
+    cudaStream_t st = e.stream;
+    if (c.explicit_scores) {
+        DQTG_CUDA(cudaFuncSetAttribute(pass_a_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        { DQTG_SPAN(e, "pass_a_kernel"); pass_a_kernel<true><<<grid, kPB, smem, st>>>(a, gh_mag, gh_sens, mask_mag, mask_sens); }
+    } else {
+        DQTG_CUDA(cudaFuncSetAttribute(pass_a_kernel<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        { DQTG_SPAN(e, "pass_a_kernel"); pass_a_kernel<false><<<grid, kPB, smem, st>>>(a, gh_mag, gh_sens, mask_mag, mask_sens); }
+    }
+    e.launched();
+}
+
+static void stage_thresholds(Engine& e, Stage& s, int64_t HS, const AlphaTables& T,
+                             unsigned long long* gh_mag, unsigned long long* gh_sens) {
+    cudaStream_t st = e.stream;
+    DQTG_CUDA(cudaMemcpyAsync(s.d_lp, s.plan.lp, sizeof(s.plan.lp), cudaMemcpyHostToDevice, st));
+    if (s.plan.jobs.empty()) return;
+    for (auto& j : s.plan.jobs) {
+        bool sens_hist = (j.which == 1) || (j.which == 2 && s.cfg.metric == 1);
+        j.hist = (sens_hist ? gh_sens : gh_mag) + (size_t)j.lt * HS;
+    }
+    QJob* d_jobs = (QJob*)e.buf(s.tag + "jobs", sizeof(QJob) * s.plan.jobs.size());
+    DQTG_CUDA(cudaMemcpyAsync(d_jobs, s.plan.jobs.data(), sizeof(QJob) * s.plan.jobs.size(),
+                              cudaMemcpyHostToDevice, st));
+    { DQTG_SPAN(e, "quantile_kernel"); quantile_kernel<<<(unsigned)s.plan.jobs.size(), 1024, 0, st>>>(d_jobs, HS, T.d_keyf, s.d_lp); }
+    e.launched();
+}
+
+static void stage_pass_b(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s,
+                         const AlphaTables& T) {
+    const Layout& L = *c.L;
+    const int ntiles = a.ntiles;
+    const int64_t HS = T.HS;
+    cudaStream_t st = e.stream;
+    DQTG_CUDA(cudaMemsetAsync(s.gh_val, 0, (size_t)kLayerTypes * HS * 8, st));
+    DQTG_CUDA(cudaMemsetAsync(s.tensor_prot, 0, (size_t)(L.nt + 1) * 8, st));
+    const size_t smem = (size_t)kWinSlots * 4;
+    int grid = stream_grid(e, ntiles, 6);
+    if (c.explicit_scores)
+        { DQTG_SPAN(e, "pass_b_kernel"); pass_b_kernel<true><<<grid, kPB, smem, st>>>(a, s.d_lp, s.gh_val, s.tile_prot, s.tensor_prot); }
+    else
+        { DQTG_SPAN(e, "pass_b_kernel"); pass_b_kernel<false><<<grid, kPB, smem, st>>>(a, s.d_lp, s.gh_val, s.tile_prot, s.tensor_prot); }
+    { DQTG_SPAN(e, "scan_u32_kernel"); scan_u32_kernel<<<1, 1024, 0, st>>>(s.tile_prot, ntiles, s.tile_off); }
+    e.launched(2);
+    compact_keys(e, s.gh_val, HS, HS, T.d_key, s.cfg.sigma, kLayerTypes, s.pts, s.kc, s.kw, HS,
+                 s.n_keys);
+    s.h_tprot.resize(L.nt + 1);
+    DQTG_CUDA(cudaMemcpyAsync(s.h_nkeys, s.n_keys, sizeof(s.h_nkeys), cudaMemcpyDeviceToHost, st));
+    DQTG_CUDA(cudaMemcpyAsync(s.h_tprot.data(), s.tensor_prot, (L.nt + 1) * 8,
+                              cudaMemcpyDeviceToHost, st));
+}
+
+// After a sync: codebooks of every stage (all k-means problems in one launch).
+static void stage_codebooks(Engine& e, std::vector<Stage*>& stages, const PassIn& a,
+                            int64_t HS) {
+    std::vector<KProblem> probs;
+    std::vector<std::pair<Stage*, int>> slots;
+    for (Stage* s : stages) {
+        DQTG_CUDA(cudaMemsetAsync(s->cb_len, 0, kLayerTypes * 4, e.stream));
+        for (int lt = 0; lt < kLayerTypes; ++lt) {
+            if (s->h_nkeys[lt] == 0) continue;  // no QUANTIZE values: empty codebook
+            DQTG_REQUIRE(s->cfg.sigma >= 0.0 && s->cfg.sigma <= 1.0, DQTG_ERROR,
+                         "sigma must be in [0, 1]");
+            const uint32_t k = lt == kEmbedding ? s->cfg.embed_bins : s->cfg.bins;
+            const uint64_t seed = mix_seed(s->seed, (uint64_t)lt);  // quantize.cpp:393
+            if ((uint32_t)s->h_nkeys[lt] < k) {
+                PassIn aa = a;
+                aa.metric = (int)s->cfg.metric;
+                distinct_value_codebook(e, aa, s->d_lp, lt, k, s->cfg, seed, s->d_cb,
+                                        (int)s->cb_stride, s->cb_len);
+                continue;
+            }
+            KProblem p{};
+            p.pts = s->pts + (size_t)lt * HS;
+            p.w = s->kw + (size_t)lt * HS;
+            p.n = s->h_nkeys[lt];
+            p.k = (int)k;
+            p.seed = seed;
+            p.slot = (int)slots.size();
+            probs.push_back(p);
+            slots.push_back({s, lt});
+        }
+    }
+    if (probs.empty()) return;
+    // all problems write to a staging codebook array, then scatter to their stages
+    int stride = 1;
+    for (auto& p : probs) stride = std::max(stride, p.k);
+    float* cb_all = (float*)e.buf("km.cb_all", probs.size() * stride * 4);
+    uint32_t* len_all = (uint32_t*)e.buf("km.len_all", probs.size() * 4);
+    run_kmeans(e, probs, cb_all, stride, len_all);
+    for (size_t i = 0; i < slots.size(); ++i) {
+        Stage* s = slots[i].first;
+        int lt = slots[i].second;
+        DQTG_CUDA(cudaMemcpyAsync(s->d_cb + (size_t)lt * s->cb_stride, cb_all + i * stride,
+                                  (size_t)probs[i].k * 4, cudaMemcpyDeviceToDevice, e.stream));
+        DQTG_CUDA(cudaMemcpyAsync(s->cb_len + lt, len_all + i, 4, cudaMemcpyDeviceToDevice,
+                                  e.stream));
+    }
+}
+
+static void stage_pass_c(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s, QState& q) {
+    const int ntiles = a.ntiles;
+    cudaStream_t st = e.stream;
+    const size_t smem = (size_t)s.cb_stride * 4 + 16;
+    if (c.explicit_scores)
+        { DQTG_SPAN(e, "pass_c_kernel"); pass_c_kernel<true><<<ntiles, kPB, smem, st>>>(a, s.d_lp, s.d_cb, (int)s.cb_stride, s.cb_len, s.tile_off, q.d_levels, q.d_ppos, q.d_pval); }
+    else
+        { DQTG_SPAN(e, "pass_c_kernel"); pass_c_kernel<false><<<ntiles, kPB, smem, st>>>(a, s.d_lp, s.d_cb, (int)s.cb_stride, s.cb_len, s.tile_off, q.d_levels, q.d_ppos, q.d_pval); }
+    e.launched();
+    DQTG_CUDA(cudaGetLastError());
+}
+
 std::unique_ptr<QState> quantize(Engine& e, const DevCkpt& c, const dqtg_config& cfg,
                                  uint64_t seed, uint64_t step) {
     const Layout& L = *c.L;
-    QuantPlan plan;
-    quantize_plan(L, cfg, c.has_sens, plan);
+    Stage s;
+    s.tag = "q.";
+    s.cfg = cfg;
+    s.seed = seed;
+    quantize_plan(L, cfg, c.has_sens, s.plan);
     auto q = std::make_unique<QState>();
     q->eng = &e;
     q->L = c.L;
     q->step = step;
     q->cfg = cfg;
-    const uint32_t kmax_bins = std::max(cfg.bins, cfg.embed_bins);
-    q->cb_stride = kmax_bins;
+    q->cb_stride = std::max(1u, std::max(cfg.bins, cfg.embed_bins));
     DQTG_CUDA(cudaMalloc(&q->d_levels, L.Np * 2));
-    DQTG_CUDA(cudaMalloc(&q->d_cb, (size_t)kLayerTypes * kmax_bins * 4));
+    DQTG_CUDA(cudaMalloc(&q->d_cb, (size_t)kLayerTypes * q->cb_stride * 4));
     q->prot_count.assign(L.nt, 0);
     q->prot_off.assign(L.nt + 1, 0);
-    const int ntiles = (int)L.tiles.size();
     if (L.N == 0) {
         DQTG_CUDA(cudaMemsetAsync(q->d_levels, 0, L.Np * 2, e.stream));
+        DQTG_CUDA(cudaMalloc(&q->d_ppos, 8));
+        DQTG_CUDA(cudaMalloc(&q->d_pval, 8));
         return q;
     }
     DQTG_REQUIRE(cfg.alpha > 0.0 && cfg.alpha < 1.0, DQTG_ALPHA_OUT_OF_RANGE,
@@ -421,126 +721,34 @@ std::unique_ptr<QState> quantize(Engine& e, const DevCkpt& c, const dqtg_config&
     AlphaTables& T = e.alpha_tables(cfg.alpha);
     const int64_t HS = T.HS;
     PassIn a = pass_in(e, c, T, (int)cfg.metric);
-    cudaStream_t st = e.stream;
-
-    // device parameters
-    LtParams* d_lp = (LtParams*)e.buf("q.lp", sizeof(LtParams) * kLayerTypes);
-    DQTG_CUDA(cudaMemcpyAsync(d_lp, plan.lp, sizeof(plan.lp), cudaMemcpyHostToDevice, st));
-
-    // pass A + thresholds
-    if (!plan.jobs.empty()) {
+    stage_alloc(e, L, HS, s, q->d_cb);
+    unsigned long long *gh_mag = nullptr, *gh_sens = nullptr;
+    if (!s.plan.jobs.empty()) {
         auto* gh = (unsigned long long*)e.buf("q.gh_scores", (size_t)2 * kLayerTypes * HS * 8);
-        DQTG_CUDA(cudaMemsetAsync(gh, 0, (size_t)2 * kLayerTypes * HS * 8, st));
-        unsigned long long* gh_mag = gh;
-        unsigned long long* gh_sens = gh + (size_t)kLayerTypes * HS;
-        const size_t smem = (size_t)2 * kWinSlots * 4;
-        int grid = stream_grid(e, ntiles, 3);
-        if (c.explicit_scores) {
-            DQTG_CUDA(cudaFuncSetAttribute(pass_a_kernel<true>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            pass_a_kernel<true><<<grid, kPB, smem, st>>>(a, gh_mag, gh_sens, plan.mask_mag,
-                                                         plan.mask_sens);
-        } else {
-            DQTG_CUDA(cudaFuncSetAttribute(pass_a_kernel<false>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            pass_a_kernel<false><<<grid, kPB, smem, st>>>(a, gh_mag, gh_sens, plan.mask_mag,
-                                                          plan.mask_sens);
-        }
-        for (auto& j : plan.jobs) {
-            bool sens_hist = (j.which == 1) || (j.which == 2 && cfg.metric == 1);
-            j.hist = (sens_hist ? gh_sens : gh_mag) + (size_t)j.lt * HS;
-        }
-        QJob* d_jobs = (QJob*)e.buf("q.jobs", sizeof(QJob) * plan.jobs.size());
-        DQTG_CUDA(cudaMemcpyAsync(d_jobs, plan.jobs.data(), sizeof(QJob) * plan.jobs.size(),
-                                  cudaMemcpyHostToDevice, st));
-        quantile_kernel<<<(unsigned)plan.jobs.size(), 1024, 0, st>>>(d_jobs, HS, T.d_keyf, d_lp);
-        e.launched(2);
+        DQTG_CUDA(cudaMemsetAsync(gh, 0, (size_t)2 * kLayerTypes * HS * 8, e.stream));
+        gh_mag = gh;
+        gh_sens = gh + (size_t)kLayerTypes * HS;
+        stage_pass_a(e, c, a, s.plan.mask_mag, s.plan.mask_sens, gh_mag, gh_sens);
     }
-
-    // pass B
-    auto* gh_val = (unsigned long long*)e.buf("q.gh_val", (size_t)kLayerTypes * HS * 8);
-    auto* tile_prot = (uint32_t*)e.buf("q.tile_prot", (size_t)ntiles * 4 + 4);
-    auto* tile_off = (unsigned long long*)e.buf("q.tile_off", (size_t)(ntiles + 1) * 8);
-    auto* tensor_prot = (unsigned long long*)e.buf("q.tensor_prot", (size_t)(L.nt + 1) * 8);
-    DQTG_CUDA(cudaMemsetAsync(gh_val, 0, (size_t)kLayerTypes * HS * 8, st));
-    DQTG_CUDA(cudaMemsetAsync(tensor_prot, 0, (size_t)(L.nt + 1) * 8, st));
-    {
-        const size_t smem = (size_t)kWinSlots * 4;
-        int grid = stream_grid(e, ntiles, 6);
-        if (c.explicit_scores)
-            pass_b_kernel<true><<<grid, kPB, smem, st>>>(a, d_lp, gh_val, tile_prot, tensor_prot);
-        else
-            pass_b_kernel<false><<<grid, kPB, smem, st>>>(a, d_lp, gh_val, tile_prot, tensor_prot);
-        scan_u32_kernel<<<1, 1024, 0, st>>>(tile_prot, ntiles, tile_off);
-        e.launched(2);
-    }
-
-    // keys + weights per layer type
-    auto* pts = (double*)e.buf("q.pts", (size_t)kLayerTypes * HS * 8);
-    auto* kw = (double*)e.buf("q.kw", (size_t)kLayerTypes * HS * 8);
-    auto* kc = (unsigned long long*)e.buf("q.kc", (size_t)kLayerTypes * HS * 8);
-    auto* n_keys = (int*)e.buf("q.nkeys", kLayerTypes * 4);
-    compact_keys(e, gh_val, HS, HS, T.d_key, cfg.sigma, kLayerTypes, pts, kc, kw, HS, n_keys);
-
-    int h_nkeys[kLayerTypes];
-    std::vector<unsigned long long> h_tprot(L.nt + 1);
-    DQTG_CUDA(cudaMemcpyAsync(h_nkeys, n_keys, sizeof(h_nkeys), cudaMemcpyDeviceToHost, st));
-    DQTG_CUDA(cudaMemcpyAsync(h_tprot.data(), tensor_prot, (L.nt + 1) * 8,
-                              cudaMemcpyDeviceToHost, st));
-    e.check_err();  // syncs
-
-    auto* cb_len_d = (uint32_t*)e.buf("q.cblen", kLayerTypes * 4);
-    DQTG_CUDA(cudaMemsetAsync(cb_len_d, 0, kLayerTypes * 4, st));
-    std::vector<KProblem> probs;
-    for (int lt = 0; lt < kLayerTypes; ++lt) {
-        if (h_nkeys[lt] == 0) continue;  // no QUANTIZE values: empty codebook
-        DQTG_REQUIRE(cfg.sigma >= 0.0 && cfg.sigma <= 1.0, DQTG_ERROR, "sigma must be in [0, 1]");
-        const uint32_t k = lt == kEmbedding ? cfg.embed_bins : cfg.bins;
-        if ((uint32_t)h_nkeys[lt] < k) {
-            distinct_value_codebook(e, a, d_lp, lt, k, cfg, mix_seed(seed, (uint64_t)lt), q->d_cb,
-                                    (int)q->cb_stride, cb_len_d);
-            continue;
-        }
-        KProblem p{};
-        p.pts = pts + (size_t)lt * HS;
-        p.w = kw + (size_t)lt * HS;
-        p.n = h_nkeys[lt];
-        p.k = (int)k;
-        p.seed = mix_seed(seed, (uint64_t)lt);  // quantize.cpp:393
-        p.slot = lt;
-        probs.push_back(p);
-    }
-    run_kmeans(e, probs, q->d_cb, (int)q->cb_stride, cb_len_d);
-
-    // pass C
-    q->prot_total = h_tprot[0];
+    stage_thresholds(e, s, HS, T, gh_mag, gh_sens);
+    stage_pass_b(e, c, a, s, T);
+    e.check_err();  // syncs: n_keys + protected counts on the host
+    std::vector<Stage*> v{&s};
+    stage_codebooks(e, v, a, HS);
     uint64_t acc = 0;
     for (uint32_t i = 0; i < L.nt; ++i) {
         q->prot_off[i] = acc;
-        q->prot_count[i] = h_tprot[i];
-        acc += h_tprot[i];
+        q->prot_count[i] = s.h_tprot[i];
+        acc += s.h_tprot[i];
     }
     q->prot_off[L.nt] = acc;
     q->prot_total = acc;
     DQTG_CUDA(cudaMalloc(&q->d_ppos, (acc + 1) * 8));
     DQTG_CUDA(cudaMalloc(&q->d_pval, (acc + 1) * 2));
-    {
-        const size_t smem = (size_t)q->cb_stride * 4 + 16;
-        if (c.explicit_scores)
-            pass_c_kernel<true><<<ntiles, kPB, smem, st>>>(a, d_lp, q->d_cb, (int)q->cb_stride,
-                                                           cb_len_d, tile_off, q->d_levels,
-                                                           q->d_ppos, q->d_pval);
-        else
-            pass_c_kernel<false><<<ntiles, kPB, smem, st>>>(a, d_lp, q->d_cb, (int)q->cb_stride,
-                                                            cb_len_d, tile_off, q->d_levels,
-                                                            q->d_ppos, q->d_pval);
-        e.launched();
-        DQTG_CUDA(cudaGetLastError());
-    }
-    // codebooks to host
+    stage_pass_c(e, c, a, s, *q);
     std::vector<float> hcb((size_t)kLayerTypes * q->cb_stride);
-    DQTG_CUDA(cudaMemcpyAsync(q->cb_len, cb_len_d, sizeof(q->cb_len), cudaMemcpyDeviceToHost, st));
-    DQTG_CUDA(cudaMemcpyAsync(hcb.data(), q->d_cb, hcb.size() * 4, cudaMemcpyDeviceToHost, st));
+    DQTG_CUDA(cudaMemcpyAsync(q->cb_len, s.cb_len, sizeof(q->cb_len), cudaMemcpyDeviceToHost, e.stream));
+    DQTG_CUDA(cudaMemcpyAsync(hcb.data(), q->d_cb, hcb.size() * 4, cudaMemcpyDeviceToHost, e.stream));
     e.check_err();
     for (int lt = 0; lt < kLayerTypes; ++lt)
         q->cb[lt].assign(hcb.begin() + (size_t)lt * q->cb_stride,
@@ -548,27 +756,233 @@ std::unique_ptr<QState> quantize(Engine& e, const DevCkpt& c, const dqtg_config&
     return q;
 }
 
+void partition(Engine& e, const DevCkpt& c, const dqtg_config& cfg, uint8_t* const* masks) {
+    const Layout& L = *c.L;
+    Stage s;
+    s.tag = "p.";
+    s.cfg = cfg;
+    quantize_plan(L, cfg, c.has_sens, s.plan);
+    if (L.N == 0) return;
+    AlphaTables* T = nullptr;
+    if (!s.plan.jobs.empty()) T = &e.alpha_tables(cfg.alpha);
+    else T = &e.alpha_tables(cfg.alpha > 0.0 && cfg.alpha < 1.0 ? cfg.alpha : 0.01);
+    const int64_t HS = T->HS;
+    PassIn a = pass_in(e, c, *T, (int)cfg.metric);
+    s.d_lp = (LtParams*)e.buf("p.lp", sizeof(LtParams) * kLayerTypes);
+    unsigned long long *gh_mag = nullptr, *gh_sens = nullptr;
+    if (!s.plan.jobs.empty()) {
+        auto* gh = (unsigned long long*)e.buf("q.gh_scores", (size_t)2 * kLayerTypes * HS * 8);
+        DQTG_CUDA(cudaMemsetAsync(gh, 0, (size_t)2 * kLayerTypes * HS * 8, e.stream));
+        gh_mag = gh;
+        gh_sens = gh + (size_t)kLayerTypes * HS;
+        stage_pass_a(e, c, a, s.plan.mask_mag, s.plan.mask_sens, gh_mag, gh_sens);
+    }
+    stage_thresholds(e, s, HS, *T, gh_mag, gh_sens);
+    uint8_t* d_mask = (uint8_t*)e.buf("p.mask", L.Np + 16);
+    if (c.explicit_scores)
+        { DQTG_SPAN(e, "mask_kernel"); mask_kernel<true><<<a.ntiles, kPB, 0, e.stream>>>(a, s.d_lp, d_mask); }
+    else
+        { DQTG_SPAN(e, "mask_kernel"); mask_kernel<false><<<a.ntiles, kPB, 0, e.stream>>>(a, s.d_lp, d_mask); }
+    e.launched();
+    for (uint32_t i = 0; i < L.nt; ++i)
+        if (L.numel[i]) e.from_device(masks[i], d_mask + L.off[i], L.numel[i]);
+    e.check_err();
+}
+
+// proxy_quality_delta + estimate_compression from device partial sums (search.cpp:30-85)
+static double quality_from(const Layout& L, const double* diff, const double* orig) {
+    uint64_t count[kLayerTypes] = {0}, total = 0;
+    for (uint32_t i = 0; i < L.nt; ++i) count[L.types[i]] += L.numel[i];
+    for (int lt = 0; lt < kLayerTypes; ++lt) total += count[lt];
+    if (total == 0) return 0.0;
+    double q = 0.0;
+    for (int lt = 0; lt < kLayerTypes; ++lt) {
+        if (!count[lt]) continue;
+        double rel = orig[lt] > 0.0 ? std::sqrt(diff[lt] / orig[lt]) : (diff[lt] > 0.0 ? 1.0 : 0.0);
+        q += (double(count[lt]) / double(total)) * rel;
+    }
+    return q;
+}
+
+double estimate_from_counts(const Layout& L, const uint64_t* counts, int lstride,
+                            const uint32_t* cb_len, const uint64_t* nprot) {
+    double raw = 4.0 * double(L.N);
+    double est = 64.0;
+    for (uint32_t i = 0; i < L.nt; ++i) {
+        const uint32_t levels = cb_len[L.types[i]] + 2;
+        const double n = double(L.numel[i]);
+        double bits = 0.0;
+        for (uint32_t l = 0; l < levels && (int)l < lstride; ++l) {
+            uint64_t c = counts[(size_t)i * lstride + l];
+            if (!c) continue;
+            double p = double(c) / n;
+            bits -= double(c) * std::log2(p);
+        }
+        est += bits / 8.0;
+        est += 10.0 * double(nprot[i]);
+    }
+    for (int lt = 0; lt < kLayerTypes; ++lt) est += 4.0 * double(cb_len[lt]);
+    return raw / est;
+}
+
+void eval_batch(Engine& e, const DevCkpt& c, const dqtg_config* cfgs, const uint64_t* seeds,
+                uint32_t m, double* quality, double* est) {
+    const Layout& L = *c.L;
+    if (!m) return;
+    const int ntiles = (int)L.tiles.size();
+    // sum of squares of the original weights per layer type (config independent)
+    auto* tile_v = (double*)e.buf("ev.tile_v", (size_t)ntiles * 8 + 8);
+    auto* d_lt = (double*)e.buf("ev.lt", 16 * 8);
+    double orig[kLayerTypes] = {0}, diff[kLayerTypes];
+    if (ntiles) {
+        { DQTG_SPAN(e, "tile_sq_kernel"); tile_sq_kernel<<<ntiles, kPB, 0, e.stream>>>(L.d_tiles, c.w, nullptr, tile_v); }
+        { DQTG_SPAN(e, "lt_sum_kernel"); lt_sum_kernel<<<1, 512, 0, e.stream>>>(L.d_tiles, L.d_types, ntiles, tile_v, d_lt); }
+        e.launched(2);
+        DQTG_CUDA(cudaMemcpyAsync(orig, d_lt, sizeof(orig), cudaMemcpyDeviceToHost, e.stream));
+    }
+    std::vector<std::unique_ptr<Stage>> stages(m);
+    std::map<uint64_t, std::pair<unsigned long long*, unsigned long long*>> scores_by_alpha;
+    int lstride = 2;
+    for (uint32_t i = 0; i < m; ++i) lstride = std::max<int>(lstride, std::max(cfgs[i].bins, cfgs[i].embed_bins) + 2);
+    DQTG_REQUIRE(lstride <= 66, DQTG_ERROR, "eval_batch supports up to 64 bins");
+    for (uint32_t i = 0; i < m; ++i) {
+        auto s = std::make_unique<Stage>();
+        s->tag = "ev" + std::to_string(i) + ".";
+        s->cfg = cfgs[i];
+        s->seed = seeds[i];
+        quantize_plan(L, cfgs[i], c.has_sens, s->plan);
+        stages[i] = std::move(s);
+    }
+    if (L.N == 0) {
+        for (uint32_t i = 0; i < m; ++i) quality[i] = 0.0, est[i] = 0.0;
+        return;
+    }
+    // pass A once per alpha, all layer types, both score kinds
+    for (uint32_t i = 0; i < m; ++i) {
+        Stage& s = *stages[i];
+        DQTG_REQUIRE(s.cfg.alpha > 0.0 && s.cfg.alpha < 1.0, DQTG_ALPHA_OUT_OF_RANGE,
+                     "alpha must be in (0, 1)");
+        AlphaTables& T = e.alpha_tables(s.cfg.alpha);
+        stage_alloc(e, L, T.HS, s, nullptr);
+        uint64_t key;
+        memcpy(&key, &s.cfg.alpha, 8);
+        auto it = scores_by_alpha.find(key);
+        if (it == scores_by_alpha.end()) {
+            auto* gh = (unsigned long long*)e.buf("ev.gh_scores" + std::to_string(scores_by_alpha.size()),
+                                                  (size_t)2 * kLayerTypes * T.HS * 8);
+            DQTG_CUDA(cudaMemsetAsync(gh, 0, (size_t)2 * kLayerTypes * T.HS * 8, e.stream));
+            PassIn a = pass_in(e, c, T, 0);
+            stage_pass_a(e, c, a, 0x7f, c.has_sens ? 0x7f : 0, gh, gh + (size_t)kLayerTypes * T.HS);
+            it = scores_by_alpha.emplace(key, std::make_pair(gh, gh + (size_t)kLayerTypes * T.HS)).first;
+        }
+        stage_thresholds(e, s, T.HS, T, it->second.first, it->second.second);
+        PassIn a = pass_in(e, c, T, (int)s.cfg.metric);
+        stage_pass_b(e, c, a, s, T);
+    }
+    e.check_err();
+    {
+        std::vector<Stage*> v;
+        for (auto& s : stages) v.push_back(s.get());
+        AlphaTables& T0 = e.alpha_tables(stages[0]->cfg.alpha);
+        PassIn a = pass_in(e, c, T0, 0);
+        // codebooks: problems of configs sharing an alpha go together
+        std::map<uint64_t, std::vector<Stage*>> by_alpha;
+        for (Stage* s : v) {
+            uint64_t key;
+            memcpy(&key, &s->cfg.alpha, 8);
+            by_alpha[key].push_back(s);
+        }
+        for (auto& kv : by_alpha) {
+            AlphaTables& T = e.alpha_tables(kv.second[0]->cfg.alpha);
+            PassIn aa = pass_in(e, c, T, 0);
+            stage_codebooks(e, kv.second, aa, T.HS);
+        }
+        (void)a;
+    }
+    auto* counts = (unsigned long long*)e.buf("ev.counts", (size_t)L.nt * lstride * 8 + 8);
+    std::vector<uint64_t> hcounts((size_t)L.nt * lstride);
+    for (uint32_t i = 0; i < m; ++i) {
+        Stage& s = *stages[i];
+        AlphaTables& T = e.alpha_tables(s.cfg.alpha);
+        PassIn a = pass_in(e, c, T, (int)s.cfg.metric);
+        DQTG_CUDA(cudaMemsetAsync(counts, 0, (size_t)L.nt * lstride * 8, e.stream));
+        const size_t smem = (size_t)s.cb_stride * 4 + 16;
+        if (c.explicit_scores)
+            { DQTG_SPAN(e, "eval_c_kernel"); eval_c_kernel<true><<<ntiles, kPB, smem, e.stream>>>(a, s.d_lp, s.d_cb, (int)s.cb_stride, s.cb_len, tile_v, counts, lstride); }
+        else
+            { DQTG_SPAN(e, "eval_c_kernel"); eval_c_kernel<false><<<ntiles, kPB, smem, e.stream>>>(a, s.d_lp, s.d_cb, (int)s.cb_stride, s.cb_len, tile_v, counts, lstride); }
+        { DQTG_SPAN(e, "lt_sum_kernel"); lt_sum_kernel<<<1, 512, 0, e.stream>>>(L.d_tiles, L.d_types, ntiles, tile_v, d_lt); }
+        e.launched(2);
+        uint32_t cbl[kLayerTypes];
+        DQTG_CUDA(cudaMemcpyAsync(diff, d_lt, sizeof(diff), cudaMemcpyDeviceToHost, e.stream));
+        DQTG_CUDA(cudaMemcpyAsync(cbl, s.cb_len, sizeof(cbl), cudaMemcpyDeviceToHost, e.stream));
+        DQTG_CUDA(cudaMemcpyAsync(hcounts.data(), counts, hcounts.size() * 8, cudaMemcpyDeviceToHost,
+                                  e.stream));
+        e.check_err();
+        quality[i] = quality_from(L, diff, orig);
+        std::vector<uint64_t> np(L.nt);
+        for (uint32_t t = 0; t < L.nt; ++t) np[t] = s.h_tprot[t];
+        est[i] = estimate_from_counts(L, hcounts.data(), lstride, cbl, np.data());
+    }
+}
+
+double proxy_quality(Engine& e, const DevCkpt& orig, const float* recon_dev) {
+    const Layout& L = *orig.L;
+    const int ntiles = (int)L.tiles.size();
+    double o[kLayerTypes] = {0}, d[kLayerTypes] = {0};
+    if (ntiles) {
+        auto* tile_v = (double*)e.buf("pq.tile_v", (size_t)ntiles * 8 + 8);
+        auto* d_lt = (double*)e.buf("pq.lt", 16 * 8);
+        { DQTG_SPAN(e, "tile_sq_kernel"); tile_sq_kernel<<<ntiles, kPB, 0, e.stream>>>(L.d_tiles, orig.w, nullptr, tile_v); }
+        { DQTG_SPAN(e, "lt_sum_kernel"); lt_sum_kernel<<<1, 512, 0, e.stream>>>(L.d_tiles, L.d_types, ntiles, tile_v, d_lt); }
+        DQTG_CUDA(cudaMemcpyAsync(o, d_lt, sizeof(o), cudaMemcpyDeviceToHost, e.stream));
+        e.sync();
+        { DQTG_SPAN(e, "tile_sq_kernel"); tile_sq_kernel<<<ntiles, kPB, 0, e.stream>>>(L.d_tiles, orig.w, recon_dev, tile_v); }
+        { DQTG_SPAN(e, "lt_sum_kernel"); lt_sum_kernel<<<1, 512, 0, e.stream>>>(L.d_tiles, L.d_types, ntiles, tile_v, d_lt); }
+        DQTG_CUDA(cudaMemcpyAsync(d, d_lt, sizeof(d), cudaMemcpyDeviceToHost, e.stream));
+        e.launched(4);
+        e.sync();
+    }
+    return quality_from(L, d, o);
+}
+
+void level_counts(Engine& e, const QState& q, uint64_t* counts, int lstride) {
+    const Layout& L = *q.L;
+    auto* d = (unsigned long long*)e.buf("lc.counts", (size_t)L.nt * lstride * 8 + 8);
+    DQTG_CUDA(cudaMemsetAsync(d, 0, (size_t)L.nt * lstride * 8, e.stream));
+    if (!L.tiles.empty()) {
+        DQTG_REQUIRE(lstride <= 1024, DQTG_ERROR, "too many levels for level_counts");
+        { DQTG_SPAN(e, "level_count_kernel"); level_count_kernel<<<(unsigned)L.tiles.size(), 256, 0, e.stream>>>(L.d_tiles, q.d_levels, d, lstride); }
+        e.launched();
+    }
+    e.from_device(counts, d, (size_t)L.nt * lstride * 8);
+    e.sync();
+}
+
 void dequantize(Engine& e, const QState& q, float* out_dev) {
     const Layout& L = *q.L;
     const int ntiles = (int)L.tiles.size();
     if (!ntiles) return;
-    // per-tile protected offsets from the levels themselves
     auto* tile_prot = (uint32_t*)e.buf("dq.tile_prot", (size_t)ntiles * 4 + 4);
     auto* tile_off = (unsigned long long*)e.buf("dq.tile_off", (size_t)(ntiles + 1) * 8);
     auto* cb_len_d = (uint32_t*)e.buf("dq.cblen", kLayerTypes * 4);
     DQTG_CUDA(cudaMemcpyAsync(cb_len_d, q.cb_len, sizeof(q.cb_len), cudaMemcpyHostToDevice,
                               e.stream));
     count_protected(e, L, q.d_levels, cb_len_d, tile_prot);
-    scan_u32_kernel<<<1, 1024, 0, e.stream>>>(tile_prot, ntiles, tile_off);
-    dequant_kernel<<<ntiles, 256, 0, e.stream>>>(L.d_tiles, L.d_types, L.d_off, q.d_cb,
+    { DQTG_SPAN(e, "scan_u32_kernel"); scan_u32_kernel<<<1, 1024, 0, e.stream>>>(tile_prot, ntiles, tile_off); }
+    unsigned long long total = 0;
+    DQTG_CUDA(cudaMemcpyAsync(&total, tile_off + ntiles, 8, cudaMemcpyDeviceToHost, e.stream));
+    e.sync();
+    DQTG_REQUIRE(total == q.prot_total, DQTG_CORRUPT_INDEX, "unreferenced protected entries");
+    { DQTG_SPAN(e, "dequant_kernel"); dequant_kernel<<<ntiles, 256, 0, e.stream>>>(L.d_tiles, L.d_types, L.d_off, q.d_cb,
                                                  (int)q.cb_stride, cb_len_d, q.d_levels, tile_off,
-                                                 q.d_pval, out_dev, e.d_err);
+                                                 q.d_ppos, q.d_pval, out_dev, e.d_err); }
     e.launched(2);
     DQTG_CUDA(cudaGetLastError());
 }
 
 void scan_tiles(Engine& e, const uint32_t* in, int n, unsigned long long* out) {
-    scan_u32_kernel<<<1, 1024, 0, e.stream>>>(in, n, out);
+    { DQTG_SPAN(e, "scan_u32_kernel"); scan_u32_kernel<<<1, 1024, 0, e.stream>>>(in, n, out); }
     e.launched();
 }
 

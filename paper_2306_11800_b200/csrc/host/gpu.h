@@ -54,6 +54,10 @@ struct StateHandle {
     StateHandle() = default;
     StateHandle(const StateHandle&) = delete;
     StateHandle(StateHandle&& o) noexcept : h(o.h) { o.h = nullptr; }
+    StateHandle& operator=(StateHandle&& o) noexcept {
+        std::swap(h, o.h);
+        return *this;
+    }
     ~StateHandle() {
         if (h) dqtg_qstate_destroy(h);
     }

@@ -76,6 +76,8 @@ def _load():
         "dqtg_engine_destroy": (None, [_P]),
         "dqtg_engine_sync": (C.c_int, [_P]),
         "dqtg_engine_launches": (C.c_uint64, [_P]),
+        "dqtg_engine_profile": (C.c_int, [_P, C.c_int]),
+        "dqtg_engine_profile_report": (C.c_int, [_P, C.c_char_p, C.c_uint64]),
         "dqtg_sketch_range": (C.c_int, [C.c_double, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
         "dqtg_sketch_build": (C.c_int, [_P, _P, C.c_uint64, C.c_double, C.POINTER(C.c_uint64),
                                         _P, _P]),
@@ -158,6 +160,13 @@ class _Meta:
         self.numel = [int(np.prod(s, dtype=np.uint64)) for s in self.shapes]
 
 
+def _as_buf(a):
+    """numpy arrays stay host buffers; ints are raw (host or device) pointers."""
+    if isinstance(a, (int, np.integer)):
+        return int(a)
+    return np.ascontiguousarray(a, np.float32)
+
+
 def _ptr_array(arrs):
     return (C.c_void_p * max(len(arrs), 1))(*[_ptr(a) for a in arrs])
 
@@ -190,21 +199,20 @@ class DevCheckpoint:
             self.h = None
 
     def set_weights(self, arrays):
-        arrs = [np.ascontiguousarray(a, np.float32) if isinstance(a, np.ndarray) else a
-                for a in arrays]
+        arrs = [_as_buf(a) for a in arrays]
         _check(LIB.dqtg_ckpt_set_weights(self.h, _ptr_array(arrs)))
 
     def set_scores(self, mag, sens=None):
-        m = [np.ascontiguousarray(a, np.float32) for a in mag]
-        s = None if sens is None else [np.ascontiguousarray(a, np.float32) for a in sens]
+        m = [_as_buf(a) for a in mag]
+        s = None if sens is None else [_as_buf(a) for a in sens]
         _check(LIB.dqtg_ckpt_set_scores(self.h, _ptr_array(m), None if s is None else _ptr_array(s)))
 
     def set_ema(self, ema):
-        e = None if ema is None else [np.ascontiguousarray(a, np.float32) for a in ema]
+        e = None if ema is None else [_as_buf(a) for a in ema]
         _check(LIB.dqtg_ckpt_set_ema(self.h, None if e is None else _ptr_array(e)))
 
     def update_ema(self, grads, beta=0.9):
-        g = [np.ascontiguousarray(a, np.float32) for a in grads]
+        g = [_as_buf(a) for a in grads]
         _check(LIB.dqtg_ckpt_update_ema(self.h, _ptr_array(g), beta))
 
     @property
@@ -275,6 +283,17 @@ class Engine:
     @property
     def launches(self):
         return LIB.dqtg_engine_launches(self.h)
+
+    def profile(self, enable=True):
+        _check(LIB.dqtg_engine_profile(self.h, 1 if enable else 0))
+
+    def profile_report(self):
+        """{kernel: (launches, total_ms)} since the last report (CUDA events)."""
+        import json
+
+        buf = C.create_string_buffer(1 << 16)
+        _check(LIB.dqtg_engine_profile_report(self.h, buf, len(buf)))
+        return {k: tuple(v) for k, v in json.loads(buf.value.decode()).items()}
 
     # -- sketch ------------------------------------------------------------
     @staticmethod
