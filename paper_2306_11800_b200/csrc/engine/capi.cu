@@ -71,6 +71,11 @@ dqtg_status dqtg_engine_create(int device, void* stream, dqtg_engine** out) {
                 e.own_stream = true;
             }
             DQTG_CUDA(cudaMalloc(&e.d_err, 16));
+            // keep freed pool memory cached: per-step states/records reuse it
+            cudaMemPool_t pool;
+            DQTG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+            uint64_t keep = ~0ull;
+            DQTG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
             DQTG_CUDA(cudaMemset(e.d_err, 0, 16));
         } catch (...) {
             delete h;
@@ -379,11 +384,12 @@ dqtg_status dqtg_qstate_upload(dqtg_engine* h, const dqtg_layout* layout, uint64
         std::vector<float> flat((size_t)kLayerTypes * stride, 0.0f);
         for (int lt = 0; lt < kLayerTypes; ++lt)
             std::copy(q->cb[lt].begin(), q->cb[lt].end(), flat.begin() + (size_t)lt * stride);
-        DQTG_CUDA(cudaMalloc(&q->d_cb, flat.size() * 4));
-        DQTG_CUDA(cudaMemcpy(q->d_cb, flat.data(), flat.size() * 4, cudaMemcpyHostToDevice));
+        q->d_cb = (decltype(q->d_cb))e.dalloc(flat.size() * 4);
+        DQTG_CUDA(cudaMemcpyAsync(q->d_cb, flat.data(), flat.size() * 4, cudaMemcpyHostToDevice,
+                                  e.stream));
         const Layout& L = *q->L;
-        DQTG_CUDA(cudaMalloc(&q->d_levels, L.Np * 2));
-        DQTG_CUDA(cudaMemset(q->d_levels, 0, L.Np * 2));
+        q->d_levels = (decltype(q->d_levels))e.dalloc(L.Np * 2);
+        DQTG_CUDA(cudaMemsetAsync(q->d_levels, 0, L.Np * 2, e.stream));
         q->prot_count.assign(L.nt, 0);
         q->prot_off.assign(L.nt + 1, 0);
         uint64_t acc = 0;
@@ -393,8 +399,8 @@ dqtg_status dqtg_qstate_upload(dqtg_engine* h, const dqtg_layout* layout, uint64
             acc += q->prot_count[i];
         }
         q->prot_off[L.nt] = q->prot_total = acc;
-        DQTG_CUDA(cudaMalloc(&q->d_ppos, (acc + 1) * 8));
-        DQTG_CUDA(cudaMalloc(&q->d_pval, (acc + 1) * 2));
+        q->d_ppos = (decltype(q->d_ppos))e.dalloc((acc + 1) * 8);
+        q->d_pval = (decltype(q->d_pval))e.dalloc((acc + 1) * 2);
         for (uint32_t i = 0; i < L.nt; ++i) {
             if (L.numel[i]) e.to_device(q->d_levels + L.off[i], levels[i], L.numel[i] * 2);
             if (q->prot_count[i]) {

@@ -99,40 +99,38 @@ __device__ __forceinline__ void add_symbol(uint32_t* f, uint32_t NS, uint32_t B,
 }
 
 // ---- E1 --------------------------------------------------------------------
+constexpr int kWords = kTile / 32;  // 32-element words per tile
+
 template <bool HAS_BASE>
 __global__ void __launch_bounds__(kCB) enc_tile_kernel(EncArgs A) {
     extern __shared__ uint32_t dyn[];
-    uint32_t* s_freq = dyn;  // B*NS
-    uint16_t* s_key = (uint16_t*)(s_freq + A.B * A.NS);
+    const uint32_t B = A.B, NS = A.NS;
+    uint32_t* s_freq = dyn;                     // B*NS
+    uint32_t* s_mask = s_freq + B * NS;         // B*kWords: element bitmask per key
+    uint16_t* s_wpre = (uint16_t*)(s_mask + B * kWords);  // B*kWords exclusive popcounts
+    uint16_t* s_key = s_wpre + B * kWords;
     uint16_t* s_d = s_key + kTile;
-    uint16_t* s_cur = s_d + kTile;
-    uint16_t* s_sd = s_cur + kTile;
+    uint16_t* s_sd = s_d + kTile;
     uint16_t* s_sk = s_sd + kTile;
     uint16_t* s_hp = s_sk + kTile;  // kTile + 2
-    __shared__ uint32_t s_cnt[kMaxB], s_start[kMaxB], s_running[kMaxB], s_run0[kMaxB],
-        s_run1[kMaxB];
-    __shared__ uint32_t s_wcnt[kCB / 32][kMaxB];
+    __shared__ uint32_t s_cnt[kMaxB], s_start[kMaxB], s_run0[kMaxB], s_run1[kMaxB];
     __shared__ uint32_t s_tab[256];
     __shared__ uint32_t s_red[kCB / 32];
     __shared__ unsigned long long s_scan[33];
 
     const int ti = blockIdx.x;
     const Tile T = A.tiles[ti];
-    const uint32_t cnt = T.count, B = A.B, NS = A.NS;
+    const uint32_t cnt = T.count;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
     for (uint32_t i = tid; i < B * NS; i += kCB) s_freq[i] = 0;
-    if (tid < (int)B) {
-        s_cnt[tid] = 0;
-        s_running[tid] = 0;
-        for (int w = 0; w < kCB / 32; ++w) s_wcnt[w][tid] = 0;
-    }
+    for (uint32_t i = tid; i < B * kWords; i += kCB) s_mask[i] = 0;
     {  // CRC byte table (codec.cpp:276-284)
         uint32_t c = tid;
         for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xedb88320u ^ (c >> 1) : c >> 1;
         s_tab[tid] = c;
     }
-    // load 16 consecutive elements per thread
+    // load 16 consecutive elements per thread (two 16-byte vectors per stream)
     {
         const uint32_t e0 = tid * kIt;
         if (e0 < cnt) {
@@ -154,10 +152,10 @@ __global__ void __launch_bounds__(kCB) enc_tile_kernel(EncArgs A) {
                 if (e < cnt) {
                     uint32_t c = c16[j], p = HAS_BASE ? p16[j] : 0u;
                     bad |= (p >= B) | (c >= B);
-                    uint32_t d = p >= c ? p - c : p + B - c;
-                    s_key[e] = (uint16_t)(p < B ? p : 0u);
-                    s_d[e] = (uint16_t)d;
-                    s_cur[e] = (uint16_t)c;
+                    p = p < B ? p : 0u;
+                    c = c < B ? c : 0u;
+                    s_key[e] = (uint16_t)p;
+                    s_d[e] = (uint16_t)(p >= c ? p - c : p + B - c);
                 }
             }
             if (bad) atomicOr(A.err, kErrCorruptIndex);
@@ -169,16 +167,27 @@ __global__ void __launch_bounds__(kCB) enc_tile_kernel(EncArgs A) {
     {
         const int lead0 = 2 * (int)kTile - 2 * (int)cnt;
         uint32_t r = 0;
-        for (int vb = tid * 32; vb < tid * 32 + 32; ++vb) {
-            int rb = vb - lead0;
+        for (int vb = tid * 32; vb < tid * 32 + 32; vb += 2) {
+            int rb = vb - lead0;  // even: whole levels
             if (rb < 0) continue;
-            uint32_t lv = s_cur[rb >> 1];
-            uint32_t byte = (rb & 1) ? (lv >> 8) : (lv & 0xff);
-            r = s_tab[(r ^ byte) & 0xff] ^ (r >> 8);
+            const uint32_t e = (uint32_t)rb >> 1;
+            const uint32_t p = s_key[e], d = s_d[e];
+            const uint32_t lv = p >= d ? p - d : p + B - d;  // target level
+            r = s_tab[(r ^ lv) & 0xff] ^ (r >> 8);
+            r = s_tab[(r ^ (lv >> 8)) & 0xff] ^ (r >> 8);
         }
         r = r ? crc_multmodp(c_crc_pw[tid], r) : 0u;
         r = warp_xor(r);
         if (lane == 0) s_red[wid] = r;
+        // ---- stable multisplit on the previous level: per-key element bitmasks
+        for (int rnd = 0; rnd < kIt; ++rnd) {
+            const uint32_t e = rnd * kCB + tid;
+            const bool valid = e < cnt;
+            const uint32_t key = valid ? s_key[e] : 0xffffu;
+            const uint32_t peers = __match_any_sync(0xffffffffu, key);
+            if (valid && (peers & ((1u << lane) - 1u)) == 0)
+                s_mask[key * kWords + (e >> 5)] = peers;
+        }
         __syncthreads();
         if (tid == 0) {
             uint32_t x = 0;
@@ -189,9 +198,17 @@ __global__ void __launch_bounds__(kCB) enc_tile_kernel(EncArgs A) {
             if (x) atomicXor(A.crc_acc, x);
         }
     }
-
-    // ---- stable group-by on the previous level (rearrange)
-    for (uint32_t e = tid; e < cnt; e += kCB) atomicAdd(&s_cnt[s_key[e]], 1u);
+    // exclusive popcount prefix per key over the 128 words
+    for (uint32_t b = tid; b < B; b += kCB) {
+        uint32_t acc = 0;
+        const uint32_t* m = s_mask + b * kWords;
+        uint16_t* w = s_wpre + b * kWords;
+        for (int i = 0; i < kWords; ++i) {
+            w[i] = (uint16_t)acc;
+            acc += __popc(m[i]);
+        }
+        s_cnt[b] = acc;
+    }
     __syncthreads();
     if (wid == 0) {
         uint32_t run = 0;
@@ -208,41 +225,14 @@ __global__ void __launch_bounds__(kCB) enc_tile_kernel(EncArgs A) {
         }
     }
     __syncthreads();
-    const int nbits = B <= 1 ? 1 : 32 - __clz((int)(B - 1));
-    const uint32_t lt_mask = (1u << lane) - 1u;
-    for (int r = 0; r < kIt; ++r) {
-        const uint32_t base = r * kCB;
-        if (base >= cnt) break;
-        const uint32_t e = base + tid;
-        const bool valid = e < cnt;
-        const uint32_t key = valid ? s_key[e] : 0u;
-        uint32_t peers = __ballot_sync(0xffffffffu, valid);
-        for (int bit = 0; bit < nbits; ++bit) {
-            uint32_t on = (key >> bit) & 1u;
-            uint32_t bb = __ballot_sync(0xffffffffu, valid && on);
-            peers &= on ? bb : ~bb;
-        }
-        const uint32_t rank = __popc(peers & lt_mask);
-        if (valid && rank == 0) s_wcnt[wid][key] = __popc(peers);
-        __syncthreads();
-        if (valid) {
-            uint32_t o = s_running[key];
-            for (int w = 0; w < wid; ++w) o += s_wcnt[w][key];
-            const uint32_t pos = s_start[key] + o + rank;
-            s_sd[pos] = s_d[e];
-            s_sk[pos] = (uint16_t)key;
-        }
-        __syncthreads();
-        if (tid < (int)B) {
-            uint32_t t = 0;
-            for (int w = 0; w < kCB / 32; ++w) {
-                t += s_wcnt[w][tid];
-                s_wcnt[w][tid] = 0;
-            }
-            s_running[tid] += t;
-        }
-        __syncthreads();
+    for (uint32_t e = tid; e < cnt; e += kCB) {
+        const uint32_t key = s_key[e], w = e >> 5;
+        const uint32_t rank = s_wpre[key * kWords + w] + __popc(s_mask[key * kWords + w] & ((1u << (e & 31)) - 1u));
+        const uint32_t pos = s_start[key] + rank;
+        s_sd[pos] = s_d[e];
+        s_sk[pos] = (uint16_t)key;
     }
+    __syncthreads();
 
     // ---- runs inside group segments
     uint32_t nh = 0;
@@ -885,11 +875,35 @@ __device__ __forceinline__ void put_bits(uint32_t* words, unsigned long long q,
     }
 }
 
+// E2b: emission.  Each (tile, group) segment owns a contiguous bit range of its
+// group's stream.  Codes are first packed MSB-first into shared-memory words
+// laid out with the destination's bit phase, then copied out as whole 32-bit
+// words: interior words with plain stores, the two boundary words with
+// atomicOr (they may share bytes with neighbouring segments or headers).
+constexpr int kStageWords = 6144;  // 24 KiB staging per tile
+
+__device__ __forceinline__ void stage_bits(uint32_t* st, unsigned long long q,
+                                           unsigned long long code, int len) {
+    while (len > 0) {
+        const uint32_t w = (uint32_t)(q >> 5), off = (uint32_t)(q & 31);
+        const int take = (int)min(32u - off, (uint32_t)len);
+        const uint32_t piece = (uint32_t)((code >> (len - take)) & ((1ull << take) - 1));
+        atomicOr(st + w, piece << (32 - off - take));
+        q += take;
+        len -= take;
+    }
+}
+
 __global__ void __launch_bounds__(kCB) enc_emit_kernel(EncArgs A, CodeTabs C,
                                                        const unsigned long long* segoff,
                                                        uint8_t* rec) {
     __shared__ unsigned long long s_scan[33];
-    __shared__ unsigned long long s_runbits[kTile + 1];
+    __shared__ uint32_t s_runbits[kTile + 1];
+    __shared__ uint32_t s_stage[kStageWords];
+    __shared__ uint32_t s_sw[kMaxB + 1];     // staging word base per segment
+    __shared__ uint32_t s_phase[kMaxB];
+    __shared__ unsigned long long s_dw[kMaxB];  // destination word of the segment start
+    __shared__ int s_overflow;
     const int ti = blockIdx.x;
     const uint32_t B = A.B, NS = A.NS;
     const Tile T = A.tiles[ti];
@@ -897,9 +911,9 @@ __global__ void __launch_bounds__(kCB) enc_emit_kernel(EncArgs A, CodeTabs C,
     const Seg* segs = A.segs + (size_t)ti * B;
     const unsigned long long* runs = A.runs + (size_t)ti * kTile;
     uint32_t* words = (uint32_t*)rec;
-    // blocked: thread handles runs [16t, 16t+16)
-    unsigned long long mine = 0;
     const uint32_t r0 = threadIdx.x * kIt;
+    // pass 1: bits per run (blocked: thread owns runs [16t, 16t+16))
+    uint32_t mine = 0;
     for (int j = 0; j < kIt; ++j) {
         const uint32_t r = r0 + j;
         if (r >= R) break;
@@ -916,9 +930,8 @@ __global__ void __launch_bounds__(kCB) enc_emit_kernel(EncArgs A, CodeTabs C,
     }
     unsigned long long tot;
     unsigned long long ex = block_exclusive_scan<unsigned long long>(mine, s_scan, &tot);
-    // per-run exclusive bit offsets
     {
-        unsigned long long acc = ex;
+        uint32_t acc = (uint32_t)ex;
         for (int j = 0; j < kIt; ++j) {
             const uint32_t r = r0 + j;
             if (r >= R) break;
@@ -934,8 +947,44 @@ __global__ void __launch_bounds__(kCB) enc_emit_kernel(EncArgs A, CodeTabs C,
             if (L > 1) code_of_len(C, tb, NS, B, L, c, l2);
             acc += l1 + l2;
         }
+        if (threadIdx.x == 0) s_runbits[R] = (uint32_t)tot;
     }
     __syncthreads();
+    // segment staging layout (one warp): words needed = ceil((phase + bits) / 32)
+    if (threadIdx.x < 32) {
+        uint32_t base = 0;
+        for (uint32_t b0 = 0; b0 < B; b0 += 32) {
+            const uint32_t b = b0 + threadIdx.x;
+            uint32_t nw = 0;
+            if (b < B) {
+                const Seg& S = segs[b];
+                uint32_t bits = S.n ? s_runbits[S.run_end] - s_runbits[S.run_begin] : 0u;
+                unsigned long long dest = 0;
+                if (bits) dest = C.gi[T.tensor * B + b].pay * 8 + segoff[(size_t)ti * B + b];
+                s_phase[b] = (uint32_t)(dest & 31);
+                s_dw[b] = dest >> 5;
+                nw = bits ? (s_phase[b] + bits + 31) / 32 : 0u;
+            }
+            uint32_t x = nw;
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if ((int)threadIdx.x >= o) x += y;
+            }
+            if (b < B) s_sw[b] = base + x - nw;
+            base += __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (threadIdx.x == 0) {
+            s_sw[B] = base;
+            s_overflow = base > (uint32_t)kStageWords;
+        }
+    }
+    __syncthreads();
+    const bool staged = !s_overflow;
+    const uint32_t nwords = s_sw[B];
+    if (staged)
+        for (uint32_t i = threadIdx.x; i < nwords; i += kCB) s_stage[i] = 0;
+    __syncthreads();
+    // pass 2: place codes
     for (int j = 0; j < kIt; ++j) {
         const uint32_t r = r0 + j;
         if (r >= R) break;
@@ -945,16 +994,41 @@ __global__ void __launch_bounds__(kCB) enc_emit_kernel(EncArgs A, CodeTabs C,
         if (!L) continue;
         const uint32_t tb = T.tensor * B + b;
         const Seg& S = segs[b];
-        unsigned long long q = C.gi[tb].pay * 8 + segoff[(size_t)ti * B + b] +
-                               (s_runbits[r] - s_runbits[S.run_begin]);
+        const uint32_t local = s_runbits[r] - s_runbits[S.run_begin];
         unsigned long long c;
         uint32_t l;
         code_of(C, tb, NS, v, c, l);
-        put_bits(words, q, c, (int)l);
-        q += l;
-        if (L > 1) {
-            code_of_len(C, tb, NS, B, L, c, l);
+        if (staged) {
+            unsigned long long q = (unsigned long long)s_sw[b] * 32 + s_phase[b] + local;
+            stage_bits(s_stage, q, c, (int)l);
+            if (L > 1) {
+                q += l;
+                code_of_len(C, tb, NS, B, L, c, l);
+                stage_bits(s_stage, q, c, (int)l);
+            }
+        } else {  // very dense tile: straight to the record
+            unsigned long long q = C.gi[tb].pay * 8 + segoff[(size_t)ti * B + b] + local;
             put_bits(words, q, c, (int)l);
+            if (L > 1) {
+                q += l;
+                code_of_len(C, tb, NS, B, L, c, l);
+                put_bits(words, q, c, (int)l);
+            }
+        }
+    }
+    if (!staged) return;
+    __syncthreads();
+    // pass 3: copy staged words to the record (big-endian bit order -> LE words)
+    for (uint32_t i = threadIdx.x; i < nwords; i += kCB) {
+        uint32_t b = 0;
+        while (b + 1 < B && s_sw[b + 1] <= i) ++b;
+        const uint32_t j = i - s_sw[b], nw = s_sw[b + 1] - s_sw[b];
+        const uint32_t v = __byte_perm(s_stage[i], 0, 0x0123);
+        uint32_t* dst = words + s_dw[b] + j;
+        if (j == 0 || j + 1 == nw) {
+            if (v) atomicOr(dst, v);
+        } else {
+            *dst = v;
         }
     }
 }
@@ -1071,8 +1145,10 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
         std::vector<uint8_t> host = pre;
         put_le(host, 0, 4);  // crc32 of nothing = 0
         rec->size = host.size();
-        DQTG_CUDA(cudaMalloc(&rec->d_buf, host.size()));
-        DQTG_CUDA(cudaMemcpy(rec->d_buf, host.data(), host.size(), cudaMemcpyHostToDevice));
+        rec->d_buf = (uint8_t*)e.dalloc(host.size());
+        DQTG_CUDA(cudaMemcpyAsync(rec->d_buf, host.data(), host.size(), cudaMemcpyHostToDevice,
+                                  e.stream));
+        e.sync();
         return rec;
     }
 
@@ -1103,7 +1179,8 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
     DQTG_CUDA(cudaMemsetAsync(small, 0, 64, st));
 
     // E1
-    const size_t e1_smem = (size_t)B * NS * 4 + (size_t)kTile * 2 * 5 + (kTile + 2) * 2 + 16;
+    const size_t e1_smem = (size_t)B * NS * 4 + (size_t)B * kWords * 6 + (size_t)kTile * 2 * 4 +
+                           (kTile + 2) * 2 + 16;
     if (base) {
         DQTG_CUDA(cudaFuncSetAttribute(enc_tile_kernel<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e1_smem));
@@ -1217,7 +1294,7 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
     // ---- writers
     rec->size = total;
     rec->cap = round_up(total, 16) + 16;
-    DQTG_CUDA(cudaMalloc(&rec->d_buf, rec->cap));
+    rec->d_buf = (uint8_t*)e.dalloc(rec->cap);
     DQTG_CUDA(cudaMemsetAsync(rec->d_buf, 0, rec->cap, st));
     DQTG_CUDA(cudaMemcpyAsync(rec->d_buf, pre.data(), pre.size(), cudaMemcpyHostToDevice, st));
     auto* d_statics = (uint8_t*)e.buf("e.statics", statics.size() + 8);

@@ -56,6 +56,16 @@ void* Engine::buf(const std::string& name, size_t bytes) {
     return slot.first;
 }
 
+void* Engine::dalloc(size_t bytes) {
+    void* p = nullptr;
+    DQTG_CUDA(cudaMallocAsync(&p, bytes ? bytes : 16, stream));
+    return p;
+}
+
+void Engine::dfree(void* p) {
+    if (p) cudaFreeAsync(p, stream);
+}
+
 void* Engine::host_pinned(size_t bytes) {
     if (pinned_cap < bytes) {
         if (pinned) {
@@ -280,12 +290,15 @@ uint32_t QState::max_levels() const {  // quantize.cpp:357-365
 }
 
 QState::~QState() {
-    cudaFree(d_cb);
-    cudaFree(d_levels);
-    cudaFree(d_ppos);
-    cudaFree(d_pval);
+    if (!eng) return;
+    eng->dfree(d_cb);
+    eng->dfree(d_levels);
+    eng->dfree(d_ppos);
+    eng->dfree(d_pval);
 }
 
-Record::~Record() { cudaFree(d_buf); }
+Record::~Record() {
+    if (eng) eng->dfree(d_buf);
+}
 
 }  // namespace dqtg

@@ -143,6 +143,9 @@ struct Engine {
         return BucketTab{t.d_U, t.kmin, t.kmax, t.NB, t.kw_lo, t.zbits, t.inv_log2_gamma};
     }
     void* buf(const std::string& name, size_t bytes);  // scratch, contents undefined
+    // stream-ordered pool allocations for per-step objects (states, records)
+    void* dalloc(size_t bytes);
+    void dfree(void* p);
     void* host_pinned(size_t bytes);
     void sync() { DQTG_CUDA(cudaStreamSynchronize(stream)); }
     void launched(int n = 1) { launches += n; }

@@ -706,14 +706,14 @@ std::unique_ptr<QState> quantize(Engine& e, const DevCkpt& c, const dqtg_config&
     q->step = step;
     q->cfg = cfg;
     q->cb_stride = std::max(1u, std::max(cfg.bins, cfg.embed_bins));
-    DQTG_CUDA(cudaMalloc(&q->d_levels, L.Np * 2));
-    DQTG_CUDA(cudaMalloc(&q->d_cb, (size_t)kLayerTypes * q->cb_stride * 4));
+    q->d_levels = (decltype(q->d_levels))e.dalloc(L.Np * 2);
+    q->d_cb = (decltype(q->d_cb))e.dalloc((size_t)kLayerTypes * q->cb_stride * 4);
     q->prot_count.assign(L.nt, 0);
     q->prot_off.assign(L.nt + 1, 0);
     if (L.N == 0) {
         DQTG_CUDA(cudaMemsetAsync(q->d_levels, 0, L.Np * 2, e.stream));
-        DQTG_CUDA(cudaMalloc(&q->d_ppos, 8));
-        DQTG_CUDA(cudaMalloc(&q->d_pval, 8));
+        q->d_ppos = (decltype(q->d_ppos))e.dalloc(8);
+        q->d_pval = (decltype(q->d_pval))e.dalloc(8);
         return q;
     }
     DQTG_REQUIRE(cfg.alpha > 0.0 && cfg.alpha < 1.0, DQTG_ALPHA_OUT_OF_RANGE,
@@ -743,8 +743,8 @@ std::unique_ptr<QState> quantize(Engine& e, const DevCkpt& c, const dqtg_config&
     }
     q->prot_off[L.nt] = acc;
     q->prot_total = acc;
-    DQTG_CUDA(cudaMalloc(&q->d_ppos, (acc + 1) * 8));
-    DQTG_CUDA(cudaMalloc(&q->d_pval, (acc + 1) * 2));
+    q->d_ppos = (decltype(q->d_ppos))e.dalloc((acc + 1) * 8);
+    q->d_pval = (decltype(q->d_pval))e.dalloc((acc + 1) * 2);
     stage_pass_c(e, c, a, s, *q);
     std::vector<float> hcb((size_t)kLayerTypes * q->cb_stride);
     DQTG_CUDA(cudaMemcpyAsync(q->cb_len, s.cb_len, sizeof(q->cb_len), cudaMemcpyDeviceToHost, e.stream));
