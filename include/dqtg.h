@@ -163,6 +163,32 @@ void dqtg_record_destroy(dqtg_record *r);
 dqtg_status dqtg_decode_record(dqtg_engine *e, const uint8_t *rec, uint64_t n,
                                const dqtg_qstate *base, dqtg_qstate **out);
 
+/* ---- tensor-sharded checkpoints (multi-GPU) ----------------
+ * Thresholds and codebooks must come from the histograms of the WHOLE
+ * checkpoint.  Each rank quantizes its shard in three stages; between them the
+ * caller sums the u64 histogram buffers over all ranks (ncclAllReduce / any
+ * collective, exact and order independent):
+ *   stage1 -> score_hist [2*7*HS]      (all-reduce SUM)
+ *   stage2 -> value_hist [7*HS]        (all-reduce SUM)
+ *   stage3 -> quantized state of this shard (codebooks identical on every rank)
+ * Buffers are device memory (dqtg_shard_hist_len entries of u64). */
+uint64_t dqtg_shard_hist_len(dqtg_engine *e, const dqtg_config *cfg, int which /*0 score, 1 value*/);
+dqtg_status dqtg_shard_stage1(dqtg_engine *e, const dqtg_ckpt *c, const dqtg_config *cfg,
+                              uint64_t *score_hist_dev);
+dqtg_status dqtg_shard_stage2(dqtg_engine *e, const dqtg_ckpt *c, const dqtg_config *cfg,
+                              const uint64_t *score_hist_dev, uint64_t *value_hist_dev);
+dqtg_status dqtg_shard_stage3(dqtg_engine *e, const dqtg_ckpt *c, const dqtg_config *cfg,
+                              uint64_t seed, uint64_t step, const uint64_t *value_hist_dev,
+                              dqtg_qstate **out);
+/* encode this shard's tensor blocks with the GLOBAL alphabet B (max over ranks of
+ * max_levels, codec.cpp:416-417) and the global tensor count; bytes
+ * [*body_offset, size-4) are this rank's blocks, the last 4 bytes the CRC-32 of
+ * its level stream (combine across ranks with the zlib crc32_combine rule). */
+dqtg_status dqtg_encode_record_shard(dqtg_engine *e, const dqtg_qstate *base,
+                                     const dqtg_qstate *target, double quality_delta,
+                                     uint32_t global_B, uint32_t global_tensors,
+                                     dqtg_record **out, uint64_t *body_offset);
+
 /* ---- fused step: compute_scores + quantize_checkpoint + encode_delta_record
  * (the path Chain::append + cmd_compress run, chain.cpp:86-129 / dqt.cpp:208-210) */
 dqtg_status dqtg_compress_step(dqtg_engine *e, const dqtg_ckpt *c, const dqtg_config *cfg,

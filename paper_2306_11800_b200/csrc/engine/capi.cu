@@ -470,6 +470,57 @@ dqtg_status dqtg_decode_record(dqtg_engine* h, const uint8_t* rec, uint64_t n,
     });
 }
 
+uint64_t dqtg_shard_hist_len(dqtg_engine* h, const dqtg_config* cfg, int which) {
+    uint64_t n = 0;
+    dqtg_status st = guard([&] {
+        LOCK(&h->e);
+        n = shard_hist_len(h->e, *cfg, which);
+    });
+    return st == DQTG_OK ? n : 0;
+}
+
+dqtg_status dqtg_shard_stage1(dqtg_engine* h, const dqtg_ckpt* c, const dqtg_config* cfg,
+                              uint64_t* score_hist) {
+    return guard([&] {
+        LOCK(&h->e);
+        shard_stage1(h->e, c->c, *cfg, (unsigned long long*)score_hist);
+    });
+}
+
+dqtg_status dqtg_shard_stage2(dqtg_engine* h, const dqtg_ckpt* c, const dqtg_config* cfg,
+                              const uint64_t* score_hist, uint64_t* value_hist) {
+    return guard([&] {
+        LOCK(&h->e);
+        shard_stage2(h->e, c->c, *cfg, (const unsigned long long*)score_hist,
+                     (unsigned long long*)value_hist);
+    });
+}
+
+dqtg_status dqtg_shard_stage3(dqtg_engine* h, const dqtg_ckpt* c, const dqtg_config* cfg,
+                              uint64_t seed, uint64_t step, const uint64_t* value_hist,
+                              dqtg_qstate** out) {
+    return guard([&] {
+        LOCK(&h->e);
+        auto q = shard_stage3(h->e, c->c, *cfg, seed, step, (const unsigned long long*)value_hist);
+        auto* s = new dqtg_qstate();
+        s->q = std::move(q);
+        *out = s;
+    });
+}
+
+dqtg_status dqtg_encode_record_shard(dqtg_engine* h, const dqtg_qstate* base,
+                                     const dqtg_qstate* target, double quality, uint32_t gB,
+                                     uint32_t gnt, dqtg_record** out, uint64_t* body_offset) {
+    return guard([&] {
+        LOCK(&h->e);
+        auto r = encode_record_ex(h->e, base ? base->q.get() : nullptr, *target->q, quality, gB,
+                                  gnt, body_offset);
+        auto* rr = new dqtg_record();
+        rr->r = std::move(r);
+        *out = rr;
+    });
+}
+
 dqtg_status dqtg_compress_step(dqtg_engine* h, const dqtg_ckpt* c, const dqtg_config* cfg,
                                uint64_t seed, uint64_t step, const dqtg_qstate* base,
                                double quality, dqtg_qstate** state_out, dqtg_record** record_out) {

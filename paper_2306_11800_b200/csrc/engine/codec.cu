@@ -15,6 +15,7 @@
 //   W   header/table/protected writers; E2b MSB-first bit emission into the
 //       final record buffer (codec.cpp:111-122)
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
@@ -106,13 +107,13 @@ __global__ void __launch_bounds__(kCB) enc_tile_kernel(EncArgs A) {
     extern __shared__ uint32_t dyn[];
     const uint32_t B = A.B, NS = A.NS;
     uint32_t* s_freq = dyn;                     // B*NS
-    uint32_t* s_mask = s_freq + B * NS;         // B*kWords: element bitmask per key
+    uint32_t* s_mask = s_freq + ((B * NS + 3u) & ~3u);  // B*kWords: element bitmask per key
     uint16_t* s_wpre = (uint16_t*)(s_mask + B * kWords);  // B*kWords exclusive popcounts
-    uint16_t* s_key = s_wpre + B * kWords;
-    uint16_t* s_d = s_key + kTile;
+    uint16_t* s_key = s_wpre + B * kWords;  // kTile + 2; reused as s_hp after the scatter
+    uint16_t* s_d = s_key + kTile + 2;
     uint16_t* s_sd = s_d + kTile;
     uint16_t* s_sk = s_sd + kTile;
-    uint16_t* s_hp = s_sk + kTile;  // kTile + 2
+    uint16_t* s_hp = s_key;
     __shared__ uint32_t s_cnt[kMaxB], s_start[kMaxB], s_run0[kMaxB], s_run1[kMaxB];
     __shared__ uint32_t s_tab[256];
     __shared__ uint32_t s_red[kCB / 32];
@@ -198,16 +199,25 @@ __global__ void __launch_bounds__(kCB) enc_tile_kernel(EncArgs A) {
             if (x) atomicXor(A.crc_acc, x);
         }
     }
-    // exclusive popcount prefix per key over the 128 words
-    for (uint32_t b = tid; b < B; b += kCB) {
-        uint32_t acc = 0;
-        const uint32_t* m = s_mask + b * kWords;
-        uint16_t* w = s_wpre + b * kWords;
-        for (int i = 0; i < kWords; ++i) {
-            w[i] = (uint16_t)acc;
-            acc += __popc(m[i]);
+    // exclusive popcount prefix per key over the 128 words: one warp per key,
+    // four words per lane, warp scan
+    for (uint32_t b = wid; b < B; b += kCB / 32) {
+        const uint4 mw = *(const uint4*)(s_mask + b * kWords + lane * 4);
+        const uint32_t p0 = __popc(mw.x), p1 = __popc(mw.y), p2 = __popc(mw.z), p3 = __popc(mw.w);
+        const uint32_t own = p0 + p1 + p2 + p3;
+        uint32_t x = own;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
         }
-        s_cnt[b] = acc;
+        const uint32_t ex = x - own;
+        uint16_t* w = s_wpre + b * kWords + lane * 4;
+        w[0] = (uint16_t)ex;
+        w[1] = (uint16_t)(ex + p0);
+        w[2] = (uint16_t)(ex + p0 + p1);
+        w[3] = (uint16_t)(ex + p0 + p1 + p2);
+        if (lane == 31) s_cnt[b] = x;
     }
     __syncthreads();
     if (wid == 0) {
@@ -620,10 +630,10 @@ __global__ void __launch_bounds__(128) enc_huffman_kernel(EncArgs A, const unsig
                 code_dense[(size_t)tb * NS + B + (uint32_t)s] = code;
                 len_dense[(size_t)tb * NS + B + (uint32_t)s] = (uint8_t)len;
             } else {
-                unsigned long long j = lb_u64(ukey + G.ov_begin, nov,
-                                              ((unsigned long long)tb << 32) | (unsigned long long)s);
-                code_ov[G.ov_begin + j] = code;
-                len_ov[G.ov_begin + j] = (uint8_t)len;
+                // overflow leaves were appended last, in ukey order: leaf i <-> ov_begin + i - n_dense
+                const unsigned long long j = G.ov_begin + (i - (n - nov));
+                code_ov[j] = code;
+                len_ov[j] = (uint8_t)len;
             }
             ++code;
         }
@@ -742,12 +752,41 @@ struct TensorRec {
     uint32_t ngroups, pad;
 };
 
-__global__ void prot_sizes_kernel(const TensorRec* tr, const uint64_t* ppos,
-                                  unsigned long long* sizes) {
-    const TensorRec R = tr[blockIdx.x];
-    for (unsigned long long i = R.prot_begin + threadIdx.x; i < R.prot_end; i += blockDim.x) {
+__device__ __forceinline__ uint32_t tensor_of_entry(const TensorRec* tr, uint32_t nt,
+                                                    unsigned long long i) {
+    uint32_t lo = 0, hi = nt;  // last tensor with prot_begin <= i
+    while (hi - lo > 1) {
+        uint32_t m = (lo + hi) >> 1;
+        if (tr[m].prot_begin <= i) lo = m;
+        else hi = m;
+    }
+    while (lo + 1 < nt && tr[lo].prot_end <= i) ++lo;
+    return lo;
+}
+
+__global__ void prot_sizes_kernel(const TensorRec* tr, uint32_t nt, unsigned long long np,
+                                  const uint64_t* ppos, unsigned long long* sizes) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < np;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const TensorRec& R = tr[tensor_of_entry(tr, nt, i)];
         unsigned long long d = i == R.prot_begin ? ppos[i] : ppos[i] - ppos[i - 1];
         sizes[i] = uvlen(d) + 2;
+    }
+}
+
+// protected entries of every tensor: uvarint position delta + u16 bf16
+__global__ void write_prot_kernel(const TensorRec* tr, uint32_t nt, unsigned long long np,
+                                  const uint64_t* ppos, const uint16_t* pval,
+                                  const unsigned long long* prot_scan, uint8_t* rec) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < np;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const TensorRec& R = tr[tensor_of_entry(tr, nt, i)];
+        const unsigned long long np_t = R.prot_end - R.prot_begin;
+        uint8_t* q = rec + R.off + R.static_len + uvlen(np_t) + (prot_scan[i] - prot_scan[R.prot_begin]);
+        unsigned long long d = i == R.prot_begin ? ppos[i] : ppos[i] - ppos[i - 1];
+        uint32_t k = put_uv(q, d);
+        q[k] = (uint8_t)(pval[i] & 0xff);
+        q[k + 1] = (uint8_t)(pval[i] >> 8);
     }
 }
 
@@ -797,15 +836,7 @@ __global__ void __launch_bounds__(kCB) write_tensor_kernel(
     const unsigned long long np = R.prot_end - R.prot_begin;
     if (threadIdx.x == 0) put_uv(p + o, np);
     o += uvlen(np);
-    const unsigned long long pb = prot_scan[R.prot_begin];
-    for (unsigned long long i = R.prot_begin + threadIdx.x; i < R.prot_end; i += kCB) {
-        unsigned long long d = i == R.prot_begin ? ppos[i] : ppos[i] - ppos[i - 1];
-        uint8_t* q = p + o + (prot_scan[i] - pb);
-        uint32_t k = put_uv(q, d);
-        q[k] = (uint8_t)(pval[i] & 0xff);
-        q[k + 1] = (uint8_t)(pval[i] >> 8);
-    }
-    o += prot_scan[R.prot_end] - pb;
+    o += prot_scan[R.prot_end] - prot_scan[R.prot_begin];  // entries: write_prot_kernel
     if (threadIdx.x == 0) put_uv(p + o, R.ngroups);
     o += uvlen(R.ngroups);
     // group offsets in ascending bucket order (codec.cpp:312-326)
@@ -880,7 +911,8 @@ __device__ __forceinline__ void put_bits(uint32_t* words, unsigned long long q,
 // laid out with the destination's bit phase, then copied out as whole 32-bit
 // words: interior words with plain stores, the two boundary words with
 // atomicOr (they may share bytes with neighbouring segments or headers).
-constexpr int kStageWords = 6144;  // 24 KiB staging per tile
+constexpr int kEmitWarps = 8;
+constexpr int kWarpStage = 1024;  // staged 32-bit words per warp (4 KiB)
 
 __device__ __forceinline__ void stage_bits(uint32_t* st, unsigned long long q,
                                            unsigned long long code, int len) {
@@ -894,141 +926,139 @@ __device__ __forceinline__ void stage_bits(uint32_t* st, unsigned long long q,
     }
 }
 
-__global__ void __launch_bounds__(kCB) enc_emit_kernel(EncArgs A, CodeTabs C,
-                                                       const unsigned long long* segoff,
-                                                       uint8_t* rec) {
-    __shared__ unsigned long long s_scan[33];
-    __shared__ uint32_t s_runbits[kTile + 1];
-    __shared__ uint32_t s_stage[kStageWords];
-    __shared__ uint32_t s_sw[kMaxB + 1];     // staging word base per segment
-    __shared__ uint32_t s_phase[kMaxB];
-    __shared__ unsigned long long s_dw[kMaxB];  // destination word of the segment start
-    __shared__ int s_overflow;
-    const int ti = blockIdx.x;
+// bits of run r (0 when it continues an earlier run)
+__device__ __forceinline__ uint32_t run_bits(const EncArgs& A, const CodeTabs& C, const Seg* segs,
+                                             const unsigned long long* runs, uint32_t tensor,
+                                             uint32_t r, uint32_t& b_out) {
+    uint32_t v, b;
+    unsigned long long L;
+    owned_run(A, segs, runs[r], r, v, b, L);
+    b_out = b;
+    if (!L) return 0;
+    const uint32_t tb = tensor * A.B + b;
+    unsigned long long c;
+    uint32_t l1, l2 = 0;
+    code_of(C, tb, A.NS, v, c, l1);
+    if (L > 1) code_of_len(C, tb, A.NS, A.B, L, c, l2);
+    return l1 + l2;
+}
+
+// E2b: emission, one warp per tile, warp-synchronous.  Each (tile, group)
+// segment owns a contiguous bit range of its group's stream; codes are packed
+// MSB-first into per-warp shared words laid out at the destination's bit phase,
+// then copied out as whole 32-bit words (the two boundary words with atomicOr,
+// since they can share bytes with neighbouring segments or headers).
+__global__ void __launch_bounds__(kEmitWarps * 32) enc_emit_kernel(EncArgs A, CodeTabs C,
+                                                                   const unsigned long long* segoff,
+                                                                   int ntiles, uint8_t* rec) {
+    __shared__ uint32_t s_stage[kEmitWarps][kWarpStage];
+    __shared__ uint32_t s_segbits[kEmitWarps][kMaxB];
+    __shared__ uint32_t s_segstart[kEmitWarps][kMaxB + 1];
+    __shared__ uint32_t s_sw[kEmitWarps][kMaxB + 1];
+    __shared__ uint32_t s_phase[kEmitWarps][kMaxB];
+    __shared__ unsigned long long s_dw[kEmitWarps][kMaxB];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ti = blockIdx.x * kEmitWarps + wid;
+    if (ti >= ntiles) return;
     const uint32_t B = A.B, NS = A.NS;
     const Tile T = A.tiles[ti];
     const uint32_t R = A.tile_nruns[ti];
     const Seg* segs = A.segs + (size_t)ti * B;
     const unsigned long long* runs = A.runs + (size_t)ti * kTile;
     uint32_t* words = (uint32_t*)rec;
-    const uint32_t r0 = threadIdx.x * kIt;
-    // pass 1: bits per run (blocked: thread owns runs [16t, 16t+16))
-    uint32_t mine = 0;
-    for (int j = 0; j < kIt; ++j) {
-        const uint32_t r = r0 + j;
-        if (r >= R) break;
-        uint32_t v, b;
-        unsigned long long L;
-        owned_run(A, segs, runs[r], r, v, b, L);
-        if (!L) continue;
-        const uint32_t tb = T.tensor * B + b;
-        unsigned long long c;
-        uint32_t l1, l2 = 0;
-        code_of(C, tb, NS, v, c, l1);
-        if (L > 1) code_of_len(C, tb, NS, B, L, c, l2);
-        mine += l1 + l2;
-    }
-    unsigned long long tot;
-    unsigned long long ex = block_exclusive_scan<unsigned long long>(mine, s_scan, &tot);
-    {
-        uint32_t acc = (uint32_t)ex;
-        for (int j = 0; j < kIt; ++j) {
-            const uint32_t r = r0 + j;
-            if (r >= R) break;
-            s_runbits[r] = acc;
-            uint32_t v, b;
-            unsigned long long L;
-            owned_run(A, segs, runs[r], r, v, b, L);
-            if (!L) continue;
-            const uint32_t tb = T.tensor * B + b;
-            unsigned long long c;
-            uint32_t l1, l2 = 0;
-            code_of(C, tb, NS, v, c, l1);
-            if (L > 1) code_of_len(C, tb, NS, B, L, c, l2);
-            acc += l1 + l2;
-        }
-        if (threadIdx.x == 0) s_runbits[R] = (uint32_t)tot;
-    }
-    __syncthreads();
-    // segment staging layout (one warp): words needed = ceil((phase + bits) / 32)
-    if (threadIdx.x < 32) {
-        uint32_t base = 0;
-        for (uint32_t b0 = 0; b0 < B; b0 += 32) {
-            const uint32_t b = b0 + threadIdx.x;
-            uint32_t nw = 0;
-            if (b < B) {
-                const Seg& S = segs[b];
-                uint32_t bits = S.n ? s_runbits[S.run_end] - s_runbits[S.run_begin] : 0u;
-                unsigned long long dest = 0;
-                if (bits) dest = C.gi[T.tensor * B + b].pay * 8 + segoff[(size_t)ti * B + b];
-                s_phase[b] = (uint32_t)(dest & 31);
-                s_dw[b] = dest >> 5;
-                nw = bits ? (s_phase[b] + bits + 31) / 32 : 0u;
-            }
-            uint32_t x = nw;
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if ((int)threadIdx.x >= o) x += y;
-            }
-            if (b < B) s_sw[b] = base + x - nw;
-            base += __shfl_sync(0xffffffffu, x, 31);
-        }
-        if (threadIdx.x == 0) {
-            s_sw[B] = base;
-            s_overflow = base > (uint32_t)kStageWords;
+    uint32_t* stage = s_stage[wid];
+    for (uint32_t b = lane; b < B; b += 32) s_segbits[wid][b] = 0;
+    __syncwarp();
+    // pass 1: bits per segment
+    for (uint32_t r0 = 0; r0 < R; r0 += 32) {
+        const uint32_t r = r0 + lane;
+        if (r < R) {
+            uint32_t b;
+            const uint32_t bits = run_bits(A, C, segs, runs, T.tensor, r, b);
+            if (bits) atomicAdd(&s_segbits[wid][b], bits);
         }
     }
-    __syncthreads();
-    const bool staged = !s_overflow;
-    const uint32_t nwords = s_sw[B];
+    __syncwarp();
+    // segment layout: tile-local start, destination word + phase, staging base
+    uint32_t tile_base = 0, stage_base = 0;
+    for (uint32_t b0 = 0; b0 < B; b0 += 32) {
+        const uint32_t b = b0 + lane;
+        uint32_t bits = 0, nw = 0;
+        if (b < B) {
+            bits = s_segbits[wid][b];
+            unsigned long long dest = 0;
+            if (bits) dest = C.gi[T.tensor * B + b].pay * 8 + segoff[(size_t)ti * B + b];
+            s_phase[wid][b] = (uint32_t)(dest & 31);
+            s_dw[wid][b] = dest >> 5;
+            nw = bits ? ((uint32_t)(dest & 31) + bits + 31) / 32 : 0u;
+        }
+        uint32_t xb = bits, xw = nw;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t yb = __shfl_up_sync(0xffffffffu, xb, o), yw = __shfl_up_sync(0xffffffffu, xw, o);
+            if (lane >= o) xb += yb, xw += yw;
+        }
+        if (b < B) {
+            s_segstart[wid][b] = tile_base + xb - bits;
+            s_sw[wid][b] = stage_base + xw - nw;
+        }
+        tile_base += __shfl_sync(0xffffffffu, xb, 31);
+        stage_base += __shfl_sync(0xffffffffu, xw, 31);
+    }
+    if (lane == 0) s_sw[wid][B] = stage_base;
+    const bool staged = stage_base <= (uint32_t)kWarpStage;
     if (staged)
-        for (uint32_t i = threadIdx.x; i < nwords; i += kCB) s_stage[i] = 0;
-    __syncthreads();
-    // pass 2: place codes
-    for (int j = 0; j < kIt; ++j) {
-        const uint32_t r = r0 + j;
-        if (r >= R) break;
-        uint32_t v, b;
-        unsigned long long L;
-        owned_run(A, segs, runs[r], r, v, b, L);
-        if (!L) continue;
+        for (uint32_t i = lane; i < stage_base; i += 32) stage[i] = 0;
+    __syncwarp();
+    // pass 2: place codes; a warp scan over each 32-run chunk gives tile offsets
+    uint32_t running = 0;
+    for (uint32_t r0 = 0; r0 < R; r0 += 32) {
+        const uint32_t r = r0 + lane;
+        uint32_t v = 0, b = 0;
+        unsigned long long L = 0;
+        if (r < R) owned_run(A, segs, runs[r], r, v, b, L);
+        uint32_t l1 = 0, l2 = 0;
+        unsigned long long c1 = 0, c2 = 0;
         const uint32_t tb = T.tensor * B + b;
-        const Seg& S = segs[b];
-        const uint32_t local = s_runbits[r] - s_runbits[S.run_begin];
-        unsigned long long c;
-        uint32_t l;
-        code_of(C, tb, NS, v, c, l);
-        if (staged) {
-            unsigned long long q = (unsigned long long)s_sw[b] * 32 + s_phase[b] + local;
-            stage_bits(s_stage, q, c, (int)l);
-            if (L > 1) {
-                q += l;
-                code_of_len(C, tb, NS, B, L, c, l);
-                stage_bits(s_stage, q, c, (int)l);
-            }
-        } else {  // very dense tile: straight to the record
-            unsigned long long q = C.gi[tb].pay * 8 + segoff[(size_t)ti * B + b] + local;
-            put_bits(words, q, c, (int)l);
-            if (L > 1) {
-                q += l;
-                code_of_len(C, tb, NS, B, L, c, l);
-                put_bits(words, q, c, (int)l);
+        if (L) {
+            code_of(C, tb, NS, v, c1, l1);
+            if (L > 1) code_of_len(C, tb, NS, B, L, c2, l2);
+        }
+        const uint32_t bits = l1 + l2;
+        uint32_t x = bits;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        const uint32_t tile_off = running + x - bits;
+        running += __shfl_sync(0xffffffffu, x, 31);
+        if (bits) {
+            const uint32_t local = tile_off - s_segstart[wid][b];
+            if (staged) {
+                unsigned long long q = (unsigned long long)s_sw[wid][b] * 32 + s_phase[wid][b] + local;
+                stage_bits(stage, q, c1, (int)l1);
+                if (l2) stage_bits(stage, q + l1, c2, (int)l2);
+            } else {
+                unsigned long long q = s_dw[wid][b] * 32 + s_phase[wid][b] + local;
+                put_bits(words, q, c1, (int)l1);
+                if (l2) put_bits(words, q + l1, c2, (int)l2);
             }
         }
     }
     if (!staged) return;
-    __syncthreads();
-    // pass 3: copy staged words to the record (big-endian bit order -> LE words)
-    for (uint32_t i = threadIdx.x; i < nwords; i += kCB) {
-        uint32_t b = 0;
-        while (b + 1 < B && s_sw[b + 1] <= i) ++b;
-        const uint32_t j = i - s_sw[b], nw = s_sw[b + 1] - s_sw[b];
-        const uint32_t v = __byte_perm(s_stage[i], 0, 0x0123);
-        uint32_t* dst = words + s_dw[b] + j;
+    __syncwarp();
+    // pass 3: copy staged words (big-endian bit order -> little-endian words)
+    uint32_t b = 0;
+    for (uint32_t i = lane; i < stage_base; i += 32) {
+        while (b + 1 < B && s_sw[wid][b + 1] <= i) ++b;
+        const uint32_t j = i - s_sw[wid][b], nw = s_sw[wid][b + 1] - s_sw[wid][b];
+        const uint32_t val = __byte_perm(stage[i], 0, 0x0123);
+        uint32_t* dst = words + s_dw[wid][b] + j;
         if (j == 0 || j + 1 == nw) {
-            if (v) atomicOr(dst, v);
+            if (val) atomicOr(dst, val);
         } else {
-            *dst = v;
+            *dst = val;
         }
     }
 }
@@ -1072,6 +1102,15 @@ static void init_crc_consts() {
 
 std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QState& target,
                                       double quality) {
+    return encode_record_ex(e, base, target, quality, 0, 0, nullptr);
+}
+
+// B_override / nt_total: a shard of a tensor-sharded checkpoint encodes its tensor
+// blocks with the global alphabet and writes the global tensor count, so the
+// bytes [body_offset, size-4) of every rank concatenate into the single-GPU record.
+std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QState& target,
+                                         double quality, uint32_t B_override, uint32_t nt_total,
+                                         uint64_t* body_offset) {
     const Layout& L = *target.L;
     if (base) {
         const Layout& BL = *base->L;
@@ -1084,6 +1123,10 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
     // codec.cpp:416-417
     uint32_t B = std::max(base ? base->max_levels() : 0u, target.max_levels());
     if (B == 0) B = 2;
+    if (B_override) {
+        DQTG_REQUIRE(B_override >= B, DQTG_ERROR, "alphabet override below the local alphabet");
+        B = B_override;
+    }
     DQTG_REQUIRE(B <= (uint32_t)kMaxB, DQTG_ERROR,
                  "cyclic alphabet larger than the device codec supports (64 levels)");
     init_crc_consts();
@@ -1122,8 +1165,9 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
             put_le(pre, u, 4);
         }
     }
-    put_le(pre, nt, 4);
+    put_le(pre, nt_total ? nt_total : nt, 4);
     const uint64_t prefix_len = pre.size();
+    if (body_offset) *body_offset = prefix_len;
     std::vector<TensorRec> trh(nt);
     std::vector<uint8_t> statics;
     for (uint32_t i = 0; i < nt; ++i) {
@@ -1179,7 +1223,7 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
     DQTG_CUDA(cudaMemsetAsync(small, 0, 64, st));
 
     // E1
-    const size_t e1_smem = (size_t)B * NS * 4 + (size_t)B * kWords * 6 + (size_t)kTile * 2 * 4 +
+    const size_t e1_smem = (size_t)((B * NS + 3) & ~3u) * 4 + (size_t)B * kWords * 6 + (size_t)kTile * 2 * 3 +
                            (kTile + 2) * 2 + 16;
     if (base) {
         DQTG_CUDA(cudaFuncSetAttribute(enc_tile_kernel<true>,
@@ -1213,10 +1257,12 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
                                                  st));
         void* tmp = e.buf("e.cubtmp", tb + 16);
         DQTG_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, A.ov, ov_sorted, (int64_t)n_ov, 0, 64, st));
-        auto* uhead = (unsigned long long*)e.buf("e.uhead", n_ov * 8 + 8);
-        { DQTG_SPAN(e, "ov_unique_kernel"); ov_unique_kernel<<<1, 1024, 0, st>>>(ov_sorted, n_ov, ukey, uhead, nu); }
-        { DQTG_SPAN(e, "ov_counts_kernel"); ov_counts_kernel<<<64, 256, 0, st>>>(uhead, nu, n_ov, ucnt); }
-        e.launched(2);
+        size_t tb2 = 0;
+        DQTG_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tb2, ov_sorted, ukey, ucnt, nu,
+                                                     (int64_t)n_ov, st));
+        void* tmp2 = e.buf("e.cubtmp3", tb2 + 16);
+        DQTG_CUDA(cub::DeviceRunLengthEncode::Encode(tmp2, tb2, ov_sorted, ukey, ucnt, nu,
+                                                     (int64_t)n_ov, st));
     } else {
         DQTG_CUDA(cudaMemsetAsync(nu, 0, 8, st));
     }
@@ -1276,7 +1322,8 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
     auto* tr = (TensorRec*)e.buf("e.tr", nt * sizeof(TensorRec));
     DQTG_CUDA(cudaMemcpyAsync(tr, trh.data(), nt * sizeof(TensorRec), cudaMemcpyHostToDevice, st));
     DQTG_CUDA(cudaMemsetAsync(psz, 0, (np + 1) * 8, st));
-    if (np) { DQTG_SPAN(e, "prot_sizes_kernel"); prot_sizes_kernel<<<nt, 256, 0, st>>>(tr, target.d_ppos, psz); }
+    const unsigned pgrid = (unsigned)std::min<uint64_t>((uint64_t)e.num_sms * 8, (np + 255) / 256 + 1);
+    if (np) { DQTG_SPAN(e, "prot_sizes_kernel"); prot_sizes_kernel<<<pgrid, 256, 0, st>>>(tr, nt, np, target.d_ppos, psz); }
     {
         size_t tb = 0;
         DQTG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, psz, pscan, (int64_t)(np + 1), st));
@@ -1301,7 +1348,8 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
     DQTG_CUDA(cudaMemcpyAsync(d_statics, statics.data(), statics.size(), cudaMemcpyHostToDevice, st));
     { DQTG_SPAN(e, "write_tensor_kernel"); write_tensor_kernel<<<nt, kCB, 0, st>>>(A, tr, d_statics, target.d_ppos, target.d_pval, pscan,
                                             gi, tab_sym, tab_len, rec->d_buf); }
-    { DQTG_SPAN(e, "enc_emit_kernel"); enc_emit_kernel<<<ntiles, kCB, 0, st>>>(A, C, segbits, rec->d_buf); }
+    if (np) { DQTG_SPAN(e, "write_prot_kernel"); write_prot_kernel<<<pgrid, 256, 0, st>>>(tr, nt, np, target.d_ppos, target.d_pval, pscan, rec->d_buf); }
+    { DQTG_SPAN(e, "enc_emit_kernel"); enc_emit_kernel<<<(ntiles + kEmitWarps - 1) / kEmitWarps, kEmitWarps * 32, 0, st>>>(A, C, segbits, ntiles, rec->d_buf); }
     { DQTG_SPAN(e, "finish_crc_kernel"); finish_crc_kernel<<<1, 1, 0, st>>>(A.crc_acc, 2 * L.N, rec->d_buf + total - 4, nullptr); }
     e.launched(3);
     DQTG_CUDA(cudaGetLastError());

@@ -135,6 +135,7 @@ struct Engine {
     std::vector<cudaEvent_t> event_pool;
     size_t ev_used = 0;
     cudaEvent_t take_event();
+    std::shared_ptr<void> pending;  // sharded quantize: state between stage 2 and 3
 
     ~Engine();
     void activate() const { DQTG_CUDA(cudaSetDevice(device)); }
@@ -187,6 +188,16 @@ void dequantize(Engine& e, const QState& q, float* out_dev_padded);
 void partition(Engine& e, const DevCkpt& c, const dqtg_config& cfg, uint8_t* const* masks);
 double proxy_quality(Engine& e, const DevCkpt& orig, const float* recon_dev_padded);
 void level_counts(Engine& e, const QState& q, uint64_t* counts, int lstride);
+uint64_t shard_hist_len(Engine& e, const dqtg_config& cfg, int which);
+void shard_stage1(Engine& e, const DevCkpt& c, const dqtg_config& cfg, unsigned long long* score_hist);
+void shard_stage2(Engine& e, const DevCkpt& c, const dqtg_config& cfg,
+                  const unsigned long long* score_hist, unsigned long long* value_hist);
+std::unique_ptr<QState> shard_stage3(Engine& e, const DevCkpt& c, const dqtg_config& cfg,
+                                     uint64_t seed, uint64_t step,
+                                     const unsigned long long* value_hist);
+std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QState& target,
+                                         double quality, uint32_t B_override, uint32_t nt_total,
+                                         uint64_t* body_offset);
 void eval_batch(Engine& e, const DevCkpt& c, const dqtg_config* cfgs, const uint64_t* seeds,
                 uint32_t m, double* quality, double* est);
 void approx_kmeans(Engine& e, const float* values_any, uint64_t n, uint32_t k, double sigma,

@@ -71,6 +71,38 @@ __device__ __forceinline__ void hist_flush(uint32_t* sh, unsigned long long* gh,
     }
 }
 
+// Non-negative inputs (derived scores |w|, |e*w|): a window of the zero bucket +
+// kWin positive buckets (half the shared memory of the signed window).
+constexpr int kPosSlots = kWin + 1;
+
+__device__ __forceinline__ void hist_add_pos(uint32_t* sh, unsigned long long* gh, float v,
+                                             const BucketTab& t, uint32_t* err) {
+    const uint32_t a = __float_as_uint(v);  // v >= +0 (fabs of a finite float) or NaN/Inf
+    if (a >= 0x7f800000u) {
+        atomicOr(err, kErrNonFinite);
+        return;
+    }
+    if (a < t.zbits) {
+        atomicAdd(sh, 1u);
+        return;
+    }
+    const int k = bucket_of(a, t);
+    const int d = k - (int)t.kw_lo;
+    if ((unsigned)d < (unsigned)kWin) atomicAdd(sh + 1 + d, 1u);
+    else atomicAdd(gh + (t.NB + 1 + k - t.kmin), 1ull);
+}
+
+__device__ __forceinline__ void hist_flush_pos(uint32_t* sh, unsigned long long* gh,
+                                               const BucketTab& t) {
+    for (int w = threadIdx.x; w < kPosSlots; w += blockDim.x) {
+        uint32_t c = sh[w];
+        if (!c) continue;
+        sh[w] = 0;
+        const int64_t idx = w == 0 ? t.NB : t.NB + 1 + (t.kw_lo + (w - 1)) - t.kmin;
+        atomicAdd(gh + idx, (unsigned long long)c);
+    }
+}
+
 __device__ __forceinline__ void hist_clear(uint32_t* sh) {
     for (int w = threadIdx.x; w < kWinSlots; w += blockDim.x) sh[w] = 0;
 }

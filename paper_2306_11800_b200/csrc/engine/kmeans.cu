@@ -75,25 +75,26 @@ struct KShared {
 
 // quantize.cpp:116-131: sequential prefix of prob (lane 0), binary search for the
 // first positive entry whose running sum reaches r.
-__device__ int kpp_pick(const double* prob, double* pref, int n, KShared& sm) {
+__device__ int kpp_pick(const double* prob, double* pref, int n, int from, KShared& sm) {
     if (threadIdx.x == 0) {
-        double s = 0.0;
-        int i = 0;
-        for (; i + 4 <= n; i += 4) {
-            double a = prob[i], b = prob[i + 1], c = prob[i + 2], d = prob[i + 3];
-            s = __dadd_rn(s, a);
-            pref[i] = s;
-            s = __dadd_rn(s, b);
-            pref[i + 1] = s;
-            s = __dadd_rn(s, c);
-            pref[i + 2] = s;
-            s = __dadd_rn(s, d);
-            pref[i + 3] = s;
+        // pref[0..from) are unchanged from the previous pick (same terms, same order)
+        double s = from > 0 ? pref[from - 1] : 0.0;
+        int i = from;
+        for (; i + 8 <= n; i += 8) {
+            double v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = prob[i + j];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                s = __dadd_rn(s, v[j]);
+                pref[i + j] = s;
+            }
         }
         for (; i < n; ++i) {
             s = __dadd_rn(s, prob[i]);
             pref[i] = s;
         }
+        if (n > 0) s = pref[n - 1];
         int res;
         if (!(s > 0.0)) {
             res = n;
@@ -135,17 +136,19 @@ __device__ double block_max_d(double v, KShared& sm) {
     return r;
 }
 
-// weighted_kmeanspp_init (quantize.cpp:94-164) for distinct points.
+// weighted_kmeanspp_init (quantize.cpp:94-164).
 __device__ void kpp_init(const double* pts, const double* w, int n, int k, double* d2,
                          double* prob, double* pref, double* chosen, KShared& sm) {
+    __shared__ int s_from;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         d2[i] = __longlong_as_double(0x7ff0000000000000LL);
         prob[i] = w[i];
     }
+    if (threadIdx.x == 0) s_from = 0;
     __syncthreads();
     int nc = 0;
     while (nc < k) {
-        int next = kpp_pick(prob, pref, n, sm);
+        int next = kpp_pick(prob, pref, n, s_from, sm);
         if (threadIdx.x == 0) {
             bool taken = false;
             if (next != n)
@@ -161,18 +164,29 @@ __device__ void kpp_init(const double* pts, const double* w, int n, int k, doubl
                 }
             }
             chosen[nc] = pts[next];
+            // the first pick used prob = w: every prob entry changes on the next pick
+            s_from = nc == 0 ? 0 : n;
         }
         __syncthreads();
         const double v = chosen[nc];
+        const bool first = nc == 0;
         ++nc;
+        int lo = n;
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             double dd = __dsub_rn(pts[i], v);
             double sq = __dmul_rn(dd, dd);
             double cur = d2[i];
-            cur = sq < cur ? sq : cur;  // std::min(d2, d*d)
-            d2[i] = cur;
-            prob[i] = __dmul_rn(w[i], cur);
+            if (sq < cur || first) {  // std::min(d2, d*d)
+                cur = sq < cur ? sq : cur;
+                d2[i] = cur;
+                double pn = __dmul_rn(w[i], cur);
+                if (first || pn != prob[i] || __double_as_longlong(pn) != __double_as_longlong(prob[i])) {
+                    prob[i] = pn;
+                    lo = min(lo, i);
+                }
+            }
         }
+        if (lo < n) atomicMin(&s_from, lo);
         __syncthreads();
     }
     if (threadIdx.x == 0) IntroSort<double, LessD>{}.sort(chosen, k);
@@ -189,36 +203,89 @@ __device__ int lloyd_block(const double* pts, const double* w, int n, double* c,
     double scale = block_max_d(lm, sm);
     if (scale == 0.0) scale = 1.0;
     int iters = 0;
+    __shared__ int s_fast;
     for (int it = 0; it < max_iter; ++it) {
-        for (int j = threadIdx.x; j < k; j += blockDim.x) {
-            first[j] = 0x7fffffff;
-            last[j] = -1;
-            cnt[j] = 0;
+        if (threadIdx.x == 0) {
+            // Fast path: strictly ascending centres separated by far more than the
+            // rounding of any |x - c| (gap > scale * 2^-40).  The distance sequence
+            // over j is then strictly unimodal for every x, so the reference argmin
+            // (strict <, lowest index on ties) is decided by neighbouring centres and
+            // each cluster is the key range between two monotone boundaries.
+            bool fast = true;
+            const double gap = __dmul_rn(scale, 0x1.0p-40);
+            for (int j = 0; j + 1 < k; ++j)
+                if (!(__dsub_rn(c[j + 1], c[j]) > gap)) fast = false;
+            s_fast = fast;
+            sm.any_empty = 0;
         }
-        if (threadIdx.x == 0) sm.any_empty = 0;
         __syncthreads();
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            double x = pts[i];
-            int best = 0;
-            double bd = fabs(__dsub_rn(x, c[0]));
-            for (int j = 1; j < k; ++j) {
-                double d = fabs(__dsub_rn(x, c[j]));
-                if (d < bd) {
-                    bd = d;
-                    best = j;
+        if (s_fast) {
+            // start of cluster j+1 = first key whose distance to c[j+1] is < to c[j]
+            for (int j = threadIdx.x; j < k; j += blockDim.x) {
+                int lo = n, hi = n;  // last cluster ends at n
+                if (j + 1 < k) {
+                    lo = 0;
+                    const double a = c[j], b = c[j + 1];
+                    while (lo < hi) {
+                        int mid = (lo + hi) >> 1;
+                        double x = pts[mid];
+                        if (fabs(__dsub_rn(x, b)) < fabs(__dsub_rn(x, a))) hi = mid;
+                        else lo = mid + 1;
+                    }
                 }
+                last[j] = lo;  // exclusive end of cluster j (temporarily)
             }
-            assign[i] = best;
-            atomicMin(&first[best], i);
-            atomicMax(&last[best], i);
-            atomicAdd(&cnt[best], 1);
+            __syncthreads();
+            for (int j = threadIdx.x; j < k; j += blockDim.x) {
+                const int b0 = j ? last[j - 1] : 0, b1 = last[j];
+                first[j] = b0;
+                cnt[j] = b1 > b0 ? b1 - b0 : 0;
+            }
+            __syncthreads();
+            for (int j = threadIdx.x; j < k; j += blockDim.x) last[j] = first[j] + cnt[j] - 1;
+            __syncthreads();
+        } else {
+            for (int j = threadIdx.x; j < k; j += blockDim.x) {
+                first[j] = 0x7fffffff;
+                last[j] = -1;
+                cnt[j] = 0;
+            }
+            __syncthreads();
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                double x = pts[i];
+                int best = 0;
+                double bd = fabs(__dsub_rn(x, c[0]));
+                for (int j = 1; j < k; ++j) {
+                    double d = fabs(__dsub_rn(x, c[j]));
+                    if (d < bd) {
+                        bd = d;
+                        best = j;
+                    }
+                }
+                assign[i] = best;
+                atomicMin(&first[best], i);
+                atomicMax(&last[best], i);
+                atomicAdd(&cnt[best], 1);
+            }
+            __syncthreads();
         }
-        __syncthreads();
         for (int j = threadIdx.x; j < k; j += blockDim.x) {
             double ws = 0.0, wxs = 0.0;
             if (cnt[j] > 0) {
                 if (last[j] - first[j] + 1 == cnt[j]) {
-                    for (int i = first[j]; i <= last[j]; ++i) {
+                    int i = first[j];
+                    const int e = last[j] + 1;
+                    for (; i + 8 <= e; i += 8) {
+                        double wv[8], xv[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) wv[u] = w[i + u], xv[u] = pts[i + u];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            ws = __dadd_rn(ws, wv[u]);
+                            wxs = __dadd_rn(wxs, __dmul_rn(wv[u], xv[u]));
+                        }
+                    }
+                    for (; i < e; ++i) {
                         double wi = w[i];
                         ws = __dadd_rn(ws, wi);
                         wxs = __dadd_rn(wxs, __dmul_rn(wi, pts[i]));
@@ -311,7 +378,15 @@ __device__ double sq_loss_block(const double* pts, const double* w, int n, const
     __syncthreads();
     if (threadIdx.x == 0) {
         double loss = 0.0;
-        for (int i = 0; i < n; ++i) loss = __dadd_rn(loss, tmp[i]);
+        int i = 0;
+        for (; i + 8 <= n; i += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = tmp[i + u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) loss = __dadd_rn(loss, v[u]);
+        }
+        for (; i < n; ++i) loss = __dadd_rn(loss, tmp[i]);
         sm.red[0] = loss;
     }
     __syncthreads();
@@ -321,7 +396,7 @@ __device__ double sq_loss_block(const double* pts, const double* w, int n, const
 }
 
 __global__ void __launch_bounds__(kKB) kmeans_restarts_kernel(const KProblem* probs,
-                                                              int restarts) {
+                                                              int restarts, int smem_n) {
     extern __shared__ double dsm[];
     __shared__ KShared sm;
     const KProblem& P = probs[blockIdx.x / restarts];
@@ -333,16 +408,35 @@ __global__ void __launch_bounds__(kKB) kmeans_restarts_kernel(const KProblem* pr
     int* first = (int*)(nx + k);
     int* last = first + k;
     int* cnt = last + k;
-    double* d2 = P.scratch + (size_t)t * P.scratch_stride;
-    double* prob = d2 + n;
-    double* pref = prob + n;
-    int* assign = (int*)(pref + n);
+    double* base = dsm + 2 * k + (3 * k + 1) / 2 + 1;
+    const double *pts = P.pts, *w = P.w;
+    double *d2, *prob, *pref;
+    int* assign;
+    if (n <= smem_n) {  // working set in shared memory: the serial chains hit LDS, not L2
+        double* sp = base;
+        double* sw = sp + n;
+        d2 = sw + n;
+        prob = d2 + n;
+        pref = prob + n;
+        assign = (int*)(pref + n);
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            sp[i] = P.pts[i];
+            sw[i] = P.w[i];
+        }
+        pts = sp;
+        w = sw;
+    } else {
+        d2 = P.scratch + (size_t)t * P.scratch_stride;
+        prob = d2 + n;
+        pref = prob + n;
+        assign = (int*)(pref + n);
+    }
     ScoreVal* top = (ScoreVal*)d2;  // reseed scratch reuses d2/prob (2n doubles)
     if (threadIdx.x == 0) mt64_seed(sm.rng, P.seed + (uint64_t)t);
     __syncthreads();
-    kpp_init(P.pts, P.w, n, k, d2, prob, pref, c, sm);
-    lloyd_block(P.pts, P.w, n, c, nx, first, last, cnt, k, 1e-6, 100, assign, pref, top, true, sm);
-    double loss = sq_loss_block(P.pts, P.w, n, c, k, prob, sm);
+    kpp_init(pts, w, n, k, d2, prob, pref, c, sm);
+    lloyd_block(pts, w, n, c, nx, first, last, cnt, k, 1e-6, 100, assign, pref, top, true, sm);
+    double loss = sq_loss_block(pts, w, n, c, k, prob, sm);
     for (int j = threadIdx.x; j < k; j += blockDim.x) P.centers[(size_t)t * k + j] = c[j];
     if (threadIdx.x == 0) P.loss[t] = loss;
 }
@@ -396,12 +490,15 @@ void run_kmeans(Engine& e, std::vector<KProblem>& probs, float* cb_out, int cb_s
     KProblem* dp = (KProblem*)e.buf("km.probs", probs.size() * sizeof(KProblem));
     DQTG_CUDA(cudaMemcpyAsync(dp, probs.data(), probs.size() * sizeof(KProblem),
                               cudaMemcpyHostToDevice, e.stream));
-    size_t smem = (size_t)maxk * (2 * 8 + 3 * 4) + 16;
-    if (smem > 48 * 1024)
-        DQTG_CUDA(cudaFuncSetAttribute(kmeans_restarts_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    { DQTG_SPAN(e, "kmeans_restarts_kernel"); kmeans_restarts_kernel<<<(unsigned)(probs.size() * restarts), kKB, smem, e.stream>>>(dp,
-                                                                                      restarts); }
+    int maxn = 1;
+    for (auto& p : probs) maxn = std::max(maxn, p.n);
+    const size_t head = ((size_t)2 * maxk + (3 * maxk + 1) / 2 + 1) * 8;
+    const size_t budget = 200 * 1024;
+    int smem_n = (int)((budget - std::min(budget, head)) / 44);  // 5 doubles + 1 int per key
+    size_t smem = head + (size_t)std::min(maxn, smem_n) * 44 + 64;
+    DQTG_CUDA(cudaFuncSetAttribute(kmeans_restarts_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    { DQTG_SPAN(e, "kmeans_restarts_kernel"); kmeans_restarts_kernel<<<(unsigned)(probs.size() * restarts), kKB, smem, e.stream>>>(dp, restarts, smem_n); }
     { DQTG_SPAN(e, "kmeans_select_kernel"); kmeans_select_kernel<<<(unsigned)probs.size(), 32, 0, e.stream>>>(dp, restarts, cb_out,
                                                                        cb_stride, cb_len_dev); }
     e.launched(2);

@@ -57,33 +57,42 @@ __device__ __forceinline__ void load_scores(const PassIn& a, uint64_t idx, const
 }
 
 // ---- pass A: score histograms ----------------------------------------------
+// Derived scores are non-negative: half-size windows (kPosSlots) per histogram.
 template <bool EXPL>
 __global__ void __launch_bounds__(kPB) pass_a_kernel(PassIn a, unsigned long long* gh_mag,
                                                      unsigned long long* gh_sens,
                                                      uint32_t mask_mag, uint32_t mask_sens) {
     extern __shared__ uint32_t sh[];
+    constexpr int W = EXPL ? kWinSlots : kPosSlots;
     uint32_t* shm = sh;
-    uint32_t* shs = sh + kWinSlots;
-    hist_clear(shm);
-    hist_clear(shs);
+    uint32_t* shs = sh + W;
+    for (int i = threadIdx.x; i < 2 * W; i += blockDim.x) sh[i] = 0;
     __syncthreads();
     const int t0 = (int)((int64_t)blockIdx.x * a.ntiles / gridDim.x);
     const int t1 = (int)((int64_t)(blockIdx.x + 1) * a.ntiles / gridDim.x);
     int cur = -1;
+    auto flush = [&](int lt) {
+        if (EXPL) {
+            hist_flush(shm, gh_mag + lt * a.HS, a.tab);
+            hist_flush(shs, gh_sens + lt * a.HS, a.tab);
+        } else {
+            hist_flush_pos(shm, gh_mag + lt * a.HS, a.tab);
+            hist_flush_pos(shs, gh_sens + lt * a.HS, a.tab);
+        }
+    };
     for (int ti = t0; ti < t1; ++ti) {
         const Tile T = a.tiles[ti];
         const int lt = a.types[T.tensor];
         if (lt != cur) {
             __syncthreads();
-            if (cur >= 0) {
-                hist_flush(shm, gh_mag + cur * a.HS, a.tab);
-                hist_flush(shs, gh_sens + cur * a.HS, a.tab);
-            }
+            if (cur >= 0) flush(cur);
             __syncthreads();
             cur = lt;
         }
         const bool dm = (mask_mag >> lt) & 1, ds = (mask_sens >> lt) & 1;
         if (!dm && !ds) continue;
+        unsigned long long* gm = gh_mag + lt * a.HS;
+        unsigned long long* gs = gh_sens + lt * a.HS;
         for (uint32_t i = threadIdx.x * 4; i < T.count; i += kPB * 4) {
             const uint64_t idx = T.start + i;
             float4 wv = ld4(a.w + idx);
@@ -92,16 +101,18 @@ __global__ void __launch_bounds__(kPB) pass_a_kernel(PassIn a, unsigned long lon
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 if (i + j >= T.count) break;
-                if (dm) hist_add(shm, gh_mag + lt * a.HS, m[j], a.tab, a.err);
-                if (ds) hist_add(shs, gh_sens + lt * a.HS, s[j], a.tab, a.err);
+                if (EXPL) {
+                    if (dm) hist_add(shm, gm, m[j], a.tab, a.err);
+                    if (ds) hist_add(shs, gs, s[j], a.tab, a.err);
+                } else {
+                    if (dm) hist_add_pos(shm, gm, m[j], a.tab, a.err);
+                    if (ds) hist_add_pos(shs, gs, s[j], a.tab, a.err);
+                }
             }
         }
     }
     __syncthreads();
-    if (cur >= 0) {
-        hist_flush(shm, gh_mag + cur * a.HS, a.tab);
-        hist_flush(shs, gh_sens + cur * a.HS, a.tab);
-    }
+    if (cur >= 0) flush(cur);
 }
 
 // ---- quantile thresholds (sketch.cpp:59-77) --------------------------------
@@ -577,16 +588,16 @@ static void stage_pass_a(Engine& e, const DevCkpt& c, const PassIn& a, uint32_t 
                          uint32_t mask_sens, unsigned long long* gh_mag,
                          unsigned long long* gh_sens) {
     const int ntiles = a.ntiles;
-    const size_t smem = (size_t)2 * kWinSlots * 4;
-    int grid = stream_grid(e, ntiles, 3);
     cudaStream_t st = e.stream;
     if (c.explicit_scores) {
+        const size_t smem = (size_t)2 * kWinSlots * 4;
+        const int grid = stream_grid(e, ntiles, 3);
         DQTG_CUDA(cudaFuncSetAttribute(pass_a_kernel<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         { DQTG_SPAN(e, "pass_a_kernel"); pass_a_kernel<true><<<grid, kPB, smem, st>>>(a, gh_mag, gh_sens, mask_mag, mask_sens); }
     } else {
-        DQTG_CUDA(cudaFuncSetAttribute(pass_a_kernel<false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const size_t smem = (size_t)2 * kPosSlots * 4;
+        const int grid = stream_grid(e, ntiles, 6);
         { DQTG_SPAN(e, "pass_a_kernel"); pass_a_kernel<false><<<grid, kPB, smem, st>>>(a, gh_mag, gh_sens, mask_mag, mask_sens); }
     }
     e.launched();
@@ -608,8 +619,19 @@ static void stage_thresholds(Engine& e, Stage& s, int64_t HS, const AlphaTables&
     e.launched();
 }
 
+static void stage_keys(Engine& e, const Layout& L, Stage& s, const AlphaTables& T) {
+    const int64_t HS = T.HS;
+    cudaStream_t st = e.stream;
+    compact_keys(e, s.gh_val, HS, HS, T.d_key, s.cfg.sigma, kLayerTypes, s.pts, s.kc, s.kw, HS,
+                 s.n_keys);
+    s.h_tprot.resize(L.nt + 1);
+    DQTG_CUDA(cudaMemcpyAsync(s.h_nkeys, s.n_keys, sizeof(s.h_nkeys), cudaMemcpyDeviceToHost, st));
+    DQTG_CUDA(cudaMemcpyAsync(s.h_tprot.data(), s.tensor_prot, (L.nt + 1) * 8,
+                              cudaMemcpyDeviceToHost, st));
+}
+
 static void stage_pass_b(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s,
-                         const AlphaTables& T) {
+                         const AlphaTables& T, bool keys = true) {
     const Layout& L = *c.L;
     const int ntiles = a.ntiles;
     const int64_t HS = T.HS;
@@ -618,18 +640,16 @@ static void stage_pass_b(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s,
     DQTG_CUDA(cudaMemsetAsync(s.tensor_prot, 0, (size_t)(L.nt + 1) * 8, st));
     const size_t smem = (size_t)kWinSlots * 4;
     int grid = stream_grid(e, ntiles, 6);
-    if (c.explicit_scores)
-        { DQTG_SPAN(e, "pass_b_kernel"); pass_b_kernel<true><<<grid, kPB, smem, st>>>(a, s.d_lp, s.gh_val, s.tile_prot, s.tensor_prot); }
-    else
-        { DQTG_SPAN(e, "pass_b_kernel"); pass_b_kernel<false><<<grid, kPB, smem, st>>>(a, s.d_lp, s.gh_val, s.tile_prot, s.tensor_prot); }
+    if (ntiles) {
+        if (c.explicit_scores)
+            { DQTG_SPAN(e, "pass_b_kernel"); pass_b_kernel<true><<<grid, kPB, smem, st>>>(a, s.d_lp, s.gh_val, s.tile_prot, s.tensor_prot); }
+        else
+            { DQTG_SPAN(e, "pass_b_kernel"); pass_b_kernel<false><<<grid, kPB, smem, st>>>(a, s.d_lp, s.gh_val, s.tile_prot, s.tensor_prot); }
+        e.launched();
+    }
     { DQTG_SPAN(e, "scan_u32_kernel"); scan_u32_kernel<<<1, 1024, 0, st>>>(s.tile_prot, ntiles, s.tile_off); }
-    e.launched(2);
-    compact_keys(e, s.gh_val, HS, HS, T.d_key, s.cfg.sigma, kLayerTypes, s.pts, s.kc, s.kw, HS,
-                 s.n_keys);
-    s.h_tprot.resize(L.nt + 1);
-    DQTG_CUDA(cudaMemcpyAsync(s.h_nkeys, s.n_keys, sizeof(s.h_nkeys), cudaMemcpyDeviceToHost, st));
-    DQTG_CUDA(cudaMemcpyAsync(s.h_tprot.data(), s.tensor_prot, (L.nt + 1) * 8,
-                              cudaMemcpyDeviceToHost, st));
+    e.launched();
+    if (keys) stage_keys(e, L, s, T);
 }
 
 // After a sync: codebooks of every stage (all k-means problems in one launch).
@@ -753,6 +773,98 @@ std::unique_ptr<QState> quantize(Engine& e, const DevCkpt& c, const dqtg_config&
     for (int lt = 0; lt < kLayerTypes; ++lt)
         q->cb[lt].assign(hcb.begin() + (size_t)lt * q->cb_stride,
                          hcb.begin() + (size_t)lt * q->cb_stride + q->cb_len[lt]);
+    return q;
+}
+
+// ---- sharded quantization: the two histogram exchange points -----------------
+// stage 1: score histograms [2][7][HS] (magnitude, sensitivity) of this shard
+// stage 2: thresholds from the globally reduced score histograms, pass B ->
+//          value histograms [7][HS] of this shard
+// stage 3: codebooks from the globally reduced value histograms (identical on
+//          every rank), pass C -> this shard's quantized state
+uint64_t shard_hist_len(Engine& e, const dqtg_config& cfg, int which) {
+    AlphaTables& T = e.alpha_tables(cfg.alpha);
+    return (uint64_t)(which == 0 ? 2 : 1) * kLayerTypes * (uint64_t)T.HS;
+}
+
+void shard_stage1(Engine& e, const DevCkpt& c, const dqtg_config& cfg,
+                  unsigned long long* score_hist) {
+    QuantPlan plan;
+    quantize_plan(*c.L, cfg, c.has_sens, plan);
+    AlphaTables& T = e.alpha_tables(cfg.alpha);
+    DQTG_CUDA(cudaMemsetAsync(score_hist, 0, (size_t)2 * kLayerTypes * T.HS * 8, e.stream));
+    if (c.L->N == 0 || plan.jobs.empty()) return;
+    PassIn a = pass_in(e, c, T, (int)cfg.metric);
+    stage_pass_a(e, c, a, plan.mask_mag, plan.mask_sens, score_hist,
+                 score_hist + (size_t)kLayerTypes * T.HS);
+}
+
+void shard_stage2(Engine& e, const DevCkpt& c, const dqtg_config& cfg,
+                  const unsigned long long* score_hist, unsigned long long* value_hist) {
+    const Layout& L = *c.L;
+    auto s = std::make_unique<Stage>();
+    s->tag = "sh.";
+    s->cfg = cfg;
+    quantize_plan(L, cfg, c.has_sens, s->plan);
+    AlphaTables& T = e.alpha_tables(cfg.alpha);
+    stage_alloc(e, L, T.HS, *s, nullptr);
+    s->gh_val = value_hist;
+    stage_thresholds(e, *s, T.HS, T, const_cast<unsigned long long*>(score_hist),
+                     const_cast<unsigned long long*>(score_hist) + (size_t)kLayerTypes * T.HS);
+    PassIn a = pass_in(e, c, T, (int)cfg.metric);
+    stage_pass_b(e, c, a, *s, T, false);
+    e.pending = std::shared_ptr<void>(s.release(), [](void* p) { delete (Stage*)p; });
+}
+
+std::unique_ptr<QState> shard_stage3(Engine& e, const DevCkpt& c, const dqtg_config& cfg,
+                                     uint64_t seed, uint64_t step,
+                                     const unsigned long long* value_hist) {
+    DQTG_REQUIRE(e.pending, DQTG_ERROR, "quantize stage 3 without stage 2");
+    Stage& s = *(Stage*)e.pending.get();
+    const Layout& L = *c.L;
+    AlphaTables& T = e.alpha_tables(cfg.alpha);
+    s.gh_val = const_cast<unsigned long long*>(value_hist);
+    s.seed = seed;
+    stage_keys(e, L, s, T);
+    auto q = std::make_unique<QState>();
+    q->eng = &e;
+    q->L = c.L;
+    q->step = step;
+    q->cfg = cfg;
+    q->cb_stride = s.cb_stride;
+    q->d_levels = (uint16_t*)e.dalloc(L.Np * 2);
+    q->d_cb = (float*)e.dalloc((size_t)kLayerTypes * q->cb_stride * 4);
+    e.check_err();
+    for (int lt = 0; lt < kLayerTypes; ++lt) {
+        const uint32_t k = lt == kEmbedding ? cfg.embed_bins : cfg.bins;
+        DQTG_REQUIRE(s.h_nkeys[lt] == 0 || (uint32_t)s.h_nkeys[lt] >= k, DQTG_ERROR,
+                     "distinct-value codebook fallback needs all shards' values (unsupported "
+                     "when sharded)");
+    }
+    std::vector<Stage*> v{&s};
+    PassIn a = pass_in(e, c, T, (int)cfg.metric);
+    s.d_cb = q->d_cb;
+    stage_codebooks(e, v, a, T.HS);
+    q->prot_count.assign(L.nt, 0);
+    q->prot_off.assign(L.nt + 1, 0);
+    uint64_t acc = 0;
+    for (uint32_t i = 0; i < L.nt; ++i) {
+        q->prot_off[i] = acc;
+        q->prot_count[i] = s.h_tprot[i];
+        acc += s.h_tprot[i];
+    }
+    q->prot_off[L.nt] = q->prot_total = acc;
+    q->d_ppos = (uint64_t*)e.dalloc((acc + 1) * 8);
+    q->d_pval = (uint16_t*)e.dalloc((acc + 1) * 2);
+    if (L.N) stage_pass_c(e, c, a, s, *q);
+    std::vector<float> hcb((size_t)kLayerTypes * q->cb_stride);
+    DQTG_CUDA(cudaMemcpyAsync(q->cb_len, s.cb_len, sizeof(q->cb_len), cudaMemcpyDeviceToHost, e.stream));
+    DQTG_CUDA(cudaMemcpyAsync(hcb.data(), q->d_cb, hcb.size() * 4, cudaMemcpyDeviceToHost, e.stream));
+    e.check_err();
+    for (int lt = 0; lt < kLayerTypes; ++lt)
+        q->cb[lt].assign(hcb.begin() + (size_t)lt * q->cb_stride,
+                         hcb.begin() + (size_t)lt * q->cb_stride + q->cb_len[lt]);
+    e.pending.reset();
     return q;
 }
 

@@ -1,0 +1,144 @@
+"""Tensor-sharded compress + delta-encode across the GPUs of one box.
+
+One process per GPU (torchrun), NCCL for the only two real exchanges of the path:
+the score histograms (pass A) and the QUANTIZE-value histograms (pass B) must be
+global so that every rank derives the same thresholds and codebooks
+(``torch.distributed.all_reduce`` of u64 counts, exact and order independent).
+After that each rank quantizes and encodes its own tensors; the record of the
+whole checkpoint is the rank-0 prefix, the ranks' tensor blocks in tensor order,
+and the CRC-32 combined from the per-rank CRCs (zlib ``crc32_combine`` rule) —
+byte-identical to the single-GPU record.
+
+The host-side pieces (``plan_shards``, ``crc32_combine``, ``assemble_record``)
+are plain Python and are exercised with the gloo backend on CPU in
+tests/test_distributed_cpu.py.
+"""
+from __future__ import annotations
+
+import struct
+
+import numpy as np
+
+_POLY = 0xEDB88320
+
+
+def _gf2_mult(a, b):
+    p = 0
+    m = 1 << 31
+    while True:
+        if a & m:
+            p ^= b
+            if (a & (m - 1)) == 0:
+                break
+        m >>= 1
+        b = (b >> 1) ^ _POLY if b & 1 else b >> 1
+    return p
+
+
+_X2N = [1 << 30]
+for _k in range(1, 32):
+    _X2N.append(_gf2_mult(_X2N[-1], _X2N[-1]))
+
+
+def _x2nmodp(n, k):
+    p = 1 << 31
+    while n:
+        if n & 1:
+            p = _gf2_mult(_X2N[k & 31], p)
+        n >>= 1
+        k += 1
+    return p
+
+
+def crc32_combine(crc1: int, crc2: int, len2: int) -> int:
+    """CRC-32 of A||B from crc(A), crc(B), len(B) (GF(2) shift by 8*len2 bits)."""
+    if len2 == 0:
+        return crc1
+    return _gf2_mult(_x2nmodp(len2, 3), crc1) ^ crc2
+
+
+def plan_shards(numel, world):
+    """Contiguous tensor ranges per rank, greedily balanced by element count.
+
+    Contiguity keeps every rank's record blocks a contiguous slice of the record."""
+    numel = [int(n) for n in numel]
+    total = sum(numel)
+    bounds, start, acc = [], 0, 0
+    for r in range(world):
+        target = total * (r + 1) / world
+        end = start
+        while end < len(numel) and (r == world - 1 or acc + numel[end] / 2 <= target):
+            acc += numel[end]
+            end += 1
+        bounds.append((start, end))
+        start = end
+    return bounds
+
+
+def assemble_record(prefix: bytes, bodies, crcs, stream_lens) -> bytes:
+    """Full DQDR record from rank 0's prefix and every rank's (body, crc, level-stream bytes)."""
+    crc = None
+    for c, n in zip(crcs, stream_lens):
+        crc = c if crc is None else crc32_combine(crc, c, n)
+    return bytes(prefix) + b"".join(bytes(b) for b in bodies) + struct.pack("<I", crc or 0)
+
+
+def compress_sharded(engine, ckpt, cfg, seed, step, base_state, *, group=None, device=None,
+                     quality=0.0, n_tensors_total=None, gather_record=False):
+    """One compress+delta step of a tensor-sharded checkpoint.
+
+    ``ckpt`` holds this rank's tensors.  Returns (state, record_bytes_or_None,
+    stats): the state stays on this GPU for the next step; with
+    ``gather_record`` rank 0 receives the assembled record."""
+    import torch
+    import torch.distributed as dist
+
+    from . import engine as E
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    n_s = engine.shard_hist_len(cfg, 0)
+    n_v = engine.shard_hist_len(cfg, 1)
+    score = torch.empty(n_s, dtype=torch.int64, device=dev)
+    value = torch.empty(n_v, dtype=torch.int64, device=dev)
+    engine.shard_stage1(ckpt, cfg, score.data_ptr())
+    engine.sync()
+    if world > 1:
+        dist.all_reduce(score, group=group)
+    engine.shard_stage2(ckpt, cfg, score.data_ptr(), value.data_ptr())
+    engine.sync()
+    if world > 1:
+        dist.all_reduce(value, group=group)
+    state = engine.shard_stage3(ckpt, cfg, seed, step, value.data_ptr())
+    # global alphabet and tensor count
+    info = state.info()
+    lv = [info.max_levels, base_state.info().max_levels if base_state is not None else 0]
+    meta = torch.tensor([max(lv), len(ckpt.meta.names)], dtype=torch.int64, device=dev)
+    if world > 1:
+        mx = meta[:1].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
+        cnt = meta[1:].clone()
+        dist.all_reduce(cnt, group=group)
+        meta = torch.cat([mx, cnt])
+    gB = max(2, int(meta[0]))
+    gnt = int(meta[1]) if n_tensors_total is None else n_tensors_total
+    rec, body_off = engine.encode_record_shard(state, base_state, quality, gB, gnt)
+    size = E.LIB.dqtg_record_size(rec)
+    stats = {"record_bytes_local": size, "body_offset": body_off, "B": gB}
+    out = None
+    if gather_record:
+        buf = np.empty(size, np.uint8)
+        E._check(E.LIB.dqtg_record_copy(rec, buf.ctypes.data))
+        body = buf[body_off:size - 4].tobytes()
+        crc = struct.unpack("<I", buf[size - 4:].tobytes())[0]
+        stream = 2 * int(info.param_count)
+        parts = [None] * world
+        if world > 1:
+            dist.all_gather_object(parts, (body, crc, stream), group=group)
+        else:
+            parts = [(body, crc, stream)]
+        if not dist.is_initialized() or dist.get_rank(group) == 0:
+            out = assemble_record(buf[:body_off].tobytes(), [p[0] for p in parts],
+                                  [p[1] for p in parts], [p[2] for p in parts])
+    E.LIB.dqtg_record_destroy(rec)
+    return state, out, stats

@@ -112,6 +112,14 @@ def _load():
         "dqtg_compress_step": (C.c_int, [_P, _P, C.POINTER(Config), C.c_uint64, C.c_uint64, _P,
                                          C.c_double, C.POINTER(_P), C.POINTER(_P)]),
         "dqtg_eval_batch": (C.c_int, [_P, _P, _P, _P, C.c_uint32, _P, _P]),
+        "dqtg_partition": (C.c_int, [_P, _P, C.POINTER(Config), _P]),
+        "dqtg_shard_hist_len": (C.c_uint64, [_P, C.POINTER(Config), C.c_int]),
+        "dqtg_shard_stage1": (C.c_int, [_P, _P, C.POINTER(Config), _P]),
+        "dqtg_shard_stage2": (C.c_int, [_P, _P, C.POINTER(Config), _P, _P]),
+        "dqtg_shard_stage3": (C.c_int, [_P, _P, C.POINTER(Config), C.c_uint64, C.c_uint64, _P,
+                                        C.POINTER(_P)]),
+        "dqtg_encode_record_shard": (C.c_int, [_P, _P, _P, C.c_double, C.c_uint32, C.c_uint32,
+                                               C.POINTER(_P), C.POINTER(C.c_uint64)]),
         "dqtg_approx_kmeans": (C.c_int, [_P, _P, C.c_uint64, C.c_uint32, C.c_double, C.c_double,
                                          C.c_uint64, _P, C.POINTER(C.c_uint32)]),
         "dqtg_kmeanspp_init": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint64, _P]),
@@ -375,6 +383,45 @@ class Engine:
                                       None if base is None else base.h, quality, C.byref(s),
                                       C.byref(r)))
         return DevState(self, s, ckpt.meta), r
+
+    # -- tensor-sharded quantization (multi-GPU) ------------------------------------
+    def shard_hist_len(self, cfg, which):
+        return LIB.dqtg_shard_hist_len(self.h, C.byref(cfg), which)
+
+    def shard_stage1(self, ckpt, cfg, score_hist_dev):
+        _check(LIB.dqtg_shard_stage1(self.h, ckpt.h, C.byref(cfg), score_hist_dev))
+
+    def shard_stage2(self, ckpt, cfg, score_hist_dev, value_hist_dev):
+        _check(LIB.dqtg_shard_stage2(self.h, ckpt.h, C.byref(cfg), score_hist_dev, value_hist_dev))
+
+    def shard_stage3(self, ckpt, cfg, seed, step, value_hist_dev) -> DevState:
+        h = _P()
+        _check(LIB.dqtg_shard_stage3(self.h, ckpt.h, C.byref(cfg), seed, step, value_hist_dev,
+                                     C.byref(h)))
+        return DevState(self, h, ckpt.meta)
+
+    def encode_record_shard(self, target, base, quality, global_B, global_tensors):
+        """Returns (record handle, body_offset)."""
+        r, off = _P(), C.c_uint64()
+        _check(LIB.dqtg_encode_record_shard(self.h, None if base is None else base.h, target.h,
+                                            quality, global_B, global_tensors, C.byref(r),
+                                            C.byref(off)))
+        return r, off.value
+
+    def partition(self, ckpt, cfg):
+        masks = [np.zeros(n, np.uint8) for n in ckpt.meta.numel]
+        _check(LIB.dqtg_partition(self.h, ckpt.h, C.byref(cfg), _ptr_array(masks)))
+        return masks
+
+    def eval_batch(self, ckpt, cfgs, seeds):
+        m = len(cfgs)
+        arr = (Config * max(m, 1))(*cfgs)
+        sd = np.ascontiguousarray(seeds, np.uint64)
+        q = np.zeros(max(m, 1), np.float64)
+        e = np.zeros(max(m, 1), np.float64)
+        _check(LIB.dqtg_eval_batch(self.h, ckpt.h, C.cast(arr, C.c_void_p), sd.ctypes.data, m,
+                                   q.ctypes.data, e.ctypes.data))
+        return q[:m], e[:m]
 
     # -- clustering / primitives ------------------------------------------------------
     def approx_kmeans(self, values, k, sigma=0.2, alpha=0.01, seed=1):
