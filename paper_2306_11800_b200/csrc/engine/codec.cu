@@ -44,6 +44,7 @@ struct Seg {
 };
 
 struct EncArgs {
+    const uint32_t* crc_shift;  // per tile
     const Tile* tiles;
     const uint8_t* types;
     const uint64_t* off;
@@ -193,9 +194,7 @@ __global__ void __launch_bounds__(kCB) enc_tile_kernel(EncArgs A) {
         if (tid == 0) {
             uint32_t x = 0;
             for (int w = 0; w < kCB / 32; ++w) x ^= s_red[w];
-            const uint64_t local = T.start - A.off[T.tensor];
-            const uint64_t end = A.stream_off[T.tensor] + local + cnt;
-            x = crc_shift(c_crc_x2n, x, 2 * (A.N - end));
+            if (x) x = crc_multmodp(A.crc_shift[ti], x);
             if (x) atomicXor(A.crc_acc, x);
         }
     }
@@ -1063,6 +1062,16 @@ __global__ void __launch_bounds__(kEmitWarps * 32) enc_emit_kernel(EncArgs A, Co
     }
 }
 
+// x^(8 * level-stream bytes after tile t) mod P, once per layout
+__global__ void crc_tile_shift_kernel(const Tile* tiles, int ntiles, const uint64_t* off,
+                                      const uint64_t* stream_off, uint64_t N, uint32_t* out) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x) {
+        const Tile T = tiles[t];
+        const uint64_t end = stream_off[T.tensor] + (T.start - off[T.tensor]) + T.count;
+        out[t] = crc_x2nmodp(c_crc_x2n, 2 * (N - end), 3);
+    }
+}
+
 __global__ void finish_crc_kernel(const uint32_t* acc, unsigned long long total_bytes,
                                   uint8_t* dst, uint32_t* crc_out) {
     if (threadIdx.x || blockIdx.x) return;
@@ -1197,7 +1206,14 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     }
 
     // ---- device scratch
+    if (!L.d_crc_shift) {
+        Layout& ML = const_cast<Layout&>(L);
+        DQTG_CUDA(cudaMalloc(&ML.d_crc_shift, (size_t)ntiles * 4 + 4));
+        { DQTG_SPAN(e, "crc_tile_shift_kernel"); crc_tile_shift_kernel<<<(ntiles + 255) / 256, 256, 0, st>>>(L.d_tiles, ntiles, L.d_off, L.d_stream_off, L.N, ML.d_crc_shift); }
+        e.launched();
+    }
     EncArgs A{};
+    A.crc_shift = L.d_crc_shift;
     A.tiles = L.d_tiles;
     A.types = L.d_types;
     A.off = L.d_off;

@@ -211,6 +211,7 @@ Layout::~Layout() {
     cudaFree(d_numel);
     cudaFree(d_tile0);
     cudaFree(d_stream_off);
+    cudaFree(d_crc_shift);
 }
 
 bool Layout::same_shape(const Layout& o) const {

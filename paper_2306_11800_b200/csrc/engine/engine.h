@@ -66,6 +66,7 @@ struct Layout {
     uint64_t* d_numel = nullptr;     // per tensor
     uint32_t* d_tile0 = nullptr;     // per tensor first tile (nt+1)
     uint64_t* d_stream_off = nullptr;  // per tensor unpadded element offset (CRC stream position)
+    uint32_t* d_crc_shift = nullptr;   // per tile x^(8*bytes after the tile) mod P (lazily built)
     Engine* eng = nullptr;
     ~Layout();
     bool same_shape(const Layout& o) const;
@@ -135,7 +136,8 @@ struct Engine {
     std::vector<cudaEvent_t> event_pool;
     size_t ev_used = 0;
     cudaEvent_t take_event();
-    std::shared_ptr<void> pending;  // sharded quantize: state between stage 2 and 3
+    // sharded quantize: per-checkpoint state between stage 2 and 3
+    std::map<const void*, std::shared_ptr<void>> pending;
 
     ~Engine();
     void activate() const { DQTG_CUDA(cudaSetDevice(device)); }

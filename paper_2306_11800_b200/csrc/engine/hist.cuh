@@ -13,9 +13,16 @@ __device__ __forceinline__ int bucket_of(uint32_t a, const BucketTab& t) {
     float lg = __log2f(__uint_as_float(a));
     int k = (int)ceilf(lg * t.inv_log2_gamma);
     k = k < kmin ? kmin : (k > kmax ? kmax : k);
-    // U(k) lives at U[k - kmin + 1]
-    while (k > kmin && __ldg(t.U + (k - kmin)) >= a) --k;
-    while (__ldg(t.U + (k - kmin + 1)) < a) ++k;
+    // U(k) lives at U[k - kmin + 1]; both bounds are fetched together (independent
+    // loads), the estimate is almost always exact or one off
+    const uint32_t lo = __ldg(t.U + (k - kmin)), hi = __ldg(t.U + (k - kmin + 1));
+    if (lo >= a && k > kmin) {
+        --k;
+        while (k > kmin && __ldg(t.U + (k - kmin)) >= a) --k;
+    } else if (hi < a) {
+        ++k;
+        while (__ldg(t.U + (k - kmin + 1)) < a) ++k;
+    }
     return k;
 }
 

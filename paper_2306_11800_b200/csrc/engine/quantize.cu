@@ -11,6 +11,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <map>
 
@@ -93,14 +94,28 @@ __global__ void __launch_bounds__(kPB) pass_a_kernel(PassIn a, unsigned long lon
         if (!dm && !ds) continue;
         unsigned long long* gm = gh_mag + lt * a.HS;
         unsigned long long* gs = gh_sens + lt * a.HS;
-        for (uint32_t i = threadIdx.x * 4; i < T.count; i += kPB * 4) {
-            const uint64_t idx = T.start + i;
-            float4 wv = ld4(a.w + idx);
-            float m[4], s[4];
-            load_scores<EXPL>(a, idx, wv, m, s);
+        // two float4 groups per iteration: twice the bytes in flight per thread
+        for (uint32_t i = threadIdx.x * 4; i < T.count; i += kPB * 8) {
+            const uint32_t i2 = i + kPB * 4;
+            const bool two = i2 < T.count;
+            float m[8], s[8];
+            {
+                float4 w0 = ld4(a.w + T.start + i);
+                float4 w1 = two ? ld4(a.w + T.start + i2) : make_float4(0, 0, 0, 0);
+                float mm[4], ss[4];
+                load_scores<EXPL>(a, T.start + i, w0, mm, ss);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (i + j >= T.count) break;
+                for (int j = 0; j < 4; ++j) m[j] = mm[j], s[j] = ss[j];
+                if (two) {
+                    load_scores<EXPL>(a, T.start + i2, w1, mm, ss);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) m[4 + j] = mm[j], s[4 + j] = ss[j];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t e = (j < 4 ? i : i2) + (j & 3);
+                if (e >= T.count) continue;
                 if (EXPL) {
                     if (dm) hist_add(shm, gm, m[j], a.tab, a.err);
                     if (ds) hist_add(shs, gs, s[j], a.tab, a.err);
@@ -179,18 +194,32 @@ __global__ void __launch_bounds__(kPB) pass_b_kernel(PassIn a, const LtParams* l
             P = lp[lt];
         }
         uint32_t np = 0;
-        for (uint32_t i = threadIdx.x * 4; i < T.count; i += kPB * 4) {
-            const uint64_t idx = T.start + i;
-            float4 wv = ld4(a.w + idx);
-            float m[4], s[4];
-            load_scores<EXPL>(a, idx, wv, m, s);
-            const float wa[4] = {wv.x, wv.y, wv.z, wv.w};
+        unsigned long long* gv = gh_val + lt * a.HS;
+        for (uint32_t i = threadIdx.x * 4; i < T.count; i += kPB * 8) {
+            const uint32_t i2 = i + kPB * 4;
+            const bool two = i2 < T.count;
+            float4 w0 = ld4(a.w + T.start + i);
+            float4 w1 = two ? ld4(a.w + T.start + i2) : make_float4(0, 0, 0, 0);
+            float m[8], s[8];
+            {
+                float mm[4], ss[4];
+                load_scores<EXPL>(a, T.start + i, w0, mm, ss);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (i + j >= T.count) break;
+                for (int j = 0; j < 4; ++j) m[j] = mm[j], s[j] = ss[j];
+                if (two) {
+                    load_scores<EXPL>(a, T.start + i2, w1, mm, ss);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) m[4 + j] = mm[j], s[4 + j] = ss[j];
+                }
+            }
+            const float wa[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t e = (j < 4 ? i : i2) + (j & 3);
+                if (e >= T.count) continue;
                 int part = classify(m[j], s[j], a.has_sens, a.metric, P);
                 np += part == 2;
-                if (part == 0) hist_add(sh, gh_val + lt * a.HS, wa[j], a.tab, a.err);
+                if (part == 0) hist_add(sh, gv, wa[j], a.tab, a.err);
             }
         }
         np = warp_sum(np);
@@ -264,46 +293,56 @@ __global__ void __launch_bounds__(kPB) pass_c_kernel(PassIn a, const LtParams* l
     const uint64_t tensor_base = a.tensor_off[T.tensor];
     __syncthreads();
     unsigned long long out = tile_prot_off[ti];
-    for (uint32_t i0 = 0; i0 < T.count; i0 += kPB * 4) {
-        const uint32_t i = i0 + threadIdx.x * 4;
-        uint16_t lv[4] = {0, 0, 0, 0};
-        unsigned long long flags = 0;
-        float wa[4] = {0, 0, 0, 0};
-        if (i < T.count) {
-            const uint64_t idx = T.start + i;
-            float4 wv = ld4(a.w + idx);
-            float m[4], s[4];
-            load_scores<EXPL>(a, idx, wv, m, s);
-            wa[0] = wv.x, wa[1] = wv.y, wa[2] = wv.z, wa[3] = wv.w;
+    // two float4 groups per thread and iteration; protected entries keep element
+    // order: group 0 (i0..i0+1023) before group 1, one packed (lo|hi) scan
+    for (uint32_t i0 = 0; i0 < T.count; i0 += kPB * 8) {
+        uint32_t flags[2] = {0, 0};
+        float wa[2][4];
+        for (int g = 0; g < 2; ++g) {
+            const uint32_t i = i0 + g * kPB * 4 + threadIdx.x * 4;
+            uint16_t lv[4] = {0, 0, 0, 0};
+            wa[g][0] = wa[g][1] = wa[g][2] = wa[g][3] = 0.0f;
+            if (i < T.count) {
+                const uint64_t idx = T.start + i;
+                float4 wv = ld4(a.w + idx);
+                float m[4], s[4];
+                load_scores<EXPL>(a, idx, wv, m, s);
+                wa[g][0] = wv.x, wa[g][1] = wv.y, wa[g][2] = wv.z, wa[g][3] = wv.w;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (i + j >= T.count) break;
-                int part = classify(m[j], s[j], a.has_sens, a.metric, P);
-                if (part == 0) lv[j] = (uint16_t)nearest_center(s_cb, k, wa[j]);
-                else if (part == 1) lv[j] = (uint16_t)k;
-                else {
-                    lv[j] = (uint16_t)(k + 1);
-                    flags |= 1ull << j;
+                for (int j = 0; j < 4; ++j) {
+                    if (i + j >= T.count) break;
+                    int part = classify(m[j], s[j], a.has_sens, a.metric, P);
+                    if (part == 0) lv[j] = (uint16_t)nearest_center(s_cb, k, wa[g][j]);
+                    else if (part == 1) lv[j] = (uint16_t)k;
+                    else {
+                        lv[j] = (uint16_t)(k + 1);
+                        flags[g] |= 1u << j;
+                    }
                 }
+                uint2 pk;
+                pk.x = (uint32_t)lv[0] | ((uint32_t)lv[1] << 16);
+                pk.y = (uint32_t)lv[2] | ((uint32_t)lv[3] << 16);
+                *(uint2*)(levels + idx) = pk;
             }
-            uint2 pk;
-            pk.x = (uint32_t)lv[0] | ((uint32_t)lv[1] << 16);
-            pk.y = (uint32_t)lv[2] | ((uint32_t)lv[3] << 16);
-            *(uint2*)(levels + idx) = pk;
         }
-        unsigned long long cnt = __popcll(flags), tot;
-        unsigned long long ex = block_exclusive_scan<unsigned long long>(cnt, s_scan, &tot);
-        if (flags) {
-            unsigned long long o = out + ex;
+        const unsigned long long packed =
+            (unsigned long long)__popc(flags[0]) | ((unsigned long long)__popc(flags[1]) << 32);
+        unsigned long long tot;
+        const unsigned long long ex = block_exclusive_scan<unsigned long long>(packed, s_scan, &tot);
+        const unsigned long long tot0 = tot & 0xffffffffull;
+        for (int g = 0; g < 2; ++g) {
+            if (!flags[g]) continue;
+            const uint32_t i = i0 + g * kPB * 4 + threadIdx.x * 4;
+            unsigned long long o = out + (g ? tot0 + (ex >> 32) : (ex & 0xffffffffull));
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-                if (flags >> j & 1) {
+                if (flags[g] >> j & 1) {
                     ppos[o] = (T.start - tensor_base) + i + j;
-                    pval[o] = bf16_rne(wa[j]);
+                    pval[o] = bf16_rne(wa[g][j]);
                     ++o;
                 }
         }
-        out += tot;
+        out += tot0 + (tot >> 32);
     }
 }
 
@@ -803,7 +842,9 @@ void shard_stage2(Engine& e, const DevCkpt& c, const dqtg_config& cfg,
                   const unsigned long long* score_hist, unsigned long long* value_hist) {
     const Layout& L = *c.L;
     auto s = std::make_unique<Stage>();
-    s->tag = "sh.";
+    char tag[40];
+    snprintf(tag, sizeof(tag), "sh%p.", (const void*)&c);
+    s->tag = tag;
     s->cfg = cfg;
     quantize_plan(L, cfg, c.has_sens, s->plan);
     AlphaTables& T = e.alpha_tables(cfg.alpha);
@@ -813,14 +854,16 @@ void shard_stage2(Engine& e, const DevCkpt& c, const dqtg_config& cfg,
                      const_cast<unsigned long long*>(score_hist) + (size_t)kLayerTypes * T.HS);
     PassIn a = pass_in(e, c, T, (int)cfg.metric);
     stage_pass_b(e, c, a, *s, T, false);
-    e.pending = std::shared_ptr<void>(s.release(), [](void* p) { delete (Stage*)p; });
+    e.pending[&c] = std::shared_ptr<void>(s.release(), [](void* p) { delete (Stage*)p; });
 }
 
 std::unique_ptr<QState> shard_stage3(Engine& e, const DevCkpt& c, const dqtg_config& cfg,
                                      uint64_t seed, uint64_t step,
                                      const unsigned long long* value_hist) {
-    DQTG_REQUIRE(e.pending, DQTG_ERROR, "quantize stage 3 without stage 2");
-    Stage& s = *(Stage*)e.pending.get();
+    auto pit = e.pending.find(&c);
+    DQTG_REQUIRE(pit != e.pending.end(), DQTG_ERROR, "quantize stage 3 without stage 2");
+    std::shared_ptr<void> keep = pit->second;
+    Stage& s = *(Stage*)keep.get();
     const Layout& L = *c.L;
     AlphaTables& T = e.alpha_tables(cfg.alpha);
     s.gh_val = const_cast<unsigned long long*>(value_hist);
@@ -864,7 +907,7 @@ std::unique_ptr<QState> shard_stage3(Engine& e, const DevCkpt& c, const dqtg_con
     for (int lt = 0; lt < kLayerTypes; ++lt)
         q->cb[lt].assign(hcb.begin() + (size_t)lt * q->cb_stride,
                          hcb.begin() + (size_t)lt * q->cb_stride + q->cb_len[lt]);
-    e.pending.reset();
+    e.pending.erase(&c);
     return q;
 }
 
