@@ -329,6 +329,35 @@ def run_ours(args):
         barrier()
     ms = t0.elapsed_time(t1)
     launches = eng.launches - launches0
+    ms_sequential = ms
+
+    # pipelined chain (N=1): quantize(i+1) on stream Q overlaps encode(i) on stream E
+    pipelined = None
+    if world == 1 and not args.no_pipeline:
+        from paper_2306_11800_b200.pipeline import ChainCompressor
+
+        cc = ChainCompressor(local)
+        pck = []
+        for i in range(n_snap):
+            c = cc.checkpoint(names, types, shapes)
+            c.set_weights([ckpts[i].weights_dev + 4 * ckpts[i].tensor_offset(j)
+                           for j in range(len(layout))])
+            c.set_ema(tensor_ptrs(ema.data_ptr(), layout))
+            pck.append(c)
+        torch.cuda.synchronize()
+        base = cc.run(pck[:args.warmup + 1], cfg, 1, list(range(args.warmup + 1)))
+        cc.sync()
+        torch.cuda.synchronize()
+        l0 = cc.launches
+        tp0 = time.perf_counter()
+        cc.run(pck[args.warmup + 1:], cfg, 1, list(range(args.warmup + 1, n_snap)), base=base)
+        cc.sync()
+        pipelined = (time.perf_counter() - tp0) * 1e3
+        launches_p = cc.launches - l0
+        del base, cc, pck
+    if pipelined is not None and pipelined < ms:
+        ms = pipelined
+        launches = launches_p
     if world > 1:
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -439,7 +468,13 @@ def run_ours(args):
                        "parallelism": (f"tensor-sharded x{world}, score/value histograms "
                                        f"all-reduced over NCCL" if world > 1 else "1 GPU"),
                        "l2": "inputs (1 GB/step) larger than L2; no flush",
-                       "record_bytes": rec_mean, "compression_ratio": cr},
+                       "record_bytes": rec_mean, "compression_ratio": cr,
+                       "ms_per_step_sequential": ms_sequential / args.steps,
+                       "ms_per_step_pipelined": None if pipelined is None else pipelined / args.steps,
+                       "timing": ("pipelined chain: quantize(i+1) || encode(i) on two streams, "
+                                  "host wall clock with device sync on both ends"
+                                  if pipelined is not None and ms == pipelined else
+                                  "CUDA events on the engine stream")},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(),
         }
@@ -456,6 +491,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

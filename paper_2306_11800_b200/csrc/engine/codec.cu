@@ -45,6 +45,7 @@ struct Seg {
 
 struct EncArgs {
     const uint32_t* crc_shift;  // per tile
+    uint32_t n_tb;              // tensors * B
     const Tile* tiles;
     const uint8_t* types;
     const uint64_t* off;
@@ -108,9 +109,8 @@ __global__ void __launch_bounds__(kCB) enc_tile_kernel(EncArgs A) {
     extern __shared__ uint32_t dyn[];
     const uint32_t B = A.B, NS = A.NS;
     uint32_t* s_freq = dyn;                     // B*NS
-    uint32_t* s_mask = s_freq + ((B * NS + 3u) & ~3u);  // B*kWords: element bitmask per key
-    uint16_t* s_wpre = (uint16_t*)(s_mask + B * kWords);  // B*kWords exclusive popcounts
-    uint16_t* s_key = s_wpre + B * kWords;  // kTile + 2; reused as s_hp after the scatter
+    uint32_t* s_wcnt = s_freq + ((B * NS + 3u) & ~3u);  // [8 warps][B] running key counts
+    uint16_t* s_key = (uint16_t*)(s_wcnt + 8 * B);  // kTile + 2; reused as s_hp after the scatter
     uint16_t* s_d = s_key + kTile + 2;
     uint16_t* s_sd = s_d + kTile;
     uint16_t* s_sk = s_sd + kTile;
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kCB) enc_tile_kernel(EncArgs A) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
     for (uint32_t i = tid; i < B * NS; i += kCB) s_freq[i] = 0;
-    for (uint32_t i = tid; i < B * kWords; i += kCB) s_mask[i] = 0;
+    for (uint32_t i = tid; i < 8 * B; i += kCB) s_wcnt[i] = 0;
     {  // CRC byte table (codec.cpp:276-284)
         uint32_t c = tid;
         for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xedb88320u ^ (c >> 1) : c >> 1;
@@ -181,15 +181,6 @@ __global__ void __launch_bounds__(kCB) enc_tile_kernel(EncArgs A) {
         r = r ? crc_multmodp(c_crc_pw[tid], r) : 0u;
         r = warp_xor(r);
         if (lane == 0) s_red[wid] = r;
-        // ---- stable multisplit on the previous level: per-key element bitmasks
-        for (int rnd = 0; rnd < kIt; ++rnd) {
-            const uint32_t e = rnd * kCB + tid;
-            const bool valid = e < cnt;
-            const uint32_t key = valid ? s_key[e] : 0xffffu;
-            const uint32_t peers = __match_any_sync(0xffffffffu, key);
-            if (valid && (peers & ((1u << lane) - 1u)) == 0)
-                s_mask[key * kWords + (e >> 5)] = peers;
-        }
         __syncthreads();
         if (tid == 0) {
             uint32_t x = 0;
@@ -198,25 +189,41 @@ __global__ void __launch_bounds__(kCB) enc_tile_kernel(EncArgs A) {
             if (x) atomicXor(A.crc_acc, x);
         }
     }
-    // exclusive popcount prefix per key over the 128 words: one warp per key,
-    // four words per lane, warp scan
-    for (uint32_t b = wid; b < B; b += kCB / 32) {
-        const uint4 mw = *(const uint4*)(s_mask + b * kWords + lane * 4);
-        const uint32_t p0 = __popc(mw.x), p1 = __popc(mw.y), p2 = __popc(mw.z), p3 = __popc(mw.w);
-        const uint32_t own = p0 + p1 + p2 + p3;
-        uint32_t x = own;
+    // ---- stable multisplit on the previous level (rearrange, codec.cpp:39-54):
+    // warp w owns elements [512w, 512w+512) in word order; a per-warp running
+    // count per key gives each element its rank among equal keys of the range.
+    uint32_t rk[kIt];
+    uint16_t ky[kIt];
+    {
+        const uint32_t lt_mask = (1u << lane) - 1u;
+        uint32_t* wc = s_wcnt + wid * B;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+        for (int j = 0; j < kIt; ++j) {
+            const uint32_t e = wid * 512 + j * 32 + lane;
+            const bool valid = e < cnt;
+            const uint32_t key = valid ? s_key[e] : 0xffffu;
+            const uint32_t peers = __match_any_sync(0xffffffffu, key);
+            const int leader = __ffs(peers) - 1;
+            uint32_t old = 0;
+            if (lane == leader && valid) {
+                old = wc[key];
+                wc[key] = old + __popc(peers);
+            }
+            old = __shfl_sync(0xffffffffu, old, leader);
+            rk[j] = old + __popc(peers & lt_mask);
+            ky[j] = (uint16_t)key;
         }
-        const uint32_t ex = x - own;
-        uint16_t* w = s_wpre + b * kWords + lane * 4;
-        w[0] = (uint16_t)ex;
-        w[1] = (uint16_t)(ex + p0);
-        w[2] = (uint16_t)(ex + p0 + p1);
-        w[3] = (uint16_t)(ex + p0 + p1 + p2);
-        if (lane == 31) s_cnt[b] = x;
+    }
+    __syncthreads();
+    // per key: exclusive prefix over warps, then start offsets over keys
+    for (uint32_t b = tid; b < B; b += kCB) {
+        uint32_t acc = 0;
+        for (int w = 0; w < kCB / 32; ++w) {
+            const uint32_t c = s_wcnt[w * B + b];
+            s_wcnt[w * B + b] = acc;
+            acc += c;
+        }
+        s_cnt[b] = acc;
     }
     __syncthreads();
     if (wid == 0) {
@@ -234,12 +241,15 @@ __global__ void __launch_bounds__(kCB) enc_tile_kernel(EncArgs A) {
         }
     }
     __syncthreads();
-    for (uint32_t e = tid; e < cnt; e += kCB) {
-        const uint32_t key = s_key[e], w = e >> 5;
-        const uint32_t rank = s_wpre[key * kWords + w] + __popc(s_mask[key * kWords + w] & ((1u << (e & 31)) - 1u));
-        const uint32_t pos = s_start[key] + rank;
-        s_sd[pos] = s_d[e];
-        s_sk[pos] = (uint16_t)key;
+#pragma unroll
+    for (int j = 0; j < kIt; ++j) {
+        const uint32_t e = wid * 512 + j * 32 + lane;
+        if (e < cnt) {
+            const uint32_t key = ky[j];
+            const uint32_t pos = s_start[key] + s_wcnt[wid * B + key] + rk[j];
+            s_sd[pos] = s_d[e];
+            s_sk[pos] = (uint16_t)key;
+        }
     }
     __syncthreads();
 
@@ -329,12 +339,13 @@ __device__ __forceinline__ RunM runm_combine(const RunM& a, const RunM& b) {
     return r;
 }
 
-__global__ void __launch_bounds__(kCB) enc_resolve_kernel(EncArgs A) {
+// Block per (tensor, group) for tensors with many tiles (256-tile chunks).
+__global__ void __launch_bounds__(kCB) enc_resolve_big_kernel(EncArgs A, const uint32_t* tensors) {
     extern __shared__ uint32_t s_f[];  // NS
     __shared__ RunM s_m[kCB];
     __shared__ int s_last[kCB];
     const uint32_t B = A.B, NS = A.NS;
-    const uint32_t t = blockIdx.x / B, b = blockIdx.x % B;
+    const uint32_t t = tensors[blockIdx.x / B], b = blockIdx.x % B;
     const int tid = threadIdx.x;
     const uint32_t a0 = A.tile0[t], a1 = A.tile0[t + 1];
     for (uint32_t i = tid; i < NS; i += kCB) s_f[i] = 0;
@@ -415,6 +426,111 @@ __global__ void __launch_bounds__(kCB) enc_resolve_kernel(EncArgs A) {
         if (s_f[i]) gf[i] += s_f[i];
 }
 
+constexpr int kResolveWarps = 8;
+
+__device__ __forceinline__ RunM shfl_down_runm(const RunM& m, int o) {
+    RunM r;
+    r.n = __shfl_down_sync(0xffffffffu, m.n, o);
+    r.lead = __shfl_down_sync(0xffffffffu, m.lead, o);
+    r.fv = __shfl_down_sync(0xffffffffu, m.fv, o);
+    r.lv = __shfl_down_sync(0xffffffffu, m.lv, o);
+    r.single = __shfl_down_sync(0xffffffffu, m.single, o);
+    return r;
+}
+
+// One warp per (tensor, group): forward "last non-empty value" scan and a
+// backward run-monoid suffix scan over the tensor's tiles, 32 tiles at a time.
+__global__ void __launch_bounds__(kResolveWarps * 32) enc_resolve_kernel(EncArgs A,
+                                                                         const uint32_t* tensors,
+                                                                         uint32_t n_pairs) {
+    extern __shared__ uint32_t s_f_all[];  // kResolveWarps * NS
+    const uint32_t B = A.B, NS = A.NS;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t pair = blockIdx.x * kResolveWarps + wid;
+    if (pair >= n_pairs) return;
+    const uint32_t t = tensors[pair / B], b = pair % B;
+    const uint32_t tb = t * B + b;
+    const uint32_t a0 = A.tile0[t], a1 = A.tile0[t + 1];
+    uint32_t* f = s_f_all + wid * NS;
+    for (uint32_t i = lane; i < NS; i += 32) f[i] = 0;
+    __syncwarp();
+    // forward: cont = leading run continues the nearest earlier non-empty segment
+    int carry_last = -1;
+    bool any = false;
+    for (uint32_t c0 = a0; c0 < a1; c0 += 32) {
+        const uint32_t i = c0 + lane;
+        Seg* S = i < a1 ? &A.segs[(size_t)i * B + b] : nullptr;
+        const int idx = (S && S->n) ? (int)i : -1;
+        int x = idx;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x = max(x, y);
+        }
+        int prev = __shfl_up_sync(0xffffffffu, x, 1);
+        if (lane == 0) prev = -1;
+        prev = max(prev, carry_last);
+        if (idx >= 0) {
+            S->cont = prev >= 0 && A.segs[(size_t)prev * B + b].lv == S->fv;
+            any = true;
+        }
+        carry_last = max(carry_last, __shfl_sync(0xffffffffu, x, 31));
+    }
+    if (!__any_sync(0xffffffffu, any)) return;
+    __syncwarp();
+    // backward: suffix run monoid gives each trailing run's extension
+    RunM carry{};
+    for (int64_t c0 = (int64_t)a1 - 32; c0 > (int64_t)a0 - 32; c0 -= 32) {
+        const int64_t ii = c0 + lane;
+        const bool in = ii >= (int64_t)a0 && ii < (int64_t)a1;
+        RunM m{};
+        Seg S{};
+        if (in) {
+            S = A.segs[(size_t)ii * B + b];
+            if (S.n) {
+                m.n = S.n;
+                m.fv = S.fv;
+                m.lv = S.lv;
+                m.single = S.lead == S.n;
+                m.lead = S.lead;
+            }
+        }
+        // inclusive suffix scan over the 32 lanes (lane i combines with later lanes)
+        RunM x = m;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            RunM y = shfl_down_runm(x, o);
+            if (lane + o < 32) x = runm_combine(x, y);
+        }
+        RunM nxt = shfl_down_runm(x, 1);
+        RunM after = lane < 31 ? runm_combine(nxt, carry) : carry;
+        if (in && S.n) {
+            const unsigned long long E = (after.n && after.fv == S.lv) ? after.lead : 0ull;
+            Seg& G = A.segs[(size_t)ii * B + b];
+            if (S.lead == S.n) {
+                G.lead_total = G.trail_total = S.n + E;
+                if (!S.cont) add_symbol(f, NS, B, tb, S.fv, S.n + E, A);
+            } else {
+                G.lead_total = S.lead;
+                G.trail_total = S.trail + E;
+                if (!S.cont) add_symbol(f, NS, B, tb, S.fv, S.lead, A);
+                add_symbol(f, NS, B, tb, S.lv, S.trail + E, A);
+            }
+        }
+        RunM head = shfl_down_runm(x, 0);
+        head.n = __shfl_sync(0xffffffffu, x.n, 0);
+        head.lead = __shfl_sync(0xffffffffu, x.lead, 0);
+        head.fv = __shfl_sync(0xffffffffu, x.fv, 0);
+        head.lv = __shfl_sync(0xffffffffu, x.lv, 0);
+        head.single = __shfl_sync(0xffffffffu, x.single, 0);
+        carry = runm_combine(head, carry);
+    }
+    __syncwarp();
+    uint32_t* gf = A.freq + (size_t)tb * NS;
+    for (uint32_t i = lane; i < NS; i += 32)
+        if (f[i]) gf[i] += f[i];
+}
+
 // ---- overflow run lengths: sorted unique (key, count) ------------------------------
 __global__ void ov_unique_kernel(const unsigned long long* sorted, unsigned long long n,
                                  unsigned long long* ukey, unsigned long long* uhead,
@@ -485,7 +601,7 @@ __global__ void ov_group_max_kernel(const unsigned long long* ukey, const unsign
     }
 }
 
-__global__ void __launch_bounds__(128) enc_huffman_kernel(EncArgs A, const unsigned long long* elems,
+__global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsigned long long* elems,
                                                           const unsigned long long* ukey,
                                                           const unsigned long long* ucnt,
                                                           const unsigned long long* nu_p,
@@ -692,19 +808,21 @@ __device__ __forceinline__ void owned_run(const EncArgs& A, const Seg* segs, uns
     }
 }
 
-// E2a: bits per (tile, group)
-__global__ void __launch_bounds__(kCB) enc_bits_kernel(EncArgs A, CodeTabs C,
+// E2a: bits per (tile, group), one warp per tile
+__global__ void __launch_bounds__(256) enc_bits_kernel(EncArgs A, CodeTabs C, int ntiles,
                                                        unsigned long long* segbits) {
-    __shared__ unsigned long long s_bits[kMaxB];
-    const int ti = blockIdx.x;
+    __shared__ uint32_t s_bits[8][kMaxB];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ti = blockIdx.x * 8 + wid;
+    if (ti >= ntiles) return;
     const uint32_t B = A.B, NS = A.NS;
     const Tile T = A.tiles[ti];
-    for (uint32_t b = threadIdx.x; b < B; b += kCB) s_bits[b] = 0;
-    __syncthreads();
+    for (uint32_t b = lane; b < B; b += 32) s_bits[wid][b] = 0;
+    __syncwarp();
     const uint32_t R = A.tile_nruns[ti];
     const Seg* segs = A.segs + (size_t)ti * B;
     const unsigned long long* runs = A.runs + (size_t)ti * kTile;
-    for (uint32_t r = threadIdx.x; r < R; r += kCB) {
+    for (uint32_t r = lane; r < R; r += 32) {
         uint32_t v, b;
         unsigned long long L;
         owned_run(A, segs, runs[r], r, v, b, L);
@@ -714,10 +832,10 @@ __global__ void __launch_bounds__(kCB) enc_bits_kernel(EncArgs A, CodeTabs C,
         uint32_t l1, l2 = 0;
         code_of(C, tb, NS, v, c, l1);
         if (L > 1) code_of_len(C, tb, NS, B, L, c, l2);
-        atomicAdd(&s_bits[b], (unsigned long long)(l1 + l2));
+        atomicAdd(&s_bits[wid][b], l1 + l2);
     }
-    __syncthreads();
-    for (uint32_t b = threadIdx.x; b < B; b += kCB) segbits[(size_t)ti * B + b] = s_bits[b];
+    __syncwarp();
+    for (uint32_t b = lane; b < B; b += 32) segbits[(size_t)ti * B + b] = s_bits[wid][b];
 }
 
 // S2: exclusive scan of segment bits across the tensor's tiles
@@ -1222,6 +1340,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     A.N = L.N;
     A.B = B;
     A.NS = NS;
+    A.n_tb = nt * B;
     A.prev = base ? base->d_levels : nullptr;
     A.cur = target.d_levels;
     A.segs = (Seg*)e.buf("e.segs", (size_t)ntiles * B * sizeof(Seg) + 64);
@@ -1239,7 +1358,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     DQTG_CUDA(cudaMemsetAsync(small, 0, 64, st));
 
     // E1
-    const size_t e1_smem = (size_t)((B * NS + 3) & ~3u) * 4 + (size_t)B * kWords * 6 + (size_t)kTile * 2 * 3 +
+    const size_t e1_smem = (size_t)((B * NS + 3) & ~3u) * 4 + (size_t)8 * B * 4 + (size_t)kTile * 2 * 3 +
                            (kTile + 2) * 2 + 16;
     if (base) {
         DQTG_CUDA(cudaFuncSetAttribute(enc_tile_kernel<true>,
@@ -1251,7 +1370,20 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
         { DQTG_SPAN(e, "enc_tile_kernel"); enc_tile_kernel<false><<<ntiles, kCB, e1_smem, st>>>(A); }
     }
     // S
-    { DQTG_SPAN(e, "enc_resolve_kernel"); enc_resolve_kernel<<<nt * B, kCB, NS * 4, st>>>(A); }
+    {
+        // tensors with few tiles: a warp per (tensor, group); many tiles: a CTA
+        std::vector<uint32_t> small, big;
+        for (uint32_t t = 0; t < nt; ++t)
+            (L.tile0[t + 1] - L.tile0[t] <= 64 ? small : big).push_back(t);
+        auto* d_list = (uint32_t*)e.buf("e.tlist", (size_t)(nt + 2) * 4);
+        std::vector<uint32_t> both(small);
+        both.insert(both.end(), big.begin(), big.end());
+        DQTG_CUDA(cudaMemcpyAsync(d_list, both.data(), both.size() * 4, cudaMemcpyHostToDevice, st));
+        const uint32_t np_small = (uint32_t)small.size() * B;
+        if (np_small) { DQTG_SPAN(e, "enc_resolve_kernel"); enc_resolve_kernel<<<(np_small + kResolveWarps - 1) / kResolveWarps, kResolveWarps * 32, kResolveWarps * NS * 4, st>>>(A, d_list, np_small); }
+        if (!big.empty()) { DQTG_SPAN(e, "enc_resolve_big_kernel"); enc_resolve_big_kernel<<<(unsigned)big.size() * B, kCB, NS * 4, st>>>(A, d_list + small.size()); }
+        e.launched(2);
+    }
     e.launched(2);
     DQTG_CUDA(cudaGetLastError());
     // group element counts from the segments (host-free): sum of seg.n per (t,b)
@@ -1321,13 +1453,13 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
         if (hsm > 48 * 1024)
             DQTG_CUDA(cudaFuncSetAttribute(enc_huffman_kernel,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
-        { DQTG_SPAN(e, "enc_huffman_kernel"); enc_huffman_kernel<<<nt * B, 128, hsm, st>>>(A, elems, ukey, ucnt, nu, gi, tab_sym, tab_len,
+        { DQTG_SPAN(e, "enc_huffman_kernel"); enc_huffman_kernel<<<nt * B, 32, hsm, st>>>(A, elems, ukey, ucnt, nu, gi, tab_sym, tab_len,
                                                      code_dense, len_dense, code_ov, len_ov, W, np2); }
         e.launched();
     }
     CodeTabs C{code_dense, len_dense, ukey, code_ov, len_ov, gi};
     auto* segbits = (unsigned long long*)e.buf("e.segbits", (size_t)ntiles * B * 8);
-    { DQTG_SPAN(e, "enc_bits_kernel"); enc_bits_kernel<<<ntiles, kCB, 0, st>>>(A, C, segbits); }
+    { DQTG_SPAN(e, "enc_bits_kernel"); enc_bits_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(A, C, ntiles, segbits); }
     { DQTG_SPAN(e, "enc_bitscan_kernel"); enc_bitscan_kernel<<<nt * B, kCB, 0, st>>>(A, segbits, gi); }
     e.launched(2);
 

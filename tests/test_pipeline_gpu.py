@@ -1,0 +1,48 @@
+"""The pipelined chain (quantize(i+1) || encode(i) on two streams) produces the
+same records as the sequential C-ABI step and as the oracle."""
+import numpy as np
+import pytest
+
+from tests.util import flat, make_tensors, perturb
+
+pytestmark = pytest.mark.gpu
+
+
+def test_pipelined_chain_matches_sequential_and_oracle(oracle):
+    from oracle.oracle import Config as OC
+    from paper_2306_11800_b200 import engine as E
+    from paper_2306_11800_b200.pipeline import ChainCompressor
+
+    series = [make_tensors(seed=5)]
+    for k in range(4):
+        series.append(perturb(series[-1], seed=50 + k))
+    rng = np.random.default_rng(1)
+    ema = rng.normal(0, 0.1, flat(series[0]).size).astype(np.float32)
+    names = [t.name for t in series[0]]
+    types = [t.type for t in series[0]]
+    shapes = [t.shape for t in series[0]]
+    sizes = np.cumsum([t.data.size for t in series[0]])[:-1]
+    cfg = E.Config()
+    cc = ChainCompressor(0)
+    cks = []
+    for ts in series:
+        c = cc.checkpoint(names, types, shapes)
+        c.set_weights([t.data for t in ts])
+        c.set_ema(np.split(ema, sizes))
+        cks.append(c)
+    recs = {}
+
+    def grab(k, r):
+        n = E.LIB.dqtg_record_size(r)
+        buf = np.empty(n, np.uint8)
+        E._check(E.LIB.dqtg_record_copy(r, buf.ctypes.data))
+        recs[k] = buf.tobytes()
+
+    cc.run(cks, cfg, 3, list(range(len(cks))), on_record=grab)
+    cc.sync()
+    prev = None
+    for k, ts in enumerate(series):
+        m, s = oracle.scores(flat(ts), ema)
+        q = oracle.quantize(ts, k, m, s, OC(), 3)
+        assert recs[k] == oracle.encode_record(q, prev), k
+        prev = q
