@@ -44,6 +44,7 @@ struct Seg {
 };
 
 struct EncArgs {
+    int ntiles;
     const uint32_t* crc_shift;  // per tile
     uint32_t n_tb;              // tensors * B
     const Tile* tiles;
@@ -102,220 +103,333 @@ __device__ __forceinline__ void add_symbol(uint32_t* f, uint32_t NS, uint32_t B,
 }
 
 // ---- E1 --------------------------------------------------------------------
-constexpr int kWords = kTile / 32;  // 32-element words per tile
+// Persistent CTAs walk contiguous tile ranges.  Per tile (4096 elements):
+//   L  16 contiguous elements per thread: key = previous level, d = cyclic delta
+//      (codec.cpp:12-24), staged as bytes (levels < 64)
+//   M  warp w owns elements [512w, 512w+512) in 32-element chunks:
+//      __match_any_sync on the key gives each element its rank among equal keys
+//      (stable group-by, codec.cpp:39-54) and its previous same-key element,
+//      whose delta decides whether the element starts a run (rle_encode,
+//      codec.cpp:79-90); the first element of a key in a warp is settled in F
+//      against the last one of the nearest earlier warp holding that key
+//   P  per key: prefix over warps, group start offsets
+//   H  only run heads are placed (sparse): head flag, value and group at the
+//      element's rearranged position
+//   B  head flags -> run start positions (block scan)
+//   R  runs (value, group, length), first/last run per group, interior-run
+//      symbol frequencies (accumulated per tensor in shared memory)
+//   C  CRC-32 of the target levels by one warp, 128 levels per lane with
+//      zero-skipping slice-by-16 tables (the high byte of every level is 0),
+//      combined with x^(8n) mod P shifts (tile virtually right-aligned)
+constexpr int kCrcTabs = 10;  // T1,T3,T5,T7,T9,T11,T12,T13,T14,T15
+__device__ uint32_t g_crc_slice[kCrcTabs][256];
+__constant__ uint32_t c_crc_pw32[32];  // x^(8*256*(31-l)) mod P
+constexpr int kCurRow = 144;           // s_cur: 128 levels per row + 16 B pad (bank spread)
+
+__device__ __forceinline__ uint32_t crc_block8(const uint32_t* T, uint32_t r, const uint32_t (&lo)[8]) {
+    const uint32_t x = r ^ (lo[0] | (lo[1] << 16));
+    return T[9 * 256 + (x & 0xff)] ^ T[8 * 256 + ((x >> 8) & 0xff)] ^
+           T[7 * 256 + ((x >> 16) & 0xff)] ^ T[6 * 256 + (x >> 24)] ^ T[5 * 256 + lo[2]] ^
+           T[4 * 256 + lo[3]] ^ T[3 * 256 + lo[4]] ^ T[2 * 256 + lo[5]] ^ T[1 * 256 + lo[6]] ^
+           T[0 * 256 + lo[7]];
+}
+
+struct E1Smem {
+    uint32_t* freq;     // B*NS, per tensor
+    uint32_t* crc;      // kCrcTabs*256
+    uint32_t* wcnt;     // 8*B
+    uint8_t* lastd;     // 8*B
+    uint8_t* firstd;    // 8*B
+    uint8_t* fhead;     // 8*B
+    uint8_t* key;       // kTile   (aliased by hp after M)
+    uint8_t* d;         // kTile
+    uint16_t* hp;       // kTile+1 (over key|d)
+    uint8_t* cur;       // 32 rows * kCurRow
+    uint8_t* hf;        // kTile
+    uint8_t* hv;        // kTile
+    uint8_t* hk;        // kTile
+};
+
+__host__ __device__ inline size_t e1_smem_bytes(uint32_t B, uint32_t NS) {
+    size_t o = 0;
+    o += ((size_t)B * NS * 4 + 15) & ~(size_t)15;
+    o += (size_t)kCrcTabs * 256 * 4;
+    o += ((size_t)8 * B * 4 + 15) & ~(size_t)15;
+    o += ((size_t)8 * B * 3 + 15) & ~(size_t)15;
+    o += 2 * (size_t)kTile + 16;  // key | d  (hp alias needs 2*kTile+2)
+    o += 32 * (size_t)kCurRow;
+    o += 3 * (size_t)kTile;
+    return o;
+}
+
+__device__ inline E1Smem e1_carve(uint8_t* base, uint32_t B, uint32_t NS) {
+    E1Smem S;
+    size_t o = 0;
+    S.freq = (uint32_t*)(base + o); o += ((size_t)B * NS * 4 + 15) & ~(size_t)15;
+    S.crc = (uint32_t*)(base + o);  o += (size_t)kCrcTabs * 256 * 4;
+    S.wcnt = (uint32_t*)(base + o); o += ((size_t)8 * B * 4 + 15) & ~(size_t)15;
+    S.lastd = base + o;
+    S.firstd = base + o + 8 * B;
+    S.fhead = base + o + 16 * B;    o += ((size_t)8 * B * 3 + 15) & ~(size_t)15;
+    S.key = base + o;
+    S.d = base + o + kTile;
+    S.hp = (uint16_t*)(base + o);   o += 2 * (size_t)kTile + 16;
+    S.cur = base + o;               o += 32 * (size_t)kCurRow;
+    S.hf = base + o;
+    S.hv = base + o + kTile;
+    S.hk = base + o + 2 * kTile;
+    return S;
+}
 
 template <bool HAS_BASE>
-__global__ void __launch_bounds__(kCB) enc_tile_kernel(EncArgs A) {
-    extern __shared__ uint32_t dyn[];
+__global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
+    extern __shared__ __align__(16) uint8_t e1_dyn[];
     const uint32_t B = A.B, NS = A.NS;
-    uint32_t* s_freq = dyn;                     // B*NS
-    uint32_t* s_wcnt = s_freq + ((B * NS + 3u) & ~3u);  // [8 warps][B] running key counts
-    uint16_t* s_key = (uint16_t*)(s_wcnt + 8 * B);  // kTile + 2; reused as s_hp after the scatter
-    uint16_t* s_d = s_key + kTile + 2;
-    uint16_t* s_sd = s_d + kTile;
-    uint16_t* s_sk = s_sd + kTile;
-    uint16_t* s_hp = s_key;
+    const E1Smem S = e1_carve(e1_dyn, B, NS);
     __shared__ uint32_t s_cnt[kMaxB], s_start[kMaxB], s_run0[kMaxB], s_run1[kMaxB];
-    __shared__ uint32_t s_tab[256];
-    __shared__ uint32_t s_red[kCB / 32];
     __shared__ unsigned long long s_scan[33];
-
-    const int ti = blockIdx.x;
-    const Tile T = A.tiles[ti];
-    const uint32_t cnt = T.count;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
 
-    for (uint32_t i = tid; i < B * NS; i += kCB) s_freq[i] = 0;
-    for (uint32_t i = tid; i < 8 * B; i += kCB) s_wcnt[i] = 0;
-    {  // CRC byte table (codec.cpp:276-284)
-        uint32_t c = tid;
-        for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xedb88320u ^ (c >> 1) : c >> 1;
-        s_tab[tid] = c;
-    }
-    // load 16 consecutive elements per thread (two 16-byte vectors per stream)
-    {
-        const uint32_t e0 = tid * kIt;
-        if (e0 < cnt) {
-            uint16_t c16[kIt], p16[kIt];
-            const uint4* cp = (const uint4*)(A.cur + T.start + e0);
-            uint4 a0 = cp[0], a1 = cp[1];
-            memcpy(c16, &a0, 16);
-            memcpy(c16 + 8, &a1, 16);
-            if (HAS_BASE) {
-                const uint4* pp = (const uint4*)(A.prev + T.start + e0);
-                uint4 b0 = pp[0], b1 = pp[1];
-                memcpy(p16, &b0, 16);
-                memcpy(p16 + 8, &b1, 16);
-            }
-            bool bad = false;
-#pragma unroll
-            for (int j = 0; j < kIt; ++j) {
-                const uint32_t e = e0 + j;
-                if (e < cnt) {
-                    uint32_t c = c16[j], p = HAS_BASE ? p16[j] : 0u;
-                    bad |= (p >= B) | (c >= B);
-                    p = p < B ? p : 0u;
-                    c = c < B ? c : 0u;
-                    s_key[e] = (uint16_t)p;
-                    s_d[e] = (uint16_t)(p >= c ? p - c : p + B - c);
+    for (uint32_t i = tid; i < kCrcTabs * 256; i += kCB) S.crc[i] = (&g_crc_slice[0][0])[i];
+    for (uint32_t i = tid; i < B * NS; i += kCB) S.freq[i] = 0;
+    const int t0 = (int)((int64_t)blockIdx.x * A.ntiles / gridDim.x);
+    const int t1 = (int)((int64_t)(blockIdx.x + 1) * A.ntiles / gridDim.x);
+    uint32_t cur_tensor = 0xffffffffu;
+
+    for (int ti = t0; ti < t1; ++ti) {
+        const Tile T = A.tiles[ti];
+        const uint32_t cnt = T.count;
+        if (T.tensor != cur_tensor) {  // flush the previous tensor's symbol counts
+            __syncthreads();
+            if (cur_tensor != 0xffffffffu) {
+                uint32_t* gf = A.freq + (size_t)cur_tensor * B * NS;
+                for (uint32_t i = tid; i < B * NS; i += kCB) {
+                    const uint32_t c = S.freq[i];
+                    if (c) {
+                        atomicAdd(gf + i, c);
+                        S.freq[i] = 0;
+                    }
                 }
             }
-            if (bad) atomicOr(A.err, kErrCorruptIndex);
+            cur_tensor = T.tensor;
         }
-    }
-    __syncthreads();
-
-    // ---- CRC of the target levels, tile right-aligned in a virtual 8 KiB block
-    {
-        const int lead0 = 2 * (int)kTile - 2 * (int)cnt;
-        uint32_t r = 0;
-        for (int vb = tid * 32; vb < tid * 32 + 32; vb += 2) {
-            int rb = vb - lead0;  // even: whole levels
-            if (rb < 0) continue;
-            const uint32_t e = (uint32_t)rb >> 1;
-            const uint32_t p = s_key[e], d = s_d[e];
-            const uint32_t lv = p >= d ? p - d : p + B - d;  // target level
-            r = s_tab[(r ^ lv) & 0xff] ^ (r >> 8);
-            r = s_tab[(r ^ (lv >> 8)) & 0xff] ^ (r >> 8);
+        // ---- L
+        for (uint32_t i = tid; i < 8 * B; i += kCB) {
+            S.wcnt[i] = 0;
+            S.lastd[i] = 0xff;
         }
-        r = r ? crc_multmodp(c_crc_pw[tid], r) : 0u;
-        r = warp_xor(r);
-        if (lane == 0) s_red[wid] = r;
+        {
+            const uint32_t e0 = tid * kIt;
+            uint32_t kw[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+            uint32_t dw[4] = {0, 0, 0, 0}, cw[4] = {0, 0, 0, 0};
+            if (e0 < cnt) {
+                uint16_t c16[kIt], p16[kIt];
+                const uint4* cp = (const uint4*)(A.cur + T.start + e0);
+                uint4 a0 = cp[0], a1 = cp[1];
+                memcpy(c16, &a0, 16);
+                memcpy(c16 + 8, &a1, 16);
+                if (HAS_BASE) {
+                    const uint4* pp = (const uint4*)(A.prev + T.start + e0);
+                    uint4 b0 = pp[0], b1 = pp[1];
+                    memcpy(p16, &b0, 16);
+                    memcpy(p16 + 8, &b1, 16);
+                }
+                bool bad = false;
+#pragma unroll
+                for (int j = 0; j < kIt; ++j) {
+                    if (e0 + j < cnt) {
+                        uint32_t c = c16[j], p = HAS_BASE ? p16[j] : 0u;
+                        bad |= (p >= B) | (c >= B);
+                        p = p < B ? p : 0u;
+                        c = c < B ? c : 0u;
+                        const uint32_t d = p >= c ? p - c : p + B - c;
+                        const int sh = 8 * (j & 3);
+                        kw[j >> 2] = (kw[j >> 2] & ~(0xffu << sh)) | (p << sh);
+                        dw[j >> 2] |= d << sh;
+                        cw[j >> 2] |= c << sh;
+                    }
+                }
+                if (bad) atomicOr(A.err, kErrCorruptIndex);
+            }
+            *(uint4*)(S.key + e0) = make_uint4(kw[0], kw[1], kw[2], kw[3]);
+            *(uint4*)(S.d + e0) = make_uint4(dw[0], dw[1], dw[2], dw[3]);
+            *(uint4*)(S.cur + (e0 >> 7) * kCurRow + (e0 & 127)) = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+            *(uint4*)(S.hf + e0) = make_uint4(0, 0, 0, 0);
+        }
         __syncthreads();
-        if (tid == 0) {
-            uint32_t x = 0;
-            for (int w = 0; w < kCB / 32; ++w) x ^= s_red[w];
-            if (x) x = crc_multmodp(A.crc_shift[ti], x);
-            if (x) atomicXor(A.crc_acc, x);
-        }
-    }
-    // ---- stable multisplit on the previous level (rearrange, codec.cpp:39-54):
-    // warp w owns elements [512w, 512w+512) in word order; a per-warp running
-    // count per key gives each element its rank among equal keys of the range.
-    uint32_t rk[kIt];
-    uint16_t ky[kIt];
-    {
-        const uint32_t lt_mask = (1u << lane) - 1u;
-        uint32_t* wc = s_wcnt + wid * B;
-#pragma unroll
-        for (int j = 0; j < kIt; ++j) {
-            const uint32_t e = wid * 512 + j * 32 + lane;
-            const bool valid = e < cnt;
-            const uint32_t key = valid ? s_key[e] : 0xffffu;
-            const uint32_t peers = __match_any_sync(0xffffffffu, key);
-            const int leader = __ffs(peers) - 1;
-            uint32_t old = 0;
-            if (lane == leader && valid) {
-                old = wc[key];
-                wc[key] = old + __popc(peers);
-            }
-            old = __shfl_sync(0xffffffffu, old, leader);
-            rk[j] = old + __popc(peers & lt_mask);
-            ky[j] = (uint16_t)key;
-        }
-    }
-    __syncthreads();
-    // per key: exclusive prefix over warps, then start offsets over keys
-    for (uint32_t b = tid; b < B; b += kCB) {
-        uint32_t acc = 0;
-        for (int w = 0; w < kCB / 32; ++w) {
-            const uint32_t c = s_wcnt[w * B + b];
-            s_wcnt[w * B + b] = acc;
-            acc += c;
-        }
-        s_cnt[b] = acc;
-    }
-    __syncthreads();
-    if (wid == 0) {
-        uint32_t run = 0;
-        for (uint32_t b0 = 0; b0 < B; b0 += 32) {
-            uint32_t b = b0 + lane;
-            uint32_t v = b < B ? s_cnt[b] : 0, x = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            if (b < B) s_start[b] = run + x - v;
-            run += __shfl_sync(0xffffffffu, x, 31);
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kIt; ++j) {
-        const uint32_t e = wid * 512 + j * 32 + lane;
-        if (e < cnt) {
-            const uint32_t key = ky[j];
-            const uint32_t pos = s_start[key] + s_wcnt[wid * B + key] + rk[j];
-            s_sd[pos] = s_d[e];
-            s_sk[pos] = (uint16_t)key;
-        }
-    }
-    __syncthreads();
 
-    // ---- runs inside group segments
-    uint32_t nh = 0;
-    uint32_t hmask = 0;
-    {
-        const uint32_t p0 = tid * kIt;
-        for (int j = 0; j < kIt; ++j) {
-            const uint32_t p = p0 + j;
-            if (p >= cnt) break;
-            const uint32_t b = s_sk[p];
-            const bool head = (p == s_start[b]) || (s_sd[p] != s_sd[p - 1]);
-            if (head) {
-                hmask |= 1u << j;
-                ++nh;
+        // ---- M: rank among equal keys, run-head test against the previous same-key element
+        uint32_t pk[kIt];  // rank | key << 12 | d << 18 | head << 24 | first << 25 | valid << 26
+        {
+            uint32_t* wc = S.wcnt + wid * B;
+            uint8_t* ld = S.lastd + wid * B;
+#pragma unroll
+            for (int j = 0; j < kIt; ++j) {
+                const uint32_t e = wid * 512 + j * 32 + lane;
+                const uint32_t key = S.key[e], d = S.d[e];
+                const bool valid = key != 0xffu;
+                const uint32_t peers = __match_any_sync(0xffffffffu, key);
+                const uint32_t lt = peers & lt_mask;
+                const int leader = __ffs(peers) - 1;
+                uint32_t old = 0;
+                if (lane == leader && valid) {
+                    old = wc[key];
+                    wc[key] = old + __popc(peers);
+                }
+                old = __shfl_sync(0xffffffffu, old, leader);
+                const int src = lt ? 31 - __clz(lt) : lane;
+                uint32_t pd = __shfl_sync(0xffffffffu, d, src);
+                if (!lt && valid) pd = ld[key];
+                __syncwarp();
+                const bool first = !lt && pd == 0xffu;
+                const bool head = !first && pd != d;
+                if (valid && lane == 31 - __clz(peers)) ld[key] = (uint8_t)d;
+                if (valid && first) S.firstd[wid * B + key] = (uint8_t)d;
+                __syncwarp();
+                pk[j] = valid ? ((old + __popc(lt)) | (key << 12) | (d << 18) | ((uint32_t)head << 24) |
+                                 ((uint32_t)first << 25) | (1u << 26))
+                              : 0u;
             }
         }
-    }
-    unsigned long long R;
-    unsigned long long hex = block_exclusive_scan<unsigned long long>(nh, s_scan, &R);
-    {
-        uint32_t r = (uint32_t)hex;
-        const uint32_t p0 = tid * kIt;
-        for (int j = 0; j < kIt; ++j)
-            if (hmask >> j & 1) s_hp[r++] = (uint16_t)(p0 + j);
-    }
-    if (tid == 0) s_hp[R] = (uint16_t)cnt;
-    __syncthreads();
-    unsigned long long* runs = A.runs + (size_t)ti * kTile;
-    for (uint32_t r = tid; r < R; r += kCB) {
-        const uint32_t p = s_hp[r], L = s_hp[r + 1] - p;
-        const uint32_t v = s_sd[p], b = s_sk[p];
-        runs[r] = (unsigned long long)v | ((unsigned long long)b << 16) |
-                  ((unsigned long long)L << 32);
-        if (p == s_start[b]) s_run0[b] = r;
-        if (p + L == s_start[b] + s_cnt[b]) s_run1[b] = r;
-    }
-    __syncthreads();
-    const uint32_t tensor = T.tensor;
-    for (uint32_t r = tid; r < R; r += kCB) {
-        const uint32_t p = s_hp[r], L = s_hp[r + 1] - p;
-        const uint32_t v = s_sd[p], b = s_sk[p];
-        if (r != s_run0[b] && r != s_run1[b])
-            add_symbol(s_freq + b * NS, NS, B, tensor * B + b, v, L, A);
-    }
-    if (tid == 0) A.tile_nruns[ti] = (uint32_t)R;
-    __syncthreads();
-    for (uint32_t b = tid; b < B; b += kCB) {
-        Seg S{};
-        S.n = s_cnt[b];
-        if (S.n) {
-            const uint32_t st = s_start[b];
-            S.fv = s_sd[st];
-            S.lv = s_sd[st + S.n - 1];
-            S.run_begin = s_run0[b];
-            S.run_end = s_run1[b] + 1;
-            S.lead = s_hp[S.run_begin + 1] - s_hp[S.run_begin];
-            S.trail = s_hp[S.run_end] - s_hp[S.run_end - 1];
+        // ---- C: CRC of the target levels (warp 0 after its M share)
+        if (wid == 0) {
+            const int off = (int)kTile - (int)cnt;  // virtual right alignment: leading levels 0
+            uint32_t r = 0;
+            for (int blk = 0; blk < 16; ++blk) {
+                const int v0 = lane * 128 + blk * 8;  // virtual level index
+                uint32_t lo[8];
+                if (off == 0) {
+                    const uint2 q = *(const uint2*)(S.cur + lane * kCurRow + blk * 8);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        lo[j] = (q.x >> (8 * j)) & 0xff;
+                        lo[4 + j] = (q.y >> (8 * j)) & 0xff;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int e = v0 + j - off;
+                        lo[j] = e >= 0 ? S.cur[(e >> 7) * kCurRow + (e & 127)] : 0u;
+                    }
+                }
+                r = crc_block8(S.crc, r, lo);
+            }
+            r = r ? crc_multmodp(c_crc_pw32[lane], r) : 0u;
+            r = warp_xor(r);
+            if (lane == 0 && r) {
+                r = crc_multmodp(A.crc_shift[ti], r);
+                if (r) atomicXor(A.crc_acc, r);
+            }
         }
-        A.segs[(size_t)ti * B + b] = S;
+        __syncthreads();
+        // ---- P + F: per key prefix over warps; first-in-warp heads against the
+        // last element of the nearest earlier warp holding the key
+        for (uint32_t b = tid; b < B; b += kCB) {
+            uint32_t acc = 0, last = 0xffu;
+            for (int w = 0; w < kCB / 32; ++w) {
+                const uint32_t c = S.wcnt[w * B + b];
+                S.wcnt[w * B + b] = acc;
+                acc += c;
+                if (c) {
+                    S.fhead[w * B + b] = (last == 0xffu) || (S.firstd[w * B + b] != last);
+                    last = S.lastd[w * B + b];
+                }
+            }
+            s_cnt[b] = acc;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t run = 0;
+            for (uint32_t b0 = 0; b0 < B; b0 += 32) {
+                const uint32_t b = b0 + lane;
+                const uint32_t v = b < B ? s_cnt[b] : 0;
+                uint32_t x = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (b < B) s_start[b] = run + x - v;
+                run += __shfl_sync(0xffffffffu, x, 31);
+            }
+        }
+        __syncthreads();
+        // ---- H: place run heads at their rearranged positions
+#pragma unroll
+        for (int j = 0; j < kIt; ++j) {
+            const uint32_t q = pk[j];
+            if (!(q >> 26)) continue;
+            const uint32_t key = (q >> 12) & 63u;
+            const bool h = (q >> 24) & 1u ? true : ((q >> 25) & 1u ? S.fhead[wid * B + key] != 0 : false);
+            if (h) {
+                const uint32_t pos = s_start[key] + S.wcnt[wid * B + key] + (q & 4095u);
+                S.hf[pos] = 1;
+                S.hv[pos] = (uint8_t)((q >> 18) & 63u);
+                S.hk[pos] = (uint8_t)key;
+            }
+        }
+        __syncthreads();
+        // ---- B: run start positions in rearranged order
+        uint32_t R;
+        {
+            const uint32_t p0 = tid * kIt;
+            const uint4 f = *(const uint4*)(S.hf + p0);
+            const uint32_t fw[4] = {f.x, f.y, f.z, f.w};
+            uint32_t m = 0;
+#pragma unroll
+            for (int j = 0; j < kIt; ++j) m |= ((fw[j >> 2] >> (8 * (j & 3))) & 1u) << j;
+            unsigned long long tot;
+            uint32_t r = (uint32_t)block_exclusive_scan<unsigned long long>(__popc(m), s_scan, &tot);
+            R = (uint32_t)tot;
+            while (m) {
+                const int j = __ffs(m) - 1;
+                m &= m - 1;
+                S.hp[r++] = (uint16_t)(p0 + j);
+            }
+            if (tid == 0) S.hp[R] = (uint16_t)cnt;
+        }
+        __syncthreads();
+        // ---- R: runs, first/last run of every group, interior-run symbols
+        unsigned long long* runs = A.runs + (size_t)ti * kTile;
+        for (uint32_t r = tid; r < R; r += kCB) {
+            const uint32_t p = S.hp[r], L = S.hp[r + 1] - p;
+            const uint32_t v = S.hv[p], b = S.hk[p];
+            runs[r] = (unsigned long long)v | ((unsigned long long)b << 16) |
+                      ((unsigned long long)L << 32);
+            if (p == s_start[b]) s_run0[b] = r;
+            if (p + L == s_start[b] + s_cnt[b]) s_run1[b] = r;
+        }
+        __syncthreads();
+        for (uint32_t r = tid; r < R; r += kCB) {
+            const uint32_t p = S.hp[r], L = S.hp[r + 1] - p;
+            const uint32_t v = S.hv[p], b = S.hk[p];
+            if (r != s_run0[b] && r != s_run1[b])
+                add_symbol(S.freq + b * NS, NS, B, cur_tensor * B + b, v, L, A);
+        }
+        if (tid == 0) A.tile_nruns[ti] = R;
+        for (uint32_t b = tid; b < B; b += kCB) {
+            Seg G{};
+            G.n = s_cnt[b];
+            if (G.n) {
+                G.run_begin = s_run0[b];
+                G.run_end = s_run1[b] + 1;
+                const uint32_t pb = S.hp[G.run_begin], pe = S.hp[G.run_end - 1];
+                G.fv = S.hv[pb];
+                G.lv = S.hv[pe];
+                G.lead = S.hp[G.run_begin + 1] - pb;
+                G.trail = S.hp[G.run_end] - pe;
+            }
+            A.segs[(size_t)ti * B + b] = G;
+        }
+        __syncthreads();
     }
-    uint32_t* gf = A.freq + (size_t)tensor * B * NS;
-    for (uint32_t i = tid; i < B * NS; i += kCB) {
-        uint32_t c = s_freq[i];
-        if (c) atomicAdd(gf + i, c);
+    if (cur_tensor != 0xffffffffu) {
+        uint32_t* gf = A.freq + (size_t)cur_tensor * B * NS;
+        for (uint32_t i = tid; i < B * NS; i += kCB) {
+            const uint32_t c = S.freq[i];
+            if (c) atomicAdd(gf + i, c);
+        }
     }
 }
 
@@ -1223,6 +1337,22 @@ static void init_crc_consts() {
     uint32_t pw[kCB];
     for (int t = 0; t < kCB; ++t) pw[t] = crc_x2nmodp(x.t, (uint64_t)32 * (kCB - 1 - t), 3);
     DQTG_CUDA(cudaMemcpyToSymbol(c_crc_pw, pw, sizeof(pw)));
+    uint32_t pw32[32];
+    for (int l = 0; l < 32; ++l) pw32[l] = crc_x2nmodp(x.t, (uint64_t)256 * (31 - l), 3);
+    DQTG_CUDA(cudaMemcpyToSymbol(c_crc_pw32, pw32, sizeof(pw32)));
+    // zero-skipping slice-by-16 tables T1,T3,...,T11,T12..T15 (T_n: byte then n zero bytes)
+    static uint32_t tn[16][256];
+    for (uint32_t b = 0; b < 256; ++b) {
+        uint32_t c = b;
+        for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xedb88320u ^ (c >> 1) : c >> 1;
+        tn[0][b] = c;
+    }
+    for (int n = 1; n < 16; ++n)
+        for (uint32_t b = 0; b < 256; ++b) tn[n][b] = (tn[n - 1][b] >> 8) ^ tn[0][tn[n - 1][b] & 0xff];
+    static const int pick[kCrcTabs] = {1, 3, 5, 7, 9, 11, 12, 13, 14, 15};
+    static uint32_t sl[kCrcTabs][256];
+    for (int i = 0; i < kCrcTabs; ++i) memcpy(sl[i], tn[pick[i]], sizeof(sl[i]));
+    DQTG_CUDA(cudaMemcpyToSymbol(g_crc_slice, sl, sizeof(sl)));
     DQTG_CUDA(cudaMemcpyToSymbol(c_crc_x2n, x.t, sizeof(x.t)));
     crc_consts_ready = true;
 }
@@ -1357,17 +1487,16 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     DQTG_CUDA(cudaMemsetAsync(A.freq, 0, freq_n * 4, st));
     DQTG_CUDA(cudaMemsetAsync(small, 0, 64, st));
 
-    // E1
-    const size_t e1_smem = (size_t)((B * NS + 3) & ~3u) * 4 + (size_t)8 * B * 4 + (size_t)kTile * 2 * 3 +
-                           (kTile + 2) * 2 + 16;
-    if (base) {
-        DQTG_CUDA(cudaFuncSetAttribute(enc_tile_kernel<true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e1_smem));
-        { DQTG_SPAN(e, "enc_tile_kernel"); enc_tile_kernel<true><<<ntiles, kCB, e1_smem, st>>>(A); }
-    } else {
-        DQTG_CUDA(cudaFuncSetAttribute(enc_tile_kernel<false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e1_smem));
-        { DQTG_SPAN(e, "enc_tile_kernel"); enc_tile_kernel<false><<<ntiles, kCB, e1_smem, st>>>(A); }
+    // E1 (persistent CTAs)
+    const size_t e1_smem = e1_smem_bytes(B, NS);
+    A.ntiles = ntiles;
+    {
+        auto kfn = base ? enc_tile_kernel<true> : enc_tile_kernel<false>;
+        DQTG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e1_smem));
+        int per_sm = 0;
+        DQTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kCB, e1_smem));
+        const int grid = std::max(1, std::min(ntiles, e.num_sms * std::max(1, per_sm)));
+        { DQTG_SPAN(e, "enc_tile_kernel"); kfn<<<grid, kCB, e1_smem, st>>>(A); }
     }
     // S
     {

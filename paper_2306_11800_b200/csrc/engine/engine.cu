@@ -1,4 +1,5 @@
 // Engine plumbing: device/stream, scratch, alpha tables, layouts, object lifetimes.
+#include <algorithm>
 #include <float.h>
 #include <math.h>
 #include <string.h>
@@ -34,6 +35,7 @@ Engine::~Engine() {
     for (auto& kv : scratch) cudaFree(kv.second.first);
     for (auto& kv : tables) {
         cudaFree(kv.second->d_U);
+        cudaFree(kv.second->d_cell);
         cudaFree(kv.second->d_key);
         cudaFree(kv.second->d_keyf);
     }
@@ -191,7 +193,39 @@ AlphaTables& Engine::alpha_tables(double alpha) {
         t->kw_lo = lo;
     }
     t->inv_log2_gamma = (float)(1.0 / log2(t->gamma));
+    // Cell table (see AlphaTables): the coarsest cell width whose cells all span
+    // at most two buckets, each cell checked against U (exact integer compares).
+    std::vector<uint2> cells;
+    auto ubits = [&](int64_t k) { return U[(size_t)(k - t->kmin + 1)]; };
+    auto host_bucket = [&](uint32_t a) {  // smallest k in [kmin, kmax] with U(k) >= a
+        int64_t lo = t->kmin, hi = t->kmax;
+        while (lo < hi) {
+            int64_t mid = lo + (hi - lo) / 2;
+            if (ubits(mid) >= a) hi = mid;
+            else lo = mid + 1;
+        }
+        return lo;
+    };
+    for (uint32_t m = 4; m <= 12 && !t->cell_shift; ++m) {
+        const uint32_t shift = 23 - m, ncell = 0x7f800000u >> shift;
+        cells.assign(ncell, uint2{0, 0xffffffffu});
+        bool ok = true;
+        for (uint32_t c = 0; c < ncell && ok; ++c) {
+            const uint32_t a0 = std::max(c << shift, t->zbits), a1 = ((c + 1) << shift) - 1;
+            if (a1 < t->zbits) continue;  // zero bucket, handled before the lookup
+            const int64_t k0 = host_bucket(a0), k1 = host_bucket(a1);
+            if (k1 > k0 + 1) ok = false;
+            cells[c].x = (uint32_t)(int32_t)k0;
+            cells[c].y = k1 == k0 ? 0xffffffffu : ubits(k0);
+        }
+        if (ok) t->cell_shift = shift;
+    }
     activate();
+    if (t->cell_shift) {
+        DQTG_CUDA(cudaMalloc(&t->d_cell, cells.size() * sizeof(uint2)));
+        DQTG_CUDA(cudaMemcpy(t->d_cell, cells.data(), cells.size() * sizeof(uint2),
+                             cudaMemcpyHostToDevice));
+    }
     DQTG_CUDA(cudaMalloc(&t->d_U, U.size() * 4));
     DQTG_CUDA(cudaMalloc(&t->d_key, t->h_key.size() * 8));
     DQTG_CUDA(cudaMalloc(&t->d_keyf, keyf.size() * 4));

@@ -37,6 +37,12 @@ struct AlphaTables {
     double* d_key = nullptr;     // representative value per signed slot (sketch.cpp:33-37)
     float* d_keyf = nullptr;     // largest float <= key (threshold compare, §7 H2)
     std::vector<double> h_key;
+    // Cell table: |x| bits >> cell_shift index cells of 2^cell_shift floats, each
+    // spanning at most two buckets; entry = {k of the cell's first float, last
+    // float bits of that bucket inside the cell (0xffffffff: whole cell)}.
+    // bucket(a) = k + (a > split), one load instead of log2 + table probes.
+    uint32_t cell_shift = 0;     // 0: no table (alpha too small), probe U instead
+    uint2* d_cell = nullptr;
 };
 
 // Device view of the bucket tables passed by value to kernels.
@@ -45,6 +51,8 @@ struct BucketTab {
     int64_t kmin, kmax, NB, kw_lo;
     uint32_t zbits;
     float inv_log2_gamma;
+    const uint2* cell;  // null: probe U
+    uint32_t cell_shift;
 };
 
 struct Engine;
@@ -143,7 +151,8 @@ struct Engine {
     void activate() const { DQTG_CUDA(cudaSetDevice(device)); }
     AlphaTables& alpha_tables(double alpha);
     BucketTab bucket_tab(const AlphaTables& t) const {
-        return BucketTab{t.d_U, t.kmin, t.kmax, t.NB, t.kw_lo, t.zbits, t.inv_log2_gamma};
+        return BucketTab{t.d_U, t.kmin, t.kmax, t.NB, t.kw_lo, t.zbits, t.inv_log2_gamma, t.d_cell,
+                         t.cell_shift};
     }
     void* buf(const std::string& name, size_t bytes);  // scratch, contents undefined
     // stream-ordered pool allocations for per-step objects (states, records)

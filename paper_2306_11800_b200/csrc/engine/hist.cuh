@@ -9,6 +9,10 @@ namespace dqtg {
 // log2 estimate is within one bucket; integer compares against the boundary
 // table make the result exact.
 __device__ __forceinline__ int bucket_of(uint32_t a, const BucketTab& t) {
+    if (t.cell) {  // one cell lookup (AlphaTables::d_cell)
+        const uint2 c = __ldg(t.cell + (a >> t.cell_shift));
+        return (int)c.x + (a > c.y ? 1 : 0);
+    }
     const int kmin = (int)t.kmin, kmax = (int)t.kmax;
     float lg = __log2f(__uint_as_float(a));
     int k = (int)ceilf(lg * t.inv_log2_gamma);

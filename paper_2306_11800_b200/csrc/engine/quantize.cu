@@ -60,7 +60,7 @@ __device__ __forceinline__ void load_scores(const PassIn& a, uint64_t idx, const
 // ---- pass A: score histograms ----------------------------------------------
 // Derived scores are non-negative: half-size windows (kPosSlots) per histogram.
 template <bool EXPL>
-__global__ void __launch_bounds__(kPB) pass_a_kernel(PassIn a, unsigned long long* gh_mag,
+__global__ void __launch_bounds__(kPB, 6) pass_a_kernel(PassIn a, unsigned long long* gh_mag,
                                                      unsigned long long* gh_sens,
                                                      uint32_t mask_mag, uint32_t mask_sens) {
     extern __shared__ uint32_t sh[];
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(1024) quantile_kernel(const QJob* jobs, int64_
 
 // ---- pass B: partition + QUANTIZE value histogram + protected counts --------
 template <bool EXPL>
-__global__ void __launch_bounds__(kPB) pass_b_kernel(PassIn a, const LtParams* lp,
+__global__ void __launch_bounds__(kPB, 6) pass_b_kernel(PassIn a, const LtParams* lp,
                                                      unsigned long long* gh_val,
                                                      uint32_t* tile_prot,
                                                      unsigned long long* tensor_prot) {
@@ -269,30 +269,80 @@ __device__ __forceinline__ uint32_t nearest_center(const float* c, uint32_t k, f
     return (__fsub_rn(c[lo], v) < __fsub_rn(v, c[lo - 1])) ? lo : lo - 1;
 }
 
+// Level boundaries: nearest_center is monotone non-decreasing in v (lower_bound
+// plus a half-gap compare whose two sides move in opposite directions), so it is
+// fully described by T[j] = smallest float (in value order) with level >= j,
+// j = 1..k-1: level(v) = #{j : v >= T[j]}.  One thread per boundary finds T[j]
+// by bisection over the ordered float encoding, evaluating the reference rule
+// itself; -0.0 and +0.0 get the same level (they compare equal everywhere in
+// the rule), so a float compare against T[j] is exact for every finite v.
+__device__ __forceinline__ uint32_t ord_of(float f) {
+    uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float float_of_ord(uint32_t o) {
+    return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+}
+
+__global__ void __launch_bounds__(64) level_bounds_kernel(const float* cb, int cb_stride,
+                                                          const uint32_t* cb_len, float* lb,
+                                                          int lb_stride) {
+    extern __shared__ float s_c[];
+    const int lt = blockIdx.x;
+    const uint32_t k = cb_len[lt];
+    for (uint32_t j = threadIdx.x; j < k; j += blockDim.x) s_c[j] = cb[lt * cb_stride + j];
+    __syncthreads();
+    for (int j = threadIdx.x; j < lb_stride; j += blockDim.x) {
+        float t = __int_as_float(0x7f800000);  // +inf: never reached by a finite value
+        if (j >= 1 && (uint32_t)j < k) {
+            uint32_t lo = ord_of(-__int_as_float(0x7f800000)), hi = ord_of(__int_as_float(0x7f800000));
+            while (lo < hi) {  // level(float_of_ord(hi)) >= j holds throughout
+                const uint32_t mid = lo + ((hi - lo) >> 1);
+                if (nearest_center(s_c, k, float_of_ord(mid)) >= (uint32_t)j) hi = mid;
+                else lo = mid + 1;
+            }
+            t = float_of_ord(lo);
+        }
+        lb[lt * lb_stride + j] = t;
+    }
+}
+
+// Level of a QUANTIZE value from the boundaries (P = power of two >= k, T[j] =
+// +inf for j >= k): branch-free bisection, log2(P) shared loads.
+__device__ __forceinline__ uint32_t level_of(const float* T, uint32_t P, float v) {
+    uint32_t pos = 0;
+    for (uint32_t st = P >> 1; st > 0; st >>= 1) pos += (v >= T[pos + st]) ? st : 0u;
+    return pos;
+}
+
+__host__ __device__ __forceinline__ uint32_t pow2_ceil(uint32_t k) {
+    uint32_t p = 1;
+    while (p < k) p <<= 1;
+    return p;
+}
+
 __device__ __forceinline__ uint16_t bf16_rne(float v) {  // quantize.cpp:337-342
     uint32_t bits = __float_as_uint(v);
     bits += 0x7fffu + ((bits >> 16) & 1u);
     return (uint16_t)(bits >> 16);
 }
 
-template <bool EXPL>
-__global__ void __launch_bounds__(kPB) pass_c_kernel(PassIn a, const LtParams* lp,
-                                                     const float* cb, int cb_stride,
-                                                     const uint32_t* cb_len,
-                                                     const unsigned long long* tile_prot_off,
-                                                     uint16_t* levels, uint64_t* ppos,
-                                                     uint16_t* pval) {
-    extern __shared__ float s_cb[];
-    __shared__ unsigned long long s_scan[33];
-    const int ti = blockIdx.x;
-    const Tile T = a.tiles[ti];
-    const int lt = a.types[T.tensor];
-    const uint32_t k = cb_len[lt];
-    for (uint32_t j = threadIdx.x; j < k; j += blockDim.x) s_cb[j] = cb[lt * cb_stride + j];
-    const LtParams P = lp[lt];
-    const uint64_t tensor_base = a.tensor_off[T.tensor];
-    __syncthreads();
-    unsigned long long out = tile_prot_off[ti];
+template <int LOGP>
+__device__ __forceinline__ uint32_t level_fixed(const float* T, float v, uint32_t kp) {
+    if (LOGP < 0) return level_of(T, kp, v);  // k > 64: runtime bisection
+    uint32_t pos = 0;
+#pragma unroll
+    for (int st = (1 << LOGP) >> 1; st > 0; st >>= 1) pos += (v >= T[pos + st]) ? (uint32_t)st : 0u;
+    return pos;
+}
+
+// One tile of pass C with the level bisection unrolled for P = 2^LOGP.
+template <bool EXPL, int LOGP>
+__device__ __forceinline__ void pass_c_tile(const PassIn& a, const LtParams& P, const Tile& T,
+                                            uint32_t k, const float* s_lb, uint64_t tensor_base,
+                                            unsigned long long out,
+                                            unsigned long long* s_scan, uint16_t* levels,
+                                            uint64_t* ppos, uint16_t* pval) {
     // two float4 groups per thread and iteration; protected entries keep element
     // order: group 0 (i0..i0+1023) before group 1, one packed (lo|hi) scan
     for (uint32_t i0 = 0; i0 < T.count; i0 += kPB * 8) {
@@ -300,7 +350,6 @@ __global__ void __launch_bounds__(kPB) pass_c_kernel(PassIn a, const LtParams* l
         float wa[2][4];
         for (int g = 0; g < 2; ++g) {
             const uint32_t i = i0 + g * kPB * 4 + threadIdx.x * 4;
-            uint16_t lv[4] = {0, 0, 0, 0};
             wa[g][0] = wa[g][1] = wa[g][2] = wa[g][3] = 0.0f;
             if (i < T.count) {
                 const uint64_t idx = T.start + i;
@@ -308,20 +357,18 @@ __global__ void __launch_bounds__(kPB) pass_c_kernel(PassIn a, const LtParams* l
                 float m[4], s[4];
                 load_scores<EXPL>(a, idx, wv, m, s);
                 wa[g][0] = wv.x, wa[g][1] = wv.y, wa[g][2] = wv.z, wa[g][3] = wv.w;
+                uint32_t lv[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    if (i + j >= T.count) break;
-                    int part = classify(m[j], s[j], a.has_sens, a.metric, P);
-                    if (part == 0) lv[j] = (uint16_t)nearest_center(s_cb, k, wa[g][j]);
-                    else if (part == 1) lv[j] = (uint16_t)k;
-                    else {
-                        lv[j] = (uint16_t)(k + 1);
-                        flags[g] |= 1u << j;
-                    }
+                    // level for every element (branch-free), then the partition decides
+                    const uint32_t q = level_fixed<LOGP>(s_lb, wa[g][j], pow2_ceil(k));
+                    const int part = classify(m[j], s[j], a.has_sens, a.metric, P);
+                    lv[j] = part == 0 ? q : (part == 1 ? k : k + 1);
+                    if (part == 2 && i + j < T.count) flags[g] |= 1u << j;
                 }
                 uint2 pk;
-                pk.x = (uint32_t)lv[0] | ((uint32_t)lv[1] << 16);
-                pk.y = (uint32_t)lv[2] | ((uint32_t)lv[3] << 16);
+                pk.x = lv[0] | (lv[1] << 16);
+                pk.y = lv[2] | (lv[3] << 16);
                 *(uint2*)(levels + idx) = pk;
             }
         }
@@ -343,6 +390,33 @@ __global__ void __launch_bounds__(kPB) pass_c_kernel(PassIn a, const LtParams* l
                 }
         }
         out += tot0 + (tot >> 32);
+    }
+}
+
+template <bool EXPL>
+__global__ void __launch_bounds__(kPB) pass_c_kernel(PassIn a, const LtParams* lp,
+                                                     const float* lb, int lb_stride,
+                                                     const uint32_t* cb_len,
+                                                     const unsigned long long* tile_prot_off,
+                                                     uint16_t* levels, uint64_t* ppos,
+                                                     uint16_t* pval) {
+    extern __shared__ float s_lb[];
+    __shared__ unsigned long long s_scan[33];
+    const int ti = blockIdx.x;
+    const Tile T = a.tiles[ti];
+    const int lt = a.types[T.tensor];
+    const uint32_t k = cb_len[lt], kp = pow2_ceil(k);
+    for (uint32_t j = threadIdx.x; j < kp; j += blockDim.x) s_lb[j] = lb[lt * lb_stride + j];
+    const LtParams P = lp[lt];
+    const uint64_t tensor_base = a.tensor_off[T.tensor];
+    __syncthreads();
+    const unsigned long long out = tile_prot_off[ti];
+    switch (__ffs(kp) - 1) {
+#define DQTG_PC(L) \
+    case L: pass_c_tile<EXPL, L>(a, P, T, k, s_lb, tensor_base, out, s_scan, levels, ppos, pval); break;
+        DQTG_PC(0) DQTG_PC(1) DQTG_PC(2) DQTG_PC(3) DQTG_PC(4) DQTG_PC(5) DQTG_PC(6)
+#undef DQTG_PC
+        default: pass_c_tile<EXPL, -1>(a, P, T, k, s_lb, tensor_base, out, s_scan, levels, ppos, pval);
     }
 }
 
@@ -415,18 +489,21 @@ __device__ __forceinline__ double block_sum_d(double v, double* red) {
 
 template <bool EXPL>
 __global__ void __launch_bounds__(kPB) eval_c_kernel(PassIn a, const LtParams* lp, const float* cb,
-                                                     int cb_stride, const uint32_t* cb_len,
+                                                     int cb_stride, const float* lb, int lb_stride,
+                                                     const uint32_t* cb_len,
                                                      double* tile_diff,
                                                      unsigned long long* lvl_counts,
                                                      int lstride) {
-    extern __shared__ float s_cb[];
+    extern __shared__ float s_cb[];  // [cb_stride] codebook, then [kp] level bounds
     __shared__ double s_red[kPB / 32];
     __shared__ uint32_t s_cnt[66];
     const int ti = blockIdx.x;
     const Tile T = a.tiles[ti];
     const int lt = a.types[T.tensor];
-    const uint32_t k = cb_len[lt];
+    const uint32_t k = cb_len[lt], kp = pow2_ceil(k);
+    float* s_lb = s_cb + cb_stride;
     for (uint32_t j = threadIdx.x; j < k; j += blockDim.x) s_cb[j] = cb[lt * cb_stride + j];
+    for (uint32_t j = threadIdx.x; j < kp; j += blockDim.x) s_lb[j] = lb[lt * lb_stride + j];
     for (int j = threadIdx.x; j < 66; j += blockDim.x) s_cnt[j] = 0;
     const LtParams P = lp[lt];
     __syncthreads();
@@ -444,7 +521,7 @@ __global__ void __launch_bounds__(kPB) eval_c_kernel(PassIn a, const LtParams* l
             uint32_t lv;
             float deq;
             if (part == 0) {
-                lv = nearest_center(s_cb, k, wa[j]);
+                lv = level_of(s_lb, kp, wa[j]);
                 deq = s_cb[lv];
             } else if (part == 1) {
                 lv = k;
@@ -603,6 +680,8 @@ struct Stage {
     float* d_cb = nullptr;  // [7][cb_stride]
     uint32_t cb_stride = 1;
     uint32_t* cb_len = nullptr;
+    float* d_lb = nullptr;  // [7][lb_stride] level boundaries (level_bounds_kernel)
+    uint32_t lb_stride = 1;
 };
 
 static void stage_alloc(Engine& e, const Layout& L, int64_t HS, Stage& s, float* cb_dst) {
@@ -620,6 +699,14 @@ static void stage_alloc(Engine& e, const Layout& L, int64_t HS, Stage& s, float*
     s.cb_len = (uint32_t*)e.buf(t + "cblen", kLayerTypes * 4);
     s.cb_stride = std::max(1u, std::max(s.cfg.bins, s.cfg.embed_bins));
     s.d_cb = cb_dst ? cb_dst : (float*)e.buf(t + "cb", (size_t)kLayerTypes * s.cb_stride * 4);
+    s.lb_stride = pow2_ceil(s.cb_stride);
+    s.d_lb = (float*)e.buf(t + "lb", (size_t)kLayerTypes * s.lb_stride * 4);
+}
+
+// level boundaries of every layer type's final codebook
+static void stage_level_bounds(Engine& e, Stage& s) {
+    { DQTG_SPAN(e, "level_bounds_kernel"); level_bounds_kernel<<<kLayerTypes, 64, s.cb_stride * 4 + 16, e.stream>>>(s.d_cb, (int)s.cb_stride, s.cb_len, s.d_lb, (int)s.lb_stride); }
+    e.launched();
 }
 
 // pass A into gh_mag/gh_sens ([7][HS] each) for the given masks
@@ -637,6 +724,8 @@ static void stage_pass_a(Engine& e, const DevCkpt& c, const PassIn& a, uint32_t 
     } else {
         const size_t smem = (size_t)2 * kPosSlots * 4;
         const int grid = stream_grid(e, ntiles, 6);
+        DQTG_CUDA(cudaFuncSetAttribute(pass_a_kernel<false>,
+                                       cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         { DQTG_SPAN(e, "pass_a_kernel"); pass_a_kernel<false><<<grid, kPB, smem, st>>>(a, gh_mag, gh_sens, mask_mag, mask_sens); }
     }
     e.launched();
@@ -679,6 +768,8 @@ static void stage_pass_b(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s,
     DQTG_CUDA(cudaMemsetAsync(s.tensor_prot, 0, (size_t)(L.nt + 1) * 8, st));
     const size_t smem = (size_t)kWinSlots * 4;
     int grid = stream_grid(e, ntiles, 6);
+    DQTG_CUDA(cudaFuncSetAttribute(pass_b_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    DQTG_CUDA(cudaFuncSetAttribute(pass_b_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     if (ntiles) {
         if (c.explicit_scores)
             { DQTG_SPAN(e, "pass_b_kernel"); pass_b_kernel<true><<<grid, kPB, smem, st>>>(a, s.d_lp, s.gh_val, s.tile_prot, s.tensor_prot); }
@@ -742,11 +833,12 @@ static void stage_codebooks(Engine& e, std::vector<Stage*>& stages, const PassIn
 static void stage_pass_c(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s, QState& q) {
     const int ntiles = a.ntiles;
     cudaStream_t st = e.stream;
-    const size_t smem = (size_t)s.cb_stride * 4 + 16;
+    stage_level_bounds(e, s);
+    const size_t smem = (size_t)s.lb_stride * 4 + 16;
     if (c.explicit_scores)
-        { DQTG_SPAN(e, "pass_c_kernel"); pass_c_kernel<true><<<ntiles, kPB, smem, st>>>(a, s.d_lp, s.d_cb, (int)s.cb_stride, s.cb_len, s.tile_off, q.d_levels, q.d_ppos, q.d_pval); }
+        { DQTG_SPAN(e, "pass_c_kernel"); pass_c_kernel<true><<<ntiles, kPB, smem, st>>>(a, s.d_lp, s.d_lb, (int)s.lb_stride, s.cb_len, s.tile_off, q.d_levels, q.d_ppos, q.d_pval); }
     else
-        { DQTG_SPAN(e, "pass_c_kernel"); pass_c_kernel<false><<<ntiles, kPB, smem, st>>>(a, s.d_lp, s.d_cb, (int)s.cb_stride, s.cb_len, s.tile_off, q.d_levels, q.d_ppos, q.d_pval); }
+        { DQTG_SPAN(e, "pass_c_kernel"); pass_c_kernel<false><<<ntiles, kPB, smem, st>>>(a, s.d_lp, s.d_lb, (int)s.lb_stride, s.cb_len, s.tile_off, q.d_levels, q.d_ppos, q.d_pval); }
     e.launched();
     DQTG_CUDA(cudaGetLastError());
 }
@@ -1061,11 +1153,12 @@ void eval_batch(Engine& e, const DevCkpt& c, const dqtg_config* cfgs, const uint
         AlphaTables& T = e.alpha_tables(s.cfg.alpha);
         PassIn a = pass_in(e, c, T, (int)s.cfg.metric);
         DQTG_CUDA(cudaMemsetAsync(counts, 0, (size_t)L.nt * lstride * 8, e.stream));
-        const size_t smem = (size_t)s.cb_stride * 4 + 16;
+        stage_level_bounds(e, s);
+        const size_t smem = (size_t)(s.cb_stride + s.lb_stride) * 4 + 16;
         if (c.explicit_scores)
-            { DQTG_SPAN(e, "eval_c_kernel"); eval_c_kernel<true><<<ntiles, kPB, smem, e.stream>>>(a, s.d_lp, s.d_cb, (int)s.cb_stride, s.cb_len, tile_v, counts, lstride); }
+            { DQTG_SPAN(e, "eval_c_kernel"); eval_c_kernel<true><<<ntiles, kPB, smem, e.stream>>>(a, s.d_lp, s.d_cb, (int)s.cb_stride, s.d_lb, (int)s.lb_stride, s.cb_len, tile_v, counts, lstride); }
         else
-            { DQTG_SPAN(e, "eval_c_kernel"); eval_c_kernel<false><<<ntiles, kPB, smem, e.stream>>>(a, s.d_lp, s.d_cb, (int)s.cb_stride, s.cb_len, tile_v, counts, lstride); }
+            { DQTG_SPAN(e, "eval_c_kernel"); eval_c_kernel<false><<<ntiles, kPB, smem, e.stream>>>(a, s.d_lp, s.d_cb, (int)s.cb_stride, s.d_lb, (int)s.lb_stride, s.cb_len, tile_v, counts, lstride); }
         { DQTG_SPAN(e, "lt_sum_kernel"); lt_sum_kernel<<<1, 512, 0, e.stream>>>(L.d_tiles, L.d_types, ntiles, tile_v, d_lt); }
         e.launched(2);
         uint32_t cbl[kLayerTypes];
