@@ -1,5 +1,6 @@
 // extern "C" surface of libdqtg.so (include/dqtg.h).  Every entry point catches
 // internal failures and turns them into a dqtg_status + thread-local message.
+#include <cstdlib>
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -109,6 +110,14 @@ dqtg_status dqtg_engine_profile_report(dqtg_engine* h, char* json, uint64_t cap)
         Engine& e = h->e;
         e.sync();
         std::vector<std::pair<std::string, std::pair<uint64_t, double>>> acc;
+        if (getenv("DQTG_TIMELINE") && !e.spans.empty()) {  // per-launch start/end (ms) on stderr
+            for (auto& s : e.spans) {
+                float a = 0.0f, b = 0.0f;
+                DQTG_CUDA(cudaEventElapsedTime(&a, e.spans[0].a, s.a));
+                DQTG_CUDA(cudaEventElapsedTime(&b, e.spans[0].a, s.b));
+                fprintf(stderr, "timeline %9.3f %9.3f %8.3f %s\n", a, b, b - a, s.name);
+            }
+        }
         for (auto& s : e.spans) {
             float ms = 0.0f;
             DQTG_CUDA(cudaEventElapsedTime(&ms, s.a, s.b));

@@ -64,6 +64,7 @@ struct EncArgs {
     unsigned long long* ov_count;
     unsigned long long ov_cap;
     uint32_t* crc_acc;
+    uint32_t* tile_crc;  // per tile, zero register, ending at the tile's last byte
     uint32_t* err;
 };
 
@@ -104,62 +105,66 @@ __device__ __forceinline__ void add_symbol(uint32_t* f, uint32_t NS, uint32_t B,
 
 // ---- E1 --------------------------------------------------------------------
 // Persistent CTAs walk contiguous tile ranges.  Per tile (4096 elements):
-//   L  16 contiguous elements per thread: key = previous level, d = cyclic delta
-//      (codec.cpp:12-24), staged as bytes (levels < 64)
+//   L  16 contiguous elements per thread, packed as bytes (levels < 64):
+//      key = previous level, d = cyclic delta (codec.cpp:12-24) with SIMD byte
+//      ops; CRC-32 of the thread's 32 level-stream bytes (zero-skipping
+//      slice-by-16, the high byte of every level is 0), moved to the tile end
+//      with nibble tables of x^(8n) mod P (lane, then warp); the tile value is
+//      moved to its stream position later (crc_tiles_kernel)
 //   M  warp w owns elements [512w, 512w+512) in 32-element chunks:
-//      __match_any_sync on the key gives each element its rank among equal keys
-//      (stable group-by, codec.cpp:39-54) and its previous same-key element,
-//      whose delta decides whether the element starts a run (rle_encode,
-//      codec.cpp:79-90); the first element of a key in a warp is settled in F
-//      against the last one of the nearest earlier warp holding that key
-//   P  per key: prefix over warps, group start offsets
-//   H  only run heads are placed (sparse): head flag, value and group at the
-//      element's rearranged position
-//   B  head flags -> run start positions (block scan)
+//      __match_any_sync on the key gives the rank inside the chunk; per-chunk
+//      key counts -> per-key prefix over chunks (stable group-by,
+//      codec.cpp:39-54)
+//   P  per key: prefix over warps, group starts
+//   S  d scattered to its rearranged position (bytes)
+//   D  run heads (rle_encode, codec.cpp:79-90) = group starts | byte changes
+//      of the rearranged stream (SIMD compare), block scan -> run starts
 //   R  runs (value, group, length), first/last run per group, interior-run
 //      symbol frequencies (accumulated per tensor in shared memory)
-//   C  CRC-32 of the target levels by one warp, 128 levels per lane with
-//      zero-skipping slice-by-16 tables (the high byte of every level is 0),
-//      combined with x^(8n) mod P shifts (tile virtually right-aligned)
-constexpr int kCrcTabs = 10;  // T1,T3,T5,T7,T9,T11,T12,T13,T14,T15
+constexpr int kCrcTabs = 10;  // T1,T3,T5,T7,T9,T11,T12,T13,T14,T15 (T_n: byte + n zero bytes)
+constexpr int kChunks = 512 / 32;  // chunks per warp range
 __device__ uint32_t g_crc_slice[kCrcTabs][256];
-__constant__ uint32_t c_crc_pw32[32];  // x^(8*256*(31-l)) mod P
-constexpr int kCurRow = 144;           // s_cur: 128 levels per row + 16 B pad (bank spread)
+// g_crc_nib[i][n][c]: nibble n at position i times x^(8*32*(31-c)) (c < 32, lanes)
+// and x^(8*1024*(7-(c-32))) (c = 32..39, warps) mod P
+__device__ uint32_t g_crc_nib[8][16][40];
 
-__device__ __forceinline__ uint32_t crc_block8(const uint32_t* T, uint32_t r, const uint32_t (&lo)[8]) {
-    const uint32_t x = r ^ (lo[0] | (lo[1] << 16));
+// 8 levels (16 stream bytes, odd bytes 0) through the CRC register
+__device__ __forceinline__ uint32_t crc_block8(const uint32_t* T, uint32_t r, uint32_t l03,
+                                               uint32_t l47) {
+    // l03 / l47: levels 0..3 / 4..7 as bytes
+    const uint32_t x = r ^ ((l03 & 0xff) | ((l03 & 0xff00) << 8));
     return T[9 * 256 + (x & 0xff)] ^ T[8 * 256 + ((x >> 8) & 0xff)] ^
-           T[7 * 256 + ((x >> 16) & 0xff)] ^ T[6 * 256 + (x >> 24)] ^ T[5 * 256 + lo[2]] ^
-           T[4 * 256 + lo[3]] ^ T[3 * 256 + lo[4]] ^ T[2 * 256 + lo[5]] ^ T[1 * 256 + lo[6]] ^
-           T[0 * 256 + lo[7]];
+           T[7 * 256 + ((x >> 16) & 0xff)] ^ T[6 * 256 + (x >> 24)] ^
+           T[5 * 256 + ((l03 >> 16) & 0xff)] ^ T[4 * 256 + (l03 >> 24)] ^
+           T[3 * 256 + (l47 & 0xff)] ^ T[2 * 256 + ((l47 >> 8) & 0xff)] ^
+           T[1 * 256 + ((l47 >> 16) & 0xff)] ^ T[0 * 256 + (l47 >> 24)];
+}
+// v * (constant c) mod P from the nibble tables (conflict-free: column = lane)
+__device__ __forceinline__ uint32_t crc_mul_nib(const uint32_t* N, uint32_t v, int c) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r ^= N[(i * 16 + ((v >> (4 * i)) & 15u)) * 40 + c];
+    return r;
 }
 
 struct E1Smem {
-    uint32_t* freq;     // B*NS, per tensor
-    uint32_t* crc;      // kCrcTabs*256
-    uint32_t* wcnt;     // 8*B
-    uint8_t* lastd;     // 8*B
-    uint8_t* firstd;    // 8*B
-    uint8_t* fhead;     // 8*B
-    uint8_t* key;       // kTile   (aliased by hp after M)
-    uint8_t* d;         // kTile
-    uint16_t* hp;       // kTile+1 (over key|d)
-    uint8_t* cur;       // 32 rows * kCurRow
-    uint8_t* hf;        // kTile
-    uint8_t* hv;        // kTile
-    uint8_t* hk;        // kTile
+    uint32_t* freq;   // B*NS, per tensor
+    uint32_t* crc;    // kCrcTabs*256
+    uint32_t* nib;    // 8*16*40
+    uint32_t* wcnt;   // 8*B: per-warp key counts -> per-warp key bases
+    uint16_t* cc;     // 8*kChunks*B: per-chunk key counts -> prefix over chunks
+    uint32_t* part;   // 8 warp CRCs
+    uint32_t* gs;     // kTile/32 group-start bitmap
+    uint16_t* kd;     // kTile: key | d << 8      (aliased by hp after M)
+    uint16_t* hp;     // kTile + 1 run starts
+    uint8_t* sd;      // kTile: rearranged deltas (sd[-1] readable)
 };
 
 __host__ __device__ inline size_t e1_smem_bytes(uint32_t B, uint32_t NS) {
-    size_t o = 0;
-    o += ((size_t)B * NS * 4 + 15) & ~(size_t)15;
-    o += (size_t)kCrcTabs * 256 * 4;
-    o += ((size_t)8 * B * 4 + 15) & ~(size_t)15;
-    o += ((size_t)8 * B * 3 + 15) & ~(size_t)15;
-    o += 2 * (size_t)kTile + 16;  // key | d  (hp alias needs 2*kTile+2)
-    o += 32 * (size_t)kCurRow;
-    o += 3 * (size_t)kTile;
-    return o;
+    return (((size_t)B * NS * 4 + 15) & ~(size_t)15) + (size_t)kCrcTabs * 256 * 4 +
+           (size_t)8 * 16 * 40 * 4 + (((size_t)8 * B * 4 + 15) & ~(size_t)15) +
+           (((size_t)8 * kChunks * B * 2 + 15) & ~(size_t)15) + 32 + kTile / 8 +
+           (2 * (size_t)kTile + 16) + (kTile + 32);
 }
 
 __device__ inline E1Smem e1_carve(uint8_t* base, uint32_t B, uint32_t NS) {
@@ -167,32 +172,41 @@ __device__ inline E1Smem e1_carve(uint8_t* base, uint32_t B, uint32_t NS) {
     size_t o = 0;
     S.freq = (uint32_t*)(base + o); o += ((size_t)B * NS * 4 + 15) & ~(size_t)15;
     S.crc = (uint32_t*)(base + o);  o += (size_t)kCrcTabs * 256 * 4;
+    S.nib = (uint32_t*)(base + o);  o += (size_t)8 * 16 * 40 * 4;
     S.wcnt = (uint32_t*)(base + o); o += ((size_t)8 * B * 4 + 15) & ~(size_t)15;
-    S.lastd = base + o;
-    S.firstd = base + o + 8 * B;
-    S.fhead = base + o + 16 * B;    o += ((size_t)8 * B * 3 + 15) & ~(size_t)15;
-    S.key = base + o;
-    S.d = base + o + kTile;
+    S.cc = (uint16_t*)(base + o);   o += ((size_t)8 * kChunks * B * 2 + 15) & ~(size_t)15;
+    S.part = (uint32_t*)(base + o); o += 32;
+    S.gs = (uint32_t*)(base + o);   o += kTile / 8;
+    S.kd = (uint16_t*)(base + o);
     S.hp = (uint16_t*)(base + o);   o += 2 * (size_t)kTile + 16;
-    S.cur = base + o;               o += 32 * (size_t)kCurRow;
-    S.hf = base + o;
-    S.hv = base + o + kTile;
-    S.hk = base + o + 2 * kTile;
+    S.sd = base + o + 16;
     return S;
 }
 
+// bit j (j = 0..3) = top bit of byte j
+__device__ __forceinline__ uint32_t byte_msbs(uint32_t x) {
+    return (((x >> 7) & 0x01010101u) * 0x10204080u) >> 28;
+}
+
+__device__ __forceinline__ uint32_t keep_mask(int keep) {  // low `keep` bytes
+    return keep >= 4 ? 0xffffffffu : (keep <= 0 ? 0u : (1u << (8 * keep)) - 1u);
+}
+
 template <bool HAS_BASE>
-__global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
+__global__ void __launch_bounds__(kCB, 3) enc_tile_kernel(EncArgs A) {
     extern __shared__ __align__(16) uint8_t e1_dyn[];
     const uint32_t B = A.B, NS = A.NS;
     const E1Smem S = e1_carve(e1_dyn, B, NS);
-    __shared__ uint32_t s_cnt[kMaxB], s_start[kMaxB], s_run0[kMaxB], s_run1[kMaxB];
+    __shared__ uint32_t s_cnt[kMaxB], s_start[kMaxB + 1], s_run0[kMaxB], s_run1[kMaxB];
     __shared__ unsigned long long s_scan[33];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
+    const uint32_t Brep = B * 0x01010101u;
 
     for (uint32_t i = tid; i < kCrcTabs * 256; i += kCB) S.crc[i] = (&g_crc_slice[0][0])[i];
+    for (uint32_t i = tid; i < 8 * 16 * 40; i += kCB) S.nib[i] = (&g_crc_nib[0][0][0])[i];
     for (uint32_t i = tid; i < B * NS; i += kCB) S.freq[i] = 0;
+    if (tid < 16) S.sd[tid - 16] = 0;
     const int t0 = (int)((int64_t)blockIdx.x * A.ntiles / gridDim.x);
     const int t1 = (int)((int64_t)(blockIdx.x + 1) * A.ntiles / gridDim.x);
     uint32_t cur_tensor = 0xffffffffu;
@@ -215,128 +229,139 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
             cur_tensor = T.tensor;
         }
         // ---- L
-        for (uint32_t i = tid; i < 8 * B; i += kCB) {
-            S.wcnt[i] = 0;
-            S.lastd[i] = 0xff;
+        if (tid < kTile / 32) S.gs[tid] = 0;
+        {
+            uint32_t* cc = (uint32_t*)(S.cc + wid * kChunks * B);
+            for (uint32_t i = lane; i < kChunks * B / 2; i += 32) cc[i] = 0;
         }
         {
             const uint32_t e0 = tid * kIt;
-            uint32_t kw[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
-            uint32_t dw[4] = {0, 0, 0, 0}, cw[4] = {0, 0, 0, 0};
-            if (e0 < cnt) {
-                uint16_t c16[kIt], p16[kIt];
+            uint32_t cw[4] = {0, 0, 0, 0}, pw[4] = {0, 0, 0, 0};
+            const uint32_t nv = e0 < cnt ? min(cnt - e0, (uint32_t)kIt) : 0u;  // valid here
+            if (nv) {
                 const uint4* cp = (const uint4*)(A.cur + T.start + e0);
-                uint4 a0 = cp[0], a1 = cp[1];
-                memcpy(c16, &a0, 16);
-                memcpy(c16 + 8, &a1, 16);
+                const uint4 a0 = cp[0], a1 = cp[1];
+                uint32_t hi[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                cw[0] = __byte_perm(a0.x, a0.y, 0x6420);
+                cw[1] = __byte_perm(a0.z, a0.w, 0x6420);
+                cw[2] = __byte_perm(a1.x, a1.y, 0x6420);
+                cw[3] = __byte_perm(a1.z, a1.w, 0x6420);
+                uint32_t hp_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                 if (HAS_BASE) {
                     const uint4* pp = (const uint4*)(A.prev + T.start + e0);
-                    uint4 b0 = pp[0], b1 = pp[1];
-                    memcpy(p16, &b0, 16);
-                    memcpy(p16 + 8, &b1, 16);
+                    const uint4 b0 = pp[0], b1 = pp[1];
+                    hp_[0] = b0.x, hp_[1] = b0.y, hp_[2] = b0.z, hp_[3] = b0.w;
+                    hp_[4] = b1.x, hp_[5] = b1.y, hp_[6] = b1.z, hp_[7] = b1.w;
+                    pw[0] = __byte_perm(b0.x, b0.y, 0x6420);
+                    pw[1] = __byte_perm(b0.z, b0.w, 0x6420);
+                    pw[2] = __byte_perm(b1.x, b1.y, 0x6420);
+                    pw[3] = __byte_perm(b1.z, b1.w, 0x6420);
                 }
-                bool bad = false;
+                // high bytes of the u16 levels (must be 0) of the valid elements
+                uint32_t bad = 0;
 #pragma unroll
-                for (int j = 0; j < kIt; ++j) {
-                    if (e0 + j < cnt) {
-                        uint32_t c = c16[j], p = HAS_BASE ? p16[j] : 0u;
-                        bad |= (p >= B) | (c >= B);
-                        p = p < B ? p : 0u;
-                        c = c < B ? c : 0u;
-                        const uint32_t d = p >= c ? p - c : p + B - c;
-                        const int sh = 8 * (j & 3);
-                        kw[j >> 2] = (kw[j >> 2] & ~(0xffu << sh)) | (p << sh);
-                        dw[j >> 2] |= d << sh;
-                        cw[j >> 2] |= c << sh;
-                    }
+                for (int j = 0; j < 8; ++j) {
+                    const int keep = (int)nv - 2 * j;
+                    const uint32_t m = keep >= 2 ? 0xff00ff00u : (keep == 1 ? 0x0000ff00u : 0u);
+                    bad |= (hi[j] | hp_[j]) & m;
                 }
-                if (bad) atomicOr(A.err, kErrCorruptIndex);
+                uint32_t big = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t m = keep_mask((int)nv - 4 * j);
+                    cw[j] &= m;
+                    pw[j] &= m;
+                    big |= __vcmpgeu4(cw[j], Brep) | __vcmpgeu4(pw[j], Brep);
+                }
+                if (bad | big) atomicOr(A.err, kErrCorruptIndex);
             }
-            *(uint4*)(S.key + e0) = make_uint4(kw[0], kw[1], kw[2], kw[3]);
-            *(uint4*)(S.d + e0) = make_uint4(dw[0], dw[1], dw[2], dw[3]);
-            *(uint4*)(S.cur + (e0 >> 7) * kCurRow + (e0 & 127)) = make_uint4(cw[0], cw[1], cw[2], cw[3]);
-            *(uint4*)(S.hf + e0) = make_uint4(0, 0, 0, 0);
+            // d = (p - c) mod B per byte
+            uint32_t kd[8];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t lt = __vcmpltu4(pw[j], cw[j]);
+                const uint32_t dw = __vadd4(__vsub4(pw[j], cw[j]), lt & Brep);
+                const uint32_t vm = keep_mask((int)nv - 4 * j);
+                const uint32_t key = (pw[j] & vm) | ~vm;  // invalid elements: key 0xff
+                kd[2 * j] = __byte_perm(key, dw, 0x5140);
+                kd[2 * j + 1] = __byte_perm(key, dw, 0x7362);
+            }
+            *(uint4*)(S.kd + e0) = make_uint4(kd[0], kd[1], kd[2], kd[3]);
+            *(uint4*)(S.kd + e0 + 8) = make_uint4(kd[4], kd[5], kd[6], kd[7]);
+            // CRC of this thread's levels (zero register), right-aligned in its
+            // 32-byte chunk when the tile ends inside it (leading zero levels are neutral)
+            uint32_t c0 = cw[0], c1 = cw[1], c2 = cw[2], c3 = cw[3];
+            if (nv && nv < (uint32_t)kIt) {
+                const int sh = kIt - (int)nv;  // bytes to move up
+                uint32_t w[8] = {0, 0, 0, 0, cw[0], cw[1], cw[2], cw[3]};
+                // shift the 16-byte little-endian value left by sh bytes
+                uint32_t o[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int src = 4 + j - (sh >> 2);
+                    const uint32_t lo_w = src - 1 >= 0 ? w[src - 1] : 0u;
+                    o[j] = (sh & 3) ? __funnelshift_l(lo_w, w[src], 8 * (sh & 3)) : w[src];
+                }
+                c0 = o[0], c1 = o[1], c2 = o[2], c3 = o[3];
+            }
+            uint32_t r = 0;
+            if (nv) r = crc_block8(S.crc, crc_block8(S.crc, 0u, c0, c1), c2, c3);
+            if (cnt == kTile) {
+                r = crc_mul_nib(S.nib, r, lane);  // to the end of the warp's 1 KiB
+                r = warp_xor(r);
+                if (lane == 0) S.part[wid] = crc_mul_nib(S.nib, r, 32 + wid);  // to the tile end
+            } else {  // ragged tile: shift by the bytes after this chunk inside the tile
+                if (r) r = crc_shift(c_crc_x2n, r, 2ull * (cnt - (e0 + nv)));
+                r = warp_xor(r);
+                if (lane == 0) S.part[wid] = r;
+            }
         }
         __syncthreads();
 
-        // ---- M: rank among equal keys, run-head test against the previous same-key element
-        uint32_t pk[kIt];  // rank | key << 12 | d << 18 | head << 24 | first << 25 | valid << 26
+        // ---- M: rank inside the chunk (match), per-chunk key counts
+        uint32_t pk[kIt];  // rank-in-chunk | key << 12 | d << 18 | valid << 24
+        uint16_t* cc = S.cc + wid * kChunks * B;
         {
-            uint32_t* wc = S.wcnt + wid * B;
-            uint8_t* ld = S.lastd + wid * B;
 #pragma unroll
             for (int j = 0; j < kIt; ++j) {
                 const uint32_t e = wid * 512 + j * 32 + lane;
-                const uint32_t key = S.key[e], d = S.d[e];
+                const uint32_t kdv = S.kd[e];
+                const uint32_t key = kdv & 0xffu;
                 const bool valid = key != 0xffu;
                 const uint32_t peers = __match_any_sync(0xffffffffu, key);
-                const uint32_t lt = peers & lt_mask;
-                const int leader = __ffs(peers) - 1;
-                uint32_t old = 0;
-                if (lane == leader && valid) {
-                    old = wc[key];
-                    wc[key] = old + __popc(peers);
-                }
-                old = __shfl_sync(0xffffffffu, old, leader);
-                const int src = lt ? 31 - __clz(lt) : lane;
-                uint32_t pd = __shfl_sync(0xffffffffu, d, src);
-                if (!lt && valid) pd = ld[key];
-                __syncwarp();
-                const bool first = !lt && pd == 0xffu;
-                const bool head = !first && pd != d;
-                if (valid && lane == 31 - __clz(peers)) ld[key] = (uint8_t)d;
-                if (valid && first) S.firstd[wid * B + key] = (uint8_t)d;
-                __syncwarp();
-                pk[j] = valid ? ((old + __popc(lt)) | (key << 12) | (d << 18) | ((uint32_t)head << 24) |
-                                 ((uint32_t)first << 25) | (1u << 26))
+                if (valid && (peers & lt_mask) == 0) cc[j * B + key] = (uint16_t)__popc(peers);
+                pk[j] = valid ? (__popc(peers & lt_mask) | (key << 12) | ((kdv >> 8) << 18) | (1u << 24))
                               : 0u;
             }
         }
-        // ---- C: CRC of the target levels (warp 0 after its M share)
-        if (wid == 0) {
-            const int off = (int)kTile - (int)cnt;  // virtual right alignment: leading levels 0
-            uint32_t r = 0;
-            for (int blk = 0; blk < 16; ++blk) {
-                const int v0 = lane * 128 + blk * 8;  // virtual level index
-                uint32_t lo[8];
-                if (off == 0) {
-                    const uint2 q = *(const uint2*)(S.cur + lane * kCurRow + blk * 8);
+        __syncwarp();
+        for (uint32_t b = lane; b < B; b += 32) {  // prefix over chunks per key
+            uint32_t acc = 0;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        lo[j] = (q.x >> (8 * j)) & 0xff;
-                        lo[4 + j] = (q.y >> (8 * j)) & 0xff;
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const int e = v0 + j - off;
-                        lo[j] = e >= 0 ? S.cur[(e >> 7) * kCurRow + (e & 127)] : 0u;
-                    }
-                }
-                r = crc_block8(S.crc, r, lo);
+            for (int j = 0; j < kChunks; ++j) {
+                const uint32_t c = cc[j * B + b];
+                cc[j * B + b] = (uint16_t)acc;
+                acc += c;
             }
-            r = r ? crc_multmodp(c_crc_pw32[lane], r) : 0u;
-            r = warp_xor(r);
-            if (lane == 0 && r) {
-                r = crc_multmodp(A.crc_shift[ti], r);
-                if (r) atomicXor(A.crc_acc, r);
-            }
+            S.wcnt[wid * B + b] = acc;
         }
         __syncthreads();
-        // ---- P + F: per key prefix over warps; first-in-warp heads against the
-        // last element of the nearest earlier warp holding the key
+        // ---- P: per key prefix over warps; group starts
         for (uint32_t b = tid; b < B; b += kCB) {
-            uint32_t acc = 0, last = 0xffu;
+            uint32_t acc = 0;
+#pragma unroll
             for (int w = 0; w < kCB / 32; ++w) {
                 const uint32_t c = S.wcnt[w * B + b];
                 S.wcnt[w * B + b] = acc;
                 acc += c;
-                if (c) {
-                    S.fhead[w * B + b] = (last == 0xffu) || (S.firstd[w * B + b] != last);
-                    last = S.lastd[w * B + b];
-                }
             }
             s_cnt[b] = acc;
+        }
+        if (tid == kCB - 1) {  // tile CRC (moved to its stream position by crc_tiles_kernel)
+            uint32_t r = 0;
+#pragma unroll
+            for (int w = 0; w < kCB / 32; ++w) r ^= S.part[w];
+            A.tile_crc[ti] = r;
         }
         __syncthreads();
         if (wid == 0) {
@@ -350,35 +375,41 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
                     const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
                     if (lane >= o) x += y;
                 }
-                if (b < B) s_start[b] = run + x - v;
+                if (b < B) {
+                    const uint32_t st = run + x - v;
+                    s_start[b] = st;
+                    if (v) atomicOr(S.gs + (st >> 5), 1u << (st & 31));
+                }
                 run += __shfl_sync(0xffffffffu, x, 31);
             }
+            if (lane == 0) s_start[B] = run;
         }
         __syncthreads();
-        // ---- H: place run heads at their rearranged positions
+        // ---- S: scatter deltas to their rearranged positions
+        {
+            const uint32_t* wb = S.wcnt + wid * B;
 #pragma unroll
-        for (int j = 0; j < kIt; ++j) {
-            const uint32_t q = pk[j];
-            if (!(q >> 26)) continue;
-            const uint32_t key = (q >> 12) & 63u;
-            const bool h = (q >> 24) & 1u ? true : ((q >> 25) & 1u ? S.fhead[wid * B + key] != 0 : false);
-            if (h) {
-                const uint32_t pos = s_start[key] + S.wcnt[wid * B + key] + (q & 4095u);
-                S.hf[pos] = 1;
-                S.hv[pos] = (uint8_t)((q >> 18) & 63u);
-                S.hk[pos] = (uint8_t)key;
+            for (int j = 0; j < kIt; ++j) {
+                const uint32_t q = pk[j];
+                if (q >> 24) {
+                    const uint32_t key = (q >> 12) & 63u;
+                    S.sd[s_start[key] + wb[key] + cc[j * B + key] + (q & 4095u)] = (uint8_t)((q >> 18) & 63u);
+                }
             }
         }
         __syncthreads();
-        // ---- B: run start positions in rearranged order
+        // ---- D: run heads = group starts | changes of the rearranged stream
         uint32_t R;
         {
             const uint32_t p0 = tid * kIt;
-            const uint4 f = *(const uint4*)(S.hf + p0);
-            const uint32_t fw[4] = {f.x, f.y, f.z, f.w};
-            uint32_t m = 0;
-#pragma unroll
-            for (int j = 0; j < kIt; ++j) m |= ((fw[j >> 2] >> (8 * (j & 3))) & 1u) << j;
+            const uint4 x = *(const uint4*)(S.sd + p0);
+            const uint32_t prevw = (uint32_t)S.sd[(int)p0 - 1] << 24;
+            uint32_t m = byte_msbs(__vcmpne4(x.x, __funnelshift_l(prevw, x.x, 8))) |
+                         (byte_msbs(__vcmpne4(x.y, __funnelshift_l(x.x, x.y, 8))) << 4) |
+                         (byte_msbs(__vcmpne4(x.z, __funnelshift_l(x.y, x.z, 8))) << 8) |
+                         (byte_msbs(__vcmpne4(x.w, __funnelshift_l(x.z, x.w, 8))) << 12);
+            m |= (S.gs[tid >> 1] >> ((tid & 1) * 16)) & 0xffffu;
+            if (p0 + kIt > cnt) m &= p0 >= cnt ? 0u : (1u << (cnt - p0)) - 1u;
             unsigned long long tot;
             uint32_t r = (uint32_t)block_exclusive_scan<unsigned long long>(__popc(m), s_scan, &tot);
             R = (uint32_t)tot;
@@ -394,20 +425,23 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
         unsigned long long* runs = A.runs + (size_t)ti * kTile;
         for (uint32_t r = tid; r < R; r += kCB) {
             const uint32_t p = S.hp[r], L = S.hp[r + 1] - p;
-            const uint32_t v = S.hv[p], b = S.hk[p];
+            const uint32_t v = S.sd[p];
+            uint32_t lo = 0, n = B + 1;  // last b with s_start[b] <= p (a non-empty group)
+            while (n > 1) {
+                const uint32_t h = n >> 1;
+                if (s_start[lo + h] <= p) lo += h, n -= h;
+                else n = h;
+            }
+            const uint32_t b = lo;
             runs[r] = (unsigned long long)v | ((unsigned long long)b << 16) |
                       ((unsigned long long)L << 32);
-            if (p == s_start[b]) s_run0[b] = r;
-            if (p + L == s_start[b] + s_cnt[b]) s_run1[b] = r;
-        }
-        __syncthreads();
-        for (uint32_t r = tid; r < R; r += kCB) {
-            const uint32_t p = S.hp[r], L = S.hp[r + 1] - p;
-            const uint32_t v = S.hv[p], b = S.hk[p];
-            if (r != s_run0[b] && r != s_run1[b])
-                add_symbol(S.freq + b * NS, NS, B, cur_tensor * B + b, v, L, A);
+            const bool first = p == s_start[b], last = p + L == s_start[b] + s_cnt[b];
+            if (first) s_run0[b] = r;
+            if (last) s_run1[b] = r;
+            if (!first && !last) add_symbol(S.freq + b * NS, NS, B, cur_tensor * B + b, v, L, A);
         }
         if (tid == 0) A.tile_nruns[ti] = R;
+        __syncthreads();
         for (uint32_t b = tid; b < B; b += kCB) {
             Seg G{};
             G.n = s_cnt[b];
@@ -415,8 +449,8 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
                 G.run_begin = s_run0[b];
                 G.run_end = s_run1[b] + 1;
                 const uint32_t pb = S.hp[G.run_begin], pe = S.hp[G.run_end - 1];
-                G.fv = S.hv[pb];
-                G.lv = S.hv[pe];
+                G.fv = S.sd[pb];
+                G.lv = S.sd[pe];
                 G.lead = S.hp[G.run_begin + 1] - pb;
                 G.trail = S.hp[G.run_end] - pe;
             }
@@ -431,6 +465,20 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
             if (c) atomicAdd(gf + i, c);
         }
     }
+}
+
+// Tile CRCs (each ending at its tile's last byte) moved to the end of the level
+// stream and XOR-combined (crc32 linearity, crc.cuh).
+__global__ void __launch_bounds__(256) crc_tiles_kernel(const uint32_t* tile_crc,
+                                                        const uint32_t* shift, int ntiles,
+                                                        uint32_t* acc) {
+    uint32_t r = 0;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x) {
+        const uint32_t v = tile_crc[t];
+        if (v) r ^= crc_multmodp(shift[t], v);
+    }
+    r = warp_xor(r);
+    if ((threadIdx.x & 31) == 0 && r) atomicXor(acc, r);
 }
 
 // ---- S: cross-tile run resolution per (tensor, group) --------------------------
@@ -1337,9 +1385,6 @@ static void init_crc_consts() {
     uint32_t pw[kCB];
     for (int t = 0; t < kCB; ++t) pw[t] = crc_x2nmodp(x.t, (uint64_t)32 * (kCB - 1 - t), 3);
     DQTG_CUDA(cudaMemcpyToSymbol(c_crc_pw, pw, sizeof(pw)));
-    uint32_t pw32[32];
-    for (int l = 0; l < 32; ++l) pw32[l] = crc_x2nmodp(x.t, (uint64_t)256 * (31 - l), 3);
-    DQTG_CUDA(cudaMemcpyToSymbol(c_crc_pw32, pw32, sizeof(pw32)));
     // zero-skipping slice-by-16 tables T1,T3,...,T11,T12..T15 (T_n: byte then n zero bytes)
     static uint32_t tn[16][256];
     for (uint32_t b = 0; b < 256; ++b) {
@@ -1353,6 +1398,14 @@ static void init_crc_consts() {
     static uint32_t sl[kCrcTabs][256];
     for (int i = 0; i < kCrcTabs; ++i) memcpy(sl[i], tn[pick[i]], sizeof(sl[i]));
     DQTG_CUDA(cudaMemcpyToSymbol(g_crc_slice, sl, sizeof(sl)));
+    static uint32_t nib[8][16][40];
+    for (int c = 0; c < 40; ++c) {
+        const uint32_t k = c < 32 ? crc_x2nmodp(x.t, (uint64_t)32 * (31 - c), 3)
+                                  : crc_x2nmodp(x.t, (uint64_t)1024 * (7 - (c - 32)), 3);
+        for (int i = 0; i < 8; ++i)
+            for (uint32_t n = 0; n < 16; ++n) nib[i][n][c] = crc_multmodp(k, n << (4 * i));
+    }
+    DQTG_CUDA(cudaMemcpyToSymbol(g_crc_nib, nib, sizeof(nib)));
     DQTG_CUDA(cudaMemcpyToSymbol(c_crc_x2n, x.t, sizeof(x.t)));
     crc_consts_ready = true;
 }
@@ -1483,6 +1536,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     auto* small = (unsigned long long*)e.buf("e.small", 64);
     A.ov_count = small;
     A.crc_acc = (uint32_t*)(small + 1);
+    A.tile_crc = (uint32_t*)e.buf("e.tile_crc", (size_t)ntiles * 4 + 4);
     A.err = e.d_err;
     DQTG_CUDA(cudaMemsetAsync(A.freq, 0, freq_n * 4, st));
     DQTG_CUDA(cudaMemsetAsync(small, 0, 64, st));
@@ -1497,6 +1551,8 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
         DQTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kCB, e1_smem));
         const int grid = std::max(1, std::min(ntiles, e.num_sms * std::max(1, per_sm)));
         { DQTG_SPAN(e, "enc_tile_kernel"); kfn<<<grid, kCB, e1_smem, st>>>(A); }
+        { DQTG_SPAN(e, "crc_tiles_kernel"); crc_tiles_kernel<<<std::max(1, std::min(e.num_sms * 2, (ntiles + 255) / 256)), 256, 0, st>>>(A.tile_crc, A.crc_shift, ntiles, A.crc_acc); }
+        e.launched();
     }
     // S
     {

@@ -2,6 +2,8 @@
 // weights, k-means++ seeding, Lloyd, loss and restart selection.  One CTA per
 // (problem, restart); see kmeans.cuh for the exactness strategy.
 #include <float.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "engine.h"
 #include "kmeans.cuh"
@@ -73,27 +75,34 @@ struct KShared {
     double red[kKB / 32];
 };
 
+// Sequential fp64 sum s += v[i] for i in [a, n) in index order (the reference's
+// order), optional running values out[i]; 16 loads in flight per block.
+__device__ __forceinline__ double seq_prefix(const double* v, int a, int n, double s, double* out) {
+    int i = a;
+    for (; i + 16 <= n; i += 16) {
+        double cv[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) cv[u] = v[i + u];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            s = __dadd_rn(s, cv[u]);
+            if (out) out[i + u] = s;
+        }
+    }
+    for (; i < n; ++i) {
+        s = __dadd_rn(s, v[i]);
+        if (out) out[i] = s;
+    }
+    return s;
+}
+
 // quantize.cpp:116-131: sequential prefix of prob (lane 0), binary search for the
 // first positive entry whose running sum reaches r.
 __device__ int kpp_pick(const double* prob, double* pref, int n, int from, KShared& sm) {
     if (threadIdx.x == 0) {
         // pref[0..from) are unchanged from the previous pick (same terms, same order)
         double s = from > 0 ? pref[from - 1] : 0.0;
-        int i = from;
-        for (; i + 8 <= n; i += 8) {
-            double v[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = prob[i + j];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                s = __dadd_rn(s, v[j]);
-                pref[i + j] = s;
-            }
-        }
-        for (; i < n; ++i) {
-            s = __dadd_rn(s, prob[i]);
-            pref[i] = s;
-        }
+        s = seq_prefix(prob, from, n, s, pref);
         if (n > 0) s = pref[n - 1];
         int res;
         if (!(s > 0.0)) {
@@ -193,58 +202,73 @@ __device__ void kpp_init(const double* pts, const double* w, int n, int k, doubl
     __syncthreads();
 }
 
+// Sequential (w, w*x) sums over keys [a, b] continuing from (ws, wxs) in key
+// order (the reference's accumulation order), running values stored for reuse.
+__device__ __forceinline__ void chain_sums(const double* w, const double* x, int a, int b,
+                                           double& ws, double& wxs, double* rw, double* rwx) {
+    int i = a;
+    const int e = b + 1;
+    for (; i + 8 <= e; i += 8) {
+        double wv[8], xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) wv[u] = w[i + u], xv[u] = x[i + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            ws = __dadd_rn(ws, wv[u]);
+            wxs = __dadd_rn(wxs, __dmul_rn(wv[u], xv[u]));
+            if (rw) rw[i + u] = ws, rwx[i + u] = wxs;
+        }
+    }
+    for (; i < e; ++i) {
+        const double wi = w[i];
+        ws = __dadd_rn(ws, wi);
+        wxs = __dadd_rn(wxs, __dmul_rn(wi, x[i]));
+        if (rw) rw[i] = ws, rwx[i] = wxs;
+    }
+}
+
 // weighted_lloyd (quantize.cpp:180-254); c (k centres) is updated in place.
+// Iterations whose centres are strictly ascending and well separated (the fast
+// path: clusters are contiguous key ranges) run on warp 0 alone with warp
+// primitives; the sequential per-cluster sums are cached per key (rw / rwx) and
+// reused while a cluster's first key is unchanged (an identical chain prefix).
+// The general assignment and the empty-cluster reseed use the whole block.
 __device__ int lloyd_block(const double* pts, const double* w, int n, double* c, double* nx,
                            int* first, int* last, int* cnt, int k, double tol, int max_iter,
                            int* assign, double* score, ScoreVal* top, bool distinct,
                            KShared& sm) {
+    __shared__ int s_cf[64], s_cl[64];  // cached chain [first, last] per cluster (-1: none)
+    __shared__ int s_fast;
+    double* rw = (double*)top;  // running sums share the reseed scratch (2n doubles)
+    double* rwx = rw + n;
+    const bool cache = k <= 64;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double lm = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) lm = fmax(lm, fabs(pts[i]));
     double scale = block_max_d(lm, sm);
     if (scale == 0.0) scale = 1.0;
+    const double gap = __dmul_rn(scale, 0x1.0p-40);
+    if (threadIdx.x < 64) s_cf[threadIdx.x] = -1;
     int iters = 0;
-    __shared__ int s_fast;
     for (int it = 0; it < max_iter; ++it) {
-        if (threadIdx.x == 0) {
+        if (wid == 0) {
             // Fast path: strictly ascending centres separated by far more than the
             // rounding of any |x - c| (gap > scale * 2^-40).  The distance sequence
             // over j is then strictly unimodal for every x, so the reference argmin
             // (strict <, lowest index on ties) is decided by neighbouring centres and
             // each cluster is the key range between two monotone boundaries.
-            bool fast = true;
-            const double gap = __dmul_rn(scale, 0x1.0p-40);
-            for (int j = 0; j + 1 < k; ++j)
-                if (!(__dsub_rn(c[j + 1], c[j]) > gap)) fast = false;
-            s_fast = fast;
-            sm.any_empty = 0;
+            bool ok = true;
+            for (int j = lane; j + 1 < k; j += 32) ok &= __dsub_rn(c[j + 1], c[j]) > gap;
+            ok = __all_sync(0xffffffffu, ok);
+            if (lane == 0) {
+                s_fast = ok;
+                sm.any_empty = 0;
+                sm.done = 0;
+            }
         }
         __syncthreads();
-        if (s_fast) {
-            // start of cluster j+1 = first key whose distance to c[j+1] is < to c[j]
-            for (int j = threadIdx.x; j < k; j += blockDim.x) {
-                int lo = n, hi = n;  // last cluster ends at n
-                if (j + 1 < k) {
-                    lo = 0;
-                    const double a = c[j], b = c[j + 1];
-                    while (lo < hi) {
-                        int mid = (lo + hi) >> 1;
-                        double x = pts[mid];
-                        if (fabs(__dsub_rn(x, b)) < fabs(__dsub_rn(x, a))) hi = mid;
-                        else lo = mid + 1;
-                    }
-                }
-                last[j] = lo;  // exclusive end of cluster j (temporarily)
-            }
-            __syncthreads();
-            for (int j = threadIdx.x; j < k; j += blockDim.x) {
-                const int b0 = j ? last[j - 1] : 0, b1 = last[j];
-                first[j] = b0;
-                cnt[j] = b1 > b0 ? b1 - b0 : 0;
-            }
-            __syncthreads();
-            for (int j = threadIdx.x; j < k; j += blockDim.x) last[j] = first[j] + cnt[j] - 1;
-            __syncthreads();
-        } else {
+        const bool fast = s_fast;
+        if (!fast) {
             for (int j = threadIdx.x; j < k; j += blockDim.x) {
                 first[j] = 0x7fffffff;
                 last[j] = -1;
@@ -269,41 +293,81 @@ __device__ int lloyd_block(const double* pts, const double* w, int n, double* c,
             }
             __syncthreads();
         }
-        for (int j = threadIdx.x; j < k; j += blockDim.x) {
-            double ws = 0.0, wxs = 0.0;
-            if (cnt[j] > 0) {
-                if (last[j] - first[j] + 1 == cnt[j]) {
-                    int i = first[j];
-                    const int e = last[j] + 1;
-                    for (; i + 8 <= e; i += 8) {
-                        double wv[8], xv[8];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) wv[u] = w[i + u], xv[u] = pts[i + u];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            ws = __dadd_rn(ws, wv[u]);
-                            wxs = __dadd_rn(wxs, __dmul_rn(wv[u], xv[u]));
+        if (wid == 0) {
+            if (fast) {
+                // start of cluster j+1 = first key whose distance to c[j+1] is < to c[j]
+                for (int j = lane; j < k; j += 32) {
+                    int lo = n, hi = n;  // last cluster ends at n
+                    if (j + 1 < k) {
+                        lo = 0;
+                        const double a = c[j], b = c[j + 1];
+                        while (lo < hi) {
+                            int mid = (lo + hi) >> 1;
+                            double x = pts[mid];
+                            if (fabs(__dsub_rn(x, b)) < fabs(__dsub_rn(x, a))) hi = mid;
+                            else lo = mid + 1;
                         }
                     }
-                    for (; i < e; ++i) {
-                        double wi = w[i];
-                        ws = __dadd_rn(ws, wi);
-                        wxs = __dadd_rn(wxs, __dmul_rn(wi, pts[i]));
+                    last[j] = lo;  // exclusive end of cluster j (temporarily)
+                }
+                __syncwarp();
+                for (int j = lane; j < k; j += 32) first[j] = j ? last[j - 1] : 0;
+                __syncwarp();
+                for (int j = lane; j < k; j += 32) {
+                    cnt[j] = last[j] > first[j] ? last[j] - first[j] : 0;
+                    last[j] = first[j] + cnt[j] - 1;
+                }
+                __syncwarp();
+            }
+            bool empty = false;
+            for (int j = lane; j < k; j += 32) {
+                double ws = 0.0, wxs = 0.0;
+                if (cnt[j] > 0) {
+                    if (last[j] - first[j] + 1 == cnt[j]) {
+                        // one code path for every lane (divergent chains would serialise):
+                        // reuse the cached chain prefix when the cluster's first key is unchanged
+                        const int a = first[j], b = last[j];
+                        int from = a;
+                        if (fast && cache && s_cf[j] == a && s_cl[j] >= a) {
+                            const int cb = min(s_cl[j], b);
+                            ws = rw[cb];
+                            wxs = rwx[cb];
+                            from = cb + 1;
+                        }
+                        chain_sums(w, pts, from, b, ws, wxs, fast && cache ? rw : nullptr, rwx);
+                        if (cache) {
+                            s_cf[j] = fast ? a : -1;
+                            s_cl[j] = b;
+                        }
+                    } else {
+                        if (cache) s_cf[j] = -1;
+                        for (int i = 0; i < n; ++i)
+                            if (assign[i] == j) {
+                                double wi = w[i];
+                                ws = __dadd_rn(ws, wi);
+                                wxs = __dadd_rn(wxs, __dmul_rn(wi, pts[i]));
+                            }
                     }
+                } else if (cache) {
+                    s_cf[j] = -1;
+                }
+                if (ws > 0.0) {
+                    nx[j] = __ddiv_rn(wxs, ws);
+                    cnt[j] = 1;  // reuse as "non-empty" flag
                 } else {
-                    for (int i = 0; i < n; ++i)
-                        if (assign[i] == j) {
-                            double wi = w[i];
-                            ws = __dadd_rn(ws, wi);
-                            wxs = __dadd_rn(wxs, __dmul_rn(wi, pts[i]));
-                        }
+                    cnt[j] = 0;
+                    empty = true;
                 }
             }
-            if (ws > 0.0) {
-                nx[j] = __ddiv_rn(wxs, ws);
-                cnt[j] = 1;  // reuse as "non-empty" flag
-            } else {
-                cnt[j] = 0;
+            empty = __any_sync(0xffffffffu, empty);
+            if (!empty) {  // convergence: max |nx - c| (exact, order-free), c <- nx
+                double mv = 0.0;
+                for (int j = lane; j < k; j += 32) mv = fmax(mv, fabs(__dsub_rn(nx[j], c[j])));
+                for (int o = 16; o > 0; o >>= 1) mv = fmax(mv, __shfl_xor_sync(0xffffffffu, mv, o));
+                __syncwarp();
+                for (int j = lane; j < k; j += 32) c[j] = nx[j];
+                if (lane == 0) sm.done = mv <= __dmul_rn(tol, scale);
+            } else if (lane == 0) {
                 sm.any_empty = 1;
             }
         }
@@ -344,18 +408,17 @@ __device__ int lloyd_block(const double* pts, const double* w, int n, double* c,
                 long used = 0;
                 for (int j = 0; j < k; ++j)
                     if (!cnt[j] && used < nt) nx[j] = top[used++].v;
+                double mv = 0.0;
+                for (int j = 0; j < k; ++j) mv = fmax(mv, fabs(__dsub_rn(nx[j], c[j])));
+                for (int j = 0; j < k; ++j) c[j] = nx[j];
+                sm.done = mv <= __dmul_rn(tol, scale);
             }
+            if (threadIdx.x < 64) s_cf[threadIdx.x] = -1;  // the scratch held `top`
             __syncthreads();
         }
-        if (threadIdx.x == 0) {
-            double mv = 0.0;
-            for (int j = 0; j < k; ++j) mv = fmax(mv, fabs(__dsub_rn(nx[j], c[j])));
-            for (int j = 0; j < k; ++j) c[j] = nx[j];
-            sm.done = mv <= __dmul_rn(tol, scale);
-        }
-        __syncthreads();
         iters = it + 1;
         if (sm.done) break;
+        __syncthreads();  // sm.done / s_fast are rewritten by the next iteration
     }
     if (threadIdx.x == 0) IntroSort<double, LessD>{}.sort(c, k);
     __syncthreads();
@@ -377,16 +440,7 @@ __device__ double sq_loss_block(const double* pts, const double* w, int n, const
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double loss = 0.0;
-        int i = 0;
-        for (; i + 8 <= n; i += 8) {
-            double v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = tmp[i + u];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) loss = __dadd_rn(loss, v[u]);
-        }
-        for (; i < n; ++i) loss = __dadd_rn(loss, tmp[i]);
+        const double loss = seq_prefix(tmp, 0, n, 0.0, nullptr);
         sm.red[0] = loss;
     }
     __syncthreads();
@@ -394,6 +448,9 @@ __device__ double sq_loss_block(const double* pts, const double* w, int n, const
     __syncthreads();
     return r;
 }
+
+// optional phase timing per CTA (DQTG_KM_TIMING=1): clocks of kpp / lloyd / loss, iterations, n
+__device__ long long g_km_timing[1024][6];
 
 __global__ void __launch_bounds__(kKB) kmeans_restarts_kernel(const KProblem* probs,
                                                               int restarts, int smem_n) {
@@ -434,9 +491,16 @@ __global__ void __launch_bounds__(kKB) kmeans_restarts_kernel(const KProblem* pr
     ScoreVal* top = (ScoreVal*)d2;  // reseed scratch reuses d2/prob (2n doubles)
     if (threadIdx.x == 0) mt64_seed(sm.rng, P.seed + (uint64_t)t);
     __syncthreads();
+    const long long c0 = clock64();
     kpp_init(pts, w, n, k, d2, prob, pref, c, sm);
-    lloyd_block(pts, w, n, c, nx, first, last, cnt, k, 1e-6, 100, assign, pref, top, true, sm);
+    const long long c1 = clock64();
+    const int its = lloyd_block(pts, w, n, c, nx, first, last, cnt, k, 1e-6, 100, assign, pref, top, true, sm);
+    const long long c2 = clock64();
     double loss = sq_loss_block(pts, w, n, c, k, prob, sm);
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {
+        long long* g = g_km_timing[blockIdx.x];
+        g[0] = c1 - c0, g[1] = c2 - c1, g[2] = clock64() - c2, g[3] = its, g[4] = n, g[5] = k;
+    }
     for (int j = threadIdx.x; j < k; j += blockDim.x) P.centers[(size_t)t * k + j] = c[j];
     if (threadIdx.x == 0) P.loss[t] = loss;
 }
@@ -503,6 +567,14 @@ void run_kmeans(Engine& e, std::vector<KProblem>& probs, float* cb_out, int cb_s
                                                                        cb_stride, cb_len_dev); }
     e.launched(2);
     DQTG_CUDA(cudaGetLastError());
+    if (getenv("DQTG_KM_TIMING")) {
+        e.sync();
+        static long long h[1024][6];
+        DQTG_CUDA(cudaMemcpyFromSymbol(h, g_km_timing, sizeof(h)));
+        for (size_t b = 0; b < probs.size() * restarts && b < 1024; ++b)
+            fprintf(stderr, "km cta %zu: kpp %lld lloyd %lld loss %lld clk, iters %lld, n %lld k %lld\n", b,
+                    h[b][0], h[b][1], h[b][2], h[b][3], h[b][4], h[b][5]);
+    }
 }
 
 void compact_keys(Engine& e, const unsigned long long* hist, int64_t hs_stride, int64_t HS,
