@@ -331,30 +331,24 @@ def run_ours(args):
     launches = eng.launches - launches0
     ms_sequential = ms
 
-    # pipelined chain (N=1): quantize(i+1) on stream Q overlaps encode(i) on stream E
+    # pipelined chain (N=1): a pool of worker streams, step k on worker k mod W;
+    # encode(k) waits on quantize(k-1) (paper_2306_11800_b200/pipeline.py)
     pipelined = None
     if world == 1 and not args.no_pipeline:
         from paper_2306_11800_b200.pipeline import ChainCompressor
 
-        cc = ChainCompressor(local)
-        pck = []
-        for i in range(n_snap):
-            c = cc.checkpoint(names, types, shapes)
-            c.set_weights([ckpts[i].weights_dev + 4 * ckpts[i].tensor_offset(j)
-                           for j in range(len(layout))])
-            c.set_ema(tensor_ptrs(ema.data_ptr(), layout))
-            pck.append(c)
+        cc = ChainCompressor(local, workers=args.workers)
         torch.cuda.synchronize()
-        base = cc.run(pck[:args.warmup + 1], cfg, 1, list(range(args.warmup + 1)))
+        base = cc.run(ckpts[:args.warmup + 1], cfg, 1, list(range(args.warmup + 1)))
         cc.sync()
         torch.cuda.synchronize()
         l0 = cc.launches
         tp0 = time.perf_counter()
-        cc.run(pck[args.warmup + 1:], cfg, 1, list(range(args.warmup + 1, n_snap)), base=base)
+        cc.run(ckpts[args.warmup + 1:], cfg, 1, list(range(args.warmup + 1, n_snap)), base=base)
         cc.sync()
         pipelined = (time.perf_counter() - tp0) * 1e3
         launches_p = cc.launches - l0
-        del base, cc, pck
+        del base, cc
     if pipelined is not None and pipelined < ms:
         ms = pipelined
         launches = launches_p
@@ -396,52 +390,78 @@ def run_ours(args):
                 "kernels_ms_per_step": {k: round(v[1] / prof_steps, 4) for k, v in
                                         sorted(prof.items(), key=lambda kv: -kv[1][1])}}
 
-    # e2e through the C ABI with host buffers (pinned), record read back each step
+    # e2e through the public API with HOST buffers: every step copies that step's
+    # weights from pinned host memory (H2D) and reads its record back into pinned
+    # host memory (D2H).  N=1: the worker-pool chain compressor (copies overlap the
+    # other workers' kernels); N>1: the tensor-sharded path.
     pinned = [torch.from_numpy(h).pin_memory() for h in host_snaps]
-    e2e_ck = E.DevCheckpoint(eng, names, types, shapes)
-    e2e_ck.set_ema(tensor_ptrs(ema.data_ptr(), layout))
-    e2e_ck.set_weights(tensor_ptrs(pinned[0].data_ptr(), layout))
-    if world > 1:
+    e2e_steps = max(6, min(args.steps, 12))
+    h2d = d2h = 0
+    if world == 1:
+        from paper_2306_11800_b200.pipeline import ChainCompressor
+
+        cc = ChainCompressor(local, workers=args.workers)
+        host = (names, types, shapes, tensor_ptrs(ema.data_ptr(), layout))
+        rec_host = [torch.empty(int(4 * N), dtype=torch.uint8).pin_memory()
+                    for _ in range(cc.nw)]
+        d2h_l = []
+
+        def grab(k, r):
+            n = E.LIB.dqtg_record_size(r)
+            E._check(E.LIB.dqtg_record_copy(r, rec_host[k % cc.nw].data_ptr()))
+            d2h_l.append(n)
+
+        def host_series(k0, n):
+            return [tensor_ptrs(pinned[(k0 + j) % len(pinned)].data_ptr(), layout)
+                    for j in range(n)]
+
+        e2e_base = cc.run(host_series(0, cc.nw + 1), cfg, 1, list(range(cc.nw + 1)), host=host)
+        cc.sync()
+        d2h_l.clear()
+        te = time.perf_counter()
+        cc.run(host_series(cc.nw + 1, e2e_steps), cfg, 1,
+               list(range(cc.nw + 1, cc.nw + 1 + e2e_steps)), base=e2e_base, on_record=grab,
+               host=host)
+        cc.sync()
+        e2e_s = time.perf_counter() - te
+        h2d = 4 * N * e2e_steps
+        d2h = sum(d2h_l)
+        e2e_path = ("ChainCompressor.run(host weights): per step H2D of the pinned snapshot + "
+                    "quantize + encode_delta_record + record D2H, worker-pool streams")
+        del cc, e2e_base
+    else:
+        e2e_ck = E.DevCheckpoint(eng, names, types, shapes)
+        e2e_ck.set_ema(tensor_ptrs(ema.data_ptr(), layout))
+        e2e_ck.set_weights(tensor_ptrs(pinned[0].data_ptr(), layout))
         e2e_state, _, _ = DIST.compress_sharded(eng, e2e_ck, cfg, 1, 0, None, device=dev,
                                                 n_tensors_total=len(names) * world)
-    else:
-        e2e_state = eng.quantize(e2e_ck, cfg, 1, 0)
-    rec_host = torch.empty(int(4 * N), dtype=torch.uint8).pin_memory()
-    e2e_steps = max(3, min(args.steps, 5))
-    h2d = d2h = 0
 
-    def e2e_step(i, prev):
-        nonlocal h2d, d2h
-        e2e_ck.set_weights(tensor_ptrs(pinned[i % len(pinned)].data_ptr(), layout))
-        h2d += 4 * N
-        if world > 1:  # per-rank blocks D2H, gathered and assembled on rank 0
+        def e2e_step(i, prev):
+            nonlocal h2d, d2h
+            e2e_ck.set_weights(tensor_ptrs(pinned[i % len(pinned)].data_ptr(), layout))
+            h2d += 4 * N
             st, rec, stats = DIST.compress_sharded(eng, e2e_ck, cfg, 1, i, prev, device=dev,
                                                    n_tensors_total=len(names) * world,
                                                    gather_record=True)
             d2h += stats["record_bytes_local"]
             return st
-        st, r = eng.compress_step(e2e_ck, cfg, 1, i, prev)
-        n = E.LIB.dqtg_record_size(r)
-        E._check(E.LIB.dqtg_record_copy(r, rec_host.data_ptr()))
-        E.LIB.dqtg_record_destroy(r)
-        d2h += n
-        return st
 
-    e2e_state = e2e_step(1, e2e_state)
-    barrier()
-    h2d = d2h = 0
-    te = time.perf_counter()
-    for i in range(2, 2 + e2e_steps):
-        e2e_state = e2e_step(i, e2e_state)
-    barrier()
-    e2e_s = time.perf_counter() - te
+        e2e_state = e2e_step(1, e2e_state)
+        barrier()
+        h2d = d2h = 0
+        te = time.perf_counter()
+        for i in range(2, 2 + e2e_steps):
+            e2e_state = e2e_step(i, e2e_state)
+        barrier()
+        e2e_s = time.perf_counter() - te
+        e2e_path = "dqtg_ckpt_set_weights(pinned host) + sharded compress + record gather"
     if world > 1:
         tt = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
     e2e = {"value": 4.0 * N * world * e2e_steps / e2e_s / 1e9, "unit": "GB/s",
            "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
-           "path": "dqtg_ckpt_set_weights(pinned host) + dqtg_compress_step + dqtg_record_copy"}
+           "path": e2e_path}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -471,8 +491,9 @@ def run_ours(args):
                        "record_bytes": rec_mean, "compression_ratio": cr,
                        "ms_per_step_sequential": ms_sequential / args.steps,
                        "ms_per_step_pipelined": None if pipelined is None else pipelined / args.steps,
-                       "timing": ("pipelined chain: quantize(i+1) || encode(i) on two streams, "
-                                  "host wall clock with device sync on both ends"
+                       "timing": (f"pipelined chain: {args.workers} worker streams (step k on "
+                                  f"worker k mod {args.workers}), host wall clock with device "
+                                  f"sync on both ends"
                                   if pipelined is not None and ms == pipelined else
                                   "CUDA events on the engine stream")},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
@@ -492,6 +513,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true")
+    ap.add_argument("--workers", type=int, default=2, help="worker streams of the chain pipeline")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -44,7 +44,7 @@ void approx_kmeans(Engine& e, const float* values_any, uint64_t n, uint32_t k, d
     auto* nk = (int*)e.buf("ak.nk", 16);
     compact_keys(e, gh, T.HS, T.HS, T.d_key, sigma, 1, pts, kc, kw, T.HS, nk);
     int h_nk = 0;
-    DQTG_CUDA(cudaMemcpyAsync(&h_nk, nk, 4, cudaMemcpyDeviceToHost, e.stream));
+    e.d2h(&h_nk, nk, 4);
     e.check_err();
     float* d_cb = (float*)e.buf("ak.cb", (size_t)k * 4 + 4);
     uint32_t* d_len = (uint32_t*)e.buf("ak.len", 16);
@@ -62,7 +62,7 @@ void approx_kmeans(Engine& e, const float* values_any, uint64_t n, uint32_t k, d
         probs[0].slot = 0;
         run_kmeans(e, probs, d_cb, (int)k, d_len);
     }
-    DQTG_CUDA(cudaMemcpyAsync(len, d_len, 4, cudaMemcpyDeviceToHost, e.stream));
+    e.d2h(len, d_len, 4);
     e.sync();
     if (*len) e.from_device(cb, d_cb, (size_t)*len * 4);
     e.check_err();

@@ -1,6 +1,7 @@
 // extern "C" surface of libdqtg.so (include/dqtg.h).  Every entry point catches
 // internal failures and turns them into a dqtg_status + thread-local message.
 #include <cstdlib>
+#include <exception>
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -44,8 +45,22 @@ static dqtg_status guard(F&& f) {
     }
 }
 
-#define LOCK(eng)                                       \
-    std::lock_guard<std::recursive_mutex> lk_((eng)->mu); \
+// Engine lock for one API call; a call that unwinds with an exception drops the
+// engine's pending staged read-backs (their host destinations are gone).
+struct EngineCall {
+    Engine* e;
+    std::lock_guard<std::recursive_mutex> lk;
+    int exc;
+    explicit EngineCall(Engine* eng) : e(eng), lk(eng->mu), exc(std::uncaught_exceptions()) {}
+    ~EngineCall() {
+        if (std::uncaught_exceptions() > exc) {
+            cudaStreamSynchronize(e->stream);
+            e->pend.clear();
+        }
+    }
+};
+#define LOCK(eng)              \
+    EngineCall lk_((eng));     \
     (eng)->activate()
 
 extern "C" {
@@ -97,10 +112,18 @@ dqtg_status dqtg_engine_sync(dqtg_engine* h) {
 
 uint64_t dqtg_engine_launches(const dqtg_engine* h) { return h->e.launches; }
 
+// process-wide reference point of the DQTG_TIMELINE dump (recorded at the first enable)
+static cudaEvent_t g_epoch = nullptr;
+
 dqtg_status dqtg_engine_profile(dqtg_engine* h, int enable) {
     return guard([&] {
         LOCK(&h->e);
         h->e.profiling = enable != 0;
+        if (enable && !g_epoch) {
+            h->e.activate();
+            DQTG_CUDA(cudaEventCreate(&g_epoch));
+            DQTG_CUDA(cudaEventRecord(g_epoch, h->e.stream));
+        }
     });
 }
 
@@ -113,9 +136,9 @@ dqtg_status dqtg_engine_profile_report(dqtg_engine* h, char* json, uint64_t cap)
         if (getenv("DQTG_TIMELINE") && !e.spans.empty()) {  // per-launch start/end (ms) on stderr
             for (auto& s : e.spans) {
                 float a = 0.0f, b = 0.0f;
-                DQTG_CUDA(cudaEventElapsedTime(&a, e.spans[0].a, s.a));
-                DQTG_CUDA(cudaEventElapsedTime(&b, e.spans[0].a, s.b));
-                fprintf(stderr, "timeline %9.3f %9.3f %8.3f %s\n", a, b, b - a, s.name);
+                DQTG_CUDA(cudaEventElapsedTime(&a, g_epoch, s.a));
+                DQTG_CUDA(cudaEventElapsedTime(&b, g_epoch, s.b));
+                fprintf(stderr, "timeline %9.3f %9.3f %8.3f %p %s\n", a, b, b - a, (void*)e.stream, s.name);
             }
         }
         for (auto& s : e.spans) {

@@ -45,6 +45,7 @@ struct Seg {
 
 struct EncArgs {
     int ntiles;
+    unsigned int* tile_ctr;  // dynamic tile scheduling (zeroed per launch)
     const uint32_t* crc_shift;  // per tile
     uint32_t n_tb;              // tensors * B
     const Tile* tiles;
@@ -207,11 +208,11 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_kernel(EncArgs A) {
     for (uint32_t i = tid; i < 8 * 16 * 40; i += kCB) S.nib[i] = (&g_crc_nib[0][0][0])[i];
     for (uint32_t i = tid; i < B * NS; i += kCB) S.freq[i] = 0;
     if (tid < 16) S.sd[tid - 16] = 0;
-    const int t0 = (int)((int64_t)blockIdx.x * A.ntiles / gridDim.x);
-    const int t1 = (int)((int64_t)(blockIdx.x + 1) * A.ntiles / gridDim.x);
+    __shared__ int s_base;
     uint32_t cur_tensor = 0xffffffffu;
 
-    for (int ti = t0; ti < t1; ++ti) {
+    for (int base; (base = grab_tiles(A.tile_ctr, 4, &s_base)) < A.ntiles;)
+    for (int ti = base; ti < min(base + 4, A.ntiles); ++ti) {
         const Tile T = A.tiles[ti];
         const uint32_t cnt = T.count;
         if (T.tensor != cur_tensor) {  // flush the previous tensor's symbol counts
@@ -1537,6 +1538,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     A.ov_count = small;
     A.crc_acc = (uint32_t*)(small + 1);
     A.tile_crc = (uint32_t*)e.buf("e.tile_crc", (size_t)ntiles * 4 + 4);
+    A.tile_ctr = (unsigned int*)(small + 5);
     A.err = e.d_err;
     DQTG_CUDA(cudaMemsetAsync(A.freq, 0, freq_n * 4, st));
     DQTG_CUDA(cudaMemsetAsync(small, 0, 64, st));
@@ -1546,7 +1548,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     A.ntiles = ntiles;
     {
         auto kfn = base ? enc_tile_kernel<true> : enc_tile_kernel<false>;
-        DQTG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e1_smem));
+        ensure_dyn_smem((const void*)kfn, e1_smem);
         int per_sm = 0;
         DQTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kCB, e1_smem));
         const int grid = std::max(1, std::min(ntiles, e.num_sms * std::max(1, per_sm)));
@@ -1577,7 +1579,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
 
     // overflow run lengths: sort + unique
     unsigned long long n_ov = 0;
-    DQTG_CUDA(cudaMemcpyAsync(&n_ov, A.ov_count, 8, cudaMemcpyDeviceToHost, st));
+    e.d2h(&n_ov, A.ov_count, 8);
     e.sync();
     DQTG_REQUIRE(n_ov <= A.ov_cap, DQTG_ERROR, "run-length overflow list exhausted");
     auto* ov_sorted = (unsigned long long*)e.buf("e.ov_sorted", n_ov * 8 + 8);
@@ -1600,7 +1602,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
         DQTG_CUDA(cudaMemsetAsync(nu, 0, 8, st));
     }
     unsigned long long n_unique = 0;
-    DQTG_CUDA(cudaMemcpyAsync(&n_unique, nu, 8, cudaMemcpyDeviceToHost, st));
+    e.d2h(&n_unique, nu, 8);
     e.sync();
     // H
     auto* gi = (GroupInfo*)e.buf("e.gi", (size_t)nt * B * sizeof(GroupInfo));
@@ -1619,7 +1621,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
             e.launched();
         }
         uint32_t h_max = 0;
-        DQTG_CUDA(cudaMemcpyAsync(&h_max, max_nov, 4, cudaMemcpyDeviceToHost, st));
+        e.d2h(&h_max, max_nov, 4);
         e.sync();
         uint32_t np2 = 1;
         while (np2 < NS + h_max) np2 <<= 1;
@@ -1636,8 +1638,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
         W.parent = (uint32_t*)e.buf("h.parent", ncap * 4);
         W.depth = (uint32_t*)e.buf("h.depth", ncap * 4);
         if (hsm > 48 * 1024)
-            DQTG_CUDA(cudaFuncSetAttribute(enc_huffman_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+            ensure_dyn_smem((const void*)enc_huffman_kernel, hsm);
         { DQTG_SPAN(e, "enc_huffman_kernel"); enc_huffman_kernel<<<nt * B, 32, hsm, st>>>(A, elems, ukey, ucnt, nu, gi, tab_sym, tab_len,
                                                      code_dense, len_dense, code_ov, len_ov, W, np2); }
         e.launched();
@@ -1668,7 +1669,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     { DQTG_SPAN(e, "tensor_scan_kernel"); tensor_scan_kernel<<<1, 1, 0, st>>>(tr, nt, prefix_len, total_d); }
     e.launched(3);
     unsigned long long total = 0;
-    DQTG_CUDA(cudaMemcpyAsync(&total, total_d, 8, cudaMemcpyDeviceToHost, st));
+    e.d2h(&total, total_d, 8);
     e.check_err();  // syncs
 
     // ---- writers
@@ -1740,7 +1741,7 @@ uint32_t crc32_device(Engine& e, const uint8_t* data, uint64_t n) {
     { DQTG_SPAN(e, "finish_crc_kernel"); finish_crc_kernel<<<1, 1, 0, e.stream>>>(acc, n, nullptr, out); }
     e.launched(2);
     uint32_t h = 0;
-    DQTG_CUDA(cudaMemcpyAsync(&h, out, 4, cudaMemcpyDeviceToHost, e.stream));
+    e.d2h(&h, out, 4);
     e.sync();
     return h;
 }

@@ -94,4 +94,15 @@ __device__ T block_exclusive_scan(T v, T* smem /* >= 33 */, T* total = nullptr) 
     return out;
 }
 
+// Dynamic tile scheduling for persistent CTAs: each grab takes `grab` consecutive
+// tiles from a global counter (zeroed before the launch), so a kernel sharing the
+// GPU with another stream's work load-balances instead of waiting on late CTAs.
+// Block-uniform; call from all threads.
+__device__ __forceinline__ int grab_tiles(unsigned int* ctr, int grab, int* s_base) {
+    __syncthreads();
+    if (threadIdx.x == 0) *s_base = (int)atomicAdd(ctr, (unsigned int)grab);
+    __syncthreads();
+    return *s_base;
+}
+
 }  // namespace dqtg

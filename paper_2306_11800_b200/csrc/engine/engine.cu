@@ -32,7 +32,8 @@ cudaEvent_t Engine::take_event() {
 Engine::~Engine() {
     cudaSetDevice(device);
     for (auto ev : event_pool) cudaEventDestroy(ev);
-    for (auto& kv : scratch) cudaFree(kv.second.first);
+    for (auto& kv : scratch) cudaFreeAsync(kv.second.first, stream);
+    cudaStreamSynchronize(stream);
     for (auto& kv : tables) {
         cudaFree(kv.second->d_U);
         cudaFree(kv.second->d_cell);
@@ -41,18 +42,18 @@ Engine::~Engine() {
     }
     if (d_err) cudaFree(d_err);
     if (pinned) cudaFreeHost(pinned);
+    for (auto& b : stage_blocks) cudaFreeHost(b.first);
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
 void* Engine::buf(const std::string& name, size_t bytes) {
     auto& slot = scratch[name];
     if (slot.second < bytes) {
-        if (slot.first) {
-            DQTG_CUDA(cudaStreamSynchronize(stream));
-            DQTG_CUDA(cudaFree(slot.first));
-        }
+        // stream-ordered: scratch is only touched by this engine's stream, so the
+        // old block is released after its last use without a device-wide sync
+        if (slot.first) DQTG_CUDA(cudaFreeAsync(slot.first, stream));
         size_t cap = bytes < 256 ? 256 : bytes + bytes / 4;
-        DQTG_CUDA(cudaMalloc(&slot.first, cap));
+        DQTG_CUDA(cudaMallocAsync(&slot.first, cap, stream));
         slot.second = cap;
     }
     return slot.first;
@@ -80,10 +81,38 @@ void* Engine::host_pinned(size_t bytes) {
     return pinned;
 }
 
+void Engine::d2h(void* dst, const void* src, size_t bytes) {
+    if (!bytes) return;
+    const size_t need = (bytes + 15) & ~(size_t)15;
+    if (stage_blocks.empty() || stage_used + need > stage_blocks.back().second) {
+        const size_t cap = std::max<size_t>(need, stage_blocks.empty() ? (1u << 20)
+                                                                       : 2 * stage_blocks.back().second);
+        uint8_t* p = nullptr;
+        DQTG_CUDA(cudaMallocHost(&p, cap));
+        stage_blocks.push_back({p, cap});
+        stage_used = 0;
+    }
+    uint8_t* at = stage_blocks.back().first + stage_used;
+    stage_used += need;
+    DQTG_CUDA(cudaMemcpyAsync(at, src, bytes, cudaMemcpyDeviceToHost, stream));
+    pend.push_back({dst, at, bytes});
+}
+
+void Engine::sync() {
+    DQTG_CUDA(cudaStreamSynchronize(stream));
+    for (auto& p : pend) memcpy(p.dst, p.staged, p.n);
+    pend.clear();
+    while (stage_blocks.size() > 1) {  // keep the largest (last) block
+        cudaFreeHost(stage_blocks.front().first);
+        stage_blocks.erase(stage_blocks.begin());
+    }
+    stage_used = 0;
+}
+
 void Engine::check_err() {
     uint32_t h = 0;
-    DQTG_CUDA(cudaMemcpyAsync(&h, d_err, 4, cudaMemcpyDeviceToHost, stream));
-    DQTG_CUDA(cudaStreamSynchronize(stream));
+    d2h(&h, d_err, 4);
+    sync();
     if (!h) return;
     DQTG_CUDA(cudaMemsetAsync(d_err, 0, 4, stream));
     if (h & kErrNonFinite) throw Fail(DQTG_NON_FINITE, "input contains NaN/Inf");
@@ -235,6 +264,16 @@ AlphaTables& Engine::alpha_tables(double alpha) {
     auto& ref = *t;
     tables[key] = std::move(t);
     return ref;
+}
+
+void ensure_dyn_smem(const void* func, size_t bytes) {
+    static std::mutex mu;
+    static std::map<const void*, size_t> set;
+    std::lock_guard<std::mutex> g(mu);
+    size_t& cur = set[func];
+    if (bytes <= cur) return;
+    DQTG_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    cur = bytes;
 }
 
 // ---- layouts --------------------------------------------------------------

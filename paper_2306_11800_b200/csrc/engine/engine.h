@@ -159,7 +159,20 @@ struct Engine {
     void* dalloc(size_t bytes);
     void dfree(void* p);
     void* host_pinned(size_t bytes);
-    void sync() { DQTG_CUDA(cudaStreamSynchronize(stream)); }
+    // Device->host read-back through a pinned staging arena: the copy is queued on
+    // the engine stream and lands in `dst` at the next sync()/check_err().  (A
+    // pageable destination would make the driver stage the copy synchronously,
+    // which serialises host threads driving other engines.)
+    void d2h(void* dst, const void* src, size_t bytes);
+    void sync();  // stream sync + pending read-backs
+    struct PendingD2H {
+        void* dst;
+        const void* staged;
+        size_t n;
+    };
+    std::vector<PendingD2H> pend;
+    std::vector<std::pair<uint8_t*, size_t>> stage_blocks;  // pinned; last = current
+    size_t stage_used = 0;
     void launched(int n = 1) { launches += n; }
     void check_err();  // reads + clears the device error word (syncs)
     // copy host-or-device memory into a device destination
@@ -168,6 +181,11 @@ struct Engine {
 };
 
 bool is_device_ptr(const void* p);
+
+// Raises a kernel's dynamic shared-memory limit to at least `bytes` and never
+// lowers it: engines on several host threads launch the same kernels with
+// different sizes, and a lowered limit would fail a concurrent launch.
+void ensure_dyn_smem(const void* func, size_t bytes);
 
 // Scoped CUDA-event span around one kernel launch (only when profiling).
 struct KSpan {

@@ -168,7 +168,7 @@ static void codebook_from_values(Engine& e, float* vals, uint64_t m, uint32_t k,
     { DQTG_SPAN(e, "zero_signs_kernel"); zero_signs_kernel<<<(unsigned)std::min<uint64_t>(1024, (m + 255) / 256 + 1), 256, 0, st>>>(
         vals, m, flags); }
     uint32_t hf = 0;
-    DQTG_CUDA(cudaMemcpyAsync(&hf, flags, 4, cudaMemcpyDeviceToHost, st));
+    e.d2h(&hf, flags, 4);
     e.sync();
     if (hf == 3u) {  // both signed zeros present: sign of the zero key follows std::sort
         float* tmp = (float*)e.buf("fb.tmp", m * 4);
@@ -187,7 +187,7 @@ static void codebook_from_values(Engine& e, float* vals, uint64_t m, uint32_t k,
     auto* nd_d = (unsigned long long*)e.buf("fb.nd", 8);
     { DQTG_SPAN(e, "unique_kernel"); unique_kernel<<<1, 1024, 0, st>>>(sorted, m, flags, flags + 1, keys, heads, nd_d); }
     unsigned long long nd = 0;
-    DQTG_CUDA(cudaMemcpyAsync(&nd, nd_d, 8, cudaMemcpyDeviceToHost, st));
+    e.d2h(&nd, nd_d, 8);
     e.sync();
     { DQTG_SPAN(e, "counts_from_heads_kernel"); counts_from_heads_kernel<<<(unsigned)((nd + 255) / 256 + 1), 256, 0, st>>>(heads, nd, m,
                                                                                counts); }
@@ -223,7 +223,7 @@ void distinct_value_codebook(Engine& e, const PassIn& a, const LtParams* d_lp, i
                                                   nullptr); }
     scan_tiles(e, tile_cnt, ntiles, tile_off);
     unsigned long long m = 0;
-    DQTG_CUDA(cudaMemcpyAsync(&m, tile_off + ntiles, 8, cudaMemcpyDeviceToHost, e.stream));
+    e.d2h(&m, tile_off + ntiles, 8);
     e.sync();
     float* vals = (float*)e.buf("fb.vals", m * 4 + 4);
     { DQTG_SPAN(e, "gather_q_kernel"); gather_q_kernel<<<ntiles, 256, 0, e.stream>>>(a, expl, d_lp, lt, 1, tile_cnt, tile_off, vals); }

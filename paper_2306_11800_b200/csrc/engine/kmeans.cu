@@ -560,8 +560,7 @@ void run_kmeans(Engine& e, std::vector<KProblem>& probs, float* cb_out, int cb_s
     const size_t budget = 200 * 1024;
     int smem_n = (int)((budget - std::min(budget, head)) / 44);  // 5 doubles + 1 int per key
     size_t smem = head + (size_t)std::min(maxn, smem_n) * 44 + 64;
-    DQTG_CUDA(cudaFuncSetAttribute(kmeans_restarts_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ensure_dyn_smem((const void*)kmeans_restarts_kernel, smem);
     { DQTG_SPAN(e, "kmeans_restarts_kernel"); kmeans_restarts_kernel<<<(unsigned)(probs.size() * restarts), kKB, smem, e.stream>>>(dp, restarts, smem_n); }
     { DQTG_SPAN(e, "kmeans_select_kernel"); kmeans_select_kernel<<<(unsigned)probs.size(), 32, 0, e.stream>>>(dp, restarts, cb_out,
                                                                        cb_stride, cb_len_dev); }
@@ -684,7 +683,7 @@ void kmeanspp_host_api(Engine& e, const double* pts, const double* w, uint64_t n
                                                              d.scr, d.c, d.st); }
     e.launched();
     int st = 0;
-    DQTG_CUDA(cudaMemcpyAsync(&st, d.st, 4, cudaMemcpyDeviceToHost, e.stream));
+    e.d2h(&st, d.st, 4);
     e.sync();
     DQTG_REQUIRE(st != 1, DQTG_ERROR, "weights must be non-negative");
     DQTG_REQUIRE(st != 2, DQTG_ERROR, "total weight must be positive");
@@ -705,7 +704,7 @@ void lloyd_host_api(Engine& e, const double* pts, const double* w, uint64_t n, d
         d.pts, d.w, (int)n, (int)k, tol, (int)max_iter, d.scr, d.c, it); }
     e.launched();
     int h = 0;
-    DQTG_CUDA(cudaMemcpyAsync(&h, it, 4, cudaMemcpyDeviceToHost, e.stream));
+    e.d2h(&h, it, 4);
     e.from_device(centers, d.c, (size_t)k * 8);
     e.sync();
     if (iters) *iters = (uint32_t)h;
@@ -717,7 +716,7 @@ double sq_loss_host_api(Engine& e, const double* pts, const double* w, uint64_t 
     { DQTG_SPAN(e, "loss_api_kernel"); loss_api_kernel<<<1, kKB, 0, e.stream>>>(d.pts, d.w, (int)n, d.c, (int)k, d.scr, d.scr + n + 1); }
     e.launched();
     double h = 0;
-    DQTG_CUDA(cudaMemcpyAsync(&h, d.scr + n + 1, 8, cudaMemcpyDeviceToHost, e.stream));
+    e.d2h(&h, d.scr + n + 1, 8);
     e.sync();
     return h;
 }

@@ -35,7 +35,7 @@ void sketch_build(Engine& e, const float* x_any, uint64_t n, double alpha, uint6
         e.launched();
     }
     std::vector<unsigned long long> h(T.HS);
-    DQTG_CUDA(cudaMemcpyAsync(h.data(), gh, T.HS * 8, cudaMemcpyDeviceToHost, e.stream));
+    e.d2h(h.data(), gh, T.HS * 8);
     e.check_err();
     *zero = h[T.NB];
     for (int64_t k = T.kmin; k <= T.kmax; ++k) {

@@ -23,6 +23,7 @@
 namespace dqtg {
 
 constexpr int kPB = 256;  // threads per streaming CTA
+constexpr int kGrab = 4;  // tiles per dynamic grab of the persistent passes
 
 __device__ __forceinline__ float4 ld4(const float* p) { return __ldg((const float4*)p); }
 
@@ -69,8 +70,7 @@ __global__ void __launch_bounds__(kPB, 6) pass_a_kernel(PassIn a, unsigned long 
     uint32_t* shs = sh + W;
     for (int i = threadIdx.x; i < 2 * W; i += blockDim.x) sh[i] = 0;
     __syncthreads();
-    const int t0 = (int)((int64_t)blockIdx.x * a.ntiles / gridDim.x);
-    const int t1 = (int)((int64_t)(blockIdx.x + 1) * a.ntiles / gridDim.x);
+    __shared__ int s_base;
     int cur = -1;
     auto flush = [&](int lt) {
         if (EXPL) {
@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(kPB, 6) pass_a_kernel(PassIn a, unsigned long 
             hist_flush_pos(shs, gh_sens + lt * a.HS, a.tab);
         }
     };
-    for (int ti = t0; ti < t1; ++ti) {
+    for (int base; (base = grab_tiles(a.tile_ctr, kGrab, &s_base)) < a.ntiles;)
+    for (int ti = base; ti < min(base + kGrab, a.ntiles); ++ti) {
         const Tile T = a.tiles[ti];
         const int lt = a.types[T.tensor];
         if (lt != cur) {
@@ -179,11 +180,11 @@ __global__ void __launch_bounds__(kPB, 6) pass_b_kernel(PassIn a, const LtParams
     __shared__ uint32_t s_red[kPB / 32];
     hist_clear(sh);
     __syncthreads();
-    const int t0 = (int)((int64_t)blockIdx.x * a.ntiles / gridDim.x);
-    const int t1 = (int)((int64_t)(blockIdx.x + 1) * a.ntiles / gridDim.x);
+    __shared__ int s_base;
     int cur = -1;
     LtParams P{};
-    for (int ti = t0; ti < t1; ++ti) {
+    for (int base; (base = grab_tiles(a.tile_ctr, kGrab, &s_base)) < a.ntiles;)
+    for (int ti = base; ti < min(base + kGrab, a.ntiles); ++ti) {
         const Tile T = a.tiles[ti];
         const int lt = a.types[T.tensor];
         if (lt != cur) {
@@ -610,6 +611,7 @@ static PassIn pass_in(Engine& e, const DevCkpt& c, const AlphaTables& T, int met
     a.tab = e.bucket_tab(T);
     a.HS = T.HS;
     a.err = e.d_err;
+    a.tile_ctr = (unsigned int*)e.buf("q.tile_ctr", 64);
     return a;
 }
 
@@ -715,11 +717,11 @@ static void stage_pass_a(Engine& e, const DevCkpt& c, const PassIn& a, uint32_t 
                          unsigned long long* gh_sens) {
     const int ntiles = a.ntiles;
     cudaStream_t st = e.stream;
+    DQTG_CUDA(cudaMemsetAsync(a.tile_ctr, 0, 4, st));
     if (c.explicit_scores) {
         const size_t smem = (size_t)2 * kWinSlots * 4;
         const int grid = stream_grid(e, ntiles, 3);
-        DQTG_CUDA(cudaFuncSetAttribute(pass_a_kernel<true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        ensure_dyn_smem((const void*)pass_a_kernel<true>, smem);
         { DQTG_SPAN(e, "pass_a_kernel"); pass_a_kernel<true><<<grid, kPB, smem, st>>>(a, gh_mag, gh_sens, mask_mag, mask_sens); }
     } else {
         const size_t smem = (size_t)2 * kPosSlots * 4;
@@ -753,9 +755,8 @@ static void stage_keys(Engine& e, const Layout& L, Stage& s, const AlphaTables& 
     compact_keys(e, s.gh_val, HS, HS, T.d_key, s.cfg.sigma, kLayerTypes, s.pts, s.kc, s.kw, HS,
                  s.n_keys);
     s.h_tprot.resize(L.nt + 1);
-    DQTG_CUDA(cudaMemcpyAsync(s.h_nkeys, s.n_keys, sizeof(s.h_nkeys), cudaMemcpyDeviceToHost, st));
-    DQTG_CUDA(cudaMemcpyAsync(s.h_tprot.data(), s.tensor_prot, (L.nt + 1) * 8,
-                              cudaMemcpyDeviceToHost, st));
+    e.d2h(s.h_nkeys, s.n_keys, sizeof(s.h_nkeys));
+    e.d2h(s.h_tprot.data(), s.tensor_prot, (L.nt + 1) * 8);
 }
 
 static void stage_pass_b(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s,
@@ -766,6 +767,7 @@ static void stage_pass_b(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s,
     cudaStream_t st = e.stream;
     DQTG_CUDA(cudaMemsetAsync(s.gh_val, 0, (size_t)kLayerTypes * HS * 8, st));
     DQTG_CUDA(cudaMemsetAsync(s.tensor_prot, 0, (size_t)(L.nt + 1) * 8, st));
+    DQTG_CUDA(cudaMemsetAsync(a.tile_ctr, 0, 4, st));
     const size_t smem = (size_t)kWinSlots * 4;
     int grid = stream_grid(e, ntiles, 6);
     DQTG_CUDA(cudaFuncSetAttribute(pass_b_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -898,8 +900,8 @@ std::unique_ptr<QState> quantize(Engine& e, const DevCkpt& c, const dqtg_config&
     q->d_pval = (decltype(q->d_pval))e.dalloc((acc + 1) * 2);
     stage_pass_c(e, c, a, s, *q);
     std::vector<float> hcb((size_t)kLayerTypes * q->cb_stride);
-    DQTG_CUDA(cudaMemcpyAsync(q->cb_len, s.cb_len, sizeof(q->cb_len), cudaMemcpyDeviceToHost, e.stream));
-    DQTG_CUDA(cudaMemcpyAsync(hcb.data(), q->d_cb, hcb.size() * 4, cudaMemcpyDeviceToHost, e.stream));
+    e.d2h(q->cb_len, s.cb_len, sizeof(q->cb_len));
+    e.d2h(hcb.data(), q->d_cb, hcb.size() * 4);
     e.check_err();
     for (int lt = 0; lt < kLayerTypes; ++lt)
         q->cb[lt].assign(hcb.begin() + (size_t)lt * q->cb_stride,
@@ -993,8 +995,8 @@ std::unique_ptr<QState> shard_stage3(Engine& e, const DevCkpt& c, const dqtg_con
     q->d_pval = (uint16_t*)e.dalloc((acc + 1) * 2);
     if (L.N) stage_pass_c(e, c, a, s, *q);
     std::vector<float> hcb((size_t)kLayerTypes * q->cb_stride);
-    DQTG_CUDA(cudaMemcpyAsync(q->cb_len, s.cb_len, sizeof(q->cb_len), cudaMemcpyDeviceToHost, e.stream));
-    DQTG_CUDA(cudaMemcpyAsync(hcb.data(), q->d_cb, hcb.size() * 4, cudaMemcpyDeviceToHost, e.stream));
+    e.d2h(q->cb_len, s.cb_len, sizeof(q->cb_len));
+    e.d2h(hcb.data(), q->d_cb, hcb.size() * 4);
     e.check_err();
     for (int lt = 0; lt < kLayerTypes; ++lt)
         q->cb[lt].assign(hcb.begin() + (size_t)lt * q->cb_stride,
@@ -1085,7 +1087,7 @@ void eval_batch(Engine& e, const DevCkpt& c, const dqtg_config* cfgs, const uint
         { DQTG_SPAN(e, "tile_sq_kernel"); tile_sq_kernel<<<ntiles, kPB, 0, e.stream>>>(L.d_tiles, c.w, nullptr, tile_v); }
         { DQTG_SPAN(e, "lt_sum_kernel"); lt_sum_kernel<<<1, 512, 0, e.stream>>>(L.d_tiles, L.d_types, ntiles, tile_v, d_lt); }
         e.launched(2);
-        DQTG_CUDA(cudaMemcpyAsync(orig, d_lt, sizeof(orig), cudaMemcpyDeviceToHost, e.stream));
+        e.d2h(orig, d_lt, sizeof(orig));
     }
     std::vector<std::unique_ptr<Stage>> stages(m);
     std::map<uint64_t, std::pair<unsigned long long*, unsigned long long*>> scores_by_alpha;
@@ -1162,10 +1164,9 @@ void eval_batch(Engine& e, const DevCkpt& c, const dqtg_config* cfgs, const uint
         { DQTG_SPAN(e, "lt_sum_kernel"); lt_sum_kernel<<<1, 512, 0, e.stream>>>(L.d_tiles, L.d_types, ntiles, tile_v, d_lt); }
         e.launched(2);
         uint32_t cbl[kLayerTypes];
-        DQTG_CUDA(cudaMemcpyAsync(diff, d_lt, sizeof(diff), cudaMemcpyDeviceToHost, e.stream));
-        DQTG_CUDA(cudaMemcpyAsync(cbl, s.cb_len, sizeof(cbl), cudaMemcpyDeviceToHost, e.stream));
-        DQTG_CUDA(cudaMemcpyAsync(hcounts.data(), counts, hcounts.size() * 8, cudaMemcpyDeviceToHost,
-                                  e.stream));
+        e.d2h(diff, d_lt, sizeof(diff));
+        e.d2h(cbl, s.cb_len, sizeof(cbl));
+        e.d2h(hcounts.data(), counts, hcounts.size() * 8);
         e.check_err();
         quality[i] = quality_from(L, diff, orig);
         std::vector<uint64_t> np(L.nt);
@@ -1183,11 +1184,11 @@ double proxy_quality(Engine& e, const DevCkpt& orig, const float* recon_dev) {
         auto* d_lt = (double*)e.buf("pq.lt", 16 * 8);
         { DQTG_SPAN(e, "tile_sq_kernel"); tile_sq_kernel<<<ntiles, kPB, 0, e.stream>>>(L.d_tiles, orig.w, nullptr, tile_v); }
         { DQTG_SPAN(e, "lt_sum_kernel"); lt_sum_kernel<<<1, 512, 0, e.stream>>>(L.d_tiles, L.d_types, ntiles, tile_v, d_lt); }
-        DQTG_CUDA(cudaMemcpyAsync(o, d_lt, sizeof(o), cudaMemcpyDeviceToHost, e.stream));
+        e.d2h(o, d_lt, sizeof(o));
         e.sync();
         { DQTG_SPAN(e, "tile_sq_kernel"); tile_sq_kernel<<<ntiles, kPB, 0, e.stream>>>(L.d_tiles, orig.w, recon_dev, tile_v); }
         { DQTG_SPAN(e, "lt_sum_kernel"); lt_sum_kernel<<<1, 512, 0, e.stream>>>(L.d_tiles, L.d_types, ntiles, tile_v, d_lt); }
-        DQTG_CUDA(cudaMemcpyAsync(d, d_lt, sizeof(d), cudaMemcpyDeviceToHost, e.stream));
+        e.d2h(d, d_lt, sizeof(d));
         e.launched(4);
         e.sync();
     }
@@ -1219,7 +1220,7 @@ void dequantize(Engine& e, const QState& q, float* out_dev) {
     count_protected(e, L, q.d_levels, cb_len_d, tile_prot);
     { DQTG_SPAN(e, "scan_u32_kernel"); scan_u32_kernel<<<1, 1024, 0, e.stream>>>(tile_prot, ntiles, tile_off); }
     unsigned long long total = 0;
-    DQTG_CUDA(cudaMemcpyAsync(&total, tile_off + ntiles, 8, cudaMemcpyDeviceToHost, e.stream));
+    e.d2h(&total, tile_off + ntiles, 8);
     e.sync();
     DQTG_REQUIRE(total == q.prot_total, DQTG_CORRUPT_INDEX, "unreferenced protected entries");
     { DQTG_SPAN(e, "dequant_kernel"); dequant_kernel<<<ntiles, 256, 0, e.stream>>>(L.d_tiles, L.d_types, L.d_off, q.d_cb,

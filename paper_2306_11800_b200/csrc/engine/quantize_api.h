@@ -39,6 +39,7 @@ struct PassIn {
     BucketTab tab;
     int64_t HS;
     uint32_t* err;
+    unsigned int* tile_ctr;  // dynamic tile scheduling of persistent passes (zeroed per launch)
 };
 
 struct QuantPlan {

@@ -1,5 +1,5 @@
-"""The pipelined chain (quantize(i+1) || encode(i) on two streams) produces the
-same records as the sequential C-ABI step and as the oracle."""
+"""The pipelined chain (worker-pool streams, encode(k) waits on quantize(k-1))
+produces the same records as the oracle, for device-resident and host inputs."""
 import numpy as np
 import pytest
 
@@ -8,7 +8,8 @@ from tests.util import flat, make_tensors, perturb
 pytestmark = pytest.mark.gpu
 
 
-def test_pipelined_chain_matches_sequential_and_oracle(oracle):
+@pytest.mark.parametrize("workers,host_inputs", [(1, False), (2, False), (3, False), (3, True)])
+def test_pipelined_chain_matches_oracle(oracle, workers, host_inputs):
     from oracle.oracle import Config as OC
     from paper_2306_11800_b200 import engine as E
     from paper_2306_11800_b200.pipeline import ChainCompressor
@@ -23,13 +24,17 @@ def test_pipelined_chain_matches_sequential_and_oracle(oracle):
     shapes = [t.shape for t in series[0]]
     sizes = np.cumsum([t.data.size for t in series[0]])[:-1]
     cfg = E.Config()
-    cc = ChainCompressor(0)
+    cc = ChainCompressor(0, workers=workers)
     cks = []
     for ts in series:
+        if host_inputs:
+            cks.append([np.ascontiguousarray(t.data, np.float32) for t in ts])
+            continue
         c = cc.checkpoint(names, types, shapes)
         c.set_weights([t.data for t in ts])
         c.set_ema(np.split(ema, sizes))
         cks.append(c)
+    host = (names, types, shapes, np.split(ema, sizes)) if host_inputs else None
     recs = {}
 
     def grab(k, r):
@@ -38,7 +43,7 @@ def test_pipelined_chain_matches_sequential_and_oracle(oracle):
         E._check(E.LIB.dqtg_record_copy(r, buf.ctypes.data))
         recs[k] = buf.tobytes()
 
-    cc.run(cks, cfg, 3, list(range(len(cks))), on_record=grab)
+    cc.run(cks, cfg, 3, list(range(len(cks))), on_record=grab, host=host)
     cc.sync()
     prev = None
     for k, ts in enumerate(series):
