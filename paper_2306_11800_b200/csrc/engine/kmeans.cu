@@ -68,6 +68,8 @@ __global__ void __launch_bounds__(1024) compact_keys_kernel(const unsigned long 
 // ---- per-restart CTA -----------------------------------------------------
 struct KShared {
     Mt64 rng;
+    const double2* wx;  // (w, x) pairs in shared memory, or null (working set in global)
+    int in_smem;        // pts/w/d2/prob/pref live in shared memory
     int pick;
     int done;
     int any_empty;
@@ -75,23 +77,46 @@ struct KShared {
     double red[kKB / 32];
 };
 
+// Explicit shared-memory accesses for the serial chains (generic loads add latency).
+__device__ __forceinline__ unsigned sh_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ double ld_sh(const double* p) {
+    double v;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(sh_addr(p)));
+    return v;
+}
+__device__ __forceinline__ double2 ld_sh2(const double2* p) {
+    double2 v;
+    asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(sh_addr(p)));
+    return v;
+}
+__device__ __forceinline__ void st_sh(double* p, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(sh_addr(p)), "d"(v) : "memory");
+}
+
 // Sequential fp64 sum s += v[i] for i in [a, n) in index order (the reference's
-// order), optional running values out[i]; 16 loads in flight per block.
+// order), optional running values out[i] (SH: both arrays in shared memory).
+template <bool SH>
 __device__ __forceinline__ double seq_prefix(const double* v, int a, int n, double s, double* out) {
     int i = a;
     for (; i + 16 <= n; i += 16) {
         double cv[16];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) cv[u] = v[i + u];
+        for (int u = 0; u < 16; ++u) cv[u] = SH ? ld_sh(v + i + u) : v[i + u];
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
             s = __dadd_rn(s, cv[u]);
-            if (out) out[i + u] = s;
+            if (out) {
+                if (SH) st_sh(out + i + u, s);
+                else out[i + u] = s;
+            }
         }
     }
     for (; i < n; ++i) {
-        s = __dadd_rn(s, v[i]);
-        if (out) out[i] = s;
+        s = __dadd_rn(s, SH ? ld_sh(v + i) : v[i]);
+        if (out) {
+            if (SH) st_sh(out + i, s);
+            else out[i] = s;
+        }
     }
     return s;
 }
@@ -102,7 +127,7 @@ __device__ int kpp_pick(const double* prob, double* pref, int n, int from, KShar
     if (threadIdx.x == 0) {
         // pref[0..from) are unchanged from the previous pick (same terms, same order)
         double s = from > 0 ? pref[from - 1] : 0.0;
-        s = seq_prefix(prob, from, n, s, pref);
+        s = sm.in_smem ? seq_prefix<true>(prob, from, n, s, pref) : seq_prefix<false>(prob, from, n, s, pref);
         if (n > 0) s = pref[n - 1];
         int res;
         if (!(s > 0.0)) {
@@ -202,12 +227,35 @@ __device__ void kpp_init(const double* pts, const double* w, int n, int k, doubl
     __syncthreads();
 }
 
-// Sequential (w, w*x) sums over keys [a, b] continuing from (ws, wxs) in key
-// order (the reference's accumulation order), running values stored for reuse.
-__device__ __forceinline__ void chain_sums(const double* w, const double* x, int a, int b,
-                                           double& ws, double& wxs, double* rw, double* rwx) {
+// optional phase timing per CTA (DQTG_KM_TIMING=1): clocks of kpp / lloyd / loss,
+// iterations, n, k, Lloyd chain steps (max over lanes, summed), Lloyd sum clocks
+__device__ long long g_km_timing[1024][8];
+
+// Sequential (w, w*x) sums over keys [a, b] from 0 in key order (the reference's
+// accumulation order).  wx: (w, x) pairs in shared memory (one 16-byte load per
+// key) or null.
+__device__ __forceinline__ void chain_sums(const double2* wx, const double* w, const double* x,
+                                           int a, int b, double& ws, double& wxs) {
     int i = a;
     const int e = b + 1;
+    if (wx) {
+        for (; i + 8 <= e; i += 8) {
+            double2 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = ld_sh2(wx + i + u);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                ws = __dadd_rn(ws, v[u].x);
+                wxs = __dadd_rn(wxs, __dmul_rn(v[u].x, v[u].y));
+            }
+        }
+        for (; i < e; ++i) {
+            const double2 v = ld_sh2(wx + i);
+            ws = __dadd_rn(ws, v.x);
+            wxs = __dadd_rn(wxs, __dmul_rn(v.x, v.y));
+        }
+        return;
+    }
     for (; i + 8 <= e; i += 8) {
         double wv[8], xv[8];
 #pragma unroll
@@ -216,39 +264,31 @@ __device__ __forceinline__ void chain_sums(const double* w, const double* x, int
         for (int u = 0; u < 8; ++u) {
             ws = __dadd_rn(ws, wv[u]);
             wxs = __dadd_rn(wxs, __dmul_rn(wv[u], xv[u]));
-            if (rw) rw[i + u] = ws, rwx[i + u] = wxs;
         }
     }
     for (; i < e; ++i) {
         const double wi = w[i];
         ws = __dadd_rn(ws, wi);
         wxs = __dadd_rn(wxs, __dmul_rn(wi, x[i]));
-        if (rw) rw[i] = ws, rwx[i] = wxs;
     }
 }
 
 // weighted_lloyd (quantize.cpp:180-254); c (k centres) is updated in place.
 // Iterations whose centres are strictly ascending and well separated (the fast
 // path: clusters are contiguous key ranges) run on warp 0 alone with warp
-// primitives; the sequential per-cluster sums are cached per key (rw / rwx) and
-// reused while a cluster's first key is unchanged (an identical chain prefix).
-// The general assignment and the empty-cluster reseed use the whole block.
+// primitives, one lane per cluster chain.  The general assignment and the
+// empty-cluster reseed use the whole block.
 __device__ int lloyd_block(const double* pts, const double* w, int n, double* c, double* nx,
                            int* first, int* last, int* cnt, int k, double tol, int max_iter,
                            int* assign, double* score, ScoreVal* top, bool distinct,
                            KShared& sm) {
-    __shared__ int s_cf[64], s_cl[64];  // cached chain [first, last] per cluster (-1: none)
     __shared__ int s_fast;
-    double* rw = (double*)top;  // running sums share the reseed scratch (2n doubles)
-    double* rwx = rw + n;
-    const bool cache = k <= 64;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double lm = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) lm = fmax(lm, fabs(pts[i]));
     double scale = block_max_d(lm, sm);
     if (scale == 0.0) scale = 1.0;
     const double gap = __dmul_rn(scale, 0x1.0p-40);
-    if (threadIdx.x < 64) s_cf[threadIdx.x] = -1;
     int iters = 0;
     for (int it = 0; it < max_iter; ++it) {
         if (wid == 0) {
@@ -320,27 +360,15 @@ __device__ int lloyd_block(const double* pts, const double* w, int n, double* c,
                 __syncwarp();
             }
             bool empty = false;
+            long long t_sum = clock64();
+            int steps_max = 0;
             for (int j = lane; j < k; j += 32) {
                 double ws = 0.0, wxs = 0.0;
                 if (cnt[j] > 0) {
                     if (last[j] - first[j] + 1 == cnt[j]) {
-                        // one code path for every lane (divergent chains would serialise):
-                        // reuse the cached chain prefix when the cluster's first key is unchanged
-                        const int a = first[j], b = last[j];
-                        int from = a;
-                        if (fast && cache && s_cf[j] == a && s_cl[j] >= a) {
-                            const int cb = min(s_cl[j], b);
-                            ws = rw[cb];
-                            wxs = rwx[cb];
-                            from = cb + 1;
-                        }
-                        chain_sums(w, pts, from, b, ws, wxs, fast && cache ? rw : nullptr, rwx);
-                        if (cache) {
-                            s_cf[j] = fast ? a : -1;
-                            s_cl[j] = b;
-                        }
+                        steps_max = max(steps_max, cnt[j]);
+                        chain_sums(sm.wx, w, pts, first[j], last[j], ws, wxs);
                     } else {
-                        if (cache) s_cf[j] = -1;
                         for (int i = 0; i < n; ++i)
                             if (assign[i] == j) {
                                 double wi = w[i];
@@ -348,8 +376,6 @@ __device__ int lloyd_block(const double* pts, const double* w, int n, double* c,
                                 wxs = __dadd_rn(wxs, __dmul_rn(wi, pts[i]));
                             }
                     }
-                } else if (cache) {
-                    s_cf[j] = -1;
                 }
                 if (ws > 0.0) {
                     nx[j] = __ddiv_rn(wxs, ws);
@@ -360,6 +386,11 @@ __device__ int lloyd_block(const double* pts, const double* w, int n, double* c,
                 }
             }
             empty = __any_sync(0xffffffffu, empty);
+            for (int o = 16; o > 0; o >>= 1) steps_max = max(steps_max, __shfl_xor_sync(0xffffffffu, steps_max, o));
+            if (lane == 0 && blockIdx.x < 1024) {
+                g_km_timing[blockIdx.x][6] += steps_max;
+                g_km_timing[blockIdx.x][7] += clock64() - t_sum;
+            }
             if (!empty) {  // convergence: max |nx - c| (exact, order-free), c <- nx
                 double mv = 0.0;
                 for (int j = lane; j < k; j += 32) mv = fmax(mv, fabs(__dsub_rn(nx[j], c[j])));
@@ -413,7 +444,6 @@ __device__ int lloyd_block(const double* pts, const double* w, int n, double* c,
                 for (int j = 0; j < k; ++j) c[j] = nx[j];
                 sm.done = mv <= __dmul_rn(tol, scale);
             }
-            if (threadIdx.x < 64) s_cf[threadIdx.x] = -1;  // the scratch held `top`
             __syncthreads();
         }
         iters = it + 1;
@@ -440,7 +470,8 @@ __device__ double sq_loss_block(const double* pts, const double* w, int n, const
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        const double loss = seq_prefix(tmp, 0, n, 0.0, nullptr);
+        const double loss = sm.in_smem ? seq_prefix<true>(tmp, 0, n, 0.0, nullptr)
+                                       : seq_prefix<false>(tmp, 0, n, 0.0, nullptr);
         sm.red[0] = loss;
     }
     __syncthreads();
@@ -450,7 +481,6 @@ __device__ double sq_loss_block(const double* pts, const double* w, int n, const
 }
 
 // optional phase timing per CTA (DQTG_KM_TIMING=1): clocks of kpp / lloyd / loss, iterations, n
-__device__ long long g_km_timing[1024][6];
 
 __global__ void __launch_bounds__(kKB) kmeans_restarts_kernel(const KProblem* probs,
                                                               int restarts, int smem_n) {
@@ -475,14 +505,18 @@ __global__ void __launch_bounds__(kKB) kmeans_restarts_kernel(const KProblem* pr
         d2 = sw + n;
         prob = d2 + n;
         pref = prob + n;
-        assign = (int*)(pref + n);
+        double2* wx = (double2*)(((uintptr_t)(pref + n) + 15) & ~(uintptr_t)15);
+        assign = (int*)(wx + n);
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             sp[i] = P.pts[i];
             sw[i] = P.w[i];
+            wx[i] = make_double2(P.w[i], P.pts[i]);
         }
         pts = sp;
         w = sw;
+        if (threadIdx.x == 0) sm.wx = wx, sm.in_smem = 1;
     } else {
+        if (threadIdx.x == 0) sm.wx = nullptr, sm.in_smem = 0;
         d2 = P.scratch + (size_t)t * P.scratch_stride;
         prob = d2 + n;
         pref = prob + n;
@@ -490,6 +524,7 @@ __global__ void __launch_bounds__(kKB) kmeans_restarts_kernel(const KProblem* pr
     }
     ScoreVal* top = (ScoreVal*)d2;  // reseed scratch reuses d2/prob (2n doubles)
     if (threadIdx.x == 0) mt64_seed(sm.rng, P.seed + (uint64_t)t);
+    if (threadIdx.x == 0 && blockIdx.x < 1024) g_km_timing[blockIdx.x][6] = g_km_timing[blockIdx.x][7] = 0;
     __syncthreads();
     const long long c0 = clock64();
     kpp_init(pts, w, n, k, d2, prob, pref, c, sm);
@@ -558,8 +593,8 @@ void run_kmeans(Engine& e, std::vector<KProblem>& probs, float* cb_out, int cb_s
     for (auto& p : probs) maxn = std::max(maxn, p.n);
     const size_t head = ((size_t)2 * maxk + (3 * maxk + 1) / 2 + 1) * 8;
     const size_t budget = 200 * 1024;
-    int smem_n = (int)((budget - std::min(budget, head)) / 44);  // 5 doubles + 1 int per key
-    size_t smem = head + (size_t)std::min(maxn, smem_n) * 44 + 64;
+    int smem_n = (int)((budget - std::min(budget, head)) / 60);  // 5 doubles + pair + int per key
+    size_t smem = head + (size_t)std::min(maxn, smem_n) * 60 + 96;
     ensure_dyn_smem((const void*)kmeans_restarts_kernel, smem);
     { DQTG_SPAN(e, "kmeans_restarts_kernel"); kmeans_restarts_kernel<<<(unsigned)(probs.size() * restarts), kKB, smem, e.stream>>>(dp, restarts, smem_n); }
     { DQTG_SPAN(e, "kmeans_select_kernel"); kmeans_select_kernel<<<(unsigned)probs.size(), 32, 0, e.stream>>>(dp, restarts, cb_out,
@@ -568,11 +603,11 @@ void run_kmeans(Engine& e, std::vector<KProblem>& probs, float* cb_out, int cb_s
     DQTG_CUDA(cudaGetLastError());
     if (getenv("DQTG_KM_TIMING")) {
         e.sync();
-        static long long h[1024][6];
+        static long long h[1024][8];
         DQTG_CUDA(cudaMemcpyFromSymbol(h, g_km_timing, sizeof(h)));
         for (size_t b = 0; b < probs.size() * restarts && b < 1024; ++b)
-            fprintf(stderr, "km cta %zu: kpp %lld lloyd %lld loss %lld clk, iters %lld, n %lld k %lld\n", b,
-                    h[b][0], h[b][1], h[b][2], h[b][3], h[b][4], h[b][5]);
+            fprintf(stderr, "km cta %zu: kpp %lld lloyd %lld loss %lld clk, iters %lld, n %lld k %lld, chain steps %lld in %lld clk\n", b,
+                    h[b][0], h[b][1], h[b][2], h[b][3], h[b][4], h[b][5], h[b][6], h[b][7]);
     }
 }
 
@@ -596,6 +631,7 @@ __global__ void __launch_bounds__(kKB) kpp_api_kernel(const double* pts, const d
                                                       double* out, int* status) {
     extern __shared__ double dsm[];
     __shared__ KShared sm;
+    if (threadIdx.x == 0) sm.wx = nullptr, sm.in_smem = 0;  // working set in global memory
     // validation (quantize.cpp:98-113): weights, total, distinct count
     if (threadIdx.x == 0) {
         int st = 0;
@@ -632,6 +668,7 @@ __global__ void __launch_bounds__(kKB) lloyd_api_kernel(const double* pts, const
                                                         int* iters) {
     extern __shared__ double dsm[];
     __shared__ KShared sm;
+    if (threadIdx.x == 0) sm.wx = nullptr, sm.in_smem = 0;  // working set in global memory
     double* c = dsm;
     double* nx = c + k;
     int* first = (int*)(nx + k);
@@ -652,6 +689,7 @@ __global__ void __launch_bounds__(kKB) loss_api_kernel(const double* pts, const 
                                                        const double* c, int k, double* tmp,
                                                        double* out) {
     __shared__ KShared sm;
+    if (threadIdx.x == 0) sm.wx = nullptr, sm.in_smem = 0;  // working set in global memory
     double l = sq_loss_block(pts, w, n, c, k, tmp, sm);
     if (threadIdx.x == 0) *out = l;
 }
