@@ -513,7 +513,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true")
-    ap.add_argument("--workers", type=int, default=2, help="worker streams of the chain pipeline")
+    ap.add_argument("--workers", type=int, default=4, help="worker streams of the chain pipeline")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -196,6 +196,29 @@ dqtg_status dqtg_compress_step(dqtg_engine *e, const dqtg_ckpt *c, const dqtg_co
                                double quality_delta, dqtg_qstate **state_out,
                                dqtg_record **record_out);
 
+/* ---- pipelined delta chain (Chain::append over a series, chain.cpp:86-129) ----
+ * A pool of `workers` engines, each on its own CUDA stream and host thread.
+ * Snapshot k runs on worker k mod W: its weights are copied into the worker's
+ * device checkpoint (from host or device memory), quantized, then encoded as a
+ * delta against snapshot k-1 (the stream waits on the event recorded after
+ * quantize(k-1)); states are released once both encodes that read them are
+ * done.  Records are identical to dqtg_compress_step run in order.
+ * weights[k * n_tensors + i] = tensor i of snapshot k (`_any`); ema[i] (`_any`,
+ * null: magnitude scores only).  on_record(user, k, record) runs on a worker
+ * thread (calls may arrive out of step order; the record is valid during the
+ * call).  *last_out (optional) receives the state of the last snapshot. */
+typedef struct dqtg_pipe dqtg_pipe;
+typedef void (*dqtg_record_fn)(void *user, uint64_t k, const dqtg_record *record);
+dqtg_status dqtg_pipe_create(int device, int workers, dqtg_pipe **out);
+void dqtg_pipe_destroy(dqtg_pipe *p);
+uint64_t dqtg_pipe_launches(const dqtg_pipe *p);
+dqtg_status dqtg_pipe_run(dqtg_pipe *p, const dqtg_layout *layout,
+                          const float *const *weights_any, uint64_t n_snapshots,
+                          const uint64_t *steps, const float *const *ema_any,
+                          const dqtg_config *cfg, uint64_t seed, const dqtg_qstate *base,
+                          double quality_delta, dqtg_record_fn on_record, void *user,
+                          dqtg_qstate **last_out);
+
 /* partition_params (quantize.cpp:34-92): per-element part codes, 0 quantize,
  * 1 prune, 2 protect, written to masks[i] (numel_i bytes each) */
 dqtg_status dqtg_partition(dqtg_engine *e, const dqtg_ckpt *c, const dqtg_config *cfg,

@@ -13,20 +13,13 @@
 
 using namespace dqtg;
 
-struct dqtg_engine {
-    Engine e;
-};
-struct dqtg_ckpt {
-    DevCkpt c;
-};
-struct dqtg_qstate {
-    std::unique_ptr<QState> q;
-};
-struct dqtg_record {
-    std::unique_ptr<Record> r;
-};
+#include "handles.h"
 
 static thread_local std::string g_err;
+
+namespace dqtg {
+void set_last_error(const std::string& m) { g_err = m; }
+}
 
 template <typename F>
 static dqtg_status guard(F&& f) {
@@ -63,6 +56,31 @@ struct EngineCall {
     EngineCall lk_((eng));     \
     (eng)->activate()
 
+namespace dqtg {
+void init_engine(Engine& e, int device, void* stream) {
+    e.device = device;
+    DQTG_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    DQTG_CUDA(cudaGetDeviceProperties(&prop, device));
+    DQTG_REQUIRE(prop.major >= 10, DQTG_CUDA,
+                 "dqtg needs a Blackwell (sm_100) device; found " + std::string(prop.name));
+    e.num_sms = prop.multiProcessorCount;
+    if (stream) {
+        e.stream = (cudaStream_t)stream;
+    } else {
+        DQTG_CUDA(cudaStreamCreateWithFlags(&e.stream, cudaStreamNonBlocking));
+        e.own_stream = true;
+    }
+    DQTG_CUDA(cudaMalloc(&e.d_err, 16));
+    // keep freed pool memory cached: per-step states/records reuse it
+    cudaMemPool_t pool;
+    DQTG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = ~0ull;
+    DQTG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    DQTG_CUDA(cudaMemset(e.d_err, 0, 16));
+}
+}  // namespace dqtg
+
 extern "C" {
 
 const char* dqtg_last_error(void) { return g_err.c_str(); }
@@ -72,27 +90,7 @@ dqtg_status dqtg_engine_create(int device, void* stream, dqtg_engine** out) {
     return guard([&] {
         auto* h = new dqtg_engine();
         try {
-            Engine& e = h->e;
-            e.device = device;
-            DQTG_CUDA(cudaSetDevice(device));
-            cudaDeviceProp prop;
-            DQTG_CUDA(cudaGetDeviceProperties(&prop, device));
-            DQTG_REQUIRE(prop.major >= 10, DQTG_CUDA,
-                         "dqtg needs a Blackwell (sm_100) device; found " + std::string(prop.name));
-            e.num_sms = prop.multiProcessorCount;
-            if (stream) {
-                e.stream = (cudaStream_t)stream;
-            } else {
-                DQTG_CUDA(cudaStreamCreateWithFlags(&e.stream, cudaStreamNonBlocking));
-                e.own_stream = true;
-            }
-            DQTG_CUDA(cudaMalloc(&e.d_err, 16));
-            // keep freed pool memory cached: per-step states/records reuse it
-            cudaMemPool_t pool;
-            DQTG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-            uint64_t keep = ~0ull;
-            DQTG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-            DQTG_CUDA(cudaMemset(e.d_err, 0, 16));
+            init_engine(h->e, device, stream);
         } catch (...) {
             delete h;
             throw;

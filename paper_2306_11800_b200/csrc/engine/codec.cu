@@ -215,6 +215,12 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_kernel(EncArgs A) {
     for (int ti = base; ti < min(base + 4, A.ntiles); ++ti) {
         const Tile T = A.tiles[ti];
         const uint32_t cnt = T.count;
+        if (tid == 0 && ti + 1 < min(base + 4, A.ntiles)) {  // next tile's levels into L2
+            const Tile N = A.tiles[ti + 1];
+            const uint32_t bytes = ((N.count + 7u) & ~7u) * 2u;
+            prefetch_l2(A.cur + N.start, bytes);
+            if (HAS_BASE) prefetch_l2(A.prev + N.start, bytes);
+        }
         if (T.tensor != cur_tensor) {  // flush the previous tensor's symbol counts
             __syncthreads();
             if (cur_tensor != 0xffffffffu) {

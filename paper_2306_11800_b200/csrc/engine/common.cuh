@@ -94,6 +94,13 @@ __device__ T block_exclusive_scan(T v, T* smem /* >= 33 */, T* total = nullptr) 
     return out;
 }
 
+// Bulk L2 prefetch (TMA engine, one instruction per region): the next tile's
+// inputs are in L2 by the time the CTA's loads reach them.  addr 16-B aligned,
+// bytes a multiple of 16.
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // Dynamic tile scheduling for persistent CTAs: each grab takes `grab` consecutive
 // tiles from a global counter (zeroed before the launch), so a kernel sharing the
 // GPU with another stream's work load-balances instead of waiting on late CTAs.

@@ -1,0 +1,217 @@
+// Pipelined delta chain (dqtg_pipe_*, include/dqtg.h): the native runtime behind
+// Chain::append over a series of snapshots (chain.cpp:86-129).
+//
+// W workers, each an engine with its own non-blocking CUDA stream and a host
+// thread.  Snapshot k runs on worker k mod W:
+//
+//   copy weights(k) -> worker checkpoint      (H2D from pinned host, or D2D)
+//   quantize(k)                               (passes A/B, k-means, pass C)
+//   record event q[k]; publish state k
+//   wait state k-1 published; stream waits on q[k-1]
+//   encode(k | k-1); on_record(k); stream sync
+//   release k-1 and k once both encodes that read them are done
+//
+// While one worker blocks on a host read-back (record size, overflow counts) or
+// a copy, the others keep the GPU fed, and the few-CTA phases (k-means restarts,
+// per-group Huffman) overlap the streaming passes of the other workers.
+#include <condition_variable>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "engine.h"
+#include "handles.h"
+
+using namespace dqtg;
+
+struct dqtg_pipe {
+    int device = 0;
+    std::vector<std::unique_ptr<Engine>> eng;
+    std::vector<std::unique_ptr<DevCkpt>> ck;  // per worker, rebuilt when the layout changes
+};
+
+namespace {
+
+bool same_layout(const Layout& a, const dqtg_layout* l) {
+    if (a.nt != l->n_tensors) return false;
+    size_t d = 0;
+    for (uint32_t i = 0; i < a.nt; ++i) {
+        if (a.types[i] != (l->types ? l->types[i] : 6) || a.ranks[i] != l->ranks[i]) return false;
+        for (uint32_t r = 0; r < a.ranks[i]; ++r)
+            if (a.dims[i][r] != l->dims[d + r]) return false;
+        d += l->ranks[i];
+        if (l->names && a.names[i] != l->names[i]) return false;
+    }
+    return true;
+}
+
+void upload(Engine& e, const Layout& L, float* dst, const float* const* src) {
+    for (uint32_t i = 0; i < L.nt; ++i)
+        if (L.numel[i]) e.to_device(dst + L.off[i], src[i], L.numel[i] * 4);
+}
+
+struct Run {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<std::unique_ptr<QState>> states;
+    std::vector<cudaEvent_t> qev;
+    std::vector<char> ready;
+    std::vector<int> users;
+    bool failed = false;
+    dqtg_status code = DQTG_OK;
+    std::string msg;
+
+    void fail(dqtg_status c, const std::string& m) {
+        std::lock_guard<std::mutex> g(mu);
+        if (!failed) failed = true, code = c, msg = m;
+        cv.notify_all();
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+dqtg_status dqtg_pipe_create(int device, int workers, dqtg_pipe** out) {
+    try {
+        DQTG_REQUIRE(workers >= 1 && workers <= 16, DQTG_ERROR, "workers must be in [1, 16]");
+        auto p = std::make_unique<dqtg_pipe>();
+        p->device = device;
+        for (int w = 0; w < workers; ++w) {
+            p->eng.push_back(std::make_unique<Engine>());
+            init_engine(*p->eng.back(), device, nullptr);
+        }
+        p->ck.resize(workers);
+        *out = p.release();
+        return DQTG_OK;
+    } catch (const Fail& x) {
+        set_last_error(x.what());
+        return x.code;
+    } catch (const std::exception& x) {
+        set_last_error(x.what());
+        return DQTG_ERROR;
+    }
+}
+
+void dqtg_pipe_destroy(dqtg_pipe* p) {
+    if (!p) return;
+    for (auto& e : p->eng) cudaStreamSynchronize(e->stream);
+    p->ck.clear();
+    p->eng.clear();
+    delete p;
+}
+
+uint64_t dqtg_pipe_launches(const dqtg_pipe* p) {
+    uint64_t n = 0;
+    for (auto& e : p->eng) n += e->launches;
+    return n;
+}
+
+dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* const* weights,
+                          uint64_t n, const uint64_t* steps, const float* const* ema,
+                          const dqtg_config* cfg, uint64_t seed, const dqtg_qstate* base,
+                          double quality, dqtg_record_fn on_record, void* user,
+                          dqtg_qstate** last_out) {
+    try {
+        const int W = (int)p->eng.size();
+        DQTG_CUDA(cudaSetDevice(p->device));
+        // worker checkpoints (weights + EMA) for this layout
+        for (int w = 0; w < W; ++w) {
+            Engine& e = *p->eng[w];
+            auto& c = p->ck[w];
+            if (!c || !same_layout(*c->L, layout)) {
+                c = std::make_unique<DevCkpt>();
+                c->eng = &e;
+                c->L = make_layout(&e, layout);
+                DQTG_CUDA(cudaMalloc(&c->w, c->L->Np * 4));
+                DQTG_CUDA(cudaMemset(c->w, 0, c->L->Np * 4));
+            }
+            c->explicit_scores = false;
+            c->has_sens = ema != nullptr;
+            if (ema) {
+                if (!c->ema) {
+                    DQTG_CUDA(cudaMalloc(&c->ema, c->L->Np * 4));
+                    DQTG_CUDA(cudaMemset(c->ema, 0, c->L->Np * 4));
+                }
+                upload(e, *c->L, c->ema, ema);
+                c->ema_seeded = true;
+            }
+            e.sync();
+        }
+        const uint32_t nt = layout->n_tensors;
+        Run R;
+        R.states.resize(n);
+        R.qev.assign(n, nullptr);
+        R.ready.assign(n, 0);
+        R.users.assign(n, 0);
+        for (uint64_t k = 0; k < n; ++k) DQTG_CUDA(cudaEventCreateWithFlags(&R.qev[k], cudaEventDisableTiming));
+
+        auto release = [&](uint64_t k) {  // caller holds R.mu
+            if (++R.users[k] == 2 && k + 1 != n) R.states[k].reset();
+        };
+        auto worker = [&](int w) {
+            Engine& e = *p->eng[w];
+            DevCkpt& c = *p->ck[w];
+            try {
+                e.activate();
+                for (uint64_t k = (uint64_t)w; k < n; k += (uint64_t)W) {
+                    {
+                        std::lock_guard<std::mutex> g(R.mu);
+                        if (R.failed) return;
+                    }
+                    upload(e, *c.L, c.w, weights + k * nt);
+                    auto q = quantize(e, c, *cfg, seed, steps ? steps[k] : k);
+                    DQTG_CUDA(cudaEventRecord(R.qev[k], e.stream));
+                    const QState* target = q.get();
+                    const QState* prev = base ? base->q.get() : nullptr;
+                    {
+                        std::unique_lock<std::mutex> g(R.mu);
+                        R.states[k] = std::move(q);
+                        R.ready[k] = 1;
+                        R.cv.notify_all();
+                        if (k > 0) {
+                            R.cv.wait(g, [&] { return R.failed || R.ready[k - 1]; });
+                            if (R.failed) return;
+                            prev = R.states[k - 1].get();
+                        }
+                    }
+                    if (k > 0) DQTG_CUDA(cudaStreamWaitEvent(e.stream, R.qev[k - 1], 0));
+                    dqtg_record rec;
+                    rec.r = encode_record(e, prev, *target, quality);
+                    if (on_record) on_record(user, k, &rec);
+                    rec.r.reset();
+                    e.sync();  // encode(k) complete: its inputs may be released
+                    std::lock_guard<std::mutex> g(R.mu);
+                    release(k);
+                    if (k > 0) release(k - 1);
+                }
+            } catch (const Fail& x) {
+                R.fail(x.code, x.what());
+            } catch (const std::exception& x) {
+                R.fail(DQTG_ERROR, x.what());
+            }
+        };
+        std::vector<std::thread> th;
+        for (int w = 0; w < W; ++w) th.emplace_back(worker, w);
+        for (auto& t : th) t.join();
+        for (auto ev : R.qev) cudaEventDestroy(ev);
+        if (R.failed) throw Fail(R.code, R.msg);
+        if (last_out) {
+            *last_out = nullptr;
+            if (n) {
+                auto* s = new dqtg_qstate();
+                s->q = std::move(R.states[n - 1]);
+                *last_out = s;
+            }
+        }
+        return DQTG_OK;
+    } catch (const Fail& x) {
+        set_last_error(x.what());
+        return x.code;
+    } catch (const std::exception& x) {
+        set_last_error(x.what());
+        return DQTG_ERROR;
+    }
+}
+
+}  // extern "C"

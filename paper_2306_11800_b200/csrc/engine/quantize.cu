@@ -23,7 +23,21 @@
 namespace dqtg {
 
 constexpr int kPB = 256;  // threads per streaming CTA
-constexpr int kGrab = 4;  // tiles per dynamic grab of the persistent passes
+constexpr int kGrab = 8;  // tiles per dynamic grab of the persistent passes
+constexpr int kPfDist = 148 * 5;  // pass C: about one wave of resident CTAs ahead
+
+// L2 prefetch of one tile's score inputs (w + EMA, or the explicit scores)
+__device__ __forceinline__ void prefetch_tile(const PassIn& a, int ti, bool expl) {
+    const Tile T = a.tiles[ti];
+    const uint32_t bytes = ((T.count + 3u) & ~3u) * 4u;
+    prefetch_l2(a.w + T.start, bytes);
+    if (expl) {
+        prefetch_l2(a.mag + T.start, bytes);
+        if (a.has_sens) prefetch_l2(a.sens + T.start, bytes);
+    } else if (a.has_sens) {
+        prefetch_l2(a.ema + T.start, bytes);
+    }
+}
 
 __device__ __forceinline__ float4 ld4(const float* p) { return __ldg((const float4*)p); }
 
@@ -85,6 +99,7 @@ __global__ void __launch_bounds__(kPB, 6) pass_a_kernel(PassIn a, unsigned long 
     for (int ti = base; ti < min(base + kGrab, a.ntiles); ++ti) {
         const Tile T = a.tiles[ti];
         const int lt = a.types[T.tensor];
+        if (threadIdx.x == 0 && ti + 1 < min(base + kGrab, a.ntiles)) prefetch_tile(a, ti + 1, EXPL);
         if (lt != cur) {
             __syncthreads();
             if (cur >= 0) flush(cur);
@@ -187,6 +202,7 @@ __global__ void __launch_bounds__(kPB, 6) pass_b_kernel(PassIn a, const LtParams
     for (int ti = base; ti < min(base + kGrab, a.ntiles); ++ti) {
         const Tile T = a.tiles[ti];
         const int lt = a.types[T.tensor];
+        if (threadIdx.x == 0 && ti + 1 < min(base + kGrab, a.ntiles)) prefetch_tile(a, ti + 1, EXPL);
         if (lt != cur) {
             __syncthreads();
             if (cur >= 0) hist_flush(sh, gh_val + cur * a.HS, a.tab);
@@ -406,6 +422,8 @@ __global__ void __launch_bounds__(kPB) pass_c_kernel(PassIn a, const LtParams* l
     const int ti = blockIdx.x;
     const Tile T = a.tiles[ti];
     const int lt = a.types[T.tensor];
+    // the tile a CTA launched about one residency later will read (L2 prefetch)
+    if (threadIdx.x == 0 && ti + kPfDist < a.ntiles) prefetch_tile(a, ti + kPfDist, EXPL);
     const uint32_t k = cb_len[lt], kp = pow2_ceil(k);
     for (uint32_t j = threadIdx.x; j < kp; j += blockDim.x) s_lb[j] = lb[lt * lb_stride + j];
     const LtParams P = lp[lt];

@@ -65,6 +65,10 @@ class _Info(C.Structure):
 _P = C.c_void_p
 
 
+# void (*)(void* user, uint64_t k, const dqtg_record* record)
+RECORD_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.c_void_p)
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() (make -C "
@@ -130,6 +134,12 @@ def _load():
         "dqtg_delta_compute": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_uint32, _P]),
         "dqtg_delta_apply": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_uint32, _P]),
         "dqtg_crc32": (C.c_int, [_P, _P, C.c_uint64, C.POINTER(C.c_uint32)]),
+        "dqtg_pipe_create": (C.c_int, [C.c_int, C.c_int, C.POINTER(_P)]),
+        "dqtg_pipe_destroy": (None, [_P]),
+        "dqtg_pipe_launches": (C.c_uint64, [_P]),
+        "dqtg_pipe_run": (C.c_int, [_P, C.POINTER(_Layout), _P, C.c_uint64, _P, _P,
+                                    C.POINTER(Config), C.c_uint64, _P, C.c_double, RECORD_FN, _P,
+                                    C.POINTER(_P)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -490,6 +500,59 @@ class Engine:
 
 
 _DEFAULT = None
+
+
+class Pipe:
+    """Native pipelined delta chain (dqtg_pipe_*, pipe.cu): `workers` engines with
+    their own streams and host threads; snapshot k runs on worker k mod W."""
+
+    def __init__(self, device=0, workers=2):
+        h = _P()
+        _check(LIB.dqtg_pipe_create(device, workers, C.byref(h)))
+        self.h = h
+        self.workers = workers
+        self._nominal = None  # engine used for calls on returned states
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            LIB.dqtg_pipe_destroy(self.h)
+            self.h = None
+
+    @property
+    def launches(self):
+        return LIB.dqtg_pipe_launches(self.h)
+
+    def run(self, names, types, shapes, snapshots, cfg, seed=1, steps=None, ema=None,
+            base=None, quality=0.0, on_record=None, engine=None):
+        """snapshots[k] = per-tensor arrays or raw (host/device) pointers of snapshot
+        k; ema = per-tensor arrays/pointers or None.  on_record(k, record_handle) is
+        called on a worker thread.  Returns the last snapshot's DevState."""
+        meta = _Meta(names, types, shapes)
+        nt = len(meta.names)
+        n = len(snapshots)
+        bufs = [_as_buf(a) for snap in snapshots for a in snap]
+        if len(bufs) != n * nt:
+            raise ValueError("every snapshot needs one array per tensor")
+        wptr = _ptr_array(bufs)
+        ebufs = None if ema is None else [_as_buf(a) for a in ema]
+        eptr = None if ebufs is None else _ptr_array(ebufs)
+        st = None
+        if steps is not None:
+            st = np.ascontiguousarray(steps, np.uint64)
+        cb = RECORD_FN(0) if on_record is None else RECORD_FN(lambda u, k, r: on_record(int(k), r))
+        h = _P()
+        _check(LIB.dqtg_pipe_run(self.h, C.byref(meta.c), wptr, n,
+                                 None if st is None else st.ctypes.data, eptr, C.byref(cfg), seed,
+                                 None if base is None else base.h, quality, cb, None, C.byref(h)))
+        if not h:
+            return base
+        if engine is None:
+            if self._nominal is None:
+                self._nominal = Engine(0)
+            engine = self._nominal
+        ds = DevState(engine, h, meta)
+        ds._owner = self  # the state's memory belongs to a pipe worker engine
+        return ds
 
 
 def default_engine() -> Engine:
