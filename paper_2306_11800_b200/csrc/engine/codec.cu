@@ -125,9 +125,10 @@ __device__ __forceinline__ void add_symbol(uint32_t* f, uint32_t NS, uint32_t B,
 constexpr int kCrcTabs = 10;  // T1,T3,T5,T7,T9,T11,T12,T13,T14,T15 (T_n: byte + n zero bytes)
 constexpr int kChunks = 512 / 32;  // chunks per warp range
 __device__ uint32_t g_crc_slice[kCrcTabs][256];
-// g_crc_nib[i][n][c]: nibble n at position i times x^(8*32*(31-c)) (c < 32, lanes)
-// and x^(8*1024*(7-(c-32))) (c = 32..39, warps) mod P
-__device__ uint32_t g_crc_nib[8][16][40];
+// g_crc_nib[s][i][n]: nibble n at position i times the shift of combine level s
+// (x^(8m) mod P with m = 32 * 2^s bytes for s < 5: lanes of a warp; m = 1024 *
+// 2^(s-5) for s = 5..7: warps of the tile)
+__device__ uint32_t g_crc_nib[8][8][16];
 
 // 8 levels (16 stream bytes, odd bytes 0) through the CRC register
 __device__ __forceinline__ uint32_t crc_block8(const uint32_t* T, uint32_t r, uint32_t l03,
@@ -140,18 +141,32 @@ __device__ __forceinline__ uint32_t crc_block8(const uint32_t* T, uint32_t r, ui
            T[3 * 256 + (l47 & 0xff)] ^ T[2 * 256 + ((l47 >> 8) & 0xff)] ^
            T[1 * 256 + ((l47 >> 16) & 0xff)] ^ T[0 * 256 + (l47 >> 24)];
 }
-// v * (constant c) mod P from the nibble tables (conflict-free: column = lane)
-__device__ __forceinline__ uint32_t crc_mul_nib(const uint32_t* N, uint32_t v, int c) {
+// v * (shift of combine level s) mod P from the nibble tables (16 consecutive words
+// per nibble position: conflict-free)
+__device__ __forceinline__ uint32_t crc_mul_nib(const uint32_t* N, uint32_t v, int s) {
     uint32_t r = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) r ^= N[(i * 16 + ((v >> (4 * i)) & 15u)) * 40 + c];
+    for (int i = 0; i < 8; ++i) r ^= N[(s * 8 + i) * 16 + ((v >> (4 * i)) & 15u)];
     return r;
+}
+
+// Binary-tree combine of per-lane chunk CRCs (each a zero-register CRC ending at
+// its chunk end) over `levels` levels starting at level s0: the left half of
+// every pair moves past the right half.  Lane 0 returns the combined value.
+__device__ __forceinline__ uint32_t crc_tree(const uint32_t* N, uint32_t v, int s0, int levels) {
+    const int lane = threadIdx.x & 31;
+    for (int l = 0; l < levels; ++l) {
+        const uint32_t o = __shfl_down_sync(0xffffffffu, v, 1 << l);
+        const uint32_t m = crc_mul_nib(N, v, s0 + l) ^ o;
+        if (((lane >> l) & 1) == 0) v = m;
+    }
+    return v;
 }
 
 struct E1Smem {
     uint32_t* freq;   // B*NS, per tensor
     uint32_t* crc;    // kCrcTabs*256
-    uint32_t* nib;    // 8*16*40
+    uint32_t* nib;    // 8*8*16
     uint32_t* wcnt;   // 8*B: per-warp key counts -> per-warp key bases
     uint16_t* cc;     // 8*kChunks*B: per-chunk key counts -> prefix over chunks
     uint32_t* part;   // 8 warp CRCs
@@ -163,7 +178,7 @@ struct E1Smem {
 
 __host__ __device__ inline size_t e1_smem_bytes(uint32_t B, uint32_t NS) {
     return (((size_t)B * NS * 4 + 15) & ~(size_t)15) + (size_t)kCrcTabs * 256 * 4 +
-           (size_t)8 * 16 * 40 * 4 + (((size_t)8 * B * 4 + 15) & ~(size_t)15) +
+           (size_t)8 * 8 * 16 * 4 + (((size_t)8 * B * 4 + 15) & ~(size_t)15) +
            (((size_t)8 * kChunks * B * 2 + 15) & ~(size_t)15) + 32 + kTile / 8 +
            (2 * (size_t)kTile + 16) + (kTile + 32);
 }
@@ -173,7 +188,7 @@ __device__ inline E1Smem e1_carve(uint8_t* base, uint32_t B, uint32_t NS) {
     size_t o = 0;
     S.freq = (uint32_t*)(base + o); o += ((size_t)B * NS * 4 + 15) & ~(size_t)15;
     S.crc = (uint32_t*)(base + o);  o += (size_t)kCrcTabs * 256 * 4;
-    S.nib = (uint32_t*)(base + o);  o += (size_t)8 * 16 * 40 * 4;
+    S.nib = (uint32_t*)(base + o);  o += (size_t)8 * 8 * 16 * 4;
     S.wcnt = (uint32_t*)(base + o); o += ((size_t)8 * B * 4 + 15) & ~(size_t)15;
     S.cc = (uint16_t*)(base + o);   o += ((size_t)8 * kChunks * B * 2 + 15) & ~(size_t)15;
     S.part = (uint32_t*)(base + o); o += 32;
@@ -194,7 +209,7 @@ __device__ __forceinline__ uint32_t keep_mask(int keep) {  // low `keep` bytes
 }
 
 template <bool HAS_BASE>
-__global__ void __launch_bounds__(kCB, 3) enc_tile_kernel(EncArgs A) {
+__global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
     extern __shared__ __align__(16) uint8_t e1_dyn[];
     const uint32_t B = A.B, NS = A.NS;
     const E1Smem S = e1_carve(e1_dyn, B, NS);
@@ -205,7 +220,7 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_kernel(EncArgs A) {
     const uint32_t Brep = B * 0x01010101u;
 
     for (uint32_t i = tid; i < kCrcTabs * 256; i += kCB) S.crc[i] = (&g_crc_slice[0][0])[i];
-    for (uint32_t i = tid; i < 8 * 16 * 40; i += kCB) S.nib[i] = (&g_crc_nib[0][0][0])[i];
+    for (uint32_t i = tid; i < 8 * 8 * 16; i += kCB) S.nib[i] = (&g_crc_nib[0][0][0])[i];
     for (uint32_t i = tid; i < B * NS; i += kCB) S.freq[i] = 0;
     if (tid < 16) S.sd[tid - 16] = 0;
     __shared__ int s_base;
@@ -314,9 +329,8 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_kernel(EncArgs A) {
             uint32_t r = 0;
             if (nv) r = crc_block8(S.crc, crc_block8(S.crc, 0u, c0, c1), c2, c3);
             if (cnt == kTile) {
-                r = crc_mul_nib(S.nib, r, lane);  // to the end of the warp's 1 KiB
-                r = warp_xor(r);
-                if (lane == 0) S.part[wid] = crc_mul_nib(S.nib, r, 32 + wid);  // to the tile end
+                r = crc_tree(S.nib, r, 0, 5);  // lane 0: CRC of the warp's 1 KiB
+                if (lane == 0) S.part[wid] = r;
             } else {  // ragged tile: shift by the bytes after this chunk inside the tile
                 if (r) r = crc_shift(c_crc_x2n, r, 2ull * (cnt - (e0 + nv)));
                 r = warp_xor(r);
@@ -364,11 +378,11 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_kernel(EncArgs A) {
             }
             s_cnt[b] = acc;
         }
-        if (tid == kCB - 1) {  // tile CRC (moved to its stream position by crc_tiles_kernel)
-            uint32_t r = 0;
-#pragma unroll
-            for (int w = 0; w < kCB / 32; ++w) r ^= S.part[w];
-            A.tile_crc[ti] = r;
+        if (wid == kCB / 32 - 1) {  // tile CRC (moved to its stream position by crc_tiles_kernel)
+            uint32_t r = lane < kCB / 32 ? S.part[lane] : 0u;
+            if (cnt == kTile) r = crc_tree(S.nib, r, 5, 3);  // warps: 1 KiB chunks
+            else r = warp_xor(r);                              // ragged: already at the tile end
+            if (lane == 0) A.tile_crc[ti] = r;
         }
         __syncthreads();
         if (wid == 0) {
@@ -1405,12 +1419,12 @@ static void init_crc_consts() {
     static uint32_t sl[kCrcTabs][256];
     for (int i = 0; i < kCrcTabs; ++i) memcpy(sl[i], tn[pick[i]], sizeof(sl[i]));
     DQTG_CUDA(cudaMemcpyToSymbol(g_crc_slice, sl, sizeof(sl)));
-    static uint32_t nib[8][16][40];
-    for (int c = 0; c < 40; ++c) {
-        const uint32_t k = c < 32 ? crc_x2nmodp(x.t, (uint64_t)32 * (31 - c), 3)
-                                  : crc_x2nmodp(x.t, (uint64_t)1024 * (7 - (c - 32)), 3);
+    static uint32_t nib[8][8][16];
+    for (int lv = 0; lv < 8; ++lv) {
+        const uint64_t m = lv < 5 ? (uint64_t)32 << lv : (uint64_t)1024 << (lv - 5);
+        const uint32_t k = crc_x2nmodp(x.t, m, 3);
         for (int i = 0; i < 8; ++i)
-            for (uint32_t n = 0; n < 16; ++n) nib[i][n][c] = crc_multmodp(k, n << (4 * i));
+            for (uint32_t n = 0; n < 16; ++n) nib[lv][i][n] = crc_multmodp(k, n << (4 * i));
     }
     DQTG_CUDA(cudaMemcpyToSymbol(g_crc_nib, nib, sizeof(nib)));
     DQTG_CUDA(cudaMemcpyToSymbol(c_crc_x2n, x.t, sizeof(x.t)));
@@ -1555,6 +1569,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     {
         auto kfn = base ? enc_tile_kernel<true> : enc_tile_kernel<false>;
         ensure_dyn_smem((const void*)kfn, e1_smem);
+        DQTG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         int per_sm = 0;
         DQTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kCB, e1_smem));
         const int grid = std::max(1, std::min(ntiles, e.num_sms * std::max(1, per_sm)));
