@@ -110,18 +110,12 @@ dqtg_status dqtg_engine_sync(dqtg_engine* h) {
 
 uint64_t dqtg_engine_launches(const dqtg_engine* h) { return h->e.launches; }
 
-// process-wide reference point of the DQTG_TIMELINE dump (recorded at the first enable)
-static cudaEvent_t g_epoch = nullptr;
 
 dqtg_status dqtg_engine_profile(dqtg_engine* h, int enable) {
     return guard([&] {
         LOCK(&h->e);
         h->e.profiling = enable != 0;
-        if (enable && !g_epoch) {
-            h->e.activate();
-            DQTG_CUDA(cudaEventCreate(&g_epoch));
-            DQTG_CUDA(cudaEventRecord(g_epoch, h->e.stream));
-        }
+        if (enable) timeline_epoch(h->e);
     });
 }
 
@@ -131,14 +125,7 @@ dqtg_status dqtg_engine_profile_report(dqtg_engine* h, char* json, uint64_t cap)
         Engine& e = h->e;
         e.sync();
         std::vector<std::pair<std::string, std::pair<uint64_t, double>>> acc;
-        if (getenv("DQTG_TIMELINE") && !e.spans.empty()) {  // per-launch start/end (ms) on stderr
-            for (auto& s : e.spans) {
-                float a = 0.0f, b = 0.0f;
-                DQTG_CUDA(cudaEventElapsedTime(&a, g_epoch, s.a));
-                DQTG_CUDA(cudaEventElapsedTime(&b, g_epoch, s.b));
-                fprintf(stderr, "timeline %9.3f %9.3f %8.3f %p %s\n", a, b, b - a, (void*)e.stream, s.name);
-            }
-        }
+        if (getenv("DQTG_TIMELINE")) dump_timeline(e);  // per-launch start/end (ms) on stderr
         for (auto& s : e.spans) {
             float ms = 0.0f;
             DQTG_CUDA(cudaEventElapsedTime(&ms, s.a, s.b));

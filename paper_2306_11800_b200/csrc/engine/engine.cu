@@ -4,6 +4,7 @@
 #include <math.h>
 #include <string.h>
 
+#include <cstdio>
 #include <cstring>
 
 #include "engine.h"
@@ -29,8 +30,54 @@ cudaEvent_t Engine::take_event() {
     return event_pool[ev_used++];
 }
 
+cudaStream_t Engine::hi() {
+    if (!hi_stream) {
+        int lo = 0, hi_p = 0;
+        DQTG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi_p));
+        DQTG_CUDA(cudaStreamCreateWithPriority(&hi_stream, cudaStreamNonBlocking, hi_p));
+        DQTG_CUDA(cudaEventCreateWithFlags(&hi_fork, cudaEventDisableTiming));
+        DQTG_CUDA(cudaEventCreateWithFlags(&hi_join, cudaEventDisableTiming));
+    }
+    DQTG_CUDA(cudaEventRecord(hi_fork, stream));
+    DQTG_CUDA(cudaStreamWaitEvent(hi_stream, hi_fork, 0));
+    return hi_stream;
+}
+
+void Engine::hi_done() {
+    DQTG_CUDA(cudaEventRecord(hi_join, hi_stream));
+    DQTG_CUDA(cudaStreamWaitEvent(stream, hi_join, 0));
+}
+
+// ---- launch timeline (DQTG_TIMELINE): spans relative to a process-wide epoch ----
+static cudaEvent_t g_epoch = nullptr;
+static std::mutex g_epoch_mu;
+
+void timeline_epoch(Engine& e) {
+    std::lock_guard<std::mutex> g(g_epoch_mu);
+    if (g_epoch) return;
+    e.activate();
+    DQTG_CUDA(cudaEventCreate(&g_epoch));
+    DQTG_CUDA(cudaEventRecord(g_epoch, e.stream));
+}
+
+void dump_timeline(Engine& e) {
+    if (!g_epoch) return;
+    for (auto& s : e.spans) {
+        float a = 0.0f, b = 0.0f;
+        if (cudaEventElapsedTime(&a, g_epoch, s.a) != cudaSuccess) continue;
+        if (cudaEventElapsedTime(&b, g_epoch, s.b) != cudaSuccess) continue;
+        fprintf(stderr, "timeline %9.3f %9.3f %8.3f %p %s\n", a, b, b - a, (void*)e.stream, s.name);
+    }
+}
+
 Engine::~Engine() {
     cudaSetDevice(device);
+    if (hi_stream) {
+        cudaStreamSynchronize(hi_stream);
+        cudaStreamDestroy(hi_stream);
+        cudaEventDestroy(hi_fork);
+        cudaEventDestroy(hi_join);
+    }
     for (auto ev : event_pool) cudaEventDestroy(ev);
     for (auto& kv : scratch) cudaFreeAsync(kv.second.first, stream);
     cudaStreamSynchronize(stream);

@@ -125,6 +125,12 @@ struct Engine {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    // high-priority side stream for latency-critical few-CTA phases (k-means):
+    // its CTAs are scheduled ahead of other streams' streaming passes
+    cudaStream_t hi_stream = nullptr;
+    cudaEvent_t hi_fork = nullptr, hi_join = nullptr;
+    cudaStream_t hi();      // forks: hi_stream waits for `stream`
+    void hi_done();         // joins: `stream` waits for hi_stream
     std::recursive_mutex mu;
     uint64_t launches = 0;
     uint32_t* d_err = nullptr;
@@ -181,6 +187,9 @@ struct Engine {
 };
 
 bool is_device_ptr(const void* p);
+
+void timeline_epoch(Engine& e);  // DQTG_TIMELINE reference event (first call records it)
+void dump_timeline(Engine& e);   // recorded spans on stderr, relative to the epoch
 
 // Raises a kernel's dynamic shared-memory limit to at least `bytes` and never
 // lowers it: engines on several host threads launch the same kernels with

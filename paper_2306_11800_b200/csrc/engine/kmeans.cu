@@ -596,7 +596,15 @@ void run_kmeans(Engine& e, std::vector<KProblem>& probs, float* cb_out, int cb_s
     int smem_n = (int)((budget - std::min(budget, head)) / 60);  // 5 doubles + pair + int per key
     size_t smem = head + (size_t)std::min(maxn, smem_n) * 60 + 96;
     ensure_dyn_smem((const void*)kmeans_restarts_kernel, smem);
-    { DQTG_SPAN(e, "kmeans_restarts_kernel"); kmeans_restarts_kernel<<<(unsigned)(probs.size() * restarts), kKB, smem, e.stream>>>(dp, restarts, smem_n); }
+    // restarts on the engine's high-priority side stream (fork/join with events)
+    if (e.profiling) {
+        DQTG_SPAN(e, "kmeans_restarts_kernel");
+        kmeans_restarts_kernel<<<(unsigned)(probs.size() * restarts), kKB, smem, e.stream>>>(dp, restarts, smem_n);
+    } else {
+        cudaStream_t hs = e.hi();
+        kmeans_restarts_kernel<<<(unsigned)(probs.size() * restarts), kKB, smem, hs>>>(dp, restarts, smem_n);
+        e.hi_done();
+    }
     { DQTG_SPAN(e, "kmeans_select_kernel"); kmeans_select_kernel<<<(unsigned)probs.size(), 32, 0, e.stream>>>(dp, restarts, cb_out,
                                                                        cb_stride, cb_len_dev); }
     e.launched(2);

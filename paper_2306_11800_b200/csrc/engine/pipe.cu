@@ -15,6 +15,7 @@
 // a copy, the others keep the GPU fed, and the few-CTA phases (k-means restarts,
 // per-group Huffman) overlap the streaming passes of the other workers.
 #include <condition_variable>
+#include <cstdlib>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -139,6 +140,11 @@ dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* 
             e.sync();
         }
         const uint32_t nt = layout->n_tensors;
+        const bool tl = getenv("DQTG_TIMELINE") != nullptr;
+        for (auto& e : p->eng) {
+            e->profiling = tl;
+            if (tl) timeline_epoch(*e);
+        }
         Run R;
         R.states.resize(n);
         R.qev.assign(n, nullptr);
@@ -195,6 +201,13 @@ dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* 
         for (int w = 0; w < W; ++w) th.emplace_back(worker, w);
         for (auto& t : th) t.join();
         for (auto ev : R.qev) cudaEventDestroy(ev);
+        if (tl)
+            for (auto& e : p->eng) {
+                e->sync();
+                dump_timeline(*e);
+                e->spans.clear();
+                e->ev_used = 0;
+            }
         if (R.failed) throw Fail(R.code, R.msg);
         if (last_out) {
             *last_out = nullptr;
