@@ -135,6 +135,11 @@ dqtg_status dqtg_qstate_info_get(const dqtg_qstate *q, dqtg_qstate_info *info);
 dqtg_status dqtg_qstate_protected_counts(const dqtg_qstate *q, uint64_t *counts);
 /* copy out: levels[i] (numel_i u16), prot_pos[i]/prot_val[i] (count_i each), codebooks[lt]
  * (codebook_len[lt] floats).  Any pointer array may be NULL to skip that part. */
+/* layout of a state (e.g. one made by dqtg_decode_record): tensor count; per tensor
+ * its name (NUL-terminated, truncated to cap bytes), layer type, rank and dims[rank] */
+uint32_t dqtg_qstate_tensor_count(const dqtg_qstate *s);
+dqtg_status dqtg_qstate_tensor_info(const dqtg_qstate *s, uint32_t i, char *name, uint64_t cap,
+                                    uint8_t *type, uint8_t *rank, uint64_t *dims);
 dqtg_status dqtg_qstate_download(const dqtg_qstate *q, uint16_t *const *levels,
                                  uint64_t *const *prot_pos, uint16_t *const *prot_val,
                                  float *const *codebooks);

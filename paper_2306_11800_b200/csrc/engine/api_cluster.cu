@@ -68,8 +68,5 @@ void approx_kmeans(Engine& e, const float* values_any, uint64_t n, uint32_t k, d
     e.check_err();
 }
 
-std::unique_ptr<QState> decode_record(Engine&, const uint8_t*, uint64_t, const QState*) {
-    throw Fail(DQTG_ERROR, "decode_record: not implemented yet");
-}
 
 }  // namespace dqtg

@@ -433,6 +433,25 @@ dqtg_status dqtg_qstate_upload(dqtg_engine* h, const dqtg_layout* layout, uint64
 }
 
 void dqtg_qstate_destroy(dqtg_qstate* s) { delete s; }
+
+uint32_t dqtg_qstate_tensor_count(const dqtg_qstate* s) { return s->q->L->nt; }
+
+dqtg_status dqtg_qstate_tensor_info(const dqtg_qstate* s, uint32_t i, char* name, uint64_t cap,
+                                    uint8_t* type, uint8_t* rank, uint64_t* dims) {
+    return guard([&] {
+        const Layout& L = *s->q->L;
+        DQTG_REQUIRE(i < L.nt, DQTG_ERROR, "tensor index out of range");
+        if (name && cap) {
+            const size_t k = std::min<size_t>(L.names[i].size(), cap - 1);
+            memcpy(name, L.names[i].data(), k);
+            name[k] = 0;
+        }
+        if (type) *type = L.types[i];
+        if (rank) *rank = L.ranks[i];
+        if (dims)
+            for (size_t r = 0; r < L.dims[i].size(); ++r) dims[r] = L.dims[i][r];
+    });
+}
 uint16_t* dqtg_qstate_levels_dev(dqtg_qstate* s) { return s->q->d_levels; }
 
 dqtg_status dqtg_dequantize(dqtg_engine* h, const dqtg_qstate* s, float* const* out) {

@@ -488,6 +488,63 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
     }
 }
 
+// CRC of one tile of a level array (zero register, ending at the tile's last byte),
+// 16 levels per thread (levels must be < 256: validated by the caller).
+__global__ void __launch_bounds__(kCB) level_crc_tile_kernel(const Tile* tiles, const uint16_t* levels,
+                                                             uint32_t* tile_crc) {
+    __shared__ uint32_t s_crc[kCrcTabs * 256];
+    __shared__ uint32_t s_nib[8 * 8 * 16];
+    __shared__ uint32_t s_part[kCB / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (uint32_t i = tid; i < kCrcTabs * 256; i += kCB) s_crc[i] = (&g_crc_slice[0][0])[i];
+    for (uint32_t i = tid; i < 8 * 8 * 16; i += kCB) s_nib[i] = (&g_crc_nib[0][0][0])[i];
+    __syncthreads();
+    const Tile T = tiles[blockIdx.x];
+    const uint32_t cnt = T.count, e0 = tid * kIt;
+    const uint32_t nv = e0 < cnt ? min(cnt - e0, (uint32_t)kIt) : 0u;
+    uint32_t cw[4] = {0, 0, 0, 0};
+    if (nv) {
+        const uint4* cp = (const uint4*)(levels + T.start + e0);
+        const uint4 a0 = cp[0], a1 = cp[1];
+        cw[0] = __byte_perm(a0.x, a0.y, 0x6420);
+        cw[1] = __byte_perm(a0.z, a0.w, 0x6420);
+        cw[2] = __byte_perm(a1.x, a1.y, 0x6420);
+        cw[3] = __byte_perm(a1.z, a1.w, 0x6420);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cw[j] &= keep_mask((int)nv - 4 * j);
+    }
+    uint32_t c0 = cw[0], c1 = cw[1], c2 = cw[2], c3 = cw[3];
+    if (nv && nv < (uint32_t)kIt) {  // right-align the tail chunk (leading zeros are neutral)
+        const int sh = kIt - (int)nv;
+        uint32_t w[8] = {0, 0, 0, 0, cw[0], cw[1], cw[2], cw[3]};
+        uint32_t o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int src = 4 + j - (sh >> 2);
+            const uint32_t lo_w = src - 1 >= 0 ? w[src - 1] : 0u;
+            o[j] = (sh & 3) ? __funnelshift_l(lo_w, w[src], 8 * (sh & 3)) : w[src];
+        }
+        c0 = o[0], c1 = o[1], c2 = o[2], c3 = o[3];
+    }
+    uint32_t r = 0;
+    if (nv) r = crc_block8(s_crc, crc_block8(s_crc, 0u, c0, c1), c2, c3);
+    if (cnt == kTile) {
+        r = crc_tree(s_nib, r, 0, 5);
+        if (lane == 0) s_part[wid] = r;
+    } else {
+        if (r) r = crc_shift(c_crc_x2n, r, 2ull * (cnt - (e0 + nv)));
+        r = warp_xor(r);
+        if (lane == 0) s_part[wid] = r;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t v = lane < kCB / 32 ? s_part[lane] : 0u;
+        if (cnt == kTile) v = crc_tree(s_nib, v, 5, 3);
+        else v = warp_xor(v);
+        if (lane == 0) tile_crc[blockIdx.x] = v;
+    }
+}
+
 // Tile CRCs (each ending at its tile's last byte) moved to the end of the level
 // stream and XOR-combined (crc32 linearity, crc.cuh).
 __global__ void __launch_bounds__(256) crc_tiles_kernel(const uint32_t* tile_crc,
@@ -1763,6 +1820,37 @@ uint32_t crc32_device(Engine& e, const uint8_t* data, uint64_t n) {
     e.launched(2);
     uint32_t h = 0;
     e.d2h(&h, out, 4);
+    e.sync();
+    return h;
+}
+
+
+static void ensure_crc_shift(Engine& e, const Layout& L) {
+    if (L.d_crc_shift || L.tiles.empty()) return;
+    Layout& ML = const_cast<Layout&>(L);
+    const int ntiles = (int)L.tiles.size();
+    DQTG_CUDA(cudaMalloc(&ML.d_crc_shift, (size_t)ntiles * 4 + 4));
+    { DQTG_SPAN(e, "crc_tile_shift_kernel"); crc_tile_shift_kernel<<<(ntiles + 255) / 256, 256, 0, e.stream>>>(L.d_tiles, ntiles, L.d_off, L.d_stream_off, L.N, ML.d_crc_shift); }
+    e.launched();
+}
+
+uint32_t level_stream_crc(Engine& e, const Layout& L, const uint16_t* levels) {
+    init_crc_consts();
+    cudaStream_t st = e.stream;
+    const int ntiles = (int)L.tiles.size();
+    auto* acc = (uint32_t*)e.buf("crc.acc", 16);
+    DQTG_CUDA(cudaMemsetAsync(acc, 0, 4, st));
+    if (ntiles) {
+        ensure_crc_shift(e, L);
+        auto* tc = (uint32_t*)e.buf("crc.tiles", (size_t)ntiles * 4 + 4);
+        { DQTG_SPAN(e, "level_crc_tile_kernel"); level_crc_tile_kernel<<<ntiles, kCB, 0, st>>>(L.d_tiles, levels, tc); }
+        { DQTG_SPAN(e, "crc_tiles_kernel"); crc_tiles_kernel<<<std::max(1, std::min(e.num_sms * 2, (ntiles + 255) / 256)), 256, 0, st>>>(tc, L.d_crc_shift, ntiles, acc); }
+        e.launched(2);
+    }
+    { DQTG_SPAN(e, "finish_crc_kernel"); finish_crc_kernel<<<1, 1, 0, st>>>(acc, 2 * L.N, nullptr, acc + 1); }
+    e.launched();
+    uint32_t h = 0;
+    e.d2h(&h, acc + 1, 4);
     e.sync();
     return h;
 }

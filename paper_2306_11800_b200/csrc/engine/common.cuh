@@ -43,6 +43,7 @@ enum DevErr : uint32_t {
     kErrHuffmanDepth = 1u << 2,
     kErrNonFinite = 1u << 3,
     kErrKmeansWeights = 1u << 4,
+    kErrCorruptBitstream = 1u << 5,
 };
 
 inline uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }

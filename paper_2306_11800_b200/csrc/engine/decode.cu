@@ -1,0 +1,727 @@
+// decode_delta_record on the device (reference codec.cpp:459-597, DQDR v1 layout in
+// SURVEY.md Appendix B).
+//
+//   host   walk the record structure: header, codebooks, per tensor the static
+//          prefix, protected entries and the (bucket, elems, nsyms, table, bytes)
+//          header of every group; canonical decode limits per group
+//   H1     every group's bitstream is cut into 4096-bit chunks, one thread per
+//          chunk.  Threads start decoding at their chunk's nominal start; a chunk's
+//          true start is the first codeword boundary the previous chunk's decode
+//          reaches at or past it.  Canonical Huffman codes self-synchronise within
+//          a few codewords, so a handful of passes (each re-decoding only chunks
+//          whose start moved) converge; symbols per chunk -> scan -> symbol index
+//   H2     decode again, writing symbols (-v run values, run lengths) in order
+//   R      RLE expansion (codec.cpp:91-107): symbols -> element counts -> scan ->
+//          run heads marked, max-scan fills every element with its run's value
+//   U      unrearrange (codec.cpp:56-77): stable rank of every element among the
+//          elements with the same previous level (per-tile match ranks + per-key
+//          prefixes over tiles) indexes its group's delta; cur = (prev - d) mod B
+//   C      CRC-32 of the decoded level stream against the stored one
+#include <cub/device/device_scan.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+
+namespace dqtg {
+
+constexpr uint32_t kChunkBits = 4096;
+constexpr int kMaxCodeLen = 64;
+
+struct GroupDesc {
+    uint64_t elem_off;  // dense rearranged position of the group's first element
+    uint64_t elems;
+    uint64_t nsyms;
+    uint64_t sym_off;   // first symbol in the symbol array
+    uint64_t bit_off;   // absolute bit offset of the stream in the device record
+    uint64_t nbits;
+    uint32_t tab_off, tsize;
+    uint32_t chunk0, nchunks;
+    uint32_t minlen, maxlen;
+    uint32_t lim_off;   // decode tables (kMaxCodeLen + 1 entries per group)
+    uint32_t pad;
+};
+
+struct ChunkDesc {
+    uint32_t group;
+    uint32_t local;  // chunk index inside its group
+};
+
+// ---- bit access: MSB-first stream (codec.cpp:111-122) -------------------------
+__device__ __forceinline__ uint64_t bswap64(uint64_t x) {
+    const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+    return ((uint64_t)__byte_perm(lo, 0, 0x0123) << 32) | __byte_perm(hi, 0, 0x0123);
+}
+// 64 bits starting at absolute bit position p (record padded by 16 zero bytes)
+__device__ __forceinline__ uint64_t peek64(const uint64_t* rec64, uint64_t p) {
+    const uint64_t w = p >> 6;
+    const uint32_t s = (uint32_t)(p & 63);
+    const uint64_t a = bswap64(__ldg(rec64 + w)), b = bswap64(__ldg(rec64 + w + 1));
+    return s ? (a << s) | (b >> (64 - s)) : a;
+}
+
+struct DecTabs {
+    const uint64_t* lim;    // left-aligned exclusive limit of codes of length <= L
+    const uint64_t* first;  // canonical first code of length L
+    const uint32_t* base;   // table index of the first symbol of length L
+    const int64_t* syms;
+};
+
+// Decodes the codeword at bit p (relative to the group stream); returns its length
+// and the table index, or length 0 for an invalid code.
+__device__ __forceinline__ uint32_t decode_one(const uint64_t* rec64, const GroupDesc& G,
+                                               const DecTabs& T, uint64_t p, uint32_t& idx) {
+    const uint64_t x = peek64(rec64, G.bit_off + p);
+    const uint64_t* lim = T.lim + G.lim_off;
+    uint32_t L = G.minlen;
+    while (L <= G.maxlen && x >= lim[L]) ++L;
+    if (L > G.maxlen) return 0;
+    const uint64_t code = x >> (64 - L);
+    idx = T.base[G.lim_off + L] + (uint32_t)(code - T.first[G.lim_off + L]);
+    return L;
+}
+
+// H1: decode chunk c from start[c] to its nominal end (dirty chunks only)
+__global__ void __launch_bounds__(256) huff_sync_kernel(const uint64_t* rec64, const GroupDesc* groups,
+                                                        const ChunkDesc* chunks, uint32_t nchunks,
+                                                        DecTabs T, const uint64_t* start,
+                                                        uint64_t* out_pos, uint32_t* count,
+                                                        const uint8_t* dirty) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nchunks || !dirty[c]) return;
+    const ChunkDesc C = chunks[c];
+    const GroupDesc G = groups[C.group];
+    const uint64_t end = min((uint64_t)(C.local + 1) * kChunkBits, G.nbits);
+    uint64_t p = start[c];
+    uint32_t n = 0;
+    while (p < end) {
+        uint32_t idx;
+        const uint32_t L = decode_one(rec64, G, T, p, idx);
+        p += L ? L : 1;  // invalid code: resynchronise (corrupt streams fail in H2)
+        ++n;
+    }
+    out_pos[c] = p;
+    count[c] = n;
+}
+
+// H1 update: a chunk's start is where the previous chunk's decode ended
+__global__ void huff_update_kernel(const ChunkDesc* chunks, uint32_t nchunks, uint64_t* start,
+                                   const uint64_t* out_pos, uint8_t* dirty, uint32_t* any) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nchunks) return;
+    uint8_t d = 0;
+    if (chunks[c].local > 0) {
+        const uint64_t s = out_pos[c - 1];
+        if (s != start[c]) {
+            start[c] = s;
+            d = 1;
+        }
+    }
+    dirty[c] = d;
+    if (d) *any = 1;
+}
+
+// H2: decode again, writing symbols at their index inside the group
+__global__ void __launch_bounds__(256) huff_write_kernel(const uint64_t* rec64, const GroupDesc* groups,
+                                                         const ChunkDesc* chunks, uint32_t nchunks,
+                                                         DecTabs T, const uint64_t* start,
+                                                         const unsigned long long* sym_scan,
+                                                         int32_t* syms, uint32_t* err) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nchunks) return;
+    const ChunkDesc C = chunks[c];
+    const GroupDesc G = groups[C.group];
+    const uint64_t end = min((uint64_t)(C.local + 1) * kChunkBits, G.nbits);
+    uint64_t k = sym_scan[c] - sym_scan[G.chunk0];
+    uint64_t p = start[c];
+    while (p < end && k < G.nsyms) {
+        uint32_t idx;
+        const uint32_t L = decode_one(rec64, G, T, p, idx);
+        if (!L || idx >= G.tsize) {
+            atomicOr(err, kErrCorruptBitstream);
+            return;
+        }
+        syms[G.sym_off + k] = (int32_t)T.syms[G.tab_off + idx];
+        p += L;
+        ++k;
+    }
+}
+
+// per group: the chunks' symbol total must cover nsyms (codec.cpp:250 overrun)
+__global__ void huff_check_kernel(const GroupDesc* groups, uint32_t ngroups,
+                                  const unsigned long long* sym_scan, uint32_t* err) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= ngroups) return;
+    const GroupDesc G = groups[g];
+    if (!G.nsyms) return;
+    const uint64_t got = sym_scan[G.chunk0 + G.nchunks] - sym_scan[G.chunk0];
+    if (got < G.nsyms) atomicOr(err, kErrCorruptBitstream);
+}
+
+// R1: elements produced by every symbol; run lengths need a preceding value
+// (codec.cpp:91-107).  flags: bit0 first symbol of its group, bit1 last.
+__global__ void rle_count_kernel(const int32_t* syms, const uint8_t* sflags, uint64_t n,
+                                 unsigned long long* cnt, uint32_t err_bits, uint32_t* err) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        const int32_t v = syms[s];
+        const uint8_t f = sflags[s];
+        unsigned long long c = 0;
+        if (v > 0) {
+            if ((f & 1) || syms[s - 1] > 0) atomicOr(err, err_bits);  // length without value
+        } else {
+            c = 1;
+            if (!(f & 2) && syms[s + 1] > 0) c = (unsigned long long)syms[s + 1];
+        }
+        cnt[s] = c;
+    }
+}
+
+// per group: the runs must produce exactly `elems` elements
+__global__ void rle_total_kernel(const GroupDesc* groups, uint32_t ngroups,
+                                 const unsigned long long* off, const unsigned long long* cnt,
+                                 uint32_t* err) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= ngroups) return;
+    const GroupDesc G = groups[g];
+    if (!G.nsyms) {
+        if (G.elems) atomicOr(err, kErrCorruptBitstream);
+        return;
+    }
+    const uint64_t last = G.sym_off + G.nsyms - 1;
+    const uint64_t total = off[last] + cnt[last] - off[G.sym_off];
+    if (total != G.elems || off[G.sym_off] != G.elem_off) atomicOr(err, kErrCorruptBitstream);
+}
+
+// R2: mark run heads with their symbol index + 1
+__global__ void rle_heads_kernel(const int32_t* syms, uint64_t n, const unsigned long long* off,
+                                 const unsigned long long* cnt, uint32_t* head, uint64_t ntot) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n;
+         s += (uint64_t)gridDim.x * blockDim.x)
+        if (cnt[s] && off[s] < ntot) head[off[s]] = (uint32_t)(s + 1);
+}
+
+struct Widen {
+    __device__ __forceinline__ unsigned long long operator()(uint32_t x) const { return x; }
+};
+
+struct MaxOp {
+    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
+};
+
+// R3: element -> its run's value (delta), as a byte
+__global__ void rle_fill_kernel(const uint32_t* sidx, uint64_t ntot, const int32_t* syms, uint32_t B,
+                                uint8_t* d, uint32_t* err) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < ntot;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = sidx[j];
+        uint32_t v = 0;
+        if (!s) {
+            atomicOr(err, kErrCorruptBitstream);
+        } else {
+            const int32_t x = syms[s - 1];
+            if (x > 0 || -x >= (int32_t)B) atomicOr(err, kErrCorruptIndex);
+            else v = (uint32_t)(-x);
+        }
+        d[j] = (uint8_t)v;
+    }
+}
+
+// ---- U: unrearrange ------------------------------------------------------------
+// U1: per tile, count of elements per previous level
+__global__ void __launch_bounds__(256) prev_count_kernel(const Tile* tiles, const uint16_t* prev,
+                                                         uint32_t B, uint32_t* tile_cnt, uint32_t* err) {
+    __shared__ uint32_t s_c[64];
+    const Tile T = tiles[blockIdx.x];
+    for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) s_c[b] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < T.count; i += blockDim.x) {
+        const uint32_t p = prev ? prev[T.start + i] : 0u;
+        if (p >= B) atomicOr(err, kErrCorruptIndex);
+        else atomicAdd(&s_c[p], 1u);
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) tile_cnt[(size_t)blockIdx.x * B + b] = s_c[b];
+}
+
+// U2: per (tensor, key): exclusive prefix of the tile counts over the tensor's
+// tiles; per tensor the keys' group starts; record group sizes must match
+__global__ void prev_scan_kernel(const uint32_t* tile0, uint32_t nt, uint32_t B, uint32_t* tile_cnt,
+                                 const unsigned long long* rec_elems /*[nt][B]*/,
+                                 unsigned long long* gstart /*[nt][B]*/, uint32_t* err) {
+    const uint32_t t = blockIdx.x;
+    if (t >= nt) return;
+    __shared__ unsigned long long s_tot[64];
+    for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) {
+        unsigned long long acc = 0;
+        for (uint32_t ti = tile0[t]; ti < tile0[t + 1]; ++ti) {
+            const uint32_t c = tile_cnt[(size_t)ti * B + b];
+            tile_cnt[(size_t)ti * B + b] = (uint32_t)acc;
+            acc += c;
+        }
+        s_tot[b] = acc;
+        if (acc != rec_elems[(size_t)t * B + b]) atomicOr(err, kErrCorruptIndex);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long acc = 0;
+        for (uint32_t b = 0; b < B; ++b) {
+            gstart[(size_t)t * B + b] = acc;
+            acc += s_tot[b];
+        }
+    }
+}
+
+// U3: per tile, stable rank of every element among equal previous levels (warp
+// ranges of 512 elements, 32-element chunks matched on the key), delta gathered
+// from the element's rearranged position, cur = (prev - d) mod B, range checks
+__global__ void __launch_bounds__(256) unrearrange_kernel(const Tile* tiles, const uint8_t* types,
+                                                          const uint64_t* stream_off,
+                                                          const uint64_t* off, const uint16_t* prev,
+                                                          uint32_t B, const uint32_t* tile_base,
+                                                          const unsigned long long* gstart,
+                                                          const uint8_t* d, const uint32_t* cb_len,
+                                                          uint16_t* cur, uint32_t* err) {
+    __shared__ uint32_t s_wc[8][64];  // per-warp key counts -> per-warp key bases
+    __shared__ uint32_t s_base[64];
+    const Tile T = tiles[blockIdx.x];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (int i = tid; i < 8 * 64; i += 256) (&s_wc[0][0])[i] = 0;
+    __syncthreads();
+    uint32_t rk[16], ky[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const uint32_t e = wid * 512 + j * 32 + lane;
+        const bool valid = e < T.count;
+        uint32_t key = valid ? (prev ? prev[T.start + e] : 0u) : 0xffffu;
+        if (key >= B && valid) key = 0;  // flagged in U1
+        const uint32_t peers = __match_any_sync(0xffffffffu, key);
+        const int leader = __ffs(peers) - 1;
+        uint32_t old = 0;
+        if (lane == leader && valid) {
+            old = s_wc[wid][key];
+            s_wc[wid][key] = old + __popc(peers);
+        }
+        __syncwarp();
+        old = __shfl_sync(0xffffffffu, old, leader);
+        rk[j] = old + __popc(peers & lt_mask);
+        ky[j] = key;
+    }
+    __syncthreads();
+    const uint32_t t = T.tensor;
+    for (uint32_t b = tid; b < B; b += 256) {
+        uint32_t acc = 0;
+        for (int w = 0; w < 8; ++w) {
+            const uint32_t c = s_wc[w][b];
+            s_wc[w][b] = acc;
+            acc += c;
+        }
+        s_base[b] = (uint32_t)gstart[(size_t)t * B + b] + tile_base[(size_t)blockIdx.x * B + b];
+    }
+    __syncthreads();
+    const uint64_t so = stream_off[t];
+    const uint32_t maxl = cb_len[types[t]] + 1;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const uint32_t e = wid * 512 + j * 32 + lane;
+        if (e >= T.count) continue;
+        const uint32_t key = ky[j];
+        const uint64_t pos = (uint64_t)s_base[key] + s_wc[wid][key] + rk[j];
+        const uint32_t dv = d[so + pos];
+        const uint32_t c = key >= dv ? key - dv : key + B - dv;
+        if (c > maxl) atomicOr(err, kErrCorruptIndex);
+        cur[T.start + e] = (uint16_t)c;
+    }
+}
+
+// ---- host ----------------------------------------------------------------------
+namespace {
+
+struct Rd {
+    const uint8_t* p;
+    uint64_t n, at = 0;
+    void need(uint64_t k) const {
+        if (n - at < k) throw Fail(DQTG_TRUNCATED, "DQDR record truncated");
+    }
+    uint8_t u8() {
+        need(1);
+        return p[at++];
+    }
+    template <typename T>
+    T le() {
+        need(sizeof(T));
+        T v = 0;
+        for (size_t i = 0; i < sizeof(T); ++i) v |= (T)p[at + i] << (8 * i);
+        at += sizeof(T);
+        return v;
+    }
+    double f64() {
+        uint64_t u = le<uint64_t>();
+        double d;
+        memcpy(&d, &u, 8);
+        return d;
+    }
+    float f32() {
+        uint32_t u = le<uint32_t>();
+        float f;
+        memcpy(&f, &u, 4);
+        return f;
+    }
+    uint64_t uv() {  // LEB128 (bytes.hpp:36-41)
+        uint64_t v = 0;
+        for (int sh = 0;; sh += 7) {
+            const uint8_t b = u8();
+            if (sh >= 64) throw Fail(DQTG_CORRUPT_BITSTREAM, "varint overflow");
+            v |= (uint64_t)(b & 0x7f) << sh;
+            if (!(b & 0x80)) return v;
+        }
+    }
+    int64_t sv() {  // zig-zag (bytes.hpp:43-47)
+        const uint64_t u = uv();
+        return (int64_t)(u >> 1) ^ -(int64_t)(u & 1);
+    }
+    std::string str() {
+        const uint16_t len = le<uint16_t>();
+        need(len);
+        std::string s((const char*)p + at, len);
+        at += len;
+        return s;
+    }
+};
+
+}  // namespace
+
+std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n, const QState* base) {
+    cudaStream_t st = e.stream;
+    // the record may live in device memory: decode from a host copy of its structure
+    std::vector<uint8_t> host_copy;
+    const uint8_t* h = rec;
+    if (is_device_ptr(rec)) {
+        host_copy.resize(n);
+        e.from_device(host_copy.data(), rec, n);
+        e.sync();
+        h = host_copy.data();
+    }
+    Rd r{h, n};
+    {
+        r.need(4);
+        if (memcmp(h, "DQDR", 4) != 0) throw Fail(DQTG_BAD_MAGIC, "not a DQDR record");
+        r.at = 4;
+        const uint32_t v = r.le<uint32_t>();
+        if (v != 1) throw Fail(DQTG_IO, "unsupported DQDR version " + std::to_string(v));
+    }
+    const bool has_base = r.u8() != 0;
+    const uint64_t base_step = r.le<uint64_t>(), target_step = r.le<uint64_t>();
+    const uint32_t B = r.le<uint32_t>();
+    if (has_base && !base) throw Fail(DQTG_CHAIN_CORRUPT, "delta record requires its base state");
+    if (!has_base) base = nullptr;
+    if (base && base->step != base_step)
+        throw Fail(DQTG_CHAIN_CORRUPT, "base step mismatch: record expects " +
+                                           std::to_string(base_step) + ", got " +
+                                           std::to_string(base->step));
+    DQTG_REQUIRE(B >= 1 && B <= 64, DQTG_CORRUPT_INDEX, "cyclic alphabet outside the device decoder's range");
+    auto q = std::make_unique<QState>();
+    q->eng = &e;
+    q->step = target_step;
+    dqtg_config& cfg = q->cfg;
+    cfg.bins = r.le<uint32_t>();
+    cfg.embed_bins = r.le<uint32_t>();
+    cfg.prune_frac = r.f64();
+    cfg.protect_frac = r.f64();
+    cfg.metric = r.u8();
+    cfg.sigma = r.f64();
+    cfg.alpha = r.f64();
+    r.f64();  // quality
+    const uint8_t nlt = r.u8();
+    for (uint8_t i = 0; i < nlt; ++i) {
+        const uint8_t lt = r.u8();
+        if (lt >= kLayerTypes) throw Fail(DQTG_CORRUPT_INDEX, "bad codebook layer type");
+        const uint32_t len = r.le<uint32_t>();
+        r.need((uint64_t)len * 4);
+        q->cb[lt].resize(len);
+        for (auto& v : q->cb[lt]) v = r.f32();
+        q->cb_len[lt] = len;
+    }
+    const uint32_t nt = r.le<uint32_t>();
+    if (base && base->L->nt != nt) throw Fail(DQTG_CHAIN_CORRUPT, "base tensor count mismatch");
+    // tensors
+    std::vector<std::string> names(nt);
+    std::vector<uint8_t> types(nt), ranks(nt);
+    std::vector<uint64_t> dims;
+    std::vector<std::vector<uint64_t>> ppos(nt);
+    std::vector<std::vector<uint16_t>> pval(nt);
+    std::vector<GroupDesc> groups;
+    std::vector<ChunkDesc> chunks;
+    std::vector<int64_t> tab_sym;
+    std::vector<uint8_t> tab_len;
+    std::vector<unsigned long long> rec_elems((size_t)nt * B, 0);
+    std::vector<uint64_t> lim, first;
+    std::vector<uint32_t> lbase;
+    uint64_t stream_pos = 0, sym_total = 0;
+    for (uint32_t i = 0; i < nt; ++i) {
+        names[i] = r.str();
+        types[i] = r.u8();
+        if (types[i] >= kLayerTypes) throw Fail(DQTG_CORRUPT_INDEX, "bad tensor layer type");
+        ranks[i] = r.u8();
+        uint64_t numel = 1;
+        for (uint8_t k = 0; k < ranks[i]; ++k) {
+            dims.push_back(r.le<uint64_t>());
+            numel *= dims.back();
+        }
+        const uint64_t np = r.uv();
+        if (np > numel) throw Fail(DQTG_CORRUPT_INDEX, "too many protected entries in " + names[i]);
+        ppos[i].resize(np);
+        pval[i].resize(np);
+        uint64_t pos = 0;
+        for (uint64_t k = 0; k < np; ++k) {
+            const uint64_t dd = r.uv();
+            pos = k == 0 ? dd : pos + dd;
+            if (pos >= numel || (k > 0 && dd == 0))
+                throw Fail(DQTG_CORRUPT_INDEX, "protected positions not ascending in " + names[i]);
+            ppos[i][k] = pos;
+            pval[i][k] = r.le<uint16_t>();
+        }
+        if (base) {
+            const Layout& BL = *base->L;
+            if (BL.names[i] != names[i] || BL.types[i] != types[i] || BL.ranks[i] != ranks[i] ||
+                !std::equal(BL.dims[i].begin(), BL.dims[i].end(), dims.end() - ranks[i]))
+                throw Fail(DQTG_CHAIN_CORRUPT, "base tensor layout mismatch at " + names[i]);
+        }
+        // groups of the payload (codec.cpp:283-300)
+        const uint64_t ng = r.uv();
+        uint64_t total = 0;
+        int64_t last_bucket = -1;
+        for (uint64_t k = 0; k < ng; ++k) {
+            GroupDesc G{};
+            const uint64_t bucket = r.uv();
+            G.elems = r.uv();
+            G.nsyms = r.uv();
+            const uint64_t tsize = r.uv();
+            if (bucket >= B || (int64_t)bucket <= last_bucket)
+                throw Fail(DQTG_CORRUPT_INDEX, "group bucket out of order in " + names[i]);
+            last_bucket = (int64_t)bucket;
+            if (tsize > (1u << 24)) throw Fail(DQTG_CORRUPT_BITSTREAM, "huffman table too large");
+            G.tab_off = (uint32_t)tab_sym.size();
+            G.tsize = (uint32_t)tsize;
+            for (uint64_t j = 0; j < tsize; ++j) {
+                const int64_t s = r.sv();
+                const uint8_t l = r.u8();
+                if (l == 0 || l > kMaxCodeLen - 1) throw Fail(DQTG_CORRUPT_BITSTREAM, "invalid code length");
+                if (s > INT32_MAX || s < -(int64_t)0xffff)
+                    throw Fail(DQTG_CORRUPT_BITSTREAM, "run value out of range");
+                if (j && (l < tab_len.back() || (l == tab_len.back() && s <= tab_sym.back())))
+                    throw Fail(DQTG_CORRUPT_BITSTREAM, "huffman table not canonical");
+                tab_sym.push_back(s);
+                tab_len.push_back(l);
+            }
+            const uint64_t nb = r.uv();
+            r.need(nb);
+            G.bit_off = r.at * 8;
+            G.nbits = nb * 8;
+            r.at += nb;
+            if (G.nsyms && !tsize) throw Fail(DQTG_CORRUPT_BITSTREAM, "empty huffman table");
+            // canonical decode limits (codec.cpp:137-214 assign_codes)
+            G.lim_off = (uint32_t)lim.size();
+            lim.resize(lim.size() + kMaxCodeLen + 1, ~0ull);
+            first.resize(first.size() + kMaxCodeLen + 1, 0);
+            lbase.resize(lbase.size() + kMaxCodeLen + 1, 0);
+            if (tsize) {
+                G.minlen = tab_len[G.tab_off];
+                G.maxlen = tab_len[G.tab_off + tsize - 1];
+                uint64_t code = 0;
+                uint32_t j = 0, prev_len = G.minlen;
+                for (uint32_t L = G.minlen; L <= G.maxlen; ++L) {
+                    if (L > prev_len) code <<= (L - prev_len);
+                    prev_len = L;
+                    first[G.lim_off + L] = code;
+                    lbase[G.lim_off + L] = j;
+                    uint32_t cntL = 0;
+                    while (j < tsize && tab_len[G.tab_off + j] == L) ++j, ++cntL;
+                    code += cntL;
+                    if (L < 64 && (code >> L) > 1) throw Fail(DQTG_CORRUPT_BITSTREAM, "oversubscribed huffman code");
+                    lim[G.lim_off + L] = L == 64 ? ~0ull : (code << (64 - L));
+                    if (L < 64 && code == (1ull << L)) lim[G.lim_off + L] = ~0ull;  // complete code
+                }
+            }
+            G.elem_off = stream_pos + total;
+            G.sym_off = sym_total;
+            sym_total += G.nsyms;
+            G.chunk0 = (uint32_t)chunks.size();
+            G.nchunks = G.nsyms ? (uint32_t)((G.nbits + kChunkBits - 1) / kChunkBits) : 0;
+            if (G.nsyms && !G.nchunks) throw Fail(DQTG_CORRUPT_BITSTREAM, "bitstream overrun");
+            for (uint32_t c = 0; c < G.nchunks; ++c) chunks.push_back(ChunkDesc{(uint32_t)groups.size(), c});
+            rec_elems[(size_t)i * B + bucket] = G.elems;
+            total += G.elems;
+            groups.push_back(G);
+        }
+        if (total != numel) throw Fail(DQTG_CORRUPT_INDEX, "group totals do not cover the tensor");
+        stream_pos += numel;
+    }
+    const uint32_t stored_crc = r.le<uint32_t>();
+    if (r.at != n) throw Fail(DQTG_IO, "trailing bytes after DQDR record");
+
+    // state layout from the record
+    dqtg_layout dl{};
+    std::vector<const char*> cn(nt);
+    for (uint32_t i = 0; i < nt; ++i) cn[i] = names[i].c_str();
+    dl.n_tensors = nt;
+    dl.names = cn.data();
+    dl.types = types.data();
+    dl.ranks = ranks.data();
+    dl.dims = dims.data();
+    q->L = make_layout(&e, &dl);
+    const Layout& L = *q->L;
+    const uint64_t N = L.N;
+    const int ntiles = (int)L.tiles.size();
+    uint32_t stride = 1;
+    for (int lt = 0; lt < kLayerTypes; ++lt) stride = std::max(stride, q->cb_len[lt]);
+    q->cb_stride = stride;
+    {
+        std::vector<float> flat((size_t)kLayerTypes * stride, 0.0f);
+        for (int lt = 0; lt < kLayerTypes; ++lt)
+            std::copy(q->cb[lt].begin(), q->cb[lt].end(), flat.begin() + (size_t)lt * stride);
+        q->d_cb = (float*)e.dalloc(flat.size() * 4);
+        DQTG_CUDA(cudaMemcpyAsync(q->d_cb, flat.data(), flat.size() * 4, cudaMemcpyHostToDevice, st));
+        e.sync();  // `flat` goes out of scope
+    }
+    // protected entries
+    q->prot_count.assign(nt, 0);
+    q->prot_off.assign(nt + 1, 0);
+    uint64_t acc = 0;
+    for (uint32_t i = 0; i < nt; ++i) {
+        q->prot_off[i] = acc;
+        q->prot_count[i] = ppos[i].size();
+        acc += ppos[i].size();
+    }
+    q->prot_off[nt] = q->prot_total = acc;
+    q->d_ppos = (uint64_t*)e.dalloc((acc + 1) * 8);
+    q->d_pval = (uint16_t*)e.dalloc((acc + 1) * 2);
+    for (uint32_t i = 0; i < nt; ++i)
+        if (!ppos[i].empty()) {
+            e.to_device(q->d_ppos + q->prot_off[i], ppos[i].data(), ppos[i].size() * 8);
+            e.to_device(q->d_pval + q->prot_off[i], pval[i].data(), pval[i].size() * 2);
+        }
+    q->d_levels = (uint16_t*)e.dalloc(L.Np * 2);
+    DQTG_CUDA(cudaMemsetAsync(q->d_levels, 0, L.Np * 2, st));
+
+    // device copies: record (+16 zero bytes), groups, chunks, tables
+    const uint32_t ng = (uint32_t)groups.size(), nc = (uint32_t)chunks.size();
+    auto* d_rec = (uint8_t*)e.buf("d.rec", n + 32);
+    DQTG_CUDA(cudaMemsetAsync(d_rec + n, 0, 32, st));
+    e.to_device(d_rec, rec, n);
+    auto* d_groups = (GroupDesc*)e.buf("d.groups", (size_t)(ng + 1) * sizeof(GroupDesc));
+    auto* d_chunks = (ChunkDesc*)e.buf("d.chunks", (size_t)(nc + 1) * sizeof(ChunkDesc));
+    auto* d_sym = (int64_t*)e.buf("d.tsym", (tab_sym.size() + 1) * 8);
+    auto* d_lim = (uint64_t*)e.buf("d.lim", (lim.size() + 1) * 8);
+    auto* d_first = (uint64_t*)e.buf("d.first", (first.size() + 1) * 8);
+    auto* d_lbase = (uint32_t*)e.buf("d.lbase", (lbase.size() + 1) * 4);
+    auto* d_relems = (unsigned long long*)e.buf("d.relems", rec_elems.size() * 8 + 8);
+    e.to_device(d_groups, groups.data(), ng * sizeof(GroupDesc));
+    e.to_device(d_chunks, chunks.data(), nc * sizeof(ChunkDesc));
+    e.to_device(d_sym, tab_sym.data(), tab_sym.size() * 8);
+    e.to_device(d_lim, lim.data(), lim.size() * 8);
+    e.to_device(d_first, first.data(), first.size() * 8);
+    e.to_device(d_lbase, lbase.data(), lbase.size() * 4);
+    e.to_device(d_relems, rec_elems.data(), rec_elems.size() * 8);
+    DecTabs T{d_lim, d_first, d_lbase, d_sym};
+    const uint64_t* rec64 = (const uint64_t*)d_rec;
+
+    // symbol flags (first / last of each group)
+    std::vector<uint8_t> fl(sym_total + 1, 0);
+    for (auto& G : groups)
+        if (G.nsyms) {
+            fl[G.sym_off] |= 1;
+            fl[G.sym_off + G.nsyms - 1] |= 2;
+        }
+    auto* d_sflags = (uint8_t*)e.buf("d.sflags", sym_total + 16);
+    e.to_device(d_sflags, fl.data(), sym_total + 1);
+
+    // ---- H1: self-synchronising chunk decode
+    auto* d_start = (uint64_t*)e.buf("d.start", (size_t)(nc + 1) * 8);
+    auto* d_out = (uint64_t*)e.buf("d.outpos", (size_t)(nc + 1) * 8);
+    auto* d_cnt = (uint32_t*)e.buf("d.cnt", (size_t)(nc + 1) * 4);
+    auto* d_dirty = (uint8_t*)e.buf("d.dirty", (size_t)nc + 16);
+    auto* d_any = (uint32_t*)e.buf("d.any", 16);
+    {
+        std::vector<uint64_t> s0(nc);
+        for (uint32_t c = 0; c < nc; ++c) s0[c] = (uint64_t)chunks[c].local * kChunkBits;
+        e.to_device(d_start, s0.data(), nc * 8);
+        DQTG_CUDA(cudaMemsetAsync(d_dirty, 1, nc, st));
+        const unsigned gb = (nc + 255) / 256;
+        for (int it = 0; nc; ++it) {
+            DQTG_REQUIRE(it < 64, DQTG_CORRUPT_BITSTREAM, "huffman chunk synchronisation did not converge");
+            { DQTG_SPAN(e, "huff_sync_kernel"); huff_sync_kernel<<<gb, 256, 0, st>>>(rec64, d_groups, d_chunks, nc, T, d_start, d_out, d_cnt, d_dirty); }
+            DQTG_CUDA(cudaMemsetAsync(d_any, 0, 4, st));
+            { DQTG_SPAN(e, "huff_update_kernel"); huff_update_kernel<<<gb, 256, 0, st>>>(d_chunks, nc, d_start, d_out, d_dirty, d_any); }
+            e.launched(2);
+            uint32_t any = 0;
+            e.d2h(&any, d_any, 4);
+            e.sync();
+            if (!any) break;
+        }
+        // chunks' symbol counts -> scan (u64)
+        auto* d_scan = (unsigned long long*)e.buf("d.scan", (size_t)(nc + 2) * 8);
+        cub::TransformInputIterator<unsigned long long, Widen, const uint32_t*> it(d_cnt, Widen{});
+        size_t tb = 0;
+        DQTG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, it, d_scan, (int64_t)nc + 1, st));
+        DQTG_CUDA(cudaMemsetAsync(d_cnt + nc, 0, 4, st));
+        void* tmp = e.buf("d.cubtmp", tb + 16);
+        DQTG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, it, d_scan, (int64_t)nc + 1, st));
+        { DQTG_SPAN(e, "huff_check_kernel"); huff_check_kernel<<<(ng + 255) / 256 + 1, 256, 0, st>>>(d_groups, ng, d_scan, e.d_err); }
+        auto* d_syms = (int32_t*)e.buf("d.syms", (sym_total + 1) * 4);
+        { DQTG_SPAN(e, "huff_write_kernel"); huff_write_kernel<<<(nc + 255) / 256 + 1, 256, 0, st>>>(rec64, d_groups, d_chunks, nc, T, d_start, d_scan, d_syms, e.d_err); }
+        e.launched(2);
+        e.check_err();
+
+        // ---- R: RLE expansion into the dense rearranged delta stream
+        auto* d_ecnt = (unsigned long long*)e.buf("d.ecnt", (sym_total + 1) * 8);
+        auto* d_eoff = (unsigned long long*)e.buf("d.eoff", (sym_total + 1) * 8);
+        const unsigned rg = (unsigned)std::min<uint64_t>((sym_total + 255) / 256 + 1, (uint64_t)e.num_sms * 16);
+        { DQTG_SPAN(e, "rle_count_kernel"); rle_count_kernel<<<rg, 256, 0, st>>>(d_syms, d_sflags, sym_total, d_ecnt, kErrCorruptBitstream, e.d_err); }
+        size_t tb2 = 0;
+        DQTG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, d_ecnt, d_eoff, (int64_t)std::max<uint64_t>(sym_total, 1), st));
+        void* tmp2 = e.buf("d.cubtmp2", tb2 + 16);
+        DQTG_CUDA(cub::DeviceScan::ExclusiveSum(tmp2, tb2, d_ecnt, d_eoff, (int64_t)std::max<uint64_t>(sym_total, 1), st));
+        { DQTG_SPAN(e, "rle_total_kernel"); rle_total_kernel<<<(ng + 255) / 256 + 1, 256, 0, st>>>(d_groups, ng, d_eoff, d_ecnt, e.d_err); }
+        e.launched(2);
+        e.check_err();
+        auto* d_head = (uint32_t*)e.buf("d.head", (N + 1) * 4);
+        auto* d_sidx = (uint32_t*)e.buf("d.sidx", (N + 1) * 4);
+        auto* d_d = (uint8_t*)e.buf("d.delta", N + 16);
+        DQTG_CUDA(cudaMemsetAsync(d_head, 0, (N + 1) * 4, st));
+        { DQTG_SPAN(e, "rle_heads_kernel"); rle_heads_kernel<<<rg, 256, 0, st>>>(d_syms, sym_total, d_eoff, d_ecnt, d_head, N); }
+        size_t tb3 = 0;
+        DQTG_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb3, d_head, d_sidx, MaxOp{}, (int64_t)std::max<uint64_t>(N, 1), st));
+        void* tmp3 = e.buf("d.cubtmp3", tb3 + 16);
+        DQTG_CUDA(cub::DeviceScan::InclusiveScan(tmp3, tb3, d_head, d_sidx, MaxOp{}, (int64_t)std::max<uint64_t>(N, 1), st));
+        const unsigned fg = (unsigned)std::min<uint64_t>((N + 255) / 256 + 1, (uint64_t)e.num_sms * 16);
+        { DQTG_SPAN(e, "rle_fill_kernel"); rle_fill_kernel<<<fg, 256, 0, st>>>(d_sidx, N, d_syms, B, d_d, e.d_err); }
+        e.launched(2);
+
+        // ---- U: unrearrange against the previous levels
+        auto* d_tc = (uint32_t*)e.buf("d.tilecnt", (size_t)ntiles * B * 4 + 4);
+        auto* d_gs = (unsigned long long*)e.buf("d.gstart", (size_t)nt * B * 8 + 8);
+        auto* d_cbl = (uint32_t*)e.buf("d.cblen", kLayerTypes * 4);
+        e.to_device(d_cbl, q->cb_len, sizeof(q->cb_len));
+        const uint16_t* prev = base ? base->d_levels : nullptr;
+        if (ntiles) {
+            { DQTG_SPAN(e, "prev_count_kernel"); prev_count_kernel<<<ntiles, 256, 0, st>>>(L.d_tiles, prev, B, d_tc, e.d_err); }
+            { DQTG_SPAN(e, "prev_scan_kernel"); prev_scan_kernel<<<nt, 64, 0, st>>>(L.d_tile0, nt, B, d_tc, d_relems, d_gs, e.d_err); }
+            { DQTG_SPAN(e, "unrearrange_kernel"); unrearrange_kernel<<<ntiles, 256, 0, st>>>(L.d_tiles, L.d_types, L.d_stream_off, L.d_off, prev, B, d_tc, d_gs, d_d, d_cbl, q->d_levels, e.d_err); }
+            e.launched(3);
+        }
+        e.check_err();
+    }
+    // ---- C: stream checksum
+    const uint32_t crc = level_stream_crc(e, L, q->d_levels);
+    if (crc != stored_crc)
+        throw Fail(DQTG_CHECKSUM_MISMATCH, "record checksum mismatch at step " + std::to_string(target_step));
+    return q;
+}
+
+}  // namespace dqtg

@@ -167,6 +167,7 @@ void Engine::check_err() {
     if (h & kErrCorruptIndex) throw Fail(DQTG_CORRUPT_INDEX, "level outside cyclic alphabet");
     if (h & kErrHuffmanDepth) throw Fail(DQTG_ERROR, "huffman code length overflow");
     if (h & kErrKmeansWeights) throw Fail(DQTG_ERROR, "total weight must be positive");
+    if (h & kErrCorruptBitstream) throw Fail(DQTG_CORRUPT_BITSTREAM, "corrupt bitstream");
     throw Fail(DQTG_ERROR, "device error");
 }
 

@@ -223,6 +223,8 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
 std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
                                       const QState* base);
 void dequantize(Engine& e, const QState& q, float* out_dev_padded);
+// crc32 (codec.cpp:275-306) of a state's level stream (u16 LE, tensor order)
+uint32_t level_stream_crc(Engine& e, const Layout& L, const uint16_t* levels_dev);
 void partition(Engine& e, const DevCkpt& c, const dqtg_config& cfg, uint8_t* const* masks);
 double proxy_quality(Engine& e, const DevCkpt& orig, const float* recon_dev_padded);
 void level_counts(Engine& e, const QState& q, uint64_t* counts, int lstride);

@@ -105,6 +105,9 @@ def _load():
         "dqtg_qstate_upload": (C.c_int, [_P, C.POINTER(_Layout), C.c_uint64, C.POINTER(Config),
                                          _P, _P, _P, _P, _P, _P, C.POINTER(_P)]),
         "dqtg_qstate_destroy": (None, [_P]),
+        "dqtg_qstate_tensor_count": (C.c_uint32, [_P]),
+        "dqtg_qstate_tensor_info": (C.c_int, [_P, C.c_uint32, C.c_char_p, C.c_uint64,
+                                              C.POINTER(C.c_uint8), C.POINTER(C.c_uint8), _P]),
         "dqtg_qstate_levels_dev": (_P, [_P]),
         "dqtg_dequantize": (C.c_int, [_P, _P, _P]),
         "dqtg_encode_record": (C.c_int, [_P, _P, _P, C.c_double, C.POINTER(_P)]),
@@ -245,6 +248,21 @@ class DevCheckpoint:
         return LIB.dqtg_ckpt_tensor_offset(self.h, i)
 
 
+def state_meta(h) -> "_Meta":
+    """Layout of a state handle (names, types, shapes) from the engine."""
+    names, types, shapes = [], [], []
+    buf = C.create_string_buffer(4096)
+    dims = np.zeros(8, np.uint64)
+    t, r = C.c_uint8(), C.c_uint8()
+    for i in range(LIB.dqtg_qstate_tensor_count(h)):
+        _check(LIB.dqtg_qstate_tensor_info(h, i, buf, len(buf), C.byref(t), C.byref(r),
+                                           dims.ctypes.data))
+        names.append(buf.value.decode())
+        types.append(t.value)
+        shapes.append(tuple(int(d) for d in dims[:r.value]))
+    return _Meta(names, types, shapes)
+
+
 class DevState:
     def __init__(self, engine, h, meta):
         self.engine, self.h, self.meta = engine, h, meta
@@ -382,10 +400,11 @@ class Engine:
         return r
 
     def decode_record(self, rec: bytes, base: DevState = None) -> DevState:
+        """decode_delta_record (codec.cpp:459-597) on the device."""
         h = _P()
         _check(LIB.dqtg_decode_record(self.h, rec, len(rec), None if base is None else base.h,
                                       C.byref(h)))
-        return h
+        return DevState(self, h, state_meta(h))
 
     def compress_step(self, ckpt, cfg, seed, step, base=None, quality=0.0):
         s, r = _P(), _P()
