@@ -472,6 +472,46 @@ def run_ours(args):
            "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
            "path": e2e_path}
 
+    # restore: decode_delta_record + dequantize_checkpoint on the device (the other
+    # half of the round trip, Chain::restore replay), records read from host memory
+    restore = None
+    if world == 1:
+        r_steps = min(args.steps, 6)
+        st_prev = eng.quantize(ckpts[0], cfg, 1, 0)
+        recs = [eng.encode_record(st_prev)]
+        for i in range(1, r_steps + 2):
+            st_i, r = eng.compress_step(ckpts[i], cfg, 1, i, st_prev)
+            buf = np.empty(E.LIB.dqtg_record_size(r), np.uint8)
+            E._check(E.LIB.dqtg_record_copy(r, buf.ctypes.data))
+            E.LIB.dqtg_record_destroy(r)
+            recs.append(buf.tobytes())
+            st_prev = st_i
+        last_levels = torch.empty(0)
+        out = torch.empty(N, dtype=torch.float32, device=dev)
+        optr = E._ptr_array(tensor_ptrs(out.data_ptr(), layout))
+        dec = eng.decode_record(recs[0])
+        dec = eng.decode_record(recs[1], base=dec)  # warm-up
+        E._check(E.LIB.dqtg_dequantize(eng.h, dec.h, optr))
+        eng.sync()
+        tr = time.perf_counter()
+        for rec in recs[2:]:
+            dec = eng.decode_record(rec, base=dec)
+            E._check(E.LIB.dqtg_dequantize(eng.h, dec.h, optr))
+        eng.sync()
+        tr = time.perf_counter() - tr
+        ok = bool(torch.equal(torch.frombuffer(bytearray(dec.download().levels[0].tobytes()),
+                                               dtype=torch.uint8),
+                              torch.frombuffer(bytearray(st_prev.download().levels[0].tobytes()),
+                                               dtype=torch.uint8)))
+        nrec = len(recs) - 2
+        restore = {"value": 4.0 * N * nrec / tr / 1e9, "unit": "GB/s (fp32 out)",
+                   "ms_per_step": 1e3 * tr / nrec, "steps": nrec,
+                   "record_bytes": float(np.mean([len(x) for x in recs[2:]])),
+                   "levels_match_encoder": ok,
+                   "path": "Engine.decode_record(host DQDR bytes, base) + dqtg_dequantize "
+                           "into HBM, device decode (chunked self-synchronising Huffman)"}
+        del last_levels
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         stepf, Ns, _ = reference_step_timer()
@@ -505,7 +545,8 @@ def run_ours(args):
                                   f"sync on both ends"
                                   if pipelined is not None and ms == pipelined else
                                   "CUDA events on the engine stream")},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "restore": restore,
+            "gpu_launches": launches,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -29,7 +29,8 @@
 
 namespace dqtg {
 
-constexpr uint32_t kChunkBits = 4096;
+constexpr uint32_t kChunkBits = 1024;
+constexpr int kBnd = 24;  // codeword starts recorded per chunk (sync shortcut)
 constexpr int kMaxCodeLen = 64;
 
 struct GroupDesc {
@@ -90,39 +91,76 @@ __global__ void __launch_bounds__(256) huff_sync_kernel(const uint64_t* rec64, c
                                                         const ChunkDesc* chunks, uint32_t nchunks,
                                                         DecTabs T, const uint64_t* start,
                                                         uint64_t* out_pos, uint32_t* count,
-                                                        const uint8_t* dirty) {
+                                                        const uint8_t* dirty, uint16_t* bounds) {
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= nchunks || !dirty[c]) return;
     const ChunkDesc C = chunks[c];
     const GroupDesc G = groups[C.group];
     const uint64_t end = min((uint64_t)(C.local + 1) * kChunkBits, G.nbits);
+    const uint64_t nom = (uint64_t)C.local * kChunkBits;
     uint64_t p = start[c];
     uint32_t n = 0;
+    uint16_t* bnd = bounds + (size_t)c * kBnd;
     while (p < end) {
+        if (n < kBnd) bnd[n] = (uint16_t)(p - nom);
         uint32_t idx;
         const uint32_t L = decode_one(rec64, G, T, p, idx);
         p += L ? L : 1;  // invalid code: resynchronise (corrupt streams fail in H2)
         ++n;
     }
+    for (uint32_t k = n; k < kBnd; ++k) bnd[k] = 0xffff;
     out_pos[c] = p;
     count[c] = n;
 }
 
-// H1 update: a chunk's start is where the previous chunk's decode ended
+// H1 update: a chunk's start is where the previous chunk's decode ended.  When that
+// position is one of the codeword starts the chunk's own (speculative) decode went
+// through, its end position is already right and only its symbol count shrinks.
 __global__ void huff_update_kernel(const ChunkDesc* chunks, uint32_t nchunks, uint64_t* start,
-                                   const uint64_t* out_pos, uint8_t* dirty, uint32_t* any) {
+                                   const uint64_t* out_pos, uint32_t* count, uint8_t* dirty,
+                                   uint16_t* bounds, uint32_t* any) {
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= nchunks) return;
     uint8_t d = 0;
-    if (chunks[c].local > 0) {
+    const uint32_t local = chunks[c].local;
+    if (local > 0) {
         const uint64_t s = out_pos[c - 1];
         if (s != start[c]) {
             start[c] = s;
-            d = 1;
+            const uint64_t rel = s - (uint64_t)local * kChunkBits;
+            uint16_t* bnd = bounds + (size_t)c * kBnd;
+            int hit = -1;
+            for (int k = 0; k < kBnd && hit < 0; ++k)
+                if (bnd[k] == rel) hit = k;
+            if (hit >= 0) {  // synchronised inside the recorded prefix
+                count[c] -= (uint32_t)hit;
+                for (int k = 0; k + hit < kBnd; ++k) bnd[k] = bnd[k + hit];
+                for (int k = kBnd - hit; k < kBnd; ++k) bnd[k] = 0xffff;
+            } else {
+                d = 1;
+            }
         }
     }
     dirty[c] = d;
     if (d) *any = 1;
+}
+
+__global__ void group_flags_kernel(const GroupDesc* groups, uint32_t ng, uint8_t* f) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= ng) return;
+    const GroupDesc G = groups[g];
+    if (!G.nsyms) return;
+    if (G.nsyms == 1) {
+        f[G.sym_off] = 3;
+    } else {
+        f[G.sym_off] = 1;
+        f[G.sym_off + G.nsyms - 1] = 2;
+    }
+}
+
+__global__ void chunk_init_kernel(const ChunkDesc* chunks, uint32_t nc, uint64_t* start) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < nc) start[c] = (uint64_t)chunks[c].local * kChunkBits;
 }
 
 // H2: decode again, writing symbols at their index inside the group
@@ -248,31 +286,39 @@ __global__ void __launch_bounds__(256) prev_count_kernel(const Tile* tiles, cons
     for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) tile_cnt[(size_t)blockIdx.x * B + b] = s_c[b];
 }
 
-// U2: per (tensor, key): exclusive prefix of the tile counts over the tensor's
-// tiles; per tensor the keys' group starts; record group sizes must match
-__global__ void prev_scan_kernel(const uint32_t* tile0, uint32_t nt, uint32_t B, uint32_t* tile_cnt,
-                                 const unsigned long long* rec_elems /*[nt][B]*/,
-                                 unsigned long long* gstart /*[nt][B]*/, uint32_t* err) {
-    const uint32_t t = blockIdx.x;
-    if (t >= nt) return;
-    __shared__ unsigned long long s_tot[64];
-    for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) {
-        unsigned long long acc = 0;
-        for (uint32_t ti = tile0[t]; ti < tile0[t + 1]; ++ti) {
-            const uint32_t c = tile_cnt[(size_t)ti * B + b];
-            tile_cnt[(size_t)ti * B + b] = (uint32_t)acc;
-            acc += c;
-        }
-        s_tot[b] = acc;
-        if (acc != rec_elems[(size_t)t * B + b]) atomicOr(err, kErrCorruptIndex);
+// U2: one block per (tensor, key): exclusive prefix of the tile counts over the
+// tensor's tiles; key totals must match the record's group sizes
+__global__ void __launch_bounds__(256) prev_scan_kernel(const uint32_t* tile0, uint32_t B,
+                                                        uint32_t* tile_cnt,
+                                                        const unsigned long long* rec_elems,
+                                                        unsigned long long* totals, uint32_t* err) {
+    __shared__ unsigned long long s_scan[33];
+    const uint32_t t = blockIdx.x / B, b = blockIdx.x % B;
+    const uint32_t t0 = tile0[t], t1 = tile0[t + 1];
+    unsigned long long run = 0;
+    for (uint32_t c0 = t0; c0 < t1; c0 += blockDim.x) {
+        const uint32_t ti = c0 + threadIdx.x;
+        const unsigned long long v = ti < t1 ? tile_cnt[(size_t)ti * B + b] : 0ull;
+        unsigned long long tot;
+        const unsigned long long ex = block_exclusive_scan<unsigned long long>(v, s_scan, &tot);
+        if (ti < t1) tile_cnt[(size_t)ti * B + b] = (uint32_t)(run + ex);
+        run += tot;
     }
-    __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned long long acc = 0;
-        for (uint32_t b = 0; b < B; ++b) {
-            gstart[(size_t)t * B + b] = acc;
-            acc += s_tot[b];
-        }
+        totals[(size_t)t * B + b] = run;
+        if (run != rec_elems[(size_t)t * B + b]) atomicOr(err, kErrCorruptIndex);
+    }
+}
+
+// U2b: per tensor, start of every key's group in the rearranged order
+__global__ void group_start_kernel(uint32_t nt, uint32_t B, const unsigned long long* totals,
+                                   unsigned long long* gstart) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    unsigned long long acc = 0;
+    for (uint32_t b = 0; b < B; ++b) {
+        gstart[(size_t)t * B + b] = acc;
+        acc += totals[(size_t)t * B + b];
     }
 }
 
@@ -632,14 +678,9 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
     const uint64_t* rec64 = (const uint64_t*)d_rec;
 
     // symbol flags (first / last of each group)
-    std::vector<uint8_t> fl(sym_total + 1, 0);
-    for (auto& G : groups)
-        if (G.nsyms) {
-            fl[G.sym_off] |= 1;
-            fl[G.sym_off + G.nsyms - 1] |= 2;
-        }
     auto* d_sflags = (uint8_t*)e.buf("d.sflags", sym_total + 16);
-    e.to_device(d_sflags, fl.data(), sym_total + 1);
+    DQTG_CUDA(cudaMemsetAsync(d_sflags, 0, sym_total + 1, st));
+    if (ng) { DQTG_SPAN(e, "group_flags_kernel"); group_flags_kernel<<<(ng + 255) / 256, 256, 0, st>>>(d_groups, ng, d_sflags); }
 
     // ---- H1: self-synchronising chunk decode
     auto* d_start = (uint64_t*)e.buf("d.start", (size_t)(nc + 1) * 8);
@@ -647,17 +688,16 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
     auto* d_cnt = (uint32_t*)e.buf("d.cnt", (size_t)(nc + 1) * 4);
     auto* d_dirty = (uint8_t*)e.buf("d.dirty", (size_t)nc + 16);
     auto* d_any = (uint32_t*)e.buf("d.any", 16);
+    auto* d_bnd = (uint16_t*)e.buf("d.bounds", (size_t)(nc + 1) * kBnd * 2);
     {
-        std::vector<uint64_t> s0(nc);
-        for (uint32_t c = 0; c < nc; ++c) s0[c] = (uint64_t)chunks[c].local * kChunkBits;
-        e.to_device(d_start, s0.data(), nc * 8);
+        if (nc) { DQTG_SPAN(e, "chunk_init_kernel"); chunk_init_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_chunks, nc, d_start); }
         DQTG_CUDA(cudaMemsetAsync(d_dirty, 1, nc, st));
         const unsigned gb = (nc + 255) / 256;
         for (int it = 0; nc; ++it) {
             DQTG_REQUIRE(it < 64, DQTG_CORRUPT_BITSTREAM, "huffman chunk synchronisation did not converge");
-            { DQTG_SPAN(e, "huff_sync_kernel"); huff_sync_kernel<<<gb, 256, 0, st>>>(rec64, d_groups, d_chunks, nc, T, d_start, d_out, d_cnt, d_dirty); }
+            { DQTG_SPAN(e, "huff_sync_kernel"); huff_sync_kernel<<<gb, 256, 0, st>>>(rec64, d_groups, d_chunks, nc, T, d_start, d_out, d_cnt, d_dirty, d_bnd); }
             DQTG_CUDA(cudaMemsetAsync(d_any, 0, 4, st));
-            { DQTG_SPAN(e, "huff_update_kernel"); huff_update_kernel<<<gb, 256, 0, st>>>(d_chunks, nc, d_start, d_out, d_dirty, d_any); }
+            { DQTG_SPAN(e, "huff_update_kernel"); huff_update_kernel<<<gb, 256, 0, st>>>(d_chunks, nc, d_start, d_out, d_cnt, d_dirty, d_bnd, d_any); }
             e.launched(2);
             uint32_t any = 0;
             e.d2h(&any, d_any, 4);
@@ -711,9 +751,11 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
         const uint16_t* prev = base ? base->d_levels : nullptr;
         if (ntiles) {
             { DQTG_SPAN(e, "prev_count_kernel"); prev_count_kernel<<<ntiles, 256, 0, st>>>(L.d_tiles, prev, B, d_tc, e.d_err); }
-            { DQTG_SPAN(e, "prev_scan_kernel"); prev_scan_kernel<<<nt, 64, 0, st>>>(L.d_tile0, nt, B, d_tc, d_relems, d_gs, e.d_err); }
+            auto* d_tot = (unsigned long long*)e.buf("d.ktot", (size_t)nt * B * 8 + 8);
+            { DQTG_SPAN(e, "prev_scan_kernel"); prev_scan_kernel<<<nt * B, 256, 0, st>>>(L.d_tile0, B, d_tc, d_relems, d_tot, e.d_err); }
+            { DQTG_SPAN(e, "group_start_kernel"); group_start_kernel<<<(nt + 127) / 128, 128, 0, st>>>(nt, B, d_tot, d_gs); }
             { DQTG_SPAN(e, "unrearrange_kernel"); unrearrange_kernel<<<ntiles, 256, 0, st>>>(L.d_tiles, L.d_types, L.d_stream_off, L.d_off, prev, B, d_tc, d_gs, d_d, d_cbl, q->d_levels, e.d_err); }
-            e.launched(3);
+            e.launched(4);
         }
         e.check_err();
     }
