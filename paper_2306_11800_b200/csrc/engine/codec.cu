@@ -579,38 +579,45 @@ __device__ __forceinline__ RunM runm_combine(const RunM& a, const RunM& b) {
     return r;
 }
 
-// Block per (tensor, group) for tensors with many tiles (256-tile chunks).
+__device__ __forceinline__ RunM shfl_down_runm(const RunM& m, int o);
+
+// Block per (tensor, group) for tensors with many tiles (256-tile chunks): warp
+// shuffle scans + one shared-memory combine of the 8 warp aggregates per chunk.
 __global__ void __launch_bounds__(kCB) enc_resolve_big_kernel(EncArgs A, const uint32_t* tensors) {
     extern __shared__ uint32_t s_f[];  // NS
-    __shared__ RunM s_m[kCB];
-    __shared__ int s_last[kCB];
+    __shared__ int s_wmax[kCB / 32];
+    __shared__ RunM s_wm[kCB / 32];
     const uint32_t B = A.B, NS = A.NS;
     const uint32_t t = tensors[blockIdx.x / B], b = blockIdx.x % B;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t a0 = A.tile0[t], a1 = A.tile0[t + 1];
     for (uint32_t i = tid; i < NS; i += kCB) s_f[i] = 0;
-    // forward: lv of the nearest earlier non-empty segment
+    // forward: lv of the nearest earlier non-empty segment (inclusive max-scan)
     int carry_last = -1;
     for (uint32_t c0 = a0; c0 < a1; c0 += kCB) {
         const uint32_t i = c0 + tid;
-        int idx = (i < a1 && A.segs[(size_t)i * B + b].n) ? (int)i : -1;
-        s_last[tid] = idx;
-        __syncthreads();
-        for (int o = 1; o < kCB; o <<= 1) {
-            int v = tid >= o ? s_last[tid - o] : -1;
-            __syncthreads();
-            if (v > s_last[tid]) s_last[tid] = v;
-            __syncthreads();
+        Seg S{};
+        if (i < a1) S = A.segs[(size_t)i * B + b];
+        const int idx = (i < a1 && S.n) ? (int)i : -1;
+        int x = idx;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o && y > x) x = y;
         }
-        int prev = tid ? s_last[tid - 1] : -1;
-        if (prev < carry_last) prev = carry_last;
-        if (idx >= 0) {
-            Seg& S = A.segs[(size_t)i * B + b];
-            S.cont = prev >= 0 && A.segs[(size_t)prev * B + b].lv == S.fv;
-        }
-        int cl = s_last[kCB - 1];
+        if (lane == 31) s_wmax[wid] = x;
         __syncthreads();
-        if (cl > carry_last) carry_last = cl;
+        int before = carry_last;
+        for (int w = 0; w < wid; ++w) before = max(before, s_wmax[w]);
+        int excl = __shfl_up_sync(0xffffffffu, x, 1);
+        if (lane == 0) excl = -1;
+        const int prev = max(before, excl);
+        if (idx >= 0)
+            A.segs[(size_t)i * B + b].cont = prev >= 0 && A.segs[(size_t)prev * B + b].lv == S.fv;
+        int cl = carry_last;
+        for (int w = 0; w < kCB / 32; ++w) cl = max(cl, s_wmax[w]);
+        __syncthreads();
+        carry_last = cl;
     }
     __syncthreads();
     // backward: suffix run monoid gives the extension of each trailing run
@@ -633,15 +640,19 @@ __global__ void __launch_bounds__(kCB) enc_resolve_big_kernel(EncArgs A, const u
                 m.lead = S.lead;
             }
         }
-        s_m[tid] = m;
-        __syncthreads();
-        for (int o = 1; o < kCB; o <<= 1) {  // inclusive suffix
-            RunM nb = tid + o < kCB ? s_m[tid + o] : RunM{};
-            __syncthreads();
-            s_m[tid] = runm_combine(s_m[tid], nb);
-            __syncthreads();
+        // inclusive suffix inside the warp
+        RunM x = m;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const RunM y = shfl_down_runm(x, o);
+            if (lane + o < 32) x = runm_combine(x, y);
         }
-        RunM after = tid + 1 < kCB ? runm_combine(s_m[tid + 1], carry) : carry;
+        if (lane == 0) s_wm[wid] = x;
+        __syncthreads();
+        RunM later = carry;  // suffix of the warps after this one, then the carry
+        for (int w = kCB / 32 - 1; w > wid; --w) later = runm_combine(s_wm[w], later);
+        RunM nxt = shfl_down_runm(x, 1);  // suffix starting at the next lane
+        RunM after = lane < 31 ? runm_combine(nxt, later) : later;
         if (i < a1 && S.n) {
             unsigned long long E = (after.n && after.fv == S.lv) ? after.lead : 0ull;
             const bool single = S.lead == S.n;
@@ -656,9 +667,10 @@ __global__ void __launch_bounds__(kCB) enc_resolve_big_kernel(EncArgs A, const u
                 add_symbol(f, NS, B, tb, S.lv, S.trail + E, A);
             }
         }
-        RunM chunk = s_m[0];
+        RunM chunk = carry;
+        for (int w = kCB / 32 - 1; w >= 0; --w) chunk = runm_combine(s_wm[w], chunk);
         __syncthreads();
-        carry = runm_combine(chunk, carry);
+        carry = chunk;
     }
     __syncthreads();
     uint32_t* gf = A.freq + (size_t)tb * NS;
