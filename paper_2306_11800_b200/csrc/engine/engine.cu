@@ -84,6 +84,7 @@ Engine::~Engine() {
     for (auto& kv : tables) {
         cudaFree(kv.second->d_U);
         cudaFree(kv.second->d_cell);
+        cudaFree(kv.second->d_slot);
         cudaFree(kv.second->d_key);
         cudaFree(kv.second->d_keyf);
     }
@@ -283,17 +284,35 @@ AlphaTables& Engine::alpha_tables(double alpha) {
         }
         return lo;
     };
+    // Slot table on the same cells: the shared-memory window slot of |x| directly
+    // (0 zero bucket, 1..kWin window bucket kw_lo + p - 1, kSlotSpill outside the
+    // window, kSlotBad non-finite); entry = (lo | hi << 16, split bits).
+    std::vector<uint2> slots;
+    auto pslot = [&](int64_t k) -> uint32_t {
+        const int64_t d = k - t->kw_lo;
+        return (d >= 0 && d < kWin) ? (uint32_t)(d + 1) : kSlotSpill;
+    };
     for (uint32_t m = 4; m <= 12 && !t->cell_shift; ++m) {
         const uint32_t shift = 23 - m, ncell = 0x7f800000u >> shift;
         cells.assign(ncell, uint2{0, 0xffffffffu});
+        slots.assign(0x80000000u >> shift, uint2{kSlotBad | (kSlotBad << 16), 0xffffffffu});
         bool ok = true;
         for (uint32_t c = 0; c < ncell && ok; ++c) {
-            const uint32_t a0 = std::max(c << shift, t->zbits), a1 = ((c + 1) << shift) - 1;
-            if (a1 < t->zbits) continue;  // zero bucket, handled before the lookup
+            const uint32_t c0 = c << shift, a0 = std::max(c0, t->zbits), a1 = ((c + 1) << shift) - 1;
+            if (a1 < t->zbits) {  // zero bucket
+                slots[c] = uint2{0u, 0xffffffffu};
+                continue;
+            }
             const int64_t k0 = host_bucket(a0), k1 = host_bucket(a1);
             if (k1 > k0 + 1) ok = false;
             cells[c].x = (uint32_t)(int32_t)k0;
             cells[c].y = k1 == k0 ? 0xffffffffu : ubits(k0);
+            if (c0 < t->zbits) {  // zero bucket below zbits, then one bucket
+                if (k1 != k0) ok = false;
+                slots[c] = uint2{0u | (pslot(k0) << 16), t->zbits - 1};
+            } else {
+                slots[c] = uint2{pslot(k0) | (pslot(k1) << 16), k1 == k0 ? 0xffffffffu : ubits(k0)};
+            }
         }
         if (ok) t->cell_shift = shift;
     }
@@ -301,6 +320,9 @@ AlphaTables& Engine::alpha_tables(double alpha) {
     if (t->cell_shift) {
         DQTG_CUDA(cudaMalloc(&t->d_cell, cells.size() * sizeof(uint2)));
         DQTG_CUDA(cudaMemcpy(t->d_cell, cells.data(), cells.size() * sizeof(uint2),
+                             cudaMemcpyHostToDevice));
+        DQTG_CUDA(cudaMalloc(&t->d_slot, slots.size() * sizeof(uint2)));
+        DQTG_CUDA(cudaMemcpy(t->d_slot, slots.data(), slots.size() * sizeof(uint2),
                              cudaMemcpyHostToDevice));
     }
     DQTG_CUDA(cudaMalloc(&t->d_U, U.size() * 4));

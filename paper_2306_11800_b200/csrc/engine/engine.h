@@ -15,6 +15,8 @@ namespace dqtg {
 // Shared-memory histogram window: kWin buckets per sign plus the zero bucket.
 constexpr int kWin = 4096;
 constexpr int kWinSlots = 2 * kWin + 1;
+// slot-table sentinels (AlphaTables::d_slot)
+constexpr uint32_t kSlotSpill = 0xffffu, kSlotBad = 0xfffeu;
 // Elements per tile of every streaming pass (a tile never crosses a tensor).
 constexpr uint32_t kTile = 4096;
 
@@ -43,6 +45,7 @@ struct AlphaTables {
     // bucket(a) = k + (a > split), one load instead of log2 + table probes.
     uint32_t cell_shift = 0;     // 0: no table (alpha too small), probe U instead
     uint2* d_cell = nullptr;
+    uint2* d_slot = nullptr;     // same cells: window slot of |x| (lo | hi << 16, split)
 };
 
 // Device view of the bucket tables passed by value to kernels.
@@ -53,6 +56,7 @@ struct BucketTab {
     float inv_log2_gamma;
     const uint2* cell;  // null: probe U
     uint32_t cell_shift;
+    const uint2* slot;  // window-slot table (null with cell)
 };
 
 struct Engine;
@@ -158,7 +162,7 @@ struct Engine {
     AlphaTables& alpha_tables(double alpha);
     BucketTab bucket_tab(const AlphaTables& t) const {
         return BucketTab{t.d_U, t.kmin, t.kmax, t.NB, t.kw_lo, t.zbits, t.inv_log2_gamma, t.d_cell,
-                         t.cell_shift};
+                         t.cell_shift, t.d_slot};
     }
     void* buf(const std::string& name, size_t bytes);  // scratch, contents undefined
     // stream-ordered pool allocations for per-step objects (states, records)

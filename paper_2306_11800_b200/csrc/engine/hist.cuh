@@ -41,9 +41,33 @@ __device__ __forceinline__ int64_t slot_of(float v, const BucketTab& t) {
 
 // Adds v to a shared-memory window histogram (sh[kWinSlots]) with spill to the
 // global u64 histogram gh[HS] for buckets outside the window.
+// Slow path of the slot-table adds: outside the window or non-finite.
+__device__ __forceinline__ void hist_spill(unsigned long long* gh, float v, const BucketTab& t,
+                                        uint32_t* err) {
+    const uint32_t b = __float_as_uint(v), a = b & 0x7fffffffu;
+    if (a >= 0x7f800000u) {
+        atomicOr(err, kErrNonFinite);
+        return;
+    }
+    const int k = bucket_of(a, t);
+    atomicAdd(gh + ((b >> 31) ? (t.kmax - k) : (t.NB + 1 + k - t.kmin)), 1ull);
+}
+
+// Window slot p of |x| from the slot table (0 zero, 1..kWin window, else spill/bad).
+__device__ __forceinline__ uint32_t slot_of_abs(uint32_t a, const BucketTab& t) {
+    const uint2 c = __ldg(t.slot + (a >> t.cell_shift));
+    return (a > c.y) ? (c.x >> 16) : (c.x & 0xffffu);
+}
+
 __device__ __forceinline__ void hist_add(uint32_t* sh, unsigned long long* gh, float v,
                                          const BucketTab& t, uint32_t* err) {
     uint32_t b = __float_as_uint(v), a = b & 0x7fffffffu;
+    if (t.slot) {  // one table load; signed window: neg kWin - p, zero kWin, pos kWin + p
+        const uint32_t p = slot_of_abs(a, t);
+        if (p <= (uint32_t)kWin) atomicAdd(sh + ((b >> 31) ? kWin - p : kWin + p), 1u);
+        else hist_spill(gh, v, t, err);
+        return;
+    }
     if (a >= 0x7f800000u) {
         atomicOr(err, kErrNonFinite);
         return;
@@ -89,6 +113,12 @@ constexpr int kPosSlots = kWin + 1;
 __device__ __forceinline__ void hist_add_pos(uint32_t* sh, unsigned long long* gh, float v,
                                              const BucketTab& t, uint32_t* err) {
     const uint32_t a = __float_as_uint(v);  // v >= +0 (fabs of a finite float) or NaN/Inf
+    if (t.slot) {
+        const uint32_t p = slot_of_abs(a, t);
+        if (p <= (uint32_t)kWin) atomicAdd(sh + p, 1u);
+        else hist_spill(gh, v, t, err);
+        return;
+    }
     if (a >= 0x7f800000u) {
         atomicOr(err, kErrNonFinite);
         return;
