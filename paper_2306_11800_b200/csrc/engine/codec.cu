@@ -125,10 +125,11 @@ __device__ __forceinline__ void add_symbol(uint32_t* f, uint32_t NS, uint32_t B,
 constexpr int kCrcTabs = 10;  // T1,T3,T5,T7,T9,T11,T12,T13,T14,T15 (T_n: byte + n zero bytes)
 constexpr int kChunks = 512 / 32;  // chunks per warp range
 __device__ uint32_t g_crc_slice[kCrcTabs][256];
-// g_crc_nib[s][i][n]: nibble n at position i times the shift of combine level s
-// (x^(8m) mod P with m = 32 * 2^s bytes for s < 5: lanes of a warp; m = 1024 *
-// 2^(s-5) for s = 5..7: warps of the tile)
-__device__ uint32_t g_crc_nib[8][8][16];
+// g_crc_nib[s][i][n]: nibble n at position i times x^(8m) mod P for the combine
+// constant s: s < 8 lane r of a group of 8 lanes (m = 32 * (7 - r) bytes), s = 8, 9
+// groups of a warp (m = 256, 512), s = 10..12 warps of the tile (m = 1024 * 2^(s-10))
+constexpr int kNibConsts = 13;
+__device__ uint32_t g_crc_nib[kNibConsts][8][16];
 
 // 8 levels (16 stream bytes, odd bytes 0) through the CRC register
 __device__ __forceinline__ uint32_t crc_block8(const uint32_t* T, uint32_t r, uint32_t l03,
@@ -150,23 +151,37 @@ __device__ __forceinline__ uint32_t crc_mul_nib(const uint32_t* N, uint32_t v, i
     return r;
 }
 
-// Binary-tree combine of per-lane chunk CRCs (each a zero-register CRC ending at
-// its chunk end) over `levels` levels starting at level s0: the left half of
-// every pair moves past the right half.  Lane 0 returns the combined value.
-__device__ __forceinline__ uint32_t crc_tree(const uint32_t* N, uint32_t v, int s0, int levels) {
+// Binary-tree combine of per-lane values over `levels` levels with constants
+// s0, s0+1, ..., lanes at multiples of `stride`: the left value of every pair
+// moves past the right one.  Lane 0 returns the combined value.
+__device__ __forceinline__ uint32_t crc_tree(const uint32_t* N, uint32_t v, int s0, int levels,
+                                             int stride = 1) {
     const int lane = threadIdx.x & 31;
     for (int l = 0; l < levels; ++l) {
-        const uint32_t o = __shfl_down_sync(0xffffffffu, v, 1 << l);
+        const int d = stride << l;
+        const uint32_t o = __shfl_down_sync(0xffffffffu, v, d);
         const uint32_t m = crc_mul_nib(N, v, s0 + l) ^ o;
-        if (((lane >> l) & 1) == 0) v = m;
+        if ((lane & (2 * d - 1)) == 0) v = m;
     }
     return v;
+}
+
+// Warp combine of 32 consecutive 32-byte chunk CRCs: each lane moves its chunk to
+// the end of its 8-lane group (one table multiply), XOR within the group, then a
+// two-level tree over the four groups.  Lane 0 returns the warp's 1 KiB CRC.
+__device__ __forceinline__ uint32_t crc_warp(const uint32_t* N, uint32_t v) {
+    const int lane = threadIdx.x & 31;
+    v = crc_mul_nib(N, v, lane & 7);
+    v ^= __shfl_down_sync(0xffffffffu, v, 1);
+    v ^= __shfl_down_sync(0xffffffffu, v, 2);
+    v ^= __shfl_down_sync(0xffffffffu, v, 4);
+    return crc_tree(N, v, 8, 2, 8);
 }
 
 struct E1Smem {
     uint32_t* freq;   // B*NS, per tensor
     uint32_t* crc;    // kCrcTabs*256
-    uint32_t* nib;    // 8*8*16
+    uint32_t* nib;    // kNibConsts*8*16
     uint32_t* wcnt;   // 8*B: per-warp key counts -> per-warp key bases
     uint16_t* cc;     // 8*kChunks*B: per-chunk key counts -> prefix over chunks
     uint32_t* part;   // 8 warp CRCs
@@ -178,7 +193,7 @@ struct E1Smem {
 
 __host__ __device__ inline size_t e1_smem_bytes(uint32_t B, uint32_t NS) {
     return (((size_t)B * NS * 4 + 15) & ~(size_t)15) + (size_t)kCrcTabs * 256 * 4 +
-           (size_t)8 * 8 * 16 * 4 + (((size_t)8 * B * 4 + 15) & ~(size_t)15) +
+           (size_t)kNibConsts * 8 * 16 * 4 + (((size_t)8 * B * 4 + 15) & ~(size_t)15) +
            (((size_t)8 * kChunks * B * 2 + 15) & ~(size_t)15) + 32 + kTile / 8 +
            (2 * (size_t)kTile + 16) + (kTile + 32);
 }
@@ -188,7 +203,7 @@ __device__ inline E1Smem e1_carve(uint8_t* base, uint32_t B, uint32_t NS) {
     size_t o = 0;
     S.freq = (uint32_t*)(base + o); o += ((size_t)B * NS * 4 + 15) & ~(size_t)15;
     S.crc = (uint32_t*)(base + o);  o += (size_t)kCrcTabs * 256 * 4;
-    S.nib = (uint32_t*)(base + o);  o += (size_t)8 * 8 * 16 * 4;
+    S.nib = (uint32_t*)(base + o);  o += (size_t)kNibConsts * 8 * 16 * 4;
     S.wcnt = (uint32_t*)(base + o); o += ((size_t)8 * B * 4 + 15) & ~(size_t)15;
     S.cc = (uint16_t*)(base + o);   o += ((size_t)8 * kChunks * B * 2 + 15) & ~(size_t)15;
     S.part = (uint32_t*)(base + o); o += 32;
@@ -220,7 +235,7 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
     const uint32_t Brep = B * 0x01010101u;
 
     for (uint32_t i = tid; i < kCrcTabs * 256; i += kCB) S.crc[i] = (&g_crc_slice[0][0])[i];
-    for (uint32_t i = tid; i < 8 * 8 * 16; i += kCB) S.nib[i] = (&g_crc_nib[0][0][0])[i];
+    for (uint32_t i = tid; i < kNibConsts * 8 * 16; i += kCB) S.nib[i] = (&g_crc_nib[0][0][0])[i];
     for (uint32_t i = tid; i < B * NS; i += kCB) S.freq[i] = 0;
     if (tid < 16) S.sd[tid - 16] = 0;
     __shared__ int s_base;
@@ -329,7 +344,7 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
             uint32_t r = 0;
             if (nv) r = crc_block8(S.crc, crc_block8(S.crc, 0u, c0, c1), c2, c3);
             if (cnt == kTile) {
-                r = crc_tree(S.nib, r, 0, 5);  // lane 0: CRC of the warp's 1 KiB
+                r = crc_warp(S.nib, r);  // lane 0: CRC of the warp's 1 KiB
                 if (lane == 0) S.part[wid] = r;
             } else {  // ragged tile: shift by the bytes after this chunk inside the tile
                 if (r) r = crc_shift(c_crc_x2n, r, 2ull * (cnt - (e0 + nv)));
@@ -340,7 +355,7 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
         __syncthreads();
 
         // ---- M: rank inside the chunk (match), per-chunk key counts
-        uint32_t pk[kIt];  // rank-in-chunk | key << 12 | d << 18 | valid << 24
+        uint32_t pk[kIt];  // rank-in-chunk | key << 8 | d << 16 (key 0xff: no element)
         uint16_t* cc = S.cc + wid * kChunks * B;
         {
 #pragma unroll
@@ -351,8 +366,7 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
                 const bool valid = key != 0xffu;
                 const uint32_t peers = __match_any_sync(0xffffffffu, key);
                 if (valid && (peers & lt_mask) == 0) cc[j * B + key] = (uint16_t)__popc(peers);
-                pk[j] = valid ? (__popc(peers & lt_mask) | (key << 12) | ((kdv >> 8) << 18) | (1u << 24))
-                              : 0u;
+                pk[j] = __popc(peers & lt_mask) | (kdv << 8);  // rank | key << 8 | d << 16
             }
         }
         __syncwarp();
@@ -380,7 +394,7 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
         }
         if (wid == kCB / 32 - 1) {  // tile CRC (moved to its stream position by crc_tiles_kernel)
             uint32_t r = lane < kCB / 32 ? S.part[lane] : 0u;
-            if (cnt == kTile) r = crc_tree(S.nib, r, 5, 3);  // warps: 1 KiB chunks
+            if (cnt == kTile) r = crc_tree(S.nib, r, 10, 3);  // warps: 1 KiB chunks
             else r = warp_xor(r);                              // ragged: already at the tile end
             if (lane == 0) A.tile_crc[ti] = r;
         }
@@ -412,10 +426,8 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
 #pragma unroll
             for (int j = 0; j < kIt; ++j) {
                 const uint32_t q = pk[j];
-                if (q >> 24) {
-                    const uint32_t key = (q >> 12) & 63u;
-                    S.sd[s_start[key] + wb[key] + cc[j * B + key] + (q & 4095u)] = (uint8_t)((q >> 18) & 63u);
-                }
+                const uint32_t key = (q >> 8) & 0xffu;
+                if (key != 0xffu) S.sd[s_start[key] + wb[key] + cc[j * B + key] + (q & 31u)] = (uint8_t)(q >> 16);
             }
         }
         __syncthreads();
@@ -493,11 +505,11 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
 __global__ void __launch_bounds__(kCB) level_crc_tile_kernel(const Tile* tiles, const uint16_t* levels,
                                                              uint32_t* tile_crc) {
     __shared__ uint32_t s_crc[kCrcTabs * 256];
-    __shared__ uint32_t s_nib[8 * 8 * 16];
+    __shared__ uint32_t s_nib[kNibConsts * 8 * 16];
     __shared__ uint32_t s_part[kCB / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     for (uint32_t i = tid; i < kCrcTabs * 256; i += kCB) s_crc[i] = (&g_crc_slice[0][0])[i];
-    for (uint32_t i = tid; i < 8 * 8 * 16; i += kCB) s_nib[i] = (&g_crc_nib[0][0][0])[i];
+    for (uint32_t i = tid; i < kNibConsts * 8 * 16; i += kCB) s_nib[i] = (&g_crc_nib[0][0][0])[i];
     __syncthreads();
     const Tile T = tiles[blockIdx.x];
     const uint32_t cnt = T.count, e0 = tid * kIt;
@@ -529,7 +541,7 @@ __global__ void __launch_bounds__(kCB) level_crc_tile_kernel(const Tile* tiles, 
     uint32_t r = 0;
     if (nv) r = crc_block8(s_crc, crc_block8(s_crc, 0u, c0, c1), c2, c3);
     if (cnt == kTile) {
-        r = crc_tree(s_nib, r, 0, 5);
+        r = crc_warp(s_nib, r);
         if (lane == 0) s_part[wid] = r;
     } else {
         if (r) r = crc_shift(c_crc_x2n, r, 2ull * (cnt - (e0 + nv)));
@@ -539,7 +551,7 @@ __global__ void __launch_bounds__(kCB) level_crc_tile_kernel(const Tile* tiles, 
     __syncthreads();
     if (wid == 0) {
         uint32_t v = lane < kCB / 32 ? s_part[lane] : 0u;
-        if (cnt == kTile) v = crc_tree(s_nib, v, 5, 3);
+        if (cnt == kTile) v = crc_tree(s_nib, v, 10, 3);
         else v = warp_xor(v);
         if (lane == 0) tile_crc[blockIdx.x] = v;
     }
@@ -1488,12 +1500,13 @@ static void init_crc_consts() {
     static uint32_t sl[kCrcTabs][256];
     for (int i = 0; i < kCrcTabs; ++i) memcpy(sl[i], tn[pick[i]], sizeof(sl[i]));
     DQTG_CUDA(cudaMemcpyToSymbol(g_crc_slice, sl, sizeof(sl)));
-    static uint32_t nib[8][8][16];
-    for (int lv = 0; lv < 8; ++lv) {
-        const uint64_t m = lv < 5 ? (uint64_t)32 << lv : (uint64_t)1024 << (lv - 5);
+    static uint32_t nib[kNibConsts][8][16];
+    for (int lv = 0; lv < kNibConsts; ++lv) {
+        const uint64_t m = lv < 8 ? (uint64_t)32 * (7 - lv)
+                                  : (lv < 10 ? (uint64_t)256 << (lv - 8) : (uint64_t)1024 << (lv - 10));
         const uint32_t k = crc_x2nmodp(x.t, m, 3);
         for (int i = 0; i < 8; ++i)
-            for (uint32_t n = 0; n < 16; ++n) nib[lv][i][n] = crc_multmodp(k, n << (4 * i));
+            for (uint32_t n = 0; n < 16; ++n) nib[lv][i][n] = m ? crc_multmodp(k, n << (4 * i)) : (n << (4 * i));
     }
     DQTG_CUDA(cudaMemcpyToSymbol(g_crc_nib, nib, sizeof(nib)));
     DQTG_CUDA(cudaMemcpyToSymbol(c_crc_x2n, x.t, sizeof(x.t)));

@@ -1,4 +1,14 @@
+# GPU round trip used during development: gpu tests, then one bench run, compact output
 set -o pipefail
-nvidia-smi -L
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -8
-timeout 400 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; cat gpurun_out/bench.json | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('value',d['value'],'ms',d['ms_per_step'],'seq',d['config']['ms_per_step_sequential'],'e2e',d['e2e']['value']); print(d['roofline']['kernels_ms_per_step'])"; tail -3 gpurun_out/bench.err
+T=$(timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -1)
+echo "TESTS: $T"
+timeout 600 python bench.py --no-cpu-baseline "$@" > gpurun_out/bench.json 2> gpurun_out/bench.err || tail -5 gpurun_out/bench.err
+python - <<'PY'
+import json
+d = json.load(open("gpurun_out/bench.json"))
+k = d["roofline"]["kernels_ms_per_step"]
+print("BENCH: value %.1f GB/s  %.3f ms/step  e2e %.1f  restore %s" % (
+    d["value"], d["ms_per_step"], d["e2e"]["value"],
+    None if not d.get("restore") else round(d["restore"]["value"], 1)))
+print("KERNELS:", ", ".join("%s %.3f" % (n.replace("_kernel", ""), v) for n, v in list(k.items())[:12]))
+PY
