@@ -876,7 +876,14 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
                                                           unsigned long long* code_ov,
                                                           uint8_t* len_ov, HufWork W,
                                                           uint32_t n_pad) {
+    // working set in shared memory (the tree build is a serial chain): n_pad >= n
     extern __shared__ unsigned long long s_keys[];  // n_pad
+    unsigned long long* f = s_keys + n_pad;          // n_pad
+    unsigned long long* nodef = f + n_pad;           // 2 n_pad
+    long long* sym = (long long*)(nodef + 2 * n_pad);  // n_pad
+    uint32_t* perm = (uint32_t*)(sym + n_pad);       // n_pad
+    uint32_t* parent = perm + n_pad;                 // 2 n_pad
+    uint32_t* depth = parent + 2 * n_pad;            // 2 n_pad
     const uint32_t B = A.B, NS = A.NS;
     const uint32_t tb = blockIdx.x, b = tb % B;
     GroupInfo G{};
@@ -886,37 +893,42 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
     G.ov_end = lb_u64(ukey, nu, (unsigned long long)(tb + 1) << 32);
     const uint32_t nov = (uint32_t)(G.ov_end - G.ov_begin);
     G.tab_base = (unsigned long long)tb * NS + G.ov_begin;
-    long long* sym = W.sym + G.tab_base;
-    unsigned long long* f = W.f + G.tab_base;
-    uint32_t* perm = W.perm + G.tab_base;
-    unsigned long long* nodef = W.nodef + 2 * G.tab_base + 2ull * tb;
-    uint32_t* parent = W.parent + 2 * G.tab_base + 2ull * tb;
-    uint32_t* depth = W.depth + 2 * G.tab_base + 2ull * tb;
-    (void)nov;
-    __shared__ uint32_t s_n;
+    (void)W;
+    // symbols in ascending order (the reference's std::map): values -(B-1)..0, dense
+    // run lengths 2..63, overflow lengths; compacted warp-wide with ballots
     const uint32_t* fr = A.freq + (size_t)tb * NS;
-    if (threadIdx.x == 0) {
-        uint32_t n = 0;
-        if (G.n_elems) {
-            for (int v = (int)B - 1; v >= 0; --v)  // symbols -(B-1) .. 0 ascending
-                if (fr[v]) {
-                    sym[n] = -(long long)v;
-                    f[n++] = fr[v];
-                }
-            for (uint32_t L = 2; L < (uint32_t)kLD; ++L)
-                if (fr[B + L]) {
-                    sym[n] = (long long)L;
-                    f[n++] = fr[B + L];
-                }
-            for (unsigned long long j = G.ov_begin; j < G.ov_end; ++j) {
-                sym[n] = (long long)(ukey[j] & 0xffffffffull);
-                f[n++] = ucnt[j];
+    const int lane = threadIdx.x;
+    uint32_t n = 0;
+    if (G.n_elems) {
+        for (uint32_t i0 = 0; i0 < B + kLD; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            long long sv = 0;
+            unsigned long long fv = 0;
+            if (i < B) {  // value -(B-1-i)
+                fv = fr[B - 1 - i];
+                sv = -(long long)(B - 1 - i);
+            } else if (i < B + kLD && i - B >= 2) {
+                fv = fr[i];
+                sv = (long long)(i - B);
             }
+            const uint32_t m = __ballot_sync(0xffffffffu, fv != 0);
+            if (fv) {
+                const uint32_t o = n + __popc(m & ((1u << lane) - 1u));
+                sym[o] = sv;
+                f[o] = fv;
+            }
+            n += __popc(m);
         }
-        s_n = n;
+        for (unsigned long long j0 = G.ov_begin; j0 < G.ov_end; j0 += 32) {
+            const unsigned long long j = j0 + lane;
+            if (j < G.ov_end) {
+                sym[n + lane] = (long long)(ukey[j] & 0xffffffffull);
+                f[n + lane] = ucnt[j];
+            }
+            n += (uint32_t)min(32ull, G.ov_end - j0);
+        }
     }
-    __syncthreads();
-    const uint32_t n = s_n;
+    __syncwarp();
     if (n == 0) {
         if (threadIdx.x == 0) gi[tb] = G;
         return;
@@ -944,7 +956,6 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
         }
     for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) perm[r] = (uint32_t)(s_keys[r] & 0xffffffu);
     __syncthreads();
-    (void)n_pad;
     if (threadIdx.x == 0) {
         unsigned long long nsyms = 0;
         for (uint32_t i = 0; i < n; ++i) nsyms += f[i];
@@ -1728,7 +1739,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
         e.sync();
         uint32_t np2 = 1;
         while (np2 < NS + h_max) np2 <<= 1;
-        const size_t hsm = (size_t)np2 * 8;
+        const size_t hsm = (size_t)np2 * 60;  // keys, f, nodef, sym, perm, parent, depth
         DQTG_REQUIRE(hsm <= 200 * 1024, DQTG_ERROR,
                      "too many distinct run lengths in one group for the device Huffman stage");
         HufWork W;
