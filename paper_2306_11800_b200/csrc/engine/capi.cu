@@ -77,7 +77,8 @@ void init_engine(Engine& e, int device, void* stream) {
     DQTG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t keep = ~0ull;
     DQTG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-    DQTG_CUDA(cudaMemset(e.d_err, 0, 16));
+    DQTG_CUDA(cudaMemsetAsync(e.d_err, 0, 16, e.stream));
+    DQTG_CUDA(cudaStreamSynchronize(e.stream));
 }
 }  // namespace dqtg
 
@@ -225,7 +226,9 @@ dqtg_status dqtg_ckpt_create(dqtg_engine* h, const dqtg_layout* layout, dqtg_ckp
             c->c.eng = &h->e;
             c->c.L = make_layout(&h->e, layout);
             DQTG_CUDA(cudaMalloc(&c->c.w, c->c.L->Np * 4));
-            DQTG_CUDA(cudaMemset(c->c.w, 0, c->c.L->Np * 4));
+            // on the engine stream: a legacy-stream memset is not ordered with the
+            // (non-blocking) engine stream's uploads
+            DQTG_CUDA(cudaMemsetAsync(c->c.w, 0, c->c.L->Np * 4, h->e.stream));
         } catch (...) {
             delete c;
             throw;
@@ -249,10 +252,10 @@ dqtg_status dqtg_ckpt_set_weights(dqtg_ckpt* c, const float* const* t) {
     });
 }
 
-static float* alloc_padded(const Layout& L) {
+static float* alloc_padded(Engine& e, const Layout& L) {
     float* p = nullptr;
     DQTG_CUDA(cudaMalloc(&p, L.Np * 4));
-    DQTG_CUDA(cudaMemset(p, 0, L.Np * 4));
+    DQTG_CUDA(cudaMemsetAsync(p, 0, L.Np * 4, e.stream));  // ordered before the uploads
     return p;
 }
 
@@ -260,10 +263,10 @@ dqtg_status dqtg_ckpt_set_scores(dqtg_ckpt* c, const float* const* mag, const fl
     return guard([&] {
         LOCK(c->c.eng);
         DevCkpt& d = c->c;
-        if (!d.mag) d.mag = alloc_padded(*d.L);
+        if (!d.mag) d.mag = alloc_padded(*d.eng, *d.L);
         upload_tensors(*d.eng, *d.L, d.mag, mag);
         if (sens) {
-            if (!d.sens) d.sens = alloc_padded(*d.L);
+            if (!d.sens) d.sens = alloc_padded(*d.eng, *d.L);
             upload_tensors(*d.eng, *d.L, d.sens, sens);
         }
         d.explicit_scores = true;
@@ -278,7 +281,7 @@ dqtg_status dqtg_ckpt_set_ema(dqtg_ckpt* c, const float* const* ema) {
         DevCkpt& d = c->c;
         d.explicit_scores = false;
         if (ema) {
-            if (!d.ema) d.ema = alloc_padded(*d.L);
+            if (!d.ema) d.ema = alloc_padded(*d.eng, *d.L);
             upload_tensors(*d.eng, *d.L, d.ema, ema);
             d.has_sens = true;
             d.ema_seeded = true;
@@ -294,7 +297,7 @@ dqtg_status dqtg_ckpt_update_ema(dqtg_ckpt* c, const float* const* grads, double
         LOCK(c->c.eng);
         DevCkpt& d = c->c;
         Engine& e = *d.eng;
-        if (!d.ema) d.ema = alloc_padded(*d.L);
+        if (!d.ema) d.ema = alloc_padded(*d.eng, *d.L);
         if (!d.ema_seeded) {  // first snapshot seeds the average (ranker.cpp:22-23)
             upload_tensors(e, *d.L, d.ema, grads);
             d.ema_seeded = true;
@@ -313,7 +316,7 @@ uint64_t dqtg_ckpt_param_count(const dqtg_ckpt* c) { return c->c.L->N; }
 float* dqtg_ckpt_weights_dev(dqtg_ckpt* c) { return c->c.w; }
 float* dqtg_ckpt_ema_dev(dqtg_ckpt* c) {
     if (!c->c.ema) {
-        c->c.ema = alloc_padded(*c->c.L);
+        c->c.ema = alloc_padded(*c->c.eng, *c->c.L);
         c->c.has_sens = true;
         c->c.ema_seeded = true;
         c->c.explicit_scores = false;

@@ -855,12 +855,15 @@ struct HufWork {
 };
 
 __global__ void ov_group_max_kernel(const unsigned long long* ukey, const unsigned long long* nu_p,
-                                    uint32_t ngroups, uint32_t* max_nov) {
+                                    uint32_t ngroups, uint32_t* max_nov,
+                                    unsigned long long* ov_range /*[ngroups][2]*/) {
     const unsigned long long nu = *nu_p;
     for (uint32_t tb = blockIdx.x * blockDim.x + threadIdx.x; tb < ngroups;
          tb += gridDim.x * blockDim.x) {
         unsigned long long a = lb_u64(ukey, nu, (unsigned long long)tb << 32);
         unsigned long long b = lb_u64(ukey, nu, (unsigned long long)(tb + 1) << 32);
+        ov_range[2 * tb] = a;
+        ov_range[2 * tb + 1] = b;
         if (b > a) atomicMax(max_nov, (uint32_t)(b - a));
     }
 }
@@ -875,9 +878,11 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
                                                           uint8_t* len_dense,
                                                           unsigned long long* code_ov,
                                                           uint8_t* len_ov, HufWork W,
-                                                          uint32_t n_pad) {
+                                                          uint32_t n_pad,
+                                                          const unsigned long long* ov_range) {
     // working set in shared memory (the tree build is a serial chain): n_pad >= n
     extern __shared__ unsigned long long s_keys[];  // n_pad
+    __shared__ uint32_t s_hist[65], s_at[65];
     unsigned long long* f = s_keys + n_pad;          // n_pad
     unsigned long long* nodef = f + n_pad;           // 2 n_pad
     long long* sym = (long long*)(nodef + 2 * n_pad);  // n_pad
@@ -888,9 +893,9 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
     const uint32_t tb = blockIdx.x, b = tb % B;
     GroupInfo G{};
     G.n_elems = elems[tb];
-    const unsigned long long nu = *nu_p;
-    G.ov_begin = lb_u64(ukey, nu, (unsigned long long)tb << 32);
-    G.ov_end = lb_u64(ukey, nu, (unsigned long long)(tb + 1) << 32);
+    (void)nu_p;
+    G.ov_begin = ov_range[2 * tb];
+    G.ov_end = ov_range[2 * tb + 1];
     const uint32_t nov = (uint32_t)(G.ov_end - G.ov_begin);
     G.tab_base = (unsigned long long)tb * NS + G.ov_begin;
     (void)W;
@@ -992,10 +997,11 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
             if (overflow) atomicOr(A.err, kErrHuffmanDepth);
         }
         // table sorted by (len, sym): counting sort over lengths, stable in sym order
-        uint32_t hist[65];
+        uint32_t* hist = s_hist;
+        uint32_t* at = s_at;
         for (int l = 0; l < 65; ++l) hist[l] = 0;
         for (uint32_t i = 0; i < n; ++i) hist[depth[i] < 64 ? depth[i] : 64]++;
-        uint32_t at[65], acc = 0;
+        uint32_t acc = 0;
         for (int l = 0; l < 65; ++l) {
             at[l] = acc;
             acc += hist[l];
@@ -1729,10 +1735,13 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     auto* len_ov = (uint8_t*)e.buf("e.lov", n_ov + 8);
     {
         auto* max_nov = (uint32_t*)(small + 4);
+        auto* ov_range = (unsigned long long*)e.buf("e.ovrange", (size_t)nt * B * 16 + 16);
         DQTG_CUDA(cudaMemsetAsync(max_nov, 0, 4, st));
         if (n_unique) {
-            { DQTG_SPAN(e, "ov_group_max_kernel"); ov_group_max_kernel<<<64, 256, 0, st>>>(ukey, nu, nt * B, max_nov); }
+            { DQTG_SPAN(e, "ov_group_max_kernel"); ov_group_max_kernel<<<(nt * B + 255) / 256, 256, 0, st>>>(ukey, nu, nt * B, max_nov, ov_range); }
             e.launched();
+        } else {
+            DQTG_CUDA(cudaMemsetAsync(ov_range, 0, (size_t)nt * B * 16, st));
         }
         uint32_t h_max = 0;
         e.d2h(&h_max, max_nov, 4);
@@ -1754,7 +1763,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
         if (hsm > 48 * 1024)
             ensure_dyn_smem((const void*)enc_huffman_kernel, hsm);
         { DQTG_SPAN(e, "enc_huffman_kernel"); enc_huffman_kernel<<<nt * B, 32, hsm, st>>>(A, elems, ukey, ucnt, nu, gi, tab_sym, tab_len,
-                                                     code_dense, len_dense, code_ov, len_ov, W, np2); }
+                                                     code_dense, len_dense, code_ov, len_ov, W, np2, ov_range); }
         e.launched();
     }
     CodeTabs C{code_dense, len_dense, ukey, code_ov, len_ov, gi};

@@ -1,5 +1,6 @@
 // Engine plumbing: device/stream, scratch, alpha tables, layouts, object lifetimes.
 #include <algorithm>
+#include <cstdlib>
 #include <float.h>
 #include <math.h>
 #include <string.h>
@@ -99,6 +100,16 @@ void* Engine::buf(const std::string& name, size_t bytes) {
     if (slot.second < bytes) {
         // stream-ordered: scratch is only touched by this engine's stream, so the
         // old block is released after its last use without a device-wide sync
+        if (getenv("DQTG_SYNC_BUF")) {  // debug: synchronous growth
+            if (slot.first) {
+                DQTG_CUDA(cudaStreamSynchronize(stream));
+                DQTG_CUDA(cudaFree(slot.first));
+            }
+            size_t cap = bytes < 256 ? 256 : bytes + bytes / 4;
+            DQTG_CUDA(cudaMalloc(&slot.first, cap));
+            slot.second = cap;
+            return slot.first;
+        }
         if (slot.first) DQTG_CUDA(cudaFreeAsync(slot.first, stream));
         size_t cap = bytes < 256 ? 256 : bytes + bytes / 4;
         DQTG_CUDA(cudaMallocAsync(&slot.first, cap, stream));
@@ -331,6 +342,9 @@ AlphaTables& Engine::alpha_tables(double alpha) {
     DQTG_CUDA(cudaMemcpy(t->d_U, U.data(), U.size() * 4, cudaMemcpyHostToDevice));
     DQTG_CUDA(cudaMemcpy(t->d_key, t->h_key.data(), t->h_key.size() * 8, cudaMemcpyHostToDevice));
     DQTG_CUDA(cudaMemcpy(t->d_keyf, keyf.data(), keyf.size() * 4, cudaMemcpyHostToDevice));
+    // pageable H2D copies may return before their DMA lands, on the legacy stream
+    // that the (non-blocking) engine streams do not wait for
+    DQTG_CUDA(cudaStreamSynchronize(0));
     auto& ref = *t;
     tables[key] = std::move(t);
     return ref;
@@ -372,6 +386,7 @@ static T* upload_vec(const std::vector<T>& v) {
     size_t bytes = (v.size() ? v.size() : 1) * sizeof(T);
     DQTG_CUDA(cudaMalloc(&d, bytes));
     if (!v.empty()) DQTG_CUDA(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    DQTG_CUDA(cudaStreamSynchronize(0));  // see alpha_tables: the DMA may still be in flight
     return d;
 }
 

@@ -79,14 +79,16 @@ struct KShared {
 
 // Explicit shared-memory accesses for the serial chains (generic loads add latency).
 __device__ __forceinline__ unsigned sh_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+// volatile + memory clobber: the loads must not move across __syncthreads() or the
+// stores that produced the data (a plain asm is a pure function to the compiler)
 __device__ __forceinline__ double ld_sh(const double* p) {
     double v;
-    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(sh_addr(p)));
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(sh_addr(p)) : "memory");
     return v;
 }
 __device__ __forceinline__ double2 ld_sh2(const double2* p) {
     double2 v;
-    asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(sh_addr(p)));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(sh_addr(p)) : "memory");
     return v;
 }
 __device__ __forceinline__ void st_sh(double* p, double v) {
@@ -597,7 +599,7 @@ void run_kmeans(Engine& e, std::vector<KProblem>& probs, float* cb_out, int cb_s
     size_t smem = head + (size_t)std::min(maxn, smem_n) * 60 + 96;
     ensure_dyn_smem((const void*)kmeans_restarts_kernel, smem);
     // restarts on the engine's high-priority side stream (fork/join with events)
-    if (e.profiling) {
+    if (e.profiling || getenv("DQTG_NO_HI")) {
         DQTG_SPAN(e, "kmeans_restarts_kernel");
         kmeans_restarts_kernel<<<(unsigned)(probs.size() * restarts), kKB, smem, e.stream>>>(dp, restarts, smem_n);
     } else {

@@ -125,14 +125,14 @@ dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* 
                 c->eng = &e;
                 c->L = make_layout(&e, layout);
                 DQTG_CUDA(cudaMalloc(&c->w, c->L->Np * 4));
-                DQTG_CUDA(cudaMemset(c->w, 0, c->L->Np * 4));
+                DQTG_CUDA(cudaMemsetAsync(c->w, 0, c->L->Np * 4, e.stream));
             }
             c->explicit_scores = false;
             c->has_sens = ema != nullptr;
             if (ema) {
                 if (!c->ema) {
                     DQTG_CUDA(cudaMalloc(&c->ema, c->L->Np * 4));
-                    DQTG_CUDA(cudaMemset(c->ema, 0, c->L->Np * 4));
+                    DQTG_CUDA(cudaMemsetAsync(c->ema, 0, c->L->Np * 4, e.stream));
                 }
                 upload(e, *c->L, c->ema, ema);
                 c->ema_seeded = true;

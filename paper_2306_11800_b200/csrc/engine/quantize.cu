@@ -192,7 +192,8 @@ __global__ void __launch_bounds__(kPB, 6) pass_b_kernel(PassIn a, const LtParams
                                                      uint32_t* tile_prot,
                                                      unsigned long long* tensor_prot) {
     extern __shared__ uint32_t sh[];
-    __shared__ uint32_t s_red[kPB / 32];
+    __shared__ uint32_t s_red[2][kPB / 32];  // by tile parity: warps may run ahead into the next tile
+    uint32_t par = 0;
     hist_clear(sh);
     __syncthreads();
     __shared__ int s_base;
@@ -240,14 +241,15 @@ __global__ void __launch_bounds__(kPB, 6) pass_b_kernel(PassIn a, const LtParams
             }
         }
         np = warp_sum(np);
-        if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = np;
+        if ((threadIdx.x & 31) == 0) s_red[par][threadIdx.x >> 5] = np;
         __syncthreads();
         if (threadIdx.x == 0) {
             uint32_t t = 0;
-            for (int wi = 0; wi < kPB / 32; ++wi) t += s_red[wi];
+            for (int wi = 0; wi < kPB / 32; ++wi) t += s_red[par][wi];
             tile_prot[ti] = t;
             if (t) atomicAdd(tensor_prot + T.tensor, (unsigned long long)t);
         }
+        par ^= 1u;
     }
     __syncthreads();
     if (cur >= 0) hist_flush(sh, gh_val + cur * a.HS, a.tab);
