@@ -72,11 +72,18 @@ void init_engine(Engine& e, int device, void* stream) {
         e.own_stream = true;
     }
     DQTG_CUDA(cudaMalloc(&e.d_err, 16));
-    // keep freed pool memory cached: per-step states/records reuse it
-    cudaMemPool_t pool;
-    DQTG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    // a private stream-ordered pool per engine; freed memory stays cached (per-step
+    // states/records reuse it) and is never handed to another engine's stream (the
+    // default pool's cross-stream reuse inserts waits on other engines' streams)
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    DQTG_CUDA(cudaMemPoolCreate(&e.pool, &props));
     uint64_t keep = ~0ull;
-    DQTG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    DQTG_CUDA(cudaMemPoolSetAttribute(e.pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    int no = 0;
+    DQTG_CUDA(cudaMemPoolSetAttribute(e.pool, cudaMemPoolReuseAllowInternalDependencies, &no));
     DQTG_CUDA(cudaMemsetAsync(e.d_err, 0, 16, e.stream));
     DQTG_CUDA(cudaStreamSynchronize(e.stream));
 }

@@ -73,6 +73,7 @@ void dump_timeline(Engine& e) {
 
 Engine::~Engine() {
     cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
     if (hi_stream) {
         cudaStreamSynchronize(hi_stream);
         cudaStreamDestroy(hi_stream);
@@ -93,6 +94,7 @@ Engine::~Engine() {
     if (pinned) cudaFreeHost(pinned);
     for (auto& b : stage_blocks) cudaFreeHost(b.first);
     if (own_stream && stream) cudaStreamDestroy(stream);
+    if (pool) cudaMemPoolDestroy(pool);  // blocks still owned by live states keep it alive
 }
 
 void* Engine::buf(const std::string& name, size_t bytes) {
@@ -112,7 +114,7 @@ void* Engine::buf(const std::string& name, size_t bytes) {
         }
         if (slot.first) DQTG_CUDA(cudaFreeAsync(slot.first, stream));
         size_t cap = bytes < 256 ? 256 : bytes + bytes / 4;
-        DQTG_CUDA(cudaMallocAsync(&slot.first, cap, stream));
+        DQTG_CUDA(cudaMallocFromPoolAsync(&slot.first, cap, pool, stream));
         slot.second = cap;
     }
     return slot.first;
@@ -120,7 +122,7 @@ void* Engine::buf(const std::string& name, size_t bytes) {
 
 void* Engine::dalloc(size_t bytes) {
     void* p = nullptr;
-    DQTG_CUDA(cudaMallocAsync(&p, bytes ? bytes : 16, stream));
+    DQTG_CUDA(cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, pool, stream));
     return p;
 }
 

@@ -129,6 +129,9 @@ struct Engine {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    // the engine's own stream-ordered pool: blocks freed by this engine are reused
+    // by it alone, so engines on other streams never wait on this stream's work
+    cudaMemPool_t pool = nullptr;
     // high-priority side stream for latency-critical few-CTA phases (k-means):
     // its CTAs are scheduled ahead of other streams' streaming passes
     cudaStream_t hi_stream = nullptr;

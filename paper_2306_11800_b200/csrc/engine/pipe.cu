@@ -14,7 +14,9 @@
 // While one worker blocks on a host read-back (record size, overflow counts) or
 // a copy, the others keep the GPU fed, and the few-CTA phases (k-means restarts,
 // per-group Huffman) overlap the streaming passes of the other workers.
+#include <chrono>
 #include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <thread>
@@ -146,6 +148,12 @@ dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* 
             if (tl) timeline_epoch(*e);
         }
         Run R;
+        const bool trace = getenv("DQTG_PIPE_TRACE") != nullptr;
+        const auto t_start = std::chrono::steady_clock::now();
+        std::vector<double> t_q(n, 0.0), t_e(n, 0.0);
+        auto now_ms = [&] {
+            return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+        };
         R.states.resize(n);
         R.qev.assign(n, nullptr);
         R.ready.assign(n, 0);
@@ -167,6 +175,7 @@ dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* 
                     }
                     upload(e, *c.L, c.w, weights + k * nt);
                     auto q = quantize(e, c, *cfg, seed, steps ? steps[k] : k);
+                    if (trace) t_q[k] = now_ms();
                     DQTG_CUDA(cudaEventRecord(R.qev[k], e.stream));
                     const QState* target = q.get();
                     const QState* prev = base ? base->q.get() : nullptr;
@@ -187,6 +196,7 @@ dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* 
                     if (on_record) on_record(user, k, &rec);
                     rec.r.reset();
                     e.sync();  // encode(k) complete: its inputs may be released
+                    if (trace) t_e[k] = now_ms();
                     std::lock_guard<std::mutex> g(R.mu);
                     release(k);
                     if (k > 0) release(k - 1);
@@ -201,6 +211,10 @@ dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* 
         for (int w = 0; w < W; ++w) th.emplace_back(worker, w);
         for (auto& t : th) t.join();
         for (auto ev : R.qev) cudaEventDestroy(ev);
+        if (trace)
+            for (uint64_t k = 0; k < n; ++k)
+                fprintf(stderr, "pipe k=%llu worker=%d quantized %.3f encoded %.3f ms\n",
+                        (unsigned long long)k, (int)(k % W), t_q[k], t_e[k]);
         if (tl)
             for (auto& e : p->eng) {
                 e->sync();
