@@ -150,7 +150,7 @@ dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* 
         Run R;
         const bool trace = getenv("DQTG_PIPE_TRACE") != nullptr;
         const auto t_start = std::chrono::steady_clock::now();
-        std::vector<double> t_q(n, 0.0), t_e(n, 0.0);
+        std::vector<double> t_q(n, 0.0), t_e(n, 0.0), t_u(n, 0.0), t_w(n, 0.0), t_c(n, 0.0), t_0(n, 0.0);
         auto now_ms = [&] {
             return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
         };
@@ -173,7 +173,9 @@ dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* 
                         std::lock_guard<std::mutex> g(R.mu);
                         if (R.failed) return;
                     }
+                    if (trace) t_0[k] = now_ms();
                     upload(e, *c.L, c.w, weights + k * nt);
+                    if (trace) t_u[k] = now_ms();
                     auto q = quantize(e, c, *cfg, seed, steps ? steps[k] : k);
                     if (trace) t_q[k] = now_ms();
                     DQTG_CUDA(cudaEventRecord(R.qev[k], e.stream));
@@ -191,8 +193,10 @@ dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* 
                         }
                     }
                     if (k > 0) DQTG_CUDA(cudaStreamWaitEvent(e.stream, R.qev[k - 1], 0));
+                    if (trace) t_w[k] = now_ms();
                     dqtg_record rec;
                     rec.r = encode_record(e, prev, *target, quality);
+                    if (trace) t_c[k] = now_ms();
                     if (on_record) on_record(user, k, &rec);
                     rec.r.reset();
                     e.sync();  // encode(k) complete: its inputs may be released
@@ -213,8 +217,8 @@ dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* 
         for (auto ev : R.qev) cudaEventDestroy(ev);
         if (trace)
             for (uint64_t k = 0; k < n; ++k)
-                fprintf(stderr, "pipe k=%llu worker=%d quantized %.3f encoded %.3f ms\n",
-                        (unsigned long long)k, (int)(k % W), t_q[k], t_e[k]);
+                fprintf(stderr, "pipe k=%llu worker=%d start %.3f uploaded %.3f quantized %.3f waited %.3f encode-call %.3f encoded %.3f ms\n",
+                        (unsigned long long)k, (int)(k % W), t_0[k], t_u[k], t_q[k], t_w[k], t_c[k], t_e[k]);
         if (tl)
             for (auto& e : p->eng) {
                 e->sync();

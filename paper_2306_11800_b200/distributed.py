@@ -142,3 +142,40 @@ def compress_sharded(engine, ckpt, cfg, seed, step, base_state, *, group=None, d
                                   [p[1] for p in parts], [p[2] for p in parts])
     E.LIB.dqtg_record_destroy(rec)
     return state, out, stats
+
+
+def assign_configs(m, world):
+    """Round-robin split of m candidate configs over the ranks (config i on rank
+    i mod world): neighbouring configs of a guided-search batch (search.cpp:247-296,
+    387-482) have similar cost, so round-robin balances the ranks."""
+    return [list(range(r, m, world)) for r in range(world)]
+
+
+def eval_batch_sharded(evaluate, cfgs, seeds, *, group=None):
+    """Batched candidate evaluation (EvalCache::prefetch, search.cpp:174-204) spread
+    over the ranks of one box: each rank evaluates its share with its own engine
+    (``evaluate(cfgs, seeds) -> (quality[], est[])``, e.g. ``Engine.eval_batch``
+    bound to the rank's copy of the checkpoint), and the results are all-gathered
+    so every rank holds the whole batch in the original order (the search control
+    then continues identically on every rank)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    mine = assign_configs(len(cfgs), world)[rank]
+    if mine:
+        q, e = evaluate([cfgs[i] for i in mine], [seeds[i] for i in mine])
+        part = (mine, [float(x) for x in q], [float(x) for x in e])
+    else:
+        part = (mine, [], [])
+    parts = [None] * world
+    if world > 1:
+        dist.all_gather_object(parts, part, group=group)
+    else:
+        parts = [part]
+    quality = [0.0] * len(cfgs)
+    est = [0.0] * len(cfgs)
+    for idx, q, e in parts:
+        for j, i in enumerate(idx):
+            quality[i], est[i] = q[j], e[j]
+    return quality, est

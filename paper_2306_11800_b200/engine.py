@@ -215,7 +215,7 @@ class DevCheckpoint:
         self.h = h
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and LIB is not None:
             LIB.dqtg_ckpt_destroy(self.h)
             self.h = None
 
@@ -268,7 +268,7 @@ class DevState:
         self.engine, self.h, self.meta = engine, h, meta
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and LIB is not None:
             LIB.dqtg_qstate_destroy(self.h)
             self.h = None
 
@@ -309,7 +309,7 @@ class Engine:
         self.h = h
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and LIB is not None:  # LIB is None at interpreter exit
             LIB.dqtg_engine_destroy(self.h)
             self.h = None
 
@@ -533,7 +533,7 @@ class Pipe:
         self._nominal = None  # engine used for calls on returned states
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and LIB is not None:
             LIB.dqtg_pipe_destroy(self.h)
             self.h = None
 

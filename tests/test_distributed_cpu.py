@@ -145,3 +145,49 @@ def test_sharded_histograms_and_record_assembly_gloo(world):
     assert all(p.exitcode == 0 for p in procs)
     assert all(r[1] for r in res), "all-reduced shard histograms != whole-checkpoint histogram"
     assert all(r[2] for r in res), "assembled record != single-process record"
+
+
+def _eval_worker(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfgs = [(b, p) for b in (4, 8, 16, 32) for p in (0.0, 0.1, 0.5)]
+        seeds = list(range(100, 100 + len(cfgs)))
+        seen = []
+
+        def evaluate(cs, ss):  # deterministic stand-in for Engine.eval_batch
+            seen.extend(cs)
+            return [b * 0.01 + p for b, p in cs], [s * 1.5 for s in ss]
+
+        qual, est = D.eval_batch_sharded(evaluate, cfgs, seeds)
+        ok = (qual == [b * 0.01 + p for b, p in cfgs] and est == [s * 1.5 for s in seeds]
+              and seen == [cfgs[i] for i in D.assign_configs(len(cfgs), world)[rank]])
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_assign_configs_round_robin():
+    parts = D.assign_configs(10, 3)
+    assert parts == [[0, 3, 6, 9], [1, 4, 7], [2, 5, 8]]
+    assert sorted(i for p in parts for i in p) == list(range(10))
+
+
+@pytest.mark.parametrize("world", [2])
+def test_eval_batch_sharded_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_eval_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(60)
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(r[1] for r in res), "sharded batch evaluation differs from the serial order"
