@@ -24,6 +24,7 @@ namespace dqtg {
 
 constexpr int kPB = 256;  // threads per streaming CTA
 constexpr int kGrab = 8;  // tiles per dynamic grab of the persistent passes
+constexpr int kItTile = kTile / (kPB * 8);  // 8-element thread iterations per tile (2)
 constexpr int kPfDist = 148 * 5;  // pass C: about one wave of resident CTAs ahead
 
 // L2 prefetch of one tile's score inputs (w + EMA, or the explicit scores)
@@ -190,7 +191,8 @@ template <bool EXPL>
 __global__ void __launch_bounds__(kPB, 6) pass_b_kernel(PassIn a, const LtParams* lp,
                                                      unsigned long long* gh_val,
                                                      uint32_t* tile_prot,
-                                                     unsigned long long* tensor_prot) {
+                                                     unsigned long long* tensor_prot,
+                                                     uint16_t* parts) {
     extern __shared__ uint32_t sh[];
     __shared__ uint32_t s_red[2][kPB / 32];  // by tile parity: warps may run ahead into the next tile
     uint32_t par = 0;
@@ -213,7 +215,8 @@ __global__ void __launch_bounds__(kPB, 6) pass_b_kernel(PassIn a, const LtParams
         }
         uint32_t np = 0;
         unsigned long long* gv = gh_val + lt * a.HS;
-        for (uint32_t i = threadIdx.x * 4; i < T.count; i += kPB * 8) {
+        int itn = 0;
+        for (uint32_t i = threadIdx.x * 4; i < T.count; i += kPB * 8, ++itn) {
             const uint32_t i2 = i + kPB * 4;
             const bool two = i2 < T.count;
             float4 w0 = ld4(a.w + T.start + i);
@@ -231,14 +234,17 @@ __global__ void __launch_bounds__(kPB, 6) pass_b_kernel(PassIn a, const LtParams
                 }
             }
             const float wa[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            uint32_t pw = 0;  // 2 bits per element: the partition pass C reuses
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const uint32_t e = (j < 4 ? i : i2) + (j & 3);
                 if (e >= T.count) continue;
                 int part = classify(m[j], s[j], a.has_sens, a.metric, P);
                 np += part == 2;
+                pw |= (uint32_t)part << (2 * j);
                 if (part == 0) hist_add(sh, gv, wa[j], a.tab, a.err);
             }
+            if (parts) parts[((size_t)ti * kItTile + itn) * kPB + threadIdx.x] = (uint16_t)pw;
         }
         np = warp_sum(np);
         if ((threadIdx.x & 31) == 0) s_red[par][threadIdx.x >> 5] = np;
@@ -356,32 +362,37 @@ __device__ __forceinline__ uint32_t level_fixed(const float* T, float v, uint32_
 }
 
 // One tile of pass C with the level bisection unrolled for P = 2^LOGP.
-template <bool EXPL, int LOGP>
+template <bool EXPL, int LOGP, bool PARTS>
 __device__ __forceinline__ void pass_c_tile(const PassIn& a, const LtParams& P, const Tile& T,
                                             uint32_t k, const float* s_lb, uint64_t tensor_base,
                                             unsigned long long out,
                                             unsigned long long* s_scan, uint16_t* levels,
-                                            uint64_t* ppos, uint16_t* pval) {
+                                            uint64_t* ppos, uint16_t* pval, const uint16_t* parts,
+                                            int ti) {
     // two float4 groups per thread and iteration; protected entries keep element
     // order: group 0 (i0..i0+1023) before group 1, one packed (lo|hi) scan
-    for (uint32_t i0 = 0; i0 < T.count; i0 += kPB * 8) {
+    int itn = 0;
+    for (uint32_t i0 = 0; i0 < T.count; i0 += kPB * 8, ++itn) {
         uint32_t flags[2] = {0, 0};
         float wa[2][4];
+        uint32_t pw = 0;
+        if (PARTS) pw = parts[((size_t)ti * kItTile + itn) * kPB + threadIdx.x];
         for (int g = 0; g < 2; ++g) {
             const uint32_t i = i0 + g * kPB * 4 + threadIdx.x * 4;
             wa[g][0] = wa[g][1] = wa[g][2] = wa[g][3] = 0.0f;
             if (i < T.count) {
                 const uint64_t idx = T.start + i;
                 float4 wv = ld4(a.w + idx);
-                float m[4], s[4];
-                load_scores<EXPL>(a, idx, wv, m, s);
+                float m[4] = {0, 0, 0, 0}, s[4] = {0, 0, 0, 0};
+                if (!PARTS) load_scores<EXPL>(a, idx, wv, m, s);
                 wa[g][0] = wv.x, wa[g][1] = wv.y, wa[g][2] = wv.z, wa[g][3] = wv.w;
                 uint32_t lv[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     // level for every element (branch-free), then the partition decides
                     const uint32_t q = level_fixed<LOGP>(s_lb, wa[g][j], pow2_ceil(k));
-                    const int part = classify(m[j], s[j], a.has_sens, a.metric, P);
+                    const int part = PARTS ? (int)((pw >> (2 * (4 * g + j))) & 3u)
+                                           : classify(m[j], s[j], a.has_sens, a.metric, P);
                     lv[j] = part == 0 ? q : (part == 1 ? k : k + 1);
                     if (part == 2 && i + j < T.count) flags[g] |= 1u << j;
                 }
@@ -412,20 +423,27 @@ __device__ __forceinline__ void pass_c_tile(const PassIn& a, const LtParams& P, 
     }
 }
 
-template <bool EXPL>
+template <bool EXPL, bool PARTS>
 __global__ void __launch_bounds__(kPB) pass_c_kernel(PassIn a, const LtParams* lp,
                                                      const float* lb, int lb_stride,
                                                      const uint32_t* cb_len,
                                                      const unsigned long long* tile_prot_off,
                                                      uint16_t* levels, uint64_t* ppos,
-                                                     uint16_t* pval) {
+                                                     uint16_t* pval, const uint16_t* parts) {
     extern __shared__ float s_lb[];
     __shared__ unsigned long long s_scan[33];
     const int ti = blockIdx.x;
     const Tile T = a.tiles[ti];
     const int lt = a.types[T.tensor];
     // the tile a CTA launched about one residency later will read (L2 prefetch)
-    if (threadIdx.x == 0 && ti + kPfDist < a.ntiles) prefetch_tile(a, ti + kPfDist, EXPL);
+    if (threadIdx.x == 0 && ti + kPfDist < a.ntiles) {
+        if (PARTS) {
+            const Tile N = a.tiles[ti + kPfDist];
+            prefetch_l2(a.w + N.start, ((N.count + 3u) & ~3u) * 4u);
+        } else {
+            prefetch_tile(a, ti + kPfDist, EXPL);
+        }
+    }
     const uint32_t k = cb_len[lt], kp = pow2_ceil(k);
     for (uint32_t j = threadIdx.x; j < kp; j += blockDim.x) s_lb[j] = lb[lt * lb_stride + j];
     const LtParams P = lp[lt];
@@ -434,10 +452,10 @@ __global__ void __launch_bounds__(kPB) pass_c_kernel(PassIn a, const LtParams* l
     const unsigned long long out = tile_prot_off[ti];
     switch (__ffs(kp) - 1) {
 #define DQTG_PC(L) \
-    case L: pass_c_tile<EXPL, L>(a, P, T, k, s_lb, tensor_base, out, s_scan, levels, ppos, pval); break;
+    case L: pass_c_tile<EXPL, L, PARTS>(a, P, T, k, s_lb, tensor_base, out, s_scan, levels, ppos, pval, parts, ti); break;
         DQTG_PC(0) DQTG_PC(1) DQTG_PC(2) DQTG_PC(3) DQTG_PC(4) DQTG_PC(5) DQTG_PC(6)
 #undef DQTG_PC
-        default: pass_c_tile<EXPL, -1>(a, P, T, k, s_lb, tensor_base, out, s_scan, levels, ppos, pval);
+        default: pass_c_tile<EXPL, -1, PARTS>(a, P, T, k, s_lb, tensor_base, out, s_scan, levels, ppos, pval, parts, ti);
     }
 }
 
@@ -704,6 +722,7 @@ struct Stage {
     uint32_t* cb_len = nullptr;
     float* d_lb = nullptr;  // [7][lb_stride] level boundaries (level_bounds_kernel)
     uint32_t lb_stride = 1;
+    uint16_t* parts = nullptr;  // pass B partition, 2 bits per element (read by pass C)
 };
 
 static void stage_alloc(Engine& e, const Layout& L, int64_t HS, Stage& s, float* cb_dst) {
@@ -722,6 +741,7 @@ static void stage_alloc(Engine& e, const Layout& L, int64_t HS, Stage& s, float*
     s.cb_stride = std::max(1u, std::max(s.cfg.bins, s.cfg.embed_bins));
     s.d_cb = cb_dst ? cb_dst : (float*)e.buf(t + "cb", (size_t)kLayerTypes * s.cb_stride * 4);
     s.lb_stride = pow2_ceil(s.cb_stride);
+    s.parts = (uint16_t*)e.buf(t + "parts", (size_t)ntiles * kItTile * kPB * 2 + 16);
     s.d_lb = (float*)e.buf(t + "lb", (size_t)kLayerTypes * s.lb_stride * 4);
 }
 
@@ -794,9 +814,9 @@ static void stage_pass_b(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s,
     DQTG_CUDA(cudaFuncSetAttribute(pass_b_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     if (ntiles) {
         if (c.explicit_scores)
-            { DQTG_SPAN(e, "pass_b_kernel"); pass_b_kernel<true><<<grid, kPB, smem, st>>>(a, s.d_lp, s.gh_val, s.tile_prot, s.tensor_prot); }
+            { DQTG_SPAN(e, "pass_b_kernel"); pass_b_kernel<true><<<grid, kPB, smem, st>>>(a, s.d_lp, s.gh_val, s.tile_prot, s.tensor_prot, s.parts); }
         else
-            { DQTG_SPAN(e, "pass_b_kernel"); pass_b_kernel<false><<<grid, kPB, smem, st>>>(a, s.d_lp, s.gh_val, s.tile_prot, s.tensor_prot); }
+            { DQTG_SPAN(e, "pass_b_kernel"); pass_b_kernel<false><<<grid, kPB, smem, st>>>(a, s.d_lp, s.gh_val, s.tile_prot, s.tensor_prot, s.parts); }
         e.launched();
     }
     { DQTG_SPAN(e, "scan_u32_kernel"); scan_u32_kernel<<<1, 1024, 0, st>>>(s.tile_prot, ntiles, s.tile_off); }
@@ -857,10 +877,8 @@ static void stage_pass_c(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s,
     cudaStream_t st = e.stream;
     stage_level_bounds(e, s);
     const size_t smem = (size_t)s.lb_stride * 4 + 16;
-    if (c.explicit_scores)
-        { DQTG_SPAN(e, "pass_c_kernel"); pass_c_kernel<true><<<ntiles, kPB, smem, st>>>(a, s.d_lp, s.d_lb, (int)s.lb_stride, s.cb_len, s.tile_off, q.d_levels, q.d_ppos, q.d_pval); }
-    else
-        { DQTG_SPAN(e, "pass_c_kernel"); pass_c_kernel<false><<<ntiles, kPB, smem, st>>>(a, s.d_lp, s.d_lb, (int)s.lb_stride, s.cb_len, s.tile_off, q.d_levels, q.d_ppos, q.d_pval); }
+    // the partition comes from pass B's 2-bit codes: w is the only stream read here
+    { DQTG_SPAN(e, "pass_c_kernel"); pass_c_kernel<false, true><<<ntiles, kPB, smem, st>>>(a, s.d_lp, s.d_lb, (int)s.lb_stride, s.cb_len, s.tile_off, q.d_levels, q.d_ppos, q.d_pval, s.parts); }
     e.launched();
     DQTG_CUDA(cudaGetLastError());
 }
