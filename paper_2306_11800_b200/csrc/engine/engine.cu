@@ -87,6 +87,7 @@ Engine::~Engine() {
         cudaFree(kv.second->d_U);
         cudaFree(kv.second->d_cell);
         cudaFree(kv.second->d_slot);
+        cudaFree(kv.second->d_ctab);
         cudaFree(kv.second->d_key);
         cudaFree(kv.second->d_keyf);
     }
@@ -337,6 +338,24 @@ AlphaTables& Engine::alpha_tables(double alpha) {
         DQTG_CUDA(cudaMalloc(&t->d_slot, slots.size() * sizeof(uint2)));
         DQTG_CUDA(cudaMemcpy(t->d_slot, slots.data(), slots.size() * sizeof(uint2),
                              cudaMemcpyHostToDevice));
+        const uint32_t m = 23 - t->cell_shift;
+        if (t->cell_shift <= 17 && m <= 7) {  // 32 binades [2^-32, 1) in <= 16 KB
+            t->ctab_lo = (95u << 23) >> t->cell_shift;
+            t->ctab_n = 32u << m;
+            std::vector<uint32_t> ct(t->ctab_n);
+            for (uint32_t r = 0; r < t->ctab_n; ++r) {
+                const uint32_t cell = t->ctab_lo + r, a0 = cell << t->cell_shift;
+                const uint2 e = slots[cell];
+                const uint32_t lo = e.x & 0xffffu, hi = e.x >> 16;
+                const bool split = e.y != 0xffffffffu;
+                const uint32_t off = split ? e.y - a0 : (1u << 17) - 1u;
+                const bool lo_sp = lo > (uint32_t)kWin;
+                const bool hi_sp = split ? (hi != lo + 1 || hi > (uint32_t)kWin) : lo_sp;
+                ct[r] = (lo & 0x1fffu) | (off << 13) | ((uint32_t)hi_sp << 30) | ((uint32_t)lo_sp << 31);
+            }
+            DQTG_CUDA(cudaMalloc(&t->d_ctab, ct.size() * 4));
+            DQTG_CUDA(cudaMemcpy(t->d_ctab, ct.data(), ct.size() * 4, cudaMemcpyHostToDevice));
+        }
     }
     DQTG_CUDA(cudaMalloc(&t->d_U, U.size() * 4));
     DQTG_CUDA(cudaMalloc(&t->d_key, t->h_key.size() * 8));

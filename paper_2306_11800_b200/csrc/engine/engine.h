@@ -46,6 +46,11 @@ struct AlphaTables {
     uint32_t cell_shift = 0;     // 0: no table (alpha too small), probe U instead
     uint2* d_cell = nullptr;
     uint2* d_slot = nullptr;     // same cells: window slot of |x| (lo | hi << 16, split)
+    // compact slot table for |x| in [2^-32, 1): 4-byte entries staged in shared memory
+    // by the streaming passes (lo slot | split offset << 13 | hi special << 30 |
+    // lo special << 31; hi = lo + 1); null when the cells are too fine
+    uint32_t* d_ctab = nullptr;
+    uint32_t ctab_lo = 0, ctab_n = 0;
 };
 
 // Device view of the bucket tables passed by value to kernels.
@@ -57,6 +62,8 @@ struct BucketTab {
     const uint2* cell;  // null: probe U
     uint32_t cell_shift;
     const uint2* slot;  // window-slot table (null with cell)
+    const uint32_t* ctab;  // compact table (global copy; kernels stage it in shared)
+    uint32_t ctab_lo, ctab_n;
 };
 
 struct Engine;
@@ -165,7 +172,7 @@ struct Engine {
     AlphaTables& alpha_tables(double alpha);
     BucketTab bucket_tab(const AlphaTables& t) const {
         return BucketTab{t.d_U, t.kmin, t.kmax, t.NB, t.kw_lo, t.zbits, t.inv_log2_gamma, t.d_cell,
-                         t.cell_shift, t.d_slot};
+                         t.cell_shift, t.d_slot, t.d_ctab, t.ctab_lo, t.ctab_n};
     }
     void* buf(const std::string& name, size_t bytes);  // scratch, contents undefined
     // stream-ordered pool allocations for per-step objects (states, records)

@@ -59,6 +59,30 @@ __device__ __forceinline__ uint32_t slot_of_abs(uint32_t a, const BucketTab& t) 
     return (a > c.y) ? (c.x >> 16) : (c.x & 0xffffu);
 }
 
+// Window slot of |x| from the compact table staged in shared memory (s_ctab), or
+// kSlotSpill when |x| is outside [2^-32, 1) or the cell needs the exact path.
+__device__ __forceinline__ uint32_t slot_shared(uint32_t a, const BucketTab& t, const uint32_t* s_ctab) {
+    const uint32_t rel = (a >> t.cell_shift) - t.ctab_lo;
+    if (rel >= t.ctab_n) return kSlotSpill;
+    const uint32_t c = s_ctab[rel];
+    const uint32_t off = a & ((1u << t.cell_shift) - 1u);
+    const bool hi = off > ((c >> 13) & 0x1ffffu);
+    const bool special = hi ? ((c >> 30) & 1u) : (c >> 31);
+    return special ? kSlotSpill : (c & 0x1fffu) + (hi ? 1u : 0u);
+}
+
+__device__ __forceinline__ void hist_add(uint32_t* sh, unsigned long long* gh, float v,
+                                         const BucketTab& t, uint32_t* err);
+
+// hist_add / hist_add_pos with the shared compact table first
+__device__ __forceinline__ void hist_add_s(uint32_t* sh, unsigned long long* gh, float v,
+                                           const BucketTab& t, uint32_t* err, const uint32_t* s_ctab) {
+    const uint32_t b = __float_as_uint(v);
+    const uint32_t p = slot_shared(b & 0x7fffffffu, t, s_ctab);
+    if (p <= (uint32_t)kWin) atomicAdd(sh + ((b >> 31) ? kWin - p : kWin + p), 1u);
+    else hist_add(sh, gh, v, t, err);
+}
+
 __device__ __forceinline__ void hist_add(uint32_t* sh, unsigned long long* gh, float v,
                                          const BucketTab& t, uint32_t* err) {
     uint32_t b = __float_as_uint(v), a = b & 0x7fffffffu;
@@ -131,6 +155,14 @@ __device__ __forceinline__ void hist_add_pos(uint32_t* sh, unsigned long long* g
     const int d = k - (int)t.kw_lo;
     if ((unsigned)d < (unsigned)kWin) atomicAdd(sh + 1 + d, 1u);
     else atomicAdd(gh + (t.NB + 1 + k - t.kmin), 1ull);
+}
+
+__device__ __forceinline__ void hist_add_pos_s(uint32_t* sh, unsigned long long* gh, float v,
+                                               const BucketTab& t, uint32_t* err,
+                                               const uint32_t* s_ctab) {
+    const uint32_t p = slot_shared(__float_as_uint(v), t, s_ctab);
+    if (p <= (uint32_t)kWin) atomicAdd(sh + p, 1u);
+    else hist_add_pos(sh, gh, v, t, err);
 }
 
 __device__ __forceinline__ void hist_flush_pos(uint32_t* sh, unsigned long long* gh,

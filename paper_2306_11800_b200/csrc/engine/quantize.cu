@@ -76,14 +76,18 @@ __device__ __forceinline__ void load_scores(const PassIn& a, uint64_t idx, const
 // ---- pass A: score histograms ----------------------------------------------
 // Derived scores are non-negative: half-size windows (kPosSlots) per histogram.
 template <bool EXPL>
-__global__ void __launch_bounds__(kPB, 6) pass_a_kernel(PassIn a, unsigned long long* gh_mag,
+__global__ void __launch_bounds__(kPB, 5) pass_a_kernel(PassIn a, unsigned long long* gh_mag,
                                                      unsigned long long* gh_sens,
                                                      uint32_t mask_mag, uint32_t mask_sens) {
     extern __shared__ uint32_t sh[];
     constexpr int W = EXPL ? kWinSlots : kPosSlots;
     uint32_t* shm = sh;
     uint32_t* shs = sh + W;
+    uint32_t* s_ctab = sh + 2 * W;  // compact slot table (a.tab.ctab_n words)
+    const bool fastc = a.tab.ctab != nullptr;
     for (int i = threadIdx.x; i < 2 * W; i += blockDim.x) sh[i] = 0;
+    if (fastc)
+        for (uint32_t i = threadIdx.x; i < a.tab.ctab_n; i += blockDim.x) s_ctab[i] = __ldg(a.tab.ctab + i);
     __syncthreads();
     __shared__ int s_base;
     int cur = -1;
@@ -134,8 +138,16 @@ __global__ void __launch_bounds__(kPB, 6) pass_a_kernel(PassIn a, unsigned long 
                 const uint32_t e = (j < 4 ? i : i2) + (j & 3);
                 if (e >= T.count) continue;
                 if (EXPL) {
-                    if (dm) hist_add(shm, gm, m[j], a.tab, a.err);
-                    if (ds) hist_add(shs, gs, s[j], a.tab, a.err);
+                    if (fastc) {
+                        if (dm) hist_add_s(shm, gm, m[j], a.tab, a.err, s_ctab);
+                        if (ds) hist_add_s(shs, gs, s[j], a.tab, a.err, s_ctab);
+                    } else {
+                        if (dm) hist_add(shm, gm, m[j], a.tab, a.err);
+                        if (ds) hist_add(shs, gs, s[j], a.tab, a.err);
+                    }
+                } else if (fastc) {
+                    if (dm) hist_add_pos_s(shm, gm, m[j], a.tab, a.err, s_ctab);
+                    if (ds) hist_add_pos_s(shs, gs, s[j], a.tab, a.err, s_ctab);
                 } else {
                     if (dm) hist_add_pos(shm, gm, m[j], a.tab, a.err);
                     if (ds) hist_add_pos(shs, gs, s[j], a.tab, a.err);
@@ -758,14 +770,16 @@ static void stage_pass_a(Engine& e, const DevCkpt& c, const PassIn& a, uint32_t 
     const int ntiles = a.ntiles;
     cudaStream_t st = e.stream;
     DQTG_CUDA(cudaMemsetAsync(a.tile_ctr, 0, 4, st));
+    const size_t ct = a.tab.ctab ? (size_t)a.tab.ctab_n * 4 : 0;
     if (c.explicit_scores) {
-        const size_t smem = (size_t)2 * kWinSlots * 4;
+        const size_t smem = (size_t)2 * kWinSlots * 4 + ct;
         const int grid = stream_grid(e, ntiles, 3);
         ensure_dyn_smem((const void*)pass_a_kernel<true>, smem);
         { DQTG_SPAN(e, "pass_a_kernel"); pass_a_kernel<true><<<grid, kPB, smem, st>>>(a, gh_mag, gh_sens, mask_mag, mask_sens); }
     } else {
-        const size_t smem = (size_t)2 * kPosSlots * 4;
-        const int grid = stream_grid(e, ntiles, 6);
+        const size_t smem = (size_t)2 * kPosSlots * 4 + ct;
+        ensure_dyn_smem((const void*)pass_a_kernel<false>, smem);
+        const int grid = stream_grid(e, ntiles, 5);
         DQTG_CUDA(cudaFuncSetAttribute(pass_a_kernel<false>,
                                        cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         { DQTG_SPAN(e, "pass_a_kernel"); pass_a_kernel<false><<<grid, kPB, smem, st>>>(a, gh_mag, gh_sens, mask_mag, mask_sens); }
