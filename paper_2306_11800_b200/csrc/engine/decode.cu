@@ -21,6 +21,9 @@
 #include <cub/iterator/transform_input_iterator.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -444,6 +447,13 @@ struct Rd {
 
 std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n, const QState* base) {
     cudaStream_t st = e.stream;
+    const bool trace = getenv("DQTG_DECODE_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (trace)
+            fprintf(stderr, "decode %-12s %8.3f ms\n", what,
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    };
     // the record may live in device memory: decode from a host copy of its structure
     std::vector<uint8_t> host_copy;
     const uint8_t* h = rec;
@@ -525,12 +535,30 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
         pval[i].resize(np);
         uint64_t pos = 0;
         for (uint64_t k = 0; k < np; ++k) {
-            const uint64_t dd = r.uv();
+            uint64_t dd;
+            if (r.n - r.at >= 12) {  // fast path: no per-byte bounds checks
+                const uint8_t* q8 = r.p + r.at;
+                dd = q8[0] & 0x7f;
+                int len = 1;
+                if (q8[0] & 0x80) {
+                    for (int sh = 7;; sh += 7) {
+                        const uint8_t b = q8[len++];
+                        dd |= (uint64_t)(b & 0x7f) << sh;
+                        if (!(b & 0x80)) break;
+                        if (len >= 10) throw Fail(DQTG_CORRUPT_BITSTREAM, "varint overflow");
+                    }
+                }
+                r.at += len;
+                pval[i][k] = (uint16_t)(r.p[r.at] | (r.p[r.at + 1] << 8));
+                r.at += 2;
+            } else {
+                dd = r.uv();
+                pval[i][k] = r.le<uint16_t>();
+            }
             pos = k == 0 ? dd : pos + dd;
             if (pos >= numel || (k > 0 && dd == 0))
                 throw Fail(DQTG_CORRUPT_INDEX, "protected positions not ascending in " + names[i]);
             ppos[i][k] = pos;
-            pval[i][k] = r.le<uint16_t>();
         }
         if (base) {
             const Layout& BL = *base->L;
@@ -610,6 +638,7 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
     }
     const uint32_t stored_crc = r.le<uint32_t>();
     if (r.at != n) throw Fail(DQTG_IO, "trailing bytes after DQDR record");
+    mark("parsed");
 
     // state layout from the record
     dqtg_layout dl{};
@@ -620,7 +649,9 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
     dl.types = types.data();
     dl.ranks = ranks.data();
     dl.dims = dims.data();
-    q->L = make_layout(&e, &dl);
+    // a delta record has the base's tensor table (checked above): share its layout
+    // (no per-record layout uploads / frees)
+    q->L = base ? base->L : make_layout(&e, &dl);
     const Layout& L = *q->L;
     const uint64_t N = L.N;
     const int ntiles = (int)L.tiles.size();
@@ -675,6 +706,7 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
     e.to_device(d_lbase, lbase.data(), lbase.size() * 4);
     e.to_device(d_relems, rec_elems.data(), rec_elems.size() * 8);
     DecTabs T{d_lim, d_first, d_lbase, d_sym};
+    mark("uploaded");
     const uint64_t* rec64 = (const uint64_t*)d_rec;
 
     // symbol flags (first / last of each group)
@@ -704,6 +736,7 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
             e.sync();
             if (!any) break;
         }
+        mark("synced");
         // chunks' symbol counts -> scan (u64)
         auto* d_scan = (unsigned long long*)e.buf("d.scan", (size_t)(nc + 2) * 8);
         cub::TransformInputIterator<unsigned long long, Widen, const uint32_t*> it(d_cnt, Widen{});
@@ -718,6 +751,7 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
         e.launched(2);
         e.check_err();
 
+        mark("huffman");
         // ---- R: RLE expansion into the dense rearranged delta stream
         auto* d_ecnt = (unsigned long long*)e.buf("d.ecnt", (sym_total + 1) * 8);
         auto* d_eoff = (unsigned long long*)e.buf("d.eoff", (sym_total + 1) * 8);
@@ -759,8 +793,10 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
         }
         e.check_err();
     }
+    mark("unrearranged");
     // ---- C: stream checksum
     const uint32_t crc = level_stream_crc(e, L, q->d_levels);
+    mark("crc");
     if (crc != stored_crc)
         throw Fail(DQTG_CHECKSUM_MISMATCH, "record checksum mismatch at step " + std::to_string(target_step));
     return q;
