@@ -255,10 +255,16 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # --share-gpu (testing the N>1 path on one GPU): every rank on device 0, gloo
+    gpu = 0 if args.share_gpu else local
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    local = gpu
 
     from paper_2306_11800_b200 import engine as E
 
@@ -564,6 +570,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true")
     ap.add_argument("--workers", type=int, default=4, help="worker streams of the chain pipeline")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="test mode for N>1 on one GPU: all ranks on device 0 with gloo")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
