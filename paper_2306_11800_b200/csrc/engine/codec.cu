@@ -1091,7 +1091,7 @@ __device__ __forceinline__ void owned_run(const EncArgs& A, const Seg* segs, uns
 
 // E2a: bits per (tile, group), one warp per tile
 __global__ void __launch_bounds__(256) enc_bits_kernel(EncArgs A, CodeTabs C, int ntiles,
-                                                       unsigned long long* segbits) {
+                                                       uint32_t* segbits) {
     __shared__ uint32_t s_bits[8][kMaxB];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ti = blockIdx.x * 8 + wid;
@@ -1120,8 +1120,8 @@ __global__ void __launch_bounds__(256) enc_bits_kernel(EncArgs A, CodeTabs C, in
 }
 
 // S2: exclusive scan of segment bits across the tensor's tiles
-__global__ void __launch_bounds__(kCB) enc_bitscan_kernel(EncArgs A, unsigned long long* segbits,
-                                                          GroupInfo* gi) {
+__global__ void __launch_bounds__(kCB) enc_bitscan_kernel(EncArgs A, const uint32_t* segbits,
+                                                          unsigned long long* segoff, GroupInfo* gi) {
     __shared__ unsigned long long s_scan[33];
     const uint32_t B = A.B;
     const uint32_t t = blockIdx.x / B, b = blockIdx.x % B;
@@ -1131,7 +1131,7 @@ __global__ void __launch_bounds__(kCB) enc_bitscan_kernel(EncArgs A, unsigned lo
         const uint32_t i = c0 + threadIdx.x;
         unsigned long long v = i < a1 ? segbits[(size_t)i * B + b] : 0ull, tot;
         unsigned long long ex = block_exclusive_scan<unsigned long long>(v, s_scan, &tot);
-        if (i < a1) segbits[(size_t)i * B + b] = base + ex;
+        if (i < a1) segoff[(size_t)i * B + b] = base + ex;
         base += tot;
     }
     if (threadIdx.x == 0) {
@@ -1348,6 +1348,7 @@ __device__ __forceinline__ uint32_t run_bits(const EncArgs& A, const CodeTabs& C
 // since they can share bytes with neighbouring segments or headers).
 __global__ void __launch_bounds__(kEmitWarps * 32) enc_emit_kernel(EncArgs A, CodeTabs C,
                                                                    const unsigned long long* segoff,
+                                                                   const uint32_t* segbits,
                                                                    int ntiles, uint8_t* rec) {
     __shared__ uint32_t s_stage[kEmitWarps][kWarpStage];
     __shared__ uint32_t s_segbits[kEmitWarps][kMaxB];
@@ -1365,17 +1366,8 @@ __global__ void __launch_bounds__(kEmitWarps * 32) enc_emit_kernel(EncArgs A, Co
     const unsigned long long* runs = A.runs + (size_t)ti * kTile;
     uint32_t* words = (uint32_t*)rec;
     uint32_t* stage = s_stage[wid];
-    for (uint32_t b = lane; b < B; b += 32) s_segbits[wid][b] = 0;
-    __syncwarp();
-    // pass 1: bits per segment
-    for (uint32_t r0 = 0; r0 < R; r0 += 32) {
-        const uint32_t r = r0 + lane;
-        if (r < R) {
-            uint32_t b;
-            const uint32_t bits = run_bits(A, C, segs, runs, T.tensor, r, b);
-            if (bits) atomicAdd(&s_segbits[wid][b], bits);
-        }
-    }
+    // bits per segment (enc_bits_kernel)
+    for (uint32_t b = lane; b < B; b += 32) s_segbits[wid][b] = segbits[(size_t)ti * B + b];
     __syncwarp();
     // segment layout: tile-local start, destination word + phase, staging base
     uint32_t tile_base = 0, stage_base = 0;
@@ -1767,9 +1759,10 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
         e.launched();
     }
     CodeTabs C{code_dense, len_dense, ukey, code_ov, len_ov, gi};
-    auto* segbits = (unsigned long long*)e.buf("e.segbits", (size_t)ntiles * B * 8);
+    auto* segbits = (uint32_t*)e.buf("e.segbits32", (size_t)ntiles * B * 4 + 4);
+    auto* segoff = (unsigned long long*)e.buf("e.segoff", (size_t)ntiles * B * 8);
     { DQTG_SPAN(e, "enc_bits_kernel"); enc_bits_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(A, C, ntiles, segbits); }
-    { DQTG_SPAN(e, "enc_bitscan_kernel"); enc_bitscan_kernel<<<nt * B, kCB, 0, st>>>(A, segbits, gi); }
+    { DQTG_SPAN(e, "enc_bitscan_kernel"); enc_bitscan_kernel<<<nt * B, kCB, 0, st>>>(A, segbits, segoff, gi); }
     e.launched(2);
 
     // protected entry sizes + layout
@@ -1806,7 +1799,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     { DQTG_SPAN(e, "write_tensor_kernel"); write_tensor_kernel<<<nt, kCB, 0, st>>>(A, tr, d_statics, target.d_ppos, target.d_pval, pscan,
                                             gi, tab_sym, tab_len, rec->d_buf); }
     if (np) { DQTG_SPAN(e, "write_prot_kernel"); write_prot_kernel<<<pgrid, 256, 0, st>>>(tr, nt, np, target.d_ppos, target.d_pval, pscan, rec->d_buf); }
-    { DQTG_SPAN(e, "enc_emit_kernel"); enc_emit_kernel<<<(ntiles + kEmitWarps - 1) / kEmitWarps, kEmitWarps * 32, 0, st>>>(A, C, segbits, ntiles, rec->d_buf); }
+    { DQTG_SPAN(e, "enc_emit_kernel"); enc_emit_kernel<<<(ntiles + kEmitWarps - 1) / kEmitWarps, kEmitWarps * 32, 0, st>>>(A, C, segoff, segbits, ntiles, rec->d_buf); }
     { DQTG_SPAN(e, "finish_crc_kernel"); finish_crc_kernel<<<1, 1, 0, st>>>(A.crc_acc, 2 * L.N, rec->d_buf + total - 4, nullptr); }
     e.launched(3);
     DQTG_CUDA(cudaGetLastError());
