@@ -215,8 +215,8 @@ def run_reference(args):
 # ---------------------------------------------------------------------------- our arm
 ALGO_BYTES = {  # algorithmic HBM bytes per parameter per launch
     "pass_a_kernel": 8.0,   # read w + EMA
-    "pass_b_kernel": 8.0,   # read w + EMA
-    "pass_c_kernel": 10.0,  # read w + EMA, write levels
+    "pass_b_kernel": 8.25,  # read w + EMA, write 2-bit partition codes
+    "pass_c_kernel": 6.25,  # read w + partition codes, write levels
     "enc_tile_kernel": 4.0,  # read levels + previous levels
 }
 
