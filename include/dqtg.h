@@ -115,6 +115,28 @@ float *dqtg_ckpt_weights_dev(dqtg_ckpt *c);
 float *dqtg_ckpt_ema_dev(dqtg_ckpt *c);
 /* element offset of tensor i inside the padded buffers */
 uint64_t dqtg_ckpt_tensor_offset(const dqtg_ckpt *c, uint32_t i);
+/* layout of tensor i (name NUL-terminated into cap bytes; dims holds `rank` entries) */
+uint32_t dqtg_ckpt_tensor_count(const dqtg_ckpt *c);
+dqtg_status dqtg_ckpt_tensor_info(const dqtg_ckpt *c, uint32_t i, char *name, uint64_t cap,
+                                  uint8_t *type, uint8_t *rank, uint64_t *dims);
+/* copy the weights back (tensor i -> out_any[i], numel floats; NULL entries skipped) */
+dqtg_status dqtg_ckpt_download(dqtg_ckpt *c, float *const *out_any);
+/* apply_layer_rules (src/tensor.cpp:225-227): replace the layer types (n_tensors entries) */
+dqtg_status dqtg_ckpt_set_types(dqtg_ckpt *c, const uint8_t *types);
+
+/* ---- DQT1 ingest: replaces read_checkpoint + validate (src/tensor.cpp:63-75,
+ * 110-149) on the compress path.  Parses the tensor headers on the host (same
+ * checks and status codes, in the same order), streams the data sections through
+ * pinned staging chunks into a new device checkpoint (`threads` reader threads,
+ * 0 = 8), and checks NaN/Inf on the device (DQTG_NON_FINITE names the first bad
+ * tensor).  *step = Checkpoint::step; the meta section is returned raw
+ * (u32 count | {u16 len, key | u32 len, value}) into meta[0..meta_cap), its
+ * full length in *meta_len.  DQTG_INGEST_DIRECT reads with O_DIRECT (bypassing the
+ * page cache) where the filesystem allows it. */
+#define DQTG_INGEST_DIRECT 1
+dqtg_status dqtg_ckpt_read_dqt1(dqtg_engine *e, const char *path, int flags, int threads,
+                                dqtg_ckpt **out, uint64_t *step, uint8_t *meta,
+                                uint64_t meta_cap, uint64_t *meta_len);
 
 /* ---- quantized state (QuantizedCheckpoint, quantize.hpp:86-110) ----------- */
 typedef struct dqtg_qstate dqtg_qstate;

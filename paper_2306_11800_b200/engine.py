@@ -97,6 +97,14 @@ def _load():
         "dqtg_ckpt_weights_dev": (_P, [_P]),
         "dqtg_ckpt_ema_dev": (_P, [_P]),
         "dqtg_ckpt_tensor_offset": (C.c_uint64, [_P, C.c_uint32]),
+        "dqtg_ckpt_tensor_count": (C.c_uint32, [_P]),
+        "dqtg_ckpt_tensor_info": (C.c_int, [_P, C.c_uint32, C.c_char_p, C.c_uint64,
+                                            C.POINTER(C.c_uint8), C.POINTER(C.c_uint8), _P]),
+        "dqtg_ckpt_download": (C.c_int, [_P, _P]),
+        "dqtg_ckpt_set_types": (C.c_int, [_P, _P]),
+        "dqtg_ckpt_read_dqt1": (C.c_int, [_P, C.c_char_p, C.c_int, C.c_int, C.POINTER(_P),
+                                          C.POINTER(C.c_uint64), _P, C.c_uint64,
+                                          C.POINTER(C.c_uint64)]),
         "dqtg_quantize": (C.c_int, [_P, _P, C.POINTER(Config), C.c_uint64, C.c_uint64,
                                     C.POINTER(_P)]),
         "dqtg_qstate_info_get": (C.c_int, [_P, C.POINTER(_Info)]),
@@ -247,6 +255,52 @@ class DevCheckpoint:
     def tensor_offset(self, i):
         return LIB.dqtg_ckpt_tensor_offset(self.h, i)
 
+    @classmethod
+    def _wrap(cls, engine, h):
+        """Adopt a checkpoint handle made by the engine (e.g. dqtg_ckpt_read_dqt1)."""
+        self = cls.__new__(cls)
+        self.engine, self.h = engine, h
+        names, types, shapes = [], [], []
+        buf = C.create_string_buffer(1 << 16)
+        dims = np.zeros(256, np.uint64)
+        t, r = C.c_uint8(), C.c_uint8()
+        for i in range(LIB.dqtg_ckpt_tensor_count(h)):
+            _check(LIB.dqtg_ckpt_tensor_info(h, i, buf, len(buf), C.byref(t), C.byref(r),
+                                             dims.ctypes.data))
+            names.append(buf.value.decode("utf-8", "surrogateescape"))
+            types.append(t.value)
+            shapes.append(tuple(int(d) for d in dims[:r.value]))
+        self.meta = _Meta(names, types, shapes)
+        return self
+
+    def set_types(self, types):
+        """Replace the layer types (apply_layer_rules, src/tensor.cpp:225-227)."""
+        t = np.array([int(x) for x in types] or [0], np.uint8)
+        _check(LIB.dqtg_ckpt_set_types(self.h, t.ctypes.data))
+        self.meta = _Meta(self.meta.names, t[:len(types)].tolist(), self.meta.shapes)
+
+    def download(self):
+        """Per-tensor float32 host copies of the weights."""
+        out = [np.empty(n, np.float32) for n in self.meta.numel]
+        _check(LIB.dqtg_ckpt_download(self.h, _ptr_array(out)))
+        return out
+
+
+def parse_dqt1_meta(raw):
+    """u32 count | {u16 len, key | u32 len, value} (tensor.cpp:83-88) -> dict
+    (a std::map in the reference: later duplicate keys win)."""
+    import struct
+    n, = struct.unpack_from("<I", raw, 0)
+    at, out = 4, {}
+    for _ in range(n):
+        k, = struct.unpack_from("<H", raw, at)
+        key = raw[at + 2:at + 2 + k].decode("utf-8", "surrogateescape")
+        at += 2 + k
+        v, = struct.unpack_from("<I", raw, at)
+        out[key] = raw[at + 4:at + 4 + v].decode("utf-8", "surrogateescape")
+        at += 4 + v
+    return out
+
 
 def state_meta(h) -> "_Meta":
     """Layout of a state handle (names, types, shapes) from the engine."""
@@ -315,6 +369,25 @@ class Engine:
 
     def sync(self):
         _check(LIB.dqtg_engine_sync(self.h))
+
+    def read_dqt1(self, path, direct=False, threads=0):
+        """DQT1 file -> (DevCheckpoint, step, meta dict) via dqtg_ckpt_read_dqt1
+        (replaces read_checkpoint, src/tensor.cpp:110-149)."""
+        h, step, mlen = _P(), C.c_uint64(), C.c_uint64()
+        meta = C.create_string_buffer(1 << 16)
+        path_b = os.fsencode(path)
+        _check(LIB.dqtg_ckpt_read_dqt1(self.h, path_b, 1 if direct else 0, int(threads), C.byref(h),
+                                       C.byref(step), meta, len(meta), C.byref(mlen)))
+        ck = DevCheckpoint._wrap(self, h)
+        raw = meta.raw[:mlen.value]
+        if mlen.value > len(meta):  # large meta section: fetch it whole
+            big = C.create_string_buffer(mlen.value)
+            h2 = _P()
+            _check(LIB.dqtg_ckpt_read_dqt1(self.h, path_b, 0, int(threads), C.byref(h2), None, big,
+                                           len(big), None))
+            LIB.dqtg_ckpt_destroy(h2)
+            raw = big.raw[:mlen.value]
+        return ck, step.value, parse_dqt1_meta(raw)
 
     @property
     def launches(self):
