@@ -103,11 +103,17 @@ dqtg_status dqtg_engine_create(int device, void* stream, dqtg_engine** out) {
             delete h;
             throw;
         }
+        h->e.owner = h;
+        h->e.deleter = [](void* o) { delete static_cast<dqtg_engine*>(o); };
         *out = h;
     });
 }
 
-void dqtg_engine_destroy(dqtg_engine* h) { delete h; }
+// drops the caller's reference; checkpoints/states/records still alive keep the
+// engine until they are destroyed
+void dqtg_engine_destroy(dqtg_engine* h) {
+    if (h) engine_release(&h->e);
+}
 
 dqtg_status dqtg_engine_sync(dqtg_engine* h) {
     return guard([&] {

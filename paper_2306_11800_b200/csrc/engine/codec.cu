@@ -223,7 +223,27 @@ __device__ __forceinline__ uint32_t keep_mask(int keep) {  // low `keep` bytes
     return keep >= 4 ? 0xffffffffu : (keep <= 0 ? 0u : (1u << (8 * keep)) - 1u);
 }
 
-template <bool HAS_BASE>
+// lanes of the warp holding the same NB-bit key: one ballot per key bit (keys are
+// < 2^NB; invalid elements carry 2^NB - 1, which no valid key reaches)
+template <int NB>
+__device__ __forceinline__ uint32_t peers_of(uint32_t key) {
+    uint32_t peers = 0xffffffffu;
+#pragma unroll
+    for (int bit = 0; bit < NB; ++bit) {
+        const bool on = (key >> bit) & 1u;
+        const uint32_t b = __ballot_sync(0xffffffffu, on);
+        peers &= on ? b : ~b;
+    }
+    return peers;
+}
+
+// MATCH.ANY is one instruction, but its unit is throughput-limited: the rank phase
+// stalled on its results.  Every third chunk ranks with ballots instead, which run
+// on the ALU/vote pipes (all-ballot ranks were slower, 0.785 vs 0.745 ms; one third:
+// 0.716 ms at C2).
+constexpr int kBallotEvery = 3;
+
+template <bool HAS_BASE, int NB>
 __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
     extern __shared__ __align__(16) uint8_t e1_dyn[];
     const uint32_t B = A.B, NS = A.NS;
@@ -364,7 +384,8 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
                 const uint32_t kdv = S.kd[e];
                 const uint32_t key = kdv & 0xffu;
                 const bool valid = key != 0xffu;
-                const uint32_t peers = __match_any_sync(0xffffffffu, key);
+                const uint32_t peers = (j % kBallotEvery) == kBallotEvery - 1
+                                           ? peers_of<NB>(key) : __match_any_sync(0xffffffffu, key);
                 if (valid && (peers & lt_mask) == 0) cc[j * B + key] = (uint16_t)__popc(peers);
                 pk[j] = __popc(peers & lt_mask) | (kdv << 8);  // rank | key << 8 | d << 16
             }
@@ -1658,7 +1679,9 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     const size_t e1_smem = e1_smem_bytes(B, NS);
     A.ntiles = ntiles;
     {
-        auto kfn = base ? enc_tile_kernel<true> : enc_tile_kernel<false>;
+        // ballot key width: keys < B, invalid elements 0xff -> 2^NB - 1 (> every key)
+        auto kfn = base ? (B <= 63 ? enc_tile_kernel<true, 6> : enc_tile_kernel<true, 7>)
+                        : (B <= 63 ? enc_tile_kernel<false, 6> : enc_tile_kernel<false, 7>);
         ensure_dyn_smem((const void*)kfn, e1_smem);
         DQTG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         int per_sm = 0;

@@ -71,6 +71,14 @@ void dump_timeline(Engine& e) {
     }
 }
 
+void engine_retain(Engine* e) { e->refs.fetch_add(1, std::memory_order_relaxed); }
+
+void engine_release(Engine* e) {
+    if (e->refs.fetch_sub(1, std::memory_order_acq_rel) != 1) return;
+    if (e->deleter) e->deleter(e->owner);
+    else delete e;
+}
+
 Engine::~Engine() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);

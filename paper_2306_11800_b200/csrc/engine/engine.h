@@ -2,6 +2,7 @@
 // device checkpoints, quantized states and records.
 #pragma once
 
+#include <atomic>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -68,6 +69,38 @@ struct BucketTab {
 
 struct Engine;
 
+// Counted reference to an engine.  Checkpoints, states and records keep their
+// engine alive (their destructors free through its stream-ordered pool), so the
+// owner may destroy the engine handle in any order relative to them (Python's
+// cycle collector finalises objects in arbitrary order).
+void engine_retain(Engine* e);
+void engine_release(Engine* e);
+class EngineRef {
+    Engine* p_ = nullptr;
+
+public:
+    EngineRef() = default;
+    EngineRef(Engine* e) : p_(e) {  // NOLINT: implicit by design
+        if (p_) engine_retain(p_);
+    }
+    EngineRef(const EngineRef& o) : EngineRef(o.p_) {}
+    EngineRef& operator=(Engine* e) {
+        if (e) engine_retain(e);
+        if (p_) engine_release(p_);
+        p_ = e;
+        return *this;
+    }
+    EngineRef& operator=(const EngineRef& o) { return *this = o.p_; }
+    ~EngineRef() {
+        if (p_) engine_release(p_);
+    }
+    Engine* get() const { return p_; }
+    Engine* operator->() const { return p_; }
+    Engine& operator*() const { return *p_; }
+    operator Engine*() const { return p_; }  // NOLINT
+    explicit operator bool() const { return p_ != nullptr; }
+};
+
 struct Layout {
     uint32_t nt = 0;
     std::vector<std::string> names;
@@ -94,7 +127,7 @@ struct Layout {
 std::shared_ptr<Layout> make_layout(Engine* e, const dqtg_layout* l);
 
 struct DevCkpt {
-    Engine* eng = nullptr;
+    EngineRef eng;
     std::shared_ptr<Layout> L;
     float* w = nullptr;
     float* ema = nullptr;  // derived-score mode
@@ -107,7 +140,7 @@ struct DevCkpt {
 };
 
 struct QState {
-    Engine* eng = nullptr;
+    EngineRef eng;
     std::shared_ptr<Layout> L;
     uint64_t step = 0;
     dqtg_config cfg{};
@@ -125,7 +158,7 @@ struct QState {
 };
 
 struct Record {
-    Engine* eng = nullptr;
+    EngineRef eng;
     uint8_t* d_buf = nullptr;
     uint64_t size = 0, cap = 0;
     std::vector<uint8_t> host;  // filled by decode-free host copies
@@ -134,6 +167,11 @@ struct Record {
 
 struct Engine {
     int device = 0;
+    // intrusive count (EngineRef): the creator holds one reference; the last release
+    // runs `deleter(owner)` (the C handle or the engine itself)
+    std::atomic<int> refs{1};
+    void* owner = nullptr;
+    void (*deleter)(void*) = nullptr;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     // the engine's own stream-ordered pool: blocks freed by this engine are reused

@@ -29,7 +29,11 @@ using namespace dqtg;
 
 struct dqtg_pipe {
     int device = 0;
-    std::vector<std::unique_ptr<Engine>> eng;
+    // worker engines: released (not deleted) so states handed out stay valid
+    struct Release {
+        void operator()(Engine* e) const { engine_release(e); }
+    };
+    std::vector<std::unique_ptr<Engine, Release>> eng;
     std::vector<std::unique_ptr<DevCkpt>> ck;  // per worker, rebuilt when the layout changes
 };
 
@@ -81,7 +85,7 @@ dqtg_status dqtg_pipe_create(int device, int workers, dqtg_pipe** out) {
         auto p = std::make_unique<dqtg_pipe>();
         p->device = device;
         for (int w = 0; w < workers; ++w) {
-            p->eng.push_back(std::make_unique<Engine>());
+            p->eng.push_back(std::unique_ptr<Engine, dqtg_pipe::Release>(new Engine()));
             init_engine(*p->eng.back(), device, nullptr);
         }
         p->ck.resize(workers);
