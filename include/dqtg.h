@@ -64,6 +64,8 @@ uint64_t dqtg_engine_launches(const dqtg_engine *e);
  * object {"kernel": [launches, total_ms], ...} (resets the accumulated spans). */
 dqtg_status dqtg_engine_profile(dqtg_engine *e, int enable);
 dqtg_status dqtg_engine_profile_report(dqtg_engine *e, char *json, uint64_t cap);
+/* host synchronisations of the engine stream so far and the host time blocked in them */
+void dqtg_engine_sync_stats(const dqtg_engine *e, uint64_t *syncs, double *blocked_ms);
 
 /* dqt::QuantConfig (quantize.hpp:13-26) */
 typedef struct dqtg_config {

@@ -133,6 +133,11 @@ dqtg_status dqtg_engine_profile(dqtg_engine* h, int enable) {
     });
 }
 
+void dqtg_engine_sync_stats(const dqtg_engine* h, uint64_t* syncs, double* blocked_ms) {
+    if (syncs) *syncs = h->e.sync_n;
+    if (blocked_ms) *blocked_ms = 1e-6 * (double)h->e.sync_ns;
+}
+
 dqtg_status dqtg_engine_profile_report(dqtg_engine* h, char* json, uint64_t cap) {
     return guard([&] {
         LOCK(&h->e);

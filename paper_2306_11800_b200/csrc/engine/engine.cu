@@ -1,3 +1,4 @@
+#include <chrono>
 // Engine plumbing: device/stream, scratch, alpha tables, layouts, object lifetimes.
 #include <algorithm>
 #include <cstdlib>
@@ -169,7 +170,11 @@ void Engine::d2h(void* dst, const void* src, size_t bytes) {
 }
 
 void Engine::sync() {
+    const auto t0 = std::chrono::steady_clock::now();
     DQTG_CUDA(cudaStreamSynchronize(stream));
+    sync_n++;
+    sync_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                   std::chrono::steady_clock::now() - t0).count();
     for (auto& p : pend) memcpy(p.dst, p.staged, p.n);
     pend.clear();
     while (stage_blocks.size() > 1) {  // keep the largest (last) block

@@ -185,6 +185,7 @@ struct Engine {
     void hi_done();         // joins: `stream` waits for hi_stream
     std::recursive_mutex mu;
     uint64_t launches = 0;
+    uint64_t sync_n = 0, sync_ns = 0;  // host syncs and time blocked in them
     uint32_t* d_err = nullptr;
     std::map<uint64_t, std::unique_ptr<AlphaTables>> tables;
     // grow-only scratch buffers keyed by name

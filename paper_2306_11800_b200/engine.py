@@ -82,6 +82,7 @@ def _load():
         "dqtg_engine_launches": (C.c_uint64, [_P]),
         "dqtg_engine_profile": (C.c_int, [_P, C.c_int]),
         "dqtg_engine_profile_report": (C.c_int, [_P, C.c_char_p, C.c_uint64]),
+        "dqtg_engine_sync_stats": (None, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]),
         "dqtg_sketch_range": (C.c_int, [C.c_double, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
         "dqtg_sketch_build": (C.c_int, [_P, _P, C.c_uint64, C.c_double, C.POINTER(C.c_uint64),
                                         _P, _P]),
@@ -392,6 +393,12 @@ class Engine:
     @property
     def launches(self):
         return LIB.dqtg_engine_launches(self.h)
+
+    def sync_stats(self):
+        """(host syncs so far, ms blocked in them)"""
+        n, ms = C.c_uint64(), C.c_double()
+        LIB.dqtg_engine_sync_stats(self.h, C.byref(n), C.byref(ms))
+        return n.value, ms.value
 
     def profile(self, enable=True):
         _check(LIB.dqtg_engine_profile(self.h, 1 if enable else 0))
