@@ -256,6 +256,25 @@ class DevCheckpoint:
     def tensor_offset(self, i):
         return LIB.dqtg_ckpt_tensor_offset(self.h, i)
 
+    def tensor_ptrs(self):
+        """Device pointers of the per-tensor weight slices (inputs to other calls)."""
+        base = self.weights_dev
+        return [base + 4 * self.tensor_offset(i) for i in range(len(self.meta.names))]
+
+    def _same_layout(self, other):
+        if other.meta.shapes != self.meta.shapes:
+            raise EngineError(4, "EMA/gradient checkpoint does not match the layout")
+
+    def set_ema_from(self, ema_ckpt):
+        """EMA from a device checkpoint (e.g. an ingested ema.dqt), copied in HBM."""
+        self._same_layout(ema_ckpt)
+        _check(LIB.dqtg_ckpt_set_ema(self.h, _ptr_array(ema_ckpt.tensor_ptrs())))
+
+    def update_ema_from(self, grads_ckpt, beta=0.9):
+        """ema_update (ranker.cpp:21-37) with gradients already in HBM."""
+        self._same_layout(grads_ckpt)
+        _check(LIB.dqtg_ckpt_update_ema(self.h, _ptr_array(grads_ckpt.tensor_ptrs()), beta))
+
     @classmethod
     def _wrap(cls, engine, h):
         """Adopt a checkpoint handle made by the engine (e.g. dqtg_ckpt_read_dqt1)."""
@@ -370,6 +389,14 @@ class Engine:
 
     def sync(self):
         _check(LIB.dqtg_engine_sync(self.h))
+
+    def read_ema_dqt1(self, path, direct=False, threads=0):
+        """ema_load (ranker.cpp:50-61) into HBM: (DevCheckpoint of the EMA, beta,
+        step_count); IoError when the beta/step_count meta is missing."""
+        ck, _, meta = self.read_dqt1(path, direct, threads)
+        if "beta" not in meta or "step_count" not in meta:
+            raise EngineError(6, f"{path}: missing beta/step_count meta")
+        return ck, float(meta["beta"]), int(meta["step_count"])
 
     def read_dqt1(self, path, direct=False, threads=0):
         """DQT1 file -> (DevCheckpoint, step, meta dict) via dqtg_ckpt_read_dqt1

@@ -187,3 +187,46 @@ def test_ingest_then_compress_matches_upload(eng, tmp_path):
     r1 = eng.encode_record(eng.quantize(ck, cfg, 1, step))
     r2 = eng.encode_record(eng.quantize(ref, cfg, 1, step))
     assert r1 == r2
+
+
+def test_ema_file_ingest(eng, tmp_path):
+    """ema_save (drop-in) -> read_ema_dqt1 -> set_ema_from: the quantized state equals
+    the one built from the host EMA arrays; update_ema_from matches host updates."""
+    from paper_2306_11800_b200 import dqt
+    from paper_2306_11800_b200 import engine as E
+
+    ts = rand_tensors(7, n=5, max_numel=100000)
+    names = [t[0] for t in ts]
+    rules = dqt.default_layer_rules()
+    types = [int(dqt.classify_layer_type(n, rules)) for n in names]
+    shapes = [t[2] for t in ts]
+    rng = np.random.default_rng(3)
+    grads = [rng.normal(0, 0.01, t[3].size).astype(np.float32) for t in ts]
+    g = dqt.Checkpoint()
+    for (name, _, shape, _), gr, lt in zip(ts, grads, types):
+        g.add_tensor(name, gr.reshape(shape), dqt.LayerType(lt))
+    ema = dqt.ema_init(0.8)
+    dqt.ema_update(ema, g)
+    p = str(tmp_path / "ema.dqt")
+    dqt.ema_save(p, ema)
+    eck, beta, count = eng.read_ema_dqt1(p)
+    assert beta == 0.8 and count == 1
+    w = [t[3] for t in ts]
+    a = eng.checkpoint(names, types, shapes, weights=w)
+    a.set_ema_from(eck)
+    b = eng.checkpoint(names, types, shapes, weights=w, ema=grads)
+    cfg = E.Config(metric=1)
+    assert eng.encode_record(eng.quantize(a, cfg, 1, 2)) == eng.encode_record(eng.quantize(b, cfg, 1, 2))
+    # a second gradient snapshot from a file, applied on the device
+    g2 = [rng.normal(0, 0.01, x.size).astype(np.float32) for x in w]
+    p2 = tmp_path / "g2.dqt"
+    p2.write_bytes(dqt1_bytes([(n, lt, s, x) for n, lt, s, x in zip(names, types, shapes, g2)]))
+    gck, _, _ = eng.read_dqt1(str(p2))
+    a.update_ema_from(gck, beta)
+    b.update_ema(g2, beta)
+    assert eng.encode_record(eng.quantize(a, cfg, 1, 3)) == eng.encode_record(eng.quantize(b, cfg, 1, 3))
+    p3 = tmp_path / "nometa.dqt"
+    p3.write_bytes(dqt1_bytes([(names[0], 6, shapes[0], w[0])]))
+    with pytest.raises(E.EngineError) as ex:
+        eng.read_ema_dqt1(str(p3))
+    assert ex.value.status == 6
