@@ -85,8 +85,24 @@ class ClockSampler:
         self.device = device
         self.proc = None
         self.lines = []
+        self.cpu = [0, 0]  # host CPU jiffies: steal, total (hypervisor steal of the VM)
+
+    @staticmethod
+    def _cpu_stat():
+        try:
+            with open("/proc/stat") as f:
+                v = [int(x) for x in f.readline().split()[1:]]
+            return v[7] if len(v) > 7 else 0, sum(v)
+        except Exception:
+            return 0, 0
+
+    def merge(self, other):
+        self.lines += other.lines
+        self.cpu = [a + b for a, b in zip(self.cpu, other.cpu)]
+        return self
 
     def __enter__(self):
+        self._c0 = self._cpu_stat()
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
@@ -104,6 +120,8 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        c1 = self._cpu_stat()
+        self.cpu = [self.cpu[0] + c1[0] - self._c0[0], self.cpu[1] + c1[1] - self._c0[1]]
         if self.proc:
             time.sleep(0.15)
             self.proc.terminate()
@@ -127,10 +145,12 @@ class ClockSampler:
             for n, v in zip(names, parts[2:6]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
+        steal = self.cpu[0] / self.cpu[1] if self.cpu[1] else None
         if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "host_cpu_steal_frac": steal}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "host_cpu_steal_frac": steal}
 
 
 # ---------------------------------------------------------------------------- reference arm
@@ -383,12 +403,16 @@ def run_ours(args):
     syncs0 = eng.sync_stats()[0]
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    mark = (lambda m: print(m, file=sys.stderr, flush=True)) if os.environ.get("DQTG_SYNC_TRACE") \
+        else (lambda m: None)
     with ClockSampler(local) as clocks:
+        mark("MARK sequential begin")
         t0.record(stream)
         for i in range(args.warmup + 1, args.warmup + 1 + args.steps):
             state = step(i, state)
         t1.record(stream)
         barrier()
+        mark("MARK sequential end")
     ms = t0.elapsed_time(t1)
     launches = eng.launches - launches0
     syncs_per_step = (eng.sync_stats()[0] - syncs0) / args.steps
@@ -413,6 +437,8 @@ def run_ours(args):
         # three timed passes of exactly K steps each; the median is reported (the
         # worker threads share the host CPU with the rest of the VM)
         pipe_reps = []
+        clocks_p = ClockSampler(local)
+        clocks_p.__enter__()
         for _ in range(3):
             l0 = cc.launches
             torch.cuda.synchronize()
@@ -422,6 +448,8 @@ def run_ours(args):
             torch.cuda.synchronize()
             pipe_reps.append((time.perf_counter() - tp0) * 1e3)
             launches_p = cc.launches - l0
+        clocks_p.__exit__(None, None, None)
+        clocks.merge(clocks_p)
         pipelined = sorted(pipe_reps)[1]
         del base, cc
     if pipelined is not None and pipelined < ms:

@@ -1510,9 +1510,10 @@ static void put_f64(std::vector<uint8_t>& v, double d) {
 void group_elems(Engine& e, const void* segs, const Layout& L, uint32_t B,
                  unsigned long long* elems);
 
-static bool crc_consts_ready = false;
-static void init_crc_consts() {
-    if (crc_consts_ready) return;
+static std::once_flag crc_consts_once;
+static void init_crc_consts_impl();
+static void init_crc_consts() { std::call_once(crc_consts_once, init_crc_consts_impl); }
+static void init_crc_consts_impl() {
     CrcX2N x = crc_x2n_table();
     uint32_t pw[kCB];
     for (int t = 0; t < kCB; ++t) pw[t] = crc_x2nmodp(x.t, (uint64_t)32 * (kCB - 1 - t), 3);
@@ -1540,7 +1541,7 @@ static void init_crc_consts() {
     }
     DQTG_CUDA(cudaMemcpyToSymbol(g_crc_nib, nib, sizeof(nib)));
     DQTG_CUDA(cudaMemcpyToSymbol(c_crc_x2n, x.t, sizeof(x.t)));
-    crc_consts_ready = true;
+
 }
 
 std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QState& target,
@@ -1885,6 +1886,19 @@ uint32_t crc32_device(Engine& e, const uint8_t* data, uint64_t n) {
     return h;
 }
 
+
+// Per-tile CRC shift constants of a layout, built once when the layout is made
+// (a lazy cudaMalloc on the first encode synchronised the device mid-step).
+void layout_crc_shift(Layout& L) {
+    if (L.d_crc_shift || L.tiles.empty()) return;
+    init_crc_consts();
+    const int ntiles = (int)L.tiles.size();
+    DQTG_CUDA(cudaMalloc(&L.d_crc_shift, (size_t)ntiles * 4 + 4));
+    crc_tile_shift_kernel<<<(ntiles + 255) / 256, 256>>>(L.d_tiles, ntiles, L.d_off, L.d_stream_off, L.N,
+                                                         L.d_crc_shift);
+    DQTG_CUDA(cudaGetLastError());
+    DQTG_CUDA(cudaStreamSynchronize(0));
+}
 
 static void ensure_crc_shift(Engine& e, const Layout& L) {
     if (L.d_crc_shift || L.tiles.empty()) return;

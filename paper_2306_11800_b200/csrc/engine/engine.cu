@@ -123,16 +123,33 @@ void* Engine::buf(const std::string& name, size_t bytes) {
             return slot.first;
         }
         if (slot.first) DQTG_CUDA(cudaFreeAsync(slot.first, stream));
-        size_t cap = bytes < 256 ? 256 : bytes + bytes / 4;
+        size_t cap = pool_size_class(bytes < 256 ? 256 : bytes + bytes / 4);
         DQTG_CUDA(cudaMallocFromPoolAsync(&slot.first, cap, pool, stream));
         slot.second = cap;
     }
     return slot.first;
 }
 
+// Pool requests are rounded to size classes (powers of two up to 1 MiB, then eighths
+// of the next power of two): steps whose record / protected-entry sizes wobble then
+// reuse the blocks the previous steps freed instead of growing the pool, which maps
+// new physical memory on the host thread (measured: 1-68 ms stalls mid-step).
+size_t pool_size_class(size_t n) {
+    if (n <= 256) return 256;
+    if (n <= (1u << 20)) {
+        size_t p = 256;
+        while (p < n) p <<= 1;
+        return p;
+    }
+    size_t p = 1;
+    while ((p << 1) <= n) p <<= 1;
+    const size_t step = p / 8;
+    return (n + step - 1) / step * step;
+}
+
 void* Engine::dalloc(size_t bytes) {
     void* p = nullptr;
-    DQTG_CUDA(cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, pool, stream));
+    DQTG_CUDA(cudaMallocFromPoolAsync(&p, pool_size_class(bytes ? bytes : 16), pool, stream));
     return p;
 }
 
@@ -169,12 +186,32 @@ void Engine::d2h(void* dst, const void* src, size_t bytes) {
     pend.push_back({dst, at, bytes});
 }
 
-void Engine::sync() {
+static thread_local std::chrono::steady_clock::time_point g_last_tp{};
+
+void Engine::tp(int line) {
+    static const bool trace = getenv("DQTG_SYNC_TRACE") != nullptr;
+    if (!trace) return;
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "tp %d %.1f us\n", line, std::chrono::duration<double, std::micro>(t - g_last_tp).count());
+    g_last_tp = std::chrono::steady_clock::now();
+}
+
+void Engine::sync(const char* fn, int line) {
+    static const bool trace = getenv("DQTG_SYNC_TRACE") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
     DQTG_CUDA(cudaStreamSynchronize(stream));
+    const auto t1 = std::chrono::steady_clock::now();
     sync_n++;
-    sync_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
-                   std::chrono::steady_clock::now() - t0).count();
+    sync_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+    if (trace) {
+        static thread_local std::chrono::steady_clock::time_point last{};
+        const double host = last.time_since_epoch().count()
+                                ? std::chrono::duration<double, std::micro>(t0 - last).count() : 0.0;
+        fprintf(stderr, "sync %-28s:%-5d host %8.1f us blocked %8.1f us\n", fn, line, host,
+                std::chrono::duration<double, std::micro>(t1 - t0).count());
+        last = std::chrono::steady_clock::now();
+        g_last_tp = last;
+    }
     for (auto& p : pend) memcpy(p.dst, p.staged, p.n);
     pend.clear();
     while (stage_blocks.size() > 1) {  // keep the largest (last) block
@@ -184,10 +221,10 @@ void Engine::sync() {
     stage_used = 0;
 }
 
-void Engine::check_err() {
+void Engine::check_err(const char* fn, int line) {
     uint32_t h = 0;
     d2h(&h, d_err, 4);
-    sync();
+    sync(fn, line);
     if (!h) return;
     DQTG_CUDA(cudaMemsetAsync(d_err, 0, 4, stream));
     if (h & kErrNonFinite) throw Fail(DQTG_NON_FINITE, "input contains NaN/Inf");
@@ -463,6 +500,7 @@ std::shared_ptr<Layout> make_layout(Engine* e, const dqtg_layout* l) {
     L->d_numel = upload_vec(L->numel);
     L->d_tile0 = upload_vec(L->tile0);
     L->d_stream_off = upload_vec(soff);
+    layout_crc_shift(*L);
     return L;
 }
 

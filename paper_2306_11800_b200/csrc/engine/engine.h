@@ -125,6 +125,8 @@ struct Layout {
 };
 
 std::shared_ptr<Layout> make_layout(Engine* e, const dqtg_layout* l);
+void layout_crc_shift(Layout& L);  // per-tile CRC shift constants (codec.cu)
+size_t pool_size_class(size_t n);   // rounding of stream-ordered pool requests
 
 struct DevCkpt {
     EngineRef eng;
@@ -223,7 +225,11 @@ struct Engine {
     // pageable destination would make the driver stage the copy synchronously,
     // which serialises host threads driving other engines.)
     void d2h(void* dst, const void* src, size_t bytes);
-    void sync();  // stream sync + pending read-backs
+    // stream sync + pending read-backs (DQTG_SYNC_TRACE=1: call site, host time since
+    // the previous sync returned, time blocked, on stderr)
+    void sync(const char* fn = __builtin_FUNCTION(), int line = __builtin_LINE());
+    // DQTG_SYNC_TRACE: host time since the previous sync / trace point (diagnostics)
+    void tp(int line = __builtin_LINE());
     struct PendingD2H {
         void* dst;
         const void* staged;
@@ -233,7 +239,7 @@ struct Engine {
     std::vector<std::pair<uint8_t*, size_t>> stage_blocks;  // pinned; last = current
     size_t stage_used = 0;
     void launched(int n = 1) { launches += n; }
-    void check_err();  // reads + clears the device error word (syncs)
+    void check_err(const char* fn = __builtin_FUNCTION(), int line = __builtin_LINE());  // reads + clears the device error word (syncs)
     // copy host-or-device memory into a device destination
     void to_device(void* dst, const void* src_any, size_t bytes);
     void from_device(void* dst_any, const void* src_dev, size_t bytes);
