@@ -184,6 +184,12 @@ typedef struct dqtg_record dqtg_record;
 dqtg_status dqtg_encode_record(dqtg_engine *e, const dqtg_qstate *base,
                                const dqtg_qstate *target, double quality_delta,
                                dqtg_record **out);
+/* payload_bytes_pe / _rle / _he (codec.cpp:615-646): encode_tensor_payload bytes of
+ * the delta base -> target summed over tensors (variant 0), or the Huffman payload
+ * size of the un-rearranged RLE stream (1) / of the raw deltas (2), computed by the
+ * device encoder in its ablation modes; no record is written. */
+dqtg_status dqtg_payload_bytes(dqtg_engine *e, const dqtg_qstate *base, const dqtg_qstate *target,
+                               int variant, uint64_t *bytes);
 uint64_t dqtg_record_size(const dqtg_record *r);
 dqtg_status dqtg_record_copy(const dqtg_record *r, void *dst_host);
 const uint8_t *dqtg_record_dev(const dqtg_record *r);

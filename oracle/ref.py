@@ -68,3 +68,29 @@ def qstate(q) -> QState:
 def tensors_of(ck):
     return [Tensor(t.name, int(t.type), tuple(t.shape), np.asarray(t.data, np.float32).ravel())
             for t in ck.tensors]
+
+
+def payload_bytes(base: QState, target: QState, variant: int) -> int:
+    """payload_bytes_pe / _rle / _he of the reference (oracle/ref_extra.cpp)."""
+    import ctypes as C
+
+    lib = C.CDLL(os.path.join(REF_DIR, "libdqtref_extra.so"))
+    fn = lib.ref_payload_bytes
+    fn.restype = C.c_uint64
+    nt = len(target.levels)
+    types = np.array([int(t) for t in target.types] or [0], np.uint8)
+    numel = np.array([np.asarray(lv).size for lv in target.levels] or [0], np.uint64)
+    keep = []
+
+    def ptrs(q):
+        arr = [np.ascontiguousarray(np.asarray(lv).ravel(), np.uint16) for lv in q.levels]
+        keep.append(arr)
+        return (C.c_void_p * max(nt, 1))(*[a.ctypes.data for a in arr])
+
+    def cbl(q):
+        a = np.array([len(c) for c in q.codebooks], np.uint32)
+        keep.append(a)
+        return a.ctypes.data
+
+    return int(fn(int(variant), nt, C.c_void_p(types.ctypes.data), C.c_void_p(numel.ctypes.data),
+                  ptrs(base), C.c_void_p(cbl(base)), ptrs(target), C.c_void_p(cbl(target))))

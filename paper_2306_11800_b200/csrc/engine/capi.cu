@@ -502,6 +502,16 @@ dqtg_status dqtg_encode_record(dqtg_engine* h, const dqtg_qstate* base, const dq
     });
 }
 
+dqtg_status dqtg_payload_bytes(dqtg_engine* h, const dqtg_qstate* base, const dqtg_qstate* target,
+                               int variant, uint64_t* bytes) {
+    return guard([&] {
+        LOCK(&h->e);
+        DQTG_REQUIRE(variant >= 0 && variant <= 2, DQTG_ERROR, "payload_bytes variant must be 0, 1 or 2");
+        DQTG_REQUIRE(base != nullptr, DQTG_ERROR, "payload_bytes needs a base state");
+        encode_record_ex(h->e, base->q.get(), *target->q, 0.0, 0, 0, nullptr, variant, bytes);
+    });
+}
+
 uint64_t dqtg_record_size(const dqtg_record* r) { return r->r->size; }
 
 dqtg_status dqtg_record_copy(const dqtg_record* r, void* dst) {

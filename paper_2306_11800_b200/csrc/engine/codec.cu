@@ -67,6 +67,10 @@ struct EncArgs {
     uint32_t* crc_acc;
     uint32_t* tile_crc;  // per tile, zero register, ending at the tile's last byte
     uint32_t* err;
+    // payload_bytes ablations (codec.cpp:601-646): 0 = record (rearranged groups),
+    // 1 = one group per tensor (no rearrange), 2 = one group and no RLE (every
+    // element its own run)
+    uint32_t mode;
 };
 
 __device__ __forceinline__ uint32_t uvlen(unsigned long long v) {
@@ -339,7 +343,8 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
                 const uint32_t lt = __vcmpltu4(pw[j], cw[j]);
                 const uint32_t dw = __vadd4(__vsub4(pw[j], cw[j]), lt & Brep);
                 const uint32_t vm = keep_mask((int)nv - 4 * j);
-                const uint32_t key = (pw[j] & vm) | ~vm;  // invalid elements: key 0xff
+                // invalid elements: key 0xff; ablation modes group by nothing (key 0)
+                const uint32_t key = ((A.mode ? 0u : pw[j]) & vm) | ~vm;
                 kd[2 * j] = __byte_perm(key, dw, 0x5140);
                 kd[2 * j + 1] = __byte_perm(key, dw, 0x7362);
             }
@@ -463,6 +468,7 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
                          (byte_msbs(__vcmpne4(x.z, __funnelshift_l(x.y, x.z, 8))) << 8) |
                          (byte_msbs(__vcmpne4(x.w, __funnelshift_l(x.z, x.w, 8))) << 12);
             m |= (S.gs[tid >> 1] >> ((tid & 1) * 16)) & 0xffffu;
+            if (A.mode == 2) m = 0xffffu;  // no RLE: every element starts a run
             if (p0 + kIt > cnt) m &= p0 >= cnt ? 0u : (1u << (cnt - p0)) - 1u;
             unsigned long long tot;
             uint32_t r = (uint32_t)block_exclusive_scan<unsigned long long>(__popc(m), s_scan, &tot);
@@ -646,7 +652,7 @@ __global__ void __launch_bounds__(kCB) enc_resolve_big_kernel(EncArgs A, const u
         if (lane == 0) excl = -1;
         const int prev = max(before, excl);
         if (idx >= 0)
-            A.segs[(size_t)i * B + b].cont = prev >= 0 && A.segs[(size_t)prev * B + b].lv == S.fv;
+            A.segs[(size_t)i * B + b].cont = A.mode != 2 && prev >= 0 && A.segs[(size_t)prev * B + b].lv == S.fv;
         int cl = carry_last;
         for (int w = 0; w < kCB / 32; ++w) cl = max(cl, s_wmax[w]);
         __syncthreads();
@@ -687,7 +693,7 @@ __global__ void __launch_bounds__(kCB) enc_resolve_big_kernel(EncArgs A, const u
         RunM nxt = shfl_down_runm(x, 1);  // suffix starting at the next lane
         RunM after = lane < 31 ? runm_combine(nxt, later) : later;
         if (i < a1 && S.n) {
-            unsigned long long E = (after.n && after.fv == S.lv) ? after.lead : 0ull;
+            unsigned long long E = (A.mode != 2 && after.n && after.fv == S.lv) ? after.lead : 0ull;
             const bool single = S.lead == S.n;
             Seg& G = A.segs[(size_t)i * B + b];
             if (single) {
@@ -756,7 +762,7 @@ __global__ void __launch_bounds__(kResolveWarps * 32) enc_resolve_kernel(EncArgs
         if (lane == 0) prev = -1;
         prev = max(prev, carry_last);
         if (idx >= 0) {
-            S->cont = prev >= 0 && A.segs[(size_t)prev * B + b].lv == S->fv;
+            S->cont = A.mode != 2 && prev >= 0 && A.segs[(size_t)prev * B + b].lv == S->fv;
             any = true;
         }
         carry_last = max(carry_last, __shfl_sync(0xffffffffu, x, 31));
@@ -790,7 +796,7 @@ __global__ void __launch_bounds__(kResolveWarps * 32) enc_resolve_kernel(EncArgs
         RunM nxt = shfl_down_runm(x, 1);
         RunM after = lane < 31 ? runm_combine(nxt, carry) : carry;
         if (in && S.n) {
-            const unsigned long long E = (after.n && after.fv == S.lv) ? after.lead : 0ull;
+            const unsigned long long E = (A.mode != 2 && after.n && after.fv == S.lv) ? after.lead : 0ull;
             Seg& G = A.segs[(size_t)ii * B + b];
             if (S.lead == S.n) {
                 G.lead_total = G.trail_total = S.n + E;
@@ -1169,6 +1175,7 @@ struct TensorRec {
     unsigned long long prot_begin, prot_end;    // protected entry range
     unsigned long long size, off;               // record bytes / offset
     uint32_t ngroups, pad;
+    unsigned long long payload;                 // encode_tensor_payload bytes (or ablation size)
 };
 
 __device__ __forceinline__ uint32_t tensor_of_entry(const TensorRec* tr, uint32_t nt,
@@ -1227,6 +1234,12 @@ __global__ void tensor_size_kernel(EncArgs A, TensorRec* tr, const unsigned long
     }
     R.ngroups = ng;
     R.size = s + uvlen(ng) + gs;
+    if (A.mode == 0) {
+        R.payload = uvlen(ng) + gs;  // encode_tensor_payload (codec.cpp:308-327)
+    } else {  // huffman_payload_size (codec.cpp:601-613) of the single group
+        const GroupInfo& G = gi[t * B];
+        R.payload = ng ? gs - 1 - uvlen(G.n_elems) : 3;  // minus uv(bucket 0), uv(n)
+    }
 }
 
 __global__ void tensor_scan_kernel(TensorRec* tr, uint32_t nt, unsigned long long prefix,
@@ -1546,7 +1559,7 @@ static void init_crc_consts_impl() {
 
 std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QState& target,
                                       double quality) {
-    return encode_record_ex(e, base, target, quality, 0, 0, nullptr);
+    return encode_record_ex(e, base, target, quality, 0, 0, nullptr, 0, nullptr);
 }
 
 // B_override / nt_total: a shard of a tensor-sharded checkpoint encodes its tensor
@@ -1554,7 +1567,7 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
 // bytes [body_offset, size-4) of every rank concatenate into the single-GPU record.
 std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QState& target,
                                          double quality, uint32_t B_override, uint32_t nt_total,
-                                         uint64_t* body_offset) {
+                                         uint64_t* body_offset, int mode, uint64_t* payload_total) {
     const Layout& L = *target.L;
     if (base) {
         const Layout& BL = *base->L;
@@ -1628,6 +1641,10 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
 
     auto rec = std::make_unique<Record>();
     rec->eng = &e;
+    if (nt == 0 && payload_total) {
+        *payload_total = 0;
+        return nullptr;
+    }
     if (nt == 0) {
         // no tensors: prefix + CRC of the empty stream
         std::vector<uint8_t> host = pre;
@@ -1673,6 +1690,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     A.tile_crc = (uint32_t*)e.buf("e.tile_crc", (size_t)ntiles * 4 + 4);
     A.tile_ctr = (unsigned int*)(small + 5);
     A.err = e.d_err;
+    A.mode = (uint32_t)mode;
     DQTG_CUDA(cudaMemsetAsync(A.freq, 0, freq_n * 4, st));
     DQTG_CUDA(cudaMemsetAsync(small, 0, 64, st));
 
@@ -1810,6 +1828,14 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     e.launched(3);
     unsigned long long total = 0;
     e.d2h(&total, total_d, 8);
+    if (payload_total) {  // sizes only (payload_bytes_*): no record is written
+        std::vector<TensorRec> th(nt);
+        e.d2h(th.data(), tr, nt * sizeof(TensorRec));
+        e.check_err();
+        *payload_total = 0;
+        for (auto& r : th) *payload_total += r.payload;
+        return nullptr;
+    }
     e.check_err();  // syncs
 
     // ---- writers

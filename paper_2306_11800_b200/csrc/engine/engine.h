@@ -294,9 +294,11 @@ void shard_stage2(Engine& e, const DevCkpt& c, const dqtg_config& cfg,
 std::unique_ptr<QState> shard_stage3(Engine& e, const DevCkpt& c, const dqtg_config& cfg,
                                      uint64_t seed, uint64_t step,
                                      const unsigned long long* value_hist);
+// mode / payload_total: payload_bytes_* ablation sizes instead of a record (codec.cu)
 std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QState& target,
                                          double quality, uint32_t B_override, uint32_t nt_total,
-                                         uint64_t* body_offset);
+                                         uint64_t* body_offset, int mode = 0,
+                                         uint64_t* payload_total = nullptr);
 void eval_batch(Engine& e, const DevCkpt& c, const dqtg_config* cfgs, const uint64_t* seeds,
                 uint32_t m, double* quality, double* est);
 void approx_kmeans(Engine& e, const float* values_any, uint64_t n, uint32_t k, double sigma,

@@ -121,6 +121,7 @@ def _load():
         "dqtg_dequantize": (C.c_int, [_P, _P, _P]),
         "dqtg_encode_record": (C.c_int, [_P, _P, _P, C.c_double, C.POINTER(_P)]),
         "dqtg_record_size": (C.c_uint64, [_P]),
+        "dqtg_payload_bytes": (C.c_int, [_P, _P, _P, C.c_int, C.POINTER(C.c_uint64)]),
         "dqtg_record_copy": (C.c_int, [_P, _P]),
         "dqtg_record_dev": (_P, [_P]),
         "dqtg_record_destroy": (None, [_P]),
@@ -499,6 +500,12 @@ class Engine:
             return out.tobytes()
         finally:
             LIB.dqtg_record_destroy(r)
+
+    def payload_bytes(self, base: DevState, target: DevState, variant=0) -> int:
+        """payload_bytes_pe (0) / _rle (1) / _he (2) (codec.cpp:615-646) on the device."""
+        n = C.c_uint64()
+        _check(LIB.dqtg_payload_bytes(self.h, base.h, target.h, int(variant), C.byref(n)))
+        return n.value
 
     def encode_record_handle(self, target, base=None, quality=0.0):
         r = _P()

@@ -144,8 +144,10 @@ def test_quantize_and_records_match_reference(oracle, ref, ci):
     assert np.array_equal(recon, flat(ref.tensors_of(ref_recon)))
     assert oracle.proxy_quality(t2, recon) == d.proxy_quality_delta(c2, ref_recon)
     assert oracle.estimate_compression(t2, q2) == d.estimate_compression(c2, rq2)
+    # ablation sizes (codec.cpp:615-646) against the reference's own functions
     for variant in range(3):
-        assert oracle.payload_bytes(q1, q2, variant) >= 0
+        assert oracle.payload_bytes(q1, q2, variant) == ref.payload_bytes(q1, q2, variant)
+        assert oracle.payload_bytes(q2, q1, variant) == ref.payload_bytes(q2, q1, variant)
 
 
 def test_config_hash_and_seed(oracle):
