@@ -147,14 +147,74 @@ size_t pool_size_class(size_t n) {
     return (n + step - 1) / step * step;
 }
 
+constexpr size_t kBigBlock = 32u << 20;
+constexpr size_t kBigKeep = 12;  // cached blocks per (device, size class)
+
+namespace {
+struct BigBlock {
+    void* p;
+    size_t cls;
+    int device;
+    cudaEvent_t ev;  // recorded on the freeing stream
+};
+struct BigCache {
+    std::mutex mu;
+    std::map<void*, std::pair<size_t, int>> live;  // block -> (size class, device)
+    std::vector<BigBlock> free;
+};
+BigCache& big_cache() {
+    static BigCache* c = new BigCache();  // process lifetime (blocks outlive engines)
+    return *c;
+}
+}  // namespace
+
 void* Engine::dalloc(size_t bytes) {
     void* p = nullptr;
-    DQTG_CUDA(cudaMallocFromPoolAsync(&p, pool_size_class(bytes ? bytes : 16), pool, stream));
+    const size_t cls = pool_size_class(bytes ? bytes : 16);
+    if (cls >= kBigBlock) {
+        BigCache& bc = big_cache();
+        std::lock_guard<std::mutex> g(bc.mu);
+        for (size_t i = bc.free.size(); i-- > 0;)
+            if (bc.free[i].cls == cls && bc.free[i].device == device) {
+                BigBlock b = bc.free[i];
+                bc.free.erase(bc.free.begin() + (long)i);
+                DQTG_CUDA(cudaStreamWaitEvent(stream, b.ev, 0));
+                cudaEventDestroy(b.ev);
+                bc.live[b.p] = {cls, device};
+                return b.p;
+            }
+    }
+    DQTG_CUDA(cudaMallocFromPoolAsync(&p, cls, pool, stream));
+    if (cls >= kBigBlock) {
+        BigCache& bc = big_cache();
+        std::lock_guard<std::mutex> g(bc.mu);
+        bc.live[p] = {cls, device};
+    }
     return p;
 }
 
 void Engine::dfree(void* p) {
-    if (p) cudaFreeAsync(p, stream);
+    if (!p) return;
+    BigCache& bc = big_cache();
+    {
+        std::lock_guard<std::mutex> g(bc.mu);
+        auto it = bc.live.find(p);
+        if (it != bc.live.end()) {
+            const size_t cls = it->second.first;
+            bc.live.erase(it);
+            size_t same = 0;
+            for (auto& b : bc.free) same += b.cls == cls && b.device == device;
+            cudaEvent_t ev;
+            if (same < kBigKeep && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) {
+                if (cudaEventRecord(ev, stream) == cudaSuccess) {
+                    bc.free.push_back(BigBlock{p, cls, device, ev});
+                    return;
+                }
+                cudaEventDestroy(ev);
+            }
+        }
+    }
+    cudaFreeAsync(p, stream);
 }
 
 void* Engine::host_pinned(size_t bytes) {
@@ -192,7 +252,9 @@ void Engine::tp(int line) {
     static const bool trace = getenv("DQTG_SYNC_TRACE") != nullptr;
     if (!trace) return;
     const auto t = std::chrono::steady_clock::now();
-    fprintf(stderr, "tp %d %.1f us\n", line, std::chrono::duration<double, std::micro>(t - g_last_tp).count());
+    const double us = g_last_tp.time_since_epoch().count()
+                          ? std::chrono::duration<double, std::micro>(t - g_last_tp).count() : -1.0;
+    fprintf(stderr, "tp %d %.1f us %p\n", line, us, (void*)this);
     g_last_tp = std::chrono::steady_clock::now();
 }
 

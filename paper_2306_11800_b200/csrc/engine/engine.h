@@ -7,6 +7,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -219,6 +220,12 @@ struct Engine {
     // stream-ordered pool allocations for per-step objects (states, records)
     void* dalloc(size_t bytes);
     void dfree(void* p);
+    // Large per-step blocks (quantized level arrays) are recycled through a per-device
+    // cache shared by all engines (engine.cu: BigCache): a freed block is kept with an
+    // event on the freeing stream and handed to the next request of its size class
+    // after the requesting stream waits on that event.  Growing the stream-ordered
+    // pools mid-step mapped new memory on the host thread (measured 11-470 ms stalls
+    // in the worker pool).
     void* host_pinned(size_t bytes);
     // Device->host read-back through a pinned staging arena: the copy is queued on
     // the engine stream and lands in `dst` at the next sync()/check_err().  (A

@@ -165,6 +165,29 @@ __device__ __forceinline__ void hist_add_pos_s(uint32_t* sh, unsigned long long*
     else hist_add_pos(sh, gh, v, t, err);
 }
 
+// Branch-free insertion of a non-negative value into a positive window histogram
+// through the shared compact table (shared-window addresses precomputed): returns
+// false when the value needs the exact path (outside the table, special cell, NaN,
+// outside the window) -- the caller batches those.  The table has a sentinel entry
+// at index ctab_n with both special bits set, so the range check is a min().
+struct FastPos {
+    uint32_t shift, lo, n, offmask, ctab_s;
+};
+__device__ __forceinline__ FastPos fast_pos(const BucketTab& t, const uint32_t* s_ctab) {
+    return FastPos{t.cell_shift, t.ctab_lo, t.ctab_n, (1u << t.cell_shift) - 1u,
+                   (uint32_t)__cvta_generic_to_shared(s_ctab)};
+}
+__device__ __forceinline__ bool hist_fast_pos(uint32_t win_s, uint32_t b, const FastPos& f) {
+    const uint32_t rel = min((b >> f.shift) - f.lo, f.n);
+    uint32_t c;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(c) : "r"(f.ctab_s + 4 * rel));
+    const uint32_t hi = (b & f.offmask) > ((c >> 13) & 0x1ffffu) ? 1u : 0u;
+    const uint32_t p = (c & 0x1fffu) + hi;
+    const bool ok = !((c >> (31 - hi)) & 1u) && p <= (uint32_t)kWin;
+    if (ok) asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(win_s + 4 * p) : "memory");
+    return ok;
+}
+
 __device__ __forceinline__ void hist_flush_pos(uint32_t* sh, unsigned long long* gh,
                                                const BucketTab& t) {
     for (int w = threadIdx.x; w < kPosSlots; w += blockDim.x) {

@@ -86,9 +86,14 @@ __global__ void __launch_bounds__(kPB, 5) pass_a_kernel(PassIn a, unsigned long 
     uint32_t* s_ctab = sh + 2 * W;  // compact slot table (a.tab.ctab_n words)
     const bool fastc = a.tab.ctab != nullptr;
     for (int i = threadIdx.x; i < 2 * W; i += blockDim.x) sh[i] = 0;
-    if (fastc)
+    if (fastc) {
         for (uint32_t i = threadIdx.x; i < a.tab.ctab_n; i += blockDim.x) s_ctab[i] = __ldg(a.tab.ctab + i);
+        if (threadIdx.x == 0) s_ctab[a.tab.ctab_n] = 0xc0000000u;  // sentinel: exact path
+    }
     __syncthreads();
+    const FastPos fp = fast_pos(a.tab, s_ctab);
+    const uint32_t shm_s = (uint32_t)__cvta_generic_to_shared(shm);
+    const uint32_t shs_s = (uint32_t)__cvta_generic_to_shared(shs);
     __shared__ int s_base;
     int cur = -1;
     auto flush = [&](int lt) {
@@ -145,9 +150,11 @@ __global__ void __launch_bounds__(kPB, 5) pass_a_kernel(PassIn a, unsigned long 
                         if (dm) hist_add(shm, gm, m[j], a.tab, a.err);
                         if (ds) hist_add(shs, gs, s[j], a.tab, a.err);
                     }
-                } else if (fastc) {
-                    if (dm) hist_add_pos_s(shm, gm, m[j], a.tab, a.err, s_ctab);
-                    if (ds) hist_add_pos_s(shs, gs, s[j], a.tab, a.err, s_ctab);
+                } else if (fastc) {  // branch-free table path; exact path for the rest
+                    if (dm && !hist_fast_pos(shm_s, __float_as_uint(m[j]), fp))
+                        hist_add_pos(shm, gm, m[j], a.tab, a.err);
+                    if (ds && !hist_fast_pos(shs_s, __float_as_uint(s[j]), fp))
+                        hist_add_pos(shs, gs, s[j], a.tab, a.err);
                 } else {
                     if (dm) hist_add_pos(shm, gm, m[j], a.tab, a.err);
                     if (ds) hist_add_pos(shs, gs, s[j], a.tab, a.err);
@@ -770,7 +777,7 @@ static void stage_pass_a(Engine& e, const DevCkpt& c, const PassIn& a, uint32_t 
     const int ntiles = a.ntiles;
     cudaStream_t st = e.stream;
     DQTG_CUDA(cudaMemsetAsync(a.tile_ctr, 0, 4, st));
-    const size_t ct = a.tab.ctab ? (size_t)a.tab.ctab_n * 4 : 0;
+    const size_t ct = a.tab.ctab ? ((size_t)a.tab.ctab_n + 1) * 4 : 0;  // + sentinel
     if (c.explicit_scores) {
         const size_t smem = (size_t)2 * kWinSlots * 4 + ct;
         const int grid = stream_grid(e, ntiles, 3);
