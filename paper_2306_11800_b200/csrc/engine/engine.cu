@@ -122,8 +122,11 @@ void* Engine::buf(const std::string& name, size_t bytes) {
             slot.second = cap;
             return slot.first;
         }
+        // at least double on growth: data-dependent scratch (overflow runs, protected
+        // entries, k-means keys) would otherwise grow by small steps, and every growth
+        // maps pool memory on the host thread mid-step
+        size_t cap = pool_size_class(std::max(bytes < 256 ? 256 : bytes + bytes / 4, 2 * slot.second));
         if (slot.first) DQTG_CUDA(cudaFreeAsync(slot.first, stream));
-        size_t cap = pool_size_class(bytes < 256 ? 256 : bytes + bytes / 4);
         DQTG_CUDA(cudaMallocFromPoolAsync(&slot.first, cap, pool, stream));
         slot.second = cap;
     }
