@@ -1249,8 +1249,9 @@ int dqo_huffman_decode(const int64_t *tsym, const uint8_t *tlen, size_t tsize,
         if (tlen[i] < tlen[i - 1] || (tlen[i] == tlen[i - 1] && tsym[i] <= tsym[i - 1]))
             return DQO_ERR_CORRUPT_BITSTREAM;
     tentry *t = malloc(tsize * sizeof(tentry));
-    for (size_t i = 0; i < tsize; ++i) t[i].sym = tsym[i], t[i].len = tlen[i];
     uint64_t *codes = malloc(tsize * 8);
+    if (!t || !codes) { free(t); free(codes); return DQO_ERR; }
+    for (size_t i = 0; i < tsize; ++i) t[i].sym = tsym[i], t[i].len = tlen[i];
     uint8_t ml;
     int rc = assign_codes(t, tsize, codes, &ml);
     if (rc) { free(t); free(codes); return rc; }
