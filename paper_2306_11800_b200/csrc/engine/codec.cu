@@ -907,15 +907,18 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
                                                           uint8_t* len_ov, HufWork W,
                                                           uint32_t n_pad,
                                                           const unsigned long long* ov_range) {
-    // working set in shared memory (the tree build is a serial chain): n_pad >= n
+    // working set in shared memory (the tree build is a serial chain): n_pad >= n.
+    // 32-bit frequencies / node weights / symbols (the host guarantees tensors below
+    // 2^31 elements) and 8-bit depths (saturated; >= 63 is an error anyway) keep it
+    // at 38 B per slot, so more single-warp CTAs stay resident per SM.
     extern __shared__ unsigned long long s_keys[];  // n_pad
     __shared__ uint32_t s_hist[65], s_at[65];
-    unsigned long long* f = s_keys + n_pad;          // n_pad
-    unsigned long long* nodef = f + n_pad;           // 2 n_pad
-    long long* sym = (long long*)(nodef + 2 * n_pad);  // n_pad
+    uint32_t* nodef = (uint32_t*)(s_keys + n_pad);   // 2 n_pad
+    uint32_t* parent = nodef + 2 * n_pad;            // 2 n_pad
+    uint32_t* f = parent + 2 * n_pad;                // n_pad
+    int32_t* sym = (int32_t*)(f + n_pad);            // n_pad
     uint32_t* perm = (uint32_t*)(sym + n_pad);       // n_pad
-    uint32_t* parent = perm + n_pad;                 // 2 n_pad
-    uint32_t* depth = parent + 2 * n_pad;            // 2 n_pad
+    uint8_t* depth = (uint8_t*)(perm + n_pad);       // 2 n_pad
     const uint32_t B = A.B, NS = A.NS;
     const uint32_t tb = blockIdx.x, b = tb % B;
     GroupInfo G{};
@@ -934,14 +937,14 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
     if (G.n_elems) {
         for (uint32_t i0 = 0; i0 < B + kLD; i0 += 32) {
             const uint32_t i = i0 + lane;
-            long long sv = 0;
-            unsigned long long fv = 0;
+            int32_t sv = 0;
+            uint32_t fv = 0;
             if (i < B) {  // value -(B-1-i)
                 fv = fr[B - 1 - i];
-                sv = -(long long)(B - 1 - i);
+                sv = -(int32_t)(B - 1 - i);
             } else if (i < B + kLD && i - B >= 2) {
                 fv = fr[i];
-                sv = (long long)(i - B);
+                sv = (int32_t)(i - B);
             }
             const uint32_t m = __ballot_sync(0xffffffffu, fv != 0);
             if (fv) {
@@ -954,8 +957,8 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
         for (unsigned long long j0 = G.ov_begin; j0 < G.ov_end; j0 += 32) {
             const unsigned long long j = j0 + lane;
             if (j < G.ov_end) {
-                sym[n + lane] = (long long)(ukey[j] & 0xffffffffull);
-                f[n + lane] = ucnt[j];
+                sym[n + lane] = (int32_t)(ukey[j] & 0x7fffffffull);
+                f[n + lane] = (uint32_t)ucnt[j];
             }
             n += (uint32_t)min(32ull, G.ov_end - j0);
         }
@@ -969,7 +972,7 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
     uint32_t np2 = 1;
     while (np2 < n) np2 <<= 1;
     for (uint32_t i = threadIdx.x; i < np2; i += blockDim.x)
-        s_keys[i] = i < n ? ((f[i] << 24) | i) : ~0ull;
+        s_keys[i] = i < n ? (((unsigned long long)f[i] << 24) | i) : ~0ull;
     __syncthreads();
     for (uint32_t k = 2; k <= np2; k <<= 1)
         for (uint32_t j = k >> 1; j > 0; j >>= 1) {
@@ -1018,8 +1021,9 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
             depth[root] = 0;
             bool overflow = false;
             for (int i = (int)root - 1; i >= 0; --i) {
-                depth[i] = depth[parent[i]] + 1;
-                if ((uint32_t)i >= n && depth[i] >= 63) overflow = true;
+                const uint32_t d = depth[parent[i]] + 1u;
+                depth[i] = (uint8_t)(d < 255u ? d : 255u);
+                if ((uint32_t)i >= n && d >= 63) overflow = true;
             }
             if (overflow) atomicOr(A.err, kErrHuffmanDepth);
         }
@@ -1045,7 +1049,7 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
             tab_sym[G.tab_base + o] = sym[i];
             tab_len[G.tab_base + o] = (uint8_t)len;
             hdr += uvlen(zigzag(sym[i])) + 1;
-            const long long s = sym[i];
+            const long long s = (long long)sym[i];
             if (s <= 0) {
                 code_dense[(size_t)tb * NS + (uint32_t)(-s)] = code;
                 len_dense[(size_t)tb * NS + (uint32_t)(-s)] = (uint8_t)len;
@@ -1569,6 +1573,9 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
                                          double quality, uint32_t B_override, uint32_t nt_total,
                                          uint64_t* body_offset, int mode, uint64_t* payload_total) {
     const Layout& L = *target.L;
+    for (uint32_t i = 0; i < L.nt; ++i)  // 32-bit run lengths / symbol counts on the device
+        DQTG_REQUIRE(L.numel[i] < (1ull << 31), DQTG_ERROR,
+                     "tensor " + L.names[i] + " has 2^31 or more elements (device codec limit)");
     if (base) {
         const Layout& BL = *base->L;
         DQTG_REQUIRE(BL.nt == L.nt, DQTG_SHAPE_MISMATCH, "base/target tensor count mismatch");
@@ -1782,7 +1789,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
         e.sync();
         uint32_t np2 = 1;
         while (np2 < NS + h_max) np2 <<= 1;
-        const size_t hsm = (size_t)np2 * 60;  // keys, f, nodef, sym, perm, parent, depth
+        const size_t hsm = (size_t)np2 * 38 + 16;  // keys, nodef, parent, f, sym, perm, depth
         DQTG_REQUIRE(hsm <= 200 * 1024, DQTG_ERROR,
                      "too many distinct run lengths in one group for the device Huffman stage");
         HufWork W;
