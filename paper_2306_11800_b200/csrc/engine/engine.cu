@@ -150,7 +150,7 @@ size_t pool_size_class(size_t n) {
     return (n + step - 1) / step * step;
 }
 
-constexpr size_t kBigBlock = 32u << 20;
+constexpr size_t kBigBlock = 1u << 20;  // level arrays, records, protected entries
 constexpr size_t kBigKeep = 12;  // cached blocks per (device, size class)
 
 namespace {
