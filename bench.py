@@ -24,6 +24,7 @@ same workload (two GPT-2 blocks + ln_f, 14.2 M params), same metric.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -405,6 +406,10 @@ def run_ours(args):
     t1 = torch.cuda.Event(enable_timing=True)
     mark = (lambda m: print(m, file=sys.stderr, flush=True)) if os.environ.get("DQTG_SYNC_TRACE") \
         else (lambda m: None)
+    # no Python garbage collection pauses inside the timed regions (the host thread
+    # drives the sequential chain between C calls)
+    gc.collect()
+    gc.disable()
     with ClockSampler(local) as clocks:
         mark("MARK sequential begin")
         t0.record(stream)
@@ -414,6 +419,7 @@ def run_ours(args):
         barrier()
         mark("MARK sequential end")
     ms = t0.elapsed_time(t1)
+    gc.enable()
     launches = eng.launches - launches0
     syncs_per_step = (eng.sync_stats()[0] - syncs0) / args.steps
     ms_sequential = ms
@@ -437,6 +443,8 @@ def run_ours(args):
         # three timed passes of exactly K steps each; the median is reported (the
         # worker threads share the host CPU with the rest of the VM)
         pipe_reps = []
+        gc.collect()
+        gc.disable()
         clocks_p = ClockSampler(local)
         clocks_p.__enter__()
         for _ in range(3):
@@ -449,6 +457,7 @@ def run_ours(args):
             pipe_reps.append((time.perf_counter() - tp0) * 1e3)
             launches_p = cc.launches - l0
         clocks_p.__exit__(None, None, None)
+        gc.enable()
         clocks.merge(clocks_p)
         pipelined = sorted(pipe_reps)[1]
         del base, cc
@@ -526,6 +535,8 @@ def run_ours(args):
         cc.sync()
         # three timed passes of e2e_steps steps; the median is reported
         e2e_reps = []
+        gc.collect()
+        gc.disable()
         for _ in range(3):
             d2h_l.clear()
             torch.cuda.synchronize()
@@ -536,6 +547,7 @@ def run_ours(args):
             cc.sync()
             torch.cuda.synchronize()
             e2e_reps.append(time.perf_counter() - te)
+        gc.enable()
         e2e_s = sorted(e2e_reps)[1]
         h2d = 4 * N * e2e_steps
         d2h = sum(d2h_l)
