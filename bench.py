@@ -279,6 +279,7 @@ def measure_ingest(eng, layout, flat, cpu=True, reps=3):
             del ck
         out = {"value": size / min(ts) / 1e9, "unit": "GB/s (DQT1 file -> HBM)",
                "file_bytes": size, "ms": 1e3 * min(ts), "bit_exact": bool(ok),
+               "timing": f"best of {reps} reads, host wall clock, page cache warm",
                "path": "Engine.read_dqt1: host header parse, 8 reader threads, pinned 4 MiB "
                        "chunks -> cudaMemcpyAsync, device NaN/Inf check; page cache warm"}
         if cpu:
