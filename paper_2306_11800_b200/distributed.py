@@ -179,3 +179,35 @@ def eval_batch_sharded(evaluate, cfgs, seeds, *, group=None):
         for j, i in enumerate(idx):
             quality[i], est[i] = q[j], e[j]
     return quality, est
+
+
+def sharded_evaluator(inner=None, *, group=None):
+    """Search control across the ranks: an Evaluator for the drop-in
+    ``guided_exhaustive_search`` / ``delta_neighborhood_search`` (search.cpp:247-296,
+    387-482) whose ``evaluate_batch`` -- called once per EvalCache::prefetch batch
+    (search.cpp:174-204) -- evaluates this rank's round-robin share with ``inner``
+    (default: the device ProxyEvaluator) and all-gathers the results.  Every rank runs
+    the same search with the same inputs, so every rank sees identical batches,
+    identical results and reaches the same outcome; the evaluation work is split
+    ``world`` ways."""
+    from . import dqt
+
+    inner = inner if inner is not None else dqt.ProxyEvaluator()
+
+    class ShardedEvaluator(dqt.Evaluator):
+        def __init__(self):
+            super().__init__()
+            self.inner = inner
+
+        def evaluate(self, checkpoint, scores, config, seed):
+            return self.inner.evaluate(checkpoint, scores, config, seed)
+
+        def evaluate_batch(self, checkpoint, scores, configs, seeds, parallelism=1):
+            def run(cfgs, sds):
+                res = self.inner.evaluate_batch(checkpoint, scores, cfgs, sds, parallelism)
+                return [r.quality_delta for r in res], [r.est_compression for r in res]
+
+            q, e = eval_batch_sharded(run, list(configs), list(seeds), group=group)
+            return [dqt.EvalResult(a, b) for a, b in zip(q, e)]
+
+    return ShardedEvaluator()

@@ -191,3 +191,52 @@ def test_eval_batch_sharded_gloo(world):
         p.join(60)
     assert all(p.exitcode == 0 for p in procs)
     assert all(r[1] for r in res), "sharded batch evaluation differs from the serial order"
+
+
+def _sharded_evaluator_worker(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+
+    from paper_2306_11800_b200 import dqt
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        seen = []
+
+        class Fake(dqt.Evaluator):  # stands in for the device ProxyEvaluator
+            def evaluate(self, c, s, cfg, seed):
+                return dqt.EvalResult(0.01 * cfg.bins + cfg.prune_frac, 1.5 * seed)
+
+            def evaluate_batch(self, c, s, cfgs, seeds, parallelism=1):
+                seen.extend(cfg.bins for cfg in cfgs)
+                return [self.evaluate(c, s, cfg, sd) for cfg, sd in zip(cfgs, seeds)]
+
+        ev = D.sharded_evaluator(Fake())
+        cfgs = [dqt.QuantConfig(bins=b, prune_frac=p) for b in (4, 8, 16, 32) for p in (0.0, 0.1)]
+        seeds = list(range(7, 7 + len(cfgs)))
+        res = ev.evaluate_batch(None, None, cfgs, seeds, 2)
+        ok = ([r.quality_delta for r in res] == [0.01 * c.bins + c.prune_frac for c in cfgs]
+              and [r.est_compression for r in res] == [1.5 * s for s in seeds]
+              and seen == [cfgs[i].bins for i in D.assign_configs(len(cfgs), world)[rank]])
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_evaluator_gloo():
+    """The Evaluator handed to the drop-in search splits each batch over the ranks
+    and returns the whole batch, in order, on every rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_evaluator_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(2)]
+    for p in procs:
+        p.join(60)
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(r[1] for r in res)
