@@ -1743,20 +1743,27 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     e.d2h(&n_ov, A.ov_count, 8);
     e.sync();
     DQTG_REQUIRE(n_ov <= A.ov_cap, DQTG_ERROR, "run-length overflow list exhausted");
-    auto* ov_sorted = (unsigned long long*)e.buf("e.ov_sorted", n_ov * 8 + 8);
-    auto* ukey = (unsigned long long*)e.buf("e.ukey", n_ov * 8 + 8);
-    auto* ucnt = (unsigned long long*)e.buf("e.ucnt", n_ov * 8 + 8);
+    // overflow buffers sized for the layout's bound (ov_cap), not this step's count:
+    // the count varies step to step and every scratch growth maps pool memory mid-step
+    const unsigned long long ov_cap = A.ov_cap;
+    auto* ov_sorted = (unsigned long long*)e.buf("e.ov_sorted", ov_cap * 8 + 8);
+    auto* ukey = (unsigned long long*)e.buf("e.ukey", ov_cap * 8 + 8);
+    auto* ucnt = (unsigned long long*)e.buf("e.ucnt", ov_cap * 8 + 8);
     auto* nu = (unsigned long long*)(small + 2);
     if (n_ov) {
-        size_t tb = 0;
+        size_t tb = 0, tb_cap = 0;
         DQTG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, A.ov, ov_sorted, (int64_t)n_ov, 0, 64,
                                                  st));
-        void* tmp = e.buf("e.cubtmp", tb + 16);
+        DQTG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb_cap, A.ov, ov_sorted, (int64_t)ov_cap, 0,
+                                                 64, st));
+        void* tmp = e.buf("e.cubtmp", std::max(tb, tb_cap) + 16);
         DQTG_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, A.ov, ov_sorted, (int64_t)n_ov, 0, 64, st));
-        size_t tb2 = 0;
+        size_t tb2 = 0, tb2_cap = 0;
         DQTG_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tb2, ov_sorted, ukey, ucnt, nu,
                                                      (int64_t)n_ov, st));
-        void* tmp2 = e.buf("e.cubtmp3", tb2 + 16);
+        DQTG_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tb2_cap, ov_sorted, ukey, ucnt, nu,
+                                                     (int64_t)ov_cap, st));
+        void* tmp2 = e.buf("e.cubtmp3", std::max(tb2, tb2_cap) + 16);
         DQTG_CUDA(cub::DeviceRunLengthEncode::Encode(tmp2, tb2, ov_sorted, ukey, ucnt, nu,
                                                      (int64_t)n_ov, st));
     } else {
@@ -1767,13 +1774,13 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     e.sync();
     // H
     auto* gi = (GroupInfo*)e.buf("e.gi", (size_t)nt * B * sizeof(GroupInfo));
-    const size_t tab_n = (size_t)nt * B * NS + n_ov + 8;
+    const size_t tab_n = (size_t)nt * B * NS + ov_cap + 8;  // bound, see above
     auto* tab_sym = (long long*)e.buf("e.tabsym", tab_n * 8);
     auto* tab_len = (uint8_t*)e.buf("e.tablen", tab_n);
     auto* code_dense = (unsigned long long*)e.buf("e.cdense", (size_t)nt * B * NS * 8);
     auto* len_dense = (uint8_t*)e.buf("e.ldense", (size_t)nt * B * NS);
-    auto* code_ov = (unsigned long long*)e.buf("e.cov", n_ov * 8 + 8);
-    auto* len_ov = (uint8_t*)e.buf("e.lov", n_ov + 8);
+    auto* code_ov = (unsigned long long*)e.buf("e.cov", ov_cap * 8 + 8);
+    auto* len_ov = (uint8_t*)e.buf("e.lov", ov_cap + 8);
     {
         auto* max_nov = (uint32_t*)(small + 4);
         auto* ov_range = (unsigned long long*)e.buf("e.ovrange", (size_t)nt * B * 16 + 16);
