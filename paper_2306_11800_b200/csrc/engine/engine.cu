@@ -177,15 +177,23 @@ void* Engine::dalloc(size_t bytes) {
     if (cls >= kBigBlock) {
         BigCache& bc = big_cache();
         std::lock_guard<std::mutex> g(bc.mu);
-        for (size_t i = bc.free.size(); i-- > 0;)
-            if (bc.free[i].cls == cls && bc.free[i].device == device) {
-                BigBlock b = bc.free[i];
-                bc.free.erase(bc.free.begin() + (long)i);
-                DQTG_CUDA(cudaStreamWaitEvent(stream, b.ev, 0));
-                cudaEventDestroy(b.ev);
-                bc.live[b.p] = {cls, device};
-                return b.p;
-            }
+        // best fit among cached blocks of this class up to 1.25x (record and
+        // protected-entry sizes wobble across class edges from step to step)
+        size_t best = bc.free.size();
+        for (size_t i = bc.free.size(); i-- > 0;) {
+            const BigBlock& b = bc.free[i];
+            if (b.device == device && b.cls >= cls && b.cls <= cls + cls / 4 &&
+                (best == bc.free.size() || b.cls < bc.free[best].cls))
+                best = i;
+        }
+        if (best != bc.free.size()) {
+            BigBlock b = bc.free[best];
+            bc.free.erase(bc.free.begin() + (long)best);
+            DQTG_CUDA(cudaStreamWaitEvent(stream, b.ev, 0));
+            cudaEventDestroy(b.ev);
+            bc.live[b.p] = {b.cls, device};
+            return b.p;
+        }
     }
     DQTG_CUDA(cudaMallocFromPoolAsync(&p, cls, pool, stream));
     if (cls >= kBigBlock) {
