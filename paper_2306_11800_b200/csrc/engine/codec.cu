@@ -990,80 +990,129 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
             __syncthreads();
         }
     for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) perm[r] = (uint32_t)(s_keys[r] & 0xffffffu);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long nsyms = 0;
-        for (uint32_t i = 0; i < n; ++i) nsyms += f[i];
-        G.nsyms = nsyms;
-        if (n == 1) {
-            depth[0] = 1;
-        } else {
-            // two queues == the reference's priority queue on (f, order)
-            for (uint32_t i = 0; i < n; ++i) nodef[i] = f[i];
-            uint32_t q1 = 0, q2 = n, made = n;
-            auto take = [&]() -> uint32_t {
-                bool use1;
-                if (q1 >= n) use1 = false;
-                else if (q2 >= made) use1 = true;
-                else {
-                    uint32_t a = perm[q1], c = q2;
-                    use1 = nodef[a] < nodef[c] || (nodef[a] == nodef[c] && a < c);
-                }
-                return use1 ? perm[q1++] : q2++;
-            };
-            for (uint32_t s = 0; s + 1 < n; ++s) {
-                uint32_t x = take(), y = take();
-                nodef[made] = nodef[x] + nodef[y];
-                parent[x] = parent[y] = made;
-                ++made;
+    {  // symbols in the group's stream (warp reduction)
+        unsigned long long ns = 0;
+        for (uint32_t i = lane; i < n; i += 32) ns += f[i];
+        for (int o = 16; o > 0; o >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, o);
+        G.nsyms = ns;
+    }
+    __syncwarp();
+    uint32_t made = n;
+    if (threadIdx.x == 0 && n > 1) {
+        // two queues == the reference's priority queue on (f, order): a serial chain
+        for (uint32_t i = 0; i < n; ++i) nodef[i] = f[i];
+        uint32_t q1 = 0, q2 = n;
+        auto take = [&]() -> uint32_t {
+            bool use1;
+            if (q1 >= n) use1 = false;
+            else if (q2 >= made) use1 = true;
+            else {
+                uint32_t a = perm[q1], c = q2;
+                use1 = nodef[a] < nodef[c] || (nodef[a] == nodef[c] && a < c);
             }
-            const uint32_t root = made - 1;
-            depth[root] = 0;
-            bool overflow = false;
-            for (int i = (int)root - 1; i >= 0; --i) {
-                const uint32_t d = depth[parent[i]] + 1u;
-                depth[i] = (uint8_t)(d < 255u ? d : 255u);
-                if ((uint32_t)i >= n && d >= 63) overflow = true;
-            }
-            if (overflow) atomicOr(A.err, kErrHuffmanDepth);
+            return use1 ? perm[q1++] : q2++;
+        };
+        for (uint32_t st = 0; st + 1 < n; ++st) {
+            uint32_t x = take(), y = take();
+            nodef[made] = nodef[x] + nodef[y];
+            parent[x] = parent[y] = made;
+            ++made;
         }
-        // table sorted by (len, sym): counting sort over lengths, stable in sym order
-        uint32_t* hist = s_hist;
-        uint32_t* at = s_at;
-        for (int l = 0; l < 65; ++l) hist[l] = 0;
-        for (uint32_t i = 0; i < n; ++i) hist[depth[i] < 64 ? depth[i] : 64]++;
+    }
+    made = __shfl_sync(0xffffffffu, made, 0);
+    __syncwarp();
+    // leaf depths by pointer jumping (6 rounds reach every depth <= 64; deeper leaves
+    // are a code-length overflow): ancestors in parent/nodef, distances in depth/s_keys
+    bool overflow = false;
+    if (n == 1) {
+        if (lane == 0) depth[0] = 1;
+    } else {
+        const uint32_t root = made - 1;
+        uint32_t* anc[2] = {parent, nodef};
+        uint8_t* dist[2] = {depth, (uint8_t*)s_keys};
+        for (uint32_t i = lane; i < made; i += 32) {
+            if (i == root) parent[i] = root;
+            depth[i] = i == root ? 0 : 1;
+        }
+        __syncwarp();
+        int cur = 0;
+        for (int round = 0; round < 6; ++round) {
+            const uint32_t* ac = anc[cur];
+            const uint8_t* dc = dist[cur];
+            uint32_t* an = anc[cur ^ 1];
+            uint8_t* dn = dist[cur ^ 1];
+            for (uint32_t i = lane; i < made; i += 32) {
+                const uint32_t a = ac[i];
+                const uint32_t d = (uint32_t)dc[i] + dc[a];
+                dn[i] = (uint8_t)(d < 255u ? d : 255u);
+                an[i] = ac[a];
+            }
+            __syncwarp();
+            cur ^= 1;
+        }
+        // cur == 0 after an even number of rounds: results are in parent/depth
+        for (uint32_t i = lane; i < n; i += 32)
+            if (anc[cur][i] != root || dist[cur][i] >= 64) overflow = true;
+    }
+    if (__any_sync(0xffffffffu, overflow) && lane == 0) atomicOr(A.err, kErrHuffmanDepth);
+    __syncwarp();
+    // table sorted by (len, sym): counting sort over lengths, stable in sym order
+    uint32_t* hist = s_hist;
+    uint32_t* at = s_at;
+    __shared__ unsigned long long s_first[65];
+    for (int l = lane; l < 65; l += 32) hist[l] = 0;
+    __syncwarp();
+    for (uint32_t i = lane; i < n; i += 32) atomicAdd(&hist[depth[i] < 64 ? depth[i] : 64], 1u);
+    __syncwarp();
+    if (lane == 0) {
+        // canonical first code per length (codec.cpp:184-214): the o-th entry in
+        // (len, sym) order gets first[len] + (o - start[len])
         uint32_t acc = 0;
+        unsigned long long code = 0;
+        int prev = -1;
         for (int l = 0; l < 65; ++l) {
+            at[l] = acc;
+            if (hist[l]) {
+                if (prev >= 0) code <<= (l - prev);
+                s_first[l] = code;
+                code += hist[l];
+                prev = l;
+            }
+            acc += hist[l];
+        }
+        for (uint32_t i = 0; i < n; ++i) perm[at[depth[i] < 64 ? depth[i] : 64]++] = i;
+        acc = 0;
+        for (int l = 0; l < 65; ++l) {  // starts again
             at[l] = acc;
             acc += hist[l];
         }
-        unsigned long long code = 0;
-        uint32_t hdr = 0;
-        for (uint32_t i = 0; i < n; ++i) perm[at[depth[i] < 64 ? depth[i] : 64]++] = i;
-        uint32_t prev_len = depth[perm[0]];
-        for (uint32_t o = 0; o < n; ++o) {
-            const uint32_t i = perm[o];
-            const uint32_t len = depth[i];
-            code <<= (len - prev_len);
-            prev_len = len;
-            tab_sym[G.tab_base + o] = sym[i];
-            tab_len[G.tab_base + o] = (uint8_t)len;
-            hdr += uvlen(zigzag(sym[i])) + 1;
-            const long long s = (long long)sym[i];
-            if (s <= 0) {
-                code_dense[(size_t)tb * NS + (uint32_t)(-s)] = code;
-                len_dense[(size_t)tb * NS + (uint32_t)(-s)] = (uint8_t)len;
-            } else if (s < kLD) {
-                code_dense[(size_t)tb * NS + B + (uint32_t)s] = code;
-                len_dense[(size_t)tb * NS + B + (uint32_t)s] = (uint8_t)len;
-            } else {
-                // overflow leaves were appended last, in ukey order: leaf i <-> ov_begin + i - n_dense
-                const unsigned long long j = G.ov_begin + (i - (n - nov));
-                code_ov[j] = code;
-                len_ov[j] = (uint8_t)len;
-            }
-            ++code;
+    }
+    __syncwarp();
+    uint32_t hdr = 0;
+    for (uint32_t o = lane; o < n; o += 32) {
+        const uint32_t i = perm[o];
+        const uint32_t len = depth[i];
+        const uint32_t lc = len < 64 ? len : 64;
+        const unsigned long long code = s_first[lc] + (o - at[lc]);
+        tab_sym[G.tab_base + o] = sym[i];
+        tab_len[G.tab_base + o] = (uint8_t)len;
+        hdr += uvlen(zigzag(sym[i])) + 1;
+        const long long sv = (long long)sym[i];
+        if (sv <= 0) {
+            code_dense[(size_t)tb * NS + (uint32_t)(-sv)] = code;
+            len_dense[(size_t)tb * NS + (uint32_t)(-sv)] = (uint8_t)len;
+        } else if (sv < kLD) {
+            code_dense[(size_t)tb * NS + B + (uint32_t)sv] = code;
+            len_dense[(size_t)tb * NS + B + (uint32_t)sv] = (uint8_t)len;
+        } else {
+            // overflow leaves were appended last, in ukey order: leaf i <-> ov_begin + i - n_dense
+            const unsigned long long j = G.ov_begin + (i - (n - nov));
+            code_ov[j] = code;
+            len_ov[j] = (uint8_t)len;
         }
+    }
+    for (int o = 16; o > 0; o >>= 1) hdr += __shfl_xor_sync(0xffffffffu, hdr, o);
+    if (lane == 0) {
         G.tsize = n;
         G.hdr = hdr + uvlen(b) + uvlen(G.n_elems) + uvlen(G.nsyms) + uvlen(n);
         gi[tb] = G;
