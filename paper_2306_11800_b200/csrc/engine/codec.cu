@@ -999,22 +999,26 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
     __syncwarp();
     uint32_t made = n;
     if (threadIdx.x == 0 && n > 1) {
-        // two queues == the reference's priority queue on (f, order): a serial chain
-        for (uint32_t i = 0; i < n; ++i) nodef[i] = f[i];
+        // two queues == the reference's priority queue on (f, order): a serial chain.
+        // Leaves come in sorted-key order (frequency in the key's high bits, index in
+        // the low 24); a leaf always precedes an internal node of equal weight (its
+        // insertion index is smaller), so the queue compare is fl <= internal weight.
         uint32_t q1 = 0, q2 = n;
-        auto take = [&]() -> uint32_t {
-            bool use1;
-            if (q1 >= n) use1 = false;
-            else if (q2 >= made) use1 = true;
-            else {
-                uint32_t a = perm[q1], c = q2;
-                use1 = nodef[a] < nodef[c] || (nodef[a] == nodef[c] && a < c);
+        unsigned long long k1 = s_keys[0];
+        auto take = [&](uint32_t& idx) -> uint32_t {
+            const uint32_t fl = (uint32_t)(k1 >> 24);
+            if (q1 < n && (q2 >= made || fl <= nodef[q2])) {
+                idx = (uint32_t)(k1 & 0xffffffu);
+                if (++q1 < n) k1 = s_keys[q1];
+                return fl;
             }
-            return use1 ? perm[q1++] : q2++;
+            idx = q2;
+            return nodef[q2++];
         };
         for (uint32_t st = 0; st + 1 < n; ++st) {
-            uint32_t x = take(), y = take();
-            nodef[made] = nodef[x] + nodef[y];
+            uint32_t x, y;
+            const uint32_t fx = take(x), fy = take(y);
+            nodef[made] = fx + fy;
             parent[x] = parent[y] = made;
             ++made;
         }
