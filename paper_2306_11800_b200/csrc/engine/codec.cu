@@ -1401,7 +1401,7 @@ __device__ __forceinline__ void put_bits(uint32_t* words, unsigned long long q,
 // words: interior words with plain stores, the two boundary words with
 // atomicOr (they may share bytes with neighbouring segments or headers).
 constexpr int kEmitWarps = 8;
-constexpr int kWarpStage = 1024;  // staged 32-bit words per warp (4 KiB)
+constexpr int kWarpStage = 512;  // staged 32-bit words per warp (2 KiB; larger tiles write directly)
 
 __device__ __forceinline__ void stage_bits(uint32_t* st, unsigned long long q,
                                            unsigned long long code, int len) {
