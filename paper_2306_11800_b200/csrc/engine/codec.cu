@@ -1210,12 +1210,25 @@ __global__ void __launch_bounds__(kCB) enc_bitscan_kernel(EncArgs A, const uint3
     const uint32_t B = A.B;
     const uint32_t t = blockIdx.x / B, b = blockIdx.x % B;
     const uint32_t a0 = A.tile0[t], a1 = A.tile0[t + 1];
+    // four consecutive tiles per thread: a quarter of the block scans (and barriers)
+    // on the long tile ranges of the large tensors
+    constexpr int kPer = 4;
     unsigned long long base = 0;
-    for (uint32_t c0 = a0; c0 < a1; c0 += kCB) {
-        const uint32_t i = c0 + threadIdx.x;
-        unsigned long long v = i < a1 ? segbits[(size_t)i * B + b] : 0ull, tot;
-        unsigned long long ex = block_exclusive_scan<unsigned long long>(v, s_scan, &tot);
-        if (i < a1) segoff[(size_t)i * B + b] = base + ex;
+    for (uint32_t c0 = a0; c0 < a1; c0 += kCB * kPer) {
+        const uint32_t i0 = c0 + threadIdx.x * kPer;
+        uint32_t v[kPer];
+        unsigned long long sum = 0, tot;
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            v[u] = i0 + u < a1 ? segbits[(size_t)(i0 + u) * B + b] : 0u;
+            sum += v[u];
+        }
+        unsigned long long ex = block_exclusive_scan<unsigned long long>(sum, s_scan, &tot);
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            if (i0 + u < a1) segoff[(size_t)(i0 + u) * B + b] = base + ex;
+            ex += v[u];
+        }
         base += tot;
     }
     if (threadIdx.x == 0) {
