@@ -623,6 +623,9 @@ __device__ __forceinline__ RunM shfl_down_runm(const RunM& m, int o);
 // Block per (tensor, group) for tensors with many tiles (256-tile chunks): warp
 // shuffle scans + one shared-memory combine of the 8 warp aggregates per chunk.
 __global__ void __launch_bounds__(kCB) enc_resolve_big_kernel(EncArgs A, const uint32_t* tensors) {
+    // four consecutive tiles per thread and chunk: a quarter of the block scans on the
+    // long tile ranges of the large tensors (the kernel's critical path)
+    constexpr int kPer = 4;
     extern __shared__ uint32_t s_f[];  // NS
     __shared__ int s_wmax[kCB / 32];
     __shared__ RunM s_wm[kCB / 32];
@@ -633,12 +636,24 @@ __global__ void __launch_bounds__(kCB) enc_resolve_big_kernel(EncArgs A, const u
     for (uint32_t i = tid; i < NS; i += kCB) s_f[i] = 0;
     // forward: lv of the nearest earlier non-empty segment (inclusive max-scan)
     int carry_last = -1;
-    for (uint32_t c0 = a0; c0 < a1; c0 += kCB) {
-        const uint32_t i = c0 + tid;
-        Seg S{};
-        if (i < a1) S = A.segs[(size_t)i * B + b];
-        const int idx = (i < a1 && S.n) ? (int)i : -1;
-        int x = idx;
+    for (uint32_t c0 = a0; c0 < a1; c0 += kCB * kPer) {
+        const uint32_t i0 = c0 + tid * kPer;
+        int idx[kPer];
+        uint32_t fv[kPer];
+        int x = -1;
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            idx[u] = -1;
+            fv[u] = 0;
+            if (i0 + u < a1) {
+                const Seg& S = A.segs[(size_t)(i0 + u) * B + b];
+                if (S.n) {
+                    idx[u] = (int)(i0 + u);
+                    fv[u] = S.fv;
+                }
+            }
+            x = max(x, idx[u]);
+        }
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(0xffffffffu, x, o);
@@ -650,9 +665,14 @@ __global__ void __launch_bounds__(kCB) enc_resolve_big_kernel(EncArgs A, const u
         for (int w = 0; w < wid; ++w) before = max(before, s_wmax[w]);
         int excl = __shfl_up_sync(0xffffffffu, x, 1);
         if (lane == 0) excl = -1;
-        const int prev = max(before, excl);
-        if (idx >= 0)
-            A.segs[(size_t)i * B + b].cont = A.mode != 2 && prev >= 0 && A.segs[(size_t)prev * B + b].lv == S.fv;
+        int prev = max(before, excl);
+#pragma unroll
+        for (int u = 0; u < kPer; ++u)
+            if (idx[u] >= 0) {
+                A.segs[(size_t)idx[u] * B + b].cont =
+                    A.mode != 2 && prev >= 0 && A.segs[(size_t)prev * B + b].lv == fv[u];
+                prev = idx[u];
+            }
         int cl = carry_last;
         for (int w = 0; w < kCB / 32; ++w) cl = max(cl, s_wmax[w]);
         __syncthreads();
@@ -662,25 +682,32 @@ __global__ void __launch_bounds__(kCB) enc_resolve_big_kernel(EncArgs A, const u
     // backward: suffix run monoid gives the extension of each trailing run
     RunM carry{};
     const uint32_t ntl = a1 - a0;
-    const uint32_t nch = (ntl + kCB - 1) / kCB;
+    const uint32_t nch = (ntl + kCB * kPer - 1) / (kCB * kPer);
     uint32_t* f = s_f;
     const uint32_t tb = t * B + b;
     for (int ch = (int)nch - 1; ch >= 0; --ch) {
-        const uint32_t i = a0 + ch * kCB + tid;
-        RunM m{};
-        Seg S{};
-        if (i < a1) {
-            S = A.segs[(size_t)i * B + b];
-            if (S.n) {
-                m.n = S.n;
-                m.fv = S.fv;
-                m.lv = S.lv;
-                m.single = S.lead == S.n;
-                m.lead = S.lead;
+        const uint32_t i0 = a0 + ch * kCB * kPer + tid * kPer;
+        RunM m[kPer];
+        Seg S[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            m[u] = RunM{};
+            S[u] = Seg{};
+            if (i0 + u < a1) {
+                S[u] = A.segs[(size_t)(i0 + u) * B + b];
+                if (S[u].n) {
+                    m[u].n = S[u].n;
+                    m[u].fv = S[u].fv;
+                    m[u].lv = S[u].lv;
+                    m[u].single = S[u].lead == S[u].n;
+                    m[u].lead = S[u].lead;
+                }
             }
         }
-        // inclusive suffix inside the warp
-        RunM x = m;
+        // this thread's suffix, then the inclusive suffix inside the warp
+        RunM x = m[kPer - 1];
+#pragma unroll
+        for (int u = kPer - 2; u >= 0; --u) x = runm_combine(m[u], x);
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const RunM y = shfl_down_runm(x, o);
@@ -692,19 +719,23 @@ __global__ void __launch_bounds__(kCB) enc_resolve_big_kernel(EncArgs A, const u
         for (int w = kCB / 32 - 1; w > wid; --w) later = runm_combine(s_wm[w], later);
         RunM nxt = shfl_down_runm(x, 1);  // suffix starting at the next lane
         RunM after = lane < 31 ? runm_combine(nxt, later) : later;
-        if (i < a1 && S.n) {
-            unsigned long long E = (A.mode != 2 && after.n && after.fv == S.lv) ? after.lead : 0ull;
-            const bool single = S.lead == S.n;
-            Seg& G = A.segs[(size_t)i * B + b];
-            if (single) {
-                G.lead_total = G.trail_total = S.n + E;
-                if (!S.cont) add_symbol(f, NS, B, tb, S.fv, S.n + E, A);
-            } else {
-                G.lead_total = S.lead;
-                G.trail_total = S.trail + E;
-                if (!S.cont) add_symbol(f, NS, B, tb, S.fv, S.lead, A);
-                add_symbol(f, NS, B, tb, S.lv, S.trail + E, A);
+#pragma unroll
+        for (int u = kPer - 1; u >= 0; --u) {  // items of this thread, last first
+            if (i0 + u < a1 && S[u].n) {
+                unsigned long long E = (A.mode != 2 && after.n && after.fv == S[u].lv) ? after.lead : 0ull;
+                const bool single = S[u].lead == S[u].n;
+                Seg& G = A.segs[(size_t)(i0 + u) * B + b];
+                if (single) {
+                    G.lead_total = G.trail_total = S[u].n + E;
+                    if (!S[u].cont) add_symbol(f, NS, B, tb, S[u].fv, S[u].n + E, A);
+                } else {
+                    G.lead_total = S[u].lead;
+                    G.trail_total = S[u].trail + E;
+                    if (!S[u].cont) add_symbol(f, NS, B, tb, S[u].fv, S[u].lead, A);
+                    add_symbol(f, NS, B, tb, S[u].lv, S[u].trail + E, A);
+                }
             }
+            after = runm_combine(m[u], after);
         }
         RunM chunk = carry;
         for (int w = kCB / 32 - 1; w >= 0; --w) chunk = runm_combine(s_wm[w], chunk);
