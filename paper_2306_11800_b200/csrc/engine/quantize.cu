@@ -284,12 +284,23 @@ __global__ void __launch_bounds__(kPB, 6) pass_b_kernel(PassIn a, const LtParams
 __global__ void __launch_bounds__(1024) scan_u32_kernel(const uint32_t* in, int n,
                                                         unsigned long long* out) {
     __shared__ unsigned long long s[33];
+    constexpr int kPer = 8;  // consecutive entries per thread: fewer block scans
     unsigned long long base = 0;
-    for (int c0 = 0; c0 < n; c0 += blockDim.x) {
-        int i = c0 + threadIdx.x;
-        unsigned long long v = i < n ? in[i] : 0ull, tot;
-        unsigned long long ex = block_exclusive_scan<unsigned long long>(v, s, &tot);
-        if (i < n) out[i] = base + ex;
+    for (int c0 = 0; c0 < n; c0 += blockDim.x * kPer) {
+        const int i0 = c0 + threadIdx.x * kPer;
+        uint32_t v[kPer];
+        unsigned long long sum = 0, tot;
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            v[u] = i0 + u < n ? in[i0 + u] : 0u;
+            sum += v[u];
+        }
+        unsigned long long ex = block_exclusive_scan<unsigned long long>(sum, s, &tot);
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            if (i0 + u < n) out[i0 + u] = base + ex;
+            ex += v[u];
+        }
         base += tot;
     }
     if (threadIdx.x == 0) out[n] = base;
