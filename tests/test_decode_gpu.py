@@ -127,3 +127,34 @@ def test_decode_errors(eng, oracle):
     flip = bytearray(full)
     flip[len(full) // 2] ^= 0x10
     assert status(bytes(flip)) in (3, 13, 14, 15)
+
+
+def test_decode_fuzzed_records(eng, oracle):
+    """Random byte flips anywhere in FULL and DELTA records: the device decoder either
+    decodes (a flip inside codebook floats or the quality field can leave a valid
+    record) or raises one of the reference's error types; it never faults, and the
+    engine keeps decoding the intact records afterwards."""
+    from paper_2306_11800_b200 import engine as E
+
+    t1 = make_tensors(seed=8)
+    t2 = perturb(t1, seed=9, frac=0.2)
+    m1, s1 = oracle.scores(flat(t1), None)
+    m2, s2 = oracle.scores(flat(t2), None)
+    q1 = oracle.quantize(t1, 1, m1, s1, CONFIGS[0], 1)
+    q2 = oracle.quantize(t2, 2, m2, s2, CONFIGS[0], 1)
+    full = oracle.encode_record(q1)
+    delta = oracle.encode_record(q2, q1)
+    base = eng.decode_record(full)
+    rng = np.random.default_rng(123)
+    allowed = {1, 2, 3, 4, 6, 13, 14, 15, 16}
+    for rec, b in ((full, None), (delta, base)):
+        for _ in range(120):
+            bad = bytearray(rec)
+            pos = int(rng.integers(0, len(bad)))
+            bad[pos] ^= int(rng.integers(1, 256))
+            try:
+                eng.decode_record(bytes(bad), base=b)
+            except E.EngineError as ex:
+                assert ex.status in allowed, (pos, ex)
+    host_equal(eng.decode_record(full), q1)
+    host_equal(eng.decode_record(delta, base=eng.decode_record(full)), q2)
