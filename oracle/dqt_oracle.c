@@ -1467,12 +1467,21 @@ static int decode_payload(rd *r, const uint16_t *prev, uint64_t n, uint32_t B, u
     uint64_t *next = calloc(B + 1, 8), *start = calloc(B + 1, 8), *gsz = calloc(B + 1, 8);
     uint8_t *have = calloc(B + 1, 1);
     uint16_t *grouped = malloc(n * 2 + 2); /* concatenated group payloads */
+    if (!deltas || !next || !start || !gsz || !have || !grouped) {
+        free(deltas); free(next); free(start); free(gsz); free(have); free(grouped);
+        return DQO_ERR; /* absurd element count from a corrupt shape */
+    }
     uint64_t total = 0;
     int rc = DQO_OK;
     for (uint64_t g = 0; g < ng && !rc; ++g) {
         uint64_t bucket = rd_uvarint(r), elems = rd_uvarint(r), nsyms = rd_uvarint(r),
                  tsize = rd_uvarint(r);
         if (r->err) { rc = r->err; break; }
+        /* absurd counts from corrupt varints: the reference's reserve() throws
+           std::length_error / bad_alloc (no dqt type); every table entry takes >= 2
+           bytes and every symbol >= 1 bit, so they are reported as truncation /
+           corrupt bitstream here instead of crashing the checker */
+        if (tsize > (r->n - r->pos) / 2) { rc = DQO_ERR_TRUNCATED; break; }
         int64_t *ts = malloc((tsize + 1) * 8);
         uint8_t *tl = malloc(tsize + 1);
         for (uint64_t i = 0; i < tsize; ++i) ts[i] = rd_svarint(r), tl[i] = (uint8_t)rd_le(r, 1);
@@ -1481,6 +1490,7 @@ static int decode_payload(rd *r, const uint16_t *prev, uint64_t n, uint32_t B, u
         if (r->err) { rc = r->err; free(ts); free(tl); break; }
         const uint8_t *bytes = r->p + r->pos;
         r->pos += nb;
+        if (nsyms > nb * 8) { rc = DQO_ERR_CORRUPT_BITSTREAM; free(ts); free(tl); break; }
         int64_t *syms = malloc((nsyms + 1) * 8);
         rc = dqo_huffman_decode(ts, tl, tsize, bytes, nb, nsyms, syms);
         if (!rc && total + elems > n) rc = DQO_ERR_CORRUPT_INDEX;
@@ -1546,6 +1556,8 @@ int dqo_decode_record(const uint8_t *rec, size_t n, const dqo_q *base, dqo_q **o
     }
     uint32_t nt = (uint32_t)rd_le(&r, 4);
     if (!rc && !r.err && base && base->nt != nt) rc = DQO_ERR_CHAIN;
+    /* an absurd tensor count (corrupt input): reported as truncation, see decode_payload */
+    if (!rc && !r.err && nt > (r.n - r.pos) / 4) rc = DQO_ERR_TRUNCATED;
     if (!rc && !r.err) {
         q->t = calloc(nt + 1, sizeof(dqo_tensor));
         q->nt = 0;
@@ -1570,6 +1582,7 @@ int dqo_decode_record(const uint8_t *rec, size_t n, const dqo_q *base, dqo_q **o
         if (r.err) break;
         if (np > t->n) { rc = DQO_ERR_CORRUPT_INDEX; break; }
         t->nprot = np;
+        if (np > (r.n - r.pos) / 3) { rc = DQO_ERR_TRUNCATED; break; } /* >= 3 bytes each (corrupt count) */
         t->ppos = malloc((np + 1) * 8);
         t->pval = malloc((np + 1) * 2);
         uint64_t pos = 0;
@@ -1591,6 +1604,7 @@ int dqo_decode_record(const uint8_t *rec, size_t n, const dqo_q *base, dqo_q **o
         } else
             prev = zero = calloc(t->n + 1, 2);
         t->levels = malloc(t->n * 2 + 2);
+        if (!prev || !t->levels) { free(zero); rc = DQO_ERR; break; }
         rc = decode_payload(&r, prev, t->n, B, t->levels);
         free(zero);
         if (rc) break;
