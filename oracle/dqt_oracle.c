@@ -1578,6 +1578,9 @@ int dqo_decode_record(const uint8_t *rec, size_t n, const dqo_q *base, dqo_q **o
         t->n = 1;
         for (uint8_t d = 0; d < t->rank; ++d) t->n *= (t->dims[d] = rd_le(&r, 8));
         if (r.err) break;
+        /* checker limit: a corrupt shape must not make the test process allocate (and
+           zero) terabytes; real test tensors are far below 2^30 elements */
+        if (t->n > (1ull << 30)) { rc = DQO_ERR; break; }
         uint64_t np = rd_uvarint(&r);
         if (r.err) break;
         if (np > t->n) { rc = DQO_ERR_CORRUPT_INDEX; break; }

@@ -182,7 +182,9 @@ __global__ void __launch_bounds__(256) huff_write_kernel(const uint64_t* rec64, 
     while (p < end && k < G.nsyms) {
         uint32_t idx;
         const uint32_t L = decode_one(rec64, G, T, p, idx);
-        if (!L || idx >= G.tsize) {
+        // invalid code, or a code running past the group's bytes (the reference's
+        // BitReader runs out: codec.cpp:258-266)
+        if (!L || idx >= G.tsize || p + L > G.nbits) {
             atomicOr(err, kErrCorruptBitstream);
             return;
         }
@@ -505,6 +507,10 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
     }
     const uint32_t nt = r.le<uint32_t>();
     if (base && base->L->nt != nt) throw Fail(DQTG_CHAIN_CORRUPT, "base tensor count mismatch");
+    std::string deferred_index;  // CorruptIndex found while parsing, reported after H/R
+    // a corrupt count must not size host tables: every tensor takes >= 6 record bytes
+    // (the reference's reserve() would throw std::length_error / bad_alloc here)
+    if (nt > (r.n - r.at) / 6) throw Fail(DQTG_TRUNCATED, "tensor count exceeds the record size");
     // tensors
     std::vector<std::string> names(nt);
     std::vector<uint8_t> types(nt), ranks(nt);
@@ -529,8 +535,13 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
             dims.push_back(r.le<uint64_t>());
             numel *= dims.back();
         }
+        // device codec limit (2^31 elements per tensor, see encode_record_ex); also keeps
+        // a corrupt shape from sizing host tables and device buffers
+        if (numel >= (1ull << 31))
+            throw Fail(DQTG_ERROR, "tensor " + names[i] + " has 2^31 or more elements (device codec limit)");
         const uint64_t np = r.uv();
         if (np > numel) throw Fail(DQTG_CORRUPT_INDEX, "too many protected entries in " + names[i]);
+        if (np > (r.n - r.at) / 3) throw Fail(DQTG_TRUNCATED, "protected entries exceed the record size");
         ppos[i].resize(np);
         pval[i].resize(np);
         uint64_t pos = 0;
@@ -576,10 +587,14 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
             G.elems = r.uv();
             G.nsyms = r.uv();
             const uint64_t tsize = r.uv();
-            if (bucket >= B || (int64_t)bucket <= last_bucket)
-                throw Fail(DQTG_CORRUPT_INDEX, "group bucket out of order in " + names[i]);
+            // the reference finds a bad bucket only in unrearrange, after the group
+            // bitstreams decoded (codec.cpp:330-355): reported after the Huffman and
+            // RLE stages so that their CorruptBitstream wins, as there
+            if ((bucket >= B || (int64_t)bucket <= last_bucket) && deferred_index.empty())
+                deferred_index = "group bucket out of order in " + names[i];
             last_bucket = (int64_t)bucket;
-            if (tsize > (1u << 24)) throw Fail(DQTG_CORRUPT_BITSTREAM, "huffman table too large");
+            // every table entry takes >= 2 bytes: a larger count runs out of record
+            if (tsize > (r.n - r.at) / 2) throw Fail(DQTG_TRUNCATED, "huffman table exceeds the record");
             G.tab_off = (uint32_t)tab_sym.size();
             G.tsize = (uint32_t)tsize;
             for (uint64_t j = 0; j < tsize; ++j) {
@@ -599,6 +614,7 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
             G.nbits = nb * 8;
             r.at += nb;
             if (G.nsyms && !tsize) throw Fail(DQTG_CORRUPT_BITSTREAM, "empty huffman table");
+            if (G.nsyms > G.nbits) throw Fail(DQTG_CORRUPT_BITSTREAM, "more symbols than bits");
             // canonical decode limits (codec.cpp:137-214 assign_codes)
             G.lim_off = (uint32_t)lim.size();
             lim.resize(lim.size() + kMaxCodeLen + 1, ~0ull);
@@ -629,7 +645,7 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
             G.nchunks = G.nsyms ? (uint32_t)((G.nbits + kChunkBits - 1) / kChunkBits) : 0;
             if (G.nsyms && !G.nchunks) throw Fail(DQTG_CORRUPT_BITSTREAM, "bitstream overrun");
             for (uint32_t c = 0; c < G.nchunks; ++c) chunks.push_back(ChunkDesc{(uint32_t)groups.size(), c});
-            rec_elems[(size_t)i * B + bucket] = G.elems;
+            if (bucket < B) rec_elems[(size_t)i * B + bucket] = G.elems;
             total += G.elems;
             groups.push_back(G);
         }
@@ -764,6 +780,7 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
         { DQTG_SPAN(e, "rle_total_kernel"); rle_total_kernel<<<(ng + 255) / 256 + 1, 256, 0, st>>>(d_groups, ng, d_eoff, d_ecnt, e.d_err); }
         e.launched(2);
         e.check_err();
+        if (!deferred_index.empty()) throw Fail(DQTG_CORRUPT_INDEX, deferred_index);
         auto* d_head = (uint32_t*)e.buf("d.head", (N + 1) * 4);
         auto* d_sidx = (uint32_t*)e.buf("d.sidx", (N + 1) * 4);
         auto* d_d = (uint8_t*)e.buf("d.delta", N + 16);
