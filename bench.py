@@ -4,9 +4,9 @@
 Workload (BASELINE.json configs[1], "C2"): GPT-2-small layout (124,439,808 fp32
 params, 148 tensors, layer types per SURVEY.md §8d), a synthetic training
 trajectory generated on the GPU with the reference generator's dynamics
-(w0 = 0.05 N(0,1); g = w + 0.0025 N(0,1); w -= lr g; lr = 0.1 * 0.9^t,
-trajectory.cpp:75-113), gradient EMA over the first two gradients, default
-QuantConfig (bins 16, embed 32, prune 0, protect 0.005, MAGNITUDE, sigma 0.2,
+(paper_2306_11800_b200/workloads.py: w0 = 0.05 N(0,1); g = w + 0.0025 N(0,1);
+w -= lr g; lr = 0.1 * 0.9^t, trajectory.cpp:75-113), gradient EMA over the first
+two gradients (the reference's ema_update arithmetic), default QuantConfig (bins 16, embed 32, prune 0, protect 0.005, MAGNITUDE, sigma 0.2,
 alpha 0.01).  One step = compute_scores (fused) + quantize_checkpoint +
 encode_delta_record against the previous snapshot's quantized state — the
 Chain::append path — for the next snapshot of the series.
@@ -18,8 +18,11 @@ step, record D2H, every step.
 Inputs per step (1 GB of weights+EMA) exceed the 126 MB L2, so no flush is needed.
 
 --impl reference: the unmodified reference library (oracle/_ref, compiled from
-/root/reference/proj sources) on the host cores, on a bounded sample of the
-same workload (two GPT-2 blocks + ln_f, 14.2 M params), same metric.
+/root/reference/proj sources) on the host cores, on the SAME workload and the
+SAME input bytes (the series is generated with the same seed by the same torch
+generator on the GPU and copied to the host): compute_scores + quantize_checkpoint
++ encode_delta_record per step, W warm-up then K timed steps, same metric.  The
+reference's compress path is single-threaded, so it uses one core.
 """
 from __future__ import annotations
 
@@ -41,29 +44,24 @@ sys.path.insert(0, ROOT)
 METRIC = "checkpoint compress+delta GB/s (fp32 in)"
 
 # ---------------------------------------------------------------------------- workload
-EMB, ATT, NORM, BIAS, LIN = 4, 2, 3, 5, 1
+from paper_2306_11800_b200 import workloads as W  # noqa: E402
+
+gpt2_small_layout = W.gpt2_small_layout
+numel = W.numel
+SEED = 1234  # rank r generates its shard's series with seed SEED + r
 
 
-def gpt2_small_layout(blocks=range(12), with_embed=True, with_lnf=True):
-    d, v, ctx = 768, 50257, 1024
-    L = []
-    if with_embed:
-        L += [("transformer.wte.weight", EMB, (v, d)), ("transformer.wpe.weight", EMB, (ctx, d))]
-    for i in blocks:
-        p = f"transformer.h.{i}."
-        L += [(p + "ln_1.weight", NORM, (d,)), (p + "ln_1.bias", BIAS, (d,)),
-              (p + "attn.c_attn.weight", ATT, (d, 3 * d)), (p + "attn.c_attn.bias", BIAS, (3 * d,)),
-              (p + "attn.c_proj.weight", ATT, (d, d)), (p + "attn.c_proj.bias", BIAS, (d,)),
-              (p + "ln_2.weight", NORM, (d,)), (p + "ln_2.bias", BIAS, (d,)),
-              (p + "mlp.c_fc.weight", LIN, (d, 4 * d)), (p + "mlp.c_fc.bias", BIAS, (4 * d,)),
-              (p + "mlp.c_proj.weight", LIN, (4 * d, d)), (p + "mlp.c_proj.bias", BIAS, (d,))]
-    if with_lnf:
-        L += [("transformer.ln_f.weight", NORM, (d,)), ("transformer.ln_f.bias", BIAS, (d,))]
-    return L
-
-
-def numel(shape):
-    return int(np.prod(shape, dtype=np.int64))
+def cpu_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
 
 
 def read_peak():
@@ -155,79 +153,87 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- reference arm
-def reference_sample_inputs(seed=7):
-    """Bounded CPU sample of the C2 workload: blocks 0-1 + ln_f of GPT-2 small."""
-    layout = gpt2_small_layout(blocks=range(2), with_embed=False)
-    N = sum(numel(s) for _, _, s in layout)
-    rng = np.random.default_rng(seed)
-    w1 = (0.05 * rng.standard_normal(N)).astype(np.float32)
-    g1 = (w1 + 0.0025 * rng.standard_normal(N)).astype(np.float32)
-    w2 = (w1 - np.float32(0.1) * g1).astype(np.float32)
-    g2 = (w2 + 0.0025 * rng.standard_normal(N)).astype(np.float32)
-    return layout, w1, w2, g1, g2
+def reference_chain(n_timed, n_warm, seed=SEED, cpu_seconds=None):
+    """The reference (oracle/_ref) on the C2 chain of the GPU arm, same bytes.
 
+    Snapshot 0 is quantized untimed (the chain's FULL base, as in our arm); step i
+    (i = 1 ...) = compute_scores + quantize_checkpoint + encode_delta_record(q_i,
+    q_{i-1}) of snapshot i, timed from the reference's Python API.  Returns
+    (per-step seconds of the timed steps, params, mean record bytes, same_bytes)."""
+    import torch
 
-def _ref_ckpt(d, layout, flat, step):
-    c = d.Checkpoint()
-    c.step = step
-    o = 0
-    for name, lt, shape in layout:
-        n = numel(shape)
-        c.add_tensor(name, flat[o:o + n].reshape(shape), d.LayerType(lt))
-        o += n
-    return c
-
-
-def reference_step_timer():
-    """Returns (time_one_step(), params, records) using the reference library."""
     from oracle import ref as R
 
     if not R.available():
         subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "ref"])
     d = R.load()
-    layout, w1, w2, g1, g2 = reference_sample_inputs()
-    c1, c2 = _ref_ckpt(d, layout, w1, 1), _ref_ckpt(d, layout, w2, 2)
+    layout = gpt2_small_layout()
+    N = W.layout_params(layout)
+    gpu = torch.cuda.is_available()
+    dev = torch.device("cuda", 0) if gpu else torch.device("cpu")
+    tr = W.Trajectory(torch, N, seed, dev)
+
+    def host_ckpt(x, step):
+        host = x.cpu().numpy()
+        c = d.Checkpoint()
+        c.step = step
+        for (name, lt, shape), v in zip(layout, W.split(host, layout)):
+            c.add_tensor(name, v.reshape(shape), d.LayerType(lt))
+        return c
+
+    s0, s1 = tr.next(), tr.next()
     ema = d.ema_init(0.9)
-    d.ema_update(ema, _ref_ckpt(d, layout, g1, 1))
-    d.ema_update(ema, _ref_ckpt(d, layout, g2, 2))
+    for k, g in enumerate(tr.grads):
+        d.ema_update(ema, host_ckpt(g, k + 1))
+    tr.grads = []
     cfg = d.QuantConfig()
-    s1 = d.compute_scores(c1, ema)
-    q1 = d.quantize_checkpoint(c1, s1, cfg, 1)
-    out = {}
-
-    def step():
+    c = host_ckpt(s0, 0)
+    q_prev = d.quantize_checkpoint(c, d.compute_scores(c, ema), cfg, 1)
+    ts, rec = [], []
+    pending = s1
+    t_end = None if cpu_seconds is None else time.perf_counter() + cpu_seconds
+    i = 0
+    while True:
+        i += 1
+        if i > n_warm + n_timed and (t_end is None or time.perf_counter() >= t_end):
+            break
+        snap = pending if pending is not None else tr.next()
+        pending = None
+        c = host_ckpt(snap, i)
+        del snap
         t = time.perf_counter()
-        s2 = d.compute_scores(c2, ema)
-        q2 = d.quantize_checkpoint(c2, s2, cfg, 1)
-        rec = d.encode_delta_record(q2, q1)
+        q = d.quantize_checkpoint(c, d.compute_scores(c, ema), cfg, 1)
+        r = d.encode_delta_record(q, q_prev)
         dt = time.perf_counter() - t
-        out["record"] = bytes(rec)
-        return dt
-
-    N = sum(numel(s) for _, _, s in layout)
-    return step, N, out
+        if i > n_warm:
+            ts.append(dt)
+            rec.append(len(r))
+        q_prev = q
+        del c
+    return ts, N, float(np.mean(rec)), gpu
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    step, N, out = reference_step_timer()
-    for _ in range(args.warmup):
-        step()
-    ts = [step() for _ in range(args.steps)]
+    ts, N, rec_mean, same = reference_chain(args.steps, args.warmup)
     t = sum(ts)
-    value = 4.0 * N * args.steps / t / 1e9
+    value = 4.0 * N * len(ts) / t / 1e9
+    sample = (f"C2 full ({N} params), {args.warmup} warm-up + {len(ts)} timed steps of "
+              f"compute_scores+quantize_checkpoint+encode_delta_record, oracle/_ref, 1 thread")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / len(ts),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
-        "config": {"workload": "C2 GPT-2-small compress+delta, bounded CPU sample "
-                               "(blocks 0-1 + ln_f, 14.2M params)", "params": N},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "reference",
-                         "sample": f"{N} params (GPT-2 small blocks 0-1 + ln_f), "
-                                   f"{args.steps} steps of quantize+encode_delta"},
+        "data": "synthetic (GPU trajectory with the reference generator dynamics)",
+        "config": {"workload": "C2: GPT-2-small layout 124.4M fp32 params, delta chain",
+                   "params_per_gpu": N, "quant_config": "default (bins16/embed32/"
+                   "protect0.005/MAGNITUDE/sigma0.2/alpha0.01), EMA sensitivity",
+                   "same_config": True, "same_bytes": same, "seed": SEED,
+                   "record_bytes": rec_mean, "compression_ratio": 4.0 * N / rec_mean},
+        "cpu_baseline": dict({"value": value, "unit": "GB/s", "cores": 1, "kind": "reference",
+                              "sample": sample}, **cpu_info()),
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -298,31 +304,7 @@ def measure_ingest(eng, layout, flat, cpu=True, reps=3):
         os.unlink(path)
 
 
-def gen_series(torch, layout, n_snap, seed, device):
-    """Synthetic trajectory on the GPU (reference generator dynamics)."""
-    N = sum(numel(s) for _, _, s in layout)
-    g = torch.Generator(device=device).manual_seed(seed)
-    w = 0.05 * torch.randn(N, generator=g, device=device, dtype=torch.float32)
-    lr = 0.1
-    snaps, grads = [], []
-    for s in range(n_snap):
-        snaps.append(w.clone())
-        gr = w + 0.0025 * torch.randn(N, generator=g, device=device, dtype=torch.float32)
-        if s < 2:
-            grads.append(gr)
-        w = w - lr * gr
-        lr *= 0.9
-    ema = grads[0].clone()
-    ema = 0.9 * grads[1] + (1.0 - 0.9) * ema
-    return snaps, ema
-
-
-def tensor_ptrs(base_ptr, layout):
-    ptrs, o = [], 0
-    for _, _, s in layout:
-        ptrs.append(base_ptr + 4 * o)
-        o += numel(s)
-    return ptrs
+tensor_ptrs = W.tensor_ptrs
 
 
 def run_ours(args):
@@ -357,7 +339,7 @@ def run_ours(args):
     cfg = E.Config()
     n_snap = args.warmup + args.steps + 1
 
-    snaps, ema = gen_series(torch, layout, n_snap, 1234 + rank, dev)
+    snaps, ema = W.series(torch, layout, n_snap, SEED + rank, dev)
     torch.cuda.synchronize()
     ckpts = []
     for s in snaps:
@@ -431,7 +413,8 @@ def run_ours(args):
     if world == 1 and not args.no_pipeline:
         from paper_2306_11800_b200.pipeline import ChainCompressor
 
-        cc = ChainCompressor(local, workers=args.workers)
+        # every run forks from / joins into `stream`: CUDA events on it time the chain
+        cc = ChainCompressor(local, workers=args.workers, stream=stream.cuda_stream)
         torch.cuda.synchronize()
         # warm-up: at least two steps per worker (scratch and pool sizes settle)
         n_warm = max(args.warmup + 1, 2 * args.workers + 2)
@@ -439,11 +422,10 @@ def run_ours(args):
         base = cc.run(warm, cfg, 1, list(range(n_warm)))
         # one untimed pass over the timed snapshots (first-pass pool/scheduling effects)
         cc.run(ckpts[args.warmup + 1:], cfg, 1, list(range(args.warmup + 1, n_snap)), base=base)
-        cc.sync()
         torch.cuda.synchronize()
         # three timed passes of exactly K steps each; the median is reported (the
         # worker threads share the host CPU with the rest of the VM)
-        pipe_reps = []
+        pipe_reps, pipe_wall = [], []
         gc.collect()
         gc.disable()
         clocks_p = ClockSampler(local)
@@ -452,10 +434,12 @@ def run_ours(args):
             l0 = cc.launches
             torch.cuda.synchronize()
             tp0 = time.perf_counter()
+            t0.record(stream)
             cc.run(ckpts[args.warmup + 1:], cfg, 1, list(range(args.warmup + 1, n_snap)), base=base)
-            cc.sync()
+            t1.record(stream)
             torch.cuda.synchronize()
-            pipe_reps.append((time.perf_counter() - tp0) * 1e3)
+            pipe_wall.append((time.perf_counter() - tp0) * 1e3)
+            pipe_reps.append(t0.elapsed_time(t1))
             launches_p = cc.launches - l0
         clocks_p.__exit__(None, None, None)
         gc.enable()
@@ -533,7 +517,6 @@ def run_ours(args):
         # one untimed pass over the timed series (first-pass pool/scheduling effects)
         e2e_base = cc.run(host_series(0, e2e_steps), cfg, 1, list(range(2 * cc.nw + 2,
                           2 * cc.nw + 2 + e2e_steps)), base=e2e_base, on_record=grab, host=host)
-        cc.sync()
         # three timed passes of e2e_steps steps; the median is reported
         e2e_reps = []
         gc.collect()
@@ -545,7 +528,6 @@ def run_ours(args):
             cc.run(host_series(2 * cc.nw + 2, e2e_steps), cfg, 1,
                    list(range(2 * cc.nw + 2, 2 * cc.nw + 2 + e2e_steps)), base=e2e_base,
                    on_record=grab, host=host)
-            cc.sync()
             torch.cuda.synchronize()
             e2e_reps.append(time.perf_counter() - te)
         gc.enable()
@@ -649,16 +631,18 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        stepf, Ns, _ = reference_step_timer()
-        stepf()
-        ts = []
-        t_end = time.perf_counter() + args.cpu_seconds
-        while time.perf_counter() < t_end or len(ts) < 2:
-            ts.append(stepf())
+        # the reference on the same C2 chain and bytes, a bounded number of steps
+        del ckpts
+        torch.cuda.empty_cache()
+        ts, Ns, rec_ref, same = reference_chain(args.cpu_steps, 0)
         v = 4.0 * Ns * len(ts) / sum(ts) / 1e9
-        cpu = {"value": v, "unit": "GB/s", "cores": 1, "kind": "reference",
-               "sample": f"{Ns} params (GPT-2 small blocks 0-1 + ln_f), {len(ts)} steps of "
-                         f"compute_scores+quantize_checkpoint+encode_delta_record, oracle/_ref"}
+        cpu = dict({"value": v, "unit": "GB/s", "cores": 1, "kind": "reference",
+                    "sample": f"C2 full ({Ns} params), steps 1..{len(ts)} of the same chain and "
+                              f"bytes (compute_scores+quantize_checkpoint+encode_delta_record, "
+                              f"oracle/_ref, 1 thread)",
+                    "same_bytes": same, "record_bytes": rec_ref,
+                    "record_bytes_match_gpu_arm": bool(rec_ref == float(np.mean(rec_bytes[:len(ts)])))
+                    if len(rec_bytes) >= len(ts) else None}, **cpu_info())
 
     if rank == 0:
         line = {
@@ -678,9 +662,11 @@ def run_ours(args):
                        "ms_per_step_pipelined_reps": None if pipelined is None else
                        [round(x / args.steps, 4) for x in pipe_reps],
                        "host_syncs_per_step": syncs_per_step,
+                       "ms_per_step_pipelined_wall": None if pipelined is None else
+                       [round(x / args.steps, 4) for x in pipe_wall],
                        "timing": (f"pipelined chain: {args.workers} worker streams (step k on "
-                                  f"worker k mod {args.workers}), host wall clock with device "
-                                  f"sync on both ends, median of 3 passes"
+                                  f"worker k mod {args.workers}) forked from and joined into the "
+                                  f"timing stream, CUDA events on it, median of 3 passes"
                                   if pipelined is not None and ms == pipelined else
                                   "CUDA events on the engine stream")},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "restore": restore,
@@ -699,7 +685,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-steps", type=int, default=2,
+                    help="timed reference steps of the cpu_baseline leg (~10 s each at C2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true")
     ap.add_argument("--workers", type=int, default=4, help="worker streams of the chain pipeline")

@@ -233,13 +233,15 @@ dqtg_status dqtg_compress_step(dqtg_engine *e, const dqtg_ckpt *c, const dqtg_co
 
 /* ---- pipelined delta chain (Chain::append over a series, chain.cpp:86-129) ----
  * A pool of `workers` engines, each on its own CUDA stream and host thread.
- * Snapshot k runs on worker k mod W: its weights are copied into the worker's
- * device checkpoint (from host or device memory), quantized, then encoded as a
- * delta against snapshot k-1 (the stream waits on the event recorded after
- * quantize(k-1)); states are released once both encodes that read them are
- * done.  Records are identical to dqtg_compress_step run in order.
- * weights[k * n_tensors + i] = tensor i of snapshot k (`_any`); ema[i] (`_any`,
- * null: magnitude scores only).  on_record(user, k, record) runs on a worker
+ * Snapshot k runs on worker k mod W: quantized, then encoded as a delta against
+ * snapshot k-1 (the stream waits on the event recorded after quantize(k-1));
+ * states are released once both encodes that read them are done.  Records are
+ * identical to dqtg_compress_step run in order.
+ * weights[k * n_tensors + i] = tensor i of snapshot k (`_any`); ema[k * n_tensors
+ * + i] = tensor i of snapshot k's gradient EMA (`_any`; the array null: magnitude
+ * scores only).  A snapshot (or EMA) whose tensors form one device buffer in the
+ * engine's padded layout (tensor i at base + off_i, as a dqtg_ckpt holds it) is
+ * read in place; other snapshots are copied into a worker buffer first.  on_record(user, k, record) runs on a worker
  * thread (calls may arrive out of step order; the record is valid during the
  * call).  *last_out (optional) receives the state of the last snapshot. */
 typedef struct dqtg_pipe dqtg_pipe;
@@ -247,6 +249,10 @@ typedef void (*dqtg_record_fn)(void *user, uint64_t k, const dqtg_record *record
 dqtg_status dqtg_pipe_create(int device, int workers, dqtg_pipe **out);
 void dqtg_pipe_destroy(dqtg_pipe *p);
 uint64_t dqtg_pipe_launches(const dqtg_pipe *p);
+/* Orders every later dqtg_pipe_run's device work after the work queued on
+ * `stream` (a cudaStream_t; null: none) before the run, and makes `stream` wait
+ * for all workers at the end, so events recorded on it bracket the whole chain. */
+void dqtg_pipe_set_stream(dqtg_pipe *p, void *stream);
 dqtg_status dqtg_pipe_run(dqtg_pipe *p, const dqtg_layout *layout,
                           const float *const *weights_any, uint64_t n_snapshots,
                           const uint64_t *steps, const float *const *ema_any,

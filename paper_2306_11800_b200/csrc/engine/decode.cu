@@ -89,16 +89,12 @@ __device__ __forceinline__ uint32_t decode_one(const uint64_t* rec64, const Grou
     return L;
 }
 
-// H1: decode chunk c from start[c] to its nominal end (dirty chunks only)
-__global__ void __launch_bounds__(256) huff_sync_kernel(const uint64_t* rec64, const GroupDesc* groups,
-                                                        const ChunkDesc* chunks, uint32_t nchunks,
-                                                        DecTabs T, const uint64_t* start,
-                                                        uint64_t* out_pos, uint32_t* count,
-                                                        const uint8_t* dirty, uint16_t* bounds) {
-    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= nchunks || !dirty[c]) return;
-    const ChunkDesc C = chunks[c];
-    const GroupDesc G = groups[C.group];
+// Decodes chunk c from start[c] to its nominal end: end position, symbol count and
+// the first kBnd codeword starts (relative to the chunk's nominal start).
+__device__ __forceinline__ void decode_chunk(const uint64_t* rec64, const GroupDesc& G,
+                                             const ChunkDesc& C, const DecTabs& T, uint32_t c,
+                                             const uint64_t* start, uint64_t* out_pos,
+                                             uint32_t* count, uint16_t* bounds) {
     const uint64_t end = min((uint64_t)(C.local + 1) * kChunkBits, G.nbits);
     const uint64_t nom = (uint64_t)C.local * kChunkBits;
     uint64_t p = start[c];
@@ -116,9 +112,38 @@ __global__ void __launch_bounds__(256) huff_sync_kernel(const uint64_t* rec64, c
     count[c] = n;
 }
 
-// H1 update: a chunk's start is where the previous chunk's decode ended.  When that
-// position is one of the codeword starts the chunk's own (speculative) decode went
-// through, its end position is already right and only its symbol count shrinks.
+// Moves chunk c's start to `s` (where the previous chunk's decode ended).  When `s`
+// is one of the codeword starts the chunk's own (speculative) decode went through,
+// its end position is already right and only its symbol count shrinks: returns
+// false.  Otherwise the chunk must be decoded again: returns true.
+__device__ __forceinline__ bool restart_chunk(uint32_t c, uint32_t local, uint64_t s,
+                                              uint64_t* start, uint32_t* count, uint16_t* bounds) {
+    start[c] = s;
+    const uint64_t rel = s - (uint64_t)local * kChunkBits;
+    uint16_t* bnd = bounds + (size_t)c * kBnd;
+    int hit = -1;
+    for (int k = 0; k < kBnd && hit < 0; ++k)
+        if (bnd[k] == rel) hit = k;
+    if (hit < 0) return true;
+    count[c] -= (uint32_t)hit;
+    for (int k = 0; k + hit < kBnd; ++k) bnd[k] = bnd[k + hit];
+    for (int k = kBnd - hit; k < kBnd; ++k) bnd[k] = 0xffff;
+    return false;
+}
+
+// H1: decode chunk c from start[c] to its nominal end (dirty chunks only)
+__global__ void __launch_bounds__(256) huff_sync_kernel(const uint64_t* rec64, const GroupDesc* groups,
+                                                        const ChunkDesc* chunks, uint32_t nchunks,
+                                                        DecTabs T, const uint64_t* start,
+                                                        uint64_t* out_pos, uint32_t* count,
+                                                        const uint8_t* dirty, uint16_t* bounds) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nchunks || !dirty[c]) return;
+    const ChunkDesc C = chunks[c];
+    decode_chunk(rec64, groups[C.group], C, T, c, start, out_pos, count, bounds);
+}
+
+// H1 update: every chunk takes the previous chunk's end as its start (in parallel)
 __global__ void huff_update_kernel(const ChunkDesc* chunks, uint32_t nchunks, uint64_t* start,
                                    const uint64_t* out_pos, uint32_t* count, uint8_t* dirty,
                                    uint16_t* bounds, uint32_t* any) {
@@ -128,24 +153,32 @@ __global__ void huff_update_kernel(const ChunkDesc* chunks, uint32_t nchunks, ui
     const uint32_t local = chunks[c].local;
     if (local > 0) {
         const uint64_t s = out_pos[c - 1];
-        if (s != start[c]) {
-            start[c] = s;
-            const uint64_t rel = s - (uint64_t)local * kChunkBits;
-            uint16_t* bnd = bounds + (size_t)c * kBnd;
-            int hit = -1;
-            for (int k = 0; k < kBnd && hit < 0; ++k)
-                if (bnd[k] == rel) hit = k;
-            if (hit >= 0) {  // synchronised inside the recorded prefix
-                count[c] -= (uint32_t)hit;
-                for (int k = 0; k + hit < kBnd; ++k) bnd[k] = bnd[k + hit];
-                for (int k = kBnd - hit; k < kBnd; ++k) bnd[k] = 0xffff;
-            } else {
-                d = 1;
-            }
-        }
+        if (s != start[c]) d = restart_chunk(c, local, s, start, count, bounds);
     }
     dirty[c] = d;
     if (d) *any = 1;
+}
+
+// H1 fallback when the parallel passes have not converged: one thread per group walks
+// its chunks in order, so every start is final after one sweep.  Codes whose lengths
+// share a common factor that does not divide the chunk size (e.g. a complete table of
+// 3-bit codes) never fall back into step from a wrong phase: the parallel passes
+// would fix one chunk per pass.  Costs at most one sequential decode of the group.
+__global__ void huff_serial_sync_kernel(const uint64_t* rec64, const GroupDesc* groups, uint32_t ngroups,
+                                        const ChunkDesc* chunks, DecTabs T, uint64_t* start,
+                                        uint64_t* out_pos, uint32_t* count, uint16_t* bounds,
+                                        const uint8_t* dirty) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= ngroups) return;
+    const GroupDesc G = groups[g];
+    for (uint32_t l = 1; l < G.nchunks; ++l) {
+        const uint32_t c = G.chunk0 + l;
+        const uint64_t s = out_pos[c - 1];
+        // dirty: start already moved by the last update, decode still pending
+        bool redo = dirty[c] != 0;
+        if (s != start[c]) redo = restart_chunk(c, l, s, start, count, bounds);
+        if (redo) decode_chunk(rec64, G, chunks[c], T, c, start, out_pos, count, bounds);
+    }
 }
 
 __global__ void group_flags_kernel(const GroupDesc* groups, uint32_t ng, uint8_t* f) {
@@ -312,18 +345,6 @@ __global__ void __launch_bounds__(256) prev_scan_kernel(const uint32_t* tile0, u
     if (threadIdx.x == 0) {
         totals[(size_t)t * B + b] = run;
         if (run != rec_elems[(size_t)t * B + b]) atomicOr(err, kErrCorruptIndex);
-    }
-}
-
-// U2b: per tensor, start of every key's group in the rearranged order
-__global__ void group_start_kernel(uint32_t nt, uint32_t B, const unsigned long long* totals,
-                                   unsigned long long* gstart) {
-    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= nt) return;
-    unsigned long long acc = 0;
-    for (uint32_t b = 0; b < B; ++b) {
-        gstart[(size_t)t * B + b] = acc;
-        acc += totals[(size_t)t * B + b];
     }
 }
 
@@ -521,7 +542,7 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
     std::vector<ChunkDesc> chunks;
     std::vector<int64_t> tab_sym;
     std::vector<uint8_t> tab_len;
-    std::vector<unsigned long long> rec_elems((size_t)nt * B, 0);
+    std::vector<unsigned long long> rec_elems((size_t)nt * B, 0), gstart_h((size_t)nt * B, 0);
     std::vector<uint64_t> lim, first;
     std::vector<uint32_t> lbase;
     uint64_t stream_pos = 0, sym_total = 0;
@@ -580,7 +601,7 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
         // groups of the payload (codec.cpp:283-300)
         const uint64_t ng = r.uv();
         uint64_t total = 0;
-        int64_t last_bucket = -1;
+        std::vector<uint8_t> seen_bucket(B, 0);
         for (uint64_t k = 0; k < ng; ++k) {
             GroupDesc G{};
             const uint64_t bucket = r.uv();
@@ -590,37 +611,54 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
             // the reference finds a bad bucket only in unrearrange, after the group
             // bitstreams decoded (codec.cpp:330-355): reported after the Huffman and
             // RLE stages so that their CorruptBitstream wins, as there
-            if ((bucket >= B || (int64_t)bucket <= last_bucket) && deferred_index.empty())
-                deferred_index = "group bucket out of order in " + names[i];
-            last_bucket = (int64_t)bucket;
+            // unrearrange (codec.cpp:56-64) takes the groups in any order but rejects
+            // out-of-range and duplicate buckets
+            if (bucket >= B || seen_bucket[bucket]) {
+                if (deferred_index.empty())
+                    deferred_index = std::string(bucket >= B ? "group bucket outside cyclic alphabet"
+                                                             : "duplicate group bucket") + " in " + names[i];
+            } else {
+                seen_bucket[bucket] = 1;
+            }
             // every table entry takes >= 2 bytes: a larger count runs out of record
             if (tsize > (r.n - r.at) / 2) throw Fail(DQTG_TRUNCATED, "huffman table exceeds the record");
             G.tab_off = (uint32_t)tab_sym.size();
             G.tsize = (uint32_t)tsize;
             for (uint64_t j = 0; j < tsize; ++j) {
-                const int64_t s = r.sv();
-                const uint8_t l = r.u8();
-                if (l == 0 || l > kMaxCodeLen - 1) throw Fail(DQTG_CORRUPT_BITSTREAM, "invalid code length");
-                if (s > INT32_MAX || s < -(int64_t)0xffff)
-                    throw Fail(DQTG_CORRUPT_BITSTREAM, "run value out of range");
-                if (j && (l < tab_len.back() || (l == tab_len.back() && s <= tab_sym.back())))
-                    throw Fail(DQTG_CORRUPT_BITSTREAM, "huffman table not canonical");
+                int64_t s = r.sv();
+                // a symbol only matters once decoded: values beyond u16 and run lengths
+                // beyond any group are clamped to sentinels the RLE stage rejects
+                // (codec.cpp:96-99), as the reference rejects them only when read
+                if (s > INT32_MAX) s = INT32_MAX;
+                if (s < -(int64_t)0x10000) s = -(int64_t)0x10000;
                 tab_sym.push_back(s);
-                tab_len.push_back(l);
+                tab_len.push_back(r.u8());
             }
             const uint64_t nb = r.uv();
             r.need(nb);
             G.bit_off = r.at * 8;
             G.nbits = nb * 8;
             r.at += nb;
-            if (G.nsyms && !tsize) throw Fail(DQTG_CORRUPT_BITSTREAM, "empty huffman table");
-            if (G.nsyms > G.nbits) throw Fail(DQTG_CORRUPT_BITSTREAM, "more symbols than bits");
-            // canonical decode limits (codec.cpp:137-214 assign_codes)
             G.lim_off = (uint32_t)lim.size();
             lim.resize(lim.size() + kMaxCodeLen + 1, ~0ull);
             first.resize(first.size() + kMaxCodeLen + 1, 0);
             lbase.resize(lbase.size() + kMaxCodeLen + 1, 0);
-            if (tsize) {
+            // huffman_decode (codec.cpp:234-250) validates the table only when the group
+            // has symbols: empty table, canonical order, lengths and the Kraft sum of
+            // assign_codes (codec.cpp:196-214)
+            if (G.nsyms) {
+                if (!tsize) throw Fail(DQTG_CORRUPT_BITSTREAM, "empty huffman table");
+                for (uint64_t j = 1; j < tsize; ++j) {
+                    const uint32_t a = G.tab_off + (uint32_t)j;
+                    if (tab_len[a] < tab_len[a - 1] || (tab_len[a] == tab_len[a - 1] && tab_sym[a] <= tab_sym[a - 1]))
+                        throw Fail(DQTG_CORRUPT_BITSTREAM, "huffman table not canonical");
+                }
+                for (uint64_t j = 0; j < tsize; ++j) {
+                    const uint8_t l = tab_len[G.tab_off + j];
+                    if (l == 0 || l > kMaxCodeLen - 1) throw Fail(DQTG_CORRUPT_BITSTREAM, "bad huffman table");
+                }
+                if (G.nsyms > G.nbits) throw Fail(DQTG_CORRUPT_BITSTREAM, "more symbols than bits");
+                // canonical decode limits
                 G.minlen = tab_len[G.tab_off];
                 G.maxlen = tab_len[G.tab_off + tsize - 1];
                 uint64_t code = 0;
@@ -633,9 +671,10 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
                     uint32_t cntL = 0;
                     while (j < tsize && tab_len[G.tab_off + j] == L) ++j, ++cntL;
                     code += cntL;
-                    if (L < 64 && (code >> L) > 1) throw Fail(DQTG_CORRUPT_BITSTREAM, "oversubscribed huffman code");
-                    lim[G.lim_off + L] = L == 64 ? ~0ull : (code << (64 - L));
-                    if (L < 64 && code == (1ull << L)) lim[G.lim_off + L] = ~0ull;  // complete code
+                    // Kraft sum > 1 <=> the next canonical code passes 2^L (L <= 63)
+                    if (code > (1ull << L)) throw Fail(DQTG_CORRUPT_BITSTREAM, "huffman table overfull");
+                    lim[G.lim_off + L] = code << (64 - L);
+                    if (code == (1ull << L)) lim[G.lim_off + L] = ~0ull;  // complete code
                 }
             }
             G.elem_off = stream_pos + total;
@@ -645,7 +684,10 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
             G.nchunks = G.nsyms ? (uint32_t)((G.nbits + kChunkBits - 1) / kChunkBits) : 0;
             if (G.nsyms && !G.nchunks) throw Fail(DQTG_CORRUPT_BITSTREAM, "bitstream overrun");
             for (uint32_t c = 0; c < G.nchunks; ++c) chunks.push_back(ChunkDesc{(uint32_t)groups.size(), c});
-            if (bucket < B) rec_elems[(size_t)i * B + bucket] = G.elems;
+            if (bucket < B) {  // the group's place in the dense rearranged stream (record order)
+                rec_elems[(size_t)i * B + bucket] = G.elems;
+                gstart_h[(size_t)i * B + bucket] = total;
+            }
             total += G.elems;
             groups.push_back(G);
         }
@@ -741,8 +783,16 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
         if (nc) { DQTG_SPAN(e, "chunk_init_kernel"); chunk_init_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_chunks, nc, d_start); }
         DQTG_CUDA(cudaMemsetAsync(d_dirty, 1, nc, st));
         const unsigned gb = (nc + 255) / 256;
+        // a few parallel passes converge for Huffman tables in practice; what is still
+        // out of step after them is finished by the sequential per-group sweep
+        constexpr int kParallelPasses = 4;
         for (int it = 0; nc; ++it) {
-            DQTG_REQUIRE(it < 64, DQTG_CORRUPT_BITSTREAM, "huffman chunk synchronisation did not converge");
+            if (it == kParallelPasses) {
+                DQTG_SPAN(e, "huff_serial_sync_kernel");
+                huff_serial_sync_kernel<<<(ng + 127) / 128, 128, 0, st>>>(rec64, d_groups, ng, d_chunks, T, d_start, d_out, d_cnt, d_bnd, d_dirty);
+                e.launched(1);
+                break;
+            }
             { DQTG_SPAN(e, "huff_sync_kernel"); huff_sync_kernel<<<gb, 256, 0, st>>>(rec64, d_groups, d_chunks, nc, T, d_start, d_out, d_cnt, d_dirty, d_bnd); }
             DQTG_CUDA(cudaMemsetAsync(d_any, 0, 4, st));
             { DQTG_SPAN(e, "huff_update_kernel"); huff_update_kernel<<<gb, 256, 0, st>>>(d_chunks, nc, d_start, d_out, d_cnt, d_dirty, d_bnd, d_any); }
@@ -797,6 +847,7 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
         // ---- U: unrearrange against the previous levels
         auto* d_tc = (uint32_t*)e.buf("d.tilecnt", (size_t)ntiles * B * 4 + 4);
         auto* d_gs = (unsigned long long*)e.buf("d.gstart", (size_t)nt * B * 8 + 8);
+        e.to_device(d_gs, gstart_h.data(), gstart_h.size() * 8);
         auto* d_cbl = (uint32_t*)e.buf("d.cblen", kLayerTypes * 4);
         e.to_device(d_cbl, q->cb_len, sizeof(q->cb_len));
         const uint16_t* prev = base ? base->d_levels : nullptr;
@@ -804,9 +855,8 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
             { DQTG_SPAN(e, "prev_count_kernel"); prev_count_kernel<<<ntiles, 256, 0, st>>>(L.d_tiles, prev, B, d_tc, e.d_err); }
             auto* d_tot = (unsigned long long*)e.buf("d.ktot", (size_t)nt * B * 8 + 8);
             { DQTG_SPAN(e, "prev_scan_kernel"); prev_scan_kernel<<<nt * B, 256, 0, st>>>(L.d_tile0, B, d_tc, d_relems, d_tot, e.d_err); }
-            { DQTG_SPAN(e, "group_start_kernel"); group_start_kernel<<<(nt + 127) / 128, 128, 0, st>>>(nt, B, d_tot, d_gs); }
             { DQTG_SPAN(e, "unrearrange_kernel"); unrearrange_kernel<<<ntiles, 256, 0, st>>>(L.d_tiles, L.d_types, L.d_stream_off, L.d_off, prev, B, d_tc, d_gs, d_d, d_cbl, q->d_levels, e.d_err); }
-            e.launched(4);
+            e.launched(3);
         }
         e.check_err();
     }

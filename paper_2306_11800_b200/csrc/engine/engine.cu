@@ -578,6 +578,7 @@ std::shared_ptr<Layout> make_layout(Engine* e, const dqtg_layout* l) {
 }
 
 DevCkpt::~DevCkpt() {
+    if (!own) return;
     cudaFree(w);
     cudaFree(ema);
     cudaFree(mag);

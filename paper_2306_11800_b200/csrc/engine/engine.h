@@ -139,6 +139,7 @@ struct DevCkpt {
     bool explicit_scores = false;
     bool has_sens = false;
     bool ema_seeded = false;
+    bool own = true;  // false: w / ema are borrowed (the worker pool aliases caller buffers)
     ~DevCkpt();
 };
 

@@ -4,7 +4,9 @@
 // W workers, each an engine with its own non-blocking CUDA stream and a host
 // thread.  Snapshot k runs on worker k mod W:
 //
-//   copy weights(k) -> worker checkpoint      (H2D from pinned host, or D2D)
+//   weights(k), EMA(k) -> worker checkpoint   (device snapshots in the padded
+//                                             layout are read in place; others
+//                                             are copied H2D / D2D)
 //   quantize(k)                               (passes A/B, k-means, pass C)
 //   record event q[k]; publish state k
 //   wait state k-1 published; stream waits on q[k-1]
@@ -29,12 +31,28 @@ using namespace dqtg;
 
 struct dqtg_pipe {
     int device = 0;
+    // optional caller stream (dqtg_pipe_set_stream): every run's device work is
+    // ordered after the work queued on it before the run, and work queued on it
+    // after the run waits for every worker, so events on it time the whole chain
+    cudaStream_t join = nullptr;
     // worker engines: released (not deleted) so states handed out stay valid
     struct Release {
         void operator()(Engine* e) const { engine_release(e); }
     };
     std::vector<std::unique_ptr<Engine, Release>> eng;
-    std::vector<std::unique_ptr<DevCkpt>> ck;  // per worker, rebuilt when the layout changes
+    // per worker: a borrowing checkpoint view + owned staging buffers for snapshots
+    // that are not device-resident in the padded layout (rebuilt when the layout changes)
+    struct Slot {
+        std::unique_ptr<DevCkpt> ck;
+        float* wbuf = nullptr;
+        float* ebuf = nullptr;
+        const float* ebuf_src = nullptr;  // EMA currently in ebuf (per run)
+        ~Slot() {
+            cudaFree(wbuf);
+            cudaFree(ebuf);
+        }
+    };
+    std::vector<std::unique_ptr<Slot>> ck;
 };
 
 namespace {
@@ -55,6 +73,27 @@ bool same_layout(const Layout& a, const dqtg_layout* l) {
 void upload(Engine& e, const Layout& L, float* dst, const float* const* src) {
     for (uint32_t i = 0; i < L.nt; ++i)
         if (L.numel[i]) e.to_device(dst + L.off[i], src[i], L.numel[i] * 4);
+}
+
+// The tensors of one snapshot form a device buffer in the engine's padded layout
+// (tensor i at base + off[i], e.g. a dqtg_ckpt): the passes read it in place.
+const float* padded_view(const Layout& L, const float* const* src) {
+    if (!L.nt || !is_device_ptr(src[0])) return nullptr;
+    const float* base = src[0] - L.off[0];
+    for (uint32_t i = 1; i < L.nt; ++i)
+        if (src[i] != base + L.off[i]) return nullptr;
+    return base;
+}
+
+// weights / EMA of snapshot k for the worker: in place or staged
+float* stage(Engine& e, const Layout& L, const float* const* src, float*& buf) {
+    if (const float* v = padded_view(L, src)) return const_cast<float*>(v);
+    if (!buf) {
+        DQTG_CUDA(cudaMalloc(&buf, L.Np * 4));
+        DQTG_CUDA(cudaMemsetAsync(buf, 0, L.Np * 4, e.stream));
+    }
+    upload(e, L, buf, src);
+    return buf;
 }
 
 struct Run {
@@ -108,6 +147,8 @@ void dqtg_pipe_destroy(dqtg_pipe* p) {
     delete p;
 }
 
+void dqtg_pipe_set_stream(dqtg_pipe* p, void* stream) { p->join = (cudaStream_t)stream; }
+
 uint64_t dqtg_pipe_launches(const dqtg_pipe* p) {
     uint64_t n = 0;
     for (auto& e : p->eng) n += e->launches;
@@ -122,28 +163,29 @@ dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* 
     try {
         const int W = (int)p->eng.size();
         DQTG_CUDA(cudaSetDevice(p->device));
-        // worker checkpoints (weights + EMA) for this layout
+        // worker checkpoint views for this layout
         for (int w = 0; w < W; ++w) {
             Engine& e = *p->eng[w];
-            auto& c = p->ck[w];
-            if (!c || !same_layout(*c->L, layout)) {
-                c = std::make_unique<DevCkpt>();
-                c->eng = &e;
-                c->L = make_layout(&e, layout);
-                DQTG_CUDA(cudaMalloc(&c->w, c->L->Np * 4));
-                DQTG_CUDA(cudaMemsetAsync(c->w, 0, c->L->Np * 4, e.stream));
+            auto& sl = p->ck[w];
+            if (!sl || !same_layout(*sl->ck->L, layout)) {
+                sl = std::make_unique<dqtg_pipe::Slot>();
+                sl->ck = std::make_unique<DevCkpt>();
+                sl->ck->eng = &e;
+                sl->ck->own = false;
+                sl->ck->L = make_layout(&e, layout);
             }
-            c->explicit_scores = false;
-            c->has_sens = ema != nullptr;
-            if (ema) {
-                if (!c->ema) {
-                    DQTG_CUDA(cudaMalloc(&c->ema, c->L->Np * 4));
-                    DQTG_CUDA(cudaMemsetAsync(c->ema, 0, c->L->Np * 4, e.stream));
-                }
-                upload(e, *c->L, c->ema, ema);
-                c->ema_seeded = true;
-            }
-            e.sync();
+            sl->ebuf_src = nullptr;
+            DevCkpt& c = *sl->ck;
+            c.explicit_scores = false;
+            c.has_sens = ema != nullptr;
+            c.ema_seeded = ema != nullptr;
+        }
+        if (p->join) {  // fork: the workers start after the caller stream's prior work
+            cudaEvent_t ev;
+            DQTG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            DQTG_CUDA(cudaEventRecord(ev, p->join));
+            for (auto& e : p->eng) DQTG_CUDA(cudaStreamWaitEvent(e->stream, ev, 0));
+            cudaEventDestroy(ev);
         }
         const uint32_t nt = layout->n_tensors;
         const bool tl = getenv("DQTG_TIMELINE") != nullptr;
@@ -169,7 +211,8 @@ dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* 
         };
         auto worker = [&](int w) {
             Engine& e = *p->eng[w];
-            DevCkpt& c = *p->ck[w];
+            dqtg_pipe::Slot& sl = *p->ck[w];
+            DevCkpt& c = *sl.ck;
             try {
                 e.activate();
                 for (uint64_t k = (uint64_t)w; k < n; k += (uint64_t)W) {
@@ -178,7 +221,17 @@ dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* 
                         if (R.failed) return;
                     }
                     if (trace) t_0[k] = now_ms();
-                    upload(e, *c.L, c.w, weights + k * nt);
+                    c.w = stage(e, *c.L, weights + k * nt, sl.wbuf);
+                    if (ema) {  // snapshot k's own EMA (the scores of step k)
+                        const float* const* ek = ema + k * nt;
+                        if (const float* v = padded_view(*c.L, ek)) {
+                            c.ema = const_cast<float*>(v);
+                        } else {
+                            if (sl.ebuf_src != ek[0]) stage(e, *c.L, ek, sl.ebuf);
+                            sl.ebuf_src = ek[0];
+                            c.ema = sl.ebuf;
+                        }
+                    }
                     if (trace) t_u[k] = now_ms();
                     auto q = quantize(e, c, *cfg, seed, steps ? steps[k] : k);
                     if (trace) t_q[k] = now_ms();
@@ -219,6 +272,15 @@ dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* 
         for (int w = 0; w < W; ++w) th.emplace_back(worker, w);
         for (auto& t : th) t.join();
         for (auto ev : R.qev) cudaEventDestroy(ev);
+        if (p->join) {  // join: the caller stream waits for every worker's last work
+            for (auto& e : p->eng) {
+                cudaEvent_t ev;
+                DQTG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                DQTG_CUDA(cudaEventRecord(ev, e->stream));
+                DQTG_CUDA(cudaStreamWaitEvent(p->join, ev, 0));
+                cudaEventDestroy(ev);
+            }
+        }
         if (trace)
             for (uint64_t k = 0; k < n; ++k)
                 fprintf(stderr, "pipe k=%llu worker=%d start %.3f uploaded %.3f quantized %.3f waited %.3f encode-call %.3f encoded %.3f ms\n",

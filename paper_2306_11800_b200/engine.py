@@ -150,6 +150,7 @@ def _load():
         "dqtg_pipe_create": (C.c_int, [C.c_int, C.c_int, C.POINTER(_P)]),
         "dqtg_pipe_destroy": (None, [_P]),
         "dqtg_pipe_launches": (C.c_uint64, [_P]),
+        "dqtg_pipe_set_stream": (None, [_P, _P]),
         "dqtg_pipe_run": (C.c_int, [_P, C.POINTER(_Layout), _P, C.c_uint64, _P, _P,
                                     C.POINTER(Config), C.c_uint64, _P, C.c_double, RECORD_FN, _P,
                                     C.POINTER(_P)]),
@@ -332,7 +333,7 @@ def state_meta(h) -> "_Meta":
     for i in range(LIB.dqtg_qstate_tensor_count(h)):
         _check(LIB.dqtg_qstate_tensor_info(h, i, buf, len(buf), C.byref(t), C.byref(r),
                                            dims.ctypes.data))
-        names.append(buf.value.decode())
+        names.append(buf.value.decode("utf-8", "surrogateescape"))
         types.append(t.value)
         shapes.append(tuple(int(d) for d in dims[:r.value]))
     return _Meta(names, types, shapes)
@@ -655,11 +656,17 @@ class Pipe:
     def launches(self):
         return LIB.dqtg_pipe_launches(self.h)
 
+    def set_stream(self, stream_ptr):
+        """Runs fork from / join into this CUDA stream (events on it time a run)."""
+        LIB.dqtg_pipe_set_stream(self.h, stream_ptr or None)
+
     def run(self, names, types, shapes, snapshots, cfg, seed=1, steps=None, ema=None,
-            base=None, quality=0.0, on_record=None, engine=None):
+            base=None, quality=0.0, on_record=None, engine=None, emas=None):
         """snapshots[k] = per-tensor arrays or raw (host/device) pointers of snapshot
-        k; ema = per-tensor arrays/pointers or None.  on_record(k, record_handle) is
-        called on a worker thread.  Returns the last snapshot's DevState."""
+        k; ema = per-tensor arrays/pointers shared by every snapshot, or emas[k] =
+        snapshot k's own (None for both: magnitude scores only).  on_record(k,
+        record_handle) is called on a worker thread.  Returns the last snapshot's
+        DevState."""
         meta = _Meta(names, types, shapes)
         nt = len(meta.names)
         n = len(snapshots)
@@ -667,7 +674,13 @@ class Pipe:
         if len(bufs) != n * nt:
             raise ValueError("every snapshot needs one array per tensor")
         wptr = _ptr_array(bufs)
-        ebufs = None if ema is None else [_as_buf(a) for a in ema]
+        if ema is not None and emas is not None:
+            raise ValueError("pass either a shared ema or per-snapshot emas")
+        if ema is not None:
+            emas = [ema] * n
+        ebufs = None if emas is None else [_as_buf(a) for e in emas for a in e]
+        if ebufs is not None and len(ebufs) != n * nt:
+            raise ValueError("every snapshot's EMA needs one array per tensor")
         eptr = None if ebufs is None else _ptr_array(ebufs)
         st = None
         if steps is not None:

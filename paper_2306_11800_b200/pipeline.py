@@ -21,10 +21,14 @@ from . import engine as E
 
 
 class ChainCompressor:
-    def __init__(self, device=0, workers=2):
+    def __init__(self, device=0, workers=2, stream=None):
+        """``stream`` (a cudaStream_t as int, optional): every run forks from and joins
+        into it, so CUDA events recorded on it bracket the run's device work."""
         self.device = device
         self.nw = max(1, int(workers))
         self.pipe = E.Pipe(device, self.nw)
+        if stream:
+            self.pipe.set_stream(stream)
         self._eng = None
 
     @property
@@ -45,10 +49,11 @@ class ChainCompressor:
     def run(self, ckpts, cfg, seed, steps, base=None, quality=0.0, on_record=None,
             host=None):
         """Compress snapshot k at ``steps[k]`` as a delta chain from ``base`` (None:
-        the first record is FULL).  ``ckpts[k]`` is a DevCheckpoint (device resident;
-        the scores use the first checkpoint's EMA), or with ``host`` = (names, types,
-        shapes, ema) a list of per-tensor host arrays / pointers (copied into HBM by
-        the worker).  ``on_record(k, handle)`` runs on a worker thread with the record
+        the first record is FULL).  ``ckpts[k]`` is a DevCheckpoint (device resident,
+        read in place by the worker; its own EMA gives snapshot k's sensitivity
+        scores, and either every checkpoint carries an EMA or none does), or with
+        ``host`` = (names, types, shapes, ema) a list of per-tensor host arrays /
+        pointers (copied into HBM by the worker; ``ema`` is shared by the series).  ``on_record(k, handle)`` runs on a worker thread with the record
         handle (valid during the call; calls may arrive out of step order).  Returns
         the last quantized state."""
         if not ckpts:
@@ -61,11 +66,14 @@ class ChainCompressor:
             names, types, shapes = c0.meta.names, c0.meta.types, c0.meta.shapes
             nt = len(names)
             snaps = [[c.weights_dev + 4 * c.tensor_offset(i) for i in range(nt)] for c in ckpts]
-            ema = None
-            if c0.ema_dev:
-                ema = [c0.ema_dev + 4 * c0.tensor_offset(i) for i in range(nt)]
+            has = [bool(c.ema_dev) for c in ckpts]
+            if any(has) and not all(has):
+                raise ValueError("either every checkpoint of the series carries an EMA or none does")
+            emas = None
+            if all(has):
+                emas = [[c.ema_dev + 4 * c.tensor_offset(i) for i in range(nt)] for c in ckpts]
+            return self.pipe.run(names, types, shapes, snaps, cfg, seed, steps, None, base, quality,
+                                 on_record, engine=self.eq, emas=emas)
         return self.pipe.run(names, types, shapes, snaps, cfg, seed, steps, ema, base, quality,
                              on_record, engine=self.eq)
 
-    def sync(self):
-        pass  # dqtg_pipe_run returns after every worker stream has drained

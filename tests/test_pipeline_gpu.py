@@ -1,5 +1,7 @@
 """The pipelined chain (worker-pool streams, encode(k) waits on quantize(k-1))
-produces the same records as the oracle, for device-resident and host inputs."""
+produces the same records as the oracle, for device-resident and host inputs.
+Device-resident snapshots carry their own gradient EMA each (the sensitivity
+scores of step k come from snapshot k's EMA); host inputs share one."""
 import numpy as np
 import pytest
 
@@ -18,7 +20,9 @@ def test_pipelined_chain_matches_oracle(oracle, workers, host_inputs):
     for k in range(4):
         series.append(perturb(series[-1], seed=50 + k))
     rng = np.random.default_rng(1)
-    ema = rng.normal(0, 0.1, flat(series[0]).size).astype(np.float32)
+    n_el = flat(series[0]).size
+    emas = [rng.normal(0, 0.1 * (1 + k), n_el).astype(np.float32) for k in range(len(series))]
+    ema = emas[0]
     names = [t.name for t in series[0]]
     types = [t.type for t in series[0]]
     shapes = [t.shape for t in series[0]]
@@ -26,13 +30,13 @@ def test_pipelined_chain_matches_oracle(oracle, workers, host_inputs):
     cfg = E.Config()
     cc = ChainCompressor(0, workers=workers)
     cks = []
-    for ts in series:
+    for k, ts in enumerate(series):
         if host_inputs:
             cks.append([np.ascontiguousarray(t.data, np.float32) for t in ts])
             continue
         c = cc.checkpoint(names, types, shapes)
         c.set_weights([t.data for t in ts])
-        c.set_ema(np.split(ema, sizes))
+        c.set_ema(np.split(emas[k], sizes))
         cks.append(c)
     host = (names, types, shapes, np.split(ema, sizes)) if host_inputs else None
     recs = {}
@@ -44,10 +48,9 @@ def test_pipelined_chain_matches_oracle(oracle, workers, host_inputs):
         recs[k] = buf.tobytes()
 
     cc.run(cks, cfg, 3, list(range(len(cks))), on_record=grab, host=host)
-    cc.sync()
     prev = None
     for k, ts in enumerate(series):
-        m, s = oracle.scores(flat(ts), ema)
+        m, s = oracle.scores(flat(ts), ema if host_inputs else emas[k])
         q = oracle.quantize(ts, k, m, s, OC(), 3)
         assert recs[k] == oracle.encode_record(q, prev), k
         prev = q
