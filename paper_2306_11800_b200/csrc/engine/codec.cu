@@ -19,6 +19,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "crc.cuh"
@@ -67,6 +68,7 @@ struct EncArgs {
     uint32_t* crc_acc;
     uint32_t* tile_crc;  // per tile, zero register, ending at the tile's last byte
     uint32_t* err;
+    uint32_t* zs;        // enc_tile_delta_kernel: per-CTA kTile words for dense tiles
     // payload_bytes ablations (codec.cpp:601-646): 0 = record (rearranged groups),
     // 1 = one group per tensor (no rearrange), 2 = one group and no RLE (every
     // element its own run)
@@ -516,6 +518,481 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
             }
             A.segs[(size_t)ti * B + b] = G;
         }
+        __syncthreads();
+    }
+    if (cur_tensor != 0xffffffffu) {
+        uint32_t* gf = A.freq + (size_t)cur_tensor * B * NS;
+        for (uint32_t i = tid; i < B * NS; i += kCB) {
+            const uint32_t c = S.freq[i];
+            if (c) atomicAdd(gf + i, c);
+        }
+    }
+}
+
+// ---- E1 for DELTA records: sparse formulation -----------------------------------
+// Between consecutive checkpoints most levels do not move, so most cyclic deltas are
+// zero (96 % at C2).  A group's RLE stream (codec.cpp:79-90) is then zero runs
+// between a few non-zero deltas, and the only per-element work needed is
+//   * the key (previous level) histogram of the tile: group sizes, and
+//   * for the non-zero elements only, the rank inside their group (the number of
+//     same-key elements before them in the tile) and among the non-zero ones.
+// Per tile (4096 elements, thread t owns elements 16t..16t+15):
+//   L  levels -> key / delta bytes (SIMD), validation, CRC (as enc_tile_kernel);
+//      per 32-element block (a thread pair) and key: element and non-zero counts
+//      (shared atomics)
+//   H  one warp scan per key over the 128 blocks -> block prefixes; key offsets
+//      of the non-zero elements
+//   Z  every non-zero element (by its owning thread): rank r in its group = block
+//      prefix + same-key bytes before it in its block (SIMD compares), slot among
+//      the key's non-zero elements likewise -> Z[key-sorted slot] = (r, v, key)
+//   R  runs from Z: a zero run before an entry whose predecessor in the group is
+//      not adjacent, a value run at every head (new value or after a gap), a
+//      trailing zero run; run positions by one packed block scan; groups without
+//      non-zero elements are one zero run.  Output (runs, segments, interior-run
+//      symbol frequencies, tile CRC) is the format enc_tile_kernel writes.
+// Seven block barriers per tile (single-barrier scans); Z lives in shared memory
+// up to kZCap non-zero elements, in a per-CTA global slice for denser tiles.
+constexpr int kBlkEl = 32;                // elements per count block (a thread pair)
+constexpr int kNBlk = kTile / kBlkEl;     // 128
+constexpr int kZCap = 2048;               // non-zero elements held in shared memory
+
+// Exclusive block scan with one barrier: warp totals in slots[kCB / 32]; the slots
+// must not be reused before every thread has passed a later barrier.
+template <typename T>
+__device__ __forceinline__ T block_exscan1(T v, T* slots, T* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    T x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) slots[wid] = x;
+    __syncthreads();
+    T base = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kCB / 32; ++w) {
+        const T s = slots[w];
+        base += w < wid ? s : T(0);
+        tot += s;
+    }
+    *total = tot;
+    return base + x - v;
+}
+
+struct DSmem {
+    uint32_t* freq;   // B*NS per tensor
+    uint32_t* crc;    // kCrcTabs*256
+    uint32_t* nib;    // kNibConsts*8*16
+    uint32_t* key32;  // kTile key bytes (0xff: no element)
+    uint32_t* d32;    // kTile delta bytes
+    uint32_t* hc;     // [B][kNBlk]: counts (lo 16) | non-zero counts (hi 16) -> exclusive prefixes
+    uint16_t* hp;     // kTile + 1: slots of run heads (aliases hc after Z)
+    uint32_t* z;      // kZCap: r | v << 16 | key << 24, key-sorted
+};
+
+__host__ __device__ inline size_t dsm_hc_bytes(uint32_t B) {
+    const size_t a = ((size_t)kNBlk * B * 4 + 15) & ~(size_t)15, b = (size_t)(kTile + 8) * 2;
+    return a > b ? a : b;
+}
+
+__host__ __device__ inline size_t dsm_bytes(uint32_t B, uint32_t NS) {
+    return (((size_t)B * NS * 4 + 15) & ~(size_t)15) + (size_t)kCrcTabs * 256 * 4 +
+           (size_t)kNibConsts * 8 * 16 * 4 + 2 * (size_t)kTile + dsm_hc_bytes(B) + (size_t)kZCap * 4;
+}
+
+__device__ inline DSmem dsm_carve(uint8_t* base, uint32_t B, uint32_t NS) {
+    DSmem S;
+    size_t o = 0;
+    S.freq = (uint32_t*)(base + o); o += ((size_t)B * NS * 4 + 15) & ~(size_t)15;
+    S.crc = (uint32_t*)(base + o);  o += (size_t)kCrcTabs * 256 * 4;
+    S.nib = (uint32_t*)(base + o);  o += (size_t)kNibConsts * 8 * 16 * 4;
+    S.key32 = (uint32_t*)(base + o); o += kTile;
+    S.d32 = (uint32_t*)(base + o);   o += kTile;
+    S.hc = (uint32_t*)(base + o);
+    S.hp = (uint16_t*)(base + o);
+    o += dsm_hc_bytes(B);
+    S.z = (uint32_t*)(base + o);
+    return S;
+}
+
+// Per-tile run state shared by the R phase helpers.
+struct DRun {
+    uint32_t *n, *nz, *zoff, *gruns, *gbase, *fv, *lv, *lead, *trail, *aux;
+};
+
+// R1: up to PER key-sorted entries per thread (consecutive slots): run counts
+// (zero run before, value run at a head, trailing zero run) and flags.
+template <int PER>
+__device__ __forceinline__ void r_count(const uint32_t* Z, const DRun& D, uint32_t nzt, uint32_t j0,
+                                        uint32_t (&zc)[PER], uint32_t (&fl)[PER],
+                                        uint32_t& cnt_runs, uint32_t& cnt_heads) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        zc[u] = 0;
+        fl[u] = 0;
+        const uint32_t j = j0 + u;
+        if (j >= nzt) continue;
+        const uint32_t z = Z[j];
+        const uint32_t r = z & 0xffffu, v = (z >> 16) & 0xffu, k = z >> 24;
+        const bool first = j == D.zoff[k], last = j + 1 == D.zoff[k + 1];
+        uint32_t pr = 0, pv = 0;
+        if (!first) {
+            const uint32_t p = Z[j - 1];
+            pr = p & 0xffffu;
+            pv = (p >> 16) & 0xffu;
+        }
+        const bool zb = first ? r > 0 : pr + 1 < r;
+        const bool head = first || pr + 1 < r || pv != v;
+        const bool tail = last && r + 1 < D.n[k];
+        zc[u] = z;
+        fl[u] = (zb ? 1u : 0u) | (head ? 2u : 0u) | (tail ? 4u : 0u) | (first ? 8u : 0u) | 16u;
+        const uint32_t c = (zb ? 1u : 0u) + (head ? 1u : 0u) + (tail ? 1u : 0u);
+        cnt_runs += c;
+        cnt_heads += head ? 1u : 0u;
+        atomicAdd(&D.gruns[k], c);
+        if (tail) D.aux[k] = 1;
+    }
+}
+
+template <int PER>
+__device__ __forceinline__ void r_heads(const DSmem& S, uint32_t j0, const uint32_t (&fl)[PER],
+                                        uint32_t h) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u)
+        if (fl[u] & 2u) S.hp[h++] = (uint16_t)(j0 + u);
+}
+
+// R2: the runs of the thread's entries at their tile positions; first / last runs
+// of a group go to the segment, interior ones to the symbol frequencies.
+template <int PER>
+__device__ __forceinline__ void r_emit(const EncArgs& A, const DSmem& S, const uint32_t* Z, const DRun& D,
+                                       uint32_t tensor, uint32_t j0, const uint32_t (&zc)[PER],
+                                       const uint32_t (&fl)[PER], uint32_t xr, uint32_t h,
+                                       unsigned long long* runs) {
+    const uint32_t B = A.B, NS = A.NS;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        if (!fl[u]) continue;
+        const uint32_t z = zc[u], f = fl[u];
+        const uint32_t r = z & 0xffffu, v = (z >> 16) & 0xffu, k = z >> 24;
+        const uint32_t j = j0 + u;
+        const uint32_t p0 = xr + (D.aux[k] >> 1);  // + one run per empty group before k
+        uint32_t p = p0;
+        uint32_t* fk = S.freq + k * NS;
+        const uint32_t tb = tensor * B + k;
+        const bool gtail = D.aux[k] & 1u;
+        if (f & 1u) {  // zero run before the entry
+            const uint32_t pr = (f & 8u) ? 0u : (Z[j - 1] & 0xffffu) + 1u;
+            const uint32_t L = r - pr;
+            runs[p++] = ((unsigned long long)k << 16) | ((unsigned long long)L << 32);
+            if (f & 8u) {
+                D.fv[k] = 0;
+                D.lead[k] = L;
+            } else {
+                add_symbol(fk, NS, B, tb, 0u, L, A);
+            }
+        }
+        if (f & 2u) {  // value run: up to the next head of the group
+            const uint32_t nxt = min((uint32_t)S.hp[h + 1], D.zoff[k + 1]);
+            const uint32_t L = nxt - j;
+            runs[p++] = (unsigned long long)v | ((unsigned long long)k << 16) |
+                        ((unsigned long long)L << 32);
+            const bool is_first = (f & 8u) && !(f & 1u);
+            const bool is_last = !gtail && nxt == D.zoff[k + 1];
+            if (is_first) {
+                D.fv[k] = v;
+                D.lead[k] = L;
+            }
+            if (is_last) {
+                D.lv[k] = v;
+                D.trail[k] = L;
+            }
+            if (!is_first && !is_last) add_symbol(fk, NS, B, tb, v, L, A);
+            ++h;
+        }
+        if (f & 4u) {  // trailing zero run
+            const uint32_t L = D.n[k] - r - 1;
+            runs[p++] = ((unsigned long long)k << 16) | ((unsigned long long)L << 32);
+            D.lv[k] = 0;
+            D.trail[k] = L;
+        }
+        xr += p - p0;
+    }
+}
+
+template <int PER>
+__device__ __forceinline__ void r_phase(const EncArgs& A, const DSmem& S, const uint32_t* Z,
+                                        const DRun& D, uint32_t tensor, uint32_t nzt,
+                                        unsigned long long* slots, unsigned long long* runs) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t B = A.B;
+    const uint32_t j0 = tid * PER;
+    uint32_t zc[PER], fl[PER];
+    uint32_t cnt_runs = 0, cnt_heads = 0;
+    r_count<PER>(Z, D, nzt, j0, zc, fl, cnt_runs, cnt_heads);
+    unsigned long long tot;
+    const unsigned long long ex = block_exscan1<unsigned long long>(
+        (unsigned long long)cnt_runs | ((unsigned long long)cnt_heads << 32), slots, &tot);
+    const uint32_t xr = (uint32_t)ex, xh = (uint32_t)(ex >> 32);
+    r_heads<PER>(S, j0, fl, xh);
+    if (tid == 0) S.hp[tot >> 32] = (uint16_t)nzt;
+    if (wid == 0) {  // per key: run base (an empty group is one zero run)
+        uint32_t run = 0, erun = 0;
+        for (uint32_t b0 = 0; b0 < B; b0 += 32) {
+            const uint32_t b = b0 + lane;
+            const uint32_t empty = (b < B && D.n[b] && !D.nz[b]) ? 1u : 0u;
+            const uint32_t v = b < B ? D.gruns[b] + empty : 0u;
+            const uint32_t vx = v | (empty << 16);  // runs (lo 16) | empty groups (hi 16)
+            uint32_t x = vx;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (b < B) {
+                D.gbase[b] = run + ((x - vx) & 0xffffu);
+                D.gruns[b] = v;
+                D.aux[b] |= (erun + ((x - vx) >> 16)) << 1;
+            }
+            const uint32_t last = __shfl_sync(0xffffffffu, x, 31);
+            run += last & 0xffffu;
+            erun += last >> 16;
+        }
+        if (lane == 0) D.gbase[B] = run;
+    }
+    __syncthreads();
+    for (uint32_t b = tid; b < B; b += kCB)  // empty groups: one zero run covering the group
+        if (D.n[b] && !D.nz[b]) {
+            runs[D.gbase[b]] = ((unsigned long long)b << 16) | ((unsigned long long)D.n[b] << 32);
+            D.fv[b] = D.lv[b] = 0;
+            D.lead[b] = D.trail[b] = D.n[b];
+        }
+    r_emit<PER>(A, S, Z, D, tensor, j0, zc, fl, xr, xh, runs);
+}
+
+__global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A) {
+    extern __shared__ __align__(16) uint8_t e1_dyn[];
+    const uint32_t B = A.B, NS = A.NS;
+    const DSmem S = dsm_carve(e1_dyn, B, NS);
+    __shared__ uint32_t s_n[kMaxB], s_nz[kMaxB], s_zoff[kMaxB + 1], s_gruns[kMaxB], s_gbase[kMaxB + 1];
+    __shared__ uint32_t s_fv[kMaxB], s_lv[kMaxB], s_lead[kMaxB], s_trail[kMaxB], s_aux[kMaxB];
+    __shared__ uint32_t s_part[kCB / 32];
+    __shared__ unsigned long long s_slots[kCB / 32];
+    __shared__ int s_base;
+    const DRun D{s_n, s_nz, s_zoff, s_gruns, s_gbase, s_fv, s_lv, s_lead, s_trail, s_aux};
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t Brep = B * 0x01010101u;
+
+    for (uint32_t i = tid; i < kCrcTabs * 256; i += kCB) S.crc[i] = (&g_crc_slice[0][0])[i];
+    for (uint32_t i = tid; i < kNibConsts * 8 * 16; i += kCB) S.nib[i] = (&g_crc_nib[0][0][0])[i];
+    for (uint32_t i = tid; i < B * NS; i += kCB) S.freq[i] = 0;
+    for (uint32_t i = tid; i < kNBlk * B; i += kCB) S.hc[i] = 0;
+    for (uint32_t b = tid; b < B; b += kCB) s_nz[b] = s_gruns[b] = s_aux[b] = 0;
+    uint32_t* zg = A.zs + (size_t)blockIdx.x * kTile;  // Z of tiles denser than kZCap
+    uint32_t cur_tensor = 0xffffffffu;
+
+    for (int base; (base = grab_tiles(A.tile_ctr, 4, &s_base)) < A.ntiles;)
+    for (int ti = base; ti < min(base + 4, A.ntiles); ++ti) {
+        const Tile T = A.tiles[ti];
+        const uint32_t cnt = T.count;
+        if (tid == 0 && ti + 1 < min(base + 4, A.ntiles)) {  // next tile's levels into L2
+            const Tile N = A.tiles[ti + 1];
+            const uint32_t bytes = ((N.count + 7u) & ~7u) * 2u;
+            prefetch_l2(A.cur + N.start, bytes);
+            prefetch_l2(A.prev + N.start, bytes);
+        }
+        if (T.tensor != cur_tensor) {  // flush the previous tensor's symbol counts
+            __syncthreads();
+            if (cur_tensor != 0xffffffffu) {
+                uint32_t* gf = A.freq + (size_t)cur_tensor * B * NS;
+                for (uint32_t i = tid; i < B * NS; i += kCB) {
+                    const uint32_t c = S.freq[i];
+                    if (c) {
+                        atomicAdd(gf + i, c);
+                        S.freq[i] = 0;
+                    }
+                }
+            }
+            cur_tensor = T.tensor;
+        }
+        // ---- L: 16 levels per thread, deltas, validation, CRC; block key counts
+        const uint32_t e0 = tid * kIt;
+        const uint32_t nv = e0 < cnt ? min(cnt - e0, (uint32_t)kIt) : 0u;
+        uint32_t kw[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu}, dwv[4] = {0, 0, 0, 0};
+        uint32_t nzm = 0;  // non-zero delta bits of the 16 elements
+        {
+            uint32_t cw[4] = {0, 0, 0, 0}, pw[4] = {0, 0, 0, 0};
+            if (nv) {
+                const uint4* cp = (const uint4*)(A.cur + T.start + e0);
+                const uint4* pp = (const uint4*)(A.prev + T.start + e0);
+                const uint4 a0 = cp[0], a1 = cp[1], b0 = pp[0], b1 = pp[1];
+                const uint32_t hi[8] = {a0.x | b0.x, a0.y | b0.y, a0.z | b0.z, a0.w | b0.w,
+                                        a1.x | b1.x, a1.y | b1.y, a1.z | b1.z, a1.w | b1.w};
+                cw[0] = __byte_perm(a0.x, a0.y, 0x6420);
+                cw[1] = __byte_perm(a0.z, a0.w, 0x6420);
+                cw[2] = __byte_perm(a1.x, a1.y, 0x6420);
+                cw[3] = __byte_perm(a1.z, a1.w, 0x6420);
+                pw[0] = __byte_perm(b0.x, b0.y, 0x6420);
+                pw[1] = __byte_perm(b0.z, b0.w, 0x6420);
+                pw[2] = __byte_perm(b1.x, b1.y, 0x6420);
+                pw[3] = __byte_perm(b1.z, b1.w, 0x6420);
+                uint32_t bad = 0;
+                if (nv == (uint32_t)kIt) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) bad |= hi[j];
+                    bad &= 0xff00ff00u;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int keep = (int)nv - 2 * j;
+                        const uint32_t m = keep >= 2 ? 0xff00ff00u : (keep == 1 ? 0x0000ff00u : 0u);
+                        bad |= hi[j] & m;
+                    }
+                }
+                uint32_t big = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t m = keep_mask((int)nv - 4 * j);
+                    cw[j] &= m;
+                    pw[j] &= m;
+                    big |= __vcmpgeu4(cw[j], Brep) | __vcmpgeu4(pw[j], Brep);
+                    const uint32_t lt = __vcmpltu4(pw[j], cw[j]);
+                    dwv[j] = __vadd4(__vsub4(pw[j], cw[j]), lt & Brep) & m;
+                    kw[j] = pw[j] | ~m;  // no element: key 0xff
+                    nzm |= byte_msbs(__vcmpne4(dwv[j], 0u)) << (4 * j);
+                }
+                if (bad | big) atomicOr(A.err, kErrCorruptIndex);
+            }
+            *(uint4*)(S.key32 + tid * 4) = make_uint4(kw[0], kw[1], kw[2], kw[3]);
+            *(uint4*)(S.d32 + tid * 4) = make_uint4(dwv[0], dwv[1], dwv[2], dwv[3]);
+            // CRC of this thread's levels (zero register), right-aligned in its 32-byte chunk
+            uint32_t c0 = cw[0], c1 = cw[1], c2 = cw[2], c3 = cw[3];
+            if (nv && nv < (uint32_t)kIt) {
+                const int sh = kIt - (int)nv;
+                uint32_t w[8] = {0, 0, 0, 0, cw[0], cw[1], cw[2], cw[3]};
+                uint32_t o[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int src = 4 + j - (sh >> 2);
+                    const uint32_t lo_w = src - 1 >= 0 ? w[src - 1] : 0u;
+                    o[j] = (sh & 3) ? __funnelshift_l(lo_w, w[src], 8 * (sh & 3)) : w[src];
+                }
+                c0 = o[0], c1 = o[1], c2 = o[2], c3 = o[3];
+            }
+            uint32_t r = 0;
+            if (nv) r = crc_block8(S.crc, crc_block8(S.crc, 0u, c0, c1), c2, c3);
+            if (cnt == kTile) {
+                r = crc_warp(S.nib, r);
+                if (lane == 0) s_part[wid] = r;
+            } else {
+                if (r) r = crc_shift(c_crc_x2n, r, 2ull * (cnt - (e0 + nv)));
+                r = warp_xor(r);
+                if (lane == 0) s_part[wid] = r;
+            }
+            // block counts: elements (lo 16 bits) and non-zero elements (hi 16 bits);
+            // per key: non-zero elements
+            uint32_t* hb = S.hc + (tid >> 1);
+#pragma unroll
+            for (int j = 0; j < kIt; ++j) {
+                if ((uint32_t)j >= nv) break;
+                const uint32_t k = (kw[j >> 2] >> (8 * (j & 3))) & 0xffu;
+                atomicAdd(hb + k * kNBlk, (nzm >> j & 1u) ? 0x10001u : 1u);
+            }
+            for (uint32_t m = nzm; m; m &= m - 1) {
+                const uint32_t j = __ffs(m) - 1;
+                atomicAdd(&s_nz[(kw[j >> 2] >> (8 * (j & 3))) & 0xffu], 1u);
+            }
+        }
+        __syncthreads();
+        // ---- H: per key, exclusive prefix over the 128 blocks (one warp per key)
+        for (uint32_t k = wid; k < B; k += kCB / 32) {
+            uint4 v = *(const uint4*)(S.hc + k * kNBlk + 4 * lane);
+            const uint32_t s1 = v.x + v.y, s2 = s1 + v.z, s3 = s2 + v.w;
+            uint32_t x = s3;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            const uint32_t ex = x - s3;
+            *(uint4*)(S.hc + k * kNBlk + 4 * lane) = make_uint4(ex, ex + v.x, ex + s1, ex + s2);
+            if (lane == 31) s_n[k] = x & 0xffffu;
+        }
+        if (wid == 0) {  // slot offsets of the keys' non-zero elements in Z
+            uint32_t run = 0;
+            for (uint32_t b0 = 0; b0 < B; b0 += 32) {
+                const uint32_t b = b0 + lane;
+                const uint32_t v = b < B ? s_nz[b] : 0u;
+                uint32_t x = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (b < B) s_zoff[b] = run + x - v;
+                run += __shfl_sync(0xffffffffu, x, 31);
+            }
+            if (lane == 0) s_zoff[B] = run;
+        }
+        if (wid == kCB / 32 - 1) {  // tile CRC (moved to its stream position by crc_tiles_kernel)
+            uint32_t r = lane < kCB / 32 ? s_part[lane] : 0u;
+            if (cnt == kTile) r = crc_tree(S.nib, r, 10, 3);
+            else r = warp_xor(r);
+            if (lane == 0) A.tile_crc[ti] = r;
+        }
+        __syncthreads();
+        // ---- Z: every non-zero element, by its owning thread
+        const uint32_t nzt = s_zoff[B];
+        uint32_t* Z = nzt <= (uint32_t)kZCap ? S.z : zg;
+        for (uint32_t m = nzm; m; m &= m - 1) {
+            const uint32_t j = __ffs(m) - 1, e = e0 + j;
+            const uint32_t k = (S.key32[e >> 2] >> (8 * (e & 3))) & 0xffu;
+            const uint32_t v = (S.d32[e >> 2] >> (8 * (e & 3))) & 0xffu;
+            const uint32_t krep = k * 0x01010101u;
+            const uint4* kb = (const uint4*)(S.key32 + (e >> 5) * 8);
+            const uint4* db = (const uint4*)(S.d32 + (e >> 5) * 8);
+            const uint32_t lim = e & 31u;  // same-key bytes before the element in its block
+            uint32_t acc = 0, accnz = 0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint4 kk = kb[h], dd = db[h];
+                const uint32_t kx[4] = {kk.x, kk.y, kk.z, kk.w}, dx[4] = {dd.x, dd.y, dd.z, dd.w};
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    // bytes before the element: the low min(max(lim - 4 wi, 0), 4) bytes
+                    const int kb4 = min(max((int)lim - 16 * h - 4 * w, 0), 4);
+                    const uint32_t eq = __vcmpeq4(kx[w], krep) & (uint32_t)((1ull << (8 * kb4)) - 1ull);
+                    acc += __popc(eq);
+                    accnz += __popc(eq & __vcmpne4(dx[w], 0u));
+                }
+            }
+            const uint32_t pre = S.hc[k * kNBlk + (e >> 5)];
+            Z[s_zoff[k] + (pre >> 16) + (accnz >> 3)] = ((pre & 0xffffu) + (acc >> 3)) | (v << 16) | (k << 24);
+        }
+        __syncthreads();
+        // ---- R: runs (key-sorted entries, consecutive slots per thread)
+        unsigned long long* runs = A.runs + (size_t)ti * kTile;
+        if (nzt <= (uint32_t)kCB) r_phase<1>(A, S, Z, D, cur_tensor, nzt, s_slots, runs);
+        else if (nzt <= 4u * kCB) r_phase<4>(A, S, Z, D, cur_tensor, nzt, s_slots, runs);
+        else r_phase<kTile / kCB>(A, S, Z, D, cur_tensor, nzt, s_slots, runs);
+        if (tid == 0) A.tile_nruns[ti] = s_gbase[B];
+        __syncthreads();
+        for (uint32_t b = tid; b < B; b += kCB) {
+            Seg G{};
+            G.n = s_n[b];
+            if (G.n) {
+                G.run_begin = s_gbase[b];
+                G.run_end = s_gbase[b + 1];  // groups' runs are contiguous, in key order
+                G.fv = (uint16_t)s_fv[b];
+                G.lv = (uint16_t)s_lv[b];
+                G.lead = s_lead[b];
+                G.trail = s_trail[b];
+            }
+            A.segs[(size_t)ti * B + b] = G;
+            s_nz[b] = s_gruns[b] = s_aux[b] = 0;
+        }
+        for (uint32_t i = tid; i < kNBlk * B; i += kCB) S.hc[i] = 0;
         __syncthreads();
     }
     if (cur_tensor != 0xffffffffu) {
@@ -1803,14 +2280,20 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     A.ntiles = ntiles;
     {
         // ballot key width: keys < B, invalid elements 0xff -> 2^NB - 1 (> every key)
-        auto kfn = base ? (B <= 63 ? enc_tile_kernel<true, 6> : enc_tile_kernel<true, 7>)
+        // DELTA records: the sparse formulation (work on the non-zero deltas only);
+        // FULL records (every delta non-zero) and the ablation modes: dense ranks
+        const bool sparse = base && mode == 0 && !getenv("DQTG_DENSE_DELTA");
+        auto kfn = sparse ? enc_tile_delta_kernel
+                 : base ? (B <= 63 ? enc_tile_kernel<true, 6> : enc_tile_kernel<true, 7>)
                         : (B <= 63 ? enc_tile_kernel<false, 6> : enc_tile_kernel<false, 7>);
-        ensure_dyn_smem((const void*)kfn, e1_smem);
+        const size_t smem = sparse ? dsm_bytes(B, NS) : e1_smem;
+        ensure_dyn_smem((const void*)kfn, smem);
         DQTG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         int per_sm = 0;
-        DQTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kCB, e1_smem));
+        DQTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kCB, smem));
         const int grid = std::max(1, std::min(ntiles, e.num_sms * std::max(1, per_sm)));
-        { DQTG_SPAN(e, "enc_tile_kernel"); kfn<<<grid, kCB, e1_smem, st>>>(A); }
+        if (sparse) A.zs = (uint32_t*)e.buf("e.zs", (size_t)grid * kTile * 4);
+        { DQTG_SPAN(e, sparse ? "enc_tile_delta_kernel" : "enc_tile_kernel"); kfn<<<grid, kCB, smem, st>>>(A); }
         { DQTG_SPAN(e, "crc_tiles_kernel"); crc_tiles_kernel<<<std::max(1, std::min(e.num_sms * 2, (ntiles + 255) / 256)), 256, 0, st>>>(A.tile_crc, A.crc_shift, ntiles, A.crc_acc); }
         e.launched();
     }

@@ -10,7 +10,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-import bench  # noqa: E402
+from paper_2306_11800_b200 import workloads as W  # noqa: E402
 
 
 def main():
@@ -22,17 +22,17 @@ def main():
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream(dev)
     eng = E.Engine(0, stream.cuda_stream)
-    layout = bench.gpt2_small_layout()
+    layout = W.gpt2_small_layout()
     names = [n for n, _, _ in layout]
     types = [t for _, t, _ in layout]
     shapes = [s for _, _, s in layout]
-    snaps, ema = bench.gen_series(torch, layout, steps + 1, 1234, dev)
+    snaps, ema = W.series(torch, layout, steps + 1, 1234, dev)
     torch.cuda.synchronize()
     ck = []
     for s in snaps:
         c = E.DevCheckpoint(eng, names, types, shapes)
-        c.set_weights(bench.tensor_ptrs(s.data_ptr(), layout))
-        c.set_ema(bench.tensor_ptrs(ema.data_ptr(), layout))
+        c.set_weights(W.tensor_ptrs(s.data_ptr(), layout))
+        c.set_ema(W.tensor_ptrs(ema.data_ptr(), layout))
         ck.append(c)
     cfg = E.Config()
     st = eng.quantize(ck[0], cfg, 1, 0)

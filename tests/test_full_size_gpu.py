@@ -11,36 +11,33 @@ through size-independent properties, where the oracle would take minutes:
   one-symbol Huffman stream per tensor.
 """
 import os
-import sys
 
 import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.fixture(scope="module")
 def c2():
     import torch
 
-    sys.path.insert(0, ROOT)
-    import bench
     from paper_2306_11800_b200 import engine as E
+    from paper_2306_11800_b200 import workloads as W
 
     dev = torch.device("cuda", 0)
     eng = E.Engine(0, torch.cuda.current_stream(dev).cuda_stream)
-    layout = bench.gpt2_small_layout()
+    layout = W.gpt2_small_layout()
     names = [n for n, _, _ in layout]
     types = [t for _, t, _ in layout]
     shapes = [s for _, _, s in layout]
-    snaps, ema = bench.gen_series(torch, layout, 4, 99, dev)
+    snaps, ema = W.series(torch, layout, 4, 99, dev)
     torch.cuda.synchronize()
     cks = []
     for s in snaps:
         c = E.DevCheckpoint(eng, names, types, shapes)
-        c.set_weights(bench.tensor_ptrs(s.data_ptr(), layout))
-        c.set_ema(bench.tensor_ptrs(ema.data_ptr(), layout))
+        c.set_weights(W.tensor_ptrs(s.data_ptr(), layout))
+        c.set_ema(W.tensor_ptrs(ema.data_ptr(), layout))
         cks.append(c)
     del snaps
     return eng, cks, layout
