@@ -513,6 +513,7 @@ Layout::~Layout() {
     cudaFree(d_tile0);
     cudaFree(d_stream_off);
     cudaFree(d_crc_shift);
+    cudaFree(d_sample);
 }
 
 bool Layout::same_shape(const Layout& o) const {
@@ -566,8 +567,19 @@ std::shared_ptr<Layout> make_layout(Engine* e, const dqtg_layout* l) {
     }
     L->tile0.push_back((uint32_t)L->tiles.size());
     if (L->Np == 0) L->Np = kAlign;
+    {
+        constexpr size_t kSampleTiles = 512;
+        std::vector<size_t> per(kLayerTypes, 0), seen(kLayerTypes, 0);
+        for (const Tile& t : L->tiles) ++per[L->types[t.tensor]];
+        for (const Tile& t : L->tiles) {
+            const int lt = L->types[t.tensor];
+            const size_t stride = std::max<size_t>(1, per[lt] / kSampleTiles);
+            if (seen[lt]++ % stride == 0) L->sample_tiles.push_back(t);
+        }
+    }
     e->activate();
     L->d_tiles = upload_vec(L->tiles);
+    L->d_sample = upload_vec(L->sample_tiles);
     L->d_types = upload_vec(L->types);
     L->d_off = upload_vec(L->off);
     L->d_numel = upload_vec(L->numel);

@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 
@@ -168,7 +169,8 @@ __global__ void __launch_bounds__(kPB, 5) pass_a_kernel(PassIn a, unsigned long 
 
 // ---- quantile thresholds (sketch.cpp:59-77) --------------------------------
 __global__ void __launch_bounds__(1024) quantile_kernel(const QJob* jobs, int64_t HS,
-                                                        const float* keyf, LtParams* lp) {
+                                                        const float* keyf, LtParams* lp,
+                                                        int* slot_out) {
     __shared__ unsigned long long s_scan[33];
     __shared__ unsigned long long s_tot;
     __shared__ int64_t s_hit;
@@ -199,6 +201,7 @@ __global__ void __launch_bounds__(1024) quantile_kernel(const QJob* jobs, int64_
     __syncthreads();
     if (threadIdx.x == 0) {
         float t = keyf[s_hit];
+        if (slot_out) slot_out[J.lt * 3 + J.which] = (int)s_hit;
         if (J.which == 0) lp[J.lt].t_mag = t;
         else if (J.which == 1) lp[J.lt].t_sens = t;
         else lp[J.lt].t_prune = t;
@@ -278,6 +281,259 @@ __global__ void __launch_bounds__(kPB, 6) pass_b_kernel(PassIn a, const LtParams
     }
     __syncthreads();
     if (cur >= 0) hist_flush(sh, gh_val + cur * a.HS, a.tab);
+}
+
+// ---- fused pass A+B (derived scores, no pruning) ------------------------------------
+// Pass B only needs the thresholds pass A's histograms produce.  With a guess of the
+// thresholds (the same quantiles over a thinned tile sample, Layout::sample_tiles),
+// one streaming pass builds everything both passes produced: the score histograms
+// (magnitude as the signed histogram of w, folded afterwards; sensitivity), and for
+// the guessed partition the 2-bit codes, per-tile and per-tensor protected counts and
+// the histogram of the protected values.  Elements whose score lies in a band of
+// kBand buckets around a guessed threshold are listed; once the exact thresholds
+// are known, the listed elements whose class differs are corrected (fixup), and
+// the QUANTIZE-value histogram is w's histogram minus the protected values'.  When
+// an exact threshold falls outside its band (or the list overflows) the host runs
+// pass B as before, so the result is exact either way (quantize.cpp:34-92, 383-393).
+constexpr int kBand = 4;
+
+struct FuseArgs {
+    const LtParams* lpg;           // guessed thresholds [7]
+    const float4* band;            // [7]: magnitude (lo, hi], sensitivity (lo, hi]
+    unsigned long long* gh_w;      // [7][HS] signed histogram of w
+    unsigned long long* gh_sens;   // [7][HS]
+    unsigned long long* prot;      // [7][HS] protected (guessed) values by signed slot
+    uint16_t* parts;
+    uint32_t* tile_prot;
+    unsigned long long* tensor_prot;
+    unsigned long long* cand;      // (tile << 32) | element
+    unsigned long long* n_cand;
+    unsigned long long cap;
+    uint32_t* flag;                // non-zero: run pass B
+};
+
+// window slot of a signed value through the shared compact table; false: exact path
+__device__ __forceinline__ bool hist_fast_signed(uint32_t win_s, uint32_t b, const FastPos& f) {
+    const uint32_t a = b & 0x7fffffffu;
+    const uint32_t rel = min((a >> f.shift) - f.lo, f.n);
+    uint32_t c;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(c) : "r"(f.ctab_s + 4 * rel));
+    const uint32_t hi = (a & f.offmask) > ((c >> 13) & 0x1ffffu) ? 1u : 0u;
+    const uint32_t p = (c & 0x1fffu) + hi;
+    const bool ok = !((c >> (31 - hi)) & 1u) && p <= (uint32_t)kWin;
+    const uint32_t w = (b >> 31) ? (uint32_t)kWin - p : (uint32_t)kWin + p;
+    if (ok) asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(win_s + 4 * w) : "memory");
+    return ok;
+}
+
+__global__ void __launch_bounds__(kPB, 4) pass_ab_kernel(PassIn a, FuseArgs f) {
+    extern __shared__ uint32_t sh[];
+    uint32_t* shw = sh;                   // kWinSlots: signed w
+    uint32_t* shs = sh + kWinSlots;       // kPosSlots: sensitivity
+    uint32_t* s_ctab = shs + kPosSlots;
+    __shared__ uint32_t s_red[2][kPB / 32];
+    uint32_t par = 0;
+    const bool fastc = a.tab.ctab != nullptr;
+    for (int i = threadIdx.x; i < kWinSlots + kPosSlots; i += blockDim.x) sh[i] = 0;
+    if (fastc) {
+        for (uint32_t i = threadIdx.x; i < a.tab.ctab_n; i += blockDim.x) s_ctab[i] = __ldg(a.tab.ctab + i);
+        if (threadIdx.x == 0) s_ctab[a.tab.ctab_n] = 0xc0000000u;
+    }
+    __syncthreads();
+    const FastPos fp = fast_pos(a.tab, s_ctab);
+    const uint32_t shw_s = (uint32_t)__cvta_generic_to_shared(shw);
+    const uint32_t shs_s = (uint32_t)__cvta_generic_to_shared(shs);
+    const int lane = threadIdx.x & 31;
+    __shared__ int s_base;
+    int cur = -1;
+    LtParams P{};
+    float4 band{};
+    for (int base; (base = grab_tiles(a.tile_ctr, kGrab, &s_base)) < a.ntiles;)
+    for (int ti = base; ti < min(base + kGrab, a.ntiles); ++ti) {
+        const Tile T = a.tiles[ti];
+        const int lt = a.types[T.tensor];
+        if (threadIdx.x == 0 && ti + 1 < min(base + kGrab, a.ntiles)) prefetch_tile(a, ti + 1, false);
+        if (lt != cur) {
+            __syncthreads();
+            if (cur >= 0) {
+                hist_flush(shw, f.gh_w + cur * a.HS, a.tab);
+                hist_flush_pos(shs, f.gh_sens + cur * a.HS, a.tab);
+            }
+            __syncthreads();
+            cur = lt;
+            P = f.lpg[lt];
+            band = f.band[lt];
+        }
+        unsigned long long* gw = f.gh_w + lt * a.HS;
+        unsigned long long* gs = f.gh_sens + lt * a.HS;
+        uint32_t np = 0;
+        int itn = 0;
+        for (uint32_t i = threadIdx.x * 4; i < T.count; i += kPB * 8, ++itn) {
+            const uint32_t i2 = i + kPB * 4;
+            const bool two = i2 < T.count;
+            const float4 w0 = ld4(a.w + T.start + i);
+            const float4 w1 = two ? ld4(a.w + T.start + i2) : make_float4(0, 0, 0, 0);
+            float m[8], s[8];
+            {
+                float mm[4], ss[4];
+                load_scores<false>(a, T.start + i, w0, mm, ss);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) m[j] = mm[j], s[j] = ss[j];
+                if (two) {
+                    load_scores<false>(a, T.start + i2, w1, mm, ss);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) m[4 + j] = mm[j], s[4 + j] = ss[j];
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) m[4 + j] = s[4 + j] = 0.0f;
+                }
+            }
+            const float wa[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            uint32_t pw = 0;
+            const uint32_t act = __activemask();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t e = (j < 4 ? i : i2) + (j & 3);
+                const bool valid = e < T.count;
+                bool c = false;
+                if (valid) {
+                    if (!(fastc && hist_fast_signed(shw_s, __float_as_uint(wa[j]), fp)))
+                        hist_add(shw, gw, wa[j], a.tab, a.err);
+                    if (a.has_sens && !(fastc && hist_fast_pos(shs_s, __float_as_uint(s[j]), fp)))
+                        hist_add_pos(shs, gs, s[j], a.tab, a.err);
+                    const int part = classify(m[j], s[j], a.has_sens, a.metric, P);
+                    np += part == 2;
+                    pw |= (uint32_t)part << (2 * j);
+                    if (part == 2 && __float_as_uint(m[j]) < 0x7f800000u)
+                        atomicAdd(f.prot + lt * a.HS + slot_of(wa[j], a.tab), 1ull);
+                    c = (m[j] > band.x && m[j] <= band.y) || (a.has_sens && s[j] > band.z && s[j] <= band.w);
+                }
+                const uint32_t bal = __ballot_sync(act, c);
+                if (bal) {  // warp-aggregated append to the band list
+                    const int leader = __ffs(bal) - 1;
+                    unsigned long long b0 = 0;
+                    if (lane == leader) b0 = atomicAdd(f.n_cand, (unsigned long long)__popc(bal));
+                    b0 = __shfl_sync(act, b0, leader);
+                    if (c) {
+                        const unsigned long long at = b0 + __popc(bal & ((1u << lane) - 1u));
+                        if (at < f.cap) f.cand[at] = ((unsigned long long)ti << 32) | e;
+                        else atomicOr(f.flag, 1u);
+                    }
+                }
+            }
+            f.parts[((size_t)ti * kItTile + itn) * kPB + threadIdx.x] = (uint16_t)pw;
+        }
+        np = warp_sum(np);
+        if (lane == 0) s_red[par][threadIdx.x >> 5] = np;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t t = 0;
+            for (int wi = 0; wi < kPB / 32; ++wi) t += s_red[par][wi];
+            f.tile_prot[ti] = t;
+            if (t) atomicAdd(f.tensor_prot + T.tensor, (unsigned long long)t);
+        }
+        par ^= 1u;
+    }
+    __syncthreads();
+    if (cur >= 0) {
+        hist_flush(shw, f.gh_w + cur * a.HS, a.tab);
+        hist_flush_pos(shs, f.gh_sens + cur * a.HS, a.tab);
+    }
+}
+
+// magnitude histogram = |w| folded from the signed histogram of w
+__global__ void fold_abs_kernel(const unsigned long long* gw, unsigned long long* gm, int64_t HS,
+                                int64_t NB) {
+    const int lt = blockIdx.y;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < HS;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long v = 0;
+        if (i == NB) v = gw[lt * HS + i];
+        else if (i > NB) v = gw[lt * HS + i] + gw[lt * HS + (2 * NB - i)];  // neg slot of the same k
+        gm[lt * HS + i] = v;
+    }
+}
+
+// band (lo, hi] around each guessed threshold: kBand buckets either side
+__global__ void band_kernel(const int* slot_g, const float* keyf, int64_t NB, int64_t HS,
+                            float4* band, int2* band_slots, LtParams* lpg, int shift) {
+    const int lt = threadIdx.x;
+    if (lt >= kLayerTypes) return;
+    float4 b = make_float4(FLT_MAX, -FLT_MAX, FLT_MAX, -FLT_MAX);
+    int2 bs = make_int2(-1, -1);  // per kind: packed lo | hi << 16 relative to NB
+    for (int which = 0; which < 2; ++which) {
+        int g = slot_g[lt * 3 + which];
+        if (g < 0) continue;
+        if (shift) {  // test hook (DQTG_FUSED_GUESS_SHIFT): a deliberately wrong guess
+            g = (int)min(HS - 1, max((int64_t)NB, (int64_t)g + shift));
+            if (which == 0) lpg[lt].t_mag = keyf[g];
+            else lpg[lt].t_sens = keyf[g];
+        }
+        const int64_t lo = max((int64_t)NB, (int64_t)g - kBand), hi = min(HS - 1, (int64_t)g + kBand);
+        if (which == 0) b.x = keyf[lo], b.y = keyf[hi], bs.x = (int)((lo - NB) | ((hi - NB) << 16));
+        else b.z = keyf[lo], b.w = keyf[hi], bs.y = (int)((lo - NB) | ((hi - NB) << 16));
+    }
+    band[lt] = b;
+    band_slots[lt] = bs;
+}
+
+// exact thresholds inside their bands?
+__global__ void band_check_kernel(const int* slot_x, const int2* band_slots, int64_t NB,
+                                  const unsigned long long* n_cand, unsigned long long cap,
+                                  uint32_t* flag) {
+    const int lt = threadIdx.x;
+    if (lt >= kLayerTypes) return;
+    const int2 bs = band_slots[lt];
+    for (int which = 0; which < 2; ++which) {
+        const int x = slot_x[lt * 3 + which];
+        const int b = which ? bs.y : bs.x;
+        if (x < 0 && b < 0) continue;
+        if (x < 0 || b < 0) {
+            atomicOr(flag, 2u);
+            continue;
+        }
+        const int64_t lo = NB + (b & 0xffff), hi = NB + (b >> 16);
+        if (x < lo || x > hi) atomicOr(flag, 2u);
+    }
+    if (lt == 0 && *n_cand > cap) atomicOr(flag, 4u);
+}
+
+// correct the listed elements whose exact class differs from the guessed one
+__global__ void fixup_kernel(PassIn a, FuseArgs f, const LtParams* lp) {
+    const unsigned long long n = min(*f.n_cand, f.cap);
+    for (unsigned long long c = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; c < n;
+         c += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long q = f.cand[c];
+        const uint32_t ti = (uint32_t)(q >> 32), o = (uint32_t)q;
+        const Tile T = a.tiles[ti];
+        const int lt = a.types[T.tensor];
+        const float w = a.w[T.start + o];
+        const float m = fabsf(w);
+        const float s = a.has_sens ? fabsf(__fmul_rn(a.ema[T.start + o], w)) : 0.0f;
+        const int g = classify(m, s, a.has_sens, a.metric, f.lpg[lt]);
+        const int x = classify(m, s, a.has_sens, a.metric, lp[lt]);
+        if (g == x) continue;
+        const bool to_prot = x == 2;  // no pruning on this path: classes 0 <-> 2
+        atomicAdd(f.prot + lt * a.HS + slot_of(w, a.tab), to_prot ? 1ull : ~0ull);
+        atomicAdd(f.tile_prot + ti, to_prot ? 1u : ~0u);
+        atomicAdd(f.tensor_prot + T.tensor, to_prot ? 1ull : ~0ull);
+        // 2-bit code of element o: iteration itn, thread, position j (pass B layout)
+        const uint32_t itn = o / (kPB * 8), r = o % (kPB * 8);
+        const uint32_t th = (r % (kPB * 4)) / 4, j = (r / (kPB * 4)) * 4 + (r & 3);
+        const size_t idx = ((size_t)ti * kItTile + itn) * kPB + th;
+        uint32_t* word = (uint32_t*)f.parts + (idx >> 1);
+        const uint32_t sh = 16 * (uint32_t)(idx & 1) + 2 * j;
+        if (to_prot) atomicOr(word, 2u << sh);
+        else atomicAnd(word, ~(3u << sh));
+    }
+}
+
+// QUANTIZE-value histogram = w's histogram minus the protected values'
+__global__ void value_hist_kernel(const unsigned long long* gw, const unsigned long long* prot,
+                                  unsigned long long* gv, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        gv[i] = gw[i] - prot[i];
 }
 
 // ---- exclusive scan of per-tile counts (single CTA) --------------------------
@@ -806,9 +1062,11 @@ static void stage_pass_a(Engine& e, const DevCkpt& c, const PassIn& a, uint32_t 
 }
 
 static void stage_thresholds(Engine& e, Stage& s, int64_t HS, const AlphaTables& T,
-                             unsigned long long* gh_mag, unsigned long long* gh_sens) {
+                             unsigned long long* gh_mag, unsigned long long* gh_sens,
+                             LtParams* lp_out = nullptr, int* slot_out = nullptr) {
     cudaStream_t st = e.stream;
-    DQTG_CUDA(cudaMemcpyAsync(s.d_lp, s.plan.lp, sizeof(s.plan.lp), cudaMemcpyHostToDevice, st));
+    if (!lp_out) lp_out = s.d_lp;
+    DQTG_CUDA(cudaMemcpyAsync(lp_out, s.plan.lp, sizeof(s.plan.lp), cudaMemcpyHostToDevice, st));
     if (s.plan.jobs.empty()) return;
     for (auto& j : s.plan.jobs) {
         bool sens_hist = (j.which == 1) || (j.which == 2 && s.cfg.metric == 1);
@@ -817,7 +1075,7 @@ static void stage_thresholds(Engine& e, Stage& s, int64_t HS, const AlphaTables&
     QJob* d_jobs = (QJob*)e.buf(s.tag + "jobs", sizeof(QJob) * s.plan.jobs.size());
     DQTG_CUDA(cudaMemcpyAsync(d_jobs, s.plan.jobs.data(), sizeof(QJob) * s.plan.jobs.size(),
                               cudaMemcpyHostToDevice, st));
-    { DQTG_SPAN(e, "quantile_kernel"); quantile_kernel<<<(unsigned)s.plan.jobs.size(), 1024, 0, st>>>(d_jobs, HS, T.d_keyf, s.d_lp); }
+    { DQTG_SPAN(e, "quantile_kernel"); quantile_kernel<<<(unsigned)s.plan.jobs.size(), 1024, 0, st>>>(d_jobs, HS, T.d_keyf, lp_out, slot_out); }
     e.launched();
 }
 
@@ -854,6 +1112,80 @@ static void stage_pass_b(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s,
     { DQTG_SPAN(e, "scan_u32_kernel"); scan_u32_kernel<<<1, 1024, 0, st>>>(s.tile_prot, ntiles, s.tile_off); }
     e.launched();
     if (keys) stage_keys(e, L, s, T);
+}
+
+// Fused pass A+B (pass_ab_kernel) for derived scores without pruning.
+// Opt-in (DQTG_FUSED_AB=1): it reads w + EMA once instead of twice, but at C2 the
+// fused kernel runs at 0.97 ms against 0.39 + 0.36 ms for passes A and B (issue-
+// and latency-bound at 3 resident CTAs per SM; pipelined chain 164 vs 188 GB/s).
+static bool fusable(const DevCkpt& c, const Stage& s) {
+    if (c.explicit_scores || c.L->sample_tiles.empty() || !getenv("DQTG_FUSED_AB")) return false;
+    for (int lt = 0; lt < kLayerTypes; ++lt)
+        if (s.plan.lp[lt].flags & (kDoPrune | kProtectAll)) return false;
+    for (const QJob& j : s.plan.jobs)
+        if (j.which == 2) return false;
+    return true;
+}
+
+// Everything pass A, the thresholds and pass B produce, from one streaming pass over
+// w + EMA; *flag_host (valid after the next sync) non-zero: a guessed threshold was
+// too far off and pass B must run.
+static void stage_fused_ab(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s,
+                           const AlphaTables& T, uint32_t* flag_host) {
+    const Layout& L = *c.L;
+    const int64_t HS = T.HS;
+    cudaStream_t st = e.stream;
+    const size_t hb = (size_t)kLayerTypes * HS * 8;
+    // 1. threshold guess: the quantiles of a thinned tile sample
+    auto* samp = (unsigned long long*)e.buf("q.samp", 2 * hb);
+    DQTG_CUDA(cudaMemsetAsync(samp, 0, 2 * hb, st));
+    PassIn as = a;
+    as.tiles = L.d_sample;
+    as.ntiles = (int)L.sample_tiles.size();
+    stage_pass_a(e, c, as, s.plan.mask_mag, s.plan.mask_sens, samp, samp + (size_t)kLayerTypes * HS);
+    auto* d_lpg = (LtParams*)e.buf("q.lpg", sizeof(LtParams) * kLayerTypes);
+    auto* slots = (int*)e.buf("q.slots", 2 * kLayerTypes * 3 * sizeof(int));
+    DQTG_CUDA(cudaMemsetAsync(slots, 0xff, 2 * kLayerTypes * 3 * sizeof(int), st));
+    stage_thresholds(e, s, HS, T, samp, samp + (size_t)kLayerTypes * HS, d_lpg, slots);
+    auto* band = (float4*)e.buf("q.band", sizeof(float4) * kLayerTypes);
+    auto* bslots = (int2*)e.buf("q.bslots", sizeof(int2) * kLayerTypes);
+    const char* shift_env = getenv("DQTG_FUSED_GUESS_SHIFT");
+    const int shift = shift_env ? atoi(shift_env) : 0;
+    { DQTG_SPAN(e, "band_kernel"); band_kernel<<<1, 32, 0, st>>>(slots, T.d_keyf, T.NB, HS, band, bslots, d_lpg, shift); }
+    // 2. the fused streaming pass
+    auto* gh_w = (unsigned long long*)e.buf("q.gh_w", hb);
+    auto* gh = (unsigned long long*)e.buf("q.gh_scores", 2 * hb);  // [magnitude][sensitivity]
+    auto* prot = (unsigned long long*)e.buf("q.prot", hb);
+    auto* small = (unsigned long long*)e.buf("q.fsmall", 32);
+    const unsigned long long cap = L.N / 25 + 1024;  // 4 % of the elements
+    auto* cand = (unsigned long long*)e.buf("q.cand", cap * 8);
+    DQTG_CUDA(cudaMemsetAsync(gh_w, 0, hb, st));
+    DQTG_CUDA(cudaMemsetAsync(gh, 0, 2 * hb, st));
+    DQTG_CUDA(cudaMemsetAsync(prot, 0, hb, st));
+    DQTG_CUDA(cudaMemsetAsync(s.tensor_prot, 0, (size_t)(L.nt + 1) * 8, st));
+    DQTG_CUDA(cudaMemsetAsync(small, 0, 32, st));
+    DQTG_CUDA(cudaMemsetAsync(a.tile_ctr, 0, 4, st));
+    FuseArgs f{d_lpg, band, gh_w, gh + (size_t)kLayerTypes * HS, prot, s.parts, s.tile_prot,
+               s.tensor_prot, cand, small, cap, (uint32_t*)(small + 1)};
+    const size_t ct = a.tab.ctab ? ((size_t)a.tab.ctab_n + 1) * 4 : 0;
+    const size_t smem = (size_t)(kWinSlots + kPosSlots) * 4 + ct;
+    ensure_dyn_smem((const void*)pass_ab_kernel, smem);
+    DQTG_CUDA(cudaFuncSetAttribute(pass_ab_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    int per_sm = 0;
+    DQTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass_ab_kernel, kPB, smem));
+    const int grid = stream_grid(e, a.ntiles, std::max(1, per_sm));
+    { DQTG_SPAN(e, "pass_ab_kernel"); pass_ab_kernel<<<grid, kPB, smem, st>>>(a, f); }
+    { DQTG_SPAN(e, "fold_abs_kernel"); fold_abs_kernel<<<dim3((unsigned)((HS + 255) / 256), kLayerTypes), 256, 0, st>>>(gh_w, gh, HS, T.NB); }
+    // 3. exact thresholds, band check, corrections, value histogram
+    stage_thresholds(e, s, HS, T, gh, gh + (size_t)kLayerTypes * HS, s.d_lp, slots + kLayerTypes * 3);
+    { DQTG_SPAN(e, "band_check_kernel"); band_check_kernel<<<1, 32, 0, st>>>(slots + kLayerTypes * 3, bslots, T.NB, small, cap, f.flag); }
+    { DQTG_SPAN(e, "fixup_kernel"); fixup_kernel<<<e.num_sms * 4, 256, 0, st>>>(a, f, s.d_lp); }
+    { DQTG_SPAN(e, "value_hist_kernel"); value_hist_kernel<<<e.num_sms, 256, 0, st>>>(gh_w, prot, s.gh_val, (int64_t)kLayerTypes * HS); }
+    e.launched(6);
+    { DQTG_SPAN(e, "scan_u32_kernel"); scan_u32_kernel<<<1, 1024, 0, st>>>(s.tile_prot, a.ntiles, s.tile_off); }
+    e.launched();
+    stage_keys(e, L, s, T);
+    e.d2h(flag_host, f.flag, 4);
 }
 
 // After a sync: codebooks of every stage (all k-means problems in one launch).
@@ -945,17 +1277,27 @@ std::unique_ptr<QState> quantize(Engine& e, const DevCkpt& c, const dqtg_config&
     const int64_t HS = T.HS;
     PassIn a = pass_in(e, c, T, (int)cfg.metric);
     stage_alloc(e, L, HS, s, q->d_cb);
-    unsigned long long *gh_mag = nullptr, *gh_sens = nullptr;
-    if (!s.plan.jobs.empty()) {
-        auto* gh = (unsigned long long*)e.buf("q.gh_scores", (size_t)2 * kLayerTypes * HS * 8);
-        DQTG_CUDA(cudaMemsetAsync(gh, 0, (size_t)2 * kLayerTypes * HS * 8, e.stream));
-        gh_mag = gh;
-        gh_sens = gh + (size_t)kLayerTypes * HS;
-        stage_pass_a(e, c, a, s.plan.mask_mag, s.plan.mask_sens, gh_mag, gh_sens);
+    if (fusable(c, s) && !s.plan.jobs.empty()) {
+        uint32_t redo = 0;
+        stage_fused_ab(e, c, a, s, T, &redo);
+        e.check_err();  // syncs: n_keys + protected counts + the band flag on the host
+        if (redo) {     // a guessed threshold outside its band: pass B with the exact ones
+            stage_pass_b(e, c, a, s, T);
+            e.check_err();
+        }
+    } else {
+        unsigned long long *gh_mag = nullptr, *gh_sens = nullptr;
+        if (!s.plan.jobs.empty()) {
+            auto* gh = (unsigned long long*)e.buf("q.gh_scores", (size_t)2 * kLayerTypes * HS * 8);
+            DQTG_CUDA(cudaMemsetAsync(gh, 0, (size_t)2 * kLayerTypes * HS * 8, e.stream));
+            gh_mag = gh;
+            gh_sens = gh + (size_t)kLayerTypes * HS;
+            stage_pass_a(e, c, a, s.plan.mask_mag, s.plan.mask_sens, gh_mag, gh_sens);
+        }
+        stage_thresholds(e, s, HS, T, gh_mag, gh_sens);
+        stage_pass_b(e, c, a, s, T);
+        e.check_err();  // syncs: n_keys + protected counts on the host
     }
-    stage_thresholds(e, s, HS, T, gh_mag, gh_sens);
-    stage_pass_b(e, c, a, s, T);
-    e.check_err();  // syncs: n_keys + protected counts on the host
     std::vector<Stage*> v{&s};
     stage_codebooks(e, v, a, HS);
     uint64_t acc = 0;
