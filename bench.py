@@ -360,16 +360,24 @@ def run_ours(args):
     # C-ABI step; N>1: the tensor-sharded path (score/value histograms all-reduced
     # over NCCL, each rank encodes its own tensor blocks).
     rec_bytes = []
+    comm = None
     if world > 1:
         from paper_2306_11800_b200 import distributed as DIST
 
+        # the engine library's own NCCL communicator (dqtg_comm_*): histogram
+        # all-reduces and the record gather on the engine stream; --share-gpu (all
+        # ranks on one GPU, where NCCL refuses duplicate devices) uses torch/gloo
+        if not args.share_gpu:
+            comm = DIST.make_comm(eng)
         state, _, _ = DIST.compress_sharded(eng, ckpts[0], cfg, 1, 0, None, device=dev,
-                                            n_tensors_total=len(names) * world)
+                                            n_tensors_total=len(names) * world, comm=comm)
 
         def step(i, prev):
             st, _, stats = DIST.compress_sharded(eng, ckpts[i], cfg, 1, i, prev, device=dev,
-                                                 n_tensors_total=len(names) * world)
-            rec_bytes.append(stats["record_bytes_local"])
+                                                 n_tensors_total=len(names) * world, comm=comm)
+            # record bytes per rank's share: the whole record (rank 0) / world
+            n = stats.get("record_bytes") or stats.get("record_bytes_local") or 0
+            rec_bytes.append(n / world if comm is not None else n)
             return st
     else:
         state = eng.quantize(ckpts[0], cfg, 1, 0)
@@ -410,11 +418,15 @@ def run_ours(args):
     # pipelined chain (N=1): a pool of worker streams, step k on worker k mod W;
     # encode(k) waits on quantize(k-1) (paper_2306_11800_b200/pipeline.py)
     pipelined = None
-    if world == 1 and not args.no_pipeline:
+    pipe_comms = None
+    if (world == 1 or comm is not None) and not args.no_pipeline:
         from paper_2306_11800_b200.pipeline import ChainCompressor
 
+        if comm is not None:  # one communicator per worker (dqtg_pipe_set_comms)
+            pipe_comms = [DIST.make_comm(eng) for _ in range(args.workers)]
         # every run forks from / joins into `stream`: CUDA events on it time the chain
-        cc = ChainCompressor(local, workers=args.workers, stream=stream.cuda_stream)
+        cc = ChainCompressor(local, workers=args.workers, stream=stream.cuda_stream,
+                             comms=pipe_comms, n_tensors_total=len(names) * world)
         torch.cuda.synchronize()
         # warm-up: at least two steps per worker (scratch and pool sizes settle)
         n_warm = max(args.warmup + 1, 2 * args.workers + 2)
@@ -456,7 +468,7 @@ def run_ours(args):
     ms_step = ms / args.steps
     value = 4.0 * N * world * args.steps / (ms / 1e3) / 1e9
     rec_mean = float(np.mean(rec_bytes[-args.steps:]))
-    cr = 4.0 * N / rec_mean  # per-rank record bytes (shard blocks) vs per-rank fp32 bytes
+    cr = 4.0 * N / rec_mean if rec_mean else None  # per-rank share of the record vs per-rank fp32 bytes
 
     # live per-kernel timing (CUDA events on the engine stream) for the roofline
     eng.profile(True)
@@ -542,7 +554,7 @@ def run_ours(args):
         e2e_ck.set_ema(tensor_ptrs(ema.data_ptr(), layout))
         e2e_ck.set_weights(tensor_ptrs(pinned[0].data_ptr(), layout))
         e2e_state, _, _ = DIST.compress_sharded(eng, e2e_ck, cfg, 1, 0, None, device=dev,
-                                                n_tensors_total=len(names) * world)
+                                                n_tensors_total=len(names) * world, comm=comm)
 
         def e2e_step(i, prev):
             nonlocal h2d, d2h
@@ -550,8 +562,10 @@ def run_ours(args):
             h2d += 4 * N
             st, rec, stats = DIST.compress_sharded(eng, e2e_ck, cfg, 1, i, prev, device=dev,
                                                    n_tensors_total=len(names) * world,
-                                                   gather_record=True)
-            d2h += stats["record_bytes_local"]
+                                                   gather_record=True, comm=comm)
+            # D2H: the whole record on rank 0 (comm), each rank's blocks otherwise
+            d2h += (len(rec) // world if rec is not None else 0) if comm is not None \
+                else stats["record_bytes_local"]
             return st
 
         e2e_state = e2e_step(1, e2e_state)
@@ -650,6 +664,10 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (GPU trajectory with the reference generator dynamics)",
+            "nccl": None if world == 1 else {
+                "nranks": world, "comm": "dqtg_comm (engine-owned NCCL communicator)"
+                if comm is not None else "torch.distributed gloo (--share-gpu)",
+                "pipeline_comms": len(pipe_comms) if pipe_comms else 0},
             "config": {"workload": "C2: GPT-2-small layout 124.4M fp32 params, delta chain",
                        "params_per_gpu": N, "quant_config": "default (bins16/embed32/"
                        "protect0.005/MAGNITUDE/sigma0.2/alpha0.01), EMA sensitivity",

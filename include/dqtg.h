@@ -231,6 +231,36 @@ dqtg_status dqtg_compress_step(dqtg_engine *e, const dqtg_ckpt *c, const dqtg_co
                                double quality_delta, dqtg_qstate **state_out,
                                dqtg_record **record_out);
 
+/* ---- NCCL communicator and the sharded step (multi-GPU) ------------
+ * One process per GPU.  Rank 0 makes an id (dqtg_comm_unique_id), the caller passes
+ * it to every rank out of band (e.g. torch.distributed.broadcast_object_list, MPI,
+ * a file), and each rank calls dqtg_comm_init with its engine.  NCCL is loaded at
+ * run time (libnccl.so.2).
+ * dqtg_compress_sharded runs one Chain::append step (chain.cpp:86-129) of a
+ * tensor-sharded checkpoint: `c` holds this rank's tensors (contiguous in the global
+ * tensor order, rank order = tensor order), `base` this rank's previous state (null:
+ * FULL record).  The score and value histograms are all-reduced on the engine
+ * stream, every rank quantizes and encodes its own tensors, and rank 0 receives the
+ * record of the whole checkpoint in *record_out (byte-identical to the single-GPU
+ * dqtg_compress_step record; other ranks get null).  n_tensors_total = 0: the sum of
+ * the ranks' tensor counts.  Replaces the reference's single-process
+ * quantize_checkpoint + encode_delta_record (quantize.cpp:373-425, codec.cpp:398-460). */
+#define DQTG_COMM_ID_BYTES 128
+typedef struct dqtg_comm dqtg_comm;
+dqtg_status dqtg_comm_unique_id(uint8_t *id_out /* DQTG_COMM_ID_BYTES */);
+dqtg_status dqtg_comm_init(dqtg_engine *e, const uint8_t *id, int nranks, int rank,
+                           dqtg_comm **out);
+void dqtg_comm_destroy(dqtg_comm *c);
+int dqtg_comm_rank(const dqtg_comm *c);
+int dqtg_comm_size(const dqtg_comm *c);
+/* in-place sum of a device u64 buffer over the ranks, on the engine stream */
+dqtg_status dqtg_comm_allreduce_u64(dqtg_engine *e, dqtg_comm *c, uint64_t *buf_dev, uint64_t n);
+dqtg_status dqtg_compress_sharded(dqtg_engine *e, dqtg_comm *c, const dqtg_ckpt *ckpt,
+                                  const dqtg_config *cfg, uint64_t seed, uint64_t step,
+                                  const dqtg_qstate *base, double quality_delta,
+                                  uint32_t n_tensors_total, dqtg_qstate **state_out,
+                                  dqtg_record **record_out);
+
 /* ---- pipelined delta chain (Chain::append over a series, chain.cpp:86-129) ----
  * A pool of `workers` engines, each on its own CUDA stream and host thread.
  * Snapshot k runs on worker k mod W: quantized, then encoded as a delta against
@@ -253,6 +283,12 @@ uint64_t dqtg_pipe_launches(const dqtg_pipe *p);
  * `stream` (a cudaStream_t; null: none) before the run, and makes `stream` wait
  * for all workers at the end, so events recorded on it bracket the whole chain. */
 void dqtg_pipe_set_stream(dqtg_pipe *p, void *stream);
+/* Multi-GPU worker pool: one communicator per worker (n == workers; 0 clears).  Every
+ * rank runs dqtg_pipe_run over its shard of each snapshot; snapshot k's sharded step
+ * (dqtg_compress_sharded) runs on worker k mod W with comms[k mod W]; on_record is
+ * called on rank 0 only, with the whole record. */
+dqtg_status dqtg_pipe_set_comms(dqtg_pipe *p, dqtg_comm *const *comms, int n,
+                                uint32_t n_tensors_total);
 dqtg_status dqtg_pipe_run(dqtg_pipe *p, const dqtg_layout *layout,
                           const float *const *weights_any, uint64_t n_snapshots,
                           const uint64_t *steps, const float *const *ema_any,

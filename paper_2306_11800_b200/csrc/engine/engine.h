@@ -12,6 +12,8 @@
 
 #include "common.cuh"
 
+struct dqtg_comm;
+
 namespace dqtg {
 
 // Shared-memory histogram window: kWin buckets per sign plus the zero bucket.
@@ -327,5 +329,10 @@ void compute_scores(Engine& e, const float* w_dev, const float* ema_dev, uint64_
 uint32_t crc32_device(Engine& e, const uint8_t* data_dev, uint64_t n);
 void delta_kernel_api(Engine& e, const uint16_t* prev, const uint16_t* x, uint64_t n, uint32_t B,
                       uint16_t* out, bool apply);
+// tensor-sharded step over an NCCL communicator (comm.cu)
+std::unique_ptr<QState> sharded_quantize(Engine& e, dqtg_comm* comm, const DevCkpt& ck,
+                                         const dqtg_config& cfg, uint64_t seed, uint64_t step);
+std::unique_ptr<Record> sharded_encode(Engine& e, dqtg_comm* comm, const QState* base,
+                                       const QState& target, double quality, uint32_t n_tensors_total);
 
 }  // namespace dqtg

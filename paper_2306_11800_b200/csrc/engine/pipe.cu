@@ -35,6 +35,11 @@ struct dqtg_pipe {
     // ordered after the work queued on it before the run, and work queued on it
     // after the run waits for every worker, so events on it time the whole chain
     cudaStream_t join = nullptr;
+    // optional (dqtg_pipe_set_comms): one NCCL communicator per worker -- worker w runs
+    // the tensor-sharded step of snapshots k = w mod W on its own communicator, so every
+    // communicator sees the same sequence of collectives on every rank
+    std::vector<dqtg_comm*> comms;
+    uint32_t nt_total = 0;
     // worker engines: released (not deleted) so states handed out stay valid
     struct Release {
         void operator()(Engine* e) const { engine_release(e); }
@@ -149,6 +154,17 @@ void dqtg_pipe_destroy(dqtg_pipe* p) {
 
 void dqtg_pipe_set_stream(dqtg_pipe* p, void* stream) { p->join = (cudaStream_t)stream; }
 
+dqtg_status dqtg_pipe_set_comms(dqtg_pipe* p, dqtg_comm* const* comms, int n,
+                                uint32_t n_tensors_total) {
+    if (n != 0 && n != (int)p->eng.size()) {
+        set_last_error("one communicator per worker");
+        return DQTG_ERROR;
+    }
+    p->comms.assign(comms, comms + n);
+    p->nt_total = n_tensors_total;
+    return DQTG_OK;
+}
+
 uint64_t dqtg_pipe_launches(const dqtg_pipe* p) {
     uint64_t n = 0;
     for (auto& e : p->eng) n += e->launches;
@@ -233,7 +249,9 @@ dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* 
                         }
                     }
                     if (trace) t_u[k] = now_ms();
-                    auto q = quantize(e, c, *cfg, seed, steps ? steps[k] : k);
+                    dqtg_comm* cm = p->comms.empty() ? nullptr : p->comms[w];
+                    auto q = cm ? sharded_quantize(e, cm, c, *cfg, seed, steps ? steps[k] : k)
+                                : quantize(e, c, *cfg, seed, steps ? steps[k] : k);
                     if (trace) t_q[k] = now_ms();
                     DQTG_CUDA(cudaEventRecord(R.qev[k], e.stream));
                     const QState* target = q.get();
@@ -252,9 +270,10 @@ dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* 
                     if (k > 0) DQTG_CUDA(cudaStreamWaitEvent(e.stream, R.qev[k - 1], 0));
                     if (trace) t_w[k] = now_ms();
                     dqtg_record rec;
-                    rec.r = encode_record(e, prev, *target, quality);
+                    rec.r = cm ? sharded_encode(e, cm, prev, *target, quality, p->nt_total)
+                               : encode_record(e, prev, *target, quality);
                     if (trace) t_c[k] = now_ms();
-                    if (on_record) on_record(user, k, &rec);
+                    if (on_record && rec.r) on_record(user, k, &rec);
                     rec.r.reset();
                     e.sync();  // encode(k) complete: its inputs may be released
                     if (trace) t_e[k] = now_ms();

@@ -83,17 +83,52 @@ def assemble_record(prefix: bytes, bodies, crcs, stream_lens) -> bytes:
     return bytes(prefix) + b"".join(bytes(b) for b in bodies) + struct.pack("<I", crc or 0)
 
 
+def make_comm(engine, group=None):
+    """The engine library's own NCCL communicator over the ranks of ``group``: rank 0
+    makes the id, torch.distributed broadcasts it (any backend)."""
+    import torch.distributed as dist
+
+    from . import engine as E
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    box = [E.Comm.unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(box, src=0, group=group)
+    return E.Comm(engine, box[0], world, rank)
+
+
 def compress_sharded(engine, ckpt, cfg, seed, step, base_state, *, group=None, device=None,
-                     quality=0.0, n_tensors_total=None, gather_record=False):
+                     quality=0.0, n_tensors_total=None, gather_record=False, comm=None):
     """One compress+delta step of a tensor-sharded checkpoint.
 
     ``ckpt`` holds this rank's tensors.  Returns (state, record_bytes_or_None,
     stats): the state stays on this GPU for the next step; with
-    ``gather_record`` rank 0 receives the assembled record."""
+    ``gather_record`` rank 0 receives the assembled record.
+
+    With ``comm`` (an engine Comm, see make_comm) the whole step runs in the engine
+    library (dqtg_compress_sharded): NCCL all-reduces on the engine stream and the
+    record gathered into rank 0's device memory.  Without it the exchanges go through
+    torch.distributed (any backend; the CPU tests use gloo)."""
     import torch
     import torch.distributed as dist
 
     from . import engine as E
+
+    if comm is not None:
+        state, rec = engine.compress_sharded(comm, ckpt, cfg, seed, step, base_state, quality,
+                                             n_tensors_total or 0)
+        stats = {"record_bytes_local": None, "comm": "dqtg_comm (NCCL)"}
+        out = None
+        if rec is not None:
+            size = E.LIB.dqtg_record_size(rec)
+            stats["record_bytes"] = size
+            if gather_record:
+                buf = np.empty(size, np.uint8)
+                E._check(E.LIB.dqtg_record_copy(rec, buf.ctypes.data))
+                out = buf.tobytes()
+            E.LIB.dqtg_record_destroy(rec)
+        return state, out, stats
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     dev = device or torch.device("cuda", torch.cuda.current_device())

@@ -151,6 +151,16 @@ def _load():
         "dqtg_pipe_destroy": (None, [_P]),
         "dqtg_pipe_launches": (C.c_uint64, [_P]),
         "dqtg_pipe_set_stream": (None, [_P, _P]),
+        "dqtg_pipe_set_comms": (C.c_int, [_P, _P, C.c_int, C.c_uint32]),
+        "dqtg_comm_unique_id": (C.c_int, [_P]),
+        "dqtg_comm_init": (C.c_int, [_P, _P, C.c_int, C.c_int, C.POINTER(_P)]),
+        "dqtg_comm_destroy": (None, [_P]),
+        "dqtg_comm_rank": (C.c_int, [_P]),
+        "dqtg_comm_size": (C.c_int, [_P]),
+        "dqtg_comm_allreduce_u64": (C.c_int, [_P, _P, _P, C.c_uint64]),
+        "dqtg_compress_sharded": (C.c_int, [_P, _P, _P, C.POINTER(Config), C.c_uint64,
+                                            C.c_uint64, _P, C.c_double, C.c_uint32,
+                                            C.POINTER(_P), C.POINTER(_P)]),
         "dqtg_pipe_run": (C.c_int, [_P, C.POINTER(_Layout), _P, C.c_uint64, _P, _P,
                                     C.POINTER(Config), C.c_uint64, _P, C.c_double, RECORD_FN, _P,
                                     C.POINTER(_P)]),
@@ -529,6 +539,17 @@ class Engine:
         return DevState(self, s, ckpt.meta), r
 
     # -- tensor-sharded quantization (multi-GPU) ------------------------------------
+    def compress_sharded(self, comm, ckpt, cfg, seed, step, base=None, quality=0.0,
+                         n_tensors_total=0):
+        """One sharded Chain::append step over the NCCL communicator `comm`
+        (dqtg_compress_sharded): returns (this rank's DevState, record handle on rank 0
+        or None).  The caller owns the record handle (dqtg_record_destroy)."""
+        s, r = _P(), _P()
+        _check(LIB.dqtg_compress_sharded(self.h, comm.h, ckpt.h, C.byref(cfg), seed, step,
+                                         None if base is None else base.h, quality,
+                                         int(n_tensors_total), C.byref(s), C.byref(r)))
+        return DevState(self, s, ckpt.meta), (r if r else None)
+
     def shard_hist_len(self, cfg, which):
         return LIB.dqtg_shard_hist_len(self.h, C.byref(cfg), which)
 
@@ -636,6 +657,39 @@ class Engine:
 _DEFAULT = None
 
 
+class Comm:
+    """NCCL communicator of the engine library (dqtg_comm_*): one per rank, built from
+    the id rank 0 makes (``Comm.unique_id()``) and hands to every rank out of band."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(LIB.dqtg_comm_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, engine, uid: bytes, nranks: int, rank: int):
+        h = _P()
+        _check(LIB.dqtg_comm_init(engine.h, uid, int(nranks), int(rank), C.byref(h)))
+        self.h = h
+        self.engine = engine
+
+    @property
+    def rank(self):
+        return LIB.dqtg_comm_rank(self.h)
+
+    @property
+    def size(self):
+        return LIB.dqtg_comm_size(self.h)
+
+    def allreduce_u64(self, ptr, n):
+        _check(LIB.dqtg_comm_allreduce_u64(self.engine.h, self.h, ptr, int(n)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and LIB is not None:
+            LIB.dqtg_comm_destroy(self.h)
+            self.h = None
+
+
 class Pipe:
     """Native pipelined delta chain (dqtg_pipe_*, pipe.cu): `workers` engines with
     their own streams and host threads; snapshot k runs on worker k mod W."""
@@ -659,6 +713,12 @@ class Pipe:
     def set_stream(self, stream_ptr):
         """Runs fork from / join into this CUDA stream (events on it time a run)."""
         LIB.dqtg_pipe_set_stream(self.h, stream_ptr or None)
+
+    def set_comms(self, comms, n_tensors_total=0):
+        """Tensor-sharded multi-GPU runs: one engine Comm per worker (dqtg_pipe_set_comms)."""
+        self._comms = list(comms)
+        arr = (_P * max(1, len(self._comms)))(*[c.h for c in self._comms])
+        _check(LIB.dqtg_pipe_set_comms(self.h, arr, len(self._comms), int(n_tensors_total)))
 
     def run(self, names, types, shapes, snapshots, cfg, seed=1, steps=None, ema=None,
             base=None, quality=0.0, on_record=None, engine=None, emas=None):

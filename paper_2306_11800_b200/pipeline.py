@@ -21,14 +21,18 @@ from . import engine as E
 
 
 class ChainCompressor:
-    def __init__(self, device=0, workers=2, stream=None):
+    def __init__(self, device=0, workers=2, stream=None, comms=None, n_tensors_total=0):
         """``stream`` (a cudaStream_t as int, optional): every run forks from and joins
-        into it, so CUDA events recorded on it bracket the run's device work."""
+        into it, so CUDA events recorded on it bracket the run's device work.
+        ``comms`` (one engine Comm per worker, distributed.make_comm): every rank runs
+        the chain over its tensor shard; records reach ``on_record`` on rank 0 only."""
         self.device = device
         self.nw = max(1, int(workers))
         self.pipe = E.Pipe(device, self.nw)
         if stream:
             self.pipe.set_stream(stream)
+        if comms:
+            self.pipe.set_comms(comms, n_tensors_total)
         self._eng = None
 
     @property
