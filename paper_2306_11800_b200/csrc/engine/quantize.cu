@@ -867,6 +867,133 @@ __global__ void __launch_bounds__(kPB) eval_c_kernel(PassIn a, const LtParams* l
         if (s_cnt[j]) atomicAdd(lvl_counts + (size_t)T.tensor * lstride + j, (unsigned long long)s_cnt[j]);
 }
 
+// ---- batched candidate evaluation: several configs per read of w ------------------
+// Candidates sharing a partition (alpha, prune_frac, protect_frac, metric) share
+// pass B; their codebooks differ (bins, embed_bins, sigma, seed).  One CTA per tile
+// classifies each element once and, for every candidate, finds its level, the
+// dequantized value (quantize.cpp:427-462) and Σ(w - deq)² (search.cpp:35-46), and
+// counts levels per tensor (search.cpp:66-81).
+constexpr int kEvalM = 8;
+
+struct EvalMulti {
+    int m;
+    const float* cb;        // [m][7][cbs]
+    int cbs;
+    const float* lb;        // [m][7][lbs]
+    int lbs;
+    const uint32_t* cb_len; // [m][7]
+    double* tile_diff;      // [m][ntiles]
+    unsigned long long* counts;  // [m][nt][lstride]
+    int lstride;
+    int ntiles;
+    int nt;                 // tensors (counts stride)
+};
+
+template <bool EXPL>
+__global__ void __launch_bounds__(kPB) eval_multi_kernel(PassIn a, const LtParams* lp, EvalMulti ev) {
+    extern __shared__ float s_tab[];  // per candidate: codebook (cbs) + bounds (lbs)
+    __shared__ double s_red[kPB / 32][kEvalM];
+    __shared__ uint32_t s_cnt[kEvalM][66];
+    __shared__ uint32_t s_k[kEvalM], s_kp[kEvalM];
+    const int ti = blockIdx.x;
+    const Tile T = a.tiles[ti];
+    const int lt = a.types[T.tensor];
+    const int m = ev.m, per = ev.cbs + ev.lbs;
+    for (int c = threadIdx.x; c < m; c += blockDim.x) {
+        s_k[c] = ev.cb_len[c * kLayerTypes + lt];
+        s_kp[c] = pow2_ceil(s_k[c]);
+    }
+    for (int i = threadIdx.x; i < m * 66; i += blockDim.x) (&s_cnt[0][0])[i] = 0;
+    __syncthreads();
+    for (int c = 0; c < m; ++c) {
+        for (int j = threadIdx.x; j < (int)s_k[c]; j += blockDim.x)
+            s_tab[c * per + j] = ev.cb[((size_t)c * kLayerTypes + lt) * ev.cbs + j];
+        for (int j = threadIdx.x; j < (int)s_kp[c]; j += blockDim.x)
+            s_tab[c * per + ev.cbs + j] = ev.lb[((size_t)c * kLayerTypes + lt) * ev.lbs + j];
+    }
+    const LtParams P = lp[lt];
+    __syncthreads();
+    double acc[kEvalM];
+#pragma unroll
+    for (int c = 0; c < kEvalM; ++c) acc[c] = 0.0;
+    for (uint32_t i = threadIdx.x * 4; i < T.count; i += kPB * 4) {
+        const uint64_t idx = T.start + i;
+        const float4 wv = ld4(a.w + idx);
+        float mg[4], sn[4];
+        load_scores<EXPL>(a, idx, wv, mg, sn);
+        const float wa[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (i + j >= T.count) break;
+            const int part = classify(mg[j], sn[j], a.has_sens, a.metric, P);
+            const float prot = __uint_as_float((uint32_t)bf16_rne(wa[j]) << 16);
+#pragma unroll
+            for (int c = 0; c < kEvalM; ++c) {
+                if (c >= m) break;
+                const uint32_t k = s_k[c];
+                uint32_t lv;
+                float deq;
+                if (part == 0) {
+                    lv = level_of(s_tab + c * per + ev.cbs, s_kp[c], wa[j]);
+                    deq = s_tab[c * per + lv];
+                } else if (part == 1) {
+                    lv = k;
+                    deq = 0.0f;
+                } else {
+                    lv = k + 1;
+                    deq = prot;
+                }
+                const double d = __dsub_rn((double)wa[j], (double)deq);
+                acc[c] = __dadd_rn(acc[c], __dmul_rn(d, d));
+                if (lv < 66) atomicAdd(&s_cnt[c][lv], 1u);
+            }
+        }
+    }
+    // per candidate: warp sums, then the warps in a fixed order
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int c = 0; c < kEvalM; ++c) {
+        double v = acc[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (lane == 0) s_red[wid][c] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < m) {
+        double t = 0.0;
+        for (int w = 0; w < kPB / 32; ++w) t = __dadd_rn(t, s_red[w][threadIdx.x]);
+        ev.tile_diff[(size_t)threadIdx.x * ev.ntiles + ti] = t;
+    }
+    for (int i = threadIdx.x; i < m * 66; i += blockDim.x) {
+        const int c = i / 66, j = i % 66;
+        if (j < (int)s_k[c] + 2 && j < ev.lstride && s_cnt[c][j])
+            atomicAdd(ev.counts + ((size_t)c * ev.nt + T.tensor) * ev.lstride + j,
+                      (unsigned long long)s_cnt[c][j]);
+    }
+}
+
+// per-layer-type sums of several candidates' tile values (grid: one block each)
+__global__ void __launch_bounds__(512) lt_sum_multi_kernel(const Tile* tiles, const uint8_t* types,
+                                                           int ntiles, const double* tile_vals,
+                                                           double* out /*[m][7]*/) {
+    __shared__ double s_part[512][kLayerTypes];
+    const double* tv = tile_vals + (size_t)blockIdx.x * ntiles;
+    double loc[kLayerTypes] = {0, 0, 0, 0, 0, 0, 0};
+    const int per = (ntiles + blockDim.x - 1) / blockDim.x;
+    const int a0 = threadIdx.x * per, a1 = min(ntiles, a0 + per);
+    for (int i = a0; i < a1; ++i) {
+        const int lt = types[tiles[i].tensor];
+        loc[lt] = __dadd_rn(loc[lt], tv[i]);
+    }
+    for (int lt = 0; lt < kLayerTypes; ++lt) s_part[threadIdx.x][lt] = loc[lt];
+    __syncthreads();
+    if (threadIdx.x < kLayerTypes) {
+        double t = 0.0;
+        for (int j = 0; j < (int)blockDim.x; ++j) t = __dadd_rn(t, s_part[j][threadIdx.x]);
+        out[blockIdx.x * kLayerTypes + threadIdx.x] = t;
+    }
+}
+
 // sum of squares (or squared differences) per tile, fixed order
 __global__ void __launch_bounds__(kPB) tile_sq_kernel(const Tile* tiles, const float* x,
                                                       const float* y, double* tile_out) {
@@ -1486,18 +1613,25 @@ double estimate_from_counts(const Layout& L, const uint64_t* counts, int lstride
     return raw / est;
 }
 
+// Partition key of a config: candidates with equal keys share pass B.
+static bool same_partition(const dqtg_config& x, const dqtg_config& y) {
+    return memcmp(&x.alpha, &y.alpha, 8) == 0 && memcmp(&x.prune_frac, &y.prune_frac, 8) == 0 &&
+           memcmp(&x.protect_frac, &y.protect_frac, 8) == 0 && x.metric == y.metric;
+}
+
 void eval_batch(Engine& e, const DevCkpt& c, const dqtg_config* cfgs, const uint64_t* seeds,
                 uint32_t m, double* quality, double* est) {
     const Layout& L = *c.L;
     if (!m) return;
     const int ntiles = (int)L.tiles.size();
+    cudaStream_t st = e.stream;
     // sum of squares of the original weights per layer type (config independent)
     auto* tile_v = (double*)e.buf("ev.tile_v", (size_t)ntiles * 8 + 8);
     auto* d_lt = (double*)e.buf("ev.lt", 16 * 8);
-    double orig[kLayerTypes] = {0}, diff[kLayerTypes];
+    double orig[kLayerTypes] = {0};
     if (ntiles) {
-        { DQTG_SPAN(e, "tile_sq_kernel"); tile_sq_kernel<<<ntiles, kPB, 0, e.stream>>>(L.d_tiles, c.w, nullptr, tile_v); }
-        { DQTG_SPAN(e, "lt_sum_kernel"); lt_sum_kernel<<<1, 512, 0, e.stream>>>(L.d_tiles, L.d_types, ntiles, tile_v, d_lt); }
+        { DQTG_SPAN(e, "tile_sq_kernel"); tile_sq_kernel<<<ntiles, kPB, 0, st>>>(L.d_tiles, c.w, nullptr, tile_v); }
+        { DQTG_SPAN(e, "lt_sum_kernel"); lt_sum_kernel<<<1, 512, 0, st>>>(L.d_tiles, L.d_types, ntiles, tile_v, d_lt); }
         e.launched(2);
         e.d2h(orig, d_lt, sizeof(orig));
     }
@@ -1518,20 +1652,45 @@ void eval_batch(Engine& e, const DevCkpt& c, const dqtg_config* cfgs, const uint
         for (uint32_t i = 0; i < m; ++i) quality[i] = 0.0, est[i] = 0.0;
         return;
     }
-    // pass A once per alpha, all layer types, both score kinds
+    // partition groups: the first candidate of each key runs pass B for all of them
+    std::vector<int> leader(m, -1);
+    std::vector<std::vector<uint32_t>> groups;
+    for (uint32_t i = 0; i < m; ++i) {
+        for (size_t g = 0; g < groups.size() && leader[i] < 0; ++g)
+            if (same_partition(cfgs[groups[g][0]], cfgs[i])) {
+                leader[i] = (int)groups[g][0];
+                groups[g].push_back(i);
+            }
+        if (leader[i] < 0) {
+            leader[i] = (int)i;
+            groups.push_back({i});
+        }
+    }
     for (uint32_t i = 0; i < m; ++i) {
         Stage& s = *stages[i];
         DQTG_REQUIRE(s.cfg.alpha > 0.0 && s.cfg.alpha < 1.0, DQTG_ALPHA_OUT_OF_RANGE,
                      "alpha must be in (0, 1)");
         AlphaTables& T = e.alpha_tables(s.cfg.alpha);
         stage_alloc(e, L, T.HS, s, nullptr);
+        if (leader[i] != (int)i) {  // shares the leader's partition, value histogram, counts
+            Stage& ld = *stages[leader[i]];
+            s.d_lp = ld.d_lp;
+            s.gh_val = ld.gh_val;
+            s.tensor_prot = ld.tensor_prot;
+            s.tile_prot = ld.tile_prot;
+            s.tile_off = ld.tile_off;
+            s.parts = ld.parts;
+            stage_keys(e, L, s, T);  // keys + weights with this candidate's sigma
+            continue;
+        }
+        // pass A once per alpha, all layer types, both score kinds
         uint64_t key;
         memcpy(&key, &s.cfg.alpha, 8);
         auto it = scores_by_alpha.find(key);
         if (it == scores_by_alpha.end()) {
             auto* gh = (unsigned long long*)e.buf("ev.gh_scores" + std::to_string(scores_by_alpha.size()),
                                                   (size_t)2 * kLayerTypes * T.HS * 8);
-            DQTG_CUDA(cudaMemsetAsync(gh, 0, (size_t)2 * kLayerTypes * T.HS * 8, e.stream));
+            DQTG_CUDA(cudaMemsetAsync(gh, 0, (size_t)2 * kLayerTypes * T.HS * 8, st));
             PassIn a = pass_in(e, c, T, 0);
             stage_pass_a(e, c, a, 0x7f, c.has_sens ? 0x7f : 0, gh, gh + (size_t)kLayerTypes * T.HS);
             it = scores_by_alpha.emplace(key, std::make_pair(gh, gh + (size_t)kLayerTypes * T.HS)).first;
@@ -1542,48 +1701,76 @@ void eval_batch(Engine& e, const DevCkpt& c, const dqtg_config* cfgs, const uint
     }
     e.check_err();
     {
-        std::vector<Stage*> v;
-        for (auto& s : stages) v.push_back(s.get());
-        AlphaTables& T0 = e.alpha_tables(stages[0]->cfg.alpha);
-        PassIn a = pass_in(e, c, T0, 0);
         // codebooks: problems of configs sharing an alpha go together
         std::map<uint64_t, std::vector<Stage*>> by_alpha;
-        for (Stage* s : v) {
+        for (auto& sp : stages) {
             uint64_t key;
-            memcpy(&key, &s->cfg.alpha, 8);
-            by_alpha[key].push_back(s);
+            memcpy(&key, &sp->cfg.alpha, 8);
+            by_alpha[key].push_back(sp.get());
         }
         for (auto& kv : by_alpha) {
             AlphaTables& T = e.alpha_tables(kv.second[0]->cfg.alpha);
             PassIn aa = pass_in(e, c, T, 0);
             stage_codebooks(e, kv.second, aa, T.HS);
         }
-        (void)a;
     }
-    auto* counts = (unsigned long long*)e.buf("ev.counts", (size_t)L.nt * lstride * 8 + 8);
-    std::vector<uint64_t> hcounts((size_t)L.nt * lstride);
-    for (uint32_t i = 0; i < m; ++i) {
-        Stage& s = *stages[i];
-        AlphaTables& T = e.alpha_tables(s.cfg.alpha);
-        PassIn a = pass_in(e, c, T, (int)s.cfg.metric);
-        DQTG_CUDA(cudaMemsetAsync(counts, 0, (size_t)L.nt * lstride * 8, e.stream));
-        stage_level_bounds(e, s);
-        const size_t smem = (size_t)(s.cb_stride + s.lb_stride) * 4 + 16;
-        if (c.explicit_scores)
-            { DQTG_SPAN(e, "eval_c_kernel"); eval_c_kernel<true><<<ntiles, kPB, smem, e.stream>>>(a, s.d_lp, s.d_cb, (int)s.cb_stride, s.d_lb, (int)s.lb_stride, s.cb_len, tile_v, counts, lstride); }
-        else
-            { DQTG_SPAN(e, "eval_c_kernel"); eval_c_kernel<false><<<ntiles, kPB, smem, e.stream>>>(a, s.d_lp, s.d_cb, (int)s.cb_stride, s.d_lb, (int)s.lb_stride, s.cb_len, tile_v, counts, lstride); }
-        { DQTG_SPAN(e, "lt_sum_kernel"); lt_sum_kernel<<<1, 512, 0, e.stream>>>(L.d_tiles, L.d_types, ntiles, tile_v, d_lt); }
-        e.launched(2);
-        uint32_t cbl[kLayerTypes];
-        e.d2h(diff, d_lt, sizeof(diff));
-        e.d2h(cbl, s.cb_len, sizeof(cbl));
-        e.d2h(hcounts.data(), counts, hcounts.size() * 8);
-        e.check_err();
-        quality[i] = quality_from(L, diff, orig);
-        std::vector<uint64_t> np(L.nt);
-        for (uint32_t t = 0; t < L.nt; ++t) np[t] = s.h_tprot[t];
-        est[i] = estimate_from_counts(L, hcounts.data(), lstride, cbl, np.data());
+    // evaluation: kEvalM candidates of one partition group per read of w
+    auto* counts = (unsigned long long*)e.buf("ev.counts", (size_t)kEvalM * L.nt * lstride * 8 + 8);
+    auto* tdiff = (double*)e.buf("ev.tdiff", (size_t)kEvalM * ntiles * 8 + 8);
+    auto* d_ltm = (double*)e.buf("ev.ltm", (size_t)kEvalM * kLayerTypes * 8);
+    std::vector<uint64_t> hcounts((size_t)kEvalM * L.nt * lstride);
+    for (const auto& grp : groups) {
+        for (size_t g0 = 0; g0 < grp.size(); g0 += kEvalM) {
+            const int mm = (int)std::min<size_t>(kEvalM, grp.size() - g0);
+            uint32_t cbs = 1, lbs = 1;
+            for (int j = 0; j < mm; ++j) {
+                Stage& s = *stages[grp[g0 + j]];
+                stage_level_bounds(e, s);
+                cbs = std::max(cbs, s.cb_stride);
+                lbs = std::max(lbs, s.lb_stride);
+            }
+            auto* mcb = (float*)e.buf("ev.mcb", (size_t)kEvalM * kLayerTypes * cbs * 4);
+            auto* mlb = (float*)e.buf("ev.mlb", (size_t)kEvalM * kLayerTypes * lbs * 4);
+            auto* mlen = (uint32_t*)e.buf("ev.mlen", (size_t)kEvalM * kLayerTypes * 4);
+            for (int j = 0; j < mm; ++j) {
+                Stage& s = *stages[grp[g0 + j]];
+                DQTG_CUDA(cudaMemcpy2DAsync(mcb + (size_t)j * kLayerTypes * cbs, cbs * 4, s.d_cb,
+                                            s.cb_stride * 4, s.cb_stride * 4, kLayerTypes,
+                                            cudaMemcpyDeviceToDevice, st));
+                DQTG_CUDA(cudaMemcpy2DAsync(mlb + (size_t)j * kLayerTypes * lbs, lbs * 4, s.d_lb,
+                                            s.lb_stride * 4, s.lb_stride * 4, kLayerTypes,
+                                            cudaMemcpyDeviceToDevice, st));
+                DQTG_CUDA(cudaMemcpyAsync(mlen + j * kLayerTypes, s.cb_len, kLayerTypes * 4,
+                                          cudaMemcpyDeviceToDevice, st));
+            }
+            DQTG_CUDA(cudaMemsetAsync(counts, 0, (size_t)mm * L.nt * lstride * 8, st));
+            Stage& s0 = *stages[grp[g0]];
+            AlphaTables& T = e.alpha_tables(s0.cfg.alpha);
+            PassIn a = pass_in(e, c, T, (int)s0.cfg.metric);
+            EvalMulti ev{mm, mcb, (int)cbs, mlb, (int)lbs, mlen, tdiff, counts, lstride, ntiles, (int)L.nt};
+            const size_t smem = (size_t)mm * (cbs + lbs) * 4 + 16;
+            if (c.explicit_scores)
+                { DQTG_SPAN(e, "eval_multi_kernel"); eval_multi_kernel<true><<<ntiles, kPB, smem, st>>>(a, s0.d_lp, ev); }
+            else
+                { DQTG_SPAN(e, "eval_multi_kernel"); eval_multi_kernel<false><<<ntiles, kPB, smem, st>>>(a, s0.d_lp, ev); }
+            { DQTG_SPAN(e, "lt_sum_multi_kernel"); lt_sum_multi_kernel<<<mm, 512, 0, st>>>(L.d_tiles, L.d_types, ntiles, tdiff, d_ltm); }
+            e.launched(2);
+            std::vector<double> diff((size_t)mm * kLayerTypes);
+            std::vector<uint32_t> cbl((size_t)mm * kLayerTypes);
+            e.d2h(diff.data(), d_ltm, diff.size() * 8);
+            e.d2h(cbl.data(), mlen, cbl.size() * 4);
+            e.d2h(hcounts.data(), counts, (size_t)mm * L.nt * lstride * 8);
+            e.check_err();
+            for (int j = 0; j < mm; ++j) {
+                const uint32_t i = grp[g0 + j];
+                Stage& s = *stages[i];
+                quality[i] = quality_from(L, diff.data() + (size_t)j * kLayerTypes, orig);
+                std::vector<uint64_t> np(L.nt);
+                for (uint32_t t = 0; t < L.nt; ++t) np[t] = s.h_tprot[t];
+                est[i] = estimate_from_counts(L, hcounts.data() + (size_t)j * L.nt * lstride, lstride,
+                                              cbl.data() + (size_t)j * kLayerTypes, np.data());
+            }
+        }
     }
 }
 
