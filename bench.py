@@ -307,6 +307,89 @@ def measure_ingest(eng, layout, flat, cpu=True, reps=3):
 tensor_ptrs = W.tensor_ptrs
 
 
+def host_checkpoint(d, layout, flat, step=0):
+    """A Checkpoint of the given module (ours: dqt; the reference: dqtref) from one
+    flat host array."""
+    c = d.Checkpoint()
+    c.step = step
+    for (name, lt, shape), v in zip(layout, W.split(flat, layout)):
+        c.add_tensor(name, v.reshape(shape), d.LayerType(lt))
+    return c
+
+
+def measure_c3(torch, dev, cpu_ref=True, ref_layers=1):
+    """BASELINE configs[2] (C3): guided_exhaustive_search (search.cpp:380-385) over the
+    default ConfigCube on a BERT-large checkpoint (335,141,888 params, synthetic, EMA
+    sensitivity), threshold 0.1, parallelism = nproc, through the drop-in module with
+    the device ProxyEvaluator (batched candidate evaluation).  The reference's
+    ProxyEvaluator::evaluate (search.cpp:107-112) is timed on a bounded sample of the
+    same bytes (embeddings + ref_layers encoder layers)."""
+    from paper_2306_11800_b200 import dqt
+
+    layout = W.bert_large_layout()
+    N = W.layout_params(layout)
+    tr = W.Trajectory(torch, N, SEED + 100, dev)
+    w = tr.next()
+    tr.next()
+    ema = tr.ema().cpu().numpy()
+    wh = w.cpu().numpy()
+    del w, tr
+    nproc = os.cpu_count() or 1
+    c = host_checkpoint(dqt, layout, wh, 1)
+    e = dqt.ema_init(0.9)
+    dqt.ema_update(e, host_checkpoint(dqt, layout, ema, 1))  # first update copies
+    scores = dqt.compute_scores(c, e)
+    ev = dqt.ProxyEvaluator()
+    params = dqt.SearchParams(threshold=0.1, parallelism=nproc, seed=1)
+    t = time.perf_counter()
+    out = dqt.guided_exhaustive_search(c, scores, dqt.ConfigCube(), ev, params)
+    dt = time.perf_counter() - t
+    res = {"workload": "C3: BERT-large 335.1M fp32 params, guided_exhaustive_search threshold 0.1, "
+                       f"parallelism {nproc}, default ConfigCube",
+           "params": N, "search_s": dt, "evaluations": out.evaluations_used,
+           "evals_per_s": out.evaluations_used / dt,
+           "eval_gbs": 4.0 * N * out.evaluations_used / dt / 1e9,
+           "chosen": {"bins": out.config.bins, "embed_bins": out.config.embed_bins,
+                      "prune_frac": out.config.prune_frac, "protect_frac": out.config.protect_frac,
+                      "metric": int(out.config.metric)},
+           "quality_delta": out.quality_delta, "est_compression": out.est_compression,
+           "feasible": out.feasible,
+           "path": "dqt.guided_exhaustive_search + dqt.ProxyEvaluator: every EvalCache::prefetch "
+                   "batch is one dqtg_eval_batch (shared pass B per partition, 8 candidates per "
+                   "read of w); checkpoint resident in HBM across batches; host wall clock"}
+    del c, scores, ev
+    if cpu_ref:
+        from oracle import ref as R
+
+        d = R.load()
+        sub = [x for x in layout if x[0].startswith("bert.embeddings")]
+        for i in range(ref_layers):
+            sub += [x for x in layout if x[0].startswith(f"bert.encoder.layer.{i}.")]
+        names = {x[0] for x in sub}
+        pick = [v for (n, _, _), v in zip(layout, W.split(wh, layout)) if n in names]
+        pick_e = [v for (n, _, _), v in zip(layout, W.split(ema, layout)) if n in names]
+        Ns = sum(int(v.size) for v in pick)
+        rc = host_checkpoint(d, sub, np.concatenate(pick), 1)
+        re_ = d.ema_init(0.9)
+        d.ema_update(re_, host_checkpoint(d, sub, np.concatenate(pick_e), 1))
+        rs = d.compute_scores(rc, re_)
+        cfg = d.QuantConfig()
+        t = time.perf_counter()  # ProxyEvaluator::evaluate (search.cpp:107-112), step by step
+        q = d.quantize_checkpoint(rc, rs, cfg, 1)
+        d.proxy_quality_delta(rc, d.dequantize_checkpoint(q))
+        d.estimate_compression(rc, q)
+        tr_ = time.perf_counter() - t
+        one = 4.0 * Ns / tr_ / 1e9
+        res["cpu_reference"] = {
+            "value": one, "unit": "GB/s per evaluation, 1 thread", "kind": "reference", "cores": 1,
+            "ideal_parallel_gbs": one * nproc, "nproc": nproc, "eval_s": tr_,
+            "sample": f"ProxyEvaluator::evaluate (quantize + dequantize + proxy_quality_delta + "
+                      f"estimate_compression), default QuantConfig, BERT-large embeddings + "
+                      f"{ref_layers} encoder layer(s) ({Ns} params) of the same bytes"}
+        res["speedup_vs_reference_ideal_parallel"] = res["eval_gbs"] / (one * nproc)
+    return res
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -643,10 +726,17 @@ def run_ours(args):
     if world == 1:
         ingest = measure_ingest(eng, layout, host_snaps[0], cpu=not args.no_cpu_baseline)
 
+    c3 = None
+    if world == 1 and not args.no_c3:
+        del ckpts
+        ckpts = None
+        torch.cuda.empty_cache()
+        c3 = measure_c3(torch, dev, cpu_ref=not args.no_cpu_baseline)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # the reference on the same C2 chain and bytes, a bounded number of steps
-        del ckpts
+        ckpts = None
         torch.cuda.empty_cache()
         ts, Ns, rec_ref, same = reference_chain(args.cpu_steps, 0)
         v = 4.0 * Ns * len(ts) / sum(ts) / 1e9
@@ -688,7 +778,7 @@ def run_ours(args):
                                   if pipelined is not None and ms == pipelined else
                                   "CUDA events on the engine stream")},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "restore": restore,
-            "ingest": ingest,
+            "ingest": ingest, "c3_search": c3,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
         }
@@ -707,6 +797,7 @@ def main():
                     help="timed reference steps of the cpu_baseline leg (~10 s each at C2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 (BERT-large search) leg")
     ap.add_argument("--workers", type=int, default=4, help="worker streams of the chain pipeline")
     ap.add_argument("--share-gpu", action="store_true",
                     help="test mode for N>1 on one GPU: all ranks on device 0 with gloo")
