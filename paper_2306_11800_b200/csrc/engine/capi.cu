@@ -593,8 +593,9 @@ dqtg_status dqtg_compress_step(dqtg_engine* h, const dqtg_ckpt* c, const dqtg_co
                                double quality, dqtg_qstate** state_out, dqtg_record** record_out) {
     return guard([&] {
         LOCK(&h->e);
-        auto q = ::dqtg::quantize(h->e, c->c, *cfg, seed, step);
-        auto r = ::dqtg::encode_record(h->e, base ? base->q.get() : nullptr, *q, quality);
+        std::unique_ptr<QState> q;
+        auto r = ::dqtg::compress_step(h->e, c->c, *cfg, seed, step, base ? base->q.get() : nullptr,
+                                       quality, q);
         auto* s = new dqtg_qstate();
         s->q = std::move(q);
         auto* rr = new dqtg_record();

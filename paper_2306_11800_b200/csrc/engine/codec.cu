@@ -552,8 +552,7 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
 //      symbol frequencies, tile CRC) is the format enc_tile_kernel writes.
 // Seven block barriers per tile (single-barrier scans); Z lives in shared memory
 // up to kZCap non-zero elements, in a per-CTA global slice for denser tiles.
-constexpr int kBlkEl = 32;                // elements per count block (a thread pair)
-constexpr int kNBlk = kTile / kBlkEl;     // 128
+constexpr int kNBlk = kCB;                // count blocks per tile: one per thread (16 elements)
 constexpr int kZCap = 2048;               // non-zero elements held in shared memory
 
 // Exclusive block scan with one barrier: warp totals in slots[kCB / 32]; the slots
@@ -584,8 +583,6 @@ struct DSmem {
     uint32_t* freq;   // B*NS per tensor
     uint32_t* crc;    // kCrcTabs*256
     uint32_t* nib;    // kNibConsts*8*16
-    uint32_t* key32;  // kTile key bytes (0xff: no element)
-    uint32_t* d32;    // kTile delta bytes
     uint32_t* hc;     // [B][kNBlk]: counts (lo 16) | non-zero counts (hi 16) -> exclusive prefixes
     uint16_t* hp;     // kTile + 1: slots of run heads (aliases hc after Z)
     uint32_t* z;      // kZCap: r | v << 16 | key << 24, key-sorted
@@ -598,7 +595,7 @@ __host__ __device__ inline size_t dsm_hc_bytes(uint32_t B) {
 
 __host__ __device__ inline size_t dsm_bytes(uint32_t B, uint32_t NS) {
     return (((size_t)B * NS * 4 + 15) & ~(size_t)15) + (size_t)kCrcTabs * 256 * 4 +
-           (size_t)kNibConsts * 8 * 16 * 4 + 2 * (size_t)kTile + dsm_hc_bytes(B) + (size_t)kZCap * 4;
+           (size_t)kNibConsts * 8 * 16 * 4 + dsm_hc_bytes(B) + (size_t)kZCap * 4;
 }
 
 __device__ inline DSmem dsm_carve(uint8_t* base, uint32_t B, uint32_t NS) {
@@ -607,8 +604,6 @@ __device__ inline DSmem dsm_carve(uint8_t* base, uint32_t B, uint32_t NS) {
     S.freq = (uint32_t*)(base + o); o += ((size_t)B * NS * 4 + 15) & ~(size_t)15;
     S.crc = (uint32_t*)(base + o);  o += (size_t)kCrcTabs * 256 * 4;
     S.nib = (uint32_t*)(base + o);  o += (size_t)kNibConsts * 8 * 16 * 4;
-    S.key32 = (uint32_t*)(base + o); o += kTile;
-    S.d32 = (uint32_t*)(base + o);   o += kTile;
     S.hc = (uint32_t*)(base + o);
     S.hp = (uint16_t*)(base + o);
     o += dsm_hc_bytes(B);
@@ -771,7 +766,42 @@ __device__ __forceinline__ void r_phase(const EncArgs& A, const DSmem& S, const 
     r_emit<PER>(A, S, Z, D, tensor, j0, zc, fl, xr, xh, runs);
 }
 
-__global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A) {
+// ---- fused pass C (quantize.cpp:396-423) ------------------------------------------
+// compress_step with a base: the target levels are computed inside the DELTA tile
+// pass from w and pass B's 2-bit partition codes, written once, and encoded from
+// registers (no level read-back); protected (pos, bf16) entries are compacted per
+// tile at pass B's per-tile offsets, in element order.
+
+// 16 levels of one thread (elements e0..e0+15 of the tile, nv valid) as bytes, and
+// the protected-element mask: nearest-centre level by branch-free bisection over the
+// boundaries (pass_c_tile), PRUNED = k, PROTECTED = k + 1.
+template <int LOGP>
+__device__ __forceinline__ void fused_levels(const float* s_lb, const float* w, uint32_t pw,
+                                             uint32_t k, uint32_t nv, uint32_t (&cw)[4],
+                                             uint32_t& pmask) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if ((uint32_t)(4 * q) < nv) v = __ldg((const float4*)(w + 4 * q));
+        const float a[4] = {v.x, v.y, v.z, v.w};
+        uint32_t word = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t pos = 0;
+#pragma unroll
+            for (int st = (1 << LOGP) >> 1; st > 0; st >>= 1)
+                pos += (a[j] >= s_lb[pos + st]) ? (uint32_t)st : 0u;
+            const uint32_t part = (pw >> (2 * (4 * q + j))) & 3u;
+            const uint32_t lv = part == 0 ? pos : (part == 1 ? k : k + 1);
+            word |= lv << (8 * j);
+            pmask |= (part == 2 ? 1u : 0u) << (4 * q + j);
+        }
+        cw[q] = word;
+    }
+}
+
+template <bool FUSED>
+__global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A, FuseC F) {
     extern __shared__ __align__(16) uint8_t e1_dyn[];
     const uint32_t B = A.B, NS = A.NS;
     const DSmem S = dsm_carve(e1_dyn, B, NS);
@@ -779,6 +809,9 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A) {
     __shared__ uint32_t s_fv[kMaxB], s_lv[kMaxB], s_lead[kMaxB], s_trail[kMaxB], s_aux[kMaxB];
     __shared__ uint32_t s_part[kCB / 32];
     __shared__ unsigned long long s_slots[kCB / 32];
+    __shared__ uint32_t s_pslots[kCB / 32];
+    __shared__ float s_lb[64];  // FUSED: level boundaries of the current layer type
+    __shared__ uint32_t s_k, s_logp;
     __shared__ int s_base;
     const DRun D{s_n, s_nz, s_zoff, s_gruns, s_gbase, s_fv, s_lv, s_lead, s_trail, s_aux};
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -787,7 +820,7 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A) {
     for (uint32_t i = tid; i < kCrcTabs * 256; i += kCB) S.crc[i] = (&g_crc_slice[0][0])[i];
     for (uint32_t i = tid; i < kNibConsts * 8 * 16; i += kCB) S.nib[i] = (&g_crc_nib[0][0][0])[i];
     for (uint32_t i = tid; i < B * NS; i += kCB) S.freq[i] = 0;
-    for (uint32_t i = tid; i < kNBlk * B; i += kCB) S.hc[i] = 0;
+    for (uint32_t i = tid; i < kNBlk * B / 4; i += kCB) ((uint4*)S.hc)[i] = make_uint4(0, 0, 0, 0);
     for (uint32_t b = tid; b < B; b += kCB) s_nz[b] = s_gruns[b] = s_aux[b] = 0;
     uint32_t* zg = A.zs + (size_t)blockIdx.x * kTile;  // Z of tiles denser than kZCap
     uint32_t cur_tensor = 0xffffffffu;
@@ -799,7 +832,12 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A) {
         if (tid == 0 && ti + 1 < min(base + 4, A.ntiles)) {  // next tile's levels into L2
             const Tile N = A.tiles[ti + 1];
             const uint32_t bytes = ((N.count + 7u) & ~7u) * 2u;
-            prefetch_l2(A.cur + N.start, bytes);
+            if (FUSED) {
+                prefetch_l2(F.w + N.start, ((N.count + 3u) & ~3u) * 4u);
+                prefetch_l2(F.parts + (N.start >> 2), ((N.count + 15u) & ~15u) >> 2);
+            } else {
+                prefetch_l2(A.cur + N.start, bytes);
+            }
             prefetch_l2(A.prev + N.start, bytes);
         }
         if (T.tensor != cur_tensor) {  // flush the previous tensor's symbol counts
@@ -815,24 +853,57 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A) {
                 }
             }
             cur_tensor = T.tensor;
+            if (FUSED) {  // level boundaries of the tensor's layer type (+inf padded to 64)
+                const int lt = A.types[T.tensor];
+                const uint32_t k = F.cb_len[lt];
+                uint32_t kp = 1, lg = 0;
+                while (kp < k) kp <<= 1, ++lg;
+                if (tid < 64) s_lb[tid] = tid < (int)kp ? F.lb[lt * F.lb_stride + tid]
+                                                        : __int_as_float(0x7f800000);
+                if (tid == 0) s_k = k, s_logp = lg;
+                __syncthreads();
+            }
         }
         // ---- L: 16 levels per thread, deltas, validation, CRC; block key counts
         const uint32_t e0 = tid * kIt;
         const uint32_t nv = e0 < cnt ? min(cnt - e0, (uint32_t)kIt) : 0u;
         uint32_t kw[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu}, dwv[4] = {0, 0, 0, 0};
         uint32_t nzm = 0;  // non-zero delta bits of the 16 elements
+        uint32_t pmask = 0;  // FUSED: protected elements
         {
             uint32_t cw[4] = {0, 0, 0, 0}, pw[4] = {0, 0, 0, 0};
             if (nv) {
-                const uint4* cp = (const uint4*)(A.cur + T.start + e0);
                 const uint4* pp = (const uint4*)(A.prev + T.start + e0);
-                const uint4 a0 = cp[0], a1 = cp[1], b0 = pp[0], b1 = pp[1];
+                const uint4 b0 = pp[0], b1 = pp[1];
+                uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0;
+                if (FUSED) {
+                    const uint32_t pc = *(const uint32_t*)(F.parts + ((T.start + e0) >> 2));
+                    const float* wp = F.w + T.start + e0;
+                    switch (s_logp) {
+#define DQTG_FL(L) case L: fused_levels<L>(s_lb, wp, pc, s_k, nv, cw, pmask); break;
+                        DQTG_FL(0) DQTG_FL(1) DQTG_FL(2) DQTG_FL(3) DQTG_FL(4) DQTG_FL(5)
+                        default: fused_levels<6>(s_lb, wp, pc, s_k, nv, cw, pmask);
+#undef DQTG_FL
+                    }
+                    if (nv < (uint32_t)kIt) pmask &= (1u << nv) - 1u;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) cw[j] &= keep_mask((int)nv - 4 * j);
+                    // u16 levels (little-endian: level, 0); the tile's padding gets 0
+                    uint16_t* lp = F.levels + T.start + e0;
+                    *(uint4*)lp = make_uint4(__byte_perm(cw[0], 0, 0x4140), __byte_perm(cw[0], 0, 0x4342),
+                                             __byte_perm(cw[1], 0, 0x4140), __byte_perm(cw[1], 0, 0x4342));
+                    *(uint4*)(lp + 8) = make_uint4(__byte_perm(cw[2], 0, 0x4140), __byte_perm(cw[2], 0, 0x4342),
+                                                   __byte_perm(cw[3], 0, 0x4140), __byte_perm(cw[3], 0, 0x4342));
+                } else {
+                    const uint4* cp = (const uint4*)(A.cur + T.start + e0);
+                    a0 = cp[0], a1 = cp[1];
+                    cw[0] = __byte_perm(a0.x, a0.y, 0x6420);
+                    cw[1] = __byte_perm(a0.z, a0.w, 0x6420);
+                    cw[2] = __byte_perm(a1.x, a1.y, 0x6420);
+                    cw[3] = __byte_perm(a1.z, a1.w, 0x6420);
+                }
                 const uint32_t hi[8] = {a0.x | b0.x, a0.y | b0.y, a0.z | b0.z, a0.w | b0.w,
                                         a1.x | b1.x, a1.y | b1.y, a1.z | b1.z, a1.w | b1.w};
-                cw[0] = __byte_perm(a0.x, a0.y, 0x6420);
-                cw[1] = __byte_perm(a0.z, a0.w, 0x6420);
-                cw[2] = __byte_perm(a1.x, a1.y, 0x6420);
-                cw[3] = __byte_perm(a1.z, a1.w, 0x6420);
                 pw[0] = __byte_perm(b0.x, b0.y, 0x6420);
                 pw[1] = __byte_perm(b0.z, b0.w, 0x6420);
                 pw[2] = __byte_perm(b1.x, b1.y, 0x6420);
@@ -864,8 +935,6 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A) {
                 }
                 if (bad | big) atomicOr(A.err, kErrCorruptIndex);
             }
-            *(uint4*)(S.key32 + tid * 4) = make_uint4(kw[0], kw[1], kw[2], kw[3]);
-            *(uint4*)(S.d32 + tid * 4) = make_uint4(dwv[0], dwv[1], dwv[2], dwv[3]);
             // CRC of this thread's levels (zero register), right-aligned in its 32-byte chunk
             uint32_t c0 = cw[0], c1 = cw[1], c2 = cw[2], c3 = cw[3];
             if (nv && nv < (uint32_t)kIt) {
@@ -890,9 +959,9 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A) {
                 r = warp_xor(r);
                 if (lane == 0) s_part[wid] = r;
             }
-            // block counts: elements (lo 16 bits) and non-zero elements (hi 16 bits);
-            // per key: non-zero elements
-            uint32_t* hb = S.hc + (tid >> 1);
+            // block (= thread) counts: elements (lo 16 bits) and non-zero elements (hi
+            // 16 bits), conflict-free (one column per thread); per key: non-zero elements
+            uint32_t* hb = S.hc + tid;
 #pragma unroll
             for (int j = 0; j < kIt; ++j) {
                 if ((uint32_t)j >= nv) break;
@@ -904,19 +973,35 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A) {
                 atomicAdd(&s_nz[(kw[j >> 2] >> (8 * (j & 3))) & 0xffu], 1u);
             }
         }
-        __syncthreads();
-        // ---- H: per key, exclusive prefix over the 128 blocks (one warp per key)
+        if (FUSED) {  // protected entries in element order (the scan's barrier ends L)
+            uint32_t ptot;
+            const uint32_t pex = block_exscan1<uint32_t>(__popc(pmask), s_pslots, &ptot);
+            unsigned long long o = F.tile_prot_off[ti] + pex;
+            const uint64_t tbase = A.off[T.tensor];
+            for (uint32_t m = pmask; m; m &= m - 1) {
+                const uint32_t j = __ffs(m) - 1;
+                F.ppos[o] = (T.start - tbase) + e0 + j;
+                F.pval[o] = bf16_rne(F.w[T.start + e0 + j]);
+                ++o;
+            }
+        } else {
+            __syncthreads();
+        }
+        // ---- H: per key, exclusive prefix over the 256 blocks (one warp per key)
         for (uint32_t k = wid; k < B; k += kCB / 32) {
-            uint4 v = *(const uint4*)(S.hc + k * kNBlk + 4 * lane);
-            const uint32_t s1 = v.x + v.y, s2 = s1 + v.z, s3 = s2 + v.w;
-            uint32_t x = s3;
+            uint4* row = (uint4*)(S.hc + k * kNBlk + 8 * lane);
+            const uint4 v = row[0], u = row[1];
+            const uint32_t s1 = v.x + v.y, s2 = s1 + v.z, s3 = s2 + v.w, s4 = s3 + u.x,
+                           s5 = s4 + u.y, s6 = s5 + u.z, s7 = s6 + u.w;
+            uint32_t x = s7;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
                 if (lane >= o) x += y;
             }
-            const uint32_t ex = x - s3;
-            *(uint4*)(S.hc + k * kNBlk + 4 * lane) = make_uint4(ex, ex + v.x, ex + s1, ex + s2);
+            const uint32_t ex = x - s7;
+            row[0] = make_uint4(ex, ex + v.x, ex + s1, ex + s2);
+            row[1] = make_uint4(ex + s3, ex + s4, ex + s5, ex + s6);
             if (lane == 31) s_n[k] = x & 0xffffu;
         }
         if (wid == 0) {  // slot offsets of the keys' non-zero elements in Z
@@ -945,29 +1030,25 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A) {
         // ---- Z: every non-zero element, by its owning thread
         const uint32_t nzt = s_zoff[B];
         uint32_t* Z = nzt <= (uint32_t)kZCap ? S.z : zg;
+        // the thread's own 16 keys / deltas are its count block: ranks from registers
+        uint32_t nzw[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) nzw[w] = __vcmpne4(dwv[w], 0u);
         for (uint32_t m = nzm; m; m &= m - 1) {
-            const uint32_t j = __ffs(m) - 1, e = e0 + j;
-            const uint32_t k = (S.key32[e >> 2] >> (8 * (e & 3))) & 0xffu;
-            const uint32_t v = (S.d32[e >> 2] >> (8 * (e & 3))) & 0xffu;
+            const uint32_t j = __ffs(m) - 1;
+            const uint32_t wj = j >> 2, sh = 8 * (j & 3);
+            const uint32_t kwj = wj == 0 ? kw[0] : wj == 1 ? kw[1] : wj == 2 ? kw[2] : kw[3];
+            const uint32_t dwj = wj == 0 ? dwv[0] : wj == 1 ? dwv[1] : wj == 2 ? dwv[2] : dwv[3];
+            const uint32_t k = (kwj >> sh) & 0xffu, v = (dwj >> sh) & 0xffu;
             const uint32_t krep = k * 0x01010101u;
-            const uint4* kb = (const uint4*)(S.key32 + (e >> 5) * 8);
-            const uint4* db = (const uint4*)(S.d32 + (e >> 5) * 8);
-            const uint32_t lim = e & 31u;  // same-key bytes before the element in its block
-            uint32_t acc = 0, accnz = 0;
+            uint32_t acc = 0, accnz = 0;  // same-key (non-zero) elements before j
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint4 kk = kb[h], dd = db[h];
-                const uint32_t kx[4] = {kk.x, kk.y, kk.z, kk.w}, dx[4] = {dd.x, dd.y, dd.z, dd.w};
-#pragma unroll
-                for (int w = 0; w < 4; ++w) {
-                    // bytes before the element: the low min(max(lim - 4 wi, 0), 4) bytes
-                    const int kb4 = min(max((int)lim - 16 * h - 4 * w, 0), 4);
-                    const uint32_t eq = __vcmpeq4(kx[w], krep) & (uint32_t)((1ull << (8 * kb4)) - 1ull);
-                    acc += __popc(eq);
-                    accnz += __popc(eq & __vcmpne4(dx[w], 0u));
-                }
+            for (int w = 0; w < 4; ++w) {
+                const uint32_t eq = __vcmpeq4(kw[w], krep) & keep_mask((int)j - 4 * w);
+                acc += __popc(eq);
+                accnz += __popc(eq & nzw[w]);
             }
-            const uint32_t pre = S.hc[k * kNBlk + (e >> 5)];
+            const uint32_t pre = S.hc[k * kNBlk + tid];
             Z[s_zoff[k] + (pre >> 16) + (accnz >> 3)] = ((pre & 0xffffu) + (acc >> 3)) | (v << 16) | (k << 24);
         }
         __syncthreads();
@@ -992,7 +1073,7 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A) {
             A.segs[(size_t)ti * B + b] = G;
             s_nz[b] = s_gruns[b] = s_aux[b] = 0;
         }
-        for (uint32_t i = tid; i < kNBlk * B; i += kCB) S.hc[i] = 0;
+        for (uint32_t i = tid; i < kNBlk * B / 4; i += kCB) ((uint4*)S.hc)[i] = make_uint4(0, 0, 0, 0);
         __syncthreads();
     }
     if (cur_tensor != 0xffffffffu) {
@@ -2140,12 +2221,39 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
     return encode_record_ex(e, base, target, quality, 0, 0, nullptr, 0, nullptr);
 }
 
+bool fused_c_enabled() {  // read per step: tests toggle it inside one process
+    return getenv("DQTG_NO_FUSED_C") == nullptr && getenv("DQTG_DENSE_DELTA") == nullptr;
+}
+
+std::unique_ptr<Record> compress_step(Engine& e, const DevCkpt& c, const dqtg_config& cfg,
+                                      uint64_t seed, uint64_t step, const QState* base,
+                                      double quality, std::unique_ptr<QState>& state_out,
+                                      const std::function<void(QState*)>& on_levels) {
+    // the fused encoder needs the sparse DELTA path with the byte codec: a base, and
+    // an alphabet the shared-memory codec holds (checked again by encode_record_ex)
+    const uint32_t kt = std::max(cfg.bins, cfg.embed_bins) + 2;
+    bool fuse = base && fused_c_enabled() && std::max(base->max_levels(), kt) <= (uint32_t)kMaxB;
+    FuseC fc;
+    state_out = quantize(e, c, cfg, seed, step, fuse ? &fc : nullptr);
+    QState* q = state_out.get();
+    if (fuse && !fc.w) {  // nothing deferred (no elements): levels are already set
+        fuse = false;
+    }
+    if (!fuse) {
+        if (on_levels) on_levels(q);
+        return encode_record(e, base, *q, quality);
+    }
+    return encode_record_ex(e, base, *q, quality, 0, 0, nullptr, 0, nullptr, &fc,
+                            [&] { if (on_levels) on_levels(q); });
+}
+
 // B_override / nt_total: a shard of a tensor-sharded checkpoint encodes its tensor
 // blocks with the global alphabet and writes the global tensor count, so the
 // bytes [body_offset, size-4) of every rank concatenate into the single-GPU record.
 std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QState& target,
                                          double quality, uint32_t B_override, uint32_t nt_total,
-                                         uint64_t* body_offset, int mode, uint64_t* payload_total) {
+                                         uint64_t* body_offset, int mode, uint64_t* payload_total,
+                                         const FuseC* fc, const std::function<void()>& on_levels) {
     const Layout& L = *target.L;
     for (uint32_t i = 0; i < L.nt; ++i)  // 32-bit run lengths / symbol counts on the device
         DQTG_REQUIRE(L.numel[i] < (1ull << 31), DQTG_ERROR,
@@ -2283,17 +2391,33 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
         // DELTA records: the sparse formulation (work on the non-zero deltas only);
         // FULL records (every delta non-zero) and the ablation modes: dense ranks
         const bool sparse = base && mode == 0 && !getenv("DQTG_DENSE_DELTA");
-        auto kfn = sparse ? enc_tile_delta_kernel
+        if (fc) {
+            FuseC* m = const_cast<FuseC*>(fc);
+            m->levels = target.d_levels;
+            m->ppos = target.d_ppos;
+            m->pval = target.d_pval;
+        }
+        DQTG_REQUIRE(!fc || sparse, DQTG_ERROR, "fused pass C needs the sparse DELTA encoder");
+        void (*dfn)(EncArgs, FuseC) = fc ? enc_tile_delta_kernel<true> : enc_tile_delta_kernel<false>;
+        auto kfn = sparse ? (void (*)(EncArgs))nullptr
                  : base ? (B <= 63 ? enc_tile_kernel<true, 6> : enc_tile_kernel<true, 7>)
                         : (B <= 63 ? enc_tile_kernel<false, 6> : enc_tile_kernel<false, 7>);
+        const void* kptr = sparse ? (const void*)dfn : (const void*)kfn;
         const size_t smem = sparse ? dsm_bytes(B, NS) : e1_smem;
-        ensure_dyn_smem((const void*)kfn, smem);
-        DQTG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        ensure_dyn_smem(kptr, smem);
+        DQTG_CUDA(cudaFuncSetAttribute(kptr, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         int per_sm = 0;
-        DQTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kCB, smem));
+        DQTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kptr, kCB, smem));
         const int grid = std::max(1, std::min(ntiles, e.num_sms * std::max(1, per_sm)));
         if (sparse) A.zs = (uint32_t*)e.buf("e.zs", (size_t)grid * kTile * 4);
-        { DQTG_SPAN(e, sparse ? "enc_tile_delta_kernel" : "enc_tile_kernel"); kfn<<<grid, kCB, smem, st>>>(A); }
+        if (sparse) {
+            FuseC F{};
+            if (fc) F = *fc;
+            { DQTG_SPAN(e, fc ? "quant_delta_kernel" : "enc_tile_delta_kernel"); dfn<<<grid, kCB, smem, st>>>(A, F); }
+        } else {
+            { DQTG_SPAN(e, "enc_tile_kernel"); kfn<<<grid, kCB, smem, st>>>(A); }
+        }
+        if (on_levels) on_levels();  // the target levels are complete after this point
         { DQTG_SPAN(e, "crc_tiles_kernel"); crc_tiles_kernel<<<std::max(1, std::min(e.num_sms * 2, (ntiles + 255) / 256)), 256, 0, st>>>(A.tile_crc, A.crc_shift, ntiles, A.crc_acc); }
         e.launched();
     }

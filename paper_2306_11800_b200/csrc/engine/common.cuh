@@ -50,6 +50,12 @@ inline uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 inline uint64_t ceil_div(uint64_t x, uint64_t a) { return (x + a - 1) / a; }
 
 // ---- device helpers ------------------------------------------------------
+__device__ __forceinline__ uint16_t bf16_rne(float v) {  // quantize.cpp:337-342
+    uint32_t bits = __float_as_uint(v);
+    bits += 0x7fffu + ((bits >> 16) & 1u);
+    return (uint16_t)(bits >> 16);
+}
+
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
 template <typename T>

@@ -4,6 +4,7 @@
 
 #include <atomic>
 #include <map>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -286,11 +287,33 @@ struct KSpan {
 };
 #define DQTG_SPAN(e, name) ::dqtg::KSpan dqtg_span_##__LINE__((e), (name))
 
+// Fused pass C (codec.cu enc_tile_delta_kernel<true>): quantize(..., defer) stops
+// before pass C and hands its inputs here; encode_record_ex then computes the target
+// levels inside the DELTA tile pass (written to target.d_levels once, never re-read).
+struct LtParams;
+struct FuseC {
+    const float* w = nullptr;
+    const uint8_t* parts = nullptr;                     // 2 bits per element, element order
+    const float* lb = nullptr;                          // [7][lb_stride] level boundaries
+    int lb_stride = 0;
+    const uint32_t* cb_len = nullptr;                   // [7] (device)
+    const unsigned long long* tile_prot_off = nullptr;  // first protected entry per tile
+    uint16_t* levels = nullptr;                         // out: target levels
+    uint64_t* ppos = nullptr;
+    uint16_t* pval = nullptr;
+    const LtParams* lp = nullptr;                       // [7] partition parameters (pass C kernel)
+};
+void run_pass_c(Engine& e, const DevCkpt& c, const FuseC& f, QState& q);
+// whether compress_step may fuse pass C into the DELTA encoder (sparse encoder, B <= 64)
+bool fused_c_enabled();
+
 // ---- pipeline entry points implemented across the .cu files ---------------
 void sketch_build(Engine& e, const float* x_any, uint64_t n, double alpha, uint64_t* zero,
                   uint64_t* pos, uint64_t* neg);
+// defer: pass C is not run; its inputs go to *defer (levels / protected entries of the
+// returned state are written by the fused encoder, encode_record_ex(..., defer))
 std::unique_ptr<QState> quantize(Engine& e, const DevCkpt& c, const dqtg_config& cfg,
-                                 uint64_t seed, uint64_t step);
+                                 uint64_t seed, uint64_t step, FuseC* defer = nullptr);
 std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QState& target,
                                       double quality);
 std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
@@ -312,7 +335,15 @@ std::unique_ptr<QState> shard_stage3(Engine& e, const DevCkpt& c, const dqtg_con
 std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QState& target,
                                          double quality, uint32_t B_override, uint32_t nt_total,
                                          uint64_t* body_offset, int mode = 0,
-                                         uint64_t* payload_total = nullptr);
+                                         uint64_t* payload_total = nullptr,
+                                         const FuseC* fc = nullptr,
+                                         const std::function<void()>& on_levels = {});
+// quantize + encode_delta_record against base (Chain::append): pass C fused into the
+// DELTA encoder when possible; on_levels runs once the target levels are enqueued
+std::unique_ptr<Record> compress_step(Engine& e, const DevCkpt& c, const dqtg_config& cfg,
+                                      uint64_t seed, uint64_t step, const QState* base,
+                                      double quality, std::unique_ptr<QState>& state_out,
+                                      const std::function<void(QState*)>& on_levels = {});
 void eval_batch(Engine& e, const DevCkpt& c, const dqtg_config* cfgs, const uint64_t* seeds,
                 uint32_t m, double* quality, double* est);
 void approx_kmeans(Engine& e, const float* values_any, uint64_t n, uint32_t k, double sigma,

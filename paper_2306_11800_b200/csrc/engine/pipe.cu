@@ -250,28 +250,68 @@ dqtg_status dqtg_pipe_run(dqtg_pipe* p, const dqtg_layout* layout, const float* 
                     }
                     if (trace) t_u[k] = now_ms();
                     dqtg_comm* cm = p->comms.empty() ? nullptr : p->comms[w];
-                    auto q = cm ? sharded_quantize(e, cm, c, *cfg, seed, steps ? steps[k] : k)
-                                : quantize(e, c, *cfg, seed, steps ? steps[k] : k);
-                    if (trace) t_q[k] = now_ms();
-                    DQTG_CUDA(cudaEventRecord(R.qev[k], e.stream));
-                    const QState* target = q.get();
-                    const QState* prev = base ? base->q.get() : nullptr;
-                    {
-                        std::unique_lock<std::mutex> g(R.mu);
+                    const uint64_t sk = steps ? steps[k] : k;
+                    // publish state k (its levels are enqueued on this stream)
+                    auto publish = [&](std::unique_ptr<QState> q) {
+                        DQTG_CUDA(cudaEventRecord(R.qev[k], e.stream));
+                        std::lock_guard<std::mutex> g(R.mu);
                         R.states[k] = std::move(q);
                         R.ready[k] = 1;
                         R.cv.notify_all();
-                        if (k > 0) {
-                            R.cv.wait(g, [&] { return R.failed || R.ready[k - 1]; });
-                            if (R.failed) return;
-                            prev = R.states[k - 1].get();
+                    };
+                    // state k-1 (the delta base): wait until it is published
+                    auto wait_prev = [&]() -> const QState* {
+                        if (k == 0) return base ? base->q.get() : nullptr;
+                        std::unique_lock<std::mutex> g(R.mu);
+                        R.cv.wait(g, [&] { return R.failed || R.ready[k - 1]; });
+                        if (R.failed) return nullptr;
+                        return R.states[k - 1].get();
+                    };
+                    dqtg_record rec;
+                    if (cm) {
+                        auto q = sharded_quantize(e, cm, c, *cfg, seed, sk);
+                        if (trace) t_q[k] = now_ms();
+                        const QState* target = q.get();
+                        publish(std::move(q));
+                        const QState* prev = wait_prev();
+                        if (k > 0 && !prev) return;
+                        if (k > 0) DQTG_CUDA(cudaStreamWaitEvent(e.stream, R.qev[k - 1], 0));
+                        if (trace) t_w[k] = now_ms();
+                        rec.r = sharded_encode(e, cm, prev, *target, quality, p->nt_total);
+                    } else {
+                        // quantize + encode with pass C fused into the DELTA encoder: the
+                        // state is published once its levels are enqueued (mid-encode), and
+                        // the base must be published before this step's encode starts
+                        const QState* prev = nullptr;
+                        bool have_prev = false;
+                        std::unique_ptr<QState> q;
+                        const uint32_t kt = std::max(cfg->bins, cfg->embed_bins) + 2;
+                        const bool fuse = (k > 0 || base) && fused_c_enabled() && kt <= 64;
+                        FuseC fc;
+                        q = quantize(e, c, *cfg, seed, sk, fuse ? &fc : nullptr);
+                        if (trace) t_q[k] = now_ms();
+                        QState* target = q.get();
+                        if (!fuse || !fc.w) {
+                            publish(std::move(q));
+                            q.reset();
+                        }
+                        prev = wait_prev();
+                        have_prev = prev != nullptr;
+                        if (k > 0 && !have_prev) return;
+                        if (k > 0) DQTG_CUDA(cudaStreamWaitEvent(e.stream, R.qev[k - 1], 0));
+                        if (trace) t_w[k] = now_ms();
+                        if (q && prev && prev->max_levels() <= 64) {
+                            QState* tq = q.get();
+                            rec.r = encode_record_ex(e, prev, *tq, quality, 0, 0, nullptr, 0, nullptr, &fc,
+                                                     [&] { publish(std::move(q)); });
+                        } else {
+                            if (q) {  // could not fuse after all: pass C, then publish
+                                run_pass_c(e, c, fc, *target);
+                                publish(std::move(q));
+                            }
+                            rec.r = encode_record(e, prev, *target, quality);
                         }
                     }
-                    if (k > 0) DQTG_CUDA(cudaStreamWaitEvent(e.stream, R.qev[k - 1], 0));
-                    if (trace) t_w[k] = now_ms();
-                    dqtg_record rec;
-                    rec.r = cm ? sharded_encode(e, cm, prev, *target, quality, p->nt_total)
-                               : encode_record(e, prev, *target, quality);
                     if (trace) t_c[k] = now_ms();
                     if (on_record && rec.r) on_record(user, k, &rec);
                     rec.r.reset();

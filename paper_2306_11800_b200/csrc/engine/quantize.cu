@@ -25,7 +25,6 @@ namespace dqtg {
 
 constexpr int kPB = 256;  // threads per streaming CTA
 constexpr int kGrab = 8;  // tiles per dynamic grab of the persistent passes
-constexpr int kItTile = kTile / (kPB * 8);  // 8-element thread iterations per tile (2)
 constexpr int kPfDist = 148 * 5;  // pass C: about one wave of resident CTAs ahead
 
 // L2 prefetch of one tile's score inputs (w + EMA, or the explicit scores)
@@ -214,7 +213,7 @@ __global__ void __launch_bounds__(kPB, 6) pass_b_kernel(PassIn a, const LtParams
                                                      unsigned long long* gh_val,
                                                      uint32_t* tile_prot,
                                                      unsigned long long* tensor_prot,
-                                                     uint16_t* parts) {
+                                                     uint8_t* parts) {
     extern __shared__ uint32_t sh[];
     __shared__ uint32_t s_red[2][kPB / 32];  // by tile parity: warps may run ahead into the next tile
     uint32_t par = 0;
@@ -266,7 +265,10 @@ __global__ void __launch_bounds__(kPB, 6) pass_b_kernel(PassIn a, const LtParams
                 pw |= (uint32_t)part << (2 * j);
                 if (part == 0) hist_add(sh, gv, wa[j], a.tab, a.err);
             }
-            if (parts) parts[((size_t)ti * kItTile + itn) * kPB + threadIdx.x] = (uint16_t)pw;
+            if (parts) {  // one byte per float4 group, element order (2 bits per element)
+                parts[(T.start + i) >> 2] = (uint8_t)pw;
+                if (two) parts[(T.start + i2) >> 2] = (uint8_t)(pw >> 8);
+            }
         }
         np = warp_sum(np);
         if ((threadIdx.x & 31) == 0) s_red[par][threadIdx.x >> 5] = np;
@@ -303,7 +305,7 @@ struct FuseArgs {
     unsigned long long* gh_w;      // [7][HS] signed histogram of w
     unsigned long long* gh_sens;   // [7][HS]
     unsigned long long* prot;      // [7][HS] protected (guessed) values by signed slot
-    uint16_t* parts;
+    uint8_t* parts;                // 2 bits per element, element order
     uint32_t* tile_prot;
     unsigned long long* tensor_prot;
     unsigned long long* cand;      // (tile << 32) | element
@@ -421,7 +423,8 @@ __global__ void __launch_bounds__(kPB, 4) pass_ab_kernel(PassIn a, FuseArgs f) {
                     }
                 }
             }
-            f.parts[((size_t)ti * kItTile + itn) * kPB + threadIdx.x] = (uint16_t)pw;
+            f.parts[(T.start + i) >> 2] = (uint8_t)pw;
+            if (two) f.parts[(T.start + i2) >> 2] = (uint8_t)(pw >> 8);
         }
         np = warp_sum(np);
         if (lane == 0) s_red[par][threadIdx.x >> 5] = np;
@@ -517,12 +520,10 @@ __global__ void fixup_kernel(PassIn a, FuseArgs f, const LtParams* lp) {
         atomicAdd(f.prot + lt * a.HS + slot_of(w, a.tab), to_prot ? 1ull : ~0ull);
         atomicAdd(f.tile_prot + ti, to_prot ? 1u : ~0u);
         atomicAdd(f.tensor_prot + T.tensor, to_prot ? 1ull : ~0ull);
-        // 2-bit code of element o: iteration itn, thread, position j (pass B layout)
-        const uint32_t itn = o / (kPB * 8), r = o % (kPB * 8);
-        const uint32_t th = (r % (kPB * 4)) / 4, j = (r / (kPB * 4)) * 4 + (r & 3);
-        const size_t idx = ((size_t)ti * kItTile + itn) * kPB + th;
-        uint32_t* word = (uint32_t*)f.parts + (idx >> 1);
-        const uint32_t sh = 16 * (uint32_t)(idx & 1) + 2 * j;
+        // 2-bit code of element o (element-order layout, 16 codes per word)
+        const uint64_t idx = T.start + o;
+        uint32_t* word = (uint32_t*)f.parts + (idx >> 4);
+        const uint32_t sh = 2 * (uint32_t)(idx & 15);
         if (to_prot) atomicOr(word, 2u << sh);
         else atomicAnd(word, ~(3u << sh));
     }
@@ -632,12 +633,6 @@ __host__ __device__ __forceinline__ uint32_t pow2_ceil(uint32_t k) {
     return p;
 }
 
-__device__ __forceinline__ uint16_t bf16_rne(float v) {  // quantize.cpp:337-342
-    uint32_t bits = __float_as_uint(v);
-    bits += 0x7fffu + ((bits >> 16) & 1u);
-    return (uint16_t)(bits >> 16);
-}
-
 template <int LOGP>
 __device__ __forceinline__ uint32_t level_fixed(const float* T, float v, uint32_t kp) {
     if (LOGP < 0) return level_of(T, kp, v);  // k > 64: runtime bisection
@@ -653,7 +648,7 @@ __device__ __forceinline__ void pass_c_tile(const PassIn& a, const LtParams& P, 
                                             uint32_t k, const float* s_lb, uint64_t tensor_base,
                                             unsigned long long out,
                                             unsigned long long* s_scan, uint16_t* levels,
-                                            uint64_t* ppos, uint16_t* pval, const uint16_t* parts,
+                                            uint64_t* ppos, uint16_t* pval, const uint8_t* parts,
                                             int ti) {
     // two float4 groups per thread and iteration; protected entries keep element
     // order: group 0 (i0..i0+1023) before group 1, one packed (lo|hi) scan
@@ -662,7 +657,11 @@ __device__ __forceinline__ void pass_c_tile(const PassIn& a, const LtParams& P, 
         uint32_t flags[2] = {0, 0};
         float wa[2][4];
         uint32_t pw = 0;
-        if (PARTS) pw = parts[((size_t)ti * kItTile + itn) * kPB + threadIdx.x];
+        if (PARTS) {
+            const uint32_t i = i0 + threadIdx.x * 4, i2 = i + kPB * 4;
+            if (i < T.count) pw = parts[(T.start + i) >> 2];
+            if (i2 < T.count) pw |= (uint32_t)parts[(T.start + i2) >> 2] << 8;
+        }
         for (int g = 0; g < 2; ++g) {
             const uint32_t i = i0 + g * kPB * 4 + threadIdx.x * 4;
             wa[g][0] = wa[g][1] = wa[g][2] = wa[g][3] = 0.0f;
@@ -715,7 +714,7 @@ __global__ void __launch_bounds__(kPB) pass_c_kernel(PassIn a, const LtParams* l
                                                      const uint32_t* cb_len,
                                                      const unsigned long long* tile_prot_off,
                                                      uint16_t* levels, uint64_t* ppos,
-                                                     uint16_t* pval, const uint16_t* parts) {
+                                                     uint16_t* pval, const uint8_t* parts) {
     extern __shared__ float s_lb[];
     __shared__ unsigned long long s_scan[33];
     const int ti = blockIdx.x;
@@ -1135,7 +1134,7 @@ struct Stage {
     uint32_t* cb_len = nullptr;
     float* d_lb = nullptr;  // [7][lb_stride] level boundaries (level_bounds_kernel)
     uint32_t lb_stride = 1;
-    uint16_t* parts = nullptr;  // pass B partition, 2 bits per element (read by pass C)
+    uint8_t* parts = nullptr;  // pass B partition, 2 bits per element in element order (pass C)
 };
 
 static void stage_alloc(Engine& e, const Layout& L, int64_t HS, Stage& s, float* cb_dst) {
@@ -1154,7 +1153,7 @@ static void stage_alloc(Engine& e, const Layout& L, int64_t HS, Stage& s, float*
     s.cb_stride = std::max(1u, std::max(s.cfg.bins, s.cfg.embed_bins));
     s.d_cb = cb_dst ? cb_dst : (float*)e.buf(t + "cb", (size_t)kLayerTypes * s.cb_stride * 4);
     s.lb_stride = pow2_ceil(s.cb_stride);
-    s.parts = (uint16_t*)e.buf(t + "parts", (size_t)ntiles * kItTile * kPB * 2 + 16);
+    s.parts = (uint8_t*)e.buf(t + "parts", (size_t)L.Np / 4 + 16);
     s.d_lb = (float*)e.buf(t + "lb", (size_t)kLayerTypes * s.lb_stride * 4);
 }
 
@@ -1374,8 +1373,26 @@ static void stage_pass_c(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s,
     DQTG_CUDA(cudaGetLastError());
 }
 
+// Pass C of a deferred quantize (FuseC) as its own kernel, for a caller that could
+// not fuse it after all.
+void run_pass_c(Engine& e, const DevCkpt& c, const FuseC& f, QState& q) {
+    const Layout& L = *c.L;
+    PassIn a{};
+    a.tiles = L.d_tiles;
+    a.ntiles = (int)L.tiles.size();
+    a.types = L.d_types;
+    a.tensor_off = L.d_off;
+    a.w = f.w;
+    a.err = e.d_err;
+    if (!a.ntiles) return;
+    const size_t smem = (size_t)f.lb_stride * 4 + 16;
+    { DQTG_SPAN(e, "pass_c_kernel"); pass_c_kernel<false, true><<<a.ntiles, kPB, smem, e.stream>>>(a, f.lp, f.lb, f.lb_stride, f.cb_len, f.tile_prot_off, q.d_levels, q.d_ppos, q.d_pval, f.parts); }
+    e.launched();
+    DQTG_CUDA(cudaGetLastError());
+}
+
 std::unique_ptr<QState> quantize(Engine& e, const DevCkpt& c, const dqtg_config& cfg,
-                                 uint64_t seed, uint64_t step) {
+                                 uint64_t seed, uint64_t step, FuseC* defer) {
     const Layout& L = *c.L;
     Stage s;
     s.tag = "q.";
@@ -1437,7 +1454,18 @@ std::unique_ptr<QState> quantize(Engine& e, const DevCkpt& c, const dqtg_config&
     q->prot_total = acc;
     q->d_ppos = (decltype(q->d_ppos))e.dalloc((acc + 1) * 8);
     q->d_pval = (decltype(q->d_pval))e.dalloc((acc + 1) * 2);
-    stage_pass_c(e, c, a, s, *q);
+    if (defer) {  // pass C runs inside the DELTA encoder (codec.cu, FuseC)
+        stage_level_bounds(e, s);
+        defer->w = c.w;
+        defer->parts = s.parts;
+        defer->lb = s.d_lb;
+        defer->lb_stride = (int)s.lb_stride;
+        defer->cb_len = s.cb_len;
+        defer->tile_prot_off = s.tile_off;
+        defer->lp = s.d_lp;
+    } else {
+        stage_pass_c(e, c, a, s, *q);
+    }
     std::vector<float> hcb((size_t)kLayerTypes * q->cb_stride);
     e.d2h(q->cb_len, s.cb_len, sizeof(q->cb_len));
     e.d2h(hcb.data(), q->d_cb, hcb.size() * 4);

@@ -512,6 +512,18 @@ class Engine:
         finally:
             LIB.dqtg_record_destroy(r)
 
+    @staticmethod
+    def record_bytes(r, destroy=True) -> bytes:
+        """Bytes of a record handle (dqtg_record_copy); destroys the handle by default."""
+        try:
+            n = LIB.dqtg_record_size(r)
+            out = np.empty(n, np.uint8)
+            _check(LIB.dqtg_record_copy(r, out.ctypes.data))
+            return out.tobytes()
+        finally:
+            if destroy:
+                LIB.dqtg_record_destroy(r)
+
     def payload_bytes(self, base: DevState, target: DevState, variant=0) -> int:
         """payload_bytes_pe (0) / _rle (1) / _he (2) (codec.cpp:615-646) on the device."""
         n = C.c_uint64()

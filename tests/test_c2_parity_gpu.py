@@ -91,3 +91,20 @@ def test_c2_records_match_reference(ref, tmp_path):
         want = ref.qstate(ref_states[t])
         for i in range(len(names)):
             assert np.array_equal(got.levels[i], want.levels[i]), (t, names[i])
+
+    # Chain::append through dqtg_compress_step: pass C fused into the DELTA encoder
+    # (the levels are computed in the encoder's tile pass and never re-read)
+    for t, b in pairs[1:]:
+        ck = E.DevCheckpoint(eng, names, types, shapes)
+        ck.set_weights(W.tensor_ptrs(snaps[t].data_ptr(), layout))
+        ck.set_ema(W.tensor_ptrs(ema.data_ptr(), layout))
+        st, rh = eng.compress_step(ck, cfg, 1, t, base=dev_states[b])
+        ours = eng.record_bytes(rh)
+        theirs = bytes(d.encode_delta_record(ref_states[t], ref_states[b]))
+        assert ours == theirs, ("compress_step", t)
+        got = st.download()
+        want = ref.qstate(ref_states[t])
+        for i, name in enumerate(names):
+            assert np.array_equal(got.levels[i], want.levels[i]), ("compress_step", t, name)
+            assert np.array_equal(got.prot_pos[i], want.prot_pos[i]), ("compress_step", t, name)
+            assert np.array_equal(got.prot_val[i], want.prot_val[i]), ("compress_step", t, name)
