@@ -124,8 +124,10 @@ __device__ __forceinline__ double seq_prefix(const double* v, int a, int n, doub
 }
 
 // quantize.cpp:116-131: sequential prefix of prob (lane 0), binary search for the
-// first positive entry whose running sum reaches r.
-__device__ int kpp_pick(const double* prob, double* pref, int n, int from, KShared& sm) {
+// first positive entry whose running sum reaches r.  u >= 0: the uniform draw was
+// already taken (by kpp_pick_par, whose certificate failed).
+__device__ int kpp_pick(const double* prob, double* pref, int n, int from, KShared& sm,
+                        double u = -1.0) {
     if (threadIdx.x == 0) {
         // pref[0..from) are unchanged from the previous pick (same terms, same order)
         double s = from > 0 ? pref[from - 1] : 0.0;
@@ -135,7 +137,7 @@ __device__ int kpp_pick(const double* prob, double* pref, int n, int from, KShar
         if (!(s > 0.0)) {
             res = n;
         } else {
-            double r = __dmul_rn(uniform01(sm.rng), s);
+            double r = __dmul_rn(u >= 0.0 ? u : uniform01(sm.rng), s);
             int lo = 0, hi = n;
             while (lo < hi) {
                 int mid = (lo + hi) >> 1;
@@ -157,6 +159,96 @@ __device__ int kpp_pick(const double* prob, double* pref, int n, int from, KShar
     return sm.pick;
 }
 
+// Block-wide exclusive scan of one double per thread; *total = block sum.
+__device__ double block_exscan_d(double v, double* slots /* kKB / 32 */, double* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = __dadd_rn(x, y);
+    }
+    if (lane == 31) slots[wid] = x;
+    __syncthreads();
+    double base = 0.0, tot = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        const double s = slots[w];
+        if (w < wid) base = __dadd_rn(base, s);
+        tot = __dadd_rn(tot, s);
+    }
+    *total = tot;
+    __syncthreads();  // slots reusable
+    return __dadd_rn(base, __dsub_rn(x, v)) ;
+}
+
+// The same pick from a parallel prefix with a rounding certificate.  Every thread
+// sums a contiguous chunk of prob, the chunk sums are scanned, and the crossing of
+// r is searched in the parallel prefix P.  The reference's sequential prefix s_i
+// and P_i both lie within eps * P_i of the exact prefix (non-negative terms: any
+// summation order of m terms errs by at most (m - 1) u times their sum), and its
+// r = fl(u * s_n) lies in [r_lo, r_hi]; the crossing index i is accepted only when
+// s_{i-1} < r <= s_i holds for every admissible value (P_{i-1} (1 + eps) < r_lo,
+// P_i (1 - eps) >= r_hi) -- the reference's index then provably equals i.  Returns
+// -1 when the certificate fails (the caller runs kpp_pick with the same draw,
+// passed back in *u_out), n when the total is zero (no draw, as the reference).
+__device__ int kpp_pick_par(const double* prob, int n, KShared& sm, double* u_out) {
+    __shared__ double s_slots[kKB / 32];
+    __shared__ double s_r[4];  // r_mid, r_lo, r_hi, u
+    __shared__ int s_idx;
+    __shared__ double s_pp[2];
+    const int nt = blockDim.x, tid = threadIdx.x;
+    const int C = (n + nt - 1) / nt;
+    const int a = min(n, tid * C), b = min(n, a + C);
+    double loc = 0.0;
+    for (int i = a; i < b; ++i) loc = __dadd_rn(loc, prob[i]);
+    double T;
+    const double base = block_exscan_d(loc, s_slots, &T);
+    const double eps = 4.0 * (double)(n + 64) * 0x1.0p-53;
+    if (tid == 0) {
+        s_idx = 0x7fffffff;
+        if (T > 0.0) {
+            const double u = uniform01(sm.rng);
+            const double tlo = __dmul_rd(T, __dsub_rd(1.0, eps)), thi = __dmul_ru(T, __dadd_ru(1.0, eps));
+            s_r[0] = __dmul_rn(u, T);
+            s_r[1] = __dmul_rd(u, tlo);
+            s_r[2] = __dmul_ru(u, thi);
+            s_r[3] = u;
+        }
+    }
+    __syncthreads();
+    if (!(T > 0.0)) return n;  // uniform across the block: T is the same everywhere
+    const double rm = s_r[0];
+    double run = base;
+    int hit = -1;
+    double pp = 0.0, pc = 0.0;
+    for (int i = a; i < b; ++i) {
+        const double nx = __dadd_rn(run, prob[i]);
+        if (nx >= rm) {
+            hit = i, pp = run, pc = nx;
+            break;
+        }
+        run = nx;
+    }
+    if (hit >= 0) atomicMin(&s_idx, hit);
+    __syncthreads();
+    if (hit >= 0 && hit == s_idx) s_pp[0] = pp, s_pp[1] = pc;
+    __syncthreads();
+    if (tid == 0) {
+        int res = -1;
+        if (s_idx != 0x7fffffff) {
+            const bool below = __dmul_ru(s_pp[0], __dadd_ru(1.0, eps)) < s_r[1];
+            const bool above = __dmul_rd(s_pp[1], __dsub_rd(1.0, eps)) >= s_r[2];
+            if (below && above) res = s_idx;
+        }
+        sm.pick = res;
+    }
+    __syncthreads();
+    const int res = sm.pick;
+    if (res < 0) *u_out = s_r[3];
+    __syncthreads();
+    return res;
+}
+
 __device__ double block_max_d(double v, KShared& sm) {
     for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
     if ((threadIdx.x & 31) == 0) sm.red[threadIdx.x >> 5] = v;
@@ -174,17 +266,19 @@ __device__ double block_max_d(double v, KShared& sm) {
 
 // weighted_kmeanspp_init (quantize.cpp:94-164).
 __device__ void kpp_init(const double* pts, const double* w, int n, int k, double* d2,
-                         double* prob, double* pref, double* chosen, KShared& sm) {
-    __shared__ int s_from;
+                         double* prob, double* pref, double* chosen, KShared& sm,
+                         bool certify = true) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         d2[i] = __longlong_as_double(0x7ff0000000000000LL);
         prob[i] = w[i];
     }
-    if (threadIdx.x == 0) s_from = 0;
     __syncthreads();
     int nc = 0;
     while (nc < k) {
-        int next = kpp_pick(prob, pref, n, s_from, sm);
+        // parallel pick with a certificate; the sequential one when it fails (rare)
+        double u = -1.0;
+        int next = certify && n >= 64 ? kpp_pick_par(prob, n, sm, &u) : -1;
+        if (next < 0) next = kpp_pick(prob, pref, n, 0, sm, u);
         if (threadIdx.x == 0) {
             bool taken = false;
             if (next != n)
@@ -200,14 +294,11 @@ __device__ void kpp_init(const double* pts, const double* w, int n, int k, doubl
                 }
             }
             chosen[nc] = pts[next];
-            // the first pick used prob = w: every prob entry changes on the next pick
-            s_from = nc == 0 ? 0 : n;
         }
         __syncthreads();
         const double v = chosen[nc];
         const bool first = nc == 0;
         ++nc;
-        int lo = n;
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             double dd = __dsub_rn(pts[i], v);
             double sq = __dmul_rn(dd, dd);
@@ -215,14 +306,9 @@ __device__ void kpp_init(const double* pts, const double* w, int n, int k, doubl
             if (sq < cur || first) {  // std::min(d2, d*d)
                 cur = sq < cur ? sq : cur;
                 d2[i] = cur;
-                double pn = __dmul_rn(w[i], cur);
-                if (first || pn != prob[i] || __double_as_longlong(pn) != __double_as_longlong(prob[i])) {
-                    prob[i] = pn;
-                    lo = min(lo, i);
-                }
+                prob[i] = __dmul_rn(w[i], cur);
             }
         }
-        if (lo < n) atomicMin(&s_from, lo);
         __syncthreads();
     }
     if (threadIdx.x == 0) IntroSort<double, LessD>{}.sort(chosen, k);
@@ -275,24 +361,210 @@ __device__ __forceinline__ void chain_sums(const double2* wx, const double* w, c
     }
 }
 
+// ---- certified Lloyd steps ------------------------------------------------------
+// The reference's cluster sums (quantize.cpp:200-205) are sequential fp64 chains, one
+// per cluster -- at C2 the cluster of the many near-zero keys is ~1100 keys long,
+// and ~40 iterations of that chain were the whole k-means time.  A certified step
+// sums every cluster in parallel instead and carries each centre as an interval
+// [lo, hi] that provably contains the reference's value (any summation order of m
+// terms errs by at most (m - 1) u sum|t|, so the sequential and the parallel sums
+// differ by at most 2 (m - 1) u sum|t|; the quotient is bounded with directed
+// rounding).  The step's decisions are accepted only when they hold for every value
+// in the intervals:
+//   * well-separated ascending centres (the contiguous-cluster condition),
+//   * every cluster boundary: the first key with |x - c[j+1]| < |x - c[j]| is
+//     monotone in both centres, so equal boundaries at the lower and the upper
+//     interval ends fix it,
+//   * no empty cluster, and the movement test (max |next - c| <= tol * scale).
+// The clusters of a certified step are then exactly the reference's, so the next
+// step's sums are over the same keys -- the interval does not compound.  When a
+// decision is not certain, the centres are made exact from the previous step's
+// clusters with the reference's sequential chains and the step runs exactly; the
+// final centres are always made exact the same way.
+struct LAux {
+    double *lo, *hi, *nlo, *nhi, *sw, *swx, *sax;
+    int *pf, *pl;  // clusters (first, last key) that produced the current intervals
+    int exact;     // lo == hi == c are the reference's values
+};
+
+// exact centres from the sequential chains over clusters [f[j], l[j]] (warp 0)
+__device__ void lloyd_exact_from(const double* pts, const double* w, const int* f, const int* l,
+                                 int k, double* c, KShared& sm) {
+    if ((threadIdx.x >> 5) == 0)
+        for (int j = threadIdx.x & 31; j < k; j += 32) {
+            double ws = 0.0, wxs = 0.0;
+            chain_sums(sm.wx, w, pts, f[j], l[j], ws, wxs);
+            c[j] = __ddiv_rn(wxs, ws);
+        }
+}
+
+// first key (exclusive end of cluster j) with |x - b| < |x - a|
+__device__ __forceinline__ int lloyd_boundary(const double* pts, int n, double a, double b) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const double x = pts[mid];
+        if (fabs(__dsub_rn(x, b)) < fabs(__dsub_rn(x, a))) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
+// One certified step.  Returns 0: converged, 1: continue (centres <- next
+// intervals), 2: not certain (nothing changed; run the exact step).
+__device__ int lloyd_interval_step(const double* pts, const double* w, int n, LAux& X,
+                                   int* first, int* last, int* cnt, int k, double gap, double thr,
+                                   KShared& sm) {
+    __shared__ int s_res;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (wid == 0) {
+        bool ok = true;
+        for (int j = lane; j + 1 < k; j += 32) ok &= __dsub_rn(X.lo[j + 1], X.hi[j]) > gap;
+        ok = __all_sync(0xffffffffu, ok);
+        if (ok) {
+            for (int j = lane; j < k; j += 32) {
+                int e = n;
+                if (j + 1 < k) {
+                    e = lloyd_boundary(pts, n, X.lo[j], X.lo[j + 1]);
+                    if (!X.exact && lloyd_boundary(pts, n, X.hi[j], X.hi[j + 1]) != e) ok = false;
+                }
+                last[j] = e;  // exclusive end
+            }
+            __syncwarp();
+            for (int j = lane; j < k; j += 32) first[j] = j ? last[j - 1] : 0;
+            __syncwarp();
+            for (int j = lane; j < k; j += 32) {
+                cnt[j] = last[j] - first[j];
+                ok &= cnt[j] > 0;  // an empty cluster: the exact step reseeds it
+            }
+            ok = __all_sync(0xffffffffu, ok);
+        }
+        if (lane == 0) s_res = ok ? 1 : 2;
+    }
+    __syncthreads();
+    if (s_res == 2) {
+        __syncthreads();
+        return 2;
+    }
+    // parallel cluster sums: one warp per cluster, lanes stride over its keys, then a
+    // shuffle reduction (any order: the bound above covers every order)
+    for (int j = wid; j < k; j += (int)(blockDim.x >> 5)) {
+        double ws = 0.0, wxs = 0.0, ax = 0.0;
+        const int e = last[j];
+        for (int i = first[j] + lane; i < e; i += 32) {
+            const double wi = w[i], tt = __dmul_rn(wi, pts[i]);
+            ws = __dadd_rn(ws, wi);
+            wxs = __dadd_rn(wxs, tt);
+            ax = __dadd_rn(ax, fabs(tt));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            ws = __dadd_rn(ws, __shfl_xor_sync(0xffffffffu, ws, o));
+            wxs = __dadd_rn(wxs, __shfl_xor_sync(0xffffffffu, wxs, o));
+            ax = __dadd_rn(ax, __shfl_xor_sync(0xffffffffu, ax, o));
+        }
+        if (lane == 0) X.sw[j] = ws, X.swx[j] = wxs, X.sax[j] = ax;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        bool ok = true;
+        double U = 0.0, L = 0.0;
+        for (int j = lane; j < k; j += 32) {
+            const double ws = X.sw[j];
+            if (!(ws > 0.0)) {  // all weights zero: an empty cluster
+                ok = false;
+                continue;
+            }
+            const double e = 4.0 * (double)(cnt[j] + 16) * 0x1.0p-53;
+            const double e2 = __dmul_ru(e, 1.0 + 0x1.0p-20);
+            const double wsl = __dmul_rd(ws, __dsub_rd(1.0, e)), wsh = __dmul_ru(ws, __dadd_ru(1.0, e));
+            const double d = __dmul_ru(e2, X.sax[j]);
+            const double wxl = __dsub_rd(X.swx[j], d), wxh = __dadd_ru(X.swx[j], d);
+            double ql, qh;
+            if (wxl >= 0.0) ql = __ddiv_rd(wxl, wsh), qh = __ddiv_ru(wxh, wsl);
+            else if (wxh <= 0.0) ql = __ddiv_rd(wxl, wsl), qh = __ddiv_ru(wxh, wsh);
+            else ql = __ddiv_rd(wxl, wsl), qh = __ddiv_ru(wxh, wsl);
+            X.nlo[j] = ql;
+            X.nhi[j] = qh;
+            // movement bounds of |next - c|
+            const double dh = __dsub_ru(qh, X.lo[j]), dl = __dsub_rd(ql, X.hi[j]);
+            U = fmax(U, fmax(fabs(dh), fabs(dl)));
+            if (dl > 0.0) L = fmax(L, dl);
+            else if (dh < 0.0) L = fmax(L, -dh);
+        }
+        ok = __all_sync(0xffffffffu, ok);
+        for (int o = 16; o > 0; o >>= 1) {
+            U = fmax(U, __shfl_xor_sync(0xffffffffu, U, o));
+            L = fmax(L, __shfl_xor_sync(0xffffffffu, L, o));
+        }
+        int res = 2;
+        if (ok) {
+            if (U <= thr) res = 0;
+            else if (L > thr) res = 1;
+        }
+        if (res != 2) {
+            for (int j = lane; j < k; j += 32) {
+                X.lo[j] = X.nlo[j];
+                X.hi[j] = X.nhi[j];
+                X.pf[j] = first[j];
+                X.pl[j] = last[j] - 1;
+            }
+        }
+        if (lane == 0) {
+            s_res = res;
+            if (res != 2) X.exact = 0;
+        }
+    }
+    __syncthreads();
+    const int r = s_res;
+    __syncthreads();
+    return r;
+}
+
 // weighted_lloyd (quantize.cpp:180-254); c (k centres) is updated in place.
-// Iterations whose centres are strictly ascending and well separated (the fast
+// With aux (LAux, 7k doubles + 2k ints), steps are certified interval steps
+// whenever their decisions are certain (above); the others run exactly:
+// iterations whose centres are strictly ascending and well separated (the fast
 // path: clusters are contiguous key ranges) run on warp 0 alone with warp
 // primitives, one lane per cluster chain.  The general assignment and the
 // empty-cluster reseed use the whole block.
 __device__ int lloyd_block(const double* pts, const double* w, int n, double* c, double* nx,
                            int* first, int* last, int* cnt, int k, double tol, int max_iter,
                            int* assign, double* score, ScoreVal* top, bool distinct,
-                           KShared& sm) {
+                           KShared& sm, double* aux = nullptr) {
     __shared__ int s_fast;
+    __shared__ LAux X;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double lm = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) lm = fmax(lm, fabs(pts[i]));
     double scale = block_max_d(lm, sm);
     if (scale == 0.0) scale = 1.0;
     const double gap = __dmul_rn(scale, 0x1.0p-40);
+    const double thr = __dmul_rn(tol, scale);
+    if (aux && threadIdx.x == 0) {
+        X.lo = aux, X.hi = aux + k, X.nlo = aux + 2 * k, X.nhi = aux + 3 * k;
+        X.sw = aux + 4 * k, X.swx = aux + 5 * k, X.sax = aux + 6 * k;
+        X.pf = (int*)(aux + 7 * k), X.pl = X.pf + k;
+        X.exact = 1;
+    }
+    __syncthreads();
+    if (aux)
+        for (int j = threadIdx.x; j < k; j += blockDim.x) X.lo[j] = X.hi[j] = c[j];
+    __syncthreads();
     int iters = 0;
     for (int it = 0; it < max_iter; ++it) {
+        if (aux) {
+            const int r = lloyd_interval_step(pts, w, n, X, first, last, cnt, k, gap, thr, sm);
+            if (r != 2) {
+                iters = it + 1;
+                if (r == 0) break;
+                continue;
+            }
+            if (!X.exact) {  // the exact step needs the reference's centres
+                lloyd_exact_from(pts, w, X.pf, X.pl, k, c, sm);
+                __syncthreads();
+            }
+        }
         if (wid == 0) {
             // Fast path: strictly ascending centres separated by far more than the
             // rounding of any |x - c| (gap > scale * 2^-40).  The distance sequence
@@ -449,8 +721,18 @@ __device__ int lloyd_block(const double* pts, const double* w, int n, double* c,
             __syncthreads();
         }
         iters = it + 1;
+        if (aux) {  // c is exact after an exact step
+            __syncthreads();
+            for (int j = threadIdx.x; j < k; j += blockDim.x) X.lo[j] = X.hi[j] = c[j];
+            if (threadIdx.x == 0) X.exact = 1;
+        }
         if (sm.done) break;
         __syncthreads();  // sm.done / s_fast are rewritten by the next iteration
+    }
+    if (aux) {
+        __syncthreads();
+        if (!X.exact) lloyd_exact_from(pts, w, X.pf, X.pl, k, c, sm);
+        __syncthreads();
     }
     if (threadIdx.x == 0) IntroSort<double, LessD>{}.sort(c, k);
     __syncthreads();
@@ -485,7 +767,7 @@ __device__ double sq_loss_block(const double* pts, const double* w, int n, const
 // optional phase timing per CTA (DQTG_KM_TIMING=1): clocks of kpp / lloyd / loss, iterations, n
 
 __global__ void __launch_bounds__(kKB) kmeans_restarts_kernel(const KProblem* probs,
-                                                              int restarts, int smem_n) {
+                                                              int restarts, int smem_n, int certify) {
     extern __shared__ double dsm[];
     __shared__ KShared sm;
     const KProblem& P = probs[blockIdx.x / restarts];
@@ -497,7 +779,8 @@ __global__ void __launch_bounds__(kKB) kmeans_restarts_kernel(const KProblem* pr
     int* first = (int*)(nx + k);
     int* last = first + k;
     int* cnt = last + k;
-    double* base = dsm + 2 * k + (3 * k + 1) / 2 + 1;
+    double* aux = dsm + 2 * k + (3 * k + 1) / 2 + 1;  // LAux: 7k doubles + 2k ints
+    double* base = aux + 8 * k + 1;
     const double *pts = P.pts, *w = P.w;
     double *d2, *prob, *pref;
     int* assign;
@@ -529,9 +812,10 @@ __global__ void __launch_bounds__(kKB) kmeans_restarts_kernel(const KProblem* pr
     if (threadIdx.x == 0 && blockIdx.x < 1024) g_km_timing[blockIdx.x][6] = g_km_timing[blockIdx.x][7] = 0;
     __syncthreads();
     const long long c0 = clock64();
-    kpp_init(pts, w, n, k, d2, prob, pref, c, sm);
+    kpp_init(pts, w, n, k, d2, prob, pref, c, sm, certify);
     const long long c1 = clock64();
-    const int its = lloyd_block(pts, w, n, c, nx, first, last, cnt, k, 1e-6, 100, assign, pref, top, true, sm);
+    const int its = lloyd_block(pts, w, n, c, nx, first, last, cnt, k, 1e-6, 100, assign, pref, top, true, sm,
+                                certify ? aux : nullptr);
     const long long c2 = clock64();
     double loss = sq_loss_block(pts, w, n, c, k, prob, sm);
     if (threadIdx.x == 0 && blockIdx.x < 1024) {
@@ -593,18 +877,20 @@ void run_kmeans(Engine& e, std::vector<KProblem>& probs, float* cb_out, int cb_s
                               cudaMemcpyHostToDevice, e.stream));
     int maxn = 1;
     for (auto& p : probs) maxn = std::max(maxn, p.n);
-    const size_t head = ((size_t)2 * maxk + (3 * maxk + 1) / 2 + 1) * 8;
+    const size_t head = ((size_t)2 * maxk + (3 * maxk + 1) / 2 + 1 + 8 * maxk + 1) * 8;
     const size_t budget = 200 * 1024;
     int smem_n = (int)((budget - std::min(budget, head)) / 60);  // 5 doubles + pair + int per key
     size_t smem = head + (size_t)std::min(maxn, smem_n) * 60 + 96;
     ensure_dyn_smem((const void*)kmeans_restarts_kernel, smem);
+    // DQTG_KM_EXACT: every sum sequential (no certified parallel steps; tests compare)
+    const int certify = getenv("DQTG_KM_EXACT") ? 0 : 1;
     // restarts on the engine's high-priority side stream (fork/join with events)
     if (e.profiling || getenv("DQTG_NO_HI")) {
         DQTG_SPAN(e, "kmeans_restarts_kernel");
-        kmeans_restarts_kernel<<<(unsigned)(probs.size() * restarts), kKB, smem, e.stream>>>(dp, restarts, smem_n);
+        kmeans_restarts_kernel<<<(unsigned)(probs.size() * restarts), kKB, smem, e.stream>>>(dp, restarts, smem_n, certify);
     } else {
         cudaStream_t hs = e.hi();
-        kmeans_restarts_kernel<<<(unsigned)(probs.size() * restarts), kKB, smem, hs>>>(dp, restarts, smem_n);
+        kmeans_restarts_kernel<<<(unsigned)(probs.size() * restarts), kKB, smem, hs>>>(dp, restarts, smem_n, certify);
         e.hi_done();
     }
     { DQTG_SPAN(e, "kmeans_select_kernel"); kmeans_select_kernel<<<(unsigned)probs.size(), 32, 0, e.stream>>>(dp, restarts, cb_out,

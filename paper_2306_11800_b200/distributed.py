@@ -83,6 +83,31 @@ def assemble_record(prefix: bytes, bodies, crcs, stream_lens) -> bytes:
     return bytes(prefix) + b"".join(bytes(b) for b in bodies) + struct.pack("<I", crc or 0)
 
 
+class RemoteRankError(RuntimeError):
+    """Another rank failed in a sharded step; raised on every rank."""
+
+
+def _agree(err, group, device):
+    """Collective status check before a data collective: a rank whose local stage
+    raised would otherwise leave the others blocked in the next all_reduce.  Every
+    rank re-raises (its own error, or RemoteRankError naming the failed ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        if err is not None:
+            raise err
+        return
+    flag = torch.tensor([0 if err is None else 1], dtype=torch.int64, device=device)
+    flags = [torch.zeros_like(flag) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(flags, flag, group=group)
+    if err is not None:
+        raise err
+    bad = [r for r, x in enumerate(flags) if int(x.item())]
+    if bad:
+        raise RemoteRankError(f"sharded step failed on rank(s) {bad}")
+
+
 def make_comm(engine, group=None):
     """The engine library's own NCCL communicator over the ranks of ``group``: rank 0
     makes the id, torch.distributed broadcasts it (any backend)."""
@@ -136,15 +161,25 @@ def compress_sharded(engine, ckpt, cfg, seed, step, base_state, *, group=None, d
     n_v = engine.shard_hist_len(cfg, 1)
     score = torch.empty(n_s, dtype=torch.int64, device=dev)
     value = torch.empty(n_v, dtype=torch.int64, device=dev)
-    engine.shard_stage1(ckpt, cfg, score.data_ptr())
-    engine.sync()
+    def local(fn):
+        try:
+            fn()
+            engine.sync()
+            return None
+        except Exception as ex:  # noqa: BLE001 - re-raised on every rank by _agree
+            return ex
+
+    _agree(local(lambda: engine.shard_stage1(ckpt, cfg, score.data_ptr())), group, dev)
     if world > 1:
         dist.all_reduce(score, group=group)
-    engine.shard_stage2(ckpt, cfg, score.data_ptr(), value.data_ptr())
-    engine.sync()
+    _agree(local(lambda: engine.shard_stage2(ckpt, cfg, score.data_ptr(), value.data_ptr())),
+           group, dev)
     if world > 1:
         dist.all_reduce(value, group=group)
-    state = engine.shard_stage3(ckpt, cfg, seed, step, value.data_ptr())
+    box = []
+    _agree(local(lambda: box.append(engine.shard_stage3(ckpt, cfg, seed, step,
+                                                        value.data_ptr()))), group, dev)
+    state = box[0]
     # global alphabet and tensor count
     info = state.info()
     lv = [info.max_levels, base_state.info().max_levels if base_state is not None else 0]
@@ -198,16 +233,25 @@ def eval_batch_sharded(evaluate, cfgs, seeds, *, group=None):
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     mine = assign_configs(len(cfgs), world)[rank]
-    if mine:
-        q, e = evaluate([cfgs[i] for i in mine], [seeds[i] for i in mine])
-        part = (mine, [float(x) for x in q], [float(x) for x in e])
-    else:
-        part = (mine, [], [])
+    err = None
+    part = (mine, [], [])
+    try:
+        if mine:
+            q, e = evaluate([cfgs[i] for i in mine], [seeds[i] for i in mine])
+            part = (mine, [float(x) for x in q], [float(x) for x in e])
+    except Exception as ex:  # noqa: BLE001 - every rank learns about it below
+        err = ex
+        part = (mine, None, f"{type(ex).__name__}: {ex}")
     parts = [None] * world
     if world > 1:
         dist.all_gather_object(parts, part, group=group)
     else:
         parts = [part]
+    if err is not None:
+        raise err
+    bad = [(r, p[2]) for r, p in enumerate(parts) if p[1] is None]
+    if bad:
+        raise RemoteRankError(f"candidate evaluation failed on rank(s): {bad}")
     quality = [0.0] * len(cfgs)
     est = [0.0] * len(cfgs)
     for idx, q, e in parts:

@@ -130,6 +130,7 @@ def _load():
                                          C.c_double, C.POINTER(_P), C.POINTER(_P)]),
         "dqtg_eval_batch": (C.c_int, [_P, _P, _P, _P, C.c_uint32, _P, _P]),
         "dqtg_partition": (C.c_int, [_P, _P, C.POINTER(Config), _P]),
+        "dqtg_proxy_quality": (C.c_int, [_P, _P, _P, _P, C.POINTER(C.c_double)]),
         "dqtg_shard_hist_len": (C.c_uint64, [_P, C.POINTER(Config), C.c_int]),
         "dqtg_shard_stage1": (C.c_int, [_P, _P, C.POINTER(Config), _P]),
         "dqtg_shard_stage2": (C.c_int, [_P, _P, C.POINTER(Config), _P, _P]),
@@ -589,6 +590,16 @@ class Engine:
         masks = [np.zeros(n, np.uint8) for n in ckpt.meta.numel]
         _check(LIB.dqtg_partition(self.h, ckpt.h, C.byref(cfg), _ptr_array(masks)))
         return masks
+
+    def proxy_quality(self, names, types, shapes, orig, recon):
+        """proxy_quality_delta (search.cpp:30-61) of per-tensor host arrays."""
+        meta = _Meta(names, types, shapes)
+        o = [np.ascontiguousarray(x, np.float32).ravel() for x in orig]
+        r = [np.ascontiguousarray(x, np.float32).ravel() for x in recon]
+        out = C.c_double()
+        _check(LIB.dqtg_proxy_quality(self.h, C.byref(meta.c), _ptr_array(o), _ptr_array(r),
+                                      C.byref(out)))
+        return out.value
 
     def eval_batch(self, ckpt, cfgs, seeds):
         m = len(cfgs)

@@ -240,3 +240,55 @@ def test_sharded_evaluator_gloo():
         p.join(60)
     assert all(p.exitcode == 0 for p in procs)
     assert all(r[1] for r in res)
+
+
+def _fail_worker(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = []
+
+        def evaluate(cs, ss):
+            if rank == 1:
+                raise ValueError("local evaluation failure")
+            return [0.0] * len(cs), [1.0] * len(cs)
+
+        try:
+            D.eval_batch_sharded(evaluate, [(4, 0.0)] * 6, list(range(6)))
+            out.append("no error")
+        except D.RemoteRankError:
+            out.append("remote")
+        except ValueError:
+            out.append("local")
+        # the status exchange in front of a data collective (compress_sharded's stages)
+        try:
+            D._agree(RuntimeError("stage") if rank == 0 else None, None, torch.device("cpu"))
+            out.append("no error")
+        except D.RemoteRankError:
+            out.append("remote")
+        except RuntimeError:
+            out.append("local")
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_rank_failure_raises_on_every_rank():
+    """a rank failing before a collective must not leave the others blocked
+    in it -- every rank raises (its own error or RemoteRankError)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fail_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=180) for _ in range(2))
+    for p in procs:
+        p.join(60)
+    assert res[0] == ["remote", "local"] and res[1] == ["local", "remote"], res
