@@ -384,6 +384,7 @@ __device__ __forceinline__ void chain_sums(const double2* wx, const double* w, c
 struct LAux {
     double *lo, *hi, *nlo, *nhi, *sw, *swx, *sax;
     int *pf, *pl;  // clusters (first, last key) that produced the current intervals
+    int* pe;       // boundaries of the previous certified step (search hint), -1: none
     int exact;     // lo == hi == c are the reference's values
 };
 
@@ -425,8 +426,19 @@ __device__ int lloyd_interval_step(const double* pts, const double* w, int n, LA
             for (int j = lane; j < k; j += 32) {
                 int e = n;
                 if (j + 1 < k) {
-                    e = lloyd_boundary(pts, n, X.lo[j], X.lo[j + 1]);
-                    if (!X.exact && lloyd_boundary(pts, n, X.hi[j], X.hi[j + 1]) != e) ok = false;
+                    // the previous step's boundary first (it rarely moves): the predicate
+                    // is monotone in the key, so e is the boundary iff P(e-1) fails and P(e) holds
+                    const double a = X.lo[j], b = X.lo[j + 1];
+                    auto P = [&](int i) { return fabs(__dsub_rn(pts[i], b)) < fabs(__dsub_rn(pts[i], a)); };
+                    const int g = X.pe ? X.pe[j] : -1;
+                    if (g >= 0 && g <= n && (g == 0 || !P(g - 1)) && (g == n || P(g))) e = g;
+                    else e = lloyd_boundary(pts, n, a, b);
+                    if (!X.exact) {  // the same boundary at the upper interval ends
+                        const double ah = X.hi[j], bh = X.hi[j + 1];
+                        auto Q = [&](int i) { return fabs(__dsub_rn(pts[i], bh)) < fabs(__dsub_rn(pts[i], ah)); };
+                        if (!((e == 0 || !Q(e - 1)) && (e == n || Q(e)))) ok = false;
+                    }
+                    if (X.pe) X.pe[j] = e;
                 }
                 last[j] = e;  // exclusive end
             }
@@ -451,12 +463,27 @@ __device__ int lloyd_interval_step(const double* pts, const double* w, int n, LA
     for (int j = wid; j < k; j += (int)(blockDim.x >> 5)) {
         double ws = 0.0, wxs = 0.0, ax = 0.0;
         const int e = last[j];
-        for (int i = first[j] + lane; i < e; i += 32) {
+        double ws2 = 0.0, wxs2 = 0.0, ax2 = 0.0;  // two chains per lane
+        int i = first[j] + lane;
+        for (; i + 32 < e; i += 64) {
+            const double wi = w[i], xi = pts[i], wj = w[i + 32], xj = pts[i + 32];
+            const double ti = __dmul_rn(wi, xi), tj = __dmul_rn(wj, xj);
+            ws = __dadd_rn(ws, wi);
+            wxs = __dadd_rn(wxs, ti);
+            ax = __dadd_rn(ax, fabs(ti));
+            ws2 = __dadd_rn(ws2, wj);
+            wxs2 = __dadd_rn(wxs2, tj);
+            ax2 = __dadd_rn(ax2, fabs(tj));
+        }
+        if (i < e) {
             const double wi = w[i], tt = __dmul_rn(wi, pts[i]);
             ws = __dadd_rn(ws, wi);
             wxs = __dadd_rn(wxs, tt);
             ax = __dadd_rn(ax, fabs(tt));
         }
+        ws = __dadd_rn(ws, ws2);
+        wxs = __dadd_rn(wxs, wxs2);
+        ax = __dadd_rn(ax, ax2);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             ws = __dadd_rn(ws, __shfl_xor_sync(0xffffffffu, ws, o));
@@ -480,10 +507,14 @@ __device__ int lloyd_interval_step(const double* pts, const double* w, int n, LA
             const double wsl = __dmul_rd(ws, __dsub_rd(1.0, e)), wsh = __dmul_ru(ws, __dadd_ru(1.0, e));
             const double d = __dmul_ru(e2, X.sax[j]);
             const double wxl = __dsub_rd(X.swx[j], d), wxh = __dadd_ru(X.swx[j], d);
+            // quotient bounds: round-to-nearest divisions widened by one ulp (cheaper
+            // than directed division; |rn(q) - q| <= ulp(q) / 2)
             double ql, qh;
-            if (wxl >= 0.0) ql = __ddiv_rd(wxl, wsh), qh = __ddiv_ru(wxh, wsl);
-            else if (wxh <= 0.0) ql = __ddiv_rd(wxl, wsl), qh = __ddiv_ru(wxh, wsh);
-            else ql = __ddiv_rd(wxl, wsl), qh = __ddiv_ru(wxh, wsl);
+            if (wxl >= 0.0) ql = __ddiv_rn(wxl, wsh), qh = __ddiv_rn(wxh, wsl);
+            else if (wxh <= 0.0) ql = __ddiv_rn(wxl, wsl), qh = __ddiv_rn(wxh, wsh);
+            else ql = __ddiv_rn(wxl, wsl), qh = __ddiv_rn(wxh, wsl);
+            ql = __dsub_rd(ql, __dmul_ru(fabs(ql), 0x1.0p-52));
+            qh = __dadd_ru(qh, __dmul_ru(fabs(qh), 0x1.0p-52));
             X.nlo[j] = ql;
             X.nhi[j] = qh;
             // movement bounds of |next - c|
@@ -522,7 +553,7 @@ __device__ int lloyd_interval_step(const double* pts, const double* w, int n, LA
 }
 
 // weighted_lloyd (quantize.cpp:180-254); c (k centres) is updated in place.
-// With aux (LAux, 7k doubles + 2k ints), steps are certified interval steps
+// With aux (LAux, 7k doubles + 3k ints), steps are certified interval steps
 // whenever their decisions are certain (above); the others run exactly:
 // iterations whose centres are strictly ascending and well separated (the fast
 // path: clusters are contiguous key ranges) run on warp 0 alone with warp
@@ -544,12 +575,12 @@ __device__ int lloyd_block(const double* pts, const double* w, int n, double* c,
     if (aux && threadIdx.x == 0) {
         X.lo = aux, X.hi = aux + k, X.nlo = aux + 2 * k, X.nhi = aux + 3 * k;
         X.sw = aux + 4 * k, X.swx = aux + 5 * k, X.sax = aux + 6 * k;
-        X.pf = (int*)(aux + 7 * k), X.pl = X.pf + k;
+        X.pf = (int*)(aux + 7 * k), X.pl = X.pf + k, X.pe = X.pl + k;
         X.exact = 1;
     }
     __syncthreads();
     if (aux)
-        for (int j = threadIdx.x; j < k; j += blockDim.x) X.lo[j] = X.hi[j] = c[j];
+        for (int j = threadIdx.x; j < k; j += blockDim.x) X.lo[j] = X.hi[j] = c[j], X.pe[j] = -1;
     __syncthreads();
     int iters = 0;
     for (int it = 0; it < max_iter; ++it) {
@@ -779,8 +810,8 @@ __global__ void __launch_bounds__(kKB) kmeans_restarts_kernel(const KProblem* pr
     int* first = (int*)(nx + k);
     int* last = first + k;
     int* cnt = last + k;
-    double* aux = dsm + 2 * k + (3 * k + 1) / 2 + 1;  // LAux: 7k doubles + 2k ints
-    double* base = aux + 8 * k + 1;
+    double* aux = dsm + 2 * k + (3 * k + 1) / 2 + 1;  // LAux: 7k doubles + 3k ints
+    double* base = aux + 9 * k + 1;
     const double *pts = P.pts, *w = P.w;
     double *d2, *prob, *pref;
     int* assign;
@@ -877,7 +908,7 @@ void run_kmeans(Engine& e, std::vector<KProblem>& probs, float* cb_out, int cb_s
                               cudaMemcpyHostToDevice, e.stream));
     int maxn = 1;
     for (auto& p : probs) maxn = std::max(maxn, p.n);
-    const size_t head = ((size_t)2 * maxk + (3 * maxk + 1) / 2 + 1 + 8 * maxk + 1) * 8;
+    const size_t head = ((size_t)2 * maxk + (3 * maxk + 1) / 2 + 1 + 9 * maxk + 1) * 8;
     const size_t budget = 200 * 1024;
     int smem_n = (int)((budget - std::min(budget, head)) / 60);  // 5 doubles + pair + int per key
     size_t smem = head + (size_t)std::min(maxn, smem_n) * 60 + 96;
