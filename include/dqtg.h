@@ -103,6 +103,10 @@ dqtg_status dqtg_ckpt_create(dqtg_engine *e, const dqtg_layout *layout, dqtg_ckp
 void dqtg_ckpt_destroy(dqtg_ckpt *c);
 /* per-tensor weight pointers (tensor.hpp:30 NamedTensor::data) */
 dqtg_status dqtg_ckpt_set_weights(dqtg_ckpt *c, const float *const *tensors_any);
+/* frees the checkpoint's device buffers (weights, EMA, scores); the layout stays and the
+ * next dqtg_ckpt_set_weights / set_ema allocates them again (a shard processed in
+ * stages keeps only its current inputs resident; no reference counterpart) */
+dqtg_status dqtg_ckpt_release(dqtg_ckpt *c);
 /* explicit ScoreSet (ranker.hpp:34-42); sens may be NULL (has_sensitivity=false) */
 dqtg_status dqtg_ckpt_set_scores(dqtg_ckpt *c, const float *const *mag_any,
                                  const float *const *sens_any);
@@ -305,6 +309,11 @@ dqtg_status dqtg_partition(dqtg_engine *e, const dqtg_ckpt *c, const dqtg_config
 dqtg_status dqtg_proxy_quality(dqtg_engine *e, const dqtg_layout *layout,
                                const float *const *orig_any, const float *const *recon_any,
                                double *quality);
+/* *equal = 1 when the two states have the same step, layout, codebooks, levels and
+ * protected entries (compared on the device; round-trip checks of decode_delta_record,
+ * codec.cpp:513-597, without a host copy of the levels) */
+dqtg_status dqtg_qstate_equal(dqtg_engine *e, const dqtg_qstate *a, const dqtg_qstate *b,
+                              int *equal);
 /* per-tensor level histograms of a state, counts[i * stride + level] — the exact
  * integer input of estimate_compression (search.cpp:63-85) */
 dqtg_status dqtg_level_counts(dqtg_engine *e, const dqtg_qstate *q, uint32_t stride,

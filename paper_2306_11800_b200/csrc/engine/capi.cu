@@ -84,6 +84,7 @@ void init_engine(Engine& e, int device, void* stream) {
     DQTG_CUDA(cudaMemPoolSetAttribute(e.pool, cudaMemPoolAttrReleaseThreshold, &keep));
     int no = 0;
     DQTG_CUDA(cudaMemPoolSetAttribute(e.pool, cudaMemPoolReuseAllowInternalDependencies, &no));
+    register_pool(e.pool, device);
     DQTG_CUDA(cudaMemsetAsync(e.d_err, 0, 16, e.stream));
     DQTG_CUDA(cudaStreamSynchronize(e.stream));
 }
@@ -243,7 +244,7 @@ dqtg_status dqtg_ckpt_create(dqtg_engine* h, const dqtg_layout* layout, dqtg_ckp
         try {
             c->c.eng = &h->e;
             c->c.L = make_layout(&h->e, layout);
-            DQTG_CUDA(cudaMalloc(&c->c.w, c->c.L->Np * 4));
+            DQTG_CUDA(dev_malloc((void**)&c->c.w, c->c.L->Np * 4, h->e.device));
             // on the engine stream: a legacy-stream memset is not ordered with the
             // (non-blocking) engine stream's uploads
             DQTG_CUDA(cudaMemsetAsync(c->c.w, 0, c->c.L->Np * 4, h->e.stream));
@@ -262,19 +263,34 @@ static void upload_tensors(Engine& e, const Layout& L, float* dst, const float* 
         if (L.numel[i]) e.to_device(dst + L.off[i], src[i], L.numel[i] * 4);
 }
 
+static float* alloc_padded(Engine& e, const Layout& L) {
+    float* p = nullptr;
+    DQTG_CUDA(dev_malloc((void**)&p, L.Np * 4, e.device));
+    DQTG_CUDA(cudaMemsetAsync(p, 0, L.Np * 4, e.stream));  // ordered before the uploads
+    return p;
+}
+
 dqtg_status dqtg_ckpt_set_weights(dqtg_ckpt* c, const float* const* t) {
     return guard([&] {
         LOCK(c->c.eng);
+        if (!c->c.w) c->c.w = alloc_padded(*c->c.eng, *c->c.L);  // after dqtg_ckpt_release
         upload_tensors(*c->c.eng, *c->c.L, c->c.w, t);
         c->c.eng->sync();
     });
 }
 
-static float* alloc_padded(Engine& e, const Layout& L) {
-    float* p = nullptr;
-    DQTG_CUDA(cudaMalloc(&p, L.Np * 4));
-    DQTG_CUDA(cudaMemsetAsync(p, 0, L.Np * 4, e.stream));  // ordered before the uploads
-    return p;
+dqtg_status dqtg_ckpt_release(dqtg_ckpt* c) {
+    return guard([&] {
+        LOCK(c->c.eng);
+        DevCkpt& d = c->c;
+        DQTG_REQUIRE(d.own, DQTG_ERROR, "checkpoint buffers are borrowed");
+        d.eng->sync();
+        for (float** p : {&d.w, &d.ema, &d.mag, &d.sens}) {
+            if (*p) cudaFree(*p);
+            *p = nullptr;
+        }
+        d.explicit_scores = d.has_sens = d.ema_seeded = false;
+    });
 }
 
 dqtg_status dqtg_ckpt_set_scores(dqtg_ckpt* c, const float* const* mag, const float* const* sens) {
@@ -630,6 +646,14 @@ dqtg_status dqtg_proxy_quality(dqtg_engine* h, const dqtg_layout* layout,
                 e.to_device(r + c.L->off[i], recon[i], c.L->numel[i] * 4);
             }
         *out = ::dqtg::proxy_quality(e, c, r);
+    });
+}
+
+dqtg_status dqtg_qstate_equal(dqtg_engine* h, const dqtg_qstate* a, const dqtg_qstate* b,
+                              int* equal) {
+    return guard([&] {
+        LOCK(&h->e);
+        *equal = ::dqtg::states_equal(h->e, *a->q, *b->q) ? 1 : 0;
     });
 }
 

@@ -1484,7 +1484,14 @@ __global__ void ov_group_max_kernel(const unsigned long long* ukey, const unsign
     }
 }
 
-__global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsigned long long* elems,
+// Groups are launched in tiers by their symbol-count bound (host: (B + kLD) + distinct
+// overflow lengths): small and medium tiers keep the working set in shared memory
+// (one warp per group, sized for the tier); BIG groups (tens of thousands of
+// distinct run lengths in billion-element tensors, C5) keep it in global memory and
+// sort with 1024 threads, then continue on warp 0.  glist: the tier's groups;
+// gws/goff (BIG): per group (byte offset, n_pad) of its global working set.
+template <bool BIG>
+__global__ void __launch_bounds__(BIG ? 1024 : 32) enc_huffman_kernel(EncArgs A, const unsigned long long* elems,
                                                           const unsigned long long* ukey,
                                                           const unsigned long long* ucnt,
                                                           const unsigned long long* nu_p,
@@ -1495,13 +1502,21 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
                                                           unsigned long long* code_ov,
                                                           uint8_t* len_ov, HufWork W,
                                                           uint32_t n_pad,
-                                                          const unsigned long long* ov_range) {
-    // working set in shared memory (the tree build is a serial chain): n_pad >= n.
-    // 32-bit frequencies / node weights / symbols (the host guarantees tensors below
-    // 2^31 elements) and 8-bit depths (saturated; >= 63 is an error anyway) keep it
-    // at 38 B per slot, so more single-warp CTAs stay resident per SM.
-    extern __shared__ unsigned long long s_keys[];  // n_pad
-    __shared__ uint32_t s_hist[65], s_at[65];
+                                                          const unsigned long long* ov_range,
+                                                          const uint32_t* glist,
+                                                          const unsigned long long* goff,
+                                                          uint8_t* gws) {
+    // working set (the tree build is a serial chain): n_pad >= n.  32-bit frequencies
+    // / node weights / symbols (the host guarantees tensors below 2^31 elements) and
+    // 8-bit depths (saturated; >= 63 is an error anyway) keep it at 38 B per slot, so
+    // more single-warp CTAs stay resident per SM.
+    extern __shared__ unsigned long long s_dyn[];
+    unsigned long long* s_keys = s_dyn;
+    if (BIG) {
+        s_keys = (unsigned long long*)(gws + goff[2 * blockIdx.x]);
+        n_pad = (uint32_t)goff[2 * blockIdx.x + 1];
+    }
+    __shared__ uint32_t s_hist[65], s_at[65], s_n;
     uint32_t* nodef = (uint32_t*)(s_keys + n_pad);   // 2 n_pad
     uint32_t* parent = nodef + 2 * n_pad;            // 2 n_pad
     uint32_t* f = parent + 2 * n_pad;                // n_pad
@@ -1509,7 +1524,7 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
     uint32_t* perm = (uint32_t*)(sym + n_pad);       // n_pad
     uint8_t* depth = (uint8_t*)(perm + n_pad);       // 2 n_pad
     const uint32_t B = A.B, NS = A.NS;
-    const uint32_t tb = blockIdx.x, b = tb % B;
+    const uint32_t tb = glist[blockIdx.x], b = tb % B;
     GroupInfo G{};
     G.n_elems = elems[tb];
     (void)nu_p;
@@ -1521,9 +1536,9 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
     // symbols in ascending order (the reference's std::map): values -(B-1)..0, dense
     // run lengths 2..63, overflow lengths; compacted warp-wide with ballots
     const uint32_t* fr = A.freq + (size_t)tb * NS;
-    const int lane = threadIdx.x;
+    const int lane = threadIdx.x & 31;
     uint32_t n = 0;
-    if (G.n_elems) {
+    if (G.n_elems && threadIdx.x < 32) {
         for (uint32_t i0 = 0; i0 < B + kLD; i0 += 32) {
             const uint32_t i = i0 + lane;
             int32_t sv = 0;
@@ -1552,6 +1567,11 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
             n += (uint32_t)min(32ull, G.ov_end - j0);
         }
     }
+    if (BIG) {  // n from warp 0
+        if (threadIdx.x == 0) s_n = n;
+        __syncthreads();
+        n = s_n;
+    }
     __syncwarp();
     if (n == 0) {
         if (threadIdx.x == 0) gi[tb] = G;
@@ -1579,6 +1599,10 @@ __global__ void __launch_bounds__(32) enc_huffman_kernel(EncArgs A, const unsign
             __syncthreads();
         }
     for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) perm[r] = (uint32_t)(s_keys[r] & 0xffffffu);
+    if (BIG) {  // the rest is warp 0's
+        __syncthreads();
+        if (threadIdx.x >= 32) return;
+    }
     {  // symbols in the group's stream (warp reduction)
         unsigned long long ns = 0;
         for (uint32_t i = lane; i < n; i += 32) ns += f[i];
@@ -2495,28 +2519,69 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
         } else {
             DQTG_CUDA(cudaMemsetAsync(ov_range, 0, (size_t)nt * B * 16, st));
         }
-        uint32_t h_max = 0;
-        e.d2h(&h_max, max_nov, 4);
+        // symbol-count bound per group -> tiers (see enc_huffman_kernel)
+        const uint32_t ng = nt * B;
+        std::vector<unsigned long long> h_rng((size_t)ng * 2), h_el(ng);
+        e.d2h(h_rng.data(), ov_range, (size_t)ng * 16);
+        e.d2h(h_el.data(), elems, (size_t)ng * 8);
         e.sync();
-        uint32_t np2 = 1;
-        while (np2 < NS + h_max) np2 <<= 1;
-        const size_t hsm = (size_t)np2 * 38 + 16;  // keys, nodef, parent, f, sym, perm, depth
-        DQTG_REQUIRE(hsm <= 200 * 1024, DQTG_ERROR,
-                     "too many distinct run lengths in one group for the device Huffman stage");
-        HufWork W;
-        const size_t cap = tab_n;
-        W.sym = (long long*)e.buf("h.sym", cap * 8);
-        W.f = (unsigned long long*)e.buf("h.f", cap * 8);
-        W.perm = (uint32_t*)e.buf("h.perm", cap * 4);
-        const size_t ncap = 2 * cap + 2 * (size_t)nt * B + 8;
-        W.nodef = (unsigned long long*)e.buf("h.nodef", ncap * 8);
-        W.parent = (uint32_t*)e.buf("h.parent", ncap * 4);
-        W.depth = (uint32_t*)e.buf("h.depth", ncap * 4);
-        if (hsm > 48 * 1024)
-            ensure_dyn_smem((const void*)enc_huffman_kernel, hsm);
-        { DQTG_SPAN(e, "enc_huffman_kernel"); enc_huffman_kernel<<<nt * B, 32, hsm, st>>>(A, elems, ukey, ucnt, nu, gi, tab_sym, tab_len,
-                                                     code_dense, len_dense, code_ov, len_ov, W, np2, ov_range); }
-        e.launched();
+        std::vector<uint32_t> tiers[3];
+        std::vector<unsigned long long> big_off;
+        uint32_t np_mid = 1;
+        unsigned long long big_bytes = 0;
+        for (uint32_t g = 0; g < ng; ++g) {
+            uint32_t np2 = 1;
+            const unsigned long long bound = h_el[g] ? NS + (h_rng[2 * g + 1] - h_rng[2 * g]) : 1;
+            while (np2 < bound) np2 <<= 1;
+            if (np2 <= 128) {
+                tiers[0].push_back(g);
+            } else if (np2 <= 2048) {
+                tiers[1].push_back(g);
+                np_mid = std::max(np_mid, np2);
+            } else {
+                tiers[2].push_back(g);
+                big_off.push_back(big_bytes);
+                big_off.push_back(np2);
+                big_bytes += round_up((unsigned long long)np2 * 38 + 16, 256);
+            }
+        }
+        auto* d_gl = (uint32_t*)e.buf("h.glist", (size_t)ng * 4 + 16);
+        auto* d_goff = (unsigned long long*)e.buf("h.goff", big_off.size() * 8 + 16);
+        uint8_t* d_gws = big_bytes ? (uint8_t*)e.buf("h.gws", big_bytes) : nullptr;
+        {
+            std::vector<uint32_t> all;
+            for (auto& v : tiers) all.insert(all.end(), v.begin(), v.end());
+            DQTG_CUDA(cudaMemcpyAsync(d_gl, all.data(), all.size() * 4, cudaMemcpyHostToDevice, st));
+            if (!big_off.empty())
+                DQTG_CUDA(cudaMemcpyAsync(d_goff, big_off.data(), big_off.size() * 8,
+                                          cudaMemcpyHostToDevice, st));
+            e.sync();  // host vectors
+        }
+        HufWork W{};  // unused: the working sets are per tier (shared memory or h.gws)
+        DQTG_SPAN(e, "enc_huffman_kernel");
+        const uint32_t* gl = d_gl;
+        if (!tiers[0].empty()) {
+            enc_huffman_kernel<false><<<(unsigned)tiers[0].size(), 32, 128 * 38 + 16, st>>>(
+                A, elems, ukey, ucnt, nu, gi, tab_sym, tab_len, code_dense, len_dense, code_ov, len_ov,
+                W, 128, ov_range, gl, nullptr, nullptr);
+            gl += tiers[0].size();
+            e.launched();
+        }
+        if (!tiers[1].empty()) {
+            const size_t hsm = (size_t)np_mid * 38 + 16;
+            ensure_dyn_smem((const void*)enc_huffman_kernel<false>, hsm);
+            enc_huffman_kernel<false><<<(unsigned)tiers[1].size(), 32, hsm, st>>>(
+                A, elems, ukey, ucnt, nu, gi, tab_sym, tab_len, code_dense, len_dense, code_ov, len_ov,
+                W, np_mid, ov_range, gl, nullptr, nullptr);
+            gl += tiers[1].size();
+            e.launched();
+        }
+        if (!tiers[2].empty()) {
+            enc_huffman_kernel<true><<<(unsigned)tiers[2].size(), 1024, 0, st>>>(
+                A, elems, ukey, ucnt, nu, gi, tab_sym, tab_len, code_dense, len_dense, code_ov, len_ov,
+                W, 0, ov_range, gl, d_goff, d_gws);
+            e.launched();
+        }
     }
     CodeTabs C{code_dense, len_dense, ukey, code_ov, len_ov, gi};
     auto* segbits = (uint32_t*)e.buf("e.segbits32", (size_t)ntiles * B * 4 + 4);

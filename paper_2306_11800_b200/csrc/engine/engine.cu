@@ -104,7 +104,56 @@ Engine::~Engine() {
     if (pinned) cudaFreeHost(pinned);
     for (auto& b : stage_blocks) cudaFreeHost(b.first);
     if (own_stream && stream) cudaStreamDestroy(stream);
-    if (pool) cudaMemPoolDestroy(pool);  // blocks still owned by live states keep it alive
+    if (pool) {
+        unregister_pool(pool);
+        cudaMemPoolDestroy(pool);  // blocks still owned by live states keep it alive
+    }
+}
+
+// ---- out-of-memory recovery --------------------------------------------------------
+// Freed memory stays cached (engine pools keep everything, BigCache keeps freed level
+// arrays and records): right for a steady chain, but a workload that moves between
+// very different sizes (C4 then C5 in one process) can find HBM held by caches.  On
+// an allocation failure every cache of the device is dropped and the pools trimmed,
+// then the allocation is retried once.
+namespace {
+std::mutex g_pools_mu;
+std::map<cudaMemPool_t, int> g_pools;  // live engine pools -> device
+}  // namespace
+
+void register_pool(cudaMemPool_t p, int device) {
+    std::lock_guard<std::mutex> g(g_pools_mu);
+    g_pools[p] = device;
+}
+void unregister_pool(cudaMemPool_t p) {
+    std::lock_guard<std::mutex> g(g_pools_mu);
+    g_pools.erase(p);
+}
+
+static void drop_big_cache(int device);
+
+void trim_device_caches(int device) {
+    cudaGetLastError();  // the failed allocation's error
+    cudaDeviceSynchronize();
+    drop_big_cache(device);
+    cudaDeviceSynchronize();
+    std::lock_guard<std::mutex> g(g_pools_mu);
+    for (auto& kv : g_pools)
+        if (kv.second == device) cudaMemPoolTrimTo(kv.first, 0);
+}
+
+template <typename F>
+static cudaError_t alloc_retry(int device, F f) {
+    cudaError_t r = f();
+    if (r == cudaErrorMemoryAllocation) {
+        trim_device_caches(device);
+        r = f();
+    }
+    return r;
+}
+
+cudaError_t dev_malloc(void** p, size_t bytes, int device) {
+    return alloc_retry(device, [&] { return cudaMalloc(p, bytes); });
 }
 
 void* Engine::buf(const std::string& name, size_t bytes) {
@@ -127,7 +176,8 @@ void* Engine::buf(const std::string& name, size_t bytes) {
         // maps pool memory on the host thread mid-step
         size_t cap = pool_size_class(std::max(bytes < 256 ? 256 : bytes + bytes / 4, 2 * slot.second));
         if (slot.first) DQTG_CUDA(cudaFreeAsync(slot.first, stream));
-        DQTG_CUDA(cudaMallocFromPoolAsync(&slot.first, cap, pool, stream));
+        slot.first = nullptr;
+        DQTG_CUDA(alloc_retry(device, [&] { return cudaMallocFromPoolAsync(&slot.first, cap, pool, stream); }));
         slot.second = cap;
     }
     return slot.first;
@@ -171,6 +221,19 @@ BigCache& big_cache() {
 }
 }  // namespace
 
+static void drop_big_cache(int device) {
+    BigCache& bc = big_cache();
+    std::lock_guard<std::mutex> g(bc.mu);
+    for (size_t i = bc.free.size(); i-- > 0;) {
+        BigBlock& b = bc.free[i];
+        if (b.device != device) continue;
+        cudaEventSynchronize(b.ev);
+        cudaEventDestroy(b.ev);
+        cudaFree(b.p);  // returns the block to its pool (synchronous)
+        bc.free.erase(bc.free.begin() + (long)i);
+    }
+}
+
 void* Engine::dalloc(size_t bytes) {
     void* p = nullptr;
     const size_t cls = pool_size_class(bytes ? bytes : 16);
@@ -195,7 +258,7 @@ void* Engine::dalloc(size_t bytes) {
             return b.p;
         }
     }
-    DQTG_CUDA(cudaMallocFromPoolAsync(&p, cls, pool, stream));
+    DQTG_CUDA(alloc_retry(device, [&] { return cudaMallocFromPoolAsync(&p, cls, pool, stream); }));
     if (cls >= kBigBlock) {
         BigCache& bc = big_cache();
         std::lock_guard<std::mutex> g(bc.mu);

@@ -307,6 +307,12 @@ void run_pass_c(Engine& e, const DevCkpt& c, const FuseC& f, QState& q);
 // whether compress_step may fuse pass C into the DELTA encoder (sparse encoder, B <= 64)
 bool fused_c_enabled();
 
+// memory: engine pools register for out-of-memory trimming (engine.cu)
+void register_pool(cudaMemPool_t p, int device);
+void unregister_pool(cudaMemPool_t p);
+void trim_device_caches(int device);
+cudaError_t dev_malloc(void** p, size_t bytes, int device);
+
 // ---- pipeline entry points implemented across the .cu files ---------------
 void sketch_build(Engine& e, const float* x_any, uint64_t n, double alpha, uint64_t* zero,
                   uint64_t* pos, uint64_t* neg);
@@ -319,6 +325,8 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
 std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
                                       const QState* base);
 void dequantize(Engine& e, const QState& q, float* out_dev_padded);
+// same step, layout, codebooks, levels and protected entries (compared on the device)
+bool states_equal(Engine& e, const QState& a, const QState& b);
 // crc32 (codec.cpp:275-306) of a state's level stream (u16 LE, tensor order)
 uint32_t level_stream_crc(Engine& e, const Layout& L, const uint16_t* levels_dev);
 void partition(Engine& e, const DevCkpt& c, const dqtg_config& cfg, uint8_t* const* masks);

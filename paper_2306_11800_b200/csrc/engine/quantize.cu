@@ -1046,6 +1046,7 @@ __global__ void __launch_bounds__(256) level_count_kernel(const Tile* tiles, con
 
 // ---- host orchestration ---------------------------------------------------------
 static PassIn pass_in(Engine& e, const DevCkpt& c, const AlphaTables& T, int metric) {
+    DQTG_REQUIRE(c.w || c.L->N == 0, DQTG_ERROR, "checkpoint has no weights (released)");
     const Layout& L = *c.L;
     PassIn a{};
     a.tiles = L.d_tiles;
@@ -1833,6 +1834,48 @@ void level_counts(Engine& e, const QState& q, uint64_t* counts, int lstride) {
     }
     e.from_device(counts, d, (size_t)L.nt * lstride * 8);
     e.sync();
+}
+
+// ---- state equality (round-trip checks without a host copy) ------------------------
+__global__ void levels_diff_kernel(const Tile* tiles, const uint16_t* a, const uint16_t* b,
+                                   unsigned int* diff) {
+    const Tile T = tiles[blockIdx.x];
+    bool d = false;
+    for (uint32_t i = threadIdx.x; i < T.count; i += blockDim.x) d |= a[T.start + i] != b[T.start + i];
+    if (__syncthreads_or(d) && threadIdx.x == 0) atomicOr(diff, 1u);
+}
+__global__ void words_diff_kernel(const uint8_t* a, const uint8_t* b, uint64_t n, unsigned int* diff) {
+    bool d = false;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        d |= a[i] != b[i];
+    if (__syncthreads_or(d) && threadIdx.x == 0) atomicOr(diff, 1u);
+}
+
+bool states_equal(Engine& e, const QState& a, const QState& b) {
+    const Layout &LA = *a.L, &LB = *b.L;
+    if (!LA.same_shape(LB) || a.step != b.step || a.prot_total != b.prot_total) return false;
+    for (uint32_t i = 0; i < LA.nt; ++i)
+        if (a.prot_count[i] != b.prot_count[i]) return false;
+    for (int lt = 0; lt < kLayerTypes; ++lt)
+        if (a.cb_len[lt] != b.cb_len[lt] || a.cb[lt] != b.cb[lt]) return false;
+    auto* d = (unsigned int*)e.buf("eq.diff", 16);
+    DQTG_CUDA(cudaMemsetAsync(d, 0, 4, e.stream));
+    if (!LA.tiles.empty()) {
+        { DQTG_SPAN(e, "levels_diff_kernel"); levels_diff_kernel<<<(unsigned)LA.tiles.size(), 256, 0, e.stream>>>(LA.d_tiles, a.d_levels, b.d_levels, d); }
+        e.launched();
+    }
+    const uint64_t np = a.prot_total;
+    if (np) {
+        const unsigned g = (unsigned)std::min<uint64_t>((uint64_t)e.num_sms * 4, (np * 8 + 255) / 256);
+        words_diff_kernel<<<g, 256, 0, e.stream>>>((const uint8_t*)a.d_ppos, (const uint8_t*)b.d_ppos, np * 8, d);
+        words_diff_kernel<<<g, 256, 0, e.stream>>>((const uint8_t*)a.d_pval, (const uint8_t*)b.d_pval, np * 2, d);
+        e.launched(2);
+    }
+    unsigned int h = 0;
+    e.d2h(&h, d, 4);
+    e.check_err();
+    return h == 0;
 }
 
 void dequantize(Engine& e, const QState& q, float* out_dev) {

@@ -131,6 +131,8 @@ def _load():
         "dqtg_eval_batch": (C.c_int, [_P, _P, _P, _P, C.c_uint32, _P, _P]),
         "dqtg_partition": (C.c_int, [_P, _P, C.POINTER(Config), _P]),
         "dqtg_proxy_quality": (C.c_int, [_P, _P, _P, _P, C.POINTER(C.c_double)]),
+        "dqtg_qstate_equal": (C.c_int, [_P, _P, _P, C.POINTER(C.c_int)]),
+        "dqtg_ckpt_release": (C.c_int, [_P]),
         "dqtg_shard_hist_len": (C.c_uint64, [_P, C.POINTER(Config), C.c_int]),
         "dqtg_shard_stage1": (C.c_int, [_P, _P, C.POINTER(Config), _P]),
         "dqtg_shard_stage2": (C.c_int, [_P, _P, C.POINTER(Config), _P, _P]),
@@ -244,6 +246,10 @@ class DevCheckpoint:
     def set_weights(self, arrays):
         arrs = [_as_buf(a) for a in arrays]
         _check(LIB.dqtg_ckpt_set_weights(self.h, _ptr_array(arrs)))
+
+    def release(self):
+        """Free the device buffers (the next set_weights / set_ema allocates them again)."""
+        _check(LIB.dqtg_ckpt_release(self.h))
 
     def set_scores(self, mag, sens=None):
         m = [_as_buf(a) for a in mag]
@@ -524,6 +530,12 @@ class Engine:
         finally:
             if destroy:
                 LIB.dqtg_record_destroy(r)
+
+    def states_equal(self, a: DevState, b: DevState) -> bool:
+        """Device comparison of two states (levels, protected entries, codebooks, step)."""
+        r = C.c_int()
+        _check(LIB.dqtg_qstate_equal(self.h, a.h, b.h, C.byref(r)))
+        return bool(r.value)
 
     def payload_bytes(self, base: DevState, target: DevState, variant=0) -> int:
         """payload_bytes_pe (0) / _rle (1) / _he (2) (codec.cpp:615-646) on the device."""

@@ -187,3 +187,34 @@ def split(flat, layout):
         out.append(flat[o:o + n])
         o += n
     return out
+
+
+class ShardSeries:
+    """Per-shard regeneration of a trajectory too large for one GPU's working set
+    (C5): shard s of the tensor plan gets its own generator (seed * 1009 + s), so any
+    snapshot of any shard can be rebuilt on demand from its seed (the reference
+    dynamics above, bf16 draws for C5).  ``load(s, k, ck)`` writes snapshot k of shard s
+    and the EMA of its first two gradients into the device checkpoint ``ck``."""
+
+    def __init__(self, torch, layout, plan, seed, device, bf16=False):
+        self.torch, self.layout, self.plan = torch, layout, plan
+        self.seed, self.device, self.bf16 = int(seed), device, bf16
+
+    def shard_layout(self, s):
+        a, b = self.plan[s]
+        return self.layout[a:b]
+
+    def load(self, s, k, ck):
+        torch = self.torch
+        lay = self.shard_layout(s)
+        tr = Trajectory(torch, layout_params(lay), self.seed * 1009 + s, self.device,
+                        bf16=self.bf16)
+        w = None
+        for _ in range(k + 1):
+            w = tr.next()
+        if len(tr.grads) < 2:
+            tr.next()
+        ema = tr.ema()
+        ck.set_weights(tensor_ptrs(w.data_ptr(), lay))
+        ck.set_ema(tensor_ptrs(ema.data_ptr(), lay))
+        del tr, w, ema

@@ -8,7 +8,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-import bench  # noqa: E402
+from paper_2306_11800_b200 import workloads as W  # noqa: E402
 
 
 def main():
@@ -19,23 +19,23 @@ def main():
     steps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
     dev = torch.device("cuda", 0)
     eng = E.Engine(0, torch.cuda.current_stream(dev).cuda_stream)
-    layout = bench.gpt2_small_layout()
+    layout = W.gpt2_small_layout()
     names = [n for n, _, _ in layout]
     types = [t for _, t, _ in layout]
     shapes = [s for _, _, s in layout]
-    N = sum(bench.numel(s) for s in shapes)
-    snaps, ema = bench.gen_series(torch, layout, steps + 2, 1234, dev)
+    N = sum(W.numel(s) for s in shapes)
+    snaps, ema = W.series(torch, layout, steps + 2, 1234, dev)
     cfg = E.Config()
     recs, prev = [], None
     for i, s in enumerate(snaps):
         c = E.DevCheckpoint(eng, names, types, shapes)
-        c.set_weights(bench.tensor_ptrs(s.data_ptr(), layout))
-        c.set_ema(bench.tensor_ptrs(ema.data_ptr(), layout))
+        c.set_weights(W.tensor_ptrs(s.data_ptr(), layout))
+        c.set_ema(W.tensor_ptrs(ema.data_ptr(), layout))
         st = eng.quantize(c, cfg, 1, i)
         recs.append(eng.encode_record(st, prev))
         prev = st
     out = torch.empty(N, dtype=torch.float32, device=dev)
-    optr = E._ptr_array(bench.tensor_ptrs(out.data_ptr(), layout))
+    optr = E._ptr_array(W.tensor_ptrs(out.data_ptr(), layout))
     dec = eng.decode_record(recs[0])
     dec = eng.decode_record(recs[1], base=dec)
     eng.profile(True)
