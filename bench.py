@@ -390,6 +390,86 @@ def measure_c3(torch, dev, cpu_ref=True, ref_layers=1):
     return res
 
 
+def measure_big(torch, dev, steps=2):
+    """BASELINE configs[3] / [4] on ONE B200 (the driver's GPUs are single).
+    C4 (GPT-2 XL, 1.56 B params): the whole-checkpoint chain (FULL, then DELTA steps)
+    on one engine, CUDA-synchronised wall time of quantize + encode per DELTA step; the
+    same snapshots as 8 tensor shards (shards.LocalShardedChain, the 8-GPU split)
+    give byte-identical records.  C5 (Llama-3-8B, 8.03 B params, bf16 draws upcast):
+    8 tensor shards on one engine, inputs regenerated per stage (excluded from the
+    time), FULL + DELTA, every shard record decoded back on the device."""
+    from paper_2306_11800_b200 import engine as E
+    from paper_2306_11800_b200 import shards as S
+
+    out = {}
+    eng = E.Engine(0, torch.cuda.current_stream(dev).cuda_stream)
+    cfg = E.Config()
+    lay = W.gpt2_xl_layout()
+    names, types, shapes = ([x[i] for x in lay] for i in range(3))
+    N = W.layout_params(lay)
+    snaps, ema = W.series(torch, lay, steps + 1, SEED + 4, dev)
+    offs = np.concatenate([[0], np.cumsum([W.numel(s) for s in shapes])])
+    whole, prev, ts = [], None, []
+    for k, w in enumerate(snaps):
+        ck = E.DevCheckpoint(eng, names, types, shapes)
+        ck.set_weights(W.tensor_ptrs(w.data_ptr(), lay))
+        ck.set_ema(W.tensor_ptrs(ema.data_ptr(), lay))
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        st, rh = eng.compress_step(ck, cfg, 1, k, base=prev)
+        eng.sync()
+        if k:
+            ts.append(time.perf_counter() - t)
+        whole.append(E.Engine.record_bytes(rh))
+        prev = st
+        del ck
+    del prev
+    ch = S.LocalShardedChain(eng, names, types, shapes, 8, cfg, seed=1, device=dev)
+    same = True
+    for k in range(len(snaps)):
+        def load(s, ck, k=k):
+            a, b = ch.plan[s]
+            ck.set_weights(W.tensor_ptrs(snaps[k].data_ptr() + 4 * int(offs[a]), lay[a:b]))
+            ck.set_ema(W.tensor_ptrs(ema.data_ptr() + 4 * int(offs[a]), lay[a:b]))
+        recs, rt = ch.step(k, load)
+        same &= ch.assemble(recs) == whole[k] and all(rt)
+    out["c4"] = {"workload": "C4: GPT-2 XL 1,557,611,200 fp32 params, delta chain, 1 GPU",
+                 "params": N, "value": 4.0 * N / float(np.median(ts)) / 1e9, "unit": "GB/s",
+                 "ms_per_step": 1e3 * float(np.median(ts)), "steps": len(ts),
+                 "record_bytes_full": len(whole[0]), "record_bytes_delta": len(whole[-1]),
+                 "sharded_8_records_identical_and_roundtrip": bool(same),
+                 "timing": "compress_step (quantize + encode_delta_record) wall time, device synced"}
+    del snaps, ema, ch, whole
+    gc.collect()
+    eng.trim()
+    torch.cuda.empty_cache()
+    lay = W.llama3_8b_layout()
+    names, types, shapes = ([x[i] for x in lay] for i in range(3))
+    N = W.layout_params(lay)
+    ch = S.LocalShardedChain(eng, names, types, shapes, 8, cfg, seed=1, device=dev)
+    gen = W.ShardSeries(torch, lay, ch.plan, SEED + 5, dev, bf16=True)
+    sizes, rts, tq, td = [], [], [], []
+    for k in range(2):
+        ch.t_engine, ch.t_decode = 0.0, 0.0
+        recs, rt = ch.step(k, lambda s, ck, k=k: gen.load(s, k, ck), keep_records=False)
+        sizes.append(int(sum(recs)))
+        rts.append(bool(all(rt)))
+        tq.append(ch.t_engine)
+        td.append(ch.t_decode)
+    out["c5"] = {"workload": "C5: Llama-3-8B 8,030,261,248 params (bf16 draws upcast to fp32), "
+                             "8 tensor shards on 1 GPU",
+                 "params": N, "compress_gbs_delta": 4.0 * N / tq[1] / 1e9,
+                 "compress_s": tq, "decompress_gbs_delta": 4.0 * N / td[1] / 1e9,
+                 "decompress_s": td, "record_bytes": sizes, "roundtrip_identical": rts,
+                 "timing": "engine calls only (per-stage input regeneration excluded), FULL "
+                           "then DELTA; decompress = decode_delta_record on the device + "
+                           "state comparison"}
+    del ch, gen
+    gc.collect()
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -733,6 +813,15 @@ def run_ours(args):
         torch.cuda.empty_cache()
         c3 = measure_c3(torch, dev, cpu_ref=not args.no_cpu_baseline)
 
+    big = None
+    if world == 1 and args.big:
+        ckpts = None
+        snaps = host_snaps = None
+        gc.collect()
+        eng.trim()
+        torch.cuda.empty_cache()
+        big = measure_big(torch, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # the reference on the same C2 chain and bytes, a bounded number of steps
@@ -778,7 +867,7 @@ def run_ours(args):
                                   if pipelined is not None and ms == pipelined else
                                   "CUDA events on the engine stream")},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "restore": restore,
-            "ingest": ingest, "c3_search": c3,
+            "ingest": ingest, "c3_search": c3, "c4_c5": big,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
         }
@@ -798,6 +887,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 (BERT-large search) leg")
+    ap.add_argument("--big", action="store_true",
+                    help="add the C4 (GPT-2 XL) and C5 (Llama-3-8B, 8 shards) legs on this GPU")
     ap.add_argument("--workers", type=int, default=4, help="worker streams of the chain pipeline")
     ap.add_argument("--share-gpu", action="store_true",
                     help="test mode for N>1 on one GPU: all ranks on device 0 with gloo")

@@ -649,6 +649,15 @@ dqtg_status dqtg_proxy_quality(dqtg_engine* h, const dqtg_layout* layout,
     });
 }
 
+dqtg_status dqtg_engine_trim(dqtg_engine* h) {
+    return guard([&] {
+        LOCK(&h->e);
+        h->e.sync();
+        h->e.drop_scratch("");
+        trim_device_caches(h->e.device);
+    });
+}
+
 dqtg_status dqtg_qstate_equal(dqtg_engine* h, const dqtg_qstate* a, const dqtg_qstate* b,
                               int* equal) {
     return guard([&] {

@@ -183,6 +183,17 @@ void* Engine::buf(const std::string& name, size_t bytes) {
     return slot.first;
 }
 
+void Engine::drop_scratch(const std::string& prefix) {
+    for (auto it = scratch.begin(); it != scratch.end();) {
+        if (it->first.compare(0, prefix.size(), prefix) == 0) {
+            if (it->second.first) cudaFreeAsync(it->second.first, stream);
+            it = scratch.erase(it);
+        } else {
+            ++it;
+        }
+    }
+}
+
 // Pool requests are rounded to size classes (powers of two up to 1 MiB, then eighths
 // of the next power of two): steps whose record / protected-entry sizes wobble then
 // reuse the blocks the previous steps freed instead of growing the pool, which maps

@@ -225,6 +225,8 @@ struct Engine {
                          t.cell_shift, t.d_slot, t.d_ctab, t.ctab_lo, t.ctab_n};
     }
     void* buf(const std::string& name, size_t bytes);  // scratch, contents undefined
+    // release the scratch buffers whose names start with prefix ("" = all)
+    void drop_scratch(const std::string& prefix);
     // stream-ordered pool allocations for per-step objects (states, records)
     void* dalloc(size_t bytes);
     void dfree(void* p);

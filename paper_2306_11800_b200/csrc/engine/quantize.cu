@@ -1570,6 +1570,7 @@ std::unique_ptr<QState> shard_stage3(Engine& e, const DevCkpt& c, const dqtg_con
         q->cb[lt].assign(hcb.begin() + (size_t)lt * q->cb_stride,
                          hcb.begin() + (size_t)lt * q->cb_stride + q->cb_len[lt]);
     e.pending.erase(&c);
+    e.drop_scratch(s.tag);  // this shard's stage buffers (partition codes, histograms)
     return q;
 }
 

@@ -133,6 +133,7 @@ def _load():
         "dqtg_proxy_quality": (C.c_int, [_P, _P, _P, _P, C.POINTER(C.c_double)]),
         "dqtg_qstate_equal": (C.c_int, [_P, _P, _P, C.POINTER(C.c_int)]),
         "dqtg_ckpt_release": (C.c_int, [_P]),
+        "dqtg_engine_trim": (C.c_int, [_P]),
         "dqtg_shard_hist_len": (C.c_uint64, [_P, C.POINTER(Config), C.c_int]),
         "dqtg_shard_stage1": (C.c_int, [_P, _P, C.POINTER(Config), _P]),
         "dqtg_shard_stage2": (C.c_int, [_P, _P, C.POINTER(Config), _P, _P]),
@@ -530,6 +531,10 @@ class Engine:
         finally:
             if destroy:
                 LIB.dqtg_record_destroy(r)
+
+    def trim(self):
+        """Release scratch buffers and cached device blocks (dqtg_engine_trim)."""
+        _check(LIB.dqtg_engine_trim(self.h))
 
     def states_equal(self, a: DevState, b: DevState) -> bool:
         """Device comparison of two states (levels, protected entries, codebooks, step)."""
