@@ -834,7 +834,7 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A, FuseC
             const uint32_t bytes = ((N.count + 7u) & ~7u) * 2u;
             if (FUSED) {
                 prefetch_l2(F.w + N.start, ((N.count + 3u) & ~3u) * 4u);
-                prefetch_l2(F.parts + (N.start >> 2), ((N.count + 15u) & ~15u) >> 2);
+                if (!F.pbits) prefetch_l2(F.parts + (N.start >> 2), ((N.count + 15u) & ~15u) >> 2);
             } else {
                 prefetch_l2(A.cur + N.start, bytes);
             }
@@ -877,7 +877,17 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A, FuseC
                 const uint4 b0 = pp[0], b1 = pp[1];
                 uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0;
                 if (FUSED) {
-                    const uint32_t pc = *(const uint32_t*)(F.parts + ((T.start + e0) >> 2));
+                    uint32_t pc;  // 2-bit partition codes of the 16 elements
+                    if (F.pbits) {  // protected bitmap (no pruning): bit -> code 2
+                        uint32_t x = (F.pbits[(T.start + e0) >> 5] >> ((T.start + e0) & 31)) & 0xffffu;
+                        x = (x | (x << 8)) & 0x00ff00ffu;
+                        x = (x | (x << 4)) & 0x0f0f0f0fu;
+                        x = (x | (x << 2)) & 0x33333333u;
+                        x = (x | (x << 1)) & 0x55555555u;
+                        pc = x << 1;
+                    } else {
+                        pc = *(const uint32_t*)(F.parts + ((T.start + e0) >> 2));
+                    }
                     const float* wp = F.w + T.start + e0;
                     switch (s_logp) {
 #define DQTG_FL(L) case L: fused_levels<L>(s_lb, wp, pc, s_k, nv, cw, pmask); break;

@@ -18,7 +18,7 @@ struct dqtg_comm;
 namespace dqtg {
 
 // Shared-memory histogram window: kWin buckets per sign plus the zero bucket.
-constexpr int kWin = 4096;
+constexpr int kWin = 2048;
 constexpr int kWinSlots = 2 * kWin + 1;
 // slot-table sentinels (AlphaTables::d_slot)
 constexpr uint32_t kSlotSpill = 0xffffu, kSlotBad = 0xfffeu;
@@ -296,6 +296,7 @@ struct LtParams;
 struct FuseC {
     const float* w = nullptr;
     const uint8_t* parts = nullptr;                     // 2 bits per element, element order
+    const uint32_t* pbits = nullptr;                    // or: protected-element bitmap (no pruning)
     const float* lb = nullptr;                          // [7][lb_stride] level boundaries
     int lb_stride = 0;
     const uint32_t* cb_len = nullptr;                   // [7] (device)

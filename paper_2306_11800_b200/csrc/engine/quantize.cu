@@ -444,6 +444,198 @@ __global__ void __launch_bounds__(kPB, 4) pass_ab_kernel(PassIn a, FuseArgs f) {
     }
 }
 
+// ---- pass A2: score histograms + protected candidates (replaces pass B) -----------
+// For derived scores without pruning (the default QuantConfig), pass B's only jobs are
+// the partition (quantize.cpp:76-89) and the QUANTIZE-value histogram (:384-393).
+// The protected set is tiny (protect_frac), so pass A2 reads w + EMA once and builds
+//   * the signed histogram of w (|w|'s histogram is its fold -- the magnitude scores),
+//   * the sensitivity histogram, and
+//   * a candidate list: every element whose magnitude or sensitivity exceeds a lower
+//     bound of its threshold (the quantile of a thinned tile sample, kCandMargin
+//     buckets lower).
+// Once the exact thresholds are known, the candidates are classified: protected ones
+// set a bit in an element bitmap (the fused encoder's partition) and are counted per
+// tile and tensor; the QUANTIZE-value histogram is w's histogram minus theirs.  If an
+// exact threshold lies below its bound (or the list overflows) pass B runs as before,
+// so the result is exact either way.
+constexpr int kCandMargin = 4;  // sketch buckets below the sample quantile (~8 % at alpha 0.01)
+
+struct A2Args {
+    const float2* lo;               // [7]: candidate lower bounds (magnitude, sensitivity)
+    unsigned long long* gh_w;       // [7][HS] signed histogram of w
+    unsigned long long* gh_sens;    // [7][HS]
+    uint4* cand;                    // (tile, element, w bits, sensitivity bits)
+    unsigned long long* n_cand;
+    unsigned long long cap;
+};
+
+__global__ void __launch_bounds__(kPB, 5) pass_a2_kernel(PassIn a, A2Args f) {
+    extern __shared__ uint32_t sh[];
+    uint32_t* shw = sh;              // kWinSlots: signed w
+    uint32_t* shs = sh + kWinSlots;  // kPosSlots: sensitivity
+    uint32_t* s_ctab = shs + kPosSlots;
+    const bool fastc = a.tab.ctab != nullptr;
+    for (int i = threadIdx.x; i < kWinSlots + kPosSlots; i += blockDim.x) sh[i] = 0;
+    if (fastc) {
+        for (uint32_t i = threadIdx.x; i < a.tab.ctab_n; i += blockDim.x) s_ctab[i] = __ldg(a.tab.ctab + i);
+        if (threadIdx.x == 0) s_ctab[a.tab.ctab_n] = 0xc0000000u;
+    }
+    __syncthreads();
+    const FastPos fp = fast_pos(a.tab, s_ctab);
+    const uint32_t shw_s = (uint32_t)__cvta_generic_to_shared(shw);
+    const uint32_t shs_s = (uint32_t)__cvta_generic_to_shared(shs);
+    const int lane = threadIdx.x & 31;
+    __shared__ int s_base;
+    int cur = -1;
+    float2 lo = make_float2(0.f, 0.f);
+    for (int base; (base = grab_tiles(a.tile_ctr, kGrab, &s_base)) < a.ntiles;)
+    for (int ti = base; ti < min(base + kGrab, a.ntiles); ++ti) {
+        const Tile T = a.tiles[ti];
+        const int lt = a.types[T.tensor];
+        if (threadIdx.x == 0 && ti + 1 < min(base + kGrab, a.ntiles)) prefetch_tile(a, ti + 1, false);
+        if (lt != cur) {
+            __syncthreads();
+            if (cur >= 0) {
+                hist_flush(shw, f.gh_w + cur * a.HS, a.tab);
+                hist_flush_pos(shs, f.gh_sens + cur * a.HS, a.tab);
+            }
+            __syncthreads();
+            cur = lt;
+            lo = f.lo[lt];
+        }
+        unsigned long long* gw = f.gh_w + lt * a.HS;
+        unsigned long long* gs = f.gh_sens + lt * a.HS;
+        for (uint32_t i = threadIdx.x * 4; i < T.count; i += kPB * 8) {
+            const uint32_t i2 = i + kPB * 4;
+            const bool two = i2 < T.count;
+            const float4 w0 = ld4(a.w + T.start + i);
+            const float4 w1 = two ? ld4(a.w + T.start + i2) : make_float4(0, 0, 0, 0);
+            float m[8], s[8];
+            {
+                float mm[4], ss[4];
+                load_scores<false>(a, T.start + i, w0, mm, ss);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) m[j] = mm[j], s[j] = ss[j];
+                if (two) {
+                    load_scores<false>(a, T.start + i2, w1, mm, ss);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) m[4 + j] = mm[j], s[4 + j] = ss[j];
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) m[4 + j] = s[4 + j] = 0.0f;
+                }
+            }
+            const float wa[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            uint32_t cm = 0;  // candidate elements of this thread
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t e = (j < 4 ? i : i2) + (j & 3);
+                if (e >= T.count) continue;
+                if (!(fastc && hist_fast_signed(shw_s, __float_as_uint(wa[j]), fp)))
+                    hist_add(shw, gw, wa[j], a.tab, a.err);
+                if (a.has_sens && !(fastc && hist_fast_pos(shs_s, __float_as_uint(s[j]), fp)))
+                    hist_add_pos(shs, gs, s[j], a.tab, a.err);
+                if (m[j] > lo.x || (a.has_sens && s[j] > lo.y)) cm |= 1u << j;
+            }
+            const uint32_t act = __activemask();
+            const uint32_t bal = __ballot_sync(act, cm != 0);
+            if (bal) {  // warp-aggregated append (rare)
+                const uint32_t cnt = __popc(cm);
+                uint32_t x = cnt;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(act, x, o);
+                    if (lane >= o) x += y;
+                }
+                const int last = 31 - __clz(act);
+                unsigned long long b0 = 0;
+                if (lane == last) b0 = atomicAdd(f.n_cand, (unsigned long long)x);
+                b0 = __shfl_sync(act, b0, last);
+                unsigned long long at = b0 + (x - cnt);
+                for (uint32_t q = cm; q; q &= q - 1) {
+                    const int j = __ffs(q) - 1;
+                    const uint32_t e = (j < 4 ? i : i2) + (j & 3);
+                    if (at < f.cap)
+                        f.cand[at] = make_uint4((uint32_t)ti, e, __float_as_uint(wa[j]), __float_as_uint(s[j]));
+                    ++at;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (cur >= 0) {
+        hist_flush(shw, f.gh_w + cur * a.HS, a.tab);
+        hist_flush_pos(shs, f.gh_sens + cur * a.HS, a.tab);
+    }
+}
+
+// candidate lower bounds from the sample's quantile slots; +inf where there is no job
+__global__ void cand_bounds_kernel(const int* slot_g, const float* keyf, int64_t NB, int64_t HS,
+                                   float2* lo, int2* lo_slot, int shift) {
+    const int lt = threadIdx.x;
+    if (lt >= kLayerTypes) return;
+    float2 b = make_float2(__int_as_float(0x7f800000), __int_as_float(0x7f800000));
+    int2 bs = make_int2(-1, -1);
+    for (int which = 0; which < 2; ++which) {
+        const int g = slot_g[lt * 3 + which];
+        if (g < 0) continue;
+        // shift: test hook (DQTG_A2_BOUND_SHIFT) -- a bound above the exact threshold
+        const int64_t l = min(HS - 1, max(NB, (int64_t)g - kCandMargin + shift));
+        if (which == 0) b.x = keyf[l], bs.x = (int)l;
+        else b.y = keyf[l], bs.y = (int)l;
+    }
+    lo[lt] = b;
+    lo_slot[lt] = bs;
+}
+
+// exact threshold slots at or above the candidate bounds? (else: pass B)
+__global__ void cand_check_kernel(const int* slot_x, const int2* lo_slot,
+                                  const unsigned long long* n_cand, unsigned long long cap,
+                                  uint32_t* flag) {
+    const int lt = threadIdx.x;
+    if (lt >= kLayerTypes) return;
+    const int2 bs = lo_slot[lt];
+    for (int which = 0; which < 2; ++which) {
+        const int x = slot_x[lt * 3 + which];
+        const int b = which ? bs.y : bs.x;
+        if (x < 0 && b < 0) continue;
+        if (x < 0 || b < 0 || x < b) atomicOr(flag, 2u);
+    }
+    if (lt == 0 && *n_cand > cap) atomicOr(flag, 4u);
+}
+
+// per-tensor sums of per-tile counts (one CTA per tensor)
+__global__ void tensor_sum_kernel(const uint32_t* tile_cnt, const uint32_t* tile0,
+                                  unsigned long long* out) {
+    __shared__ unsigned long long s[33];
+    const uint32_t t = blockIdx.x;
+    unsigned long long acc = 0;
+    for (uint32_t i = tile0[t] + threadIdx.x; i < tile0[t + 1]; i += blockDim.x) acc += tile_cnt[i];
+    unsigned long long tot;
+    block_exclusive_scan<unsigned long long>(acc, s, &tot);
+    if (threadIdx.x == 0) out[t] = tot;
+}
+
+// classify the candidates with the exact thresholds: protected ones into the bitmap,
+// the per-tile / per-tensor counts and the protected-value histogram
+__global__ void cand_classify_kernel(PassIn a, const uint4* cand, const unsigned long long* n_cand,
+                                     unsigned long long cap, const LtParams* lp, uint32_t* pbits,
+                                     uint32_t* tile_prot, unsigned long long* tensor_prot,
+                                     unsigned long long* prot_hist) {
+    const unsigned long long n = min(*n_cand, cap);
+    for (unsigned long long c = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; c < n;
+         c += (unsigned long long)gridDim.x * blockDim.x) {
+        const uint4 q = cand[c];
+        const Tile T = a.tiles[q.x];
+        const int lt = a.types[T.tensor];
+        const float w = __uint_as_float(q.z);
+        if (classify(fabsf(w), __uint_as_float(q.w), a.has_sens, a.metric, lp[lt]) != 2) continue;
+        const uint64_t idx = T.start + q.y;
+        atomicOr(pbits + (idx >> 5), 1u << (idx & 31));
+        atomicAdd(tile_prot + q.x, 1u);
+        if (__float_as_uint(fabsf(w)) < 0x7f800000u) atomicAdd(prot_hist + lt * a.HS + slot_of(w, a.tab), 1ull);
+    }
+}
+
 // magnitude histogram = |w| folded from the signed histogram of w
 __global__ void fold_abs_kernel(const unsigned long long* gw, unsigned long long* gm, int64_t HS,
                                 int64_t NB) {
@@ -1315,6 +1507,83 @@ static void stage_fused_ab(Engine& e, const DevCkpt& c, const PassIn& a, Stage& 
     e.d2h(flag_host, f.flag, 4);
 }
 
+// Pass A2 + candidate classification (see pass_a2_kernel) for the fused step: fills
+// s.gh_val, s.tile_prot / tile_off / tensor_prot, s.d_lp and the protected bitmap.
+// *flag_host (valid after the next sync) non-zero: fall back to pass B.
+static bool a2_eligible(const DevCkpt& c, const Stage& s) {
+    if (c.explicit_scores || c.L->sample_tiles.empty() || getenv("DQTG_NO_PASS_A2")) return false;
+    for (int lt = 0; lt < kLayerTypes; ++lt)
+        if (s.plan.lp[lt].flags & (kDoPrune | kProtectAll)) return false;
+    for (const QJob& j : s.plan.jobs)
+        if (j.which == 2) return false;
+    return true;
+}
+
+static void stage_pass_a2(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s,
+                          const AlphaTables& T, uint32_t* pbits, uint32_t* flag_host) {
+    const Layout& L = *c.L;
+    const int64_t HS = T.HS;
+    cudaStream_t st = e.stream;
+    const size_t hb = (size_t)kLayerTypes * HS * 8;
+    // 1. threshold guess: the quantiles of a thinned tile sample
+    auto* samp = (unsigned long long*)e.buf("q.samp", 2 * hb);
+    DQTG_CUDA(cudaMemsetAsync(samp, 0, 2 * hb, st));
+    PassIn as = a;
+    as.tiles = L.d_sample;
+    as.ntiles = (int)L.sample_tiles.size();
+    stage_pass_a(e, c, as, s.plan.mask_mag, s.plan.mask_sens, samp, samp + (size_t)kLayerTypes * HS);
+    auto* d_lpg = (LtParams*)e.buf("q.lpg", sizeof(LtParams) * kLayerTypes);
+    auto* slots = (int*)e.buf("q.slots", 2 * kLayerTypes * 3 * sizeof(int));
+    DQTG_CUDA(cudaMemsetAsync(slots, 0xff, 2 * kLayerTypes * 3 * sizeof(int), st));
+    stage_thresholds(e, s, HS, T, samp, samp + (size_t)kLayerTypes * HS, d_lpg, slots);
+    auto* lo = (float2*)e.buf("q.clo", sizeof(float2) * kLayerTypes);
+    auto* lo_slot = (int2*)e.buf("q.closlot", sizeof(int2) * kLayerTypes);
+    const char* sh_env = getenv("DQTG_A2_BOUND_SHIFT");
+    { DQTG_SPAN(e, "cand_bounds_kernel"); cand_bounds_kernel<<<1, 32, 0, st>>>(slots, T.d_keyf, T.NB, HS, lo, lo_slot, sh_env ? atoi(sh_env) : 0); }
+    // 2. the streaming pass
+    auto* gh_w = (unsigned long long*)e.buf("q.gh_w", hb);
+    auto* gh = (unsigned long long*)e.buf("q.gh_scores", 2 * hb);  // [magnitude][sensitivity]
+    auto* prot = (unsigned long long*)e.buf("q.prot", hb);
+    auto* small = (unsigned long long*)e.buf("q.a2small", 32);
+    const unsigned long long cap = L.N / 16 + 4096;  // 6 % of the elements
+    auto* cand = (uint4*)e.buf("q.cand2", cap * 16);
+    DQTG_CUDA(cudaMemsetAsync(gh_w, 0, hb, st));
+    DQTG_CUDA(cudaMemsetAsync(gh + (size_t)kLayerTypes * HS, 0, hb, st));
+    DQTG_CUDA(cudaMemsetAsync(prot, 0, hb, st));
+    DQTG_CUDA(cudaMemsetAsync(small, 0, 32, st));
+    DQTG_CUDA(cudaMemsetAsync(a.tile_ctr, 0, 4, st));
+    A2Args f{lo, gh_w, gh + (size_t)kLayerTypes * HS, cand, small, cap};
+    const size_t ct = a.tab.ctab ? ((size_t)a.tab.ctab_n + 1) * 4 : 0;
+    const size_t smem = (size_t)(kWinSlots + kPosSlots) * 4 + ct;
+    ensure_dyn_smem((const void*)pass_a2_kernel, smem);
+    DQTG_CUDA(cudaFuncSetAttribute(pass_a2_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    int per_sm = 0;
+    DQTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass_a2_kernel, kPB, smem));
+    { DQTG_SPAN(e, "pass_a2_kernel"); pass_a2_kernel<<<stream_grid(e, a.ntiles, std::max(1, per_sm)), kPB, smem, st>>>(a, f); }
+    { DQTG_SPAN(e, "fold_abs_kernel"); fold_abs_kernel<<<dim3((unsigned)((HS + 255) / 256), kLayerTypes), 256, 0, st>>>(gh_w, gh, HS, T.NB); }
+    // 3. exact thresholds, bound check, classification, value histogram
+    stage_thresholds(e, s, HS, T, gh, gh + (size_t)kLayerTypes * HS, s.d_lp, slots + kLayerTypes * 3);
+    auto* flag = (uint32_t*)(small + 1);
+    { DQTG_SPAN(e, "cand_check_kernel"); cand_check_kernel<<<1, 32, 0, st>>>(slots + kLayerTypes * 3, lo_slot, small, cap, flag); }
+    DQTG_CUDA(cudaMemsetAsync(pbits, 0, (L.Np + 31) / 32 * 4, st));
+    DQTG_CUDA(cudaMemsetAsync(s.tile_prot, 0, (size_t)a.ntiles * 4 + 4, st));
+    DQTG_CUDA(cudaMemsetAsync(s.tensor_prot, 0, (size_t)(L.nt + 1) * 8, st));
+    { DQTG_SPAN(e, "cand_classify_kernel"); cand_classify_kernel<<<e.num_sms * 4, 256, 0, st>>>(a, cand, small, cap, s.d_lp, pbits, s.tile_prot, s.tensor_prot, prot); }
+    if (L.nt) { DQTG_SPAN(e, "tensor_sum_kernel"); tensor_sum_kernel<<<L.nt, 256, 0, st>>>(s.tile_prot, L.d_tile0, s.tensor_prot); }
+    { DQTG_SPAN(e, "value_hist_kernel"); value_hist_kernel<<<e.num_sms, 256, 0, st>>>(gh_w, prot, s.gh_val, (int64_t)kLayerTypes * HS); }
+    { DQTG_SPAN(e, "scan_u32_kernel"); scan_u32_kernel<<<1, 1024, 0, st>>>(s.tile_prot, a.ntiles, s.tile_off); }
+    e.launched(8);
+    stage_keys(e, L, s, T);
+    e.d2h(flag_host, flag, 4);
+    if (getenv("DQTG_A2_TRACE")) {
+        unsigned long long nc = 0;
+        e.d2h(&nc, small, 8);
+        e.sync();
+        fprintf(stderr, "pass A2: %llu candidates (%.2f %% of %llu), flag %u\n", nc,
+                100.0 * (double)nc / (double)std::max<uint64_t>(1, L.N), (unsigned long long)L.N, *flag_host);
+    }
+}
+
 // After a sync: codebooks of every stage (all k-means problems in one launch).
 static void stage_codebooks(Engine& e, std::vector<Stage*>& stages, const PassIn& a,
                             int64_t HS) {
@@ -1378,6 +1647,7 @@ static void stage_pass_c(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s,
 // not fuse it after all.
 void run_pass_c(Engine& e, const DevCkpt& c, const FuseC& f, QState& q) {
     const Layout& L = *c.L;
+    DQTG_REQUIRE(f.parts, DQTG_ERROR, "deferred pass C without partition codes");
     PassIn a{};
     a.tiles = L.d_tiles;
     a.ntiles = (int)L.tiles.size();
@@ -1422,7 +1692,19 @@ std::unique_ptr<QState> quantize(Engine& e, const DevCkpt& c, const dqtg_config&
     const int64_t HS = T.HS;
     PassIn a = pass_in(e, c, T, (int)cfg.metric);
     stage_alloc(e, L, HS, s, q->d_cb);
-    if (fusable(c, s) && !s.plan.jobs.empty()) {
+    uint32_t* pbits = nullptr;
+    if (defer && !s.plan.jobs.empty() && a2_eligible(c, s)) {
+        // fused step: pass A2 + candidates instead of pass B (partition as a bitmap)
+        uint32_t redo = 0;
+        pbits = (uint32_t*)e.buf("q.pbits", (L.Np + 31) / 32 * 4 + 16);
+        stage_pass_a2(e, c, a, s, T, pbits, &redo);
+        e.check_err();  // syncs: n_keys + protected counts + the bound flag on the host
+        if (redo) {     // an exact threshold below its candidate bound: pass B
+            pbits = nullptr;
+            stage_pass_b(e, c, a, s, T);
+            e.check_err();
+        }
+    } else if (fusable(c, s) && !s.plan.jobs.empty()) {
         uint32_t redo = 0;
         stage_fused_ab(e, c, a, s, T, &redo);
         e.check_err();  // syncs: n_keys + protected counts + the band flag on the host
@@ -1458,7 +1740,8 @@ std::unique_ptr<QState> quantize(Engine& e, const DevCkpt& c, const dqtg_config&
     if (defer) {  // pass C runs inside the DELTA encoder (codec.cu, FuseC)
         stage_level_bounds(e, s);
         defer->w = c.w;
-        defer->parts = s.parts;
+        defer->parts = pbits ? nullptr : s.parts;
+        defer->pbits = pbits;
         defer->lb = s.d_lb;
         defer->lb_stride = (int)s.lb_stride;
         defer->cb_len = s.cb_len;

@@ -1,9 +1,9 @@
 """Pass C fused into the DELTA encoder (codec.cu enc_tile_delta_kernel<true>,
 reached through dqtg_compress_step = Chain::append, chain.cpp:86-129).
 
-The target levels are computed from w and pass B's partition codes inside the
-encoder's tile pass (quantize.cpp:396-423) instead of being written by pass C and
-read back.  Asserted against the oracle, bit for bit: the DELTA record
+The target levels are computed from w and the partition (pass B's 2-bit codes, or
+the protected bitmap of pass A2's candidate list) inside the encoder's tile pass
+(quantize.cpp:396-423) instead of being written by pass C and read back.  Asserted against the oracle, bit for bit: the DELTA record
 (codec.cpp:398-460), the state's levels, protected (pos, bf16) entries and
 codebooks, for every test config (prune / protect / metric / alpha), explicit and
 EMA-derived scores, ragged tensors (sizes that are not multiples of 4, 16 or 64)
@@ -66,17 +66,18 @@ def _step(eng, oracle, cfg, t0, t1, ema, derived, seed=7):
     o0 = oracle.quantize(t0, 3, m0, s0, cfg, seed)
     o1 = oracle.quantize(t1, 4, m1, s1, cfg, seed)
     out = {}
-    for fused in (True, False):
-        if fused:
-            os.environ.pop("DQTG_NO_FUSED_C", None)
-        else:
-            os.environ["DQTG_NO_FUSED_C"] = "1"
+    # fused with pass A2 + candidates (default), fused with pass B, unfused
+    for mode, env in (("fused", {}), ("fused_passb", {"DQTG_NO_PASS_A2": "1"}),
+                      ("fused_a2_fallback", {"DQTG_A2_BOUND_SHIFT": "40"}),
+                      ("unfused", {"DQTG_NO_FUSED_C": "1"})):
+        os.environ.update(env)
         try:
             st, rh = eng.compress_step(_ckpt(eng, t1, ema, derived, oracle), dcfg, seed, 4,
                                        base=base, quality=0.5)
         finally:
-            os.environ.pop("DQTG_NO_FUSED_C", None)
-        out[fused] = (st.download(), eng.record_bytes(rh))
+            for k in env:
+                os.environ.pop(k, None)
+        out[mode] = (st.download(), eng.record_bytes(rh))
     want_rec = oracle.encode_record(o1, o0, 0.5)
     for fused, (got, rec) in out.items():
         assert _qs(got) == o1, ("state", fused)
