@@ -30,7 +30,13 @@ namespace dqtg {
 
 constexpr int kCB = 256;   // threads per codec CTA
 constexpr int kLD = 64;    // dense run-length slots: lengths 2..63
-constexpr int kMaxB = 64;  // cyclic alphabet supported by the shared-memory codec
+constexpr int kMaxB = 64;  // cyclic alphabet of the shared-memory fast path (sparse DELTA, fused)
+// Larger alphabets (quantize.cpp:400-401: u16 levels, B = max levels + 2, codec.cpp:416)
+// run the dense tile kernel with 8-bit ballot keys, the symbol frequencies accumulated
+// in global memory, and the tail kernels' per-group arrays sized for kMaxBLarge; the
+// byte-packed tile codec keeps one byte per key and per delta, with 0xff reserved for
+// "no element", so B <= 255.
+constexpr int kMaxBLarge = 255;
 constexpr int kIt = kTile / kCB;  // 16 elements per thread
 
 __constant__ uint32_t c_crc_pw[kCB];   // x^(8*32*(255-t)) mod P
@@ -198,7 +204,7 @@ struct E1Smem {
 };
 
 __host__ __device__ inline size_t e1_smem_bytes(uint32_t B, uint32_t NS) {
-    return (((size_t)B * NS * 4 + 15) & ~(size_t)15) + (size_t)kCrcTabs * 256 * 4 +
+    return (B > (uint32_t)kMaxB ? 16 : (((size_t)B * NS * 4 + 15) & ~(size_t)15)) + (size_t)kCrcTabs * 256 * 4 +
            (size_t)kNibConsts * 8 * 16 * 4 + (((size_t)8 * B * 4 + 15) & ~(size_t)15) +
            (((size_t)8 * kChunks * B * 2 + 15) & ~(size_t)15) + 32 + kTile / 8 +
            (2 * (size_t)kTile + 16) + (kTile + 32);
@@ -207,7 +213,8 @@ __host__ __device__ inline size_t e1_smem_bytes(uint32_t B, uint32_t NS) {
 __device__ inline E1Smem e1_carve(uint8_t* base, uint32_t B, uint32_t NS) {
     E1Smem S;
     size_t o = 0;
-    S.freq = (uint32_t*)(base + o); o += ((size_t)B * NS * 4 + 15) & ~(size_t)15;
+    S.freq = (uint32_t*)(base + o);  // KB > kMaxB: unused (frequencies in global memory)
+    o += B > (uint32_t)kMaxB ? 16 : (((size_t)B * NS * 4 + 15) & ~(size_t)15);
     S.crc = (uint32_t*)(base + o);  o += (size_t)kCrcTabs * 256 * 4;
     S.nib = (uint32_t*)(base + o);  o += (size_t)kNibConsts * 8 * 16 * 4;
     S.wcnt = (uint32_t*)(base + o); o += ((size_t)8 * B * 4 + 15) & ~(size_t)15;
@@ -249,12 +256,13 @@ __device__ __forceinline__ uint32_t peers_of(uint32_t key) {
 // 0.716 ms at C2).
 constexpr int kBallotEvery = 3;
 
-template <bool HAS_BASE, int NB>
+template <bool HAS_BASE, int NB, int KB>
 __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
     extern __shared__ __align__(16) uint8_t e1_dyn[];
     const uint32_t B = A.B, NS = A.NS;
     const E1Smem S = e1_carve(e1_dyn, B, NS);
-    __shared__ uint32_t s_cnt[kMaxB], s_start[kMaxB + 1], s_run0[kMaxB], s_run1[kMaxB];
+    constexpr bool GF = KB > kMaxB;  // symbol frequencies straight into global memory
+    __shared__ uint32_t s_cnt[KB], s_start[KB + 1], s_run0[KB], s_run1[KB];
     __shared__ unsigned long long s_scan[33];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
@@ -262,7 +270,8 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
 
     for (uint32_t i = tid; i < kCrcTabs * 256; i += kCB) S.crc[i] = (&g_crc_slice[0][0])[i];
     for (uint32_t i = tid; i < kNibConsts * 8 * 16; i += kCB) S.nib[i] = (&g_crc_nib[0][0][0])[i];
-    for (uint32_t i = tid; i < B * NS; i += kCB) S.freq[i] = 0;
+    if (!GF)
+        for (uint32_t i = tid; i < B * NS; i += kCB) S.freq[i] = 0;
     if (tid < 16) S.sd[tid - 16] = 0;
     __shared__ int s_base;
     uint32_t cur_tensor = 0xffffffffu;
@@ -279,7 +288,7 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
         }
         if (T.tensor != cur_tensor) {  // flush the previous tensor's symbol counts
             __syncthreads();
-            if (cur_tensor != 0xffffffffu) {
+            if (!GF && cur_tensor != 0xffffffffu) {
                 uint32_t* gf = A.freq + (size_t)cur_tensor * B * NS;
                 for (uint32_t i = tid; i < B * NS; i += kCB) {
                     const uint32_t c = S.freq[i];
@@ -500,7 +509,9 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
             const bool first = p == s_start[b], last = p + L == s_start[b] + s_cnt[b];
             if (first) s_run0[b] = r;
             if (last) s_run1[b] = r;
-            if (!first && !last) add_symbol(S.freq + b * NS, NS, B, cur_tensor * B + b, v, L, A);
+            if (!first && !last)
+                add_symbol((GF ? A.freq + (size_t)cur_tensor * B * NS : S.freq) + b * NS, NS, B,
+                           cur_tensor * B + b, v, L, A);
         }
         if (tid == 0) A.tile_nruns[ti] = R;
         __syncthreads();
@@ -520,7 +531,7 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
         }
         __syncthreads();
     }
-    if (cur_tensor != 0xffffffffu) {
+    if (!GF && cur_tensor != 0xffffffffu) {
         uint32_t* gf = A.freq + (size_t)cur_tensor * B * NS;
         for (uint32_t i = tid; i < B * NS; i += kCB) {
             const uint32_t c = S.freq[i];
@@ -1797,9 +1808,10 @@ __device__ __forceinline__ void owned_run(const EncArgs& A, const Seg* segs, uns
 }
 
 // E2a: bits per (tile, group), one warp per tile
+template <int KB>
 __global__ void __launch_bounds__(256) enc_bits_kernel(EncArgs A, CodeTabs C, int ntiles,
                                                        uint32_t* segbits) {
-    __shared__ uint32_t s_bits[8][kMaxB];
+    __shared__ uint32_t s_bits[8][KB];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ti = blockIdx.x * 8 + wid;
     if (ti >= ntiles) return;
@@ -1947,6 +1959,7 @@ __global__ void tensor_scan_kernel(TensorRec* tr, uint32_t nt, unsigned long lon
 }
 
 // W: per tensor CTA: static prefix, protected entries, group headers + tables.
+template <int KB>
 __global__ void __launch_bounds__(kCB) write_tensor_kernel(
     EncArgs A, const TensorRec* tr, const uint8_t* statics, const uint64_t* ppos,
     const uint16_t* pval, const unsigned long long* prot_scan, GroupInfo* gi,
@@ -1965,7 +1978,7 @@ __global__ void __launch_bounds__(kCB) write_tensor_kernel(
     if (threadIdx.x == 0) put_uv(p + o, R.ngroups);
     o += uvlen(R.ngroups);
     // group offsets in ascending bucket order (codec.cpp:312-326)
-    __shared__ unsigned long long s_goff[kMaxB];
+    __shared__ unsigned long long s_goff[KB];
     if (threadIdx.x == 0) {
         unsigned long long g = o;
         for (uint32_t b = 0; b < B; ++b) {
@@ -2073,18 +2086,19 @@ __device__ __forceinline__ uint32_t run_bits(const EncArgs& A, const CodeTabs& C
 // MSB-first into per-warp shared words laid out at the destination's bit phase,
 // then copied out as whole 32-bit words (the two boundary words with atomicOr,
 // since they can share bytes with neighbouring segments or headers).
-__global__ void __launch_bounds__(kEmitWarps * 32) enc_emit_kernel(EncArgs A, CodeTabs C,
+template <int KB, int EW = (KB > kMaxB ? 2 : kEmitWarps)>
+__global__ void __launch_bounds__(EW * 32) enc_emit_kernel(EncArgs A, CodeTabs C,
                                                                    const unsigned long long* segoff,
                                                                    const uint32_t* segbits,
                                                                    int ntiles, uint8_t* rec) {
-    __shared__ uint32_t s_stage[kEmitWarps][kWarpStage];
-    __shared__ uint32_t s_segbits[kEmitWarps][kMaxB];
-    __shared__ uint32_t s_segstart[kEmitWarps][kMaxB + 1];
-    __shared__ uint32_t s_sw[kEmitWarps][kMaxB + 1];
-    __shared__ uint32_t s_phase[kEmitWarps][kMaxB];
-    __shared__ unsigned long long s_dw[kEmitWarps][kMaxB];
+    __shared__ uint32_t s_stage[EW][kWarpStage];
+    __shared__ uint32_t s_segbits[EW][KB];
+    __shared__ uint32_t s_segstart[EW][KB + 1];
+    __shared__ uint32_t s_sw[EW][KB + 1];
+    __shared__ uint32_t s_phase[EW][KB];
+    __shared__ unsigned long long s_dw[EW][KB];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ti = blockIdx.x * kEmitWarps + wid;
+    const int ti = blockIdx.x * EW + wid;
     if (ti >= ntiles) return;
     const uint32_t B = A.B, NS = A.NS;
     const Tile T = A.tiles[ti];
@@ -2307,8 +2321,9 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
         DQTG_REQUIRE(B_override >= B, DQTG_ERROR, "alphabet override below the local alphabet");
         B = B_override;
     }
-    DQTG_REQUIRE(B <= (uint32_t)kMaxB, DQTG_ERROR,
-                 "cyclic alphabet larger than the device codec supports (64 levels)");
+    DQTG_REQUIRE(B <= (uint32_t)kMaxBLarge, DQTG_ERROR,
+                 "cyclic alphabet larger than the device codec supports (255 levels)");
+    const bool large = B > (uint32_t)kMaxB;  // 8-bit keys, global frequencies, larger tails
     init_crc_consts();
     cudaStream_t st = e.stream;
     const uint32_t NS = B + kLD;
@@ -2424,7 +2439,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
         // ballot key width: keys < B, invalid elements 0xff -> 2^NB - 1 (> every key)
         // DELTA records: the sparse formulation (work on the non-zero deltas only);
         // FULL records (every delta non-zero) and the ablation modes: dense ranks
-        const bool sparse = base && mode == 0 && !getenv("DQTG_DENSE_DELTA");
+        const bool sparse = base && mode == 0 && !large && !getenv("DQTG_DENSE_DELTA");
         if (fc) {
             FuseC* m = const_cast<FuseC*>(fc);
             m->levels = target.d_levels;
@@ -2434,8 +2449,12 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
         DQTG_REQUIRE(!fc || sparse, DQTG_ERROR, "fused pass C needs the sparse DELTA encoder");
         void (*dfn)(EncArgs, FuseC) = fc ? enc_tile_delta_kernel<true> : enc_tile_delta_kernel<false>;
         auto kfn = sparse ? (void (*)(EncArgs))nullptr
-                 : base ? (B <= 63 ? enc_tile_kernel<true, 6> : enc_tile_kernel<true, 7>)
-                        : (B <= 63 ? enc_tile_kernel<false, 6> : enc_tile_kernel<false, 7>);
+                 : base ? (B <= 63 ? enc_tile_kernel<true, 6, kMaxB>
+                           : B <= 64 ? enc_tile_kernel<true, 7, kMaxB>
+                           : B <= 127 ? enc_tile_kernel<true, 7, kMaxBLarge> : enc_tile_kernel<true, 8, kMaxBLarge>)
+                        : (B <= 63 ? enc_tile_kernel<false, 6, kMaxB>
+                           : B <= 64 ? enc_tile_kernel<false, 7, kMaxB>
+                           : B <= 127 ? enc_tile_kernel<false, 7, kMaxBLarge> : enc_tile_kernel<false, 8, kMaxBLarge>);
         const void* kptr = sparse ? (const void*)dfn : (const void*)kfn;
         const size_t smem = sparse ? dsm_bytes(B, NS) : e1_smem;
         ensure_dyn_smem(kptr, smem);
@@ -2596,7 +2615,11 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     CodeTabs C{code_dense, len_dense, ukey, code_ov, len_ov, gi};
     auto* segbits = (uint32_t*)e.buf("e.segbits32", (size_t)ntiles * B * 4 + 4);
     auto* segoff = (unsigned long long*)e.buf("e.segoff", (size_t)ntiles * B * 8);
-    { DQTG_SPAN(e, "enc_bits_kernel"); enc_bits_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(A, C, ntiles, segbits); }
+    {
+        DQTG_SPAN(e, "enc_bits_kernel");
+        if (large) enc_bits_kernel<kMaxBLarge><<<(ntiles + 7) / 8, 256, 0, st>>>(A, C, ntiles, segbits);
+        else enc_bits_kernel<kMaxB><<<(ntiles + 7) / 8, 256, 0, st>>>(A, C, ntiles, segbits);
+    }
     { DQTG_SPAN(e, "enc_bitscan_kernel"); enc_bitscan_kernel<<<nt * B, kCB, 0, st>>>(A, segbits, segoff, gi); }
     e.launched(2);
 
@@ -2639,10 +2662,14 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     DQTG_CUDA(cudaMemcpyAsync(rec->d_buf, pre.data(), pre.size(), cudaMemcpyHostToDevice, st));
     auto* d_statics = (uint8_t*)e.buf("e.statics", statics.size() + 8);
     DQTG_CUDA(cudaMemcpyAsync(d_statics, statics.data(), statics.size(), cudaMemcpyHostToDevice, st));
-    { DQTG_SPAN(e, "write_tensor_kernel"); write_tensor_kernel<<<nt, kCB, 0, st>>>(A, tr, d_statics, target.d_ppos, target.d_pval, pscan,
+    { DQTG_SPAN(e, "write_tensor_kernel"); (large ? write_tensor_kernel<kMaxBLarge> : write_tensor_kernel<kMaxB>)<<<nt, kCB, 0, st>>>(A, tr, d_statics, target.d_ppos, target.d_pval, pscan,
                                             gi, tab_sym, tab_len, rec->d_buf); }
     if (np) { DQTG_SPAN(e, "write_prot_kernel"); write_prot_kernel<<<pgrid, 256, 0, st>>>(tr, nt, np, target.d_ppos, target.d_pval, pscan, rec->d_buf); }
-    { DQTG_SPAN(e, "enc_emit_kernel"); enc_emit_kernel<<<(ntiles + kEmitWarps - 1) / kEmitWarps, kEmitWarps * 32, 0, st>>>(A, C, segoff, segbits, ntiles, rec->d_buf); }
+    {
+        DQTG_SPAN(e, "enc_emit_kernel");
+        if (large) enc_emit_kernel<kMaxBLarge><<<(ntiles + 1) / 2, 2 * 32, 0, st>>>(A, C, segoff, segbits, ntiles, rec->d_buf);
+        else enc_emit_kernel<kMaxB><<<(ntiles + kEmitWarps - 1) / kEmitWarps, kEmitWarps * 32, 0, st>>>(A, C, segoff, segbits, ntiles, rec->d_buf);
+    }
     { DQTG_SPAN(e, "finish_crc_kernel"); finish_crc_kernel<<<1, 1, 0, st>>>(A.crc_acc, 2 * L.N, rec->d_buf + total - 4, nullptr); }
     e.launched(3);
     DQTG_CUDA(cudaGetLastError());

@@ -309,9 +309,10 @@ __global__ void rle_fill_kernel(const uint32_t* sidx, uint64_t ntot, const int32
 
 // ---- U: unrearrange ------------------------------------------------------------
 // U1: per tile, count of elements per previous level
+template <int KB>
 __global__ void __launch_bounds__(256) prev_count_kernel(const Tile* tiles, const uint16_t* prev,
                                                          uint32_t B, uint32_t* tile_cnt, uint32_t* err) {
-    __shared__ uint32_t s_c[64];
+    __shared__ uint32_t s_c[KB];
     const Tile T = tiles[blockIdx.x];
     for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) s_c[b] = 0;
     __syncthreads();
@@ -351,6 +352,7 @@ __global__ void __launch_bounds__(256) prev_scan_kernel(const uint32_t* tile0, u
 // U3: per tile, stable rank of every element among equal previous levels (warp
 // ranges of 512 elements, 32-element chunks matched on the key), delta gathered
 // from the element's rearranged position, cur = (prev - d) mod B, range checks
+template <int KB>
 __global__ void __launch_bounds__(256) unrearrange_kernel(const Tile* tiles, const uint8_t* types,
                                                           const uint64_t* stream_off,
                                                           const uint64_t* off, const uint16_t* prev,
@@ -358,12 +360,12 @@ __global__ void __launch_bounds__(256) unrearrange_kernel(const Tile* tiles, con
                                                           const unsigned long long* gstart,
                                                           const uint8_t* d, const uint32_t* cb_len,
                                                           uint16_t* cur, uint32_t* err) {
-    __shared__ uint32_t s_wc[8][64];  // per-warp key counts -> per-warp key bases
-    __shared__ uint32_t s_base[64];
+    __shared__ uint32_t s_wc[8][KB];  // per-warp key counts -> per-warp key bases
+    __shared__ uint32_t s_base[KB];
     const Tile T = tiles[blockIdx.x];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
-    for (int i = tid; i < 8 * 64; i += 256) (&s_wc[0][0])[i] = 0;
+    for (int i = tid; i < 8 * KB; i += 256) (&s_wc[0][0])[i] = 0;
     __syncthreads();
     uint32_t rk[16], ky[16];
 #pragma unroll
@@ -503,7 +505,8 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
         throw Fail(DQTG_CHAIN_CORRUPT, "base step mismatch: record expects " +
                                            std::to_string(base_step) + ", got " +
                                            std::to_string(base->step));
-    DQTG_REQUIRE(B >= 1 && B <= 64, DQTG_CORRUPT_INDEX, "cyclic alphabet outside the device decoder's range");
+    // deltas are staged as bytes and keys index per-tile shared arrays: B <= 255
+    DQTG_REQUIRE(B >= 1 && B <= 255, DQTG_CORRUPT_INDEX, "cyclic alphabet outside the device decoder's range");
     auto q = std::make_unique<QState>();
     q->eng = &e;
     q->step = target_step;
@@ -852,10 +855,10 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
         e.to_device(d_cbl, q->cb_len, sizeof(q->cb_len));
         const uint16_t* prev = base ? base->d_levels : nullptr;
         if (ntiles) {
-            { DQTG_SPAN(e, "prev_count_kernel"); prev_count_kernel<<<ntiles, 256, 0, st>>>(L.d_tiles, prev, B, d_tc, e.d_err); }
+            { DQTG_SPAN(e, "prev_count_kernel"); (B <= 64 ? prev_count_kernel<64> : prev_count_kernel<256>)<<<ntiles, 256, 0, st>>>(L.d_tiles, prev, B, d_tc, e.d_err); }
             auto* d_tot = (unsigned long long*)e.buf("d.ktot", (size_t)nt * B * 8 + 8);
             { DQTG_SPAN(e, "prev_scan_kernel"); prev_scan_kernel<<<nt * B, 256, 0, st>>>(L.d_tile0, B, d_tc, d_relems, d_tot, e.d_err); }
-            { DQTG_SPAN(e, "unrearrange_kernel"); unrearrange_kernel<<<ntiles, 256, 0, st>>>(L.d_tiles, L.d_types, L.d_stream_off, L.d_off, prev, B, d_tc, d_gs, d_d, d_cbl, q->d_levels, e.d_err); }
+            { DQTG_SPAN(e, "unrearrange_kernel"); (B <= 64 ? unrearrange_kernel<64> : unrearrange_kernel<256>)<<<ntiles, 256, 0, st>>>(L.d_tiles, L.d_types, L.d_stream_off, L.d_off, prev, B, d_tc, d_gs, d_d, d_cbl, q->d_levels, e.d_err); }
             e.launched(3);
         }
         e.check_err();

@@ -1049,6 +1049,8 @@ __global__ void __launch_bounds__(kPB) eval_c_kernel(PassIn a, const LtParams* l
             double d = __dsub_rn((double)wa[j], (double)deq);
             acc = __dadd_rn(acc, __dmul_rn(d, d));
             if (lv < 66) atomicAdd(&s_cnt[lv], 1u);
+            else if ((int)lv < lstride)  // large alphabets: straight to the tensor's counts
+                atomicAdd(lvl_counts + (size_t)T.tensor * lstride + lv, 1ull);
         }
     }
     double t = block_sum_d(acc, s_red);
@@ -1137,6 +1139,8 @@ __global__ void __launch_bounds__(kPB) eval_multi_kernel(PassIn a, const LtParam
                 const double d = __dsub_rn((double)wa[j], (double)deq);
                 acc[c] = __dadd_rn(acc[c], __dmul_rn(d, d));
                 if (lv < 66) atomicAdd(&s_cnt[c][lv], 1u);
+                else if ((int)lv < ev.lstride)  // large alphabets: straight to global
+                    atomicAdd(ev.counts + ((size_t)c * ev.nt + T.tensor) * ev.lstride + lv, 1ull);
             }
         }
     }
@@ -1952,7 +1956,7 @@ void eval_batch(Engine& e, const DevCkpt& c, const dqtg_config* cfgs, const uint
     std::map<uint64_t, std::pair<unsigned long long*, unsigned long long*>> scores_by_alpha;
     int lstride = 2;
     for (uint32_t i = 0; i < m; ++i) lstride = std::max<int>(lstride, std::max(cfgs[i].bins, cfgs[i].embed_bins) + 2);
-    DQTG_REQUIRE(lstride <= 66, DQTG_ERROR, "eval_batch supports up to 64 bins");
+    DQTG_REQUIRE(lstride <= 4098, DQTG_ERROR, "eval_batch supports up to 4096 bins");
     for (uint32_t i = 0; i < m; ++i) {
         auto s = std::make_unique<Stage>();
         s->tag = "ev" + std::to_string(i) + ".";
