@@ -241,11 +241,17 @@ def run_reference(args):
 
 # ---------------------------------------------------------------------------- our arm
 ALGO_BYTES = {  # algorithmic HBM bytes per parameter per launch
-    "pass_a_kernel": 8.0,   # read w + EMA
+    # fused pass C + sparse DELTA tile pass (compress_step): read w, the protected
+    # bitmap (1/8 B) and the previous levels, write the target levels once
+    "quant_delta_kernel": 4.0 + 0.125 + 2.0 + 2.0,
+    "pass_a2_kernel": 8.0,  # read w + EMA (score histograms + protected candidates)
     "pass_b_kernel": 8.25,  # read w + EMA, write 2-bit partition codes
     "pass_c_kernel": 6.25,  # read w + partition codes, write levels
+    "enc_tile_delta_kernel": 4.0,  # read levels + previous levels
     "enc_tile_kernel": 4.0,  # read levels + previous levels
 }
+# span name -> kernel name in the ncu report (profiles/ncu_traffic.json)
+NCU_NAME = {"quant_delta_kernel": "enc_tile_delta_kernel"}
 
 
 def write_dqt1(path, layout, flat, step=0):
@@ -650,7 +656,7 @@ def run_ours(args):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(dom)
+            traffic = json.load(f).get(NCU_NAME.get(dom, dom))
     except Exception:
         pass
     step_algo = (12.0 + 4.0 / cr) * N  # SURVEY.md §8d, sensitivity present
