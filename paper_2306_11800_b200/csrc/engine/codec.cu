@@ -1511,8 +1511,8 @@ __global__ void ov_group_max_kernel(const unsigned long long* ukey, const unsign
 // distinct run lengths in billion-element tensors, C5) keep it in global memory and
 // sort with 1024 threads, then continue on warp 0.  glist: the tier's groups;
 // gws/goff (BIG): per group (byte offset, n_pad) of its global working set.
-template <bool BIG>
-__global__ void __launch_bounds__(BIG ? 1024 : 32) enc_huffman_kernel(EncArgs A, const unsigned long long* elems,
+template <bool GWS, int NT>  // GWS: working set in global memory (gws/goff); NT threads per group
+__global__ void __launch_bounds__(NT) enc_huffman_kernel(EncArgs A, const unsigned long long* elems,
                                                           const unsigned long long* ukey,
                                                           const unsigned long long* ucnt,
                                                           const unsigned long long* nu_p,
@@ -1533,7 +1533,7 @@ __global__ void __launch_bounds__(BIG ? 1024 : 32) enc_huffman_kernel(EncArgs A,
     // more single-warp CTAs stay resident per SM.
     extern __shared__ unsigned long long s_dyn[];
     unsigned long long* s_keys = s_dyn;
-    if (BIG) {
+    if (GWS) {
         s_keys = (unsigned long long*)(gws + goff[2 * blockIdx.x]);
         n_pad = (uint32_t)goff[2 * blockIdx.x + 1];
     }
@@ -1588,7 +1588,7 @@ __global__ void __launch_bounds__(BIG ? 1024 : 32) enc_huffman_kernel(EncArgs A,
             n += (uint32_t)min(32ull, G.ov_end - j0);
         }
     }
-    if (BIG) {  // n from warp 0
+    if (NT > 32) {  // n from warp 0
         if (threadIdx.x == 0) s_n = n;
         __syncthreads();
         n = s_n;
@@ -1620,7 +1620,7 @@ __global__ void __launch_bounds__(BIG ? 1024 : 32) enc_huffman_kernel(EncArgs A,
             __syncthreads();
         }
     for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) perm[r] = (uint32_t)(s_keys[r] & 0xffffffu);
-    if (BIG) {  // the rest is warp 0's
+    if (NT > 32) {  // the rest is warp 0's
         __syncthreads();
         if (threadIdx.x >= 32) return;
     }
@@ -2590,7 +2590,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
         DQTG_SPAN(e, "enc_huffman_kernel");
         const uint32_t* gl = d_gl;
         if (!tiers[0].empty()) {
-            enc_huffman_kernel<false><<<(unsigned)tiers[0].size(), 32, 128 * 38 + 16, st>>>(
+            enc_huffman_kernel<false, 32><<<(unsigned)tiers[0].size(), 32, 128 * 38 + 16, st>>>(
                 A, elems, ukey, ucnt, nu, gi, tab_sym, tab_len, code_dense, len_dense, code_ov, len_ov,
                 W, 128, ov_range, gl, nullptr, nullptr);
             gl += tiers[0].size();
@@ -2598,15 +2598,16 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
         }
         if (!tiers[1].empty()) {
             const size_t hsm = (size_t)np_mid * 38 + 16;
-            ensure_dyn_smem((const void*)enc_huffman_kernel<false>, hsm);
-            enc_huffman_kernel<false><<<(unsigned)tiers[1].size(), 32, hsm, st>>>(
+            // the bitonic sort of a mid-size alphabet with 256 threads, then warp 0
+            ensure_dyn_smem((const void*)enc_huffman_kernel<false, 256>, hsm);
+            enc_huffman_kernel<false, 256><<<(unsigned)tiers[1].size(), 256, hsm, st>>>(
                 A, elems, ukey, ucnt, nu, gi, tab_sym, tab_len, code_dense, len_dense, code_ov, len_ov,
                 W, np_mid, ov_range, gl, nullptr, nullptr);
             gl += tiers[1].size();
             e.launched();
         }
         if (!tiers[2].empty()) {
-            enc_huffman_kernel<true><<<(unsigned)tiers[2].size(), 1024, 0, st>>>(
+            enc_huffman_kernel<true, 1024><<<(unsigned)tiers[2].size(), 1024, 0, st>>>(
                 A, elems, ukey, ucnt, nu, gi, tab_sym, tab_len, code_dense, len_dense, code_ov, len_ov,
                 W, 0, ov_range, gl, d_goff, d_gws);
             e.launched();

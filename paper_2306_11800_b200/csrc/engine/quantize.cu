@@ -621,18 +621,40 @@ __global__ void cand_classify_kernel(PassIn a, const uint4* cand, const unsigned
                                      unsigned long long cap, const LtParams* lp, uint32_t* pbits,
                                      uint32_t* tile_prot, unsigned long long* tensor_prot,
                                      unsigned long long* prot_hist) {
+    // consecutive candidates come from the same warp append, i.e. the same tile and
+    // nearby elements: the atomics are aggregated over the lanes that share a target
     const unsigned long long n = min(*n_cand, cap);
-    for (unsigned long long c = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; c < n;
-         c += (unsigned long long)gridDim.x * blockDim.x) {
-        const uint4 q = cand[c];
-        const Tile T = a.tiles[q.x];
-        const int lt = a.types[T.tensor];
-        const float w = __uint_as_float(q.z);
-        if (classify(fabsf(w), __uint_as_float(q.w), a.has_sens, a.metric, lp[lt]) != 2) continue;
-        const uint64_t idx = T.start + q.y;
-        atomicOr(pbits + (idx >> 5), 1u << (idx & 31));
-        atomicAdd(tile_prot + q.x, 1u);
-        if (__float_as_uint(fabsf(w)) < 0x7f800000u) atomicAdd(prot_hist + lt * a.HS + slot_of(w, a.tab), 1ull);
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long c0 = blockIdx.x * (unsigned long long)blockDim.x; c0 < n; c0 += stride) {
+        const unsigned long long c = c0 + threadIdx.x;
+        bool prot = false;
+        uint32_t tile = 0xffffffffu, word = 0xffffffffu, bit = 0;
+        long long slot = -1;
+        int lt = 0;
+        if (c < n) {
+            const uint4 q = cand[c];
+            const Tile T = a.tiles[q.x];
+            lt = a.types[T.tensor];
+            const float w = __uint_as_float(q.z);
+            prot = classify(fabsf(w), __uint_as_float(q.w), a.has_sens, a.metric, lp[lt]) == 2;
+            if (prot) {
+                const uint64_t idx = T.start + q.y;
+                tile = q.x;
+                word = (uint32_t)(idx >> 5);
+                bit = 1u << (idx & 31);
+                if (__float_as_uint(fabsf(w)) < 0x7f800000u) slot = lt * a.HS + slot_of(w, a.tab);
+            }
+        }
+        const uint32_t act = __ballot_sync(0xffffffffu, prot);
+        if (!prot) continue;
+        const int lane = threadIdx.x & 31;
+        const uint32_t pw = __match_any_sync(act, word);
+        const uint32_t ob = __reduce_or_sync(pw, bit);
+        if (lane == __ffs(pw) - 1) atomicOr(pbits + word, ob);
+        const uint32_t pt = __match_any_sync(act, tile);
+        if (lane == __ffs(pt) - 1) atomicAdd(tile_prot + tile, (uint32_t)__popc(pt));
+        const uint32_t ps = __match_any_sync(act, (unsigned long long)slot);
+        if (slot >= 0 && lane == __ffs(ps) - 1) atomicAdd(prot_hist + slot, (unsigned long long)__popc(ps));
     }
 }
 
