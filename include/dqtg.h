@@ -201,6 +201,14 @@ void dqtg_record_destroy(dqtg_record *r);
 /* decode_delta_record(record, base) (codec.cpp:513-597) */
 dqtg_status dqtg_decode_record(dqtg_engine *e, const uint8_t *rec, uint64_t n,
                                const dqtg_qstate *base, dqtg_qstate **out);
+/* Chain::restore (chain.cpp:131-154): host records recs[0..n) decoded in order, each
+ * against the previous one (recs[0] against base, or none for a FULL record); the host
+ * walk of record k+1 overlaps the device decode of record k.  fn(user, k, state) sees
+ * every decoded state (borrowed for the call); *last_out receives the last one. */
+typedef void (*dqtg_state_fn)(void *user, uint64_t k, const dqtg_qstate *state);
+dqtg_status dqtg_decode_chain(dqtg_engine *e, uint32_t n, const uint8_t *const *recs,
+                              const uint64_t *sizes, const dqtg_qstate *base, dqtg_state_fn fn,
+                              void *user, dqtg_qstate **last_out);
 
 /* ---- tensor-sharded checkpoints (multi-GPU) ----------------
  * Thresholds and codebooks must come from the histograms of the WHOLE

@@ -15,6 +15,7 @@ records on the device (``Engine.decode_record``).
 from __future__ import annotations
 
 import os
+import struct
 import secrets
 from dataclasses import dataclass
 from typing import Optional
@@ -190,14 +191,29 @@ class DeviceChain:
             if start == 0:
                 raise _corrupt(f"no FULL record precedes step {step}")
             start -= 1
-        state = None
-        for e in self.entries[start:idx + 1]:
+        ents = self.entries[start:idx + 1]
+        recs = []
+        for e in ents:
             with open(self.record_path(e), "rb") as f:
-                rec = f.read()
-            state = self.engine.decode_record(rec, base=None if e.full else state)
-            if int(state.info().step) != e.step:
-                raise _corrupt(f"record step {int(state.info().step)} disagrees with manifest "
-                               f"step {e.step}")
+                recs.append(f.read())
+        # the decoded step is the record header's target step (bytes 17..24): the first
+        # record whose header disagrees with the manifest ends the replay there -- after
+        # the records up to it decoded, as the reference's sequential restore checks it
+        stop = None
+        for k, (e, rec) in enumerate(zip(ents, recs)):
+            if len(rec) >= 25 and struct.unpack_from("<Q", rec, 17)[0] != e.step:
+                stop = k
+                break
+        last = len(recs) if stop is None else stop + 1
+        # a manifest FULL entry restarts the chain with no base (chain.cpp:146)
+        state, k0 = None, 0
+        for k in range(1, last + 1):
+            if k == last or ents[k].full:
+                state = self.engine.decode_chain(recs[k0:k], base=None if ents[k0].full else state)
+                k0 = k
+        if stop is not None:
+            raise _corrupt(f"record step {int(state.info().step)} disagrees with manifest "
+                           f"step {ents[stop].step}")
         return state
 
     def restore_latest(self) -> E.DevState:

@@ -553,6 +553,31 @@ dqtg_status dqtg_decode_record(dqtg_engine* h, const uint8_t* rec, uint64_t n,
     });
 }
 
+dqtg_status dqtg_decode_chain(dqtg_engine* h, uint32_t n, const uint8_t* const* recs,
+                              const uint64_t* sizes, const dqtg_qstate* base, dqtg_state_fn fn,
+                              void* user, dqtg_qstate** last_out) {
+    return guard([&] {
+        LOCK(&h->e);
+        auto last = ::dqtg::decode_chain(
+            h->e, recs, sizes, n, base ? base->q.get() : nullptr,
+            [&](uint32_t k, const ::dqtg::QState& s) {
+                if (!fn) return;
+                dqtg_qstate tmp;  // borrowed for the callback
+                tmp.q.reset(const_cast<::dqtg::QState*>(&s));
+                fn(user, k, &tmp);
+                (void)tmp.q.release();
+            });
+        if (last_out) {
+            *last_out = nullptr;
+            if (last) {
+                auto* s = new dqtg_qstate();
+                s->q = std::move(last);
+                *last_out = s;
+            }
+        }
+    });
+}
+
 uint64_t dqtg_shard_hist_len(dqtg_engine* h, const dqtg_config* cfg, int which) {
     uint64_t n = 0;
     dqtg_status st = guard([&] {

@@ -25,7 +25,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
+#include <functional>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "engine.h"
@@ -53,6 +56,40 @@ struct GroupDesc {
 struct ChunkDesc {
     uint32_t group;
     uint32_t local;  // chunk index inside its group
+};
+
+// the delta base as the host walk needs it: its step and tensor table
+struct BaseInfo {
+    uint64_t step = 0;
+    std::vector<std::string> names;
+    std::vector<uint8_t> types, ranks;
+    std::vector<std::vector<uint64_t>> dims;
+};
+
+// a record after the host walk (decode_plan), before the device decode (decode_run)
+struct DecodePlan {
+    std::vector<uint8_t> host_copy;  // the record, when it was handed over in device memory
+    const uint8_t* h = nullptr;
+    uint64_t n = 0;
+    bool has_base = false;
+    uint64_t target_step = 0;
+    uint32_t B = 0, nt = 0;
+    std::unique_ptr<QState> q;  // step, config, codebooks
+    std::vector<std::string> names;
+    std::vector<uint8_t> types, ranks;
+    std::vector<uint64_t> dims;
+    std::vector<std::vector<uint64_t>> ppos;
+    std::vector<std::vector<uint16_t>> pval;
+    std::vector<GroupDesc> groups;
+    std::vector<ChunkDesc> chunks;
+    std::vector<int64_t> tab_sym;
+    std::vector<uint8_t> tab_len;
+    std::vector<unsigned long long> rec_elems, gstart_h;
+    std::vector<uint64_t> lim, first;
+    std::vector<uint32_t> lbase;
+    uint64_t sym_total = 0;
+    std::string deferred_index;
+    uint32_t stored_crc = 0;
 };
 
 // ---- bit access: MSB-first stream (codec.cpp:111-122) -------------------------
@@ -470,7 +507,13 @@ struct Rd {
 
 }  // namespace
 
-std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n, const QState* base) {
+// Host walk of a record (decode_delta_record's parse, codec.cpp:513-597): everything
+// that does not need the base's levels, in the reference's validation order.  `base`
+// describes the delta base (step + tensor table) -- a decoded state, or the plan of
+// the previous record of a chain, so the walk of record k+1 can overlap the device
+// decode of record k (decode_chain).
+std::unique_ptr<DecodePlan> decode_plan(Engine& e, const uint8_t* rec, uint64_t n, const BaseInfo* base) {
+    auto P = std::make_unique<DecodePlan>();
     cudaStream_t st = e.stream;
     const bool trace = getenv("DQTG_DECODE_TRACE") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
@@ -480,7 +523,7 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     };
     // the record may live in device memory: decode from a host copy of its structure
-    std::vector<uint8_t> host_copy;
+    auto& host_copy = P->host_copy;
     const uint8_t* h = rec;
     if (is_device_ptr(rec)) {
         host_copy.resize(n);
@@ -488,6 +531,8 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
         e.sync();
         h = host_copy.data();
     }
+    P->h = h;
+    P->n = n;
     Rd r{h, n};
     {
         r.need(4);
@@ -499,6 +544,9 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
     const bool has_base = r.u8() != 0;
     const uint64_t base_step = r.le<uint64_t>(), target_step = r.le<uint64_t>();
     const uint32_t B = r.le<uint32_t>();
+    P->has_base = has_base;
+    P->target_step = target_step;
+    P->B = B;
     if (has_base && !base) throw Fail(DQTG_CHAIN_CORRUPT, "delta record requires its base state");
     if (!has_base) base = nullptr;
     if (base && base->step != base_step)
@@ -507,7 +555,8 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
                                            std::to_string(base->step));
     // deltas are staged as bytes and keys index per-tile shared arrays: B <= 255
     DQTG_REQUIRE(B >= 1 && B <= 255, DQTG_CORRUPT_INDEX, "cyclic alphabet outside the device decoder's range");
-    auto q = std::make_unique<QState>();
+    P->q = std::make_unique<QState>();
+    QState* q = P->q.get();
     q->eng = &e;
     q->step = target_step;
     dqtg_config& cfg = q->cfg;
@@ -530,24 +579,35 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
         q->cb_len[lt] = len;
     }
     const uint32_t nt = r.le<uint32_t>();
-    if (base && base->L->nt != nt) throw Fail(DQTG_CHAIN_CORRUPT, "base tensor count mismatch");
-    std::string deferred_index;  // CorruptIndex found while parsing, reported after H/R
+    P->nt = nt;
+    if (base && base->names.size() != nt) throw Fail(DQTG_CHAIN_CORRUPT, "base tensor count mismatch");
+    std::string& deferred_index = P->deferred_index;  // CorruptIndex found while parsing, reported after H/R
     // a corrupt count must not size host tables: every tensor takes >= 6 record bytes
     // (the reference's reserve() would throw std::length_error / bad_alloc here)
     if (nt > (r.n - r.at) / 6) throw Fail(DQTG_TRUNCATED, "tensor count exceeds the record size");
     // tensors
-    std::vector<std::string> names(nt);
-    std::vector<uint8_t> types(nt), ranks(nt);
-    std::vector<uint64_t> dims;
-    std::vector<std::vector<uint64_t>> ppos(nt);
-    std::vector<std::vector<uint16_t>> pval(nt);
-    std::vector<GroupDesc> groups;
-    std::vector<ChunkDesc> chunks;
-    std::vector<int64_t> tab_sym;
-    std::vector<uint8_t> tab_len;
-    std::vector<unsigned long long> rec_elems((size_t)nt * B, 0), gstart_h((size_t)nt * B, 0);
-    std::vector<uint64_t> lim, first;
-    std::vector<uint32_t> lbase;
+    auto& names = P->names;
+    auto& types = P->types;
+    auto& ranks = P->ranks;
+    auto& dims = P->dims;
+    auto& ppos = P->ppos;
+    auto& pval = P->pval;
+    auto& groups = P->groups;
+    auto& chunks = P->chunks;
+    auto& tab_sym = P->tab_sym;
+    auto& tab_len = P->tab_len;
+    auto& rec_elems = P->rec_elems;
+    auto& gstart_h = P->gstart_h;
+    auto& lim = P->lim;
+    auto& first = P->first;
+    auto& lbase = P->lbase;
+    names.resize(nt);
+    types.resize(nt);
+    ranks.resize(nt);
+    ppos.resize(nt);
+    pval.resize(nt);
+    rec_elems.assign((size_t)nt * B, 0);
+    gstart_h.assign((size_t)nt * B, 0);
     uint64_t stream_pos = 0, sym_total = 0;
     for (uint32_t i = 0; i < nt; ++i) {
         names[i] = r.str();
@@ -596,9 +656,8 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
             ppos[i][k] = pos;
         }
         if (base) {
-            const Layout& BL = *base->L;
-            if (BL.names[i] != names[i] || BL.types[i] != types[i] || BL.ranks[i] != ranks[i] ||
-                !std::equal(BL.dims[i].begin(), BL.dims[i].end(), dims.end() - ranks[i]))
+            if (base->names[i] != names[i] || base->types[i] != types[i] || base->ranks[i] != ranks[i] ||
+                !std::equal(base->dims[i].begin(), base->dims[i].end(), dims.end() - ranks[i]))
                 throw Fail(DQTG_CHAIN_CORRUPT, "base tensor layout mismatch at " + names[i]);
         }
         // groups of the payload (codec.cpp:283-300)
@@ -697,9 +756,44 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
         if (total != numel) throw Fail(DQTG_CORRUPT_INDEX, "group totals do not cover the tensor");
         stream_pos += numel;
     }
-    const uint32_t stored_crc = r.le<uint32_t>();
+    P->stored_crc = r.le<uint32_t>();
     if (r.at != n) throw Fail(DQTG_IO, "trailing bytes after DQDR record");
-    mark("parsed");
+    P->sym_total = sym_total;
+    return P;
+}
+
+// Device decode of a planned record against its base state (the base's levels are
+// only read here).
+std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base) {
+    cudaStream_t st = e.stream;
+    const bool trace = getenv("DQTG_DECODE_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (trace)
+            fprintf(stderr, "decode %-12s %8.3f ms\n", what,
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    };
+    if (!P.has_base) base = nullptr;
+    std::unique_ptr<QState> q = std::move(P.q);
+    const uint32_t B = P.B, nt = P.nt;
+    const uint64_t n = P.n, target_step = P.target_step, sym_total = P.sym_total;
+    const uint8_t* rec = P.h;
+    auto& names = P.names;
+    auto& types = P.types;
+    auto& ranks = P.ranks;
+    auto& dims = P.dims;
+    auto& ppos = P.ppos;
+    auto& pval = P.pval;
+    auto& groups = P.groups;
+    auto& chunks = P.chunks;
+    auto& tab_sym = P.tab_sym;
+    auto& lim = P.lim;
+    auto& first = P.first;
+    auto& lbase = P.lbase;
+    auto& rec_elems = P.rec_elems;
+    auto& gstart_h = P.gstart_h;
+    const std::string& deferred_index = P.deferred_index;
+    const uint32_t stored_crc = P.stored_crc;
 
     // state layout from the record
     dqtg_layout dl{};
@@ -870,6 +964,86 @@ std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
     if (crc != stored_crc)
         throw Fail(DQTG_CHECKSUM_MISMATCH, "record checksum mismatch at step " + std::to_string(target_step));
     return q;
+}
+
+BaseInfo base_info(const QState& s) {
+    BaseInfo b;
+    b.step = s.step;
+    b.names = s.L->names;
+    b.types = s.L->types;
+    b.ranks = s.L->ranks;
+    b.dims = s.L->dims;
+    return b;
+}
+
+// the target of a planned record as the base of the next record of a chain
+BaseInfo base_info(const DecodePlan& p) {
+    BaseInfo b;
+    b.step = p.target_step;
+    b.names = p.names;
+    b.types = p.types;
+    b.ranks = p.ranks;
+    size_t o = 0;
+    for (uint32_t i = 0; i < p.nt; ++i) {
+        b.dims.emplace_back(p.dims.begin() + (long)o, p.dims.begin() + (long)(o + p.ranks[i]));
+        o += p.ranks[i];
+    }
+    return b;
+}
+
+// Chain::restore (chain.cpp:131-154) over host records: the host walk of record k+1
+// runs on a helper thread while the device decodes record k (the walk needs only the
+// previous record's step and tensor table, not its levels).  on_state(k, state) sees
+// every decoded state; the last one is returned.  An error in record k+1 surfaces
+// after record k is decoded, as in the reference's sequential restore.
+std::unique_ptr<QState> decode_chain(Engine& e, const uint8_t* const* recs, const uint64_t* sizes,
+                                     uint32_t n, const QState* base,
+                                     const std::function<void(uint32_t, const QState&)>& on_state) {
+    if (!n) return nullptr;
+    for (uint32_t k = 0; k < n; ++k)
+        DQTG_REQUIRE(!is_device_ptr(recs[k]), DQTG_ERROR, "decode_chain takes host records");
+    BaseInfo b0;
+    if (base) b0 = base_info(*base);
+    std::unique_ptr<DecodePlan> cur = decode_plan(e, recs[0], sizes[0], base ? &b0 : nullptr);
+    std::unique_ptr<QState> prev;
+    const QState* pb = base;
+    for (uint32_t k = 0; k < n; ++k) {
+        std::unique_ptr<DecodePlan> next;
+        std::exception_ptr perr;
+        std::thread th;
+        BaseInfo bn;
+        if (k + 1 < n) {
+            bn = base_info(*cur);
+            th = std::thread([&] {
+                try {
+                    next = decode_plan(e, recs[k + 1], sizes[k + 1], &bn);
+                } catch (...) {
+                    perr = std::current_exception();
+                }
+            });
+        }
+        std::unique_ptr<QState> s;
+        try {
+            s = decode_run(e, *cur, pb);
+            if (on_state) on_state(k, *s);
+        } catch (...) {
+            if (th.joinable()) th.join();
+            throw;
+        }
+        if (th.joinable()) th.join();
+        if (perr) std::rethrow_exception(perr);
+        prev = std::move(s);
+        pb = prev.get();
+        cur = std::move(next);
+    }
+    return prev;
+}
+
+std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n, const QState* base) {
+    BaseInfo bi;
+    if (base) bi = base_info(*base);
+    auto plan = decode_plan(e, rec, n, base ? &bi : nullptr);
+    return decode_run(e, *plan, base);
 }
 
 }  // namespace dqtg

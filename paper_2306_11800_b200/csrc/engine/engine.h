@@ -327,6 +327,10 @@ std::unique_ptr<Record> encode_record(Engine& e, const QState* base, const QStat
                                       double quality);
 std::unique_ptr<QState> decode_record(Engine& e, const uint8_t* rec, uint64_t n,
                                       const QState* base);
+// records of a chain decoded in order (host walk of k+1 overlapping the device decode of k)
+std::unique_ptr<QState> decode_chain(Engine& e, const uint8_t* const* recs, const uint64_t* sizes,
+                                     uint32_t n, const QState* base,
+                                     const std::function<void(uint32_t, const QState&)>& on_state);
 void dequantize(Engine& e, const QState& q, float* out_dev_padded);
 // same step, layout, codebooks, levels and protected entries (compared on the device)
 bool states_equal(Engine& e, const QState& a, const QState& b);

@@ -67,6 +67,8 @@ _P = C.c_void_p
 
 # void (*)(void* user, uint64_t k, const dqtg_record* record)
 RECORD_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.c_void_p)
+# void (*)(void* user, uint64_t k, const dqtg_qstate* state)
+STATE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.c_void_p)
 
 
 def _load():
@@ -134,6 +136,7 @@ def _load():
         "dqtg_qstate_equal": (C.c_int, [_P, _P, _P, C.POINTER(C.c_int)]),
         "dqtg_ckpt_release": (C.c_int, [_P]),
         "dqtg_engine_trim": (C.c_int, [_P]),
+        "dqtg_decode_chain": (C.c_int, [_P, C.c_uint32, _P, _P, _P, _P, _P, C.POINTER(_P)]),
         "dqtg_shard_hist_len": (C.c_uint64, [_P, C.POINTER(Config), C.c_int]),
         "dqtg_shard_stage1": (C.c_int, [_P, _P, C.POINTER(Config), _P]),
         "dqtg_shard_stage2": (C.c_int, [_P, _P, C.POINTER(Config), _P, _P]),
@@ -553,6 +556,23 @@ class Engine:
         _check(LIB.dqtg_encode_record(self.h, None if base is None else base.h, target.h,
                                       quality, C.byref(r)))
         return r
+
+    def decode_chain(self, records, base: DevState = None, on_state=None):
+        """Chain::restore over host records (dqtg_decode_chain): record k+1's host walk
+        overlaps the device decode of record k.  on_state(k, state_handle) is called
+        with a borrowed dqtg_qstate handle for every record; returns the last state."""
+        recs = [bytes(r) for r in records]
+        n = len(recs)
+        ptrs = (C.c_char_p * max(n, 1))(*recs)
+        sizes = np.array([len(r) for r in recs] or [0], np.uint64)
+        cb = STATE_FN((lambda user, k, st: on_state(int(k), st)) if on_state else 0)
+        out = _P()
+        _check(LIB.dqtg_decode_chain(self.h, n, C.cast(ptrs, C.c_void_p), sizes.ctypes.data,
+                                     None if base is None else base.h, cb if on_state else None,
+                                     None, C.byref(out)))
+        if not out:
+            return None
+        return DevState(self, out, state_meta(out))
 
     def decode_record(self, rec: bytes, base: DevState = None) -> DevState:
         """decode_delta_record (codec.cpp:459-597) on the device."""

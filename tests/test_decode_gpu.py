@@ -158,3 +158,42 @@ def test_decode_fuzzed_records(eng, oracle):
                 assert ex.status in allowed, (pos, ex)
     host_equal(eng.decode_record(full), q1)
     host_equal(eng.decode_record(delta, base=eng.decode_record(full)), q2)
+
+
+def test_decode_chain_matches_sequential(oracle):
+    """dqtg_decode_chain (host walk of record k+1 overlapping the device decode of k)
+    gives the states decode_record gives one by one, and the oracle's."""
+    from paper_2306_11800_b200 import engine as E
+    from tests.util import CONFIGS, flat, make_tensors, perturb
+
+    eng = E.Engine(0)
+    cfg = CONFIGS[1]
+    ts = [make_tensors(seed=3)]
+    for k in range(4):
+        ts.append(perturb(ts[-1], seed=10 + k))
+    ema = np.random.default_rng(1).normal(0, 0.1, flat(ts[0]).size).astype(np.float32)
+    qs, recs, prev = [], [], None
+    for k, t in enumerate(ts):
+        m, s = oracle.scores(flat(t), ema)
+        q = oracle.quantize(t, k, m, s, cfg, 1)
+        recs.append(oracle.encode_record(q, prev))
+        qs.append(q)
+        prev = q
+    seen = []
+    last = eng.decode_chain(recs, on_state=lambda k, h: seen.append(k))
+    assert seen == list(range(len(recs)))
+    got = last.download()
+    want = qs[-1]
+    assert [x.tolist() for x in got.levels] == [np.asarray(x).tolist() for x in want.levels]
+    # the same chain one record at a time
+    st = None
+    for r in recs:
+        st = eng.decode_record(r, base=st)
+    assert eng.states_equal(st, last)
+    # a corrupt record in the middle: raised after the records before it decoded
+    bad = list(recs)
+    bad[2] = bad[2][:-5]
+    seen.clear()
+    with pytest.raises(E.EngineError):
+        eng.decode_chain(bad, on_state=lambda k, h: seen.append(k))
+    assert seen == [0, 1]
