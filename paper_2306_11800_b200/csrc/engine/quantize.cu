@@ -505,38 +505,34 @@ __global__ void __launch_bounds__(kPB, 5) pass_a2_kernel(PassIn a, A2Args f) {
         }
         unsigned long long* gw = f.gh_w + lt * a.HS;
         unsigned long long* gs = f.gh_sens + lt * a.HS;
-        for (uint32_t i = threadIdx.x * 4; i < T.count; i += kPB * 8) {
-            const uint32_t i2 = i + kPB * 4;
-            const bool two = i2 < T.count;
-            const float4 w0 = ld4(a.w + T.start + i);
-            const float4 w1 = two ? ld4(a.w + T.start + i2) : make_float4(0, 0, 0, 0);
-            float m[8], s[8];
-            {
-                float mm[4], ss[4];
-                load_scores<false>(a, T.start + i, w0, mm, ss);
+        // the whole tile's loads first (4 float4 of w and of EMA per thread: twice the
+        // bytes in flight of a two-group iteration), then the 16 elements
+        float4 wv[4], ev[4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) m[j] = mm[j], s[j] = ss[j];
-                if (two) {
-                    load_scores<false>(a, T.start + i2, w1, mm, ss);
+        for (int g = 0; g < 4; ++g) {
+            const uint32_t i = g * kPB * 4 + threadIdx.x * 4;
+            wv[g] = i < T.count ? ld4(a.w + T.start + i) : make_float4(0, 0, 0, 0);
+            ev[g] = (a.has_sens && i < T.count) ? ld4(a.ema + T.start + i) : make_float4(0, 0, 0, 0);
+        }
+        uint32_t cm = 0;  // candidate elements of this thread (bit 4g + j)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) m[4 + j] = mm[j], s[4 + j] = ss[j];
-                } else {
+        for (int g = 0; g < 4; ++g) {
+            const uint32_t i = g * kPB * 4 + threadIdx.x * 4;
+            const float wa[4] = {wv[g].x, wv[g].y, wv[g].z, wv[g].w};
+            const float ea[4] = {ev[g].x, ev[g].y, ev[g].z, ev[g].w};
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) m[4 + j] = s[4 + j] = 0.0f;
-                }
-            }
-            const float wa[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-            uint32_t cm = 0;  // candidate elements of this thread
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const uint32_t e = (j < 4 ? i : i2) + (j & 3);
-                if (e >= T.count) continue;
+            for (int j = 0; j < 4; ++j) {
+                if (i + j >= T.count) continue;
+                const float m = fabsf(wa[j]);
+                const float s = a.has_sens ? fabsf(__fmul_rn(ea[j], wa[j])) : 0.0f;  // ranker.cpp:96
                 if (!(fastc && hist_fast_signed(shw_s, __float_as_uint(wa[j]), fp)))
                     hist_add(shw, gw, wa[j], a.tab, a.err);
-                if (a.has_sens && !(fastc && hist_fast_pos(shs_s, __float_as_uint(s[j]), fp)))
-                    hist_add_pos(shs, gs, s[j], a.tab, a.err);
-                if (m[j] > lo.x || (a.has_sens && s[j] > lo.y)) cm |= 1u << j;
+                if (a.has_sens && !(fastc && hist_fast_pos(shs_s, __float_as_uint(s), fp)))
+                    hist_add_pos(shs, gs, s, a.tab, a.err);
+                if (m > lo.x || (a.has_sens && s > lo.y)) cm |= 1u << (4 * g + j);
             }
+        }
+        {
             const uint32_t act = __activemask();
             const uint32_t bal = __ballot_sync(act, cm != 0);
             if (bal) {  // warp-aggregated append (rare)
@@ -552,10 +548,13 @@ __global__ void __launch_bounds__(kPB, 5) pass_a2_kernel(PassIn a, A2Args f) {
                 b0 = __shfl_sync(act, b0, last);
                 unsigned long long at = b0 + (x - cnt);
                 for (uint32_t q = cm; q; q &= q - 1) {
-                    const int j = __ffs(q) - 1;
-                    const uint32_t e = (j < 4 ? i : i2) + (j & 3);
+                    const int bit = __ffs(q) - 1, g = bit >> 2, j = bit & 3;
+                    const uint32_t e = g * kPB * 4 + threadIdx.x * 4 + j;
+                    // re-read (cached): the register arrays stay statically indexed
+                    const float w = a.w[T.start + e];
+                    const float s = a.has_sens ? fabsf(__fmul_rn(a.ema[T.start + e], w)) : 0.0f;
                     if (at < f.cap)
-                        f.cand[at] = make_uint4((uint32_t)ti, e, __float_as_uint(wa[j]), __float_as_uint(s[j]));
+                        f.cand[at] = make_uint4((uint32_t)ti, e, __float_as_uint(w), __float_as_uint(s));
                     ++at;
                 }
             }
