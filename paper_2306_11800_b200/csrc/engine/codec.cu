@@ -1199,29 +1199,127 @@ __device__ __forceinline__ RunM runm_combine(const RunM& a, const RunM& b) {
 
 __device__ __forceinline__ RunM shfl_down_runm(const RunM& m, int o);
 
-// Block per (tensor, group) for tensors with many tiles (256-tile chunks): warp
-// shuffle scans + one shared-memory combine of the 8 warp aggregates per chunk.
-__global__ void __launch_bounds__(kCB) enc_resolve_big_kernel(EncArgs A, const uint32_t* tensors) {
-    // four consecutive tiles per thread and chunk: a quarter of the block scans on the
-    // long tile ranges of the large tensors (the kernel's critical path)
-    constexpr int kPer = 4;
+// Tensors with many tiles: chunks of kResChunk tiles, three launches.
+//   R1 (block per (chunk, group)): the chunk's aggregates -- the last non-empty
+//      segment (forward) and the run monoid of its segments (backward);
+//   R2 (thread per (tensor, group)): carries over the tensor's chunks -- the last
+//      non-empty segment before each chunk, the monoid of the segments after it;
+//   R3 (block per (chunk, group)): the forward continuation flags and the backward
+//      run extensions of the chunk's segments with those carries, symbol counts
+//      added to the tensor's frequencies.
+// Every chunk works in parallel (the run across tiles, codec.cpp:79-90, of one
+// 38.6 M-element tensor used to be walked by a single block).
+constexpr int kResPer = 4;                       // tiles per thread
+constexpr uint32_t kResChunk = kCB * kResPer;    // tiles per chunk
+struct ResChunk {
+    uint32_t t, c0, c1, k;  // tensor, tile range [c0, c1), chunk index within the tensor
+    uint32_t first;         // index of the tensor's first chunk in the chunk list
+};
+
+__device__ __forceinline__ RunM seg_runm(const Seg& S) {
+    RunM m{};
+    if (S.n) {
+        m.n = S.n;
+        m.fv = S.fv;
+        m.lv = S.lv;
+        m.single = S.lead == S.n;
+        m.lead = S.lead;
+    }
+    return m;
+}
+
+__global__ void __launch_bounds__(kCB) enc_resolve_agg_kernel(EncArgs A, const ResChunk* chunks,
+                                                              int* fwd_last, RunM* bwd_agg) {
+    __shared__ int s_wmax[kCB / 32];
+    __shared__ RunM s_wm[kCB / 32];
+    const uint32_t B = A.B;
+    const ResChunk C = chunks[blockIdx.x / B];
+    const uint32_t b = blockIdx.x % B;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t i0 = C.c0 + tid * kResPer;
+    int x = -1;
+    RunM m[kResPer];
+#pragma unroll
+    for (int u = 0; u < kResPer; ++u) {
+        m[u] = RunM{};
+        if (i0 + u < C.c1) {
+            const Seg S = A.segs[(size_t)(i0 + u) * B + b];
+            m[u] = seg_runm(S);
+            if (S.n) x = (int)(i0 + u);
+        }
+    }
+    RunM r = m[kResPer - 1];
+#pragma unroll
+    for (int u = kResPer - 2; u >= 0; --u) r = runm_combine(m[u], r);
+    for (int o = 16; o > 0; o >>= 1) {
+        x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {  // warp suffix: lane 0 holds the warp's monoid
+        const RunM y = shfl_down_runm(r, o);
+        if (lane + o < 32) r = runm_combine(r, y);
+    }
+    if (lane == 0) s_wmax[wid] = x, s_wm[wid] = r;
+    __syncthreads();
+    if (tid == 0) {
+        int mx = -1;
+        RunM agg{};
+        for (int w = kCB / 32 - 1; w >= 0; --w) {
+            mx = max(mx, s_wmax[w]);
+            agg = runm_combine(s_wm[w], agg);
+        }
+        fwd_last[blockIdx.x] = mx;
+        bwd_agg[blockIdx.x] = agg;
+    }
+}
+
+__global__ void enc_resolve_carry_kernel(const ResChunk* chunks, uint32_t nchunks, uint32_t B,
+                                         int* fwd_last, RunM* bwd_agg) {
+    // one thread per (tensor, group): chunk indices of its tensor are consecutive
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= nchunks * B) return;
+    const uint32_t ci = g / B, b = g % B;
+    const ResChunk C = chunks[ci];
+    if (C.k != 0) return;  // the tensor's first chunk drives its tensor
+    uint32_t n = 0;
+    while (ci + n < nchunks && chunks[ci + n].t == C.t) ++n;
+    int carry = -1;  // exclusive: last non-empty segment before each chunk
+    for (uint32_t j = 0; j < n; ++j) {
+        const size_t s = (size_t)(ci + j) * B + b;
+        const int v = fwd_last[s];
+        fwd_last[s] = carry;
+        carry = max(carry, v);
+    }
+    RunM after{};  // exclusive: monoid of the segments after each chunk
+    for (uint32_t j = n; j-- > 0;) {
+        const size_t s = (size_t)(ci + j) * B + b;
+        const RunM v = bwd_agg[s];
+        bwd_agg[s] = after;
+        after = runm_combine(v, after);
+    }
+}
+
+__global__ void __launch_bounds__(kCB) enc_resolve_big_kernel(EncArgs A, const ResChunk* chunks,
+                                                              const int* fwd_carry,
+                                                              const RunM* bwd_carry) {
     extern __shared__ uint32_t s_f[];  // NS
     __shared__ int s_wmax[kCB / 32];
     __shared__ RunM s_wm[kCB / 32];
     const uint32_t B = A.B, NS = A.NS;
-    const uint32_t t = tensors[blockIdx.x / B], b = blockIdx.x % B;
+    const ResChunk C = chunks[blockIdx.x / B];
+    const uint32_t t = C.t, b = blockIdx.x % B;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t a0 = A.tile0[t], a1 = A.tile0[t + 1];
+    const uint32_t a1 = C.c1;
     for (uint32_t i = tid; i < NS; i += kCB) s_f[i] = 0;
     // forward: lv of the nearest earlier non-empty segment (inclusive max-scan)
-    int carry_last = -1;
-    for (uint32_t c0 = a0; c0 < a1; c0 += kCB * kPer) {
-        const uint32_t i0 = c0 + tid * kPer;
-        int idx[kPer];
-        uint32_t fv[kPer];
+    {
+        const int carry_last = fwd_carry[blockIdx.x];
+        const uint32_t i0 = C.c0 + tid * kResPer;
+        int idx[kResPer];
+        uint32_t fv[kResPer];
         int x = -1;
 #pragma unroll
-        for (int u = 0; u < kPer; ++u) {
+        for (int u = 0; u < kResPer; ++u) {
             idx[u] = -1;
             fv[u] = 0;
             if (i0 + u < a1) {
@@ -1246,47 +1344,34 @@ __global__ void __launch_bounds__(kCB) enc_resolve_big_kernel(EncArgs A, const u
         if (lane == 0) excl = -1;
         int prev = max(before, excl);
 #pragma unroll
-        for (int u = 0; u < kPer; ++u)
+        for (int u = 0; u < kResPer; ++u)
             if (idx[u] >= 0) {
                 A.segs[(size_t)idx[u] * B + b].cont =
                     A.mode != 2 && prev >= 0 && A.segs[(size_t)prev * B + b].lv == fv[u];
                 prev = idx[u];
             }
-        int cl = carry_last;
-        for (int w = 0; w < kCB / 32; ++w) cl = max(cl, s_wmax[w]);
-        __syncthreads();
-        carry_last = cl;
     }
     __syncthreads();
     // backward: suffix run monoid gives the extension of each trailing run
-    RunM carry{};
-    const uint32_t ntl = a1 - a0;
-    const uint32_t nch = (ntl + kCB * kPer - 1) / (kCB * kPer);
-    uint32_t* f = s_f;
-    const uint32_t tb = t * B + b;
-    for (int ch = (int)nch - 1; ch >= 0; --ch) {
-        const uint32_t i0 = a0 + ch * kCB * kPer + tid * kPer;
-        RunM m[kPer];
-        Seg S[kPer];
+    {
+        const RunM carry = bwd_carry[blockIdx.x];
+        uint32_t* f = s_f;
+        const uint32_t tb = t * B + b;
+        const uint32_t i0 = C.c0 + tid * kResPer;
+        RunM m[kResPer];
+        Seg S[kResPer];
 #pragma unroll
-        for (int u = 0; u < kPer; ++u) {
+        for (int u = 0; u < kResPer; ++u) {
             m[u] = RunM{};
             S[u] = Seg{};
             if (i0 + u < a1) {
                 S[u] = A.segs[(size_t)(i0 + u) * B + b];
-                if (S[u].n) {
-                    m[u].n = S[u].n;
-                    m[u].fv = S[u].fv;
-                    m[u].lv = S[u].lv;
-                    m[u].single = S[u].lead == S[u].n;
-                    m[u].lead = S[u].lead;
-                }
+                m[u] = seg_runm(S[u]);
             }
         }
-        // this thread's suffix, then the inclusive suffix inside the warp
-        RunM x = m[kPer - 1];
+        RunM x = m[kResPer - 1];
 #pragma unroll
-        for (int u = kPer - 2; u >= 0; --u) x = runm_combine(m[u], x);
+        for (int u = kResPer - 2; u >= 0; --u) x = runm_combine(m[u], x);
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const RunM y = shfl_down_runm(x, o);
@@ -1299,7 +1384,7 @@ __global__ void __launch_bounds__(kCB) enc_resolve_big_kernel(EncArgs A, const u
         RunM nxt = shfl_down_runm(x, 1);  // suffix starting at the next lane
         RunM after = lane < 31 ? runm_combine(nxt, later) : later;
 #pragma unroll
-        for (int u = kPer - 1; u >= 0; --u) {  // items of this thread, last first
+        for (int u = kResPer - 1; u >= 0; --u) {  // items of this thread, last first
             if (i0 + u < a1 && S[u].n) {
                 unsigned long long E = (A.mode != 2 && after.n && after.fv == S[u].lv) ? after.lead : 0ull;
                 const bool single = S[u].lead == S[u].n;
@@ -1316,15 +1401,11 @@ __global__ void __launch_bounds__(kCB) enc_resolve_big_kernel(EncArgs A, const u
             }
             after = runm_combine(m[u], after);
         }
-        RunM chunk = carry;
-        for (int w = kCB / 32 - 1; w >= 0; --w) chunk = runm_combine(s_wm[w], chunk);
-        __syncthreads();
-        carry = chunk;
     }
     __syncthreads();
-    uint32_t* gf = A.freq + (size_t)tb * NS;
+    uint32_t* gf = A.freq + (size_t)(t * B + b) * NS;
     for (uint32_t i = tid; i < NS; i += kCB)
-        if (s_f[i]) gf[i] += s_f[i];
+        if (s_f[i]) atomicAdd(gf + i, s_f[i]);
 }
 
 constexpr int kResolveWarps = 8;
@@ -2486,7 +2567,25 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
         DQTG_CUDA(cudaMemcpyAsync(d_list, both.data(), both.size() * 4, cudaMemcpyHostToDevice, st));
         const uint32_t np_small = (uint32_t)small.size() * B;
         if (np_small) { DQTG_SPAN(e, "enc_resolve_kernel"); enc_resolve_kernel<<<(np_small + kResolveWarps - 1) / kResolveWarps, kResolveWarps * 32, kResolveWarps * NS * 4, st>>>(A, d_list, np_small); }
-        if (!big.empty()) { DQTG_SPAN(e, "enc_resolve_big_kernel"); enc_resolve_big_kernel<<<(unsigned)big.size() * B, kCB, NS * 4, st>>>(A, d_list + small.size()); }
+        if (!big.empty()) {
+            std::vector<ResChunk> ch;
+            for (uint32_t tt : big) {
+                const uint32_t first = (uint32_t)ch.size();
+                uint32_t k = 0;
+                for (uint32_t c0 = L.tile0[tt]; c0 < L.tile0[tt + 1]; c0 += kResChunk, ++k)
+                    ch.push_back(ResChunk{tt, c0, std::min(c0 + kResChunk, L.tile0[tt + 1]), k, first});
+            }
+            const uint32_t nch = (uint32_t)ch.size();
+            auto* d_ch = (ResChunk*)e.buf("e.reschunks", nch * sizeof(ResChunk) + 16);
+            auto* d_fl = (int*)e.buf("e.resfwd", (size_t)nch * B * 4 + 16);
+            auto* d_ba = (RunM*)e.buf("e.resbwd", (size_t)nch * B * sizeof(RunM) + 16);
+            DQTG_CUDA(cudaMemcpyAsync(d_ch, ch.data(), nch * sizeof(ResChunk), cudaMemcpyHostToDevice, st));
+            DQTG_SPAN(e, "enc_resolve_big_kernel");
+            enc_resolve_agg_kernel<<<nch * B, kCB, 0, st>>>(A, d_ch, d_fl, d_ba);
+            enc_resolve_carry_kernel<<<(nch * B + 255) / 256, 256, 0, st>>>(d_ch, nch, B, d_fl, d_ba);
+            enc_resolve_big_kernel<<<nch * B, kCB, NS * 4, st>>>(A, d_ch, d_fl, d_ba);
+            e.launched(2);  // (a pageable source is staged before cudaMemcpyAsync returns)
+        }
         e.launched(2);
     }
     e.launched(2);
