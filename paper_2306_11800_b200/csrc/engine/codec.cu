@@ -1889,9 +1889,19 @@ __device__ __forceinline__ void owned_run(const EncArgs& A, const Seg* segs, uns
 }
 
 // E2a: bits per (tile, group), one warp per tile
+// Resolved codes per run (enc_bits_kernel -> enc_emit_kernel): the run's value code
+// and length code concatenated, its group and its bit count, so the emission reads one
+// word per run instead of the segment, two code tables and -- for long runs -- a
+// binary search in the group's overflow-length list.  Bit counts above kRcMaxBits are
+// marked kRcSlow and resolved again by the emission.
+constexpr uint32_t kRcMaxBits = 49, kRcSlow = 127;
+__device__ __forceinline__ unsigned long long rc_pack(unsigned long long code, uint32_t b, uint32_t bits) {
+    return bits > kRcMaxBits ? (unsigned long long)kRcSlow : (code << 15) | ((unsigned long long)b << 7) | bits;
+}
+
 template <int KB>
 __global__ void __launch_bounds__(256) enc_bits_kernel(EncArgs A, CodeTabs C, int ntiles,
-                                                       uint32_t* segbits) {
+                                                       uint32_t* segbits, unsigned long long* rc) {
     __shared__ uint32_t s_bits[8][KB];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ti = blockIdx.x * 8 + wid;
@@ -1903,16 +1913,21 @@ __global__ void __launch_bounds__(256) enc_bits_kernel(EncArgs A, CodeTabs C, in
     const uint32_t R = A.tile_nruns[ti];
     const Seg* segs = A.segs + (size_t)ti * B;
     const unsigned long long* runs = A.runs + (size_t)ti * kTile;
+    unsigned long long* rct = rc + (size_t)ti * kTile;
     for (uint32_t r = lane; r < R; r += 32) {
         uint32_t v, b;
         unsigned long long L;
         owned_run(A, segs, runs[r], r, v, b, L);
-        if (!L) continue;
+        if (!L) {
+            rct[r] = 0;
+            continue;
+        }
         const uint32_t tb = T.tensor * B + b;
-        unsigned long long c;
+        unsigned long long c1, c2 = 0;
         uint32_t l1, l2 = 0;
-        code_of(C, tb, NS, v, c, l1);
-        if (L > 1) code_of_len(C, tb, NS, B, L, c, l2);
+        code_of(C, tb, NS, v, c1, l1);
+        if (L > 1) code_of_len(C, tb, NS, B, L, c2, l2);
+        rct[r] = rc_pack(l2 ? (c1 << l2) | c2 : c1, b, l1 + l2);
         atomicAdd(&s_bits[wid][b], l1 + l2);
     }
     __syncwarp();
@@ -2171,6 +2186,7 @@ template <int KB, int EW = (KB > kMaxB ? 2 : kEmitWarps)>
 __global__ void __launch_bounds__(EW * 32) enc_emit_kernel(EncArgs A, CodeTabs C,
                                                                    const unsigned long long* segoff,
                                                                    const uint32_t* segbits,
+                                                                   const unsigned long long* rc,
                                                                    int ntiles, uint8_t* rec) {
     __shared__ uint32_t s_stage[EW][kWarpStage];
     __shared__ uint32_t s_segbits[EW][KB];
@@ -2226,13 +2242,18 @@ __global__ void __launch_bounds__(EW * 32) enc_emit_kernel(EncArgs A, CodeTabs C
     uint32_t running = 0;
     for (uint32_t r0 = 0; r0 < R; r0 += 32) {
         const uint32_t r = r0 + lane;
-        uint32_t v = 0, b = 0;
-        unsigned long long L = 0;
-        if (r < R) owned_run(A, segs, runs[r], r, v, b, L);
-        uint32_t l1 = 0, l2 = 0;
+        uint32_t b = 0, l1 = 0, l2 = 0;
         unsigned long long c1 = 0, c2 = 0;
-        const uint32_t tb = T.tensor * B + b;
-        if (L) {
+        const unsigned long long w = r < R ? rc[(size_t)ti * kTile + r] : 0ull;
+        if ((w & 127) != kRcSlow) {  // resolved by enc_bits_kernel: one code of l1 bits
+            l1 = (uint32_t)(w & 127);
+            b = (uint32_t)((w >> 7) & 0xff);
+            c1 = w >> 15;
+        } else {  // more than kRcMaxBits bits: resolve again
+            uint32_t v = 0;
+            unsigned long long L = 0;
+            owned_run(A, segs, runs[r], r, v, b, L);
+            const uint32_t tb = T.tensor * B + b;
             code_of(C, tb, NS, v, c1, l1);
             if (L > 1) code_of_len(C, tb, NS, B, L, c2, l2);
         }
@@ -2714,11 +2735,12 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     }
     CodeTabs C{code_dense, len_dense, ukey, code_ov, len_ov, gi};
     auto* segbits = (uint32_t*)e.buf("e.segbits32", (size_t)ntiles * B * 4 + 4);
+    auto* rcodes = (unsigned long long*)e.buf("e.rcodes", (size_t)ntiles * kTile * 8);
     auto* segoff = (unsigned long long*)e.buf("e.segoff", (size_t)ntiles * B * 8);
     {
         DQTG_SPAN(e, "enc_bits_kernel");
-        if (large) enc_bits_kernel<kMaxBLarge><<<(ntiles + 7) / 8, 256, 0, st>>>(A, C, ntiles, segbits);
-        else enc_bits_kernel<kMaxB><<<(ntiles + 7) / 8, 256, 0, st>>>(A, C, ntiles, segbits);
+        if (large) enc_bits_kernel<kMaxBLarge><<<(ntiles + 7) / 8, 256, 0, st>>>(A, C, ntiles, segbits, rcodes);
+        else enc_bits_kernel<kMaxB><<<(ntiles + 7) / 8, 256, 0, st>>>(A, C, ntiles, segbits, rcodes);
     }
     { DQTG_SPAN(e, "enc_bitscan_kernel"); enc_bitscan_kernel<<<nt * B, kCB, 0, st>>>(A, segbits, segoff, gi); }
     e.launched(2);
@@ -2767,8 +2789,8 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     if (np) { DQTG_SPAN(e, "write_prot_kernel"); write_prot_kernel<<<pgrid, 256, 0, st>>>(tr, nt, np, target.d_ppos, target.d_pval, pscan, rec->d_buf); }
     {
         DQTG_SPAN(e, "enc_emit_kernel");
-        if (large) enc_emit_kernel<kMaxBLarge><<<(ntiles + 1) / 2, 2 * 32, 0, st>>>(A, C, segoff, segbits, ntiles, rec->d_buf);
-        else enc_emit_kernel<kMaxB><<<(ntiles + kEmitWarps - 1) / kEmitWarps, kEmitWarps * 32, 0, st>>>(A, C, segoff, segbits, ntiles, rec->d_buf);
+        if (large) enc_emit_kernel<kMaxBLarge><<<(ntiles + 1) / 2, 2 * 32, 0, st>>>(A, C, segoff, segbits, rcodes, ntiles, rec->d_buf);
+        else enc_emit_kernel<kMaxB><<<(ntiles + kEmitWarps - 1) / kEmitWarps, kEmitWarps * 32, 0, st>>>(A, C, segoff, segbits, rcodes, ntiles, rec->d_buf);
     }
     { DQTG_SPAN(e, "finish_crc_kernel"); finish_crc_kernel<<<1, 1, 0, st>>>(A.crc_acc, 2 * L.N, rec->d_buf + total - 4, nullptr); }
     e.launched(3);
