@@ -642,7 +642,7 @@ std::shared_ptr<Layout> make_layout(Engine* e, const dqtg_layout* l) {
     L->tile0.push_back((uint32_t)L->tiles.size());
     if (L->Np == 0) L->Np = kAlign;
     {
-        constexpr size_t kSampleTiles = 512;
+        constexpr size_t kSampleTiles = 192;
         std::vector<size_t> per(kLayerTypes, 0), seen(kLayerTypes, 0);
         for (const Tile& t : L->tiles) ++per[L->types[t.tensor]];
         for (const Tile& t : L->tiles) {

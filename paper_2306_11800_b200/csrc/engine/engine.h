@@ -115,7 +115,7 @@ struct Layout {
     bool has_names = false;
     std::vector<Tile> tiles;
     std::vector<uint32_t> tile0;  // first tile of each tensor (size nt+1)
-    // every layer type's tiles, thinned to <= kSampleTiles per type (threshold guess
+    // every layer type's tiles, thinned to ~kSampleTiles (192) per type (threshold guess
     // of the fused score/partition pass, quantize.cu)
     std::vector<Tile> sample_tiles;
     Tile* d_sample = nullptr;

@@ -1382,22 +1382,24 @@ static void stage_level_bounds(Engine& e, Stage& s) {
 }
 
 // pass A into gh_mag/gh_sens ([7][HS] each) for the given masks
+// per_sm_cap: resident CTAs per SM at most (the sample pass: one -- a CTA's setup and
+// histogram flush cost more than its handful of tiles)
 static void stage_pass_a(Engine& e, const DevCkpt& c, const PassIn& a, uint32_t mask_mag,
                          uint32_t mask_sens, unsigned long long* gh_mag,
-                         unsigned long long* gh_sens) {
+                         unsigned long long* gh_sens, int per_sm_cap = 8) {
     const int ntiles = a.ntiles;
     cudaStream_t st = e.stream;
     DQTG_CUDA(cudaMemsetAsync(a.tile_ctr, 0, 4, st));
     const size_t ct = a.tab.ctab ? ((size_t)a.tab.ctab_n + 1) * 4 : 0;  // + sentinel
     if (c.explicit_scores) {
         const size_t smem = (size_t)2 * kWinSlots * 4 + ct;
-        const int grid = stream_grid(e, ntiles, 3);
+        const int grid = stream_grid(e, ntiles, std::min(3, per_sm_cap));
         ensure_dyn_smem((const void*)pass_a_kernel<true>, smem);
         { DQTG_SPAN(e, "pass_a_kernel"); pass_a_kernel<true><<<grid, kPB, smem, st>>>(a, gh_mag, gh_sens, mask_mag, mask_sens); }
     } else {
         const size_t smem = (size_t)2 * kPosSlots * 4 + ct;
         ensure_dyn_smem((const void*)pass_a_kernel<false>, smem);
-        const int grid = stream_grid(e, ntiles, 5);
+        const int grid = stream_grid(e, ntiles, std::min(5, per_sm_cap));
         DQTG_CUDA(cudaFuncSetAttribute(pass_a_kernel<false>,
                                        cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         { DQTG_SPAN(e, "pass_a_kernel"); pass_a_kernel<false><<<grid, kPB, smem, st>>>(a, gh_mag, gh_sens, mask_mag, mask_sens); }
@@ -1486,7 +1488,7 @@ static void stage_fused_ab(Engine& e, const DevCkpt& c, const PassIn& a, Stage& 
     PassIn as = a;
     as.tiles = L.d_sample;
     as.ntiles = (int)L.sample_tiles.size();
-    stage_pass_a(e, c, as, s.plan.mask_mag, s.plan.mask_sens, samp, samp + (size_t)kLayerTypes * HS);
+    stage_pass_a(e, c, as, s.plan.mask_mag, s.plan.mask_sens, samp, samp + (size_t)kLayerTypes * HS, 1);
     auto* d_lpg = (LtParams*)e.buf("q.lpg", sizeof(LtParams) * kLayerTypes);
     auto* slots = (int*)e.buf("q.slots", 2 * kLayerTypes * 3 * sizeof(int));
     DQTG_CUDA(cudaMemsetAsync(slots, 0xff, 2 * kLayerTypes * 3 * sizeof(int), st));
@@ -1556,7 +1558,7 @@ static void stage_pass_a2(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s
     PassIn as = a;
     as.tiles = L.d_sample;
     as.ntiles = (int)L.sample_tiles.size();
-    stage_pass_a(e, c, as, s.plan.mask_mag, s.plan.mask_sens, samp, samp + (size_t)kLayerTypes * HS);
+    stage_pass_a(e, c, as, s.plan.mask_mag, s.plan.mask_sens, samp, samp + (size_t)kLayerTypes * HS, 1);
     auto* d_lpg = (LtParams*)e.buf("q.lpg", sizeof(LtParams) * kLayerTypes);
     auto* slots = (int*)e.buf("q.slots", 2 * kLayerTypes * 3 * sizeof(int));
     DQTG_CUDA(cudaMemsetAsync(slots, 0xff, 2 * kLayerTypes * 3 * sizeof(int), st));
