@@ -310,37 +310,51 @@ __global__ void rle_total_kernel(const GroupDesc* groups, uint32_t ngroups,
     if (total != G.elems || off[G.sym_off] != G.elem_off) atomicOr(err, kErrCorruptBitstream);
 }
 
-// R2: mark run heads with their symbol index + 1
-__global__ void rle_heads_kernel(const int32_t* syms, uint64_t n, const unsigned long long* off,
-                                 const unsigned long long* cnt, uint32_t* head, uint64_t ntot) {
-    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n;
-         s += (uint64_t)gridDim.x * blockDim.x)
-        if (cnt[s] && off[s] < ntot) head[off[s]] = (uint32_t)(s + 1);
-}
-
 struct Widen {
     __device__ __forceinline__ unsigned long long operator()(uint32_t x) const { return x; }
 };
 
-struct MaxOp {
-    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
-};
-
-// R3: element -> its run's value (delta), as a byte
-__global__ void rle_fill_kernel(const uint32_t* sidx, uint64_t ntot, const int32_t* syms, uint32_t B,
-                                uint8_t* d, uint32_t* err) {
-    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < ntot;
-         j += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t s = sidx[j];
-        uint32_t v = 0;
-        if (!s) {
-            atomicOr(err, kErrCorruptBitstream);
-        } else {
-            const int32_t x = syms[s - 1];
-            if (x > 0 || -x >= (int32_t)B) atomicOr(err, kErrCorruptIndex);
-            else v = (uint32_t)(-x);
+// R2+R3 (sparse): the delta stream starts zeroed; every value symbol writes its run's
+// non-zero value over [off, off + cnt) -- the work follows the non-zero runs, not the
+// elements (DELTA records are mostly zero runs).  Runs longer than kLongRun are queued
+// for a block each.  Values outside the alphabet are CorruptIndex (codec.cpp:96-99,
+// as rle_fill_kernel reported them).
+constexpr unsigned long long kLongRun = 256;
+__global__ void rle_fill_sparse_kernel(const int32_t* syms, uint64_t n, const unsigned long long* off,
+                                       const unsigned long long* cnt, uint32_t B, uint8_t* d,
+                                       unsigned long long* longs, unsigned int* nlong, uint32_t cap,
+                                       uint32_t* err) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long c = cnt[s];
+        if (!c) continue;  // a length symbol
+        const int32_t x = syms[s];
+        if (-x >= (int32_t)B) {
+            atomicOr(err, kErrCorruptIndex);
+            continue;
         }
-        d[j] = (uint8_t)v;
+        if (x == 0) continue;
+        const uint8_t v = (uint8_t)(-x);
+        const unsigned long long o = off[s];
+        if (c <= kLongRun) {
+            for (unsigned long long j = 0; j < c; ++j) d[o + j] = v;
+        } else {
+            const unsigned int k = atomicAdd(nlong, 1u);
+            if (k < cap) longs[k] = s;
+            else atomicOr(err, kErrCorruptBitstream);  // cannot happen: cap bounds the list
+        }
+    }
+}
+
+__global__ void rle_fill_long_kernel(const int32_t* syms, const unsigned long long* off,
+                                     const unsigned long long* cnt, const unsigned long long* longs,
+                                     const unsigned int* nlong, uint32_t cap, uint8_t* d) {
+    const unsigned int n = min(*nlong, cap);
+    for (unsigned int k = blockIdx.x; k < n; k += gridDim.x) {
+        const unsigned long long s = longs[k];
+        const uint8_t v = (uint8_t)(-syms[s]);
+        const unsigned long long o = off[s], c = cnt[s];
+        for (unsigned long long j = threadIdx.x; j < c; j += blockDim.x) d[o + j] = v;
     }
 }
 
@@ -928,17 +942,15 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
         e.launched(2);
         e.check_err();
         if (!deferred_index.empty()) throw Fail(DQTG_CORRUPT_INDEX, deferred_index);
-        auto* d_head = (uint32_t*)e.buf("d.head", (N + 1) * 4);
-        auto* d_sidx = (uint32_t*)e.buf("d.sidx", (N + 1) * 4);
         auto* d_d = (uint8_t*)e.buf("d.delta", N + 16);
-        DQTG_CUDA(cudaMemsetAsync(d_head, 0, (N + 1) * 4, st));
-        { DQTG_SPAN(e, "rle_heads_kernel"); rle_heads_kernel<<<rg, 256, 0, st>>>(d_syms, sym_total, d_eoff, d_ecnt, d_head, N); }
-        size_t tb3 = 0;
-        DQTG_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb3, d_head, d_sidx, MaxOp{}, (int64_t)std::max<uint64_t>(N, 1), st));
-        void* tmp3 = e.buf("d.cubtmp3", tb3 + 16);
-        DQTG_CUDA(cub::DeviceScan::InclusiveScan(tmp3, tb3, d_head, d_sidx, MaxOp{}, (int64_t)std::max<uint64_t>(N, 1), st));
-        const unsigned fg = (unsigned)std::min<uint64_t>((N + 255) / 256 + 1, (uint64_t)e.num_sms * 16);
-        { DQTG_SPAN(e, "rle_fill_kernel"); rle_fill_kernel<<<fg, 256, 0, st>>>(d_sidx, N, d_syms, B, d_d, e.d_err); }
+        DQTG_CUDA(cudaMemsetAsync(d_d, 0, N + 16, st));
+        // long runs: at most N / kLongRun of them
+        const uint32_t lcap = (uint32_t)std::min<uint64_t>(N / kLongRun + 16, 0xffffffffull);
+        auto* d_long = (unsigned long long*)e.buf("d.longruns", (size_t)lcap * 8 + 8);
+        auto* d_nlong = (unsigned int*)e.buf("d.nlong", 16);
+        DQTG_CUDA(cudaMemsetAsync(d_nlong, 0, 4, st));
+        { DQTG_SPAN(e, "rle_fill_kernel"); rle_fill_sparse_kernel<<<rg, 256, 0, st>>>(d_syms, sym_total, d_eoff, d_ecnt, B, d_d, d_long, d_nlong, lcap, e.d_err); }
+        { DQTG_SPAN(e, "rle_fill_long_kernel"); rle_fill_long_kernel<<<e.num_sms * 4, 256, 0, st>>>(d_syms, d_eoff, d_ecnt, d_long, d_nlong, lcap, d_d); }
         e.launched(2);
 
         // ---- U: unrearrange against the previous levels
