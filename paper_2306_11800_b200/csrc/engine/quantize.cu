@@ -567,6 +567,155 @@ __global__ void __launch_bounds__(kPB, 5) pass_a2_kernel(PassIn a, A2Args f) {
     }
 }
 
+// Pass A2 with the inputs staged in shared memory by the TMA engine: half tiles
+// (2048 elements of w and EMA, 16 KB) are copied with cp.async.bulk into a
+// two-stage ring completed on mbarriers, the next half-tile's copy issued before the
+// current one is processed, so the histogram work never waits on global loads.
+constexpr uint32_t kA2Half = kTile / 2;
+
+struct A2Stage {
+    float w[kA2Half];
+    float e[kA2Half];
+};
+
+__global__ void __launch_bounds__(kPB, 3) pass_a2_tma_kernel(PassIn a, A2Args f) {
+    extern __shared__ __align__(16) uint8_t a2_dyn[];
+    A2Stage* stg = (A2Stage*)a2_dyn;  // [2]
+    uint32_t* sh = (uint32_t*)(a2_dyn + 2 * sizeof(A2Stage));
+    uint32_t* shw = sh;              // kWinSlots: signed w
+    uint32_t* shs = sh + kWinSlots;  // kPosSlots: sensitivity
+    uint32_t* s_ctab = shs + kPosSlots;
+    __shared__ __align__(8) uint64_t s_mbar[2];
+    __shared__ int s_next;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const bool fastc = a.tab.ctab != nullptr;
+    for (int i = tid; i < kWinSlots + kPosSlots; i += blockDim.x) sh[i] = 0;
+    if (fastc) {
+        for (uint32_t i = tid; i < a.tab.ctab_n; i += blockDim.x) s_ctab[i] = __ldg(a.tab.ctab + i);
+        if (tid == 0) s_ctab[a.tab.ctab_n] = 0xc0000000u;
+    }
+    // work items: (tile, half), 2 * tile + half; thread 0 walks them in grabs of
+    // kGrab tiles and keeps one item in flight ahead of the one being processed
+    int g_end = 0, g_item = 0;  // thread 0 only
+    auto next_item = [&](int item) -> int {
+        for (;;) {
+            int n = item + 1;
+            if (item >= 0 && (item & 1) == 0 && a.tiles[item >> 1].count <= kA2Half) ++n;  // no second half
+            if (item >= 0 && n < g_end) return n;
+            const int gb = (int)atomicAdd(a.tile_ctr, (unsigned)kGrab);
+            if (gb >= a.ntiles) return 2 * a.ntiles;
+            g_item = 2 * gb;
+            g_end = 2 * min(gb + kGrab, a.ntiles);
+            return g_item;
+        }
+    };
+    auto issue = [&](int item, int slot) {
+        const Tile T = a.tiles[item >> 1];
+        const uint32_t h0 = (item & 1) * kA2Half;
+        const uint32_t n = min(T.count - h0, kA2Half);
+        const uint32_t bytes = ((n + 3u) & ~3u) * 4u;
+        mbar_arrive_expect_tx(&s_mbar[slot], a.has_sens ? 2 * bytes : bytes);
+        bulk_g2s(stg[slot].w, a.w + T.start + h0, bytes, &s_mbar[slot]);
+        if (a.has_sens) bulk_g2s(stg[slot].e, a.ema + T.start + h0, bytes, &s_mbar[slot]);
+    };
+    if (tid == 0) {
+        mbar_init(&s_mbar[0], 1);
+        mbar_init(&s_mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const int first = next_item(-1);
+        s_next = first;
+        if (first < 2 * a.ntiles) issue(first, 0);
+    }
+    __syncthreads();
+    const FastPos fp = fast_pos(a.tab, s_ctab);
+    const uint32_t shw_s = (uint32_t)__cvta_generic_to_shared(shw);
+    const uint32_t shs_s = (uint32_t)__cvta_generic_to_shared(shs);
+    int cur = -1;
+    float2 lo = make_float2(0.f, 0.f);
+    int item = s_next;
+    for (uint32_t it = 0; item < 2 * a.ntiles; ++it) {
+        const int slot = it & 1;
+        if (tid == 0) {  // the next item's copy into the other stage (free since the last barrier)
+            const int nx = next_item(item);
+            s_next = nx;
+            if (nx < 2 * a.ntiles) {
+                fence_proxy_async_smem();
+                issue(nx, slot ^ 1);
+            }
+        }
+        const int ti = item >> 1;
+        const Tile T = a.tiles[ti];
+        const int lt = a.types[T.tensor];
+        if (lt != cur) {
+            __syncthreads();
+            if (cur >= 0) {
+                hist_flush(shw, f.gh_w + cur * a.HS, a.tab);
+                hist_flush_pos(shs, f.gh_sens + cur * a.HS, a.tab);
+            }
+            __syncthreads();
+            cur = lt;
+            lo = f.lo[lt];
+        }
+        unsigned long long* gw = f.gh_w + lt * a.HS;
+        unsigned long long* gs = f.gh_sens + lt * a.HS;
+        const uint32_t h0 = (item & 1) * kA2Half;
+        const uint32_t n = min(T.count - h0, kA2Half);
+        mbar_wait(&s_mbar[slot], (it >> 1) & 1);
+        uint32_t cm = 0;  // candidate elements of this thread (bit 4g + j)
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+            const uint32_t i = g * kPB * 4 + tid * 4;  // within the half tile
+            if (i >= n) continue;
+            const float4 wv = *(const float4*)(stg[slot].w + i);
+            const float4 ev = a.has_sens ? *(const float4*)(stg[slot].e + i) : make_float4(0, 0, 0, 0);
+            const float wa[4] = {wv.x, wv.y, wv.z, wv.w};
+            const float ea[4] = {ev.x, ev.y, ev.z, ev.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (i + j >= n) continue;
+                const float m = fabsf(wa[j]);
+                const float s = a.has_sens ? fabsf(__fmul_rn(ea[j], wa[j])) : 0.0f;  // ranker.cpp:96
+                if (!(fastc && hist_fast_signed(shw_s, __float_as_uint(wa[j]), fp)))
+                    hist_add(shw, gw, wa[j], a.tab, a.err);
+                if (a.has_sens && !(fastc && hist_fast_pos(shs_s, __float_as_uint(s), fp)))
+                    hist_add_pos(shs, gs, s, a.tab, a.err);
+                if (m > lo.x || (a.has_sens && s > lo.y)) cm |= 1u << (4 * g + j);
+            }
+        }
+        {
+            const uint32_t bal = __ballot_sync(0xffffffffu, cm != 0);
+            if (bal) {  // warp-aggregated append (rare)
+                const uint32_t cnt = __popc(cm);
+                uint32_t x = cnt;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                unsigned long long b0 = 0;
+                if (lane == 31) b0 = atomicAdd(f.n_cand, (unsigned long long)x);
+                b0 = __shfl_sync(0xffffffffu, b0, 31);
+                unsigned long long at = b0 + (x - cnt);
+                for (uint32_t qm = cm; qm; qm &= qm - 1) {
+                    const int bit = __ffs(qm) - 1, g = bit >> 2, j = bit & 3;
+                    const uint32_t i = g * kPB * 4 + tid * 4 + j;
+                    const float w = stg[slot].w[i];
+                    const float s = a.has_sens ? fabsf(__fmul_rn(stg[slot].e[i], w)) : 0.0f;
+                    if (at < f.cap)
+                        f.cand[at] = make_uint4((uint32_t)ti, h0 + i, __float_as_uint(w), __float_as_uint(s));
+                    ++at;
+                }
+            }
+        }
+        __syncthreads();  // stage `slot` free for the copy after next; s_next visible
+        item = s_next;
+    }
+    __syncthreads();
+    if (cur >= 0) {
+        hist_flush(shw, f.gh_w + cur * a.HS, a.tab);
+        hist_flush_pos(shs, f.gh_sens + cur * a.HS, a.tab);
+    }
+}
+
 // candidate lower bounds from the sample's quantile slots; +inf where there is no job
 __global__ void cand_bounds_kernel(const int* slot_g, const float* keyf, int64_t NB, int64_t HS,
                                    float2* lo, int2* lo_slot, int shift) {
@@ -1582,11 +1731,20 @@ static void stage_pass_a2(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s
     A2Args f{lo, gh_w, gh + (size_t)kLayerTypes * HS, cand, small, cap};
     const size_t ct = a.tab.ctab ? ((size_t)a.tab.ctab_n + 1) * 4 : 0;
     const size_t smem = (size_t)(kWinSlots + kPosSlots) * 4 + ct;
-    ensure_dyn_smem((const void*)pass_a2_kernel, smem);
-    DQTG_CUDA(cudaFuncSetAttribute(pass_a2_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    int per_sm = 0;
-    DQTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass_a2_kernel, kPB, smem));
-    { DQTG_SPAN(e, "pass_a2_kernel"); pass_a2_kernel<<<stream_grid(e, a.ntiles, std::max(1, per_sm)), kPB, smem, st>>>(a, f); }
+    if (getenv("DQTG_A2_REGS")) {  // the register-staged variant
+        ensure_dyn_smem((const void*)pass_a2_kernel, smem);
+        DQTG_CUDA(cudaFuncSetAttribute(pass_a2_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        int per_sm = 0;
+        DQTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass_a2_kernel, kPB, smem));
+        { DQTG_SPAN(e, "pass_a2_kernel"); pass_a2_kernel<<<stream_grid(e, a.ntiles, std::max(1, per_sm)), kPB, smem, st>>>(a, f); }
+    } else {
+        const size_t smem2 = 2 * sizeof(A2Stage) + smem;
+        ensure_dyn_smem((const void*)pass_a2_tma_kernel, smem2);
+        DQTG_CUDA(cudaFuncSetAttribute(pass_a2_tma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        int per_sm = 0;
+        DQTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass_a2_tma_kernel, kPB, smem2));
+        { DQTG_SPAN(e, "pass_a2_kernel"); pass_a2_tma_kernel<<<stream_grid(e, a.ntiles, std::max(1, per_sm)), kPB, smem2, st>>>(a, f); }
+    }
     { DQTG_SPAN(e, "fold_abs_kernel"); fold_abs_kernel<<<dim3((unsigned)((HS + 255) / 256), kLayerTypes), 256, 0, st>>>(gh_w, gh, HS, T.NB); }
     // 3. exact thresholds, bound check, classification, value histogram
     stage_thresholds(e, s, HS, T, gh, gh + (size_t)kLayerTypes * HS, s.d_lp, slots + kLayerTypes * 3);
