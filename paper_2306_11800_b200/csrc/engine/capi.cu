@@ -259,8 +259,15 @@ dqtg_status dqtg_ckpt_create(dqtg_engine* h, const dqtg_layout* layout, dqtg_ckp
 void dqtg_ckpt_destroy(dqtg_ckpt* c) { delete c; }
 
 static void upload_tensors(Engine& e, const Layout& L, float* dst, const float* const* src) {
-    for (uint32_t i = 0; i < L.nt; ++i)
-        if (L.numel[i]) e.to_device(dst + L.off[i], src[i], L.numel[i] * 4);
+    // merged while sources and padded destinations are both contiguous (pipe.cu upload)
+    uint32_t i = 0;
+    while (i < L.nt) {
+        uint32_t j = i + 1;
+        uint64_t n = L.numel[i];
+        while (j < L.nt && src[j] == src[i] + n && L.off[j] == L.off[i] + n) n += L.numel[j++];
+        if (n) e.to_device(dst + L.off[i], src[i], n * 4);
+        i = j;
+    }
 }
 
 static float* alloc_padded(Engine& e, const Layout& L) {

@@ -75,9 +75,17 @@ bool same_layout(const Layout& a, const dqtg_layout* l) {
     return true;
 }
 
+// per-tensor copies, merged while both the sources and the padded destinations are
+// contiguous (C2: every tensor is a multiple of 64 elements -> one copy per snapshot)
 void upload(Engine& e, const Layout& L, float* dst, const float* const* src) {
-    for (uint32_t i = 0; i < L.nt; ++i)
-        if (L.numel[i]) e.to_device(dst + L.off[i], src[i], L.numel[i] * 4);
+    uint32_t i = 0;
+    while (i < L.nt) {
+        uint32_t j = i + 1;
+        uint64_t n = L.numel[i];
+        while (j < L.nt && src[j] == src[i] + n && L.off[j] == L.off[i] + n) n += L.numel[j++];
+        if (n) e.to_device(dst + L.off[i], src[i], n * 4);
+        i = j;
+    }
 }
 
 // The tensors of one snapshot form a device buffer in the engine's padded layout
