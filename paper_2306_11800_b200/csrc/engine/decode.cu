@@ -78,8 +78,9 @@ struct DecodePlan {
     std::vector<std::string> names;
     std::vector<uint8_t> types, ranks;
     std::vector<uint64_t> dims;
-    std::vector<std::vector<uint64_t>> ppos;
-    std::vector<std::vector<uint16_t>> pval;
+    std::vector<uint64_t> ppos;  // protected entries of all tensors, flat (one upload)
+    std::vector<uint16_t> pval;
+    std::vector<uint64_t> pcount;  // per tensor
     std::vector<GroupDesc> groups;
     std::vector<ChunkDesc> chunks;
     std::vector<int64_t> tab_sym;
@@ -618,8 +619,7 @@ std::unique_ptr<DecodePlan> decode_plan(Engine& e, const uint8_t* rec, uint64_t 
     names.resize(nt);
     types.resize(nt);
     ranks.resize(nt);
-    ppos.resize(nt);
-    pval.resize(nt);
+    P->pcount.assign(nt, 0);
     rec_elems.assign((size_t)nt * B, 0);
     gstart_h.assign((size_t)nt * B, 0);
     uint64_t stream_pos = 0, sym_total = 0;
@@ -640,8 +640,10 @@ std::unique_ptr<DecodePlan> decode_plan(Engine& e, const uint8_t* rec, uint64_t 
         const uint64_t np = r.uv();
         if (np > numel) throw Fail(DQTG_CORRUPT_INDEX, "too many protected entries in " + names[i]);
         if (np > (r.n - r.at) / 3) throw Fail(DQTG_TRUNCATED, "protected entries exceed the record size");
-        ppos[i].resize(np);
-        pval[i].resize(np);
+        P->pcount[i] = np;
+        const size_t pb = ppos.size();
+        ppos.resize(pb + np);
+        pval.resize(pb + np);
         uint64_t pos = 0;
         for (uint64_t k = 0; k < np; ++k) {
             uint64_t dd;
@@ -658,16 +660,16 @@ std::unique_ptr<DecodePlan> decode_plan(Engine& e, const uint8_t* rec, uint64_t 
                     }
                 }
                 r.at += len;
-                pval[i][k] = (uint16_t)(r.p[r.at] | (r.p[r.at + 1] << 8));
+                pval[pb + k] = (uint16_t)(r.p[r.at] | (r.p[r.at + 1] << 8));
                 r.at += 2;
             } else {
                 dd = r.uv();
-                pval[i][k] = r.le<uint16_t>();
+                pval[pb + k] = r.le<uint16_t>();
             }
             pos = k == 0 ? dd : pos + dd;
             if (pos >= numel || (k > 0 && dd == 0))
                 throw Fail(DQTG_CORRUPT_INDEX, "protected positions not ascending in " + names[i]);
-            ppos[i][k] = pos;
+            ppos[pb + k] = pos;
         }
         if (base) {
             if (base->names[i] != names[i] || base->types[i] != types[i] || base->ranks[i] != ranks[i] ||
@@ -841,17 +843,16 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
     uint64_t acc = 0;
     for (uint32_t i = 0; i < nt; ++i) {
         q->prot_off[i] = acc;
-        q->prot_count[i] = ppos[i].size();
-        acc += ppos[i].size();
+        q->prot_count[i] = P.pcount[i];
+        acc += P.pcount[i];
     }
     q->prot_off[nt] = q->prot_total = acc;
     q->d_ppos = (uint64_t*)e.dalloc((acc + 1) * 8);
     q->d_pval = (uint16_t*)e.dalloc((acc + 1) * 2);
-    for (uint32_t i = 0; i < nt; ++i)
-        if (!ppos[i].empty()) {
-            e.to_device(q->d_ppos + q->prot_off[i], ppos[i].data(), ppos[i].size() * 8);
-            e.to_device(q->d_pval + q->prot_off[i], pval[i].data(), pval[i].size() * 2);
-        }
+    if (acc) {
+        e.to_device(q->d_ppos, ppos.data(), acc * 8);
+        e.to_device(q->d_pval, pval.data(), acc * 2);
+    }
     q->d_levels = (uint16_t*)e.dalloc(L.Np * 2);
     DQTG_CUDA(cudaMemsetAsync(q->d_levels, 0, L.Np * 2, st));
 
