@@ -1799,8 +1799,25 @@ __global__ void __launch_bounds__(NT) enc_huffman_kernel(EncArgs A, const unsign
             }
             acc += hist[l];
         }
-        for (uint32_t i = 0; i < n; ++i) perm[at[depth[i] < 64 ? depth[i] : 64]++] = i;
-        acc = 0;
+    }
+    __syncwarp();
+    // stable placement by length, 32 symbols at a time: lanes of equal length take
+    // consecutive slots in lane (= symbol) order
+    for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        const uint32_t d = i < n ? (depth[i] < 64 ? depth[i] : 64u) : 65u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (lane == leader && d < 65) base = at[d];
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (d < 65) perm[base + __popc(peers & ((1u << lane) - 1u))] = i;
+        __syncwarp();
+        if (lane == leader && d < 65) at[d] = base + __popc(peers);
+        __syncwarp();
+    }
+    if (lane == 0) {
+        uint32_t acc = 0;
         for (int l = 0; l < 65; ++l) {  // starts again
             at[l] = acc;
             acc += hist[l];
