@@ -1718,22 +1718,31 @@ __global__ void __launch_bounds__(NT) enc_huffman_kernel(EncArgs A, const unsign
         // Leaves come in sorted-key order (frequency in the key's high bits, index in
         // the low 24); a leaf always precedes an internal node of equal weight (its
         // insertion index is smaller), so the queue compare is fl <= internal weight.
+        // Both queue fronts stay in registers (the next leaf key; the oldest unmerged
+        // internal weight f2), so the chain per merge is compares and selects; the
+        // loads that refill them do not depend on the node being built (the internal
+        // queue's next weight was written merges ago, except when the queue empties).
         uint32_t q1 = 0, q2 = n;
         unsigned long long k1 = s_keys[0];
+        uint32_t f2 = 0;  // nodef[q2] when q2 < made
         auto take = [&](uint32_t& idx) -> uint32_t {
             const uint32_t fl = (uint32_t)(k1 >> 24);
-            if (q1 < n && (q2 >= made || fl <= nodef[q2])) {
+            if (q1 < n && (q2 >= made || fl <= f2)) {
                 idx = (uint32_t)(k1 & 0xffffffu);
                 if (++q1 < n) k1 = s_keys[q1];
                 return fl;
             }
             idx = q2;
-            return nodef[q2++];
+            const uint32_t f = f2;
+            if (++q2 < made) f2 = nodef[q2];
+            return f;
         };
         for (uint32_t st = 0; st + 1 < n; ++st) {
             uint32_t x, y;
             const uint32_t fx = take(x), fy = take(y);
-            nodef[made] = fx + fy;
+            const uint32_t w = fx + fy;
+            nodef[made] = w;
+            if (q2 == made) f2 = w;  // the internal queue was empty: its new front
             parent[x] = parent[y] = made;
             ++made;
         }
