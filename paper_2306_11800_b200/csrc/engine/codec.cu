@@ -1564,6 +1564,7 @@ __device__ __forceinline__ unsigned long long lb_u64(const unsigned long long* a
 }
 
 struct HufWork {
+    unsigned long long* ovh;    // overflow-length hash: [2 ov_begin, 2 ov_end) per group
     long long* sym;             // [tab_base + i]
     unsigned long long* f;      // [tab_base + i]
     uint32_t* perm;             // [tab_base + i]
@@ -1854,6 +1855,13 @@ __global__ void __launch_bounds__(NT) enc_huffman_kernel(EncArgs A, const unsign
             const unsigned long long j = G.ov_begin + (i - (n - nov));
             code_ov[j] = code;
             len_ov[j] = (uint8_t)len;
+            // hash slot for the emission's lookup: (length, local index), linear probing
+            // in 2 nov slots (lengths >= kLD, so 0 marks an empty slot)
+            unsigned long long* H = W.ovh + 2 * G.ov_begin;
+            const uint32_t m = 2 * nov;
+            uint32_t h = (uint32_t)(((unsigned long long)(uint32_t)sv * 2654435761ull) % m);
+            const unsigned long long ent = ((unsigned long long)(uint32_t)sv << 32) | (uint32_t)(j - G.ov_begin);
+            while (atomicCAS(H + h, 0ull, ent) != 0ull) h = h + 1 == m ? 0 : h + 1;
         }
     }
     for (int o = 16; o > 0; o >>= 1) hdr += __shfl_xor_sync(0xffffffffu, hdr, o);
@@ -1866,6 +1874,7 @@ __global__ void __launch_bounds__(NT) enc_huffman_kernel(EncArgs A, const unsign
 
 // ---- symbol walk shared by E2a / E2b ---------------------------------------------
 struct CodeTabs {
+    const unsigned long long* ovh;  // overflow-length hash (enc_huffman_kernel)
     const unsigned long long* code_dense;
     const uint8_t* len_dense;
     const unsigned long long* ukey;
@@ -1887,8 +1896,12 @@ __device__ __forceinline__ void code_of_len(const CodeTabs& C, uint32_t tb, uint
         code_of(C, tb, NS, B + (uint32_t)L, code, len);
     } else {
         const GroupInfo& G = C.gi[tb];
-        unsigned long long j = G.ov_begin + lb_u64(C.ukey + G.ov_begin, G.ov_end - G.ov_begin,
-                                                   ((unsigned long long)tb << 32) | L);
+        const unsigned long long* H = C.ovh + 2 * G.ov_begin;
+        const uint32_t m = 2 * (uint32_t)(G.ov_end - G.ov_begin);
+        uint32_t h = (uint32_t)((L * 2654435761ull) % m);
+        unsigned long long ent;
+        while (((ent = H[h]) >> 32) != L) h = h + 1 == m ? 0 : h + 1;  // present by construction
+        const unsigned long long j = G.ov_begin + (uint32_t)ent;
         code = C.code_ov[j];
         len = C.len_ov[j];
     }
@@ -2683,6 +2696,8 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
     auto* code_dense = (unsigned long long*)e.buf("e.cdense", (size_t)nt * B * NS * 8);
     auto* len_dense = (uint8_t*)e.buf("e.ldense", (size_t)nt * B * NS);
     auto* code_ov = (unsigned long long*)e.buf("e.cov", ov_cap * 8 + 8);
+    auto* ovh = (unsigned long long*)e.buf("e.ovhash", 2 * ov_cap * 8 + 16);
+    if (n_unique) DQTG_CUDA(cudaMemsetAsync(ovh, 0, 2 * n_unique * 8, st));
     auto* len_ov = (uint8_t*)e.buf("e.lov", ov_cap + 8);
     {
         auto* max_nov = (uint32_t*)(small + 4);
@@ -2732,7 +2747,8 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
                                           cudaMemcpyHostToDevice, st));
             e.sync();  // host vectors
         }
-        HufWork W{};  // unused: the working sets are per tier (shared memory or h.gws)
+        HufWork W{};  // the working sets are per tier (shared memory or h.gws)
+        W.ovh = ovh;
         DQTG_SPAN(e, "enc_huffman_kernel");
         const uint32_t* gl = d_gl;
         if (!tiers[0].empty()) {
@@ -2759,7 +2775,7 @@ std::unique_ptr<Record> encode_record_ex(Engine& e, const QState* base, const QS
             e.launched();
         }
     }
-    CodeTabs C{code_dense, len_dense, ukey, code_ov, len_ov, gi};
+    CodeTabs C{ovh, code_dense, len_dense, ukey, code_ov, len_ov, gi};
     auto* segbits = (uint32_t*)e.buf("e.segbits32", (size_t)ntiles * B * 4 + 4);
     auto* rcodes = (unsigned long long*)e.buf("e.rcodes", (size_t)ntiles * kTile * 8);
     auto* segoff = (unsigned long long*)e.buf("e.segoff", (size_t)ntiles * B * 8);
