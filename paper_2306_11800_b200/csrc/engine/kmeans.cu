@@ -264,10 +264,17 @@ __device__ double block_max_d(double v, KShared& sm) {
     return r;
 }
 
+__device__ void kpp_init_fast(const double* pts, const double* w, int n, int k, double* d2,
+                              double* prob, double* pref, double* chosen, KShared& sm);
+
 // weighted_kmeanspp_init (quantize.cpp:94-164).
 __device__ void kpp_init(const double* pts, const double* w, int n, int k, double* d2,
                          double* prob, double* pref, double* chosen, KShared& sm,
                          bool certify = true) {
+    if (certify && n >= 64) {
+        kpp_init_fast(pts, w, n, k, d2, prob, pref, chosen, sm);
+        return;
+    }
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         d2[i] = __longlong_as_double(0x7ff0000000000000LL);
         prob[i] = w[i];
@@ -315,9 +322,122 @@ __device__ void kpp_init(const double* pts, const double* w, int n, int k, doubl
     __syncthreads();
 }
 
+// kpp_init with the certified parallel pick, two block barriers per pick.  Every
+// thread owns a contiguous chunk of keys for the whole seeding: it sums its chunk's
+// prob, searches its chunk for the crossing and updates its chunk's d2 / prob after
+// the pick, so no barrier separates the update from the next pick's sums.  The draw
+// is taken speculatively before the total is known (thread 0) and given back when
+// the total is zero (the reference draws only for a positive total; mt64_next
+// reads mt[mti++] after an optional regeneration, so mti-- undoes it exactly).
+// Each candidate crossing carries its own certificate in the atomicMin key (index
+// << 1 | failed), so the smallest crossing and its verdict arrive together.  A
+// certified pick has prob > 0 (d2 > 0), so it is never an already-chosen centre;
+// a failed certificate or a zero total takes kpp_pick / the first-unchosen scan.
+__device__ void kpp_init_fast(const double* pts, const double* w, int n, int k, double* d2,
+                              double* prob, double* pref, double* chosen, KShared& sm) {
+    __shared__ double s_slots[2][kKB / 32];
+    __shared__ double s_u[2];
+    __shared__ unsigned long long s_key[2];
+    const int nt = blockDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int C = (n + nt - 1) / nt;
+    const int a = min(n, tid * C), b = min(n, a + C);
+    for (int i = a; i < b; ++i) {
+        d2[i] = __longlong_as_double(0x7ff0000000000000LL);
+        prob[i] = w[i];
+    }
+    if (tid == 0) s_key[0] = s_key[1] = ~0ull;
+    const double eps = 4.0 * (double)(n + 64) * 0x1.0p-53;
+    for (int nc = 0; nc < k; ++nc) {
+        const int par = nc & 1;
+        if (tid == 0) s_u[par] = uniform01(sm.rng);
+        double loc = 0.0;
+        for (int i = a; i < b; ++i) loc = __dadd_rn(loc, prob[i]);
+        double x = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x = __dadd_rn(x, y);
+        }
+        double ex = __shfl_up_sync(0xffffffffu, x, 1);
+        if (lane == 0) ex = 0.0;
+        if (lane == 31) s_slots[par][wid] = x;
+        __syncthreads();  // B1
+        if (tid == 0) s_key[par ^ 1] = ~0ull;  // the previous pick's key is read by now
+        double T = 0.0, base = 0.0;
+        for (int q = 0; q < nt / 32; ++q) {
+            const double sv = s_slots[par][q];
+            if (q < wid) base = __dadd_rn(base, sv);
+            T = __dadd_rn(T, sv);
+        }
+        base = __dadd_rn(base, ex);
+        int next = -1;
+        double u = -1.0;
+        if (T > 0.0) {
+            u = s_u[par];
+            const double tlo = __dmul_rd(T, __dsub_rd(1.0, eps)), thi = __dmul_ru(T, __dadd_ru(1.0, eps));
+            const double rm = __dmul_rn(u, T), rlo = __dmul_rd(u, tlo), rhi = __dmul_ru(u, thi);
+            double run = base;
+            for (int i = a; i < b; ++i) {
+                const double nx = __dadd_rn(run, prob[i]);
+                if (nx >= rm) {
+                    const bool below = __dmul_ru(run, __dadd_ru(1.0, eps)) < rlo;
+                    const bool above = __dmul_rd(nx, __dsub_rd(1.0, eps)) >= rhi;
+                    atomicMin(&s_key[par], ((unsigned long long)i << 1) | ((below && above) ? 0ull : 1ull));
+                    break;
+                }
+                run = nx;
+            }
+        } else if (tid == 0) {
+            --sm.rng.mti;  // no draw for a zero total
+        }
+        __syncthreads();  // B2
+        if (T > 0.0) {
+            const unsigned long long key = s_key[par];
+            if (key != ~0ull && !(key & 1ull)) next = (int)(key >> 1);
+        }
+        if (next < 0) {  // uncertain (or zero total): the reference's sequential pick
+            next = kpp_pick(prob, pref, n, 0, sm, u);
+            if (tid == 0) {
+                bool taken = false;
+                if (next != n)
+                    for (int j = 0; j < nc; ++j) taken |= (chosen[j] == pts[next]);
+                if (next == n || taken) {  // first unchosen point
+                    for (int i = 0; i < n; ++i) {
+                        bool c2 = false;
+                        for (int j = 0; j < nc; ++j) c2 |= (chosen[j] == pts[i]);
+                        if (!c2) {
+                            next = i;
+                            break;
+                        }
+                    }
+                }
+                sm.pick = next;
+            }
+            __syncthreads();
+            next = sm.pick;
+        }
+        const double v = pts[next];
+        if (tid == 0) chosen[nc] = v;
+        const bool first = nc == 0;
+        for (int i = a; i < b; ++i) {
+            const double dd = __dsub_rn(pts[i], v);
+            const double sq = __dmul_rn(dd, dd);
+            double cur = d2[i];
+            if (sq < cur || first) {  // std::min(d2, d*d)
+                cur = sq < cur ? sq : cur;
+                d2[i] = cur;
+                prob[i] = __dmul_rn(w[i], cur);
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) IntroSort<double, LessD>{}.sort(chosen, k);
+    __syncthreads();
+}
+
 // optional phase timing per CTA (DQTG_KM_TIMING=1): clocks of kpp / lloyd / loss,
 // iterations, n, k, Lloyd chain steps (max over lanes, summed), Lloyd sum clocks
-__device__ long long g_km_timing[1024][8];
+__device__ long long g_km_timing[1024][12];
 
 // Sequential (w, w*x) sums over keys [a, b] from 0 in key order (the reference's
 // accumulation order).  wx: (w, x) pairs in shared memory (one 16-byte load per
@@ -381,11 +501,13 @@ __device__ __forceinline__ void chain_sums(const double2* wx, const double* w, c
 // decision is not certain, the centres are made exact from the previous step's
 // clusters with the reference's sequential chains and the step runs exactly; the
 // final centres are always made exact the same way.
+// The pointers are per-thread values derived from the kernel's shared-memory carve
+// (not loaded from a shared struct), so the compiler emits shared loads for them.
 struct LAux {
     double *lo, *hi, *nlo, *nhi, *sw, *swx, *sax;
     int *pf, *pl;  // clusters (first, last key) that produced the current intervals
     int* pe;       // boundaries of the previous certified step (search hint), -1: none
-    int exact;     // lo == hi == c are the reference's values
+    int* exact;    // (shared) lo == hi == c are the reference's values
 };
 
 // exact centres from the sequential chains over clusters [f[j], l[j]] (warp 0)
@@ -418,6 +540,7 @@ __device__ int lloyd_interval_step(const double* pts, const double* w, int n, LA
                                    KShared& sm) {
     __shared__ int s_res;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const long long t0 = clock64();
     if (wid == 0) {
         bool ok = true;
         for (int j = lane; j + 1 < k; j += 32) ok &= __dsub_rn(X.lo[j + 1], X.hi[j]) > gap;
@@ -431,9 +554,28 @@ __device__ int lloyd_interval_step(const double* pts, const double* w, int n, LA
                     const double a = X.lo[j], b = X.lo[j + 1];
                     auto P = [&](int i) { return fabs(__dsub_rn(pts[i], b)) < fabs(__dsub_rn(pts[i], a)); };
                     const int g = X.pe ? X.pe[j] : -1;
-                    if (g >= 0 && g <= n && (g == 0 || !P(g - 1)) && (g == n || P(g))) e = g;
-                    else e = lloyd_boundary(pts, n, a, b);
-                    if (!X.exact) {  // the same boundary at the upper interval ends
+                    if (g < 0 || g > n) {
+                        e = lloyd_boundary(pts, n, a, b);
+                    } else {  // galloping search outward from the hint, then bisection
+                        auto first_true = [&](int lo, int hi) {  // P(hi) holds or hi == n
+                            while (lo < hi) {
+                                const int mid = (lo + hi) >> 1;
+                                if (P(mid)) hi = mid;
+                                else lo = mid + 1;
+                            }
+                            return lo;
+                        };
+                        if (g == n || P(g)) {
+                            int hi = g, lo = g - 1, d = 2;
+                            while (lo >= 0 && P(lo)) hi = lo, lo = hi - d, d <<= 1;
+                            e = first_true(max(lo + 1, 0), hi);
+                        } else {
+                            int lo = g + 1, hi = g + 1, d = 2;
+                            while (hi < n && !P(hi)) lo = hi + 1, hi = lo + d - 1, d <<= 1;
+                            e = first_true(lo, min(hi, n));
+                        }
+                    }
+                    if (!*X.exact) {  // the same boundary at the upper interval ends
                         const double ah = X.hi[j], bh = X.hi[j + 1];
                         auto Q = [&](int i) { return fabs(__dsub_rn(pts[i], bh)) < fabs(__dsub_rn(pts[i], ah)); };
                         if (!((e == 0 || !Q(e - 1)) && (e == n || Q(e)))) ok = false;
@@ -454,6 +596,7 @@ __device__ int lloyd_interval_step(const double* pts, const double* w, int n, LA
         if (lane == 0) s_res = ok ? 1 : 2;
     }
     __syncthreads();
+    const long long t1 = clock64();
     if (s_res == 2) {
         __syncthreads();
         return 2;
@@ -493,6 +636,7 @@ __device__ int lloyd_interval_step(const double* pts, const double* w, int n, LA
         if (lane == 0) X.sw[j] = ws, X.swx[j] = wxs, X.sax[j] = ax;
     }
     __syncthreads();
+    const long long t2 = clock64();
     if (wid == 0) {
         bool ok = true;
         double U = 0.0, L = 0.0;
@@ -543,12 +687,16 @@ __device__ int lloyd_interval_step(const double* pts, const double* w, int n, LA
         }
         if (lane == 0) {
             s_res = res;
-            if (res != 2) X.exact = 0;
+            if (res != 2) *X.exact = 0;
         }
     }
     __syncthreads();
     const int r = s_res;
     __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {
+        long long* g = g_km_timing[blockIdx.x];
+        g[8] += t1 - t0, g[9] += t2 - t1, g[10] += clock64() - t2;
+    }
     return r;
 }
 
@@ -563,8 +711,8 @@ __device__ int lloyd_block(const double* pts, const double* w, int n, double* c,
                            int* first, int* last, int* cnt, int k, double tol, int max_iter,
                            int* assign, double* score, ScoreVal* top, bool distinct,
                            KShared& sm, double* aux = nullptr) {
-    __shared__ int s_fast;
-    __shared__ LAux X;
+    __shared__ int s_fast, s_exact;
+    LAux X;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double lm = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) lm = fmax(lm, fabs(pts[i]));
@@ -572,12 +720,11 @@ __device__ int lloyd_block(const double* pts, const double* w, int n, double* c,
     if (scale == 0.0) scale = 1.0;
     const double gap = __dmul_rn(scale, 0x1.0p-40);
     const double thr = __dmul_rn(tol, scale);
-    if (aux && threadIdx.x == 0) {
-        X.lo = aux, X.hi = aux + k, X.nlo = aux + 2 * k, X.nhi = aux + 3 * k;
-        X.sw = aux + 4 * k, X.swx = aux + 5 * k, X.sax = aux + 6 * k;
-        X.pf = (int*)(aux + 7 * k), X.pl = X.pf + k, X.pe = X.pl + k;
-        X.exact = 1;
-    }
+    X.lo = aux, X.hi = aux + k, X.nlo = aux + 2 * k, X.nhi = aux + 3 * k;
+    X.sw = aux + 4 * k, X.swx = aux + 5 * k, X.sax = aux + 6 * k;
+    X.pf = (int*)(aux + 7 * k), X.pl = X.pf + k, X.pe = X.pl + k;
+    X.exact = &s_exact;
+    if (threadIdx.x == 0) s_exact = 1;
     __syncthreads();
     if (aux)
         for (int j = threadIdx.x; j < k; j += blockDim.x) X.lo[j] = X.hi[j] = c[j], X.pe[j] = -1;
@@ -591,7 +738,7 @@ __device__ int lloyd_block(const double* pts, const double* w, int n, double* c,
                 if (r == 0) break;
                 continue;
             }
-            if (!X.exact) {  // the exact step needs the reference's centres
+            if (!s_exact) {  // the exact step needs the reference's centres
                 lloyd_exact_from(pts, w, X.pf, X.pl, k, c, sm);
                 __syncthreads();
             }
@@ -755,14 +902,14 @@ __device__ int lloyd_block(const double* pts, const double* w, int n, double* c,
         if (aux) {  // c is exact after an exact step
             __syncthreads();
             for (int j = threadIdx.x; j < k; j += blockDim.x) X.lo[j] = X.hi[j] = c[j];
-            if (threadIdx.x == 0) X.exact = 1;
+            if (threadIdx.x == 0) s_exact = 1;
         }
         if (sm.done) break;
         __syncthreads();  // sm.done / s_fast are rewritten by the next iteration
     }
     if (aux) {
         __syncthreads();
-        if (!X.exact) lloyd_exact_from(pts, w, X.pf, X.pl, k, c, sm);
+        if (!s_exact) lloyd_exact_from(pts, w, X.pf, X.pl, k, c, sm);
         __syncthreads();
     }
     if (threadIdx.x == 0) IntroSort<double, LessD>{}.sort(c, k);
@@ -797,6 +944,10 @@ __device__ double sq_loss_block(const double* pts, const double* w, int n, const
 
 // optional phase timing per CTA (DQTG_KM_TIMING=1): clocks of kpp / lloyd / loss, iterations, n
 
+// SMEM: every problem's working set (n <= smem_n) lives in shared memory; the
+// pointers are then derived from the shared carve in this instantiation, so every
+// access to them compiles to a shared load (not a generic one).
+template <bool SMEM>
 __global__ void __launch_bounds__(kKB) kmeans_restarts_kernel(const KProblem* probs,
                                                               int restarts, int smem_n, int certify) {
     extern __shared__ double dsm[];
@@ -812,10 +963,10 @@ __global__ void __launch_bounds__(kKB) kmeans_restarts_kernel(const KProblem* pr
     int* cnt = last + k;
     double* aux = dsm + 2 * k + (3 * k + 1) / 2 + 1;  // LAux: 7k doubles + 3k ints
     double* base = aux + 9 * k + 1;
-    const double *pts = P.pts, *w = P.w;
+    const double *pts, *w;
     double *d2, *prob, *pref;
     int* assign;
-    if (n <= smem_n) {  // working set in shared memory: the serial chains hit LDS, not L2
+    if (SMEM) {  // working set in shared memory: the serial chains hit LDS, not L2
         double* sp = base;
         double* sw = sp + n;
         d2 = sw + n;
@@ -824,24 +975,33 @@ __global__ void __launch_bounds__(kKB) kmeans_restarts_kernel(const KProblem* pr
         double2* wx = (double2*)(((uintptr_t)(pref + n) + 15) & ~(uintptr_t)15);
         assign = (int*)(wx + n);
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            sp[i] = P.pts[i];
-            sw[i] = P.w[i];
-            wx[i] = make_double2(P.w[i], P.pts[i]);
+            const double pv = P.pts[i], wv = P.w[i];
+            sp[i] = pv;
+            sw[i] = wv;
+            wx[i] = make_double2(wv, pv);
         }
         pts = sp;
         w = sw;
         if (threadIdx.x == 0) sm.wx = wx, sm.in_smem = 1;
     } else {
         if (threadIdx.x == 0) sm.wx = nullptr, sm.in_smem = 0;
+        pts = P.pts;
+        w = P.w;
         d2 = P.scratch + (size_t)t * P.scratch_stride;
         prob = d2 + n;
         pref = prob + n;
         assign = (int*)(pref + n);
     }
     ScoreVal* top = (ScoreVal*)d2;  // reseed scratch reuses d2/prob (2n doubles)
-    if (threadIdx.x == 0) mt64_seed(sm.rng, P.seed + (uint64_t)t);
-    if (threadIdx.x == 0 && blockIdx.x < 1024) g_km_timing[blockIdx.x][6] = g_km_timing[blockIdx.x][7] = 0;
+    if (threadIdx.x == 0 && blockIdx.x < 1024)
+        for (int q = 6; q < 12; ++q) g_km_timing[blockIdx.x][q] = 0;
+    if (threadIdx.x == 0) {
+        const long long m0 = clock64();
+        mt64_seed(sm.rng, P.seed + (uint64_t)t);
+        if (blockIdx.x < 1024) g_km_timing[blockIdx.x][11] = clock64() - m0;
+    }
     __syncthreads();
+    mt64_regen_block(sm.rng);  // the first draw's regeneration, block-parallel
     const long long c0 = clock64();
     kpp_init(pts, w, n, k, d2, prob, pref, c, sm, certify);
     const long long c1 = clock64();
@@ -912,16 +1072,18 @@ void run_kmeans(Engine& e, std::vector<KProblem>& probs, float* cb_out, int cb_s
     const size_t budget = 200 * 1024;
     int smem_n = (int)((budget - std::min(budget, head)) / 60);  // 5 doubles + pair + int per key
     size_t smem = head + (size_t)std::min(maxn, smem_n) * 60 + 96;
-    ensure_dyn_smem((const void*)kmeans_restarts_kernel, smem);
     // DQTG_KM_EXACT: every sum sequential (no certified parallel steps; tests compare)
     const int certify = getenv("DQTG_KM_EXACT") ? 0 : 1;
     // restarts on the engine's high-priority side stream (fork/join with events)
+    void (*kfn)(const KProblem*, int, int, int) =
+        maxn <= smem_n ? kmeans_restarts_kernel<true> : kmeans_restarts_kernel<false>;
+    ensure_dyn_smem((const void*)kfn, smem);
     if (e.profiling || getenv("DQTG_NO_HI")) {
         DQTG_SPAN(e, "kmeans_restarts_kernel");
-        kmeans_restarts_kernel<<<(unsigned)(probs.size() * restarts), kKB, smem, e.stream>>>(dp, restarts, smem_n, certify);
+        kfn<<<(unsigned)(probs.size() * restarts), kKB, smem, e.stream>>>(dp, restarts, smem_n, certify);
     } else {
         cudaStream_t hs = e.hi();
-        kmeans_restarts_kernel<<<(unsigned)(probs.size() * restarts), kKB, smem, hs>>>(dp, restarts, smem_n, certify);
+        kfn<<<(unsigned)(probs.size() * restarts), kKB, smem, hs>>>(dp, restarts, smem_n, certify);
         e.hi_done();
     }
     { DQTG_SPAN(e, "kmeans_select_kernel"); kmeans_select_kernel<<<(unsigned)probs.size(), 32, 0, e.stream>>>(dp, restarts, cb_out,
@@ -930,11 +1092,12 @@ void run_kmeans(Engine& e, std::vector<KProblem>& probs, float* cb_out, int cb_s
     DQTG_CUDA(cudaGetLastError());
     if (getenv("DQTG_KM_TIMING")) {
         e.sync();
-        static long long h[1024][8];
+        static long long h[1024][12];
         DQTG_CUDA(cudaMemcpyFromSymbol(h, g_km_timing, sizeof(h)));
         for (size_t b = 0; b < probs.size() * restarts && b < 1024; ++b)
-            fprintf(stderr, "km cta %zu: kpp %lld lloyd %lld loss %lld clk, iters %lld, n %lld k %lld, chain steps %lld in %lld clk\n", b,
-                    h[b][0], h[b][1], h[b][2], h[b][3], h[b][4], h[b][5], h[b][6], h[b][7]);
+            fprintf(stderr, "km cta %zu: kpp %lld lloyd %lld loss %lld clk, iters %lld, n %lld k %lld, chain steps %lld in %lld clk, "
+                    "interval bnd %lld sums %lld cert %lld, mt %lld\n", b,
+                    h[b][0], h[b][1], h[b][2], h[b][3], h[b][4], h[b][5], h[b][6], h[b][7], h[b][8], h[b][9], h[b][10], h[b][11]);
     }
 }
 

@@ -49,6 +49,35 @@ __device__ inline uint64_t mt64_next(Mt64& r) {
     return x;
 }
 
+// The regeneration of mt64_next run by a whole block (blockDim >= 156): elements
+// 0..155 read only old words, 156..310 the new word i - 156 and old words, 311 the
+// new words 0 and 155, as in the sequential loop.  Same state, mti = 0.
+__device__ inline void mt64_regen_block(Mt64& r) {
+    const uint64_t UM = 0xFFFFFFFF80000000ULL, LM = 0x7FFFFFFFULL, A = 0xB5026F5AA96619E9ULL;
+    const int t = threadIdx.x;
+    uint64_t v = 0;
+    if (t < 156) {
+        const uint64_t x = (r.mt[t] & UM) | (r.mt[t + 1] & LM);
+        v = r.mt[t + 156] ^ (x >> 1) ^ ((x & 1ULL) ? A : 0ULL);
+    }
+    __syncthreads();
+    if (t < 156) r.mt[t] = v;
+    __syncthreads();
+    if (t >= 156 && t < 311) {
+        const uint64_t x = (r.mt[t] & UM) | (r.mt[t + 1] & LM);
+        v = r.mt[t - 156] ^ (x >> 1) ^ ((x & 1ULL) ? A : 0ULL);
+    }
+    __syncthreads();
+    if (t >= 156 && t < 311) r.mt[t] = v;
+    __syncthreads();
+    if (t == 0) {
+        const uint64_t x = (r.mt[311] & UM) | (r.mt[0] & LM);
+        r.mt[311] = r.mt[155] ^ (x >> 1) ^ ((x & 1ULL) ? A : 0ULL);
+        r.mti = 0;
+    }
+    __syncthreads();
+}
+
 // quantize.cpp:23
 __device__ inline double uniform01(Mt64& r) {
     return __dmul_rn((double)(mt64_next(r) >> 11), 0x1.0p-53);
