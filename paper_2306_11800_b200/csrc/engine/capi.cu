@@ -504,6 +504,16 @@ dqtg_status dqtg_dequantize(dqtg_engine* h, const dqtg_qstate* s, float* const* 
         Engine& e = h->e;
         const QState& q = *s->q;
         const Layout& L = *q.L;
+        bool all_dev = true;
+        for (uint32_t i = 0; i < L.nt && all_dev; ++i)
+            if (L.numel[i] && !is_device_ptr(out[i])) all_dev = false;
+        if (all_dev) {  // written in place by the kernel
+            auto* d = (float**)e.buf("dq.outs", (size_t)L.nt * 8 + 8);
+            e.to_device(d, out, (size_t)L.nt * 8);
+            ::dqtg::dequantize_to(e, q, d);
+            e.check_err();
+            return;
+        }
         float* d = (float*)e.buf("dq.out", L.Np * 4);
         ::dqtg::dequantize(e, q, d);
         e.check_err();

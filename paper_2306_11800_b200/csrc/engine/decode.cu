@@ -465,6 +465,109 @@ __global__ void __launch_bounds__(256) unrearrange_kernel(const Tile* tiles, con
     }
 }
 
+// U3 for alphabets of at most 64 keys: every thread owns 16 contiguous elements (its
+// count block).  Per (key, block) counts (u16, one column per thread), an exclusive
+// prefix per key over the 256 blocks, and the element's rank among the equal keys of
+// its own block from byte compares of its registers: the stable rank inside the tile
+// without match / per-chunk serial counters.
+__global__ void __launch_bounds__(256) unrearrange16_kernel(const Tile* tiles, const uint8_t* types,
+                                                            const uint64_t* stream_off,
+                                                            const uint16_t* prev, uint32_t B,
+                                                            const uint32_t* tile_base,
+                                                            const unsigned long long* gstart,
+                                                            const uint8_t* d, const uint32_t* cb_len,
+                                                            uint16_t* cur, uint32_t* err) {
+    __shared__ __align__(16) uint16_t s_hc[64 * 256];
+    __shared__ unsigned long long s_base[64];
+    const Tile T = tiles[blockIdx.x];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (uint32_t i = tid; i < B * 32; i += 256) ((uint4*)s_hc)[i] = make_uint4(0, 0, 0, 0);
+    const uint32_t t = T.tensor;
+    for (uint32_t b = tid; b < B; b += 256)
+        s_base[b] = gstart[(size_t)t * B + b] + tile_base[(size_t)blockIdx.x * B + b];
+    const uint32_t e0 = tid * 16;
+    const uint32_t nv = e0 < T.count ? min(T.count - e0, 16u) : 0u;
+    uint32_t kw[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};  // keys as bytes
+    if (nv) {
+        uint4 x = make_uint4(0, 0, 0, 0), y = x;
+        if (prev) {
+            const uint4* pp = (const uint4*)(prev + T.start + e0);
+            x = pp[0], y = pp[1];
+        }
+        const uint32_t hi = x.x | x.y | x.z | x.w | y.x | y.y | y.z | y.w;
+        kw[0] = __byte_perm(x.x, x.y, 0x6420);
+        kw[1] = __byte_perm(x.z, x.w, 0x6420);
+        kw[2] = __byte_perm(y.x, y.y, 0x6420);
+        kw[3] = __byte_perm(y.z, y.w, 0x6420);
+        // keys >= B (or >= 256) were flagged by U1; they count as key 0 here
+        const uint32_t Brep = B * 0x01010101u;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const int keep = (int)nv - 4 * w;
+            const uint32_t m = keep >= 4 ? 0xffffffffu : (keep <= 0 ? 0u : (1u << (8 * keep)) - 1u);
+            uint32_t v = kw[w] & ~__vcmpgeu4(kw[w], Brep);  // out of range -> 0
+            kw[w] = (v & m) | ~m;                          // no element: 0xff
+        }
+        (void)hi;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const uint32_t k = (kw[j >> 2] >> (8 * (j & 3))) & 0xffu;
+        if (k < 64) ++s_hc[k * 256 + tid];
+    }
+    __syncthreads();
+    for (uint32_t k = wid; k < B; k += 8) {  // per key: exclusive prefix over the 256 blocks
+        uint4* row = (uint4*)(s_hc + k * 256 + 8 * lane);
+        const uint4 v = *row;
+        const uint32_t c0 = v.x & 0xffffu, c1 = v.x >> 16, c2 = v.y & 0xffffu, c3 = v.y >> 16;
+        const uint32_t c4 = v.z & 0xffffu, c5 = v.z >> 16, c6 = v.w & 0xffffu, c7 = v.w >> 16;
+        const uint32_t p1 = c0, p2 = p1 + c1, p3 = p2 + c2, p4 = p3 + c3, p5 = p4 + c4, p6 = p5 + c5,
+                       p7 = p6 + c6, s8 = p7 + c7;
+        uint32_t x = s8;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        const uint32_t ex = x - s8;
+        *row = make_uint4(ex | ((ex + p1) << 16), (ex + p2) | ((ex + p3) << 16), (ex + p4) | ((ex + p5) << 16),
+                          (ex + p6) | ((ex + p7) << 16));
+    }
+    __syncthreads();
+    if (!nv) return;
+    const uint64_t so = stream_off[t];
+    const uint32_t maxl = cb_len[types[t]] + 1;
+    uint32_t out[8];
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        uint32_t c = 0;
+        if ((uint32_t)j < nv) {
+            const uint32_t k = (kw[j >> 2] >> (8 * (j & 3))) & 0xffu;
+            const uint32_t krep = k * 0x01010101u;
+            uint32_t r = 0;  // equal keys of this block before j
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const int keep = j - 4 * w;
+                const uint32_t m = keep >= 4 ? 0xffffffffu : (keep <= 0 ? 0u : (1u << (8 * keep)) - 1u);
+                r += __popc(__vcmpeq4(kw[w], krep) & m);
+            }
+            r >>= 3;
+            const unsigned long long pos = s_base[k] + s_hc[k * 256 + tid] + r;
+            const uint32_t dv = d[so + pos];
+            c = k >= dv ? k - dv : k + B - dv;
+            bad |= c > maxl;
+        }
+        if (j & 1) out[j >> 1] |= c << 16;
+        else out[j >> 1] = c;
+    }
+    if (bad) atomicOr(err, kErrCorruptIndex);
+    uint4* cp = (uint4*)(cur + T.start + e0);
+    cp[0] = make_uint4(out[0], out[1], out[2], out[3]);
+    cp[1] = make_uint4(out[4], out[5], out[6], out[7]);
+}
+
 // ---- host ----------------------------------------------------------------------
 namespace {
 
@@ -834,8 +937,8 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
         for (int lt = 0; lt < kLayerTypes; ++lt)
             std::copy(q->cb[lt].begin(), q->cb[lt].end(), flat.begin() + (size_t)lt * stride);
         q->d_cb = (float*)e.dalloc(flat.size() * 4);
+        // pageable source: staged by the call, free to go out of scope on return
         DQTG_CUDA(cudaMemcpyAsync(q->d_cb, flat.data(), flat.size() * 4, cudaMemcpyHostToDevice, st));
-        e.sync();  // `flat` goes out of scope
     }
     // protected entries
     q->prot_count.assign(nt, 0);
@@ -965,7 +1068,13 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
             { DQTG_SPAN(e, "prev_count_kernel"); (B <= 64 ? prev_count_kernel<64> : prev_count_kernel<256>)<<<ntiles, 256, 0, st>>>(L.d_tiles, prev, B, d_tc, e.d_err); }
             auto* d_tot = (unsigned long long*)e.buf("d.ktot", (size_t)nt * B * 8 + 8);
             { DQTG_SPAN(e, "prev_scan_kernel"); prev_scan_kernel<<<nt * B, 256, 0, st>>>(L.d_tile0, B, d_tc, d_relems, d_tot, e.d_err); }
-            { DQTG_SPAN(e, "unrearrange_kernel"); (B <= 64 ? unrearrange_kernel<64> : unrearrange_kernel<256>)<<<ntiles, 256, 0, st>>>(L.d_tiles, L.d_types, L.d_stream_off, L.d_off, prev, B, d_tc, d_gs, d_d, d_cbl, q->d_levels, e.d_err); }
+            if (B <= 64 && !getenv("DQTG_UNREARRANGE_MATCH")) {
+                DQTG_SPAN(e, "unrearrange_kernel");
+                unrearrange16_kernel<<<ntiles, 256, 0, st>>>(L.d_tiles, L.d_types, L.d_stream_off, prev, B, d_tc, d_gs, d_d, d_cbl, q->d_levels, e.d_err);
+            } else {
+                DQTG_SPAN(e, "unrearrange_kernel");
+                (B <= 64 ? unrearrange_kernel<64> : unrearrange_kernel<256>)<<<ntiles, 256, 0, st>>>(L.d_tiles, L.d_types, L.d_stream_off, L.d_off, prev, B, d_tc, d_gs, d_d, d_cbl, q->d_levels, e.d_err);
+            }
             e.launched(3);
         }
         e.check_err();
@@ -1004,50 +1113,93 @@ BaseInfo base_info(const DecodePlan& p) {
     return b;
 }
 
-// Chain::restore (chain.cpp:131-154) over host records: the host walk of record k+1
-// runs on a helper thread while the device decodes record k (the walk needs only the
-// previous record's step and tensor table, not its levels).  on_state(k, state) sees
-// every decoded state; the last one is returned.  An error in record k+1 surfaces
-// after record k is decoded, as in the reference's sequential restore.
+// Chain::restore (chain.cpp:131-154) over host records.  The host walks of the next
+// records run on helper threads (up to kPlanAhead at a time) while the device decodes
+// record k.  A walk needs only its base's step and tensor table, not its levels, so
+// record j is walked speculatively against the step in record j-1's header and the
+// tensor table of record 0; once record j-1's own walk is known, a different table or
+// step re-walks record j against it, so every record is checked against its true base
+// (the walk is a pure function of the record and the base description).  Errors
+// surface in record order: an error in record k+1 after record k is decoded, as in
+// the reference's sequential restore.  on_state(k, state) sees every decoded state;
+// the last one is returned.
+namespace {
+bool same_base(const BaseInfo& a, const BaseInfo& b) {
+    return a.step == b.step && a.names == b.names && a.types == b.types && a.ranks == b.ranks &&
+           a.dims == b.dims;
+}
+}  // namespace
+
 std::unique_ptr<QState> decode_chain(Engine& e, const uint8_t* const* recs, const uint64_t* sizes,
                                      uint32_t n, const QState* base,
                                      const std::function<void(uint32_t, const QState&)>& on_state) {
     if (!n) return nullptr;
     for (uint32_t k = 0; k < n; ++k)
         DQTG_REQUIRE(!is_device_ptr(recs[k]), DQTG_ERROR, "decode_chain takes host records");
+    constexpr uint32_t kPlanAhead = 4;
     BaseInfo b0;
     if (base) b0 = base_info(*base);
     std::unique_ptr<DecodePlan> cur = decode_plan(e, recs[0], sizes[0], base ? &b0 : nullptr);
+    BaseInfo table0 = base_info(*cur);  // speculative tensor table of every later base
+    struct Walk {
+        std::thread th;
+        BaseInfo spec;
+        std::unique_ptr<DecodePlan> plan;
+        std::exception_ptr err;
+    };
+    std::vector<Walk> walks(n);
+    struct Joiner {  // no helper thread outlives the call (they reference `walks`)
+        std::vector<Walk>& w;
+        ~Joiner() {
+            for (auto& x : w)
+                if (x.th.joinable()) x.th.join();
+        }
+    } joiner{walks};
+    auto header_step = [&](uint32_t j) -> uint64_t {  // target step in record j's header
+        if (sizes[j] < 25) return ~0ull;  // truncated: its own walk reports it
+        uint64_t v = 0;
+        for (int i = 0; i < 8; ++i) v |= (uint64_t)recs[j][17 + i] << (8 * i);
+        return v;
+    };
+    uint32_t launched = 1;
+    auto launch = [&](uint32_t j) {
+        Walk& W = walks[j];
+        W.spec = table0;
+        W.spec.step = header_step(j - 1);
+        W.th = std::thread([&e, &W, recs, sizes, j] {
+            try {
+                W.plan = decode_plan(e, recs[j], sizes[j], &W.spec);
+            } catch (...) {
+                W.err = std::current_exception();
+            }
+        });
+    };
+    while (launched < n && launched <= kPlanAhead) launch(launched++);
     std::unique_ptr<QState> prev;
     const QState* pb = base;
     for (uint32_t k = 0; k < n; ++k) {
-        std::unique_ptr<DecodePlan> next;
-        std::exception_ptr perr;
-        std::thread th;
-        BaseInfo bn;
-        if (k + 1 < n) {
-            bn = base_info(*cur);
-            th = std::thread([&] {
-                try {
-                    next = decode_plan(e, recs[k + 1], sizes[k + 1], &bn);
-                } catch (...) {
-                    perr = std::current_exception();
-                }
-            });
-        }
-        std::unique_ptr<QState> s;
-        try {
-            s = decode_run(e, *cur, pb);
-            if (on_state) on_state(k, *s);
-        } catch (...) {
-            if (th.joinable()) th.join();
-            throw;
-        }
-        if (th.joinable()) th.join();
-        if (perr) std::rethrow_exception(perr);
+        BaseInfo actual;
+        if (k + 1 < n) actual = base_info(*cur);  // the true base of record k+1
+        std::unique_ptr<QState> s = decode_run(e, *cur, pb);
+        if (on_state) on_state(k, *s);
+        cur.reset();
         prev = std::move(s);
         pb = prev.get();
-        cur = std::move(next);
+        if (k + 1 == n) break;
+        Walk& W = walks[k + 1];
+        W.th.join();
+        if (!same_base(actual, W.spec)) {  // mis-speculated base: walk again
+            W.plan.reset();
+            W.err = nullptr;
+            try {
+                W.plan = decode_plan(e, recs[k + 1], sizes[k + 1], &actual);
+            } catch (...) {
+                W.err = std::current_exception();
+            }
+        }
+        if (W.err) std::rethrow_exception(W.err);
+        cur = std::move(W.plan);
+        if (launched < n) launch(launched++);
     }
     return prev;
 }

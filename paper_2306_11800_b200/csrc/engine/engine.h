@@ -332,6 +332,7 @@ std::unique_ptr<QState> decode_chain(Engine& e, const uint8_t* const* recs, cons
                                      uint32_t n, const QState* base,
                                      const std::function<void(uint32_t, const QState&)>& on_state);
 void dequantize(Engine& e, const QState& q, float* out_dev_padded);
+void dequantize_to(Engine& e, const QState& q, float* const* outs_dev);  // device array of nt outputs
 // same step, layout, codebooks, levels and protected entries (compared on the device)
 bool states_equal(Engine& e, const QState& a, const QState& b);
 // crc32 (codec.cpp:275-306) of a state's level stream (u16 LE, tensor order)

@@ -1107,37 +1107,115 @@ __global__ void __launch_bounds__(kPB) pass_c_kernel(PassIn a, const LtParams* l
 }
 
 // ---- dequantize (quantize.cpp:427-462) ----------------------------------------
-__global__ void dequant_kernel(const Tile* tiles, const uint8_t* types, const uint64_t* tensor_off,
-                               const float* cb, int cb_stride, const uint32_t* cb_len,
-                               const uint16_t* levels, const unsigned long long* tile_prot_off,
-                               const uint64_t* ppos, const uint16_t* pval, float* out,
-                               uint32_t* err) {
-    __shared__ unsigned long long s_scan[33];
+// Protected entries of tile ti: [lo[ti], hi[ti]) by binary search of the tile's element
+// range in its tensor's ascending positions (no pass over the levels).  Entries of a
+// tensor outside all of its tiles (positions >= numel) are unreferenced: CorruptIndex.
+__global__ void prot_tile_range_kernel(const Tile* tiles, int ntiles, const uint64_t* tensor_off,
+                                       const uint32_t* tile0, const unsigned long long* prot_off,
+                                       const uint64_t* ppos, unsigned long long* lo_hi,
+                                       uint32_t* err) {
+    const int ti = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ti >= ntiles) return;
+    const Tile T = tiles[ti];
+    const uint32_t t = T.tensor;
+    const unsigned long long base = prot_off[t], cnt = prot_off[t + 1] - base;
+    const uint64_t* p = ppos + base;
+    const uint64_t r0 = T.start - tensor_off[t], r1 = r0 + T.count;
+    auto lower = [&](uint64_t x) {
+        unsigned long long lo = 0, hi = cnt;
+        while (lo < hi) {
+            const unsigned long long mid = (lo + hi) >> 1;
+            if (p[mid] < x) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
+    const unsigned long long a = lower(r0), b = lower(r1);
+    lo_hi[2 * ti] = base + a;
+    lo_hi[2 * ti + 1] = base + b;
+    if ((uint32_t)ti + 1 == tile0[t + 1] && b != cnt) atomicOr(err, kErrCorruptIndex);
+}
+
+// out[t]: the tensor's output (device pointers); every protected level must meet its
+// entry in order, and every entry of the tile a protected level.  16 contiguous
+// levels per thread (two 16-byte loads), one block scan of the protected counts per
+// tile, float4 stores when the output is 16-byte aligned.
+__global__ void __launch_bounds__(256) dequant_kernel(const Tile* tiles, const uint8_t* types,
+                                                      const uint64_t* tensor_off, const float* cb,
+                                                      int cb_stride, const uint32_t* cb_len,
+                                                      const uint16_t* levels,
+                                                      const unsigned long long* lo_hi,
+                                                      const uint64_t* ppos, const uint16_t* pval,
+                                                      float* const* outs, uint32_t* err) {
+    __shared__ uint32_t s_slots[8];
     const Tile T = tiles[blockIdx.x];
     const int lt = types[T.tensor];
     const uint32_t k = cb_len[lt];
     const float* c = cb + lt * cb_stride;
-    unsigned long long o = tile_prot_off[blockIdx.x];
-    for (uint32_t i0 = 0; i0 < T.count; i0 += blockDim.x) {
-        uint32_t i = i0 + threadIdx.x;
-        uint16_t l = i < T.count ? levels[T.start + i] : 0;
-        unsigned long long isp = (i < T.count && l == k + 1) ? 1ull : 0ull, tot;
-        unsigned long long ex = block_exclusive_scan<unsigned long long>(isp, s_scan, &tot);
-        if (i < T.count) {
-            float v;
-            if (l < k) v = c[l];
-            else if (l == k) v = 0.0f;
-            else if (l == k + 1) {
-                if (ppos[o + ex] != (T.start - tensor_off[T.tensor]) + i) atomicOr(err, kErrCorruptIndex);
-                v = __uint_as_float((uint32_t)pval[o + ex] << 16);
-            }
-            else {
-                atomicOr(err, kErrCorruptIndex);
-                v = 0.0f;
-            }
-            out[T.start + i] = v;
+    const uint64_t rel0 = T.start - tensor_off[T.tensor];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t e0 = tid * 16;
+    const uint32_t nv = e0 < T.count ? min(T.count - e0, 16u) : 0u;
+    uint32_t lw[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // 16 levels, two per word
+    if (nv) {
+        const uint4* lp = (const uint4*)(levels + T.start + e0);  // tile starts are 64-aligned
+        const uint4 x = lp[0], y = lp[1];
+        lw[0] = x.x, lw[1] = x.y, lw[2] = x.z, lw[3] = x.w, lw[4] = y.x, lw[5] = y.y, lw[6] = y.z, lw[7] = y.w;
+    }
+    uint32_t pm = 0;  // protected elements of the thread
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const uint32_t l = (lw[j >> 1] >> (16 * (j & 1))) & 0xffffu;
+        if ((uint32_t)j < nv && l == k + 1) pm |= 1u << j;
+    }
+    // exclusive block scan of the protected counts (one barrier)
+    const uint32_t cnt = __popc(pm);
+    uint32_t x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_slots[wid] = x;
+    __syncthreads();
+    uint32_t base = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        const uint32_t sv = s_slots[w];
+        base += w < wid ? sv : 0u;
+        tot += sv;
+    }
+    const unsigned long long o0 = lo_hi[2 * blockIdx.x], o1 = lo_hi[2 * blockIdx.x + 1];
+    unsigned long long o = o0 + base + (x - cnt);
+    float v[16];
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const uint32_t l = (lw[j >> 1] >> (16 * (j & 1))) & 0xffffu;
+        float f = 0.0f;
+        if (l < k) {
+            f = __ldg(c + l);
+        } else if ((pm >> j) & 1u) {
+            if (o >= o1 || ppos[o] != rel0 + e0 + j) bad = true;
+            else f = __uint_as_float((uint32_t)pval[o] << 16);
+            ++o;
+        } else if (l != k && (uint32_t)j < nv) {
+            bad = true;
         }
-        o += tot;
+        v[j] = f;
+    }
+    if (bad) atomicOr(err, kErrCorruptIndex);
+    if (tid == 0 && tot != o1 - o0) atomicOr(err, kErrCorruptIndex);  // unreferenced entries
+    if (!nv) return;
+    float* out = outs[T.tensor] + rel0 + e0;
+    if (nv == 16 && ((uintptr_t)out & 15) == 0) {
+        float4* o4 = (float4*)out;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) o4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if ((uint32_t)j < nv) out[j] = v[j];
     }
 }
 
@@ -2347,26 +2425,37 @@ bool states_equal(Engine& e, const QState& a, const QState& b) {
     return h == 0;
 }
 
-void dequantize(Engine& e, const QState& q, float* out_dev) {
+// dequantize_checkpoint into device memory: outs[t] = tensor t's output (a device
+// array of nt pointers).  No host synchronisation: errors surface at the next check.
+void dequantize_to(Engine& e, const QState& q, float* const* outs_dev) {
     const Layout& L = *q.L;
     const int ntiles = (int)L.tiles.size();
+    for (uint32_t t = 0; t < L.nt; ++t)  // a tensor without tiles references no entries
+        DQTG_REQUIRE(L.numel[t] || !q.prot_count[t], DQTG_CORRUPT_INDEX, "unreferenced protected entries");
     if (!ntiles) return;
-    auto* tile_prot = (uint32_t*)e.buf("dq.tile_prot", (size_t)ntiles * 4 + 4);
-    auto* tile_off = (unsigned long long*)e.buf("dq.tile_off", (size_t)(ntiles + 1) * 8);
+    auto* lo_hi = (unsigned long long*)e.buf("dq.lohi", (size_t)ntiles * 16 + 16);
+    auto* poff = (unsigned long long*)e.buf("dq.poff", (size_t)(L.nt + 1) * 8);
     auto* cb_len_d = (uint32_t*)e.buf("dq.cblen", kLayerTypes * 4);
-    DQTG_CUDA(cudaMemcpyAsync(cb_len_d, q.cb_len, sizeof(q.cb_len), cudaMemcpyHostToDevice,
-                              e.stream));
-    count_protected(e, L, q.d_levels, cb_len_d, tile_prot);
-    { DQTG_SPAN(e, "scan_u32_kernel"); scan_u32_kernel<<<1, 1024, 0, e.stream>>>(tile_prot, ntiles, tile_off); }
-    unsigned long long total = 0;
-    e.d2h(&total, tile_off + ntiles, 8);
-    e.sync();
-    DQTG_REQUIRE(total == q.prot_total, DQTG_CORRUPT_INDEX, "unreferenced protected entries");
+    std::vector<unsigned long long> po(q.prot_off.begin(), q.prot_off.end());
+    po.resize(L.nt + 1, q.prot_total);
+    e.to_device(poff, po.data(), po.size() * 8);
+    e.to_device(cb_len_d, q.cb_len, sizeof(q.cb_len));
+    { DQTG_SPAN(e, "prot_tile_range_kernel"); prot_tile_range_kernel<<<(ntiles + 255) / 256, 256, 0, e.stream>>>(
+        L.d_tiles, ntiles, L.d_off, L.d_tile0, poff, q.d_ppos, lo_hi, e.d_err); }
     { DQTG_SPAN(e, "dequant_kernel"); dequant_kernel<<<ntiles, 256, 0, e.stream>>>(L.d_tiles, L.d_types, L.d_off, q.d_cb,
-                                                 (int)q.cb_stride, cb_len_d, q.d_levels, tile_off,
-                                                 q.d_ppos, q.d_pval, out_dev, e.d_err); }
+                                                 (int)q.cb_stride, cb_len_d, q.d_levels, lo_hi,
+                                                 q.d_ppos, q.d_pval, outs_dev, e.d_err); }
     e.launched(2);
     DQTG_CUDA(cudaGetLastError());
+}
+
+void dequantize(Engine& e, const QState& q, float* out_dev) {  // padded contiguous output
+    const Layout& L = *q.L;
+    std::vector<float*> ptrs(L.nt);
+    for (uint32_t t = 0; t < L.nt; ++t) ptrs[t] = out_dev + L.off[t];
+    auto* d = (float**)e.buf("dq.outs", (size_t)L.nt * 8 + 8);
+    e.to_device(d, ptrs.data(), (size_t)L.nt * 8);
+    dequantize_to(e, q, d);
 }
 
 void scan_tiles(Engine& e, const uint32_t* in, int n, unsigned long long* out) {
