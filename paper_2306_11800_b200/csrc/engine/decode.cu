@@ -91,6 +91,50 @@ struct DecodePlan {
     uint64_t sym_total = 0;
     std::string deferred_index;
     uint32_t stored_crc = 0;
+    // the device decode's uploads packed into one pinned block by the walk
+    Engine* eng = nullptr;
+    void* pin = nullptr;
+    size_t pin_cap = 0;
+    size_t o_rec = 0, o_groups = 0, o_chunks = 0, o_sym = 0, o_lim = 0, o_first = 0, o_lbase = 0,
+           o_relems = 0, o_gstart = 0, o_ppos = 0, o_pval = 0;
+    ~DecodePlan() {
+        if (pin) eng->pin_release(pin, pin_cap);
+    }
+    void stage() {
+        size_t o = 0;
+        auto take = [&](size_t bytes) {
+            const size_t at = o;
+            o += (bytes + 15) & ~(size_t)15;
+            return at;
+        };
+        o_rec = take(n);
+        o_groups = take(groups.size() * sizeof(GroupDesc));
+        o_chunks = take(chunks.size() * sizeof(ChunkDesc));
+        o_sym = take(tab_sym.size() * 8);
+        o_lim = take(lim.size() * 8);
+        o_first = take(first.size() * 8);
+        o_lbase = take(lbase.size() * 4);
+        o_relems = take(rec_elems.size() * 8);
+        o_gstart = take(gstart_h.size() * 8);
+        o_ppos = take(ppos.size() * 8);
+        o_pval = take(pval.size() * 2);
+        pin = eng->pin_acquire(o + 16, &pin_cap);
+        uint8_t* S = (uint8_t*)pin;
+        auto put = [&](size_t at, const void* src, size_t bytes) {
+            if (bytes) memcpy(S + at, src, bytes);
+        };
+        put(o_rec, h, n);
+        put(o_groups, groups.data(), groups.size() * sizeof(GroupDesc));
+        put(o_chunks, chunks.data(), chunks.size() * sizeof(ChunkDesc));
+        put(o_sym, tab_sym.data(), tab_sym.size() * 8);
+        put(o_lim, lim.data(), lim.size() * 8);
+        put(o_first, first.data(), first.size() * 8);
+        put(o_lbase, lbase.data(), lbase.size() * 4);
+        put(o_relems, rec_elems.data(), rec_elems.size() * 8);
+        put(o_gstart, gstart_h.data(), gstart_h.size() * 8);
+        put(o_ppos, ppos.data(), ppos.size() * 8);
+        put(o_pval, pval.data(), pval.size() * 2);
+    }
 };
 
 // ---- bit access: MSB-first stream (codec.cpp:111-122) -------------------------
@@ -878,6 +922,8 @@ std::unique_ptr<DecodePlan> decode_plan(Engine& e, const uint8_t* rec, uint64_t 
     P->stored_crc = r.le<uint32_t>();
     if (r.at != n) throw Fail(DQTG_IO, "trailing bytes after DQDR record");
     P->sym_total = sym_total;
+    P->eng = &e;
+    P->stage();
     return P;
 }
 
@@ -952,9 +998,13 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
     q->prot_off[nt] = q->prot_total = acc;
     q->d_ppos = (uint64_t*)e.dalloc((acc + 1) * 8);
     q->d_pval = (uint16_t*)e.dalloc((acc + 1) * 2);
+    const uint8_t* S = (const uint8_t*)P.pin;  // pinned staging of the walk
+    auto up = [&](void* dst, size_t off, size_t bytes) {
+        if (bytes) DQTG_CUDA(cudaMemcpyAsync(dst, S + off, bytes, cudaMemcpyHostToDevice, st));
+    };
     if (acc) {
-        e.to_device(q->d_ppos, ppos.data(), acc * 8);
-        e.to_device(q->d_pval, pval.data(), acc * 2);
+        up(q->d_ppos, P.o_ppos, acc * 8);
+        up(q->d_pval, P.o_pval, acc * 2);
     }
     q->d_levels = (uint16_t*)e.dalloc(L.Np * 2);
     DQTG_CUDA(cudaMemsetAsync(q->d_levels, 0, L.Np * 2, st));
@@ -963,7 +1013,7 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
     const uint32_t ng = (uint32_t)groups.size(), nc = (uint32_t)chunks.size();
     auto* d_rec = (uint8_t*)e.buf("d.rec", n + 32);
     DQTG_CUDA(cudaMemsetAsync(d_rec + n, 0, 32, st));
-    e.to_device(d_rec, rec, n);
+    up(d_rec, P.o_rec, n);
     auto* d_groups = (GroupDesc*)e.buf("d.groups", (size_t)(ng + 1) * sizeof(GroupDesc));
     auto* d_chunks = (ChunkDesc*)e.buf("d.chunks", (size_t)(nc + 1) * sizeof(ChunkDesc));
     auto* d_sym = (int64_t*)e.buf("d.tsym", (tab_sym.size() + 1) * 8);
@@ -971,13 +1021,13 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
     auto* d_first = (uint64_t*)e.buf("d.first", (first.size() + 1) * 8);
     auto* d_lbase = (uint32_t*)e.buf("d.lbase", (lbase.size() + 1) * 4);
     auto* d_relems = (unsigned long long*)e.buf("d.relems", rec_elems.size() * 8 + 8);
-    e.to_device(d_groups, groups.data(), ng * sizeof(GroupDesc));
-    e.to_device(d_chunks, chunks.data(), nc * sizeof(ChunkDesc));
-    e.to_device(d_sym, tab_sym.data(), tab_sym.size() * 8);
-    e.to_device(d_lim, lim.data(), lim.size() * 8);
-    e.to_device(d_first, first.data(), first.size() * 8);
-    e.to_device(d_lbase, lbase.data(), lbase.size() * 4);
-    e.to_device(d_relems, rec_elems.data(), rec_elems.size() * 8);
+    up(d_groups, P.o_groups, ng * sizeof(GroupDesc));
+    up(d_chunks, P.o_chunks, nc * sizeof(ChunkDesc));
+    up(d_sym, P.o_sym, tab_sym.size() * 8);
+    up(d_lim, P.o_lim, lim.size() * 8);
+    up(d_first, P.o_first, first.size() * 8);
+    up(d_lbase, P.o_lbase, lbase.size() * 4);
+    up(d_relems, P.o_relems, rec_elems.size() * 8);
     DecTabs T{d_lim, d_first, d_lbase, d_sym};
     mark("uploaded");
     const uint64_t* rec64 = (const uint64_t*)d_rec;
@@ -1060,7 +1110,7 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
         // ---- U: unrearrange against the previous levels
         auto* d_tc = (uint32_t*)e.buf("d.tilecnt", (size_t)ntiles * B * 4 + 4);
         auto* d_gs = (unsigned long long*)e.buf("d.gstart", (size_t)nt * B * 8 + 8);
-        e.to_device(d_gs, gstart_h.data(), gstart_h.size() * 8);
+        up(d_gs, P.o_gstart, gstart_h.size() * 8);
         auto* d_cbl = (uint32_t*)e.buf("d.cblen", kLayerTypes * 4);
         e.to_device(d_cbl, q->cb_len, sizeof(q->cb_len));
         const uint16_t* prev = base ? base->d_levels : nullptr;
@@ -1083,6 +1133,8 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
     // ---- C: stream checksum
     const uint32_t crc = level_stream_crc(e, L, q->d_levels);
     mark("crc");
+    e.pin_release(P.pin, P.pin_cap);  // every upload has completed (the CRC read synced)
+    P.pin = nullptr;
     if (crc != stored_crc)
         throw Fail(DQTG_CHECKSUM_MISMATCH, "record checksum mismatch at step " + std::to_string(target_step));
     return q;

@@ -102,6 +102,7 @@ Engine::~Engine() {
     }
     if (d_err) cudaFree(d_err);
     if (pinned) cudaFreeHost(pinned);
+    for (auto& b : pin_free) cudaFreeHost(b.first);
     for (auto& b : stage_blocks) cudaFreeHost(b.first);
     if (own_stream && stream) cudaStreamDestroy(stream);
     if (pool) {
@@ -300,6 +301,34 @@ void Engine::dfree(void* p) {
         }
     }
     cudaFreeAsync(p, stream);
+}
+
+void* Engine::pin_acquire(size_t bytes, size_t* cap) {
+    {
+        std::lock_guard<std::mutex> g(pin_mu);
+        size_t best = pin_free.size();
+        for (size_t i = 0; i < pin_free.size(); ++i)  // smallest block that fits
+            if (pin_free[i].second >= bytes && (best == pin_free.size() || pin_free[i].second < pin_free[best].second))
+                best = i;
+        if (best < pin_free.size()) {
+            auto b = pin_free[best];
+            pin_free.erase(pin_free.begin() + (long)best);
+            *cap = b.second;
+            return b.first;
+        }
+    }
+    void* p = nullptr;
+    const size_t c = bytes + bytes / 4 + 4096;
+    activate();  // may run on a helper thread: the engine's device, not device 0
+    DQTG_CUDA(cudaHostAlloc(&p, c, cudaHostAllocPortable));
+    *cap = c;
+    return p;
+}
+
+void Engine::pin_release(void* p, size_t cap) {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(pin_mu);
+    pin_free.emplace_back(p, cap);
 }
 
 void* Engine::host_pinned(size_t bytes) {

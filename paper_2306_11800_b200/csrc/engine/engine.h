@@ -237,6 +237,13 @@ struct Engine {
     // pools mid-step mapped new memory on the host thread (measured 11-470 ms stalls
     // in the worker pool).
     void* host_pinned(size_t bytes);
+    // Thread-safe pool of pinned host blocks (decode staging: a record's uploads are
+    // packed into one block by the walk thread, so the device decode issues
+    // asynchronous copies from pinned memory instead of staged pageable ones).
+    std::mutex pin_mu;
+    std::vector<std::pair<void*, size_t>> pin_free;
+    void* pin_acquire(size_t bytes, size_t* cap);
+    void pin_release(void* p, size_t cap);
     // Device->host read-back through a pinned staging arena: the copy is queued on
     // the engine stream and lands in `dst` at the next sync()/check_err().  (A
     // pageable destination would make the driver stage the copy synchronously,
