@@ -54,7 +54,8 @@ const char *dqtg_version(void);
 
 /* ---- engine ------------------------------------------------------------ */
 typedef struct dqtg_engine dqtg_engine;
-/* device: CUDA ordinal; stream: cudaStream_t to run on (NULL = engine-owned). */
+/* device: CUDA ordinal; stream: cudaStream_t to run on (NULL = an engine-owned
+ * non-blocking stream; pass cudaStreamLegacy to run on the legacy default stream). */
 dqtg_status dqtg_engine_create(int device, void *stream, dqtg_engine **out);
 void dqtg_engine_destroy(dqtg_engine *e);
 dqtg_status dqtg_engine_sync(dqtg_engine *e);

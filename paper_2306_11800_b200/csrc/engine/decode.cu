@@ -35,7 +35,7 @@
 
 namespace dqtg {
 
-constexpr uint32_t kChunkBits = 1024;
+constexpr uint32_t kChunkBits = 512;
 constexpr int kBnd = 24;  // codeword starts recorded per chunk (sync shortcut)
 constexpr int kMaxCodeLen = 64;
 

@@ -2090,7 +2090,9 @@ std::unique_ptr<QState> shard_stage3(Engine& e, const DevCkpt& c, const dqtg_con
         const uint32_t k = lt == kEmbedding ? cfg.embed_bins : cfg.bins;
         DQTG_REQUIRE(s.h_nkeys[lt] == 0 || (uint32_t)s.h_nkeys[lt] >= k, DQTG_ERROR,
                      "distinct-value codebook fallback needs all shards' values (unsupported "
-                     "when sharded)");
+                     "when sharded): layer type " + std::to_string(lt) + " has " +
+                         std::to_string(s.h_nkeys[lt]) + " distinct keys for " + std::to_string(k) +
+                         " bins");
     }
     std::vector<Stage*> v{&s};
     PassIn a = pass_in(e, c, T, (int)cfg.metric);

@@ -399,9 +399,21 @@ class DevState:
         return outs
 
 
+# cudaStreamLegacy: the handle of the legacy default stream (value 0 is NULL in the
+# C ABI, which means "the engine creates its own non-blocking stream")
+_CUDA_STREAM_LEGACY = 1
+
+
 class Engine:
     def __init__(self, device=0, stream=None):
+        """stream: a CUDA stream handle the engine works on, e.g.
+        ``torch.cuda.current_stream().cuda_stream``; None = the engine's own stream.
+        Handle 0 (torch's default stream) is the legacy default stream, so the engine
+        stays ordered with torch work issued there (a NULL handle would give the engine
+        a private non-blocking stream that races with it)."""
         h = _P()
+        if stream is not None and int(stream) == 0:
+            stream = _CUDA_STREAM_LEGACY
         _check(LIB.dqtg_engine_create(device, stream, C.byref(h)))
         self.h = h
 

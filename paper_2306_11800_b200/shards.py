@@ -49,6 +49,9 @@ class LocalShardedChain:
         self.t_engine = 0.0  # seconds spent in engine calls (loads excluded)
 
     def _timed(self, fn, *a):
+        # the histogram sums (torch ops) are complete before the engine reads them,
+        # whichever stream the engine runs on
+        self.torch.cuda.current_stream(self.dev).synchronize()
         t = time.perf_counter()
         r = fn(*a)
         self.eng.sync()
