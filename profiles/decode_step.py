@@ -38,6 +38,17 @@ def main():
     optr = E._ptr_array(W.tensor_ptrs(out.data_ptr(), layout))
     dec = eng.decode_record(recs[0])
     dec = eng.decode_record(recs[1], base=dec)
+    if os.environ.get("DQTG_CHAIN"):  # Chain::restore timing through decode_chain
+        def deq(k, h):
+            E._check(E.LIB.dqtg_dequantize(eng.h, h, optr))
+        for rep in range(3):
+            t = time.perf_counter()
+            d = eng.decode_chain(recs[2:], base=dec, on_state=deq)
+            eng.sync()
+            dt = time.perf_counter() - t
+            print(f"chain pass {rep}: {1e3 * dt / len(recs[2:]):.2f} ms/record, "
+                  f"{4.0 * N * len(recs[2:]) / dt / 1e9:.1f} GB/s fp32 out", flush=True)
+        return
     eng.profile(True)
     for rec in recs[2:]:
         t = time.perf_counter()
