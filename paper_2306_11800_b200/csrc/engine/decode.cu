@@ -214,11 +214,14 @@ __device__ __forceinline__ bool restart_chunk(uint32_t c, uint32_t local, uint64
 }
 
 // H1: decode chunk c from start[c] to its nominal end (dirty chunks only)
+// gate: null, or the previous pass's "some start moved" flag (0: converged, nothing to do)
 __global__ void __launch_bounds__(256) huff_sync_kernel(const uint64_t* rec64, const GroupDesc* groups,
                                                         const ChunkDesc* chunks, uint32_t nchunks,
                                                         DecTabs T, const uint64_t* start,
                                                         uint64_t* out_pos, uint32_t* count,
-                                                        const uint8_t* dirty, uint16_t* bounds) {
+                                                        const uint8_t* dirty, uint16_t* bounds,
+                                                        const uint32_t* gate) {
+    if (gate && !*gate) return;
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= nchunks || !dirty[c]) return;
     const ChunkDesc C = chunks[c];
@@ -228,7 +231,8 @@ __global__ void __launch_bounds__(256) huff_sync_kernel(const uint64_t* rec64, c
 // H1 update: every chunk takes the previous chunk's end as its start (in parallel)
 __global__ void huff_update_kernel(const ChunkDesc* chunks, uint32_t nchunks, uint64_t* start,
                                    const uint64_t* out_pos, uint32_t* count, uint8_t* dirty,
-                                   uint16_t* bounds, uint32_t* any) {
+                                   uint16_t* bounds, uint32_t* any, const uint32_t* gate) {
+    if (gate && !*gate) return;
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= nchunks) return;
     uint8_t d = 0;
@@ -249,7 +253,8 @@ __global__ void huff_update_kernel(const ChunkDesc* chunks, uint32_t nchunks, ui
 __global__ void huff_serial_sync_kernel(const uint64_t* rec64, const GroupDesc* groups, uint32_t ngroups,
                                         const ChunkDesc* chunks, DecTabs T, uint64_t* start,
                                         uint64_t* out_pos, uint32_t* count, uint16_t* bounds,
-                                        const uint8_t* dirty) {
+                                        const uint8_t* dirty, const uint32_t* gate) {
+    if (gate && !*gate) return;
     const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= ngroups) return;
     const GroupDesc G = groups[g];
@@ -923,7 +928,9 @@ std::unique_ptr<DecodePlan> decode_plan(Engine& e, const uint8_t* rec, uint64_t 
     if (r.at != n) throw Fail(DQTG_IO, "trailing bytes after DQDR record");
     P->sym_total = sym_total;
     P->eng = &e;
+    mark("walked");
     P->stage();
+    mark("staged");
     return P;
 }
 
@@ -1042,30 +1049,28 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
     auto* d_out = (uint64_t*)e.buf("d.outpos", (size_t)(nc + 1) * 8);
     auto* d_cnt = (uint32_t*)e.buf("d.cnt", (size_t)(nc + 1) * 4);
     auto* d_dirty = (uint8_t*)e.buf("d.dirty", (size_t)nc + 16);
-    auto* d_any = (uint32_t*)e.buf("d.any", 16);
+    auto* d_any = (uint32_t*)e.buf("d.any", 64);
     auto* d_bnd = (uint16_t*)e.buf("d.bounds", (size_t)(nc + 1) * kBnd * 2);
     {
         if (nc) { DQTG_SPAN(e, "chunk_init_kernel"); chunk_init_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_chunks, nc, d_start); }
         DQTG_CUDA(cudaMemsetAsync(d_dirty, 1, nc, st));
         const unsigned gb = (nc + 255) / 256;
         // a few parallel passes converge for Huffman tables in practice; what is still
-        // out of step after them is finished by the sequential per-group sweep
+        // out of step after them is finished by the sequential per-group sweep.  Every
+        // pass is gated on the previous pass's flag on the device (no host round trip):
+        // passes after convergence exit at once
         constexpr int kParallelPasses = 4;
-        for (int it = 0; nc; ++it) {
-            if (it == kParallelPasses) {
-                DQTG_SPAN(e, "huff_serial_sync_kernel");
-                huff_serial_sync_kernel<<<(ng + 127) / 128, 128, 0, st>>>(rec64, d_groups, ng, d_chunks, T, d_start, d_out, d_cnt, d_bnd, d_dirty);
-                e.launched(1);
-                break;
+        if (nc) {
+            DQTG_CUDA(cudaMemsetAsync(d_any, 0, 4 * kParallelPasses, st));
+            for (int it = 0; it < kParallelPasses; ++it) {
+                const uint32_t* gate = it ? d_any + it - 1 : nullptr;
+                { DQTG_SPAN(e, "huff_sync_kernel"); huff_sync_kernel<<<gb, 256, 0, st>>>(rec64, d_groups, d_chunks, nc, T, d_start, d_out, d_cnt, d_dirty, d_bnd, gate); }
+                { DQTG_SPAN(e, "huff_update_kernel"); huff_update_kernel<<<gb, 256, 0, st>>>(d_chunks, nc, d_start, d_out, d_cnt, d_dirty, d_bnd, d_any + it, gate); }
+                e.launched(2);
             }
-            { DQTG_SPAN(e, "huff_sync_kernel"); huff_sync_kernel<<<gb, 256, 0, st>>>(rec64, d_groups, d_chunks, nc, T, d_start, d_out, d_cnt, d_dirty, d_bnd); }
-            DQTG_CUDA(cudaMemsetAsync(d_any, 0, 4, st));
-            { DQTG_SPAN(e, "huff_update_kernel"); huff_update_kernel<<<gb, 256, 0, st>>>(d_chunks, nc, d_start, d_out, d_cnt, d_dirty, d_bnd, d_any); }
-            e.launched(2);
-            uint32_t any = 0;
-            e.d2h(&any, d_any, 4);
-            e.sync();
-            if (!any) break;
+            { DQTG_SPAN(e, "huff_serial_sync_kernel");
+              huff_serial_sync_kernel<<<(ng + 127) / 128, 128, 0, st>>>(rec64, d_groups, ng, d_chunks, T, d_start, d_out, d_cnt, d_bnd, d_dirty, d_any + kParallelPasses - 1); }
+            e.launched(1);
         }
         mark("synced");
         // chunks' symbol counts -> scan (u64)
@@ -1080,7 +1085,8 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
         auto* d_syms = (int32_t*)e.buf("d.syms", (sym_total + 1) * 4);
         { DQTG_SPAN(e, "huff_write_kernel"); huff_write_kernel<<<(nc + 255) / 256 + 1, 256, 0, st>>>(rec64, d_groups, d_chunks, nc, T, d_start, d_scan, d_syms, e.d_err); }
         e.launched(2);
-        e.check_err();
+        // Huffman and RLE-count errors are both CorruptBitstream: one check after both
+        // (the RLE kernels only read and write within the symbol arrays)
 
         mark("huffman");
         // ---- R: RLE expansion into the dense rearranged delta stream
@@ -1127,11 +1133,12 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
             }
             e.launched(3);
         }
-        e.check_err();
     }
     mark("unrearranged");
-    // ---- C: stream checksum
+    // ---- C: stream checksum (queued behind the unrearrange; its errors are checked
+    // first, as before the CRC compare)
     const uint32_t crc = level_stream_crc(e, L, q->d_levels);
+    e.check_err();
     mark("crc");
     e.pin_release(P.pin, P.pin_cap);  // every upload has completed (the CRC read synced)
     P.pin = nullptr;
@@ -1188,7 +1195,7 @@ std::unique_ptr<QState> decode_chain(Engine& e, const uint8_t* const* recs, cons
     if (!n) return nullptr;
     for (uint32_t k = 0; k < n; ++k)
         DQTG_REQUIRE(!is_device_ptr(recs[k]), DQTG_ERROR, "decode_chain takes host records");
-    constexpr uint32_t kPlanAhead = 4;
+    constexpr uint32_t kPlanAhead = 8;
     BaseInfo b0;
     if (base) b0 = base_info(*base);
     std::unique_ptr<DecodePlan> cur = decode_plan(e, recs[0], sizes[0], base ? &b0 : nullptr);
