@@ -49,7 +49,7 @@ struct GroupDesc {
     uint32_t tab_off, tsize;
     uint32_t chunk0, nchunks;
     uint32_t minlen, maxlen;
-    uint32_t lim_off;   // decode tables (kMaxCodeLen + 1 entries per group)
+    uint32_t lim_off;   // decode tables: entries for code lengths minlen..maxlen
     uint32_t pad;
 };
 
@@ -164,10 +164,10 @@ __device__ __forceinline__ uint32_t decode_one(const uint64_t* rec64, const Grou
     const uint64_t x = peek64(rec64, G.bit_off + p);
     const uint64_t* lim = T.lim + G.lim_off;
     uint32_t L = G.minlen;
-    while (L <= G.maxlen && x >= lim[L]) ++L;
+    while (L <= G.maxlen && x >= lim[L - G.minlen]) ++L;
     if (L > G.maxlen) return 0;
     const uint64_t code = x >> (64 - L);
-    idx = T.base[G.lim_off + L] + (uint32_t)(code - T.first[G.lim_off + L]);
+    idx = T.base[G.lim_off + L - G.minlen] + (uint32_t)(code - T.first[G.lim_off + L - G.minlen]);
     return L;
 }
 
@@ -870,9 +870,6 @@ std::unique_ptr<DecodePlan> decode_plan(Engine& e, const uint8_t* rec, uint64_t 
             G.nbits = nb * 8;
             r.at += nb;
             G.lim_off = (uint32_t)lim.size();
-            lim.resize(lim.size() + kMaxCodeLen + 1, ~0ull);
-            first.resize(first.size() + kMaxCodeLen + 1, 0);
-            lbase.resize(lbase.size() + kMaxCodeLen + 1, 0);
             // huffman_decode (codec.cpp:234-250) validates the table only when the group
             // has symbols: empty table, canonical order, lengths and the Kraft sum of
             // assign_codes (codec.cpp:196-214)
@@ -891,20 +888,25 @@ std::unique_ptr<DecodePlan> decode_plan(Engine& e, const uint8_t* rec, uint64_t 
                 // canonical decode limits
                 G.minlen = tab_len[G.tab_off];
                 G.maxlen = tab_len[G.tab_off + tsize - 1];
+                const size_t span = G.maxlen - G.minlen + 1;  // tables for minlen..maxlen only
+                lim.resize(lim.size() + span, ~0ull);
+                first.resize(first.size() + span, 0);
+                lbase.resize(lbase.size() + span, 0);
                 uint64_t code = 0;
                 uint32_t j = 0, prev_len = G.minlen;
                 for (uint32_t L = G.minlen; L <= G.maxlen; ++L) {
                     if (L > prev_len) code <<= (L - prev_len);
                     prev_len = L;
-                    first[G.lim_off + L] = code;
-                    lbase[G.lim_off + L] = j;
+                    const size_t at = G.lim_off + (L - G.minlen);
+                    first[at] = code;
+                    lbase[at] = j;
                     uint32_t cntL = 0;
                     while (j < tsize && tab_len[G.tab_off + j] == L) ++j, ++cntL;
                     code += cntL;
                     // Kraft sum > 1 <=> the next canonical code passes 2^L (L <= 63)
                     if (code > (1ull << L)) throw Fail(DQTG_CORRUPT_BITSTREAM, "huffman table overfull");
-                    lim[G.lim_off + L] = code << (64 - L);
-                    if (code == (1ull << L)) lim[G.lim_off + L] = ~0ull;  // complete code
+                    lim[at] = code << (64 - L);
+                    if (code == (1ull << L)) lim[at] = ~0ull;  // complete code
                 }
             }
             G.elem_off = stream_pos + total;
