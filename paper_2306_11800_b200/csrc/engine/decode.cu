@@ -372,8 +372,8 @@ struct Widen {
 constexpr unsigned long long kLongRun = 256;
 __global__ void rle_fill_sparse_kernel(const int32_t* syms, uint64_t n, const unsigned long long* off,
                                        const unsigned long long* cnt, uint32_t B, uint8_t* d,
-                                       unsigned long long* longs, unsigned int* nlong, uint32_t cap,
-                                       uint32_t* err) {
+                                       uint64_t nd, unsigned long long* longs, unsigned int* nlong,
+                                       uint32_t cap, uint32_t* err) {
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n;
          s += (uint64_t)gridDim.x * blockDim.x) {
         const unsigned long long c = cnt[s];
@@ -386,6 +386,10 @@ __global__ void rle_fill_sparse_kernel(const int32_t* syms, uint64_t n, const un
         if (x == 0) continue;
         const uint8_t v = (uint8_t)(-x);
         const unsigned long long o = off[s];
+        if (o + c > nd || o + c < o) {  // corrupt counts (flagged by rle_total too)
+            atomicOr(err, kErrCorruptBitstream);
+            continue;
+        }
         if (c <= kLongRun) {
             for (unsigned long long j = 0; j < c; ++j) d[o + j] = v;
         } else {
@@ -459,7 +463,8 @@ __global__ void __launch_bounds__(256) unrearrange_kernel(const Tile* tiles, con
                                                           const uint64_t* off, const uint16_t* prev,
                                                           uint32_t B, const uint32_t* tile_base,
                                                           const unsigned long long* gstart,
-                                                          const uint8_t* d, const uint32_t* cb_len,
+                                                          const uint8_t* d, uint64_t nd,
+                                                          const uint32_t* cb_len,
                                                           uint16_t* cur, uint32_t* err) {
     __shared__ uint32_t s_wc[8][KB];  // per-warp key counts -> per-warp key bases
     __shared__ uint32_t s_base[KB];
@@ -507,7 +512,7 @@ __global__ void __launch_bounds__(256) unrearrange_kernel(const Tile* tiles, con
         if (e >= T.count) continue;
         const uint32_t key = ky[j];
         const uint64_t pos = (uint64_t)s_base[key] + s_wc[wid][key] + rk[j];
-        const uint32_t dv = d[so + pos];
+        const uint32_t dv = so + pos < nd ? d[so + pos] : 0u;  // see unrearrange16_kernel
         const uint32_t c = key >= dv ? key - dv : key + B - dv;
         if (c > maxl) atomicOr(err, kErrCorruptIndex);
         cur[T.start + e] = (uint16_t)c;
@@ -524,7 +529,8 @@ __global__ void __launch_bounds__(256) unrearrange16_kernel(const Tile* tiles, c
                                                             const uint16_t* prev, uint32_t B,
                                                             const uint32_t* tile_base,
                                                             const unsigned long long* gstart,
-                                                            const uint8_t* d, const uint32_t* cb_len,
+                                                            const uint8_t* d, uint64_t nd,
+                                                            const uint32_t* cb_len,
                                                             uint16_t* cur, uint32_t* err) {
     __shared__ __align__(16) uint16_t s_hc[64 * 256];
     __shared__ unsigned long long s_base[64];
@@ -604,7 +610,9 @@ __global__ void __launch_bounds__(256) unrearrange16_kernel(const Tile* tiles, c
             }
             r >>= 3;
             const unsigned long long pos = s_base[k] + s_hc[k * 256 + tid] + r;
-            const uint32_t dv = d[so + pos];
+            // a key count that disagrees with the record's groups is flagged by U2;
+            // its positions may leave the stream
+            const uint32_t dv = so + pos < nd ? d[so + pos] : 0u;
             c = k >= dv ? k - dv : k + B - dv;
             bad |= c > maxl;
         }
@@ -1053,6 +1061,7 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
     auto* d_dirty = (uint8_t*)e.buf("d.dirty", (size_t)nc + 16);
     auto* d_any = (uint32_t*)e.buf("d.any", 64);
     auto* d_bnd = (uint16_t*)e.buf("d.bounds", (size_t)(nc + 1) * kBnd * 2);
+    uint32_t* d_err2 = nullptr;  // error word of the stages after the RLE counts
     {
         if (nc) { DQTG_SPAN(e, "chunk_init_kernel"); chunk_init_kernel<<<(nc + 255) / 256, 256, 0, st>>>(d_chunks, nc, d_start); }
         DQTG_CUDA(cudaMemsetAsync(d_dirty, 1, nc, st));
@@ -1102,8 +1111,13 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
         DQTG_CUDA(cub::DeviceScan::ExclusiveSum(tmp2, tb2, d_ecnt, d_eoff, (int64_t)std::max<uint64_t>(sym_total, 1), st));
         { DQTG_SPAN(e, "rle_total_kernel"); rle_total_kernel<<<(ng + 255) / 256 + 1, 256, 0, st>>>(d_groups, ng, d_eoff, d_ecnt, e.d_err); }
         e.launched(2);
-        e.check_err();
-        if (!deferred_index.empty()) throw Fail(DQTG_CORRUPT_INDEX, deferred_index);
+        // The later stages report into a second error word, read with the first one at
+        // the end (one synchronisation per record): bitstream errors of the Huffman /
+        // RLE-count stages first, then a bad group bucket found by the walk, then the
+        // later stages' index errors -- the reference's order.  The later kernels stay
+        // inside their buffers on corrupt input.
+        d_err2 = (uint32_t*)e.buf("d.err2", 16);
+        DQTG_CUDA(cudaMemsetAsync(d_err2, 0, 4, st));
         auto* d_d = (uint8_t*)e.buf("d.delta", N + 16);
         DQTG_CUDA(cudaMemsetAsync(d_d, 0, N + 16, st));
         // long runs: at most N / kLongRun of them
@@ -1111,7 +1125,7 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
         auto* d_long = (unsigned long long*)e.buf("d.longruns", (size_t)lcap * 8 + 8);
         auto* d_nlong = (unsigned int*)e.buf("d.nlong", 16);
         DQTG_CUDA(cudaMemsetAsync(d_nlong, 0, 4, st));
-        { DQTG_SPAN(e, "rle_fill_kernel"); rle_fill_sparse_kernel<<<rg, 256, 0, st>>>(d_syms, sym_total, d_eoff, d_ecnt, B, d_d, d_long, d_nlong, lcap, e.d_err); }
+        { DQTG_SPAN(e, "rle_fill_kernel"); rle_fill_sparse_kernel<<<rg, 256, 0, st>>>(d_syms, sym_total, d_eoff, d_ecnt, B, d_d, N, d_long, d_nlong, lcap, d_err2); }
         { DQTG_SPAN(e, "rle_fill_long_kernel"); rle_fill_long_kernel<<<e.num_sms * 4, 256, 0, st>>>(d_syms, d_eoff, d_ecnt, d_long, d_nlong, lcap, d_d); }
         e.launched(2);
 
@@ -1123,24 +1137,32 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
         e.to_device(d_cbl, q->cb_len, sizeof(q->cb_len));
         const uint16_t* prev = base ? base->d_levels : nullptr;
         if (ntiles) {
-            { DQTG_SPAN(e, "prev_count_kernel"); (B <= 64 ? prev_count_kernel<64> : prev_count_kernel<256>)<<<ntiles, 256, 0, st>>>(L.d_tiles, prev, B, d_tc, e.d_err); }
+            { DQTG_SPAN(e, "prev_count_kernel"); (B <= 64 ? prev_count_kernel<64> : prev_count_kernel<256>)<<<ntiles, 256, 0, st>>>(L.d_tiles, prev, B, d_tc, d_err2); }
             auto* d_tot = (unsigned long long*)e.buf("d.ktot", (size_t)nt * B * 8 + 8);
-            { DQTG_SPAN(e, "prev_scan_kernel"); prev_scan_kernel<<<nt * B, 256, 0, st>>>(L.d_tile0, B, d_tc, d_relems, d_tot, e.d_err); }
+            { DQTG_SPAN(e, "prev_scan_kernel"); prev_scan_kernel<<<nt * B, 256, 0, st>>>(L.d_tile0, B, d_tc, d_relems, d_tot, d_err2); }
             if (B <= 64 && !getenv("DQTG_UNREARRANGE_MATCH")) {
                 DQTG_SPAN(e, "unrearrange_kernel");
-                unrearrange16_kernel<<<ntiles, 256, 0, st>>>(L.d_tiles, L.d_types, L.d_stream_off, prev, B, d_tc, d_gs, d_d, d_cbl, q->d_levels, e.d_err);
+                unrearrange16_kernel<<<ntiles, 256, 0, st>>>(L.d_tiles, L.d_types, L.d_stream_off, prev, B, d_tc, d_gs, d_d, N, d_cbl, q->d_levels, d_err2);
             } else {
                 DQTG_SPAN(e, "unrearrange_kernel");
-                (B <= 64 ? unrearrange_kernel<64> : unrearrange_kernel<256>)<<<ntiles, 256, 0, st>>>(L.d_tiles, L.d_types, L.d_stream_off, L.d_off, prev, B, d_tc, d_gs, d_d, d_cbl, q->d_levels, e.d_err);
+                (B <= 64 ? unrearrange_kernel<64> : unrearrange_kernel<256>)<<<ntiles, 256, 0, st>>>(L.d_tiles, L.d_types, L.d_stream_off, L.d_off, prev, B, d_tc, d_gs, d_d, N, d_cbl, q->d_levels, d_err2);
             }
             e.launched(3);
         }
     }
     mark("unrearranged");
-    // ---- C: stream checksum (queued behind the unrearrange; its errors are checked
-    // first, as before the CRC compare)
+    // ---- C: stream checksum (queued behind the unrearrange; the error words are read
+    // with it and checked first, in stage order)
+    uint32_t h1 = 0, h2 = 0;
+    e.d2h(&h1, e.d_err, 4);
+    if (d_err2) e.d2h(&h2, d_err2, 4);
     const uint32_t crc = level_stream_crc(e, L, q->d_levels);
-    e.check_err();
+    if (h1 | h2) {
+        DQTG_CUDA(cudaMemsetAsync(e.d_err, 0, 4, st));
+        throw_err_bits(h1);
+    }
+    if (!deferred_index.empty()) throw Fail(DQTG_CORRUPT_INDEX, deferred_index);
+    throw_err_bits(h2);
     mark("crc");
     e.pin_release(P.pin, P.pin_cap);  // every upload has completed (the CRC read synced)
     P.pin = nullptr;
@@ -1200,8 +1222,8 @@ std::unique_ptr<QState> decode_chain(Engine& e, const uint8_t* const* recs, cons
     constexpr uint32_t kPlanAhead = 8;
     BaseInfo b0;
     if (base) b0 = base_info(*base);
-    std::unique_ptr<DecodePlan> cur = decode_plan(e, recs[0], sizes[0], base ? &b0 : nullptr);
-    BaseInfo table0 = base_info(*cur);  // speculative tensor table of every later base
+    BaseInfo table0;  // speculative tensor table of every later base
+    std::unique_ptr<DecodePlan> cur;
     struct Walk {
         std::thread th;
         BaseInfo spec;
@@ -1223,7 +1245,7 @@ std::unique_ptr<QState> decode_chain(Engine& e, const uint8_t* const* recs, cons
         return v;
     };
     uint32_t launched = 1;
-    auto launch = [&](uint32_t j) {
+    auto launch = [&](uint32_t j) {  // table0 is set
         Walk& W = walks[j];
         W.spec = table0;
         W.spec.step = header_step(j - 1);
@@ -1235,7 +1257,17 @@ std::unique_ptr<QState> decode_chain(Engine& e, const uint8_t* const* recs, cons
             }
         });
     };
-    while (launched < n && launched <= kPlanAhead) launch(launched++);
+    // With a base state, its tensor table is the speculation and the later walks start
+    // together with record 0's; otherwise they start from record 0's table
+    if (base) {
+        table0 = b0;
+        while (launched < n && launched <= kPlanAhead) launch(launched++);
+    }
+    cur = decode_plan(e, recs[0], sizes[0], base ? &b0 : nullptr);
+    if (!base) {
+        table0 = base_info(*cur);
+        while (launched < n && launched <= kPlanAhead) launch(launched++);
+    }
     std::unique_ptr<QState> prev;
     const QState* pb = base;
     for (uint32_t k = 0; k < n; ++k) {

@@ -318,7 +318,8 @@ void* Engine::pin_acquire(size_t bytes, size_t* cap) {
         }
     }
     void* p = nullptr;
-    const size_t c = bytes + bytes / 4 + 4096;
+    size_t c = 1u << 20;  // power-of-two classes: records of a chain wobble in size
+    while (c < bytes + bytes / 4) c <<= 1;
     activate();  // may run on a helper thread: the engine's device, not device 0
     DQTG_CUDA(cudaHostAlloc(&p, c, cudaHostAllocPortable));
     *cap = c;
@@ -403,6 +404,11 @@ void Engine::check_err(const char* fn, int line) {
     sync(fn, line);
     if (!h) return;
     DQTG_CUDA(cudaMemsetAsync(d_err, 0, 4, stream));
+    throw_err_bits(h);
+}
+
+void throw_err_bits(uint32_t h) {
+    if (!h) return;
     if (h & kErrNonFinite) throw Fail(DQTG_NON_FINITE, "input contains NaN/Inf");
     if (h & kErrEmptySketch) throw Fail(DQTG_EMPTY_SKETCH, "quantile of empty sketch");
     if (h & kErrCorruptIndex) throw Fail(DQTG_CORRUPT_INDEX, "level outside cyclic alphabet");

@@ -270,6 +270,7 @@ struct Engine {
 };
 
 bool is_device_ptr(const void* p);
+void throw_err_bits(uint32_t h);  // the Fail that check_err raises for device error bits h
 
 void timeline_epoch(Engine& e);  // DQTG_TIMELINE reference event (first call records it)
 void dump_timeline(Engine& e);   // recorded spans on stderr, relative to the epoch
