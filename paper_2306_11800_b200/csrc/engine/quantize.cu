@@ -462,6 +462,10 @@ constexpr int kCandMargin = 4;  // sketch buckets below the sample quantile (~8 
 
 struct A2Args {
     const float2* lo;               // [7]: candidate lower bounds (magnitude, sensitivity)
+    // [7]: bound slots; a layer type with a sensitivity bound (y >= 0) skips its
+    // sensitivity histogram here: the buckets above the bound are rebuilt from the
+    // candidates and everything below is one count (sens_from_cand / sens_lump)
+    const int2* lo_slot;
     unsigned long long* gh_w;       // [7][HS] signed histogram of w
     unsigned long long* gh_sens;    // [7][HS]
     uint4* cand;                    // (tile, element, w bits, sensitivity bits)
@@ -488,6 +492,7 @@ __global__ void __launch_bounds__(kPB, 5) pass_a2_kernel(PassIn a, A2Args f) {
     __shared__ int s_base;
     int cur = -1;
     float2 lo = make_float2(0.f, 0.f);
+    bool sens_hist = true;
     for (int base; (base = grab_tiles(a.tile_ctr, kGrab, &s_base)) < a.ntiles;)
     for (int ti = base; ti < min(base + kGrab, a.ntiles); ++ti) {
         const Tile T = a.tiles[ti];
@@ -502,6 +507,7 @@ __global__ void __launch_bounds__(kPB, 5) pass_a2_kernel(PassIn a, A2Args f) {
             __syncthreads();
             cur = lt;
             lo = f.lo[lt];
+            sens_hist = f.lo_slot[lt].y < 0;
         }
         unsigned long long* gw = f.gh_w + lt * a.HS;
         unsigned long long* gs = f.gh_sens + lt * a.HS;
@@ -527,8 +533,14 @@ __global__ void __launch_bounds__(kPB, 5) pass_a2_kernel(PassIn a, A2Args f) {
                 const float s = a.has_sens ? fabsf(__fmul_rn(ea[j], wa[j])) : 0.0f;  // ranker.cpp:96
                 if (!(fastc && hist_fast_signed(shw_s, __float_as_uint(wa[j]), fp)))
                     hist_add(shw, gw, wa[j], a.tab, a.err);
-                if (a.has_sens && !(fastc && hist_fast_pos(shs_s, __float_as_uint(s), fp)))
-                    hist_add_pos(shs, gs, s, a.tab, a.err);
+                if (a.has_sens) {
+                    if (sens_hist) {
+                        if (!(fastc && hist_fast_pos(shs_s, __float_as_uint(s), fp)))
+                            hist_add_pos(shs, gs, s, a.tab, a.err);
+                    } else if (__float_as_uint(s) >= 0x7f800000u) {
+                        atomicOr(a.err, kErrNonFinite);
+                    }
+                }
                 if (m > lo.x || (a.has_sens && s > lo.y)) cm |= 1u << (4 * g + j);
             }
         }
@@ -632,6 +644,7 @@ __global__ void __launch_bounds__(kPB, 3) pass_a2_tma_kernel(PassIn a, A2Args f)
     const uint32_t shs_s = (uint32_t)__cvta_generic_to_shared(shs);
     int cur = -1;
     float2 lo = make_float2(0.f, 0.f);
+    bool sens_hist = true;
     int item = s_next;
     for (uint32_t it = 0; item < 2 * a.ntiles; ++it) {
         const int slot = it & 1;
@@ -655,6 +668,7 @@ __global__ void __launch_bounds__(kPB, 3) pass_a2_tma_kernel(PassIn a, A2Args f)
             __syncthreads();
             cur = lt;
             lo = f.lo[lt];
+            sens_hist = f.lo_slot[lt].y < 0;
         }
         unsigned long long* gw = f.gh_w + lt * a.HS;
         unsigned long long* gs = f.gh_sens + lt * a.HS;
@@ -677,8 +691,14 @@ __global__ void __launch_bounds__(kPB, 3) pass_a2_tma_kernel(PassIn a, A2Args f)
                 const float s = a.has_sens ? fabsf(__fmul_rn(ea[j], wa[j])) : 0.0f;  // ranker.cpp:96
                 if (!(fastc && hist_fast_signed(shw_s, __float_as_uint(wa[j]), fp)))
                     hist_add(shw, gw, wa[j], a.tab, a.err);
-                if (a.has_sens && !(fastc && hist_fast_pos(shs_s, __float_as_uint(s), fp)))
-                    hist_add_pos(shs, gs, s, a.tab, a.err);
+                if (a.has_sens) {
+                    if (sens_hist) {
+                        if (!(fastc && hist_fast_pos(shs_s, __float_as_uint(s), fp)))
+                            hist_add_pos(shs, gs, s, a.tab, a.err);
+                    } else if (__float_as_uint(s) >= 0x7f800000u) {
+                        atomicOr(a.err, kErrNonFinite);  // the histogram would have said so
+                    }
+                }
                 if (m > lo.x || (a.has_sens && s > lo.y)) cm |= 1u << (4 * g + j);
             }
         }
@@ -735,7 +755,9 @@ __global__ void cand_bounds_kernel(const int* slot_g, const float* keyf, int64_t
     lo_slot[lt] = bs;
 }
 
-// exact threshold slots at or above the candidate bounds? (else: pass B)
+// exact threshold slots at or above the candidate bounds? (else: pass B)  The
+// sensitivity threshold must lie strictly above its bound: the bound's bucket holds
+// the lumped count of everything below (sens_lump_kernel)
 __global__ void cand_check_kernel(const int* slot_x, const int2* lo_slot,
                                   const unsigned long long* n_cand, unsigned long long cap,
                                   uint32_t* flag) {
@@ -746,9 +768,67 @@ __global__ void cand_check_kernel(const int* slot_x, const int2* lo_slot,
         const int x = slot_x[lt * 3 + which];
         const int b = which ? bs.y : bs.x;
         if (x < 0 && b < 0) continue;
-        if (x < 0 || b < 0 || x < b) atomicOr(flag, 2u);
+        if (x < 0 || b < 0 || x < b || (which == 1 && x == b)) atomicOr(flag, 2u);
     }
     if (lt == 0 && *n_cand > cap) atomicOr(flag, 4u);
+}
+
+// Sensitivity histogram of the layer types with a bound, from the candidate list: the
+// buckets above the bound's bucket hold candidates only (every element of them
+// exceeds the bound, the bucket's representative), so their counts are exact.
+// The candidates' sensitivities crowd into the few buckets above the bound: counted
+// per block in shared memory (a window of kSensWin buckets above each layer type's
+// bound), flushed once per block.
+constexpr int kSensWin = 512;
+__global__ void __launch_bounds__(256) sens_from_cand_kernel(PassIn a, const uint4* cand,
+                                                             const unsigned long long* n_cand,
+                                                             unsigned long long cap,
+                                                             const int2* lo_slot,
+                                                             unsigned long long* gh_sens) {
+    __shared__ uint32_t h[kLayerTypes * kSensWin];
+    __shared__ int s_l[kLayerTypes];
+    for (int i = threadIdx.x; i < kLayerTypes * kSensWin; i += blockDim.x) h[i] = 0;
+    if (threadIdx.x < kLayerTypes) s_l[threadIdx.x] = lo_slot[threadIdx.x].y;
+    __syncthreads();
+    const unsigned long long n = min(*n_cand, cap);
+    for (unsigned long long c = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; c < n;
+         c += (unsigned long long)gridDim.x * blockDim.x) {
+        const uint4 x = cand[c];
+        const int lt = a.types[a.tiles[x.x].tensor];
+        const int l = s_l[lt];
+        if (l < 0 || x.w >= 0x7f800000u) continue;  // non-finite: flagged by pass A2
+        const int64_t idx = slot_of(__uint_as_float(x.w), a.tab);
+        if (idx <= l) continue;
+        if (idx - l - 1 < kSensWin) atomicAdd(&h[lt * kSensWin + (idx - l - 1)], 1u);
+        else atomicAdd(gh_sens + (int64_t)lt * a.HS + idx, 1ull);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kLayerTypes * kSensWin; i += blockDim.x) {
+        const uint32_t v = h[i];
+        if (!v) continue;
+        const int lt = i / kSensWin;
+        atomicAdd(gh_sens + (int64_t)lt * a.HS + s_l[lt] + 1 + (i % kSensWin), (unsigned long long)v);
+    }
+}
+
+struct LtCounts {
+    unsigned long long n[kLayerTypes];
+};
+
+// ... and everything at or below the bound's bucket as one count in that bucket
+// (a quantile depends only on cumulative counts and the crossing bucket, sketch.cpp:59-78)
+__global__ void sens_lump_kernel(const int2* lo_slot, unsigned long long* gh_sens, int64_t HS,
+                                 LtCounts total) {
+    __shared__ unsigned long long s[33];
+    const int lt = blockIdx.x;
+    const int l = lo_slot[lt].y;
+    if (l < 0) return;
+    unsigned long long* g = gh_sens + (int64_t)lt * HS;
+    unsigned long long acc = 0;
+    for (int64_t i = l + 1 + threadIdx.x; i < HS; i += blockDim.x) acc += g[i];
+    unsigned long long tot;
+    block_exclusive_scan<unsigned long long>(acc, s, &tot);
+    if (threadIdx.x == 0) g[l] = total.n[lt] - tot;
 }
 
 // per-tensor sums of per-tile counts (one CTA per tensor)
@@ -1806,7 +1886,7 @@ static void stage_pass_a2(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s
     DQTG_CUDA(cudaMemsetAsync(prot, 0, hb, st));
     DQTG_CUDA(cudaMemsetAsync(small, 0, 32, st));
     DQTG_CUDA(cudaMemsetAsync(a.tile_ctr, 0, 4, st));
-    A2Args f{lo, gh_w, gh + (size_t)kLayerTypes * HS, cand, small, cap};
+    A2Args f{lo, lo_slot, gh_w, gh + (size_t)kLayerTypes * HS, cand, small, cap};
     const size_t ct = a.tab.ctab ? ((size_t)a.tab.ctab_n + 1) * 4 : 0;
     const size_t smem = (size_t)(kWinSlots + kPosSlots) * 4 + ct;
     if (getenv("DQTG_A2_REGS")) {  // the register-staged variant
@@ -1824,6 +1904,13 @@ static void stage_pass_a2(Engine& e, const DevCkpt& c, const PassIn& a, Stage& s
         { DQTG_SPAN(e, "pass_a2_kernel"); pass_a2_tma_kernel<<<stream_grid(e, a.ntiles, std::max(1, per_sm)), kPB, smem2, st>>>(a, f); }
     }
     { DQTG_SPAN(e, "fold_abs_kernel"); fold_abs_kernel<<<dim3((unsigned)((HS + 255) / 256), kLayerTypes), 256, 0, st>>>(gh_w, gh, HS, T.NB); }
+    if (c.has_sens) {  // the sensitivity histograms pass A2 left to the candidates
+        LtCounts tot{};
+        for (uint32_t i = 0; i < L.nt; ++i) tot.n[L.types[i]] += L.numel[i];
+        { DQTG_SPAN(e, "sens_from_cand_kernel"); sens_from_cand_kernel<<<e.num_sms * 2, 256, 0, st>>>(a, cand, small, cap, lo_slot, gh + (size_t)kLayerTypes * HS); }
+        { DQTG_SPAN(e, "sens_lump_kernel"); sens_lump_kernel<<<kLayerTypes, 256, 0, st>>>(lo_slot, gh + (size_t)kLayerTypes * HS, HS, tot); }
+        e.launched(2);
+    }
     // 3. exact thresholds, bound check, classification, value histogram
     stage_thresholds(e, s, HS, T, gh, gh + (size_t)kLayerTypes * HS, s.d_lp, slots + kLayerTypes * 3);
     auto* flag = (uint32_t*)(small + 1);
@@ -1962,8 +2049,14 @@ std::unique_ptr<QState> quantize(Engine& e, const DevCkpt& c, const dqtg_config&
         pbits = (uint32_t*)e.buf("q.pbits", (L.Np + 31) / 32 * 4 + 16);
         stage_pass_a2(e, c, a, s, T, pbits, &redo);
         e.check_err();  // syncs: n_keys + protected counts + the bound flag on the host
-        if (redo) {     // an exact threshold below its candidate bound: pass B
+        if (redo) {  // an exact threshold below its candidate bound: passes A + B
+            // (the sensitivity histograms of pass A2 were rebuilt above the bounds only,
+            // so the exact thresholds come from a full pass A)
             pbits = nullptr;
+            auto* gh = (unsigned long long*)e.buf("q.gh_scores", (size_t)2 * kLayerTypes * HS * 8);
+            DQTG_CUDA(cudaMemsetAsync(gh, 0, (size_t)2 * kLayerTypes * HS * 8, e.stream));
+            stage_pass_a(e, c, a, s.plan.mask_mag, s.plan.mask_sens, gh, gh + (size_t)kLayerTypes * HS);
+            stage_thresholds(e, s, HS, T, gh, gh + (size_t)kLayerTypes * HS);
             stage_pass_b(e, c, a, s, T);
             e.check_err();
         }
