@@ -69,6 +69,11 @@ def _step(eng, oracle, cfg, t0, t1, ema, derived, seed=7):
     # fused with pass A2 + candidates (default), fused with pass B, unfused
     for mode, env in (("fused", {}), ("fused_passb", {"DQTG_NO_PASS_A2": "1"}),
                       ("fused_a2_fallback", {"DQTG_A2_BOUND_SHIFT": "40"}),
+                      # bounds next to the thresholds: the sensitivity threshold in the
+                      # lumped bound bucket must fall back, one bucket above must not
+                      ("fused_a2_edge3", {"DQTG_A2_BOUND_SHIFT": "3"}),
+                      ("fused_a2_edge4", {"DQTG_A2_BOUND_SHIFT": "4"}),
+                      ("fused_a2_edge5", {"DQTG_A2_BOUND_SHIFT": "5"}),
                       ("unfused", {"DQTG_NO_FUSED_C": "1"})):
         os.environ.update(env)
         try:
