@@ -338,9 +338,10 @@ __global__ void __launch_bounds__(kCB, 4) enc_tile_kernel(EncArgs A) {
                     bad |= (hi[j] | hp_[j]) & m;
                 }
                 uint32_t big = 0;
+                const bool full = nv == (uint32_t)kIt;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const uint32_t m = keep_mask((int)nv - 4 * j);
+                    const uint32_t m = full ? 0xffffffffu : keep_mask((int)nv - 4 * j);
                     cw[j] &= m;
                     pw[j] &= m;
                     big |= __vcmpgeu4(cw[j], Brep) | __vcmpgeu4(pw[j], Brep);
@@ -906,9 +907,11 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A, FuseC
                         default: fused_levels<6>(s_lb, wp, pc, s_k, nv, cw, pmask);
 #undef DQTG_FL
                     }
-                    if (nv < (uint32_t)kIt) pmask &= (1u << nv) - 1u;
+                    if (nv < (uint32_t)kIt) {
+                        pmask &= (1u << nv) - 1u;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) cw[j] &= keep_mask((int)nv - 4 * j);
+                        for (int j = 0; j < 4; ++j) cw[j] &= keep_mask((int)nv - 4 * j);
+                    }
                     // u16 levels (little-endian: level, 0); the tile's padding gets 0
                     uint16_t* lp = F.levels + T.start + e0;
                     *(uint4*)lp = make_uint4(__byte_perm(cw[0], 0, 0x4140), __byte_perm(cw[0], 0, 0x4342),
@@ -943,9 +946,10 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A, FuseC
                     }
                 }
                 uint32_t big = 0;
+                const bool full = nv == (uint32_t)kIt;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const uint32_t m = keep_mask((int)nv - 4 * j);
+                    const uint32_t m = full ? 0xffffffffu : keep_mask((int)nv - 4 * j);
                     cw[j] &= m;
                     pw[j] &= m;
                     big |= __vcmpgeu4(cw[j], Brep) | __vcmpgeu4(pw[j], Brep);
@@ -1052,9 +1056,7 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A, FuseC
         const uint32_t nzt = s_zoff[B];
         uint32_t* Z = nzt <= (uint32_t)kZCap ? S.z : zg;
         // the thread's own 16 keys / deltas are its count block: ranks from registers
-        uint32_t nzw[4];
-#pragma unroll
-        for (int w = 0; w < 4; ++w) nzw[w] = __vcmpne4(dwv[w], 0u);
+        // (16-bit mask of the equal keys, counted below j)
         for (uint32_t m = nzm; m; m &= m - 1) {
             const uint32_t j = __ffs(m) - 1;
             const uint32_t wj = j >> 2, sh = 8 * (j & 3);
@@ -1062,15 +1064,13 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A, FuseC
             const uint32_t dwj = wj == 0 ? dwv[0] : wj == 1 ? dwv[1] : wj == 2 ? dwv[2] : dwv[3];
             const uint32_t k = (kwj >> sh) & 0xffu, v = (dwj >> sh) & 0xffu;
             const uint32_t krep = k * 0x01010101u;
-            uint32_t acc = 0, accnz = 0;  // same-key (non-zero) elements before j
+            uint32_t em = 0;
 #pragma unroll
-            for (int w = 0; w < 4; ++w) {
-                const uint32_t eq = __vcmpeq4(kw[w], krep) & keep_mask((int)j - 4 * w);
-                acc += __popc(eq);
-                accnz += __popc(eq & nzw[w]);
-            }
+            for (int w = 0; w < 4; ++w) em |= byte_msbs(__vcmpeq4(kw[w], krep)) << (4 * w);
+            const uint32_t below = em & ((1u << j) - 1u);
+            const uint32_t acc = __popc(below), accnz = __popc(below & nzm);  // same key before j
             const uint32_t pre = S.hc[k * kNBlk + tid];
-            Z[s_zoff[k] + (pre >> 16) + (accnz >> 3)] = ((pre & 0xffffu) + (acc >> 3)) | (v << 16) | (k << 24);
+            Z[s_zoff[k] + (pre >> 16) + accnz] = ((pre & 0xffffu) + acc) | (v << 16) | (k << 24);
         }
         __syncthreads();
         // ---- R: runs (key-sorted entries, consecutive slots per thread)
