@@ -799,14 +799,17 @@ __device__ __forceinline__ void fused_levels(const float* s_lb, const float* w, 
         uint32_t word = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            uint32_t pos = 0;
+            // the search walks a shared-memory pointer: one load with an immediate
+            // offset, one compare and one predicated add per step
+            const float* p = s_lb;
 #pragma unroll
             for (int st = (1 << LOGP) >> 1; st > 0; st >>= 1)
-                pos += (a[j] >= s_lb[pos + st]) ? (uint32_t)st : 0u;
+                if (a[j] >= p[st]) p += st;
+            const uint32_t pos = (uint32_t)(p - s_lb);
             const uint32_t part = (pw >> (2 * (4 * q + j))) & 3u;
-            const uint32_t lv = part == 0 ? pos : (part == 1 ? k : k + 1);
+            const uint32_t lv = part ? k + (part >> 1) : pos;  // PRUNED = k, PROTECTED = k + 1
             word |= lv << (8 * j);
-            pmask |= (part == 2 ? 1u : 0u) << (4 * q + j);
+            pmask |= (part >> 1) << (4 * q + j);
         }
         cw[q] = word;
     }
