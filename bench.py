@@ -452,6 +452,8 @@ def measure_big(torch, dev, steps=2):
     lay = W.llama3_8b_layout()
     names, types, shapes = ([x[i] for x in lay] for i in range(3))
     N = W.layout_params(lay)
+    if os.environ.get("DQTG_C5_OWN_STREAM"):  # diagnostics: the engine on a private stream
+        eng = E.Engine(0)
     ch = S.LocalShardedChain(eng, names, types, shapes, 8, cfg, seed=1, device=dev)
     gen = W.ShardSeries(torch, lay, ch.plan, SEED + 5, dev, bf16=True)
     sizes, rts, tq, td = [], [], [], []

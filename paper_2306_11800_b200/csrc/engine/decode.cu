@@ -66,6 +66,8 @@ struct BaseInfo {
     std::vector<std::vector<uint64_t>> dims;
 };
 
+constexpr size_t kPinStageMax = (size_t)96 << 20;
+
 // a record after the host walk (decode_plan), before the device decode (decode_run)
 struct DecodePlan {
     std::vector<uint8_t> host_copy;  // the record, when it was handed over in device memory
@@ -118,6 +120,10 @@ struct DecodePlan {
         o_gstart = take(gstart_h.size() * 8);
         o_ppos = take(ppos.size() * 8);
         o_pval = take(pval.size() * 2);
+        // very large records (billion-element shards) upload from the walk's own
+        // vectors: packing hundreds of MB into fresh pinned blocks costs more than the
+        // pageable copies save
+        if (o > kPinStageMax) return;
         pin = eng->pin_acquire(o + 16, &pin_cap);
         uint8_t* S = (uint8_t*)pin;
         auto put = [&](size_t at, const void* src, size_t bytes) {
@@ -432,7 +438,10 @@ __global__ void __launch_bounds__(256) prev_count_kernel(const Tile* tiles, cons
 
 // U2: one block per (tensor, key): exclusive prefix of the tile counts over the
 // tensor's tiles; key totals must match the record's group sizes
+// (tile_in: the counts, row stride in_stride -- the U1 counts, or the base state's
+// per-tile level histogram; tile_cnt: the prefixes, row stride B)
 __global__ void __launch_bounds__(256) prev_scan_kernel(const uint32_t* tile0, uint32_t B,
+                                                        const uint32_t* tile_in, uint32_t in_stride,
                                                         uint32_t* tile_cnt,
                                                         const unsigned long long* rec_elems,
                                                         unsigned long long* totals, uint32_t* err) {
@@ -442,7 +451,7 @@ __global__ void __launch_bounds__(256) prev_scan_kernel(const uint32_t* tile0, u
     unsigned long long run = 0;
     for (uint32_t c0 = t0; c0 < t1; c0 += blockDim.x) {
         const uint32_t ti = c0 + threadIdx.x;
-        const unsigned long long v = ti < t1 ? tile_cnt[(size_t)ti * B + b] : 0ull;
+        const unsigned long long v = ti < t1 ? tile_in[(size_t)ti * in_stride + b] : 0ull;
         unsigned long long tot;
         const unsigned long long ex = block_exclusive_scan<unsigned long long>(v, s_scan, &tot);
         if (ti < t1) tile_cnt[(size_t)ti * B + b] = (uint32_t)(run + ex);
@@ -531,7 +540,8 @@ __global__ void __launch_bounds__(256) unrearrange16_kernel(const Tile* tiles, c
                                                             const unsigned long long* gstart,
                                                             const uint8_t* d, uint64_t nd,
                                                             const uint32_t* cb_len,
-                                                            uint16_t* cur, uint32_t* err) {
+                                                            uint16_t* cur, uint32_t* hist_out,
+                                                            uint32_t* err) {
     __shared__ __align__(16) uint16_t s_hc[64 * 256];
     __shared__ unsigned long long s_base[64];
     const Tile T = tiles[blockIdx.x];
@@ -590,10 +600,9 @@ __global__ void __launch_bounds__(256) unrearrange16_kernel(const Tile* tiles, c
                           (ex + p6) | ((ex + p7) << 16));
     }
     __syncthreads();
-    if (!nv) return;
     const uint64_t so = stream_off[t];
     const uint32_t maxl = cb_len[types[t]] + 1;
-    uint32_t out[8];
+    uint32_t out[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     bool bad = false;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
@@ -620,9 +629,39 @@ __global__ void __launch_bounds__(256) unrearrange16_kernel(const Tile* tiles, c
         else out[j >> 1] = c;
     }
     if (bad) atomicOr(err, kErrCorruptIndex);
-    uint4* cp = (uint4*)(cur + T.start + e0);
-    cp[0] = make_uint4(out[0], out[1], out[2], out[3]);
-    cp[1] = make_uint4(out[4], out[5], out[6], out[7]);
+    if (nv) {
+        uint4* cp = (uint4*)(cur + T.start + e0);
+        cp[0] = make_uint4(out[0], out[1], out[2], out[3]);
+        cp[1] = make_uint4(out[4], out[5], out[6], out[7]);
+    }
+    if (!hist_out) return;
+    // per-tile counts of the decoded levels (< B <= 64), for the next record's decode:
+    // the count blocks again, one column per thread, then a sum per level
+    __syncthreads();  // every prefix of s_hc has been read
+    for (uint32_t i = tid; i < 64 * 32; i += 256) ((uint4*)s_hc)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+        if ((uint32_t)j < nv) ++s_hc[((out[j >> 1] >> (16 * (j & 1))) & 63u) * 256 + tid];
+    __syncthreads();
+    for (uint32_t v = wid; v < 64; v += 8) {
+        const uint4 x = ((const uint4*)(s_hc + v * 256))[lane];
+        uint32_t c = (x.x & 0xffffu) + (x.x >> 16) + (x.y & 0xffffu) + (x.y >> 16) + (x.z & 0xffffu) +
+                     (x.z >> 16) + (x.w & 0xffffu) + (x.w >> 16);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) hist_out[(size_t)blockIdx.x * 64 + v] = c;
+    }
+}
+
+// the base's level histogram as key counts: levels >= B are outside the alphabet
+// (U1 reports them when it counts the levels itself)
+__global__ void hist_range_check_kernel(const uint32_t* hist, int ntiles, uint32_t B, uint32_t* err) {
+    const int ti = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ti >= ntiles) return;
+    uint32_t any = 0;
+    for (uint32_t v = B; v < 64; ++v) any |= hist[(size_t)ti * 64 + v];
+    if (any) atomicOr(err, kErrCorruptIndex);
 }
 
 // ---- host ----------------------------------------------------------------------
@@ -946,7 +985,9 @@ std::unique_ptr<DecodePlan> decode_plan(Engine& e, const uint8_t* rec, uint64_t 
 
 // Device decode of a planned record against its base state (the base's levels are
 // only read here).
-std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base) {
+// base_hist: the base's per-tile level histogram may replace the key count pass (a
+// state decoded within the same chain restore, never handed to the caller in between)
+std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base, bool base_hist = false) {
     cudaStream_t st = e.stream;
     const bool trace = getenv("DQTG_DECODE_TRACE") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
@@ -1015,13 +1056,15 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
     q->prot_off[nt] = q->prot_total = acc;
     q->d_ppos = (uint64_t*)e.dalloc((acc + 1) * 8);
     q->d_pval = (uint16_t*)e.dalloc((acc + 1) * 2);
-    const uint8_t* S = (const uint8_t*)P.pin;  // pinned staging of the walk
-    auto up = [&](void* dst, size_t off, size_t bytes) {
-        if (bytes) DQTG_CUDA(cudaMemcpyAsync(dst, S + off, bytes, cudaMemcpyHostToDevice, st));
+    const uint8_t* S = (const uint8_t*)P.pin;  // pinned staging of the walk, if packed
+    auto up = [&](void* dst, size_t off, size_t bytes, const void* src) {
+        if (!bytes) return;
+        if (S) DQTG_CUDA(cudaMemcpyAsync(dst, S + off, bytes, cudaMemcpyHostToDevice, st));
+        else e.to_device(dst, src, bytes);
     };
     if (acc) {
-        up(q->d_ppos, P.o_ppos, acc * 8);
-        up(q->d_pval, P.o_pval, acc * 2);
+        up(q->d_ppos, P.o_ppos, acc * 8, ppos.data());
+        up(q->d_pval, P.o_pval, acc * 2, pval.data());
     }
     q->d_levels = (uint16_t*)e.dalloc(L.Np * 2);
     DQTG_CUDA(cudaMemsetAsync(q->d_levels, 0, L.Np * 2, st));
@@ -1030,7 +1073,7 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
     const uint32_t ng = (uint32_t)groups.size(), nc = (uint32_t)chunks.size();
     auto* d_rec = (uint8_t*)e.buf("d.rec", n + 32);
     DQTG_CUDA(cudaMemsetAsync(d_rec + n, 0, 32, st));
-    up(d_rec, P.o_rec, n);
+    up(d_rec, P.o_rec, n, rec);
     auto* d_groups = (GroupDesc*)e.buf("d.groups", (size_t)(ng + 1) * sizeof(GroupDesc));
     auto* d_chunks = (ChunkDesc*)e.buf("d.chunks", (size_t)(nc + 1) * sizeof(ChunkDesc));
     auto* d_sym = (int64_t*)e.buf("d.tsym", (tab_sym.size() + 1) * 8);
@@ -1038,13 +1081,13 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
     auto* d_first = (uint64_t*)e.buf("d.first", (first.size() + 1) * 8);
     auto* d_lbase = (uint32_t*)e.buf("d.lbase", (lbase.size() + 1) * 4);
     auto* d_relems = (unsigned long long*)e.buf("d.relems", rec_elems.size() * 8 + 8);
-    up(d_groups, P.o_groups, ng * sizeof(GroupDesc));
-    up(d_chunks, P.o_chunks, nc * sizeof(ChunkDesc));
-    up(d_sym, P.o_sym, tab_sym.size() * 8);
-    up(d_lim, P.o_lim, lim.size() * 8);
-    up(d_first, P.o_first, first.size() * 8);
-    up(d_lbase, P.o_lbase, lbase.size() * 4);
-    up(d_relems, P.o_relems, rec_elems.size() * 8);
+    up(d_groups, P.o_groups, ng * sizeof(GroupDesc), groups.data());
+    up(d_chunks, P.o_chunks, nc * sizeof(ChunkDesc), chunks.data());
+    up(d_sym, P.o_sym, tab_sym.size() * 8, tab_sym.data());
+    up(d_lim, P.o_lim, lim.size() * 8, lim.data());
+    up(d_first, P.o_first, first.size() * 8, first.data());
+    up(d_lbase, P.o_lbase, lbase.size() * 4, lbase.data());
+    up(d_relems, P.o_relems, rec_elems.size() * 8, rec_elems.data());
     DecTabs T{d_lim, d_first, d_lbase, d_sym};
     mark("uploaded");
     const uint64_t* rec64 = (const uint64_t*)d_rec;
@@ -1132,17 +1175,28 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
         // ---- U: unrearrange against the previous levels
         auto* d_tc = (uint32_t*)e.buf("d.tilecnt", (size_t)ntiles * B * 4 + 4);
         auto* d_gs = (unsigned long long*)e.buf("d.gstart", (size_t)nt * B * 8 + 8);
-        up(d_gs, P.o_gstart, gstart_h.size() * 8);
+        up(d_gs, P.o_gstart, gstart_h.size() * 8, gstart_h.data());
         auto* d_cbl = (uint32_t*)e.buf("d.cblen", kLayerTypes * 4);
         e.to_device(d_cbl, q->cb_len, sizeof(q->cb_len));
         const uint16_t* prev = base ? base->d_levels : nullptr;
         if (ntiles) {
-            { DQTG_SPAN(e, "prev_count_kernel"); (B <= 64 ? prev_count_kernel<64> : prev_count_kernel<256>)<<<ntiles, 256, 0, st>>>(L.d_tiles, prev, B, d_tc, d_err2); }
+            const bool fast = B <= 64 && !getenv("DQTG_UNREARRANGE_MATCH");
+            const uint32_t* tin = d_tc;
+            uint32_t in_stride = B;
+            if (fast && base && base_hist && base->d_tile_hist && !getenv("DQTG_NO_TILE_HIST")) {
+                tin = base->d_tile_hist;  // U1 from the previous decode
+                in_stride = 64;
+                { DQTG_SPAN(e, "hist_range_check_kernel"); hist_range_check_kernel<<<(ntiles + 255) / 256, 256, 0, st>>>(tin, ntiles, B, d_err2); }
+            } else {
+                DQTG_SPAN(e, "prev_count_kernel");
+                (B <= 64 ? prev_count_kernel<64> : prev_count_kernel<256>)<<<ntiles, 256, 0, st>>>(L.d_tiles, prev, B, d_tc, d_err2);
+            }
             auto* d_tot = (unsigned long long*)e.buf("d.ktot", (size_t)nt * B * 8 + 8);
-            { DQTG_SPAN(e, "prev_scan_kernel"); prev_scan_kernel<<<nt * B, 256, 0, st>>>(L.d_tile0, B, d_tc, d_relems, d_tot, d_err2); }
-            if (B <= 64 && !getenv("DQTG_UNREARRANGE_MATCH")) {
+            { DQTG_SPAN(e, "prev_scan_kernel"); prev_scan_kernel<<<nt * B, 256, 0, st>>>(L.d_tile0, B, tin, in_stride, d_tc, d_relems, d_tot, d_err2); }
+            if (fast) {
+                q->d_tile_hist = (uint32_t*)e.dalloc((size_t)ntiles * 64 * 4);
                 DQTG_SPAN(e, "unrearrange_kernel");
-                unrearrange16_kernel<<<ntiles, 256, 0, st>>>(L.d_tiles, L.d_types, L.d_stream_off, prev, B, d_tc, d_gs, d_d, N, d_cbl, q->d_levels, d_err2);
+                unrearrange16_kernel<<<ntiles, 256, 0, st>>>(L.d_tiles, L.d_types, L.d_stream_off, prev, B, d_tc, d_gs, d_d, N, d_cbl, q->d_levels, q->d_tile_hist, d_err2);
             } else {
                 DQTG_SPAN(e, "unrearrange_kernel");
                 (B <= 64 ? unrearrange_kernel<64> : unrearrange_kernel<256>)<<<ntiles, 256, 0, st>>>(L.d_tiles, L.d_types, L.d_stream_off, L.d_off, prev, B, d_tc, d_gs, d_d, N, d_cbl, q->d_levels, d_err2);
@@ -1164,7 +1218,7 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base)
     if (!deferred_index.empty()) throw Fail(DQTG_CORRUPT_INDEX, deferred_index);
     throw_err_bits(h2);
     mark("crc");
-    e.pin_release(P.pin, P.pin_cap);  // every upload has completed (the CRC read synced)
+    if (P.pin) e.pin_release(P.pin, P.pin_cap);  // every upload has completed (the CRC read synced)
     P.pin = nullptr;
     if (crc != stored_crc)
         throw Fail(DQTG_CHECKSUM_MISMATCH, "record checksum mismatch at step " + std::to_string(target_step));
@@ -1273,7 +1327,7 @@ std::unique_ptr<QState> decode_chain(Engine& e, const uint8_t* const* recs, cons
     for (uint32_t k = 0; k < n; ++k) {
         BaseInfo actual;
         if (k + 1 < n) actual = base_info(*cur);  // the true base of record k+1
-        std::unique_ptr<QState> s = decode_run(e, *cur, pb);
+        std::unique_ptr<QState> s = decode_run(e, *cur, pb, k > 0);
         if (on_state) on_state(k, *s);
         cur.reset();
         prev = std::move(s);

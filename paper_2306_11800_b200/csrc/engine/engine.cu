@@ -721,6 +721,7 @@ QState::~QState() {
     eng->dfree(d_levels);
     eng->dfree(d_ppos);
     eng->dfree(d_pval);
+    eng->dfree(d_tile_hist);
 }
 
 Record::~Record() {

@@ -162,6 +162,9 @@ struct QState {
     uint16_t* d_levels = nullptr;  // padded flat
     uint64_t* d_ppos = nullptr;    // protected positions (tensor-local), tensor order
     uint16_t* d_pval = nullptr;
+    // decoded states (alphabet <= 64): per tile, counts of each level value 0..63 -- the
+    // next record's per-tile key counts, so its decode skips a pass over these levels
+    uint32_t* d_tile_hist = nullptr;
     std::vector<uint64_t> prot_count, prot_off;  // per tensor
     uint64_t prot_total = 0;
     uint32_t max_levels() const;
