@@ -987,7 +987,9 @@ std::unique_ptr<DecodePlan> decode_plan(Engine& e, const uint8_t* rec, uint64_t 
 // only read here).
 // base_hist: the base's per-tile level histogram may replace the key count pass (a
 // state decoded within the same chain restore, never handed to the caller in between)
-std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base, bool base_hist = false) {
+// want_hist: the decoded state will be the base of the next record of the chain
+std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base, bool base_hist = false,
+                                   bool want_hist = false) {
     cudaStream_t st = e.stream;
     const bool trace = getenv("DQTG_DECODE_TRACE") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
@@ -1194,7 +1196,7 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base,
             auto* d_tot = (unsigned long long*)e.buf("d.ktot", (size_t)nt * B * 8 + 8);
             { DQTG_SPAN(e, "prev_scan_kernel"); prev_scan_kernel<<<nt * B, 256, 0, st>>>(L.d_tile0, B, tin, in_stride, d_tc, d_relems, d_tot, d_err2); }
             if (fast) {
-                q->d_tile_hist = (uint32_t*)e.dalloc((size_t)ntiles * 64 * 4);
+                if (want_hist) q->d_tile_hist = (uint32_t*)e.dalloc((size_t)ntiles * 64 * 4);
                 DQTG_SPAN(e, "unrearrange_kernel");
                 unrearrange16_kernel<<<ntiles, 256, 0, st>>>(L.d_tiles, L.d_types, L.d_stream_off, prev, B, d_tc, d_gs, d_d, N, d_cbl, q->d_levels, q->d_tile_hist, d_err2);
             } else {
@@ -1327,7 +1329,7 @@ std::unique_ptr<QState> decode_chain(Engine& e, const uint8_t* const* recs, cons
     for (uint32_t k = 0; k < n; ++k) {
         BaseInfo actual;
         if (k + 1 < n) actual = base_info(*cur);  // the true base of record k+1
-        std::unique_ptr<QState> s = decode_run(e, *cur, pb, k > 0);
+        std::unique_ptr<QState> s = decode_run(e, *cur, pb, k > 0, k + 1 < n);
         if (on_state) on_state(k, *s);
         cur.reset();
         prev = std::move(s);
