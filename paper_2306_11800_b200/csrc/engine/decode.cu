@@ -50,7 +50,7 @@ struct GroupDesc {
     uint32_t chunk0, nchunks;
     uint32_t minlen, maxlen;
     uint32_t lim_off;   // decode tables: entries for code lengths minlen..maxlen
-    uint32_t pad;
+    uint32_t lut;       // the group's index: its 1024-entry first-10-bits table
 };
 
 struct ChunkDesc {
@@ -161,20 +161,55 @@ struct DecTabs {
     const uint64_t* first;  // canonical first code of length L
     const uint32_t* base;   // table index of the first symbol of length L
     const int64_t* syms;
+    const uint32_t* lut;    // per group, indexed by the next 10 bits: idx << 8 | length
+                            // for codes of <= 10 bits, 0 otherwise
 };
+constexpr int kLutBits = 10;
 
 // Decodes the codeword at bit p (relative to the group stream); returns its length
 // and the table index, or length 0 for an invalid code.
 __device__ __forceinline__ uint32_t decode_one(const uint64_t* rec64, const GroupDesc& G,
                                                const DecTabs& T, uint64_t p, uint32_t& idx) {
     const uint64_t x = peek64(rec64, G.bit_off + p);
+    const uint32_t ent = T.lut[(size_t)G.lut << kLutBits | (uint32_t)(x >> (64 - kLutBits))];
+    if (ent & 0xffu) {  // a code of at most kLutBits bits: one lookup
+        idx = ent >> 8;
+        return ent & 0xffu;
+    }
+    // longer codes: the canonical limits from length kLutBits + 1 (every shorter
+    // length's limit is <= x, which is what a zero table entry records)
     const uint64_t* lim = T.lim + G.lim_off;
-    uint32_t L = G.minlen;
+    uint32_t L = max(G.minlen, (uint32_t)kLutBits + 1);
     while (L <= G.maxlen && x >= lim[L - G.minlen]) ++L;
     if (L > G.maxlen) return 0;
     const uint64_t code = x >> (64 - L);
     idx = T.base[G.lim_off + L - G.minlen] + (uint32_t)(code - T.first[G.lim_off + L - G.minlen]);
     return L;
+}
+
+// The first-kLutBits table of every group with symbols (one CTA per group): entry e
+// is the canonical decode of the bits e followed by zeros when its code is at most
+// kLutBits long (codes of length L are decided by their first L bits alone).
+__global__ void huff_lut_kernel(const GroupDesc* groups, DecTabs T, uint32_t* lut) {
+    const GroupDesc G = groups[blockIdx.x];
+    uint32_t* out = lut + ((size_t)blockIdx.x << kLutBits);
+    const uint64_t* lim = T.lim + G.lim_off;
+    const uint32_t top = min(G.maxlen, (uint32_t)kLutBits);
+    for (uint32_t e = threadIdx.x; e < (1u << kLutBits); e += blockDim.x) {
+        uint32_t ent = 0;
+        if (G.nsyms) {
+            const uint64_t x = (uint64_t)e << (64 - kLutBits);
+            uint32_t L = G.minlen;
+            while (L <= top && x >= lim[L - G.minlen]) ++L;
+            if (L <= top) {
+                const uint64_t code = x >> (64 - L);
+                const uint32_t idx = T.base[G.lim_off + L - G.minlen] +
+                                     (uint32_t)(code - T.first[G.lim_off + L - G.minlen]);
+                if (idx < (1u << 24)) ent = idx << 8 | L;
+            }
+        }
+        out[e] = ent;
+    }
 }
 
 // Decodes chunk c from start[c] to its nominal end: end position, symbol count and
@@ -968,6 +1003,7 @@ std::unique_ptr<DecodePlan> decode_plan(Engine& e, const uint8_t* rec, uint64_t 
                 gstart_h[(size_t)i * B + bucket] = total;
             }
             total += G.elems;
+            G.lut = (uint32_t)groups.size();
             groups.push_back(G);
         }
         if (total != numel) throw Fail(DQTG_CORRUPT_INDEX, "group totals do not cover the tensor");
@@ -1090,7 +1126,9 @@ std::unique_ptr<QState> decode_run(Engine& e, DecodePlan& P, const QState* base,
     up(d_first, P.o_first, first.size() * 8, first.data());
     up(d_lbase, P.o_lbase, lbase.size() * 4, lbase.data());
     up(d_relems, P.o_relems, rec_elems.size() * 8, rec_elems.data());
-    DecTabs T{d_lim, d_first, d_lbase, d_sym};
+    auto* d_lut = (uint32_t*)e.buf("d.lut", ((size_t)ng << kLutBits) * 4 + 4);
+    DecTabs T{d_lim, d_first, d_lbase, d_sym, d_lut};
+    if (ng) { DQTG_SPAN(e, "huff_lut_kernel"); huff_lut_kernel<<<ng, 256, 0, st>>>(d_groups, T, d_lut); }
     mark("uploaded");
     const uint64_t* rec64 = (const uint64_t*)d_rec;
 
