@@ -11,7 +11,7 @@
 
 namespace dqtg {
 
-constexpr int kKB = 256;  // threads per k-means CTA
+constexpr int kKB = 512;  // threads per k-means CTA
 
 // ---- key compaction + mix_weights (quantize.cpp:263-279) --------------------
 // One CTA per problem: hist[HS] (u64, signed-slot order = ascending value) ->
