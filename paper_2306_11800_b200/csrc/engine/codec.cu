@@ -788,13 +788,11 @@ __device__ __forceinline__ void r_phase(const EncArgs& A, const DSmem& S, const 
 // the protected-element mask: nearest-centre level by branch-free bisection over the
 // boundaries (pass_c_tile), PRUNED = k, PROTECTED = k + 1.
 template <int LOGP>
-__device__ __forceinline__ void fused_levels(const float* s_lb, const float* w, uint32_t pw,
-                                             uint32_t k, uint32_t nv, uint32_t (&cw)[4],
-                                             uint32_t& pmask) {
+__device__ __forceinline__ void fused_levels(const float* s_lb, const float4 (&wv)[4], uint32_t pw,
+                                             uint32_t k, uint32_t (&cw)[4], uint32_t& pmask) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if ((uint32_t)(4 * q) < nv) v = __ldg((const float4*)(w + 4 * q));
+        const float4 v = wv[q];
         const float a[4] = {v.x, v.y, v.z, v.w};
         uint32_t word = 0;
 #pragma unroll
@@ -892,6 +890,13 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A, FuseC
                 const uint4 b0 = pp[0], b1 = pp[1];
                 uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0;
                 if (FUSED) {
+                    // w's loads first: their latency overlaps the partition word's
+                    const float* wp = F.w + T.start + e0;
+                    float4 wv[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        wv[q] = (uint32_t)(4 * q) < nv ? __ldg((const float4*)(wp + 4 * q))
+                                                      : make_float4(0.f, 0.f, 0.f, 0.f);
                     uint32_t pc;  // 2-bit partition codes of the 16 elements
                     if (F.pbits) {  // protected bitmap (no pruning): bit -> code 2
                         uint32_t x = (F.pbits[(T.start + e0) >> 5] >> ((T.start + e0) & 31)) & 0xffffu;
@@ -903,11 +908,10 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A, FuseC
                     } else {
                         pc = *(const uint32_t*)(F.parts + ((T.start + e0) >> 2));
                     }
-                    const float* wp = F.w + T.start + e0;
                     switch (s_logp) {
-#define DQTG_FL(L) case L: fused_levels<L>(s_lb, wp, pc, s_k, nv, cw, pmask); break;
+#define DQTG_FL(L) case L: fused_levels<L>(s_lb, wv, pc, s_k, cw, pmask); break;
                         DQTG_FL(0) DQTG_FL(1) DQTG_FL(2) DQTG_FL(3) DQTG_FL(4) DQTG_FL(5)
-                        default: fused_levels<6>(s_lb, wp, pc, s_k, nv, cw, pmask);
+                        default: fused_levels<6>(s_lb, wv, pc, s_k, cw, pmask);
 #undef DQTG_FL
                     }
                     if (nv < (uint32_t)kIt) {
