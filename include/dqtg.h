@@ -318,8 +318,9 @@ dqtg_status dqtg_partition(dqtg_engine *e, const dqtg_ckpt *c, const dqtg_config
 dqtg_status dqtg_proxy_quality(dqtg_engine *e, const dqtg_layout *layout,
                                const float *const *orig_any, const float *const *recon_any,
                                double *quality);
-/* releases the engine's scratch buffers and the device's cached blocks (between
- * workloads of very different sizes; no reference counterpart) */
+/* releases the engine's scratch buffers, its pooled pinned decode staging and the
+ * device's cached blocks (between workloads of very different sizes; no reference
+ * counterpart) */
 dqtg_status dqtg_engine_trim(dqtg_engine *e);
 /* *equal = 1 when the two states have the same step, layout, codebooks, levels and
  * protected entries (compared on the device; round-trip checks of decode_delta_record,

@@ -697,6 +697,9 @@ dqtg_status dqtg_engine_trim(dqtg_engine* h) {
         h->e.sync();
         h->e.drop_scratch("");
         trim_device_caches(h->e.device);
+        std::lock_guard<std::mutex> g(h->e.pin_mu);  // pooled pinned decode staging
+        for (auto& b : h->e.pin_free) cudaFreeHost(b.first);
+        h->e.pin_free.clear();
     });
 }
 
