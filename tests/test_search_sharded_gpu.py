@@ -1,7 +1,10 @@
 """Search control across ranks: guided_exhaustive_search and
 delta_neighborhood_search with distributed.sharded_evaluator on two ranks (gloo,
 both on cuda:0) reach exactly the outcome of the single-process search with the
-device ProxyEvaluator, while each rank evaluates only its share of every batch."""
+device ProxyEvaluator, while each rank evaluates only its share of every batch --
+and that outcome is the reference's own (oracle/_ref: the same configs, evaluation
+counts and compression estimates; quality deltas within the reference's sequential
+sum bound, search.cpp:35-46)."""
 import os
 import socket
 
@@ -68,15 +71,27 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_sharded_search_matches_single_process():
+def _search(m):
+    c, s = _problem(m)
+    params = m.SearchParams(threshold=0.1, seed=4)
+    ev = m.ProxyEvaluator()
+    g = m.guided_exhaustive_search(c, s, m.ConfigCube(), ev, params)
+    d = m.delta_neighborhood_search(c, s, m.ConfigCube(), ev, g.config, 1, params)
+    return g, d
+
+
+def test_sharded_search_matches_single_process(ref):
     from paper_2306_11800_b200 import dqt
 
-    c, s = _problem(dqt)
-    params = dqt.SearchParams(threshold=0.1, seed=4)
-    ev = dqt.ProxyEvaluator()
-    g = dqt.guided_exhaustive_search(c, s, dqt.ConfigCube(), ev, params)
-    d = dqt.delta_neighborhood_search(c, s, dqt.ConfigCube(), ev, g.config, 1, params)
+    g, d = _search(dqt)
     want = (_outcome(g), _outcome(d))
+    # the single-process device search is the reference's search
+    n = 300 * 64 + 128 * 128 + 128 * 256 + 128  # elements of _problem
+    tol = max(1e-12, n * 2.0 ** -53)
+    for mine, theirs in zip((g, d), _search(ref.load())):
+        a, b = _outcome(mine), _outcome(theirs)
+        assert a[:5] == b[:5] and a[6:] == b[6:], (a, b)
+        assert abs(a[5] - b[5]) <= tol * max(abs(b[5]), 1e-300), (a, b)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
