@@ -1960,21 +1960,46 @@ __global__ void __launch_bounds__(256) enc_bits_kernel(EncArgs A, CodeTabs C, in
     const Seg* segs = A.segs + (size_t)ti * B;
     const unsigned long long* runs = A.runs + (size_t)ti * kTile;
     unsigned long long* rct = rc + (size_t)ti * kTile;
-    for (uint32_t r = lane; r < R; r += 32) {
-        uint32_t v, b;
-        unsigned long long L;
-        owned_run(A, segs, runs[r], r, v, b, L);
-        if (!L) {
-            rct[r] = 0;
-            continue;
+    // four runs per lane in flight: their words, segments and code-table loads are
+    // issued together before any result is stored
+    constexpr int kU = 4;
+    for (uint32_t r0 = lane; r0 < R; r0 += 32 * kU) {
+        unsigned long long rw[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t r = r0 + 32 * u;
+            rw[u] = r < R ? runs[r] : 0ull;
         }
-        const uint32_t tb = T.tensor * B + b;
-        unsigned long long c1, c2 = 0;
-        uint32_t l1, l2 = 0;
-        code_of(C, tb, NS, v, c1, l1);
-        if (L > 1) code_of_len(C, tb, NS, B, L, c2, l2);
-        rct[r] = rc_pack(l2 ? (c1 << l2) | c2 : c1, b, l1 + l2);
-        atomicAdd(&s_bits[wid][b], l1 + l2);
+        uint32_t v[kU], b[kU];
+        unsigned long long L[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t r = r0 + 32 * u;
+            if (r < R) owned_run(A, segs, rw[u], r, v[u], b[u], L[u]);
+            else v[u] = b[u] = 0, L[u] = 0;
+        }
+        unsigned long long out[kU];
+        uint32_t bits[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            out[u] = 0;
+            bits[u] = 0;
+            if (!L[u]) continue;
+            const uint32_t tb = T.tensor * B + b[u];
+            unsigned long long c1, c2 = 0;
+            uint32_t l1, l2 = 0;
+            code_of(C, tb, NS, v[u], c1, l1);
+            if (L[u] > 1) code_of_len(C, tb, NS, B, L[u], c2, l2);
+            out[u] = rc_pack(l2 ? (c1 << l2) | c2 : c1, b[u], l1 + l2);
+            bits[u] = l1 + l2;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t r = r0 + 32 * u;
+            if (r >= R) break;
+            rct[r] = out[u];
+            if (bits[u]) atomicAdd(&s_bits[wid][b[u]], bits[u]);
+        }
     }
     __syncwarp();
     for (uint32_t b = lane; b < B; b += 32) segbits[(size_t)ti * B + b] = s_bits[wid][b];
