@@ -2311,11 +2311,14 @@ __global__ void __launch_bounds__(EW * 32) enc_emit_kernel(EncArgs A, CodeTabs C
     __syncwarp();
     // pass 2: place codes; a warp scan over each 32-run chunk gives tile offsets
     uint32_t running = 0;
+    const unsigned long long* rct = rc + (size_t)ti * kTile;
+    unsigned long long wn = lane < R ? rct[lane] : 0ull;  // the next chunk's word, in flight
     for (uint32_t r0 = 0; r0 < R; r0 += 32) {
         const uint32_t r = r0 + lane;
         uint32_t b = 0, l1 = 0, l2 = 0;
         unsigned long long c1 = 0, c2 = 0;
-        const unsigned long long w = r < R ? rc[(size_t)ti * kTile + r] : 0ull;
+        const unsigned long long w = wn;
+        wn = r + 32 < R ? rct[r + 32] : 0ull;
         if ((w & 127) != kRcSlow) {  // resolved by enc_bits_kernel: one code of l1 bits
             l1 = (uint32_t)(w & 127);
             b = (uint32_t)((w >> 7) & 0xff);
