@@ -676,6 +676,30 @@ __global__ void __launch_bounds__(kPB, 3) pass_a2_tma_kernel(PassIn a, A2Args f)
         const uint32_t n = min(T.count - h0, kA2Half);
         mbar_wait(&s_mbar[slot], (it >> 1) & 1);
         uint32_t cm = 0;  // candidate elements of this thread (bit 4g + j)
+        if (a.has_sens && !sens_hist && fastc && n == kA2Half) {
+            // the default step's path, its branches hoisted: EMA scores, the sensitivity
+            // histogram left to the candidates, a full half tile; non-finite
+            // sensitivities reported once per half tile
+            uint32_t smax = 0;
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+                const uint32_t i = g * kPB * 4 + tid * 4;
+                const float4 wv = *(const float4*)(stg[slot].w + i);
+                const float4 ev = *(const float4*)(stg[slot].e + i);
+                const float wa[4] = {wv.x, wv.y, wv.z, wv.w};
+                const float ea[4] = {ev.x, ev.y, ev.z, ev.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float m = fabsf(wa[j]);
+                    const float sv = fabsf(__fmul_rn(ea[j], wa[j]));  // ranker.cpp:96
+                    if (!hist_fast_signed(shw_s, __float_as_uint(wa[j]), fp))
+                        hist_add(shw, gw, wa[j], a.tab, a.err);
+                    smax = max(smax, __float_as_uint(sv));
+                    if (m > lo.x || sv > lo.y) cm |= 1u << (4 * g + j);
+                }
+            }
+            if (smax >= 0x7f800000u) atomicOr(a.err, kErrNonFinite);  // the histogram would have said so
+        } else
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
             const uint32_t i = g * kPB * 4 + tid * 4;  // within the half tile
