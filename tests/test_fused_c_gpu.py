@@ -126,3 +126,36 @@ def test_fused_large_tensor(eng, oracle):
     t1 = perturb(t0, seed=2, frac=0.03, scale=0.02)
     ema = np.random.default_rng(3).normal(0, 0.1, flat(t0).size).astype(np.float32)
     _step(eng, oracle, cfg, t0, t1, ema, True)
+
+
+@pytest.mark.parametrize("where", ["ema_nan", "ema_inf", "w_inf"])
+def test_fused_step_non_finite(eng, oracle, where):
+    """NaN / Inf scores or weights raise NonFiniteData on the fused step -- also where pass
+    A2 builds no sensitivity histogram (it checks the sensitivities itself) -- as the
+    unfused path and the reference's sketch do."""
+    from paper_2306_11800_b200.engine import Config, EngineError
+
+    cfg = CONFIGS[0]
+    lay = [("tok_embed.weight", 4, (3000, 97)), ("blk.fc1.weight", 1, (700, 300))]
+    t0 = make_tensors(lay, seed=1)
+    t1 = perturb(t0, seed=2, frac=0.03, scale=0.02)
+    ema = np.random.default_rng(3).normal(0, 0.1, flat(t0).size).astype(np.float32)
+    dcfg = Config(*cfg.astuple())
+    base = eng.quantize(_ckpt(eng, t0, ema, True, oracle), dcfg, 7, 3)
+    bad_ema, bad_t1 = ema.copy(), [Tensor(t.name, t.type, t.shape, t.data.copy()) for t in t1]
+    at = 200_000 + 123  # inside the second tensor, a full half tile
+    if where == "ema_nan":
+        bad_ema[at] = np.nan
+    elif where == "ema_inf":
+        bad_ema[at] = np.inf
+    else:
+        bad_t1[1].data.reshape(-1)[at - t1[0].data.size] = np.inf
+    for env in ({}, {"DQTG_NO_PASS_A2": "1"}, {"DQTG_NO_FUSED_C": "1"}):
+        os.environ.update(env)
+        try:
+            with pytest.raises(EngineError) as ei:
+                eng.compress_step(_ckpt(eng, bad_t1, bad_ema, True, oracle), dcfg, 7, 4, base=base)
+            assert ei.value.status == 5, (where, env, ei.value)
+        finally:
+            for k in env:
+                os.environ.pop(k, None)
