@@ -994,11 +994,19 @@ __global__ void __launch_bounds__(kCB, 3) enc_tile_delta_kernel(EncArgs A, FuseC
             // block (= thread) counts: elements (lo 16 bits) and non-zero elements (hi
             // 16 bits), conflict-free (one column per thread); per key: non-zero elements
             uint32_t* hb = S.hc + tid;
+            if (nv == (uint32_t)kIt) {  // full threads: no per-element bound checks
 #pragma unroll
-            for (int j = 0; j < kIt; ++j) {
-                if ((uint32_t)j >= nv) break;
-                const uint32_t k = (kw[j >> 2] >> (8 * (j & 3))) & 0xffu;
-                atomicAdd(hb + k * kNBlk, (nzm >> j & 1u) ? 0x10001u : 1u);
+                for (int j = 0; j < kIt; ++j) {
+                    const uint32_t k = (kw[j >> 2] >> (8 * (j & 3))) & 0xffu;
+                    atomicAdd(hb + k * kNBlk, 1u + ((nzm >> j & 1u) << 16));
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < kIt; ++j) {
+                    if ((uint32_t)j >= nv) break;
+                    const uint32_t k = (kw[j >> 2] >> (8 * (j & 3))) & 0xffu;
+                    atomicAdd(hb + k * kNBlk, (nzm >> j & 1u) ? 0x10001u : 1u);
+                }
             }
             for (uint32_t m = nzm; m; m &= m - 1) {
                 const uint32_t j = __ffs(m) - 1;
